@@ -1,0 +1,203 @@
+/*
+ * eva.h -- C ABI of the B200-native FlashEVA hot path (libeva.so).
+ *
+ * FlashEVA (arxiv 2511.00576) evaluates EVA attention as softmax attention
+ * over an augmented key/value set (Eq.12-14): every query
+ * n attends to its exact local window E(n) and to one summary pair
+ * (k~_c, beta^_c) per chunk c that lies entirely before the window, under the
+ * "custom causal mask" of P:124.  Citations: P:NN = PAPER.md line NN,
+ * S:NN = SPEC.md line NN; DESIGN.md lists every reading R1..R13 taken where
+ * the paper is silent.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - All tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA memory)
+ *    owned by the caller.  The library allocates no device memory and keeps
+ *    no global state except a thread-local error string and a cache of the
+ *    device attributes it queried.
+ *  - Layout: row-major, contiguous.  A "unit" is one (batch, head) pair with
+ *    global flattened index u = b*H + h.  Per-unit tensors are [units, rows, d].
+ *    Every call works on units [bh_begin, bh_begin + bh_count): tensor
+ *    pointers address the FIRST unit of that shard (slot 0 <-> unit bh_begin);
+ *    bh_begin only keys the random draws, so a sharded run is bitwise equal
+ *    to the same slice of an unsharded run.
+ *  - Element type of Q/K/V/O/summaries/ring: cfg.dtype (fp32 or bf16).  LSE
+ *    and eps are always fp32.  Accumulation is always fp32.
+ *  - All calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream).  Argument validation is synchronous: on any non-OK
+ *    status nothing has been enqueued and eva_last_error() says why.
+ *  - Positions are 0-indexed.  Chunk c covers positions [c*C, c*C + C).
+ *    nC = floor(T / C) complete chunks are summarised; a trailing partial
+ *    chunk never is (it is always inside the window, reading R8).
+ */
+#ifndef EVA_H_
+#define EVA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef struct CUstream_st* eva_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  EVA_OK = 0,
+  EVA_ERR_INVALID_ARG = 1, /* null pointer, non-positive size, W % C != 0, shard outside [0, B*H), misaligned */
+  EVA_ERR_UNSUPPORTED = 2, /* samples != 1, or d_head not supported for the dtype */
+  EVA_ERR_CAPACITY = 3,    /* cache append would exceed the summary capacity */
+  EVA_ERR_CUDA = 4         /* a CUDA launch/runtime error (message in eva_last_error) */
+} eva_status;
+
+typedef enum { EVA_F32 = 0, EVA_BF16 = 1 } eva_dtype;
+
+/* Partition of the past ("local set E and disjoint subsets P_c"; P:126,
+ * P:298 "local attention" vs "sliding window"), reading R7:
+ *   SLIDING (window start quantised to a chunk boundary):
+ *       nsum(n) = max(0, floor(n/C) - W/C + 1),  lo(n) = nsum(n)*C
+ *   BLOCK (original EVA's non-overlapping local blocks of width W):
+ *       lo(n) = floor(n/W)*W,                    nsum(n) = lo(n)/C
+ * Query n attends to locals m in [lo(n), n] and to summaries c < nsum(n). */
+typedef enum { EVA_WINDOW_SLIDING = 0, EVA_WINDOW_BLOCK = 1 } eva_window_mode;
+
+/* Proposal of Eq.15, reading R3:
+ *   AS_PRINTED:     omega_c = lambda * clip(k~_c + eps_c, -clip, clip)   (default)
+ *   SHIFTED_NOISE:  omega_c = k~_c + lambda * clip(eps_c, -clip, clip)   */
+typedef enum { EVA_OMEGA_AS_PRINTED = 0, EVA_OMEGA_SHIFTED_NOISE = 1 } eva_omega_mode;
+
+typedef struct {
+  int32_t B, H;               /* global batch and heads (the RNG is keyed by b*H + h)   */
+  int32_t bh_begin, bh_count; /* this call's shard of units; full problem = (0, B*H)    */
+  int32_t T;                  /* sequence length (prefill / summarize); ignored by decode */
+  int32_t d_head;             /* head dim d: fp32 {16,32,64,128}, bf16 {16,32,64,128}    */
+  int32_t chunk;              /* C: tokens per summary ("number of keys/values compressed") */
+  int32_t window;             /* W: local window, W >= C and W % C == 0  */
+  int32_t samples;            /* S: random samples per chunk; only 1 is supported */
+  int32_t mode;               /* eva_window_mode */
+  int32_t dtype;              /* eva_dtype */
+  int32_t omega_mode;         /* eva_omega_mode */
+  float scale;                /* logit scale s on q.k and q.k~ (reading R5), e.g. 1/sqrt(d) */
+  float lambda;               /* Eq.15 lambda, paper value 0.1                 */
+  float clip;                 /* Eq.15 clip bound, paper value 1               */
+  uint32_t layer;             /* RNG key component (reading R9)                         */
+  uint64_t seed;              /* RNG key when eps == NULL (reading R9)                  */
+} eva_config;
+
+/* Fill *cfg with the paper's defaults for (B, H, T, d, C, W):
+ * full shard, S = 1, sliding, scale = 1/sqrt(d), lambda = 0.1, clip = 1,
+ * omega as printed, seed = 1234, layer = 0, dtype bf16. */
+void eva_config_default(eva_config* cfg, int32_t B, int32_t H, int32_t T, int32_t d,
+                        int32_t chunk, int32_t window);
+
+/* ---------------------------------------------------------------- summaries
+ * eva_summarize: per-chunk summaries of every complete chunk (S = 1):
+ *   k~_c     = (1/C) sum_{i<C} k_{cC+i}                        (Eq.10; reading R1)
+ *   omega_c  = Eq.15 with mu_c = k~_c                          (readings R2, R3)
+ *   a_i      = omega_c . k_{cC+i} - |k_{cC+i}|^2 / 2           (log xi)
+ *   beta^_c  = sum_i softmax(a)_i v_{cC+i}                     (Eq.9 ratio sum g / sum h)
+ * K, V : [bh_count, T, d] cfg.dtype
+ * eps  : [bh_count, nC, d] fp32 caller-supplied N(0, I) draws, or NULL to draw
+ *        them in-kernel with Philox4x32-10 + Box-Muller keyed by
+ *        (seed, layer, b*H + h, c) (reading R9; identical to oracle_eps()).
+ * Ksum : [bh_count, nC, d] cfg.dtype (out)  -- k~_c
+ * Vsum : [bh_count, nC, d] cfg.dtype (out)  -- beta^_c
+ * T < C (nC = 0) is valid and enqueues nothing. */
+eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, const float* eps,
+                         void* Ksum, void* Vsum, eva_stream_t stream);
+
+/* ---------------------------------------------------------------- prefill
+ * eva_attn_prefill: chunk-causal FlashEVA attention for all T queries
+ * (Eq.12-14, mask P:124, sliding window P:126):
+ *   o_n = sum_{x in E(n) U {c < nsum(n)}} softmax_x(s q_n . key_x) value_x
+ *   lse_n = log sum_x exp(s q_n . key_x)          (natural log)
+ * Q, K, V, O : [bh_count, T, d] cfg.dtype
+ * Ksum, Vsum : [bh_count, nC, d] cfg.dtype; read when EVA_SUMMARIES_PROVIDED,
+ *              otherwise written (they are computed inside this call).
+ * eps        : as in eva_summarize (ignored with EVA_SUMMARIES_PROVIDED).
+ * lse        : [bh_count, T] fp32 (out) or NULL.
+ * flags      : EVA_SUMMARIES_PROVIDED -- use the caller's Ksum/Vsum as is;
+ *              EVA_PREFILL_SIMT       -- force the SIMT kernel (parity/debug);
+ *              0                      -- compute summaries, then attend.
+ * bf16 runs the tcgen05/TMEM/TMA kernel for d in {64, 128} (requires 16-byte
+ * aligned base pointers); other cases run the SIMT kernel. */
+#define EVA_SUMMARIES_PROVIDED 1u
+#define EVA_PREFILL_SIMT 4u
+eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K, const void* V,
+                            void* Ksum, void* Vsum, const float* eps, void* O, float* lse,
+                            uint32_t flags, eva_stream_t stream);
+
+/* ---------------------------------------------------------------- decode cache
+ * Compressed decode cache ("cache of (compressed) past
+ * context"): a ring of the last W tokens plus one summary per
+ * completed chunk.  Summaries are written eagerly when a chunk's last token
+ * arrives; the attention only ever reads c < nsum(n), so this equals SPEC's
+ * lazy compress-on-eviction -- reading R13.
+ *   ring_k, ring_v : [bh_count, W, d]           cfg.dtype, slot p mod W holds position p
+ *   sum_k,  sum_v  : [bh_count, cap_chunks, d]  cfg.dtype, row c = chunk c
+ *   pos            : number of tokens appended so far (uniform over the shard)
+ * The descriptor is a plain caller-owned struct; the library only reads it,
+ * except eva_cache_append which advances pos.  Single writer. */
+typedef struct {
+  eva_config cfg; /* cfg.T is ignored */
+  int64_t pos;
+  int32_t cap_chunks;
+  int32_t reserved;
+  void* ring_k;
+  void* ring_v;
+  void* sum_k;
+  void* sum_v;
+} eva_cache;
+
+/* Append n_new >= 1 tokens per unit at positions [pos, pos + n_new):
+ * K_new, V_new : [bh_count, n_new, d] cfg.dtype
+ * eps          : [bh_count, cap_chunks, d] fp32 indexed by ABSOLUTE chunk index, or NULL (Philox).
+ * Every chunk completed by these tokens is summarised (eva_summarize's formulas),
+ * and the last min(n_new, W) tokens are written to the ring.  n_new = T is the
+ * prefill hand-off.  EVA_ERR_CAPACITY if (pos + n_new) / C > cap_chunks.
+ * On success cache->pos += n_new. */
+eva_status eva_cache_append(eva_cache* cache, const void* K_new, const void* V_new, int32_t n_new,
+                            const float* eps, eva_stream_t stream);
+
+/* One query per unit at position n = pos - 1 over the cache (Eq.12, one row):
+ * Q, O : [bh_count, d] cfg.dtype;  lse : [bh_count] fp32 or NULL.
+ * workspace : device scratch of eva_decode_workspace_bytes(cache) bytes (may be
+ *             NULL when that is 0).  pos must be >= 1. */
+eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float* lse,
+                           void* workspace, size_t workspace_bytes, eva_stream_t stream);
+size_t eva_decode_workspace_bytes(const eva_cache* cache);
+
+/* ---------------------------------------------------------------- debug / introspection
+ * eva_mask_ranges: the (lo(n), nsum(n)) the kernels use, for n in
+ * [n_begin, n_begin + count), written to device int64 arrays lo, nsum
+ * (bit-exact mask tests).  Uses cfg.chunk, cfg.window, cfg.mode only. */
+eva_status eva_mask_ranges(const eva_config* cfg, int64_t n_begin, int64_t count, int64_t* lo,
+                           int64_t* nsum, eva_stream_t stream);
+
+/* eva_philox: the device Philox4x32-10 on n blocks.  in: [n, 6] uint32
+ * (ctr0..ctr3, key0, key1), out: [n, 4] uint32.  Device pointers. */
+eva_status eva_philox(const uint32_t* in, uint32_t* out, int32_t n, eva_stream_t stream);
+
+/* eva_draw_eps: the eps the kernels draw when eps == NULL, materialised as
+ * [bh_count, nC, d] fp32 (nC = floor(cfg.T / C)). */
+eva_status eva_draw_eps(const eva_config* cfg, float* eps, eva_stream_t stream);
+
+/* Thread-local text of the last non-OK status ("" if none). */
+const char* eva_last_error(void);
+/* Library version string, e.g. "flasheva-b200 0.1 sm_100a". */
+const char* eva_version(void);
+/* Number of kernels this library enqueued since load (a per-process counter). */
+uint64_t eva_launch_count(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVA_H_ */

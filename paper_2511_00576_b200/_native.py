@@ -1,0 +1,88 @@
+"""ctypes declarations of libeva.so (include/eva.h).  Argument marshalling only.
+
+The library is loaded from this package directory; if it is missing the import
+fails loudly (there is no CPU or eager fallback of any kind).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libeva.so")
+
+EVA_OK, EVA_ERR_INVALID_ARG, EVA_ERR_UNSUPPORTED, EVA_ERR_CAPACITY, EVA_ERR_CUDA = range(5)
+EVA_F32, EVA_BF16 = 0, 1
+EVA_WINDOW_SLIDING, EVA_WINDOW_BLOCK = 0, 1
+EVA_OMEGA_AS_PRINTED, EVA_OMEGA_SHIFTED_NOISE = 0, 1
+EVA_SUMMARIES_PROVIDED = 1
+EVA_PREFILL_SIMT = 4
+
+_STATUS = {0: "EVA_OK", 1: "EVA_ERR_INVALID_ARG", 2: "EVA_ERR_UNSUPPORTED", 3: "EVA_ERR_CAPACITY",
+           4: "EVA_ERR_CUDA"}
+
+
+class EvaConfig(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32),
+                ("bh_begin", ctypes.c_int32), ("bh_count", ctypes.c_int32),
+                ("T", ctypes.c_int32), ("d_head", ctypes.c_int32),
+                ("chunk", ctypes.c_int32), ("window", ctypes.c_int32),
+                ("samples", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("omega_mode", ctypes.c_int32),
+                ("scale", ctypes.c_float), ("lambda_", ctypes.c_float), ("clip", ctypes.c_float),
+                ("layer", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
+
+
+class EvaCache(ctypes.Structure):
+    _fields_ = [("cfg", EvaConfig), ("pos", ctypes.c_int64), ("cap_chunks", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("ring_k", ctypes.c_void_p),
+                ("ring_v", ctypes.c_void_p), ("sum_k", ctypes.c_void_p), ("sum_v", ctypes.c_void_p)]
+
+
+EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache_append",
+           "eva_attn_decode", "eva_decode_workspace_bytes", "eva_mask_ranges", "eva_philox",
+           "eva_draw_eps", "eva_last_error", "eva_version", "eva_launch_count"]
+
+
+class EvaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2511_00576_b200.build` "
+                          "(there is no fallback path)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    CFG = ctypes.POINTER(EvaConfig)
+    CACHE = ctypes.POINTER(EvaCache)
+    st = ctypes.c_int
+    sig = {
+        "eva_config_default": (None, [CFG] + [ctypes.c_int32] * 6),
+        "eva_summarize": (st, [CFG, P, P, P, P, P, P]),
+        "eva_attn_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_uint32, P]),
+        "eva_cache_append": (st, [CACHE, P, P, ctypes.c_int32, P, P]),
+        "eva_attn_decode": (st, [CACHE, P, P, P, P, ctypes.c_size_t, P]),
+        "eva_decode_workspace_bytes": (ctypes.c_size_t, [CACHE]),
+        "eva_mask_ranges": (st, [CFG, ctypes.c_int64, ctypes.c_int64, P, P, P]),
+        "eva_philox": (st, [P, P, ctypes.c_int32, P]),
+        "eva_draw_eps": (st, [CFG, P, P]),
+        "eva_last_error": (ctypes.c_char_p, []),
+        "eva_version": (ctypes.c_char_p, []),
+        "eva_launch_count": (ctypes.c_uint64, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int) -> None:
+    if status != EVA_OK:
+        raise EvaError(status, lib.eva_last_error().decode())

@@ -1,0 +1,227 @@
+"""Thin torch-facing binding of libeva.so with the C ABI's names (include/eva.h).
+
+Argument marshalling only: every step of the FlashEVA path runs in the CUDA
+kernels behind the C ABI.  Tensors must be CUDA, contiguous, of the dtype the
+config names; outputs are allocated with torch (the library allocates nothing).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional
+
+import torch
+
+from . import _native as N
+from ._native import EvaCache, EvaConfig, EvaError, check, lib
+
+__all__ = ["make_config", "eva_summarize", "eva_attn_prefill", "eva_cache_append",
+           "eva_attn_decode", "DecodeCache", "eva_mask_ranges", "eva_philox", "eva_draw_eps",
+           "EvaConfig", "EvaError", "launch_count", "version"]
+
+_DT = {torch.float32: N.EVA_F32, torch.bfloat16: N.EVA_BF16}
+_MODE = {"sliding": N.EVA_WINDOW_SLIDING, "block": N.EVA_WINDOW_BLOCK}
+
+
+def version() -> str:
+    return lib.eva_version().decode()
+
+
+def launch_count() -> int:
+    """Kernels libeva.so has enqueued in this process."""
+    return int(lib.eva_launch_count())
+
+
+def make_config(B: int, H: int, T: int, d: int, chunk: int, window: int, *, bh_begin: int = 0,
+                bh_count: Optional[int] = None, mode: str = "sliding", dtype=torch.bfloat16,
+                scale: Optional[float] = None, lam: float = 0.1, clip: float = 1.0,
+                seed: int = 1234, layer: int = 0, omega_mode: int = 0, samples: int = 1) -> EvaConfig:
+    cfg = EvaConfig()
+    lib.eva_config_default(ctypes.byref(cfg), B, H, T, d, chunk, window)
+    cfg.bh_begin = bh_begin
+    cfg.bh_count = B * H - bh_begin if bh_count is None else bh_count
+    cfg.mode = _MODE[mode] if isinstance(mode, str) else int(mode)
+    cfg.dtype = _DT[dtype]
+    cfg.scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    cfg.lambda_ = lam
+    cfg.clip = clip
+    cfg.seed = seed
+    cfg.layer = layer
+    cfg.omega_mode = omega_mode
+    cfg.samples = samples
+    return cfg
+
+
+def _tdtype(cfg) -> torch.dtype:
+    return torch.bfloat16 if cfg.dtype == N.EVA_BF16 else torch.float32
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(dev) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _need(t: torch.Tensor, name: str, shape, dtype) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def eva_summarize(cfg: EvaConfig, K: torch.Tensor, V: torch.Tensor,
+                  eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
+                  Vsum: Optional[torch.Tensor] = None):
+    """Chunk summaries (k~_c, beta^_c) of all complete chunks -> Ksum, Vsum [bh, nC, d]."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    nC = T // cfg.chunk
+    _need(K, "K", (bh, T, d), dt)
+    _need(V, "V", (bh, T, d), dt)
+    if eps is not None:
+        _need(eps, "eps", (bh, nC, d), torch.float32)
+    Ksum = torch.empty(bh, nC, d, dtype=dt, device=K.device) if Ksum is None else Ksum
+    Vsum = torch.empty(bh, nC, d, dtype=dt, device=K.device) if Vsum is None else Vsum
+    check(lib.eva_summarize(ctypes.byref(cfg), _ptr(K), _ptr(V), _ptr(eps), _ptr(Ksum), _ptr(Vsum),
+                            _stream(K.device)))
+    return Ksum, Vsum
+
+
+def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, *,
+                     eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
+                     Vsum: Optional[torch.Tensor] = None, summaries_provided: bool = False,
+                     want_lse: bool = True, simt: bool = False, O: Optional[torch.Tensor] = None,
+                     lse: Optional[torch.Tensor] = None):
+    """FlashEVA chunk-causal prefill.  Returns (O, lse, Ksum, Vsum)."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    nC = T // cfg.chunk
+    for t, nm in ((Q, "Q"), (K, "K"), (V, "V")):
+        _need(t, nm, (bh, T, d), dt)
+    if summaries_provided:
+        if Ksum is None or Vsum is None:
+            raise ValueError("summaries_provided needs Ksum and Vsum")
+    if Ksum is None:
+        Ksum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=Q.device)[:, :nC]
+    if Vsum is None:
+        Vsum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=Q.device)[:, :nC]
+    if nC:
+        _need(Ksum, "Ksum", (bh, nC, d), dt)
+        _need(Vsum, "Vsum", (bh, nC, d), dt)
+    if eps is not None:
+        _need(eps, "eps", (bh, nC, d), torch.float32)
+    O = torch.empty_like(Q) if O is None else O
+    _need(O, "O", (bh, T, d), dt)
+    if want_lse and lse is None:
+        lse = torch.empty(bh, T, dtype=torch.float32, device=Q.device)
+    flags = (N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0) | (N.EVA_PREFILL_SIMT if simt else 0)
+    check(lib.eva_attn_prefill(ctypes.byref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum), _ptr(Vsum),
+                               _ptr(eps), _ptr(O), _ptr(lse if want_lse else None), flags,
+                               _stream(Q.device)))
+    return O, (lse if want_lse else None), Ksum, Vsum
+
+
+class DecodeCache:
+    """Compressed decode cache: ring [bh, W, d] x2 + summaries [bh, cap, d] x2 (torch-owned)."""
+
+    def __init__(self, cfg: EvaConfig, cap_chunks: int, device="cuda"):
+        dt, bh, W, d = _tdtype(cfg), cfg.bh_count, cfg.window, cfg.d_head
+        self.ring_k = torch.zeros(bh, W, d, dtype=dt, device=device)
+        self.ring_v = torch.zeros(bh, W, d, dtype=dt, device=device)
+        self.sum_k = torch.zeros(bh, max(cap_chunks, 1), d, dtype=dt, device=device)
+        self.sum_v = torch.zeros(bh, max(cap_chunks, 1), d, dtype=dt, device=device)
+        self.c = EvaCache()
+        self.c.cfg = cfg
+        self.c.pos = 0
+        self.c.cap_chunks = cap_chunks
+        self.c.ring_k, self.c.ring_v = self.ring_k.data_ptr(), self.ring_v.data_ptr()
+        self.c.sum_k, self.c.sum_v = self.sum_k.data_ptr(), self.sum_v.data_ptr()
+        self.device = torch.device(device)
+        self._ws = None
+
+    @property
+    def pos(self) -> int:
+        return int(self.c.pos)
+
+    @property
+    def cfg(self) -> EvaConfig:
+        return self.c.cfg
+
+    def workspace_bytes(self) -> int:
+        return int(lib.eva_decode_workspace_bytes(ctypes.byref(self.c)))
+
+    def eva_cache_append(self, K_new: torch.Tensor, V_new: torch.Tensor,
+                         eps: Optional[torch.Tensor] = None) -> None:
+        """Append n_new tokens per unit: K_new, V_new [bh, n_new, d]."""
+        cfg = self.c.cfg
+        dt, bh, d = _tdtype(cfg), cfg.bh_count, cfg.d_head
+        if K_new.dim() == 2:
+            K_new, V_new = K_new.unsqueeze(1), V_new.unsqueeze(1)
+        n_new = K_new.shape[1]
+        _need(K_new, "K_new", (bh, n_new, d), dt)
+        _need(V_new, "V_new", (bh, n_new, d), dt)
+        if eps is not None:
+            _need(eps, "eps", (bh, self.c.cap_chunks, d), torch.float32)
+        check(lib.eva_cache_append(ctypes.byref(self.c), _ptr(K_new), _ptr(V_new), n_new, _ptr(eps),
+                                   _stream(self.device)))
+
+    append = eva_cache_append
+
+    def eva_attn_decode(self, q: torch.Tensor, O: Optional[torch.Tensor] = None,
+                        lse: Optional[torch.Tensor] = None, want_lse: bool = True):
+        """One query per unit at position pos-1: q [bh, d] -> (o [bh, d], lse [bh])."""
+        cfg = self.c.cfg
+        dt, bh, d = _tdtype(cfg), cfg.bh_count, cfg.d_head
+        _need(q, "q", (bh, d), dt)
+        O = torch.empty_like(q) if O is None else O
+        if want_lse and lse is None:
+            lse = torch.empty(bh, dtype=torch.float32, device=q.device)
+        nbytes = self.workspace_bytes()
+        if nbytes and (self._ws is None or self._ws.numel() * 4 < nbytes):
+            self._ws = torch.empty((nbytes + 3) // 4 * 2, dtype=torch.float32, device=q.device)
+        ws = self._ws if nbytes else None
+        check(lib.eva_attn_decode(ctypes.byref(self.c), _ptr(q), _ptr(O),
+                                  _ptr(lse if want_lse else None), _ptr(ws),
+                                  0 if ws is None else ws.numel() * 4, _stream(q.device)))
+        return O, (lse if want_lse else None)
+
+    decode = eva_attn_decode
+
+
+def eva_mask_ranges(cfg: EvaConfig, n_begin: int, count: int, device="cuda"):
+    lo = torch.empty(count, dtype=torch.int64, device=device)
+    ns = torch.empty(count, dtype=torch.int64, device=device)
+    check(lib.eva_mask_ranges(ctypes.byref(cfg), n_begin, count, _ptr(lo), _ptr(ns),
+                              _stream(torch.device(device))))
+    return lo, ns
+
+
+def eva_philox(blocks: torch.Tensor) -> torch.Tensor:
+    """blocks: integer [n, 6] (ctr0..3, key0, key1) -> Philox4x32-10 words as int64 [n, 4]."""
+    x = blocks.to(torch.int64) & 0xFFFFFFFF
+    x = torch.where(x >= 2 ** 31, x - 2 ** 32, x).to(torch.int32).contiguous().cuda()
+    out = torch.empty(x.shape[0], 4, dtype=torch.int32, device=x.device)
+    check(lib.eva_philox(_ptr(x), _ptr(out), x.shape[0], _stream(x.device)))
+    return out.to(torch.int64) & 0xFFFFFFFF
+
+
+def eva_cache_append(cache: "DecodeCache", K_new: torch.Tensor, V_new: torch.Tensor,
+                     eps: Optional[torch.Tensor] = None) -> None:
+    """C-ABI-named alias of DecodeCache.eva_cache_append."""
+    cache.eva_cache_append(K_new, V_new, eps)
+
+
+def eva_attn_decode(cache: "DecodeCache", q: torch.Tensor, **kw):
+    """C-ABI-named alias of DecodeCache.eva_attn_decode."""
+    return cache.eva_attn_decode(q, **kw)
+
+
+def eva_draw_eps(cfg: EvaConfig, device="cuda") -> torch.Tensor:
+    nC = cfg.T // cfg.chunk
+    eps = torch.empty(cfg.bh_count, max(nC, 1), cfg.d_head, dtype=torch.float32, device=device)
+    check(lib.eva_draw_eps(ctypes.byref(cfg), _ptr(eps), _stream(torch.device(device))))
+    return eps[:, :nC]

@@ -1,0 +1,256 @@
+// api.cu -- the C ABI of libeva.so (include/eva.h): synchronous argument
+// validation, kernel selection and launch on the caller's stream.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/eva.h"
+#include "common.cuh"
+#include "launch.h"
+
+namespace eva {
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+}  // namespace eva
+
+namespace {
+
+thread_local std::string g_err;
+
+eva_status fail(eva_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+eva_status ok() {
+  g_err.clear();
+  return EVA_OK;
+}
+
+eva_status cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return ok();
+  return fail(EVA_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool d_supported(int d) { return d == 16 || d == 32 || d == 64 || d == 128; }
+
+// Validation shared by all entry points.  need_T: the call uses cfg.T.
+eva_status check_cfg(const eva_config* cfg, bool need_T) {
+  if (!cfg) return fail(EVA_ERR_INVALID_ARG, "cfg is NULL");
+  if (cfg->B < 1 || cfg->H < 1) return fail(EVA_ERR_INVALID_ARG, "B=%d H=%d must be >= 1", cfg->B, cfg->H);
+  const int64_t BH = (int64_t)cfg->B * cfg->H;
+  if (cfg->bh_begin < 0 || cfg->bh_count < 0 || (int64_t)cfg->bh_begin + cfg->bh_count > BH)
+    return fail(EVA_ERR_INVALID_ARG, "shard [%d, %d+%d) outside [0, B*H=%lld)", cfg->bh_begin,
+                cfg->bh_begin, cfg->bh_count, (long long)BH);
+  if (need_T && cfg->T < 1) return fail(EVA_ERR_INVALID_ARG, "T=%d must be >= 1", cfg->T);
+  if (cfg->d_head < 1) return fail(EVA_ERR_INVALID_ARG, "d_head=%d must be >= 1", cfg->d_head);
+  if (cfg->chunk < 1 || cfg->window < 1)
+    return fail(EVA_ERR_INVALID_ARG, "chunk=%d window=%d must be >= 1", cfg->chunk, cfg->window);
+  if (cfg->window % cfg->chunk != 0)
+    return fail(EVA_ERR_INVALID_ARG, "window %d is not a multiple of chunk %d (S:211)", cfg->window,
+                cfg->chunk);
+  if (cfg->mode != EVA_WINDOW_SLIDING && cfg->mode != EVA_WINDOW_BLOCK)
+    return fail(EVA_ERR_INVALID_ARG, "mode=%d", cfg->mode);
+  if (cfg->dtype != EVA_F32 && cfg->dtype != EVA_BF16)
+    return fail(EVA_ERR_INVALID_ARG, "dtype=%d", cfg->dtype);
+  if (cfg->omega_mode != EVA_OMEGA_AS_PRINTED && cfg->omega_mode != EVA_OMEGA_SHIFTED_NOISE)
+    return fail(EVA_ERR_INVALID_ARG, "omega_mode=%d", cfg->omega_mode);
+  if (!std::isfinite(cfg->scale) || !std::isfinite(cfg->lambda) || !std::isfinite(cfg->clip) ||
+      cfg->clip < 0.f)
+    return fail(EVA_ERR_INVALID_ARG, "scale/lambda/clip must be finite, clip >= 0");
+  if (cfg->samples != 1)
+    return fail(EVA_ERR_UNSUPPORTED, "samples=%d: only S=1 makes beta query-independent (P:101)",
+                cfg->samples);
+  if (!d_supported(cfg->d_head))
+    return fail(EVA_ERR_UNSUPPORTED, "d_head=%d not in {16,32,64,128}", cfg->d_head);
+  return EVA_OK;
+}
+
+eva_status check_ptrs(int n, const void* const* ptrs, const char* const* names) {
+  for (int i = 0; i < n; ++i) {
+    if (!ptrs[i]) return fail(EVA_ERR_INVALID_ARG, "%s is NULL", names[i]);
+    if (!aligned16(ptrs[i])) return fail(EVA_ERR_INVALID_ARG, "%s is not 16-byte aligned", names[i]);
+  }
+  return EVA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void eva_config_default(eva_config* cfg, int32_t B, int32_t H, int32_t T, int32_t d,
+                        int32_t chunk, int32_t window) {
+  if (!cfg) return;
+  cfg->B = B;
+  cfg->H = H;
+  cfg->bh_begin = 0;
+  cfg->bh_count = B * H;
+  cfg->T = T;
+  cfg->d_head = d;
+  cfg->chunk = chunk;
+  cfg->window = window;
+  cfg->samples = 1;
+  cfg->mode = EVA_WINDOW_SLIDING;
+  cfg->dtype = EVA_BF16;
+  cfg->omega_mode = EVA_OMEGA_AS_PRINTED;
+  cfg->scale = d > 0 ? 1.0f / std::sqrt((float)d) : 1.0f;
+  cfg->lambda = 0.1f;
+  cfg->clip = 1.0f;
+  cfg->layer = 0;
+  cfg->seed = 1234;
+}
+
+eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, const float* eps,
+                         void* Ksum, void* Vsum, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (cfg->bh_count == 0 || cfg->T / cfg->chunk == 0) return ok();
+  const void* p[] = {K, V, Ksum, Vsum};
+  const char* nm[] = {"K", "V", "Ksum", "Vsum"};
+  if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  return cuda_status(eva::launch_summarize(*cfg, K, V, eps, Ksum, Vsum, (cudaStream_t)stream),
+                     "eva_summarize");
+}
+
+eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K, const void* V,
+                            void* Ksum, void* Vsum, const float* eps, void* O, float* lse,
+                            uint32_t flags, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT))
+    return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  if (cfg->bh_count == 0) return ok();
+  const void* p[] = {Q, K, V, O};
+  const char* nm[] = {"Q", "K", "V", "O"};
+  if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+  const bool have_sums = cfg->T / cfg->chunk > 0;
+  if (have_sums) {
+    const void* p2[] = {Ksum, Vsum};
+    const char* nm2[] = {"Ksum", "Vsum"};
+    if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+  }
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  if (lse && !aligned16(lse)) return fail(EVA_ERR_INVALID_ARG, "lse is not 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (have_sums && !(flags & EVA_SUMMARIES_PROVIDED)) {
+    cudaError_t e = eva::launch_summarize(*cfg, K, V, eps, Ksum, Vsum, s);
+    if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill(summaries)");
+  }
+  const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) &&
+                  eva::prefill_sm100_supported(*cfg);
+  cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, Q, K, V, Ksum, Vsum, O, lse, s)
+                     : eva::launch_prefill_simt(*cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  return cuda_status(e, tc ? "eva_attn_prefill(sm100)" : "eva_attn_prefill(simt)");
+}
+
+eva_status eva_cache_append(eva_cache* cache, const void* K_new, const void* V_new, int32_t n_new,
+                            const float* eps, eva_stream_t stream) {
+  if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
+  eva_status st = check_cfg(&cache->cfg, false);
+  if (st != EVA_OK) return st;
+  if (n_new < 1) return fail(EVA_ERR_INVALID_ARG, "n_new=%d must be >= 1", n_new);
+  if (cache->pos < 0 || cache->cap_chunks < 0)
+    return fail(EVA_ERR_INVALID_ARG, "pos=%lld cap_chunks=%d", (long long)cache->pos, cache->cap_chunks);
+  if ((cache->pos + n_new) / cache->cfg.chunk > cache->cap_chunks)
+    return fail(EVA_ERR_CAPACITY, "append of %d at pos %lld needs %lld summaries > cap %d", n_new,
+                (long long)cache->pos, (long long)((cache->pos + n_new) / cache->cfg.chunk),
+                cache->cap_chunks);
+  if (cache->cfg.bh_count > 0) {
+    const void* p[] = {K_new, V_new, cache->ring_k, cache->ring_v};
+    const char* nm[] = {"K_new", "V_new", "ring_k", "ring_v"};
+    if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+    if (cache->cap_chunks > 0) {
+      const void* p2[] = {cache->sum_k, cache->sum_v};
+      const char* nm2[] = {"sum_k", "sum_v"};
+      if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+    }
+    if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+    cudaError_t e = eva::launch_cache_append(*cache, K_new, V_new, n_new, eps, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "eva_cache_append");
+  }
+  cache->pos += n_new;
+  return ok();
+}
+
+size_t eva_decode_workspace_bytes(const eva_cache* cache) {
+  if (!cache || cache->pos < 1 || cache->cfg.chunk < 1 || cache->cfg.window < 1 ||
+      !d_supported(cache->cfg.d_head))
+    return 0;
+  const int S = eva::decode_splits(*cache);
+  if (S <= 1) return 0;
+  return (size_t)cache->cfg.bh_count * S * (cache->cfg.d_head + 2) * sizeof(float);
+}
+
+eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float* lse,
+                           void* workspace, size_t workspace_bytes, eva_stream_t stream) {
+  if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
+  eva_status st = check_cfg(&cache->cfg, false);
+  if (st != EVA_OK) return st;
+  if (cache->pos < 1) return fail(EVA_ERR_INVALID_ARG, "decode needs pos >= 1 (pos=%lld)", (long long)cache->pos);
+  if (cache->cfg.bh_count == 0) return ok();
+  const void* p[] = {Q, O, cache->ring_k, cache->ring_v};
+  const char* nm[] = {"Q", "O", "ring_k", "ring_v"};
+  if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+  const eva::Range r = eva::mask_range(cache->pos - 1, cache->cfg.chunk, cache->cfg.window, cache->cfg.mode);
+  if (r.nsum > 0) {
+    if (r.nsum > cache->cap_chunks)
+      return fail(EVA_ERR_CAPACITY, "query needs %lld summaries > cap %d", (long long)r.nsum, cache->cap_chunks);
+    const void* p2[] = {cache->sum_k, cache->sum_v};
+    const char* nm2[] = {"sum_k", "sum_v"};
+    if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+  }
+  if (lse && !aligned16(lse)) return fail(EVA_ERR_INVALID_ARG, "lse is not 16-byte aligned");
+  const int S = eva::decode_splits(*cache);
+  const size_t need = S > 1 ? (size_t)cache->cfg.bh_count * S * (cache->cfg.d_head + 2) * sizeof(float) : 0;
+  if (need > 0 && (!workspace || workspace_bytes < need))
+    return fail(EVA_ERR_INVALID_ARG, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
+  if (workspace && !aligned16(workspace)) return fail(EVA_ERR_INVALID_ARG, "workspace is not 16-byte aligned");
+  return cuda_status(eva::launch_decode(*cache, Q, O, lse, (float*)workspace, S, (cudaStream_t)stream),
+                     "eva_attn_decode");
+}
+
+eva_status eva_mask_ranges(const eva_config* cfg, int64_t n_begin, int64_t count, int64_t* lo,
+                           int64_t* nsum, eva_stream_t stream) {
+  if (!cfg) return fail(EVA_ERR_INVALID_ARG, "cfg is NULL");
+  if (cfg->chunk < 1 || cfg->window < 1 || cfg->window % cfg->chunk != 0)
+    return fail(EVA_ERR_INVALID_ARG, "chunk=%d window=%d", cfg->chunk, cfg->window);
+  if (cfg->mode != EVA_WINDOW_SLIDING && cfg->mode != EVA_WINDOW_BLOCK)
+    return fail(EVA_ERR_INVALID_ARG, "mode=%d", cfg->mode);
+  if (n_begin < 0 || count < 0) return fail(EVA_ERR_INVALID_ARG, "n_begin/count must be >= 0");
+  if (count > 0 && (!lo || !nsum)) return fail(EVA_ERR_INVALID_ARG, "lo/nsum is NULL");
+  return cuda_status(eva::launch_mask_ranges(*cfg, n_begin, count, lo, nsum, (cudaStream_t)stream),
+                     "eva_mask_ranges");
+}
+
+eva_status eva_philox(const uint32_t* in, uint32_t* out, int32_t n, eva_stream_t stream) {
+  if (n < 0) return fail(EVA_ERR_INVALID_ARG, "n=%d", n);
+  if (n > 0 && (!in || !out)) return fail(EVA_ERR_INVALID_ARG, "in/out is NULL");
+  return cuda_status(eva::launch_philox(in, out, n, (cudaStream_t)stream), "eva_philox");
+}
+
+eva_status eva_draw_eps(const eva_config* cfg, float* eps, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (cfg->bh_count > 0 && cfg->T / cfg->chunk > 0 && !eps) return fail(EVA_ERR_INVALID_ARG, "eps is NULL");
+  return cuda_status(eva::launch_draw_eps(*cfg, eps, (cudaStream_t)stream), "eva_draw_eps");
+}
+
+const char* eva_last_error(void) { return g_err.c_str(); }
+
+const char* eva_version(void) { return "flasheva-b200 0.1 sm_100a"; }
+
+uint64_t eva_launch_count(void) { return eva::g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

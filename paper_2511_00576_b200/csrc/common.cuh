@@ -1,0 +1,130 @@
+// common.cuh -- device helpers shared by the FlashEVA kernels (sm_100a).
+// No code here is shared with oracle/ (the oracle has its own Philox, mask and
+// arithmetic); see DESIGN.md §4 for the independence rule.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/eva.h"
+
+namespace eva {
+
+// ---------------------------------------------------------------- element I/O
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  static __device__ __forceinline__ float to_f(float x) { return x; }
+  static __device__ __forceinline__ float from_f(float x) { return x; }
+};
+template <> struct Elem<__nv_bfloat16> {
+  static __device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  static __device__ __forceinline__ __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+
+// Load N contiguous elements starting at p (N in {1,2,4,8}) into floats.
+template <typename T, int N> __device__ __forceinline__ void load_vec(const T* p, float* out) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[i] = Elem<T>::to_f(p[i]);
+}
+template <> __device__ __forceinline__ void load_vec<float, 4>(const float* p, float* out) {
+  float4 v = *reinterpret_cast<const float4*>(p);
+  out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+}
+template <> __device__ __forceinline__ void load_vec<__nv_bfloat16, 4>(const __nv_bfloat16* p, float* out) {
+  uint2 v = *reinterpret_cast<const uint2*>(p);
+  __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&v.x), b = *reinterpret_cast<__nv_bfloat162*>(&v.y);
+  float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+  out[0] = fa.x; out[1] = fa.y; out[2] = fb.x; out[3] = fb.y;
+}
+template <> __device__ __forceinline__ void load_vec<__nv_bfloat16, 8>(const __nv_bfloat16* p, float* out) {
+  uint4 v = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+    out[2 * i] = f.x; out[2 * i + 1] = f.y;
+  }
+}
+
+template <typename T, int N> __device__ __forceinline__ void store_vec(T* p, const float* in) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) p[i] = Elem<T>::from_f(in[i]);
+}
+
+// ---------------------------------------------------------------- warp helpers
+template <int WIDTH> __device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = WIDTH / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) { return group_sum<32>(v); }
+
+// ---------------------------------------------------------------- partition (reading R7)
+// Query n sees locals [lo, n] and summaries c < nsum.  Integer-exact.
+struct Range { int64_t lo, nsum; };
+__host__ __device__ __forceinline__ Range mask_range(int64_t n, int C, int W, int mode) {
+  Range r;
+  if (mode == EVA_WINDOW_SLIDING) {
+    int64_t s = n / C - W / C + 1;
+    r.nsum = s > 0 ? s : 0;
+    r.lo = r.nsum * C;
+  } else {
+    r.lo = (n / W) * W;
+    r.nsum = r.lo / C;
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------- Philox4x32-10 (reading R9)
+struct U4 { uint32_t x, y, z, w; };
+__host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#ifdef __CUDA_ARCH__
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+#else
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x, p1 = (uint64_t)0xCD9E8D57u * c.z;
+    const uint32_t lo0 = (uint32_t)p0, hi0 = (uint32_t)(p0 >> 32);
+    const uint32_t lo1 = (uint32_t)p1, hi1 = (uint32_t)(p1 >> 32);
+#endif
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Four N(0,1) draws eps[c][4i .. 4i+3] of unit bh: Philox block (i, c, bh, layer),
+// u = ((x >> 8) + 0.5) * 2^-24, Box-Muller pairs (u0,u1) and (u2,u3).
+__device__ __forceinline__ float4 philox_normal4(uint64_t seed, uint32_t layer, uint32_t bh,
+                                                 uint32_t c, uint32_t i) {
+  U4 x = philox4x32_10(U4{i, c, bh, layer}, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const float s = 5.9604644775390625e-08f;  // 2^-24
+  float u0 = ((float)(x.x >> 8) + 0.5f) * s, u1 = ((float)(x.y >> 8) + 0.5f) * s;
+  float u2 = ((float)(x.z >> 8) + 0.5f) * s, u3 = ((float)(x.w >> 8) + 0.5f) * s;
+  float r0 = sqrtf(-2.0f * logf(u0)), r1 = sqrtf(-2.0f * logf(u2));
+  float s0, c0, s1, c1;
+  sincospif(2.0f * u1, &s0, &c0);
+  sincospif(2.0f * u3, &s1, &c1);
+  return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+}
+
+// eps component j of chunk c (used where a lane holds a non-multiple-of-4 channel group).
+__device__ __forceinline__ float philox_normal1(uint64_t seed, uint32_t layer, uint32_t bh,
+                                                uint32_t c, uint32_t j) {
+  float4 z = philox_normal4(seed, layer, bh, c, j >> 2);
+  switch (j & 3) { case 0: return z.x; case 1: return z.y; case 2: return z.z; default: return z.w; }
+}
+
+// Eq.15 with mu_c = k~_c; reading R3 selects the composition.
+__device__ __forceinline__ float omega_of(float kt, float e, const eva_config& cfg) {
+  if (cfg.omega_mode == EVA_OMEGA_AS_PRINTED)
+    return cfg.lambda * fminf(fmaxf(kt + e, -cfg.clip), cfg.clip);
+  return kt + cfg.lambda * fminf(fmaxf(e, -cfg.clip), cfg.clip);
+}
+
+// Launch counter (eva_launch_count): incremented on the host per enqueue.
+void note_launch(int n = 1);
+
+}  // namespace eva

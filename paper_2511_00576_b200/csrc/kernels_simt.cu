@@ -1,0 +1,466 @@
+// kernels_simt.cu -- SIMT kernels of the FlashEVA hot path (sm_100a):
+//   summarize (one warp per chunk), the fp32 parity prefill, cache append,
+//   split-K decode + merge, and the debug mask / Philox / eps dumps.
+// The bf16 tensor-core prefill lives in prefill_sm100.cu.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+#include "summarize.cuh"
+
+namespace eva {
+
+// ============================================================================ summarize
+// grid: (ceil(nC / 4), bh_count); block 128 = 4 warps, warp w -> chunk 4*blockIdx.x + w.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) summarize_kernel(eva_config cfg, const T* __restrict__ K,
+                                                        const T* __restrict__ V,
+                                                        const float* __restrict__ eps,
+                                                        T* __restrict__ Ksum, T* __restrict__ Vsum) {
+  const int nC = cfg.T / cfg.chunk;
+  const int c = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int u = blockIdx.y;
+  if (c >= nC) return;
+  const int C = cfg.chunk;
+  const T* Kc = K + ((size_t)u * cfg.T + (size_t)c * C) * D;
+  const T* Vc = V + ((size_t)u * cfg.T + (size_t)c * C) * D;
+  auto rowK = [&](int i) { return Kc + (size_t)i * D; };
+  auto rowV = [&](int i) { return Vc + (size_t)i * D; };
+  const float* e = eps ? eps + ((size_t)u * nC + c) * D : nullptr;
+  summarize_chunk_warp<T, D>(rowK, rowV, C, e, (uint32_t)(cfg.bh_begin + u), (uint32_t)c, cfg,
+                             Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D);
+}
+
+// ============================================================================ SIMT prefill
+// One CTA = one unit x QT queries.  G threads cooperate on one query (thread gi
+// owns channels gi, gi+G, ... -> conflict-free smem reads); key/value tiles of
+// KT rows are staged in shared memory as fp32.  Two segments are walked in
+// order: the summary prefix [0, nsum(n_last)) and the local span
+// [lo(n_first), n_last]; each query applies its own (lo, nsum) (P:124 mask).
+template <typename T, int D>
+__global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, const T* __restrict__ Q,
+                                                           const T* __restrict__ K,
+                                                           const T* __restrict__ V,
+                                                           const T* __restrict__ Ksum,
+                                                           const T* __restrict__ Vsum,
+                                                           T* __restrict__ O, float* __restrict__ lse) {
+  constexpr int G = D >= 32 ? D / 32 : 1;
+  constexpr int CH = D / G;
+  constexpr int QT = 128 / G;
+  constexpr int KT = 32;
+  __shared__ float Ks[KT][D];
+  __shared__ float Vs[KT][D];
+
+  const int Tn = cfg.T, C = cfg.chunk, W = cfg.window;
+  const int nC = Tn / C;
+  const int u = blockIdx.y;
+  const int n0 = blockIdx.x * QT;
+  const int tid = threadIdx.x, qi = tid / G, gi = tid % G;
+  const int64_t n = (int64_t)n0 + qi;
+  const bool valid = n < Tn;
+  const int64_t nlast = min((int64_t)n0 + QT - 1, (int64_t)Tn - 1);
+  const Range rme = mask_range(valid ? n : nlast, C, W, cfg.mode);
+  const Range rfirst = mask_range(n0, C, W, cfg.mode);
+  const Range rlast = mask_range(nlast, C, W, cfg.mode);
+
+  float q[CH], acc[CH];
+  const T* qp = Q + ((size_t)u * Tn + (size_t)(valid ? n : nlast)) * D;
+#pragma unroll
+  for (int j = 0; j < CH; ++j) {
+    q[j] = Elem<T>::to_f(qp[j * G + gi]) * cfg.scale;
+    acc[j] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+
+  for (int seg = 0; seg < 2; ++seg) {
+    const T* kb = seg == 0 ? Ksum + (size_t)u * nC * D : K + (size_t)u * Tn * D;
+    const T* vb = seg == 0 ? Vsum + (size_t)u * nC * D : V + (size_t)u * Tn * D;
+    const int64_t beg = seg == 0 ? 0 : rfirst.lo;
+    const int64_t end = seg == 0 ? rlast.nsum : nlast + 1;
+    for (int64_t t0 = beg; t0 < end; t0 += KT) {
+      const int nk = (int)min((int64_t)KT, end - t0);
+      __syncthreads();
+      for (int i = tid; i < nk * D; i += 128) {
+        const int r = i / D, cc = i % D;
+        Ks[r][cc] = Elem<T>::to_f(kb[(size_t)(t0 + r) * D + cc]);
+        Vs[r][cc] = Elem<T>::to_f(vb[(size_t)(t0 + r) * D + cc]);
+      }
+      __syncthreads();
+      for (int j = 0; j < nk; ++j) {
+        float s = 0.f;
+#pragma unroll
+        for (int c2 = 0; c2 < CH; ++c2) s += q[c2] * Ks[j][c2 * G + gi];
+        s = group_sum<G>(s);
+        const int64_t t = t0 + j;
+        const bool vis = valid && (seg == 0 ? (t < rme.nsum) : (t >= rme.lo && t <= n));
+        if (vis) {
+          const float mn = fmaxf(m, s);
+          const float corr = __expf(m - mn);
+          const float p = __expf(s - mn);
+          l = l * corr + p;
+#pragma unroll
+          for (int c2 = 0; c2 < CH; ++c2) acc[c2] = acc[c2] * corr + p * Vs[j][c2 * G + gi];
+          m = mn;
+        }
+      }
+    }
+  }
+  if (valid) {
+    const float il = 1.0f / l;
+    T* op = O + ((size_t)u * Tn + (size_t)n) * D;
+#pragma unroll
+    for (int j = 0; j < CH; ++j) op[j * G + gi] = Elem<T>::from_f(acc[j] * il);
+    if (lse && gi == 0) lse[(size_t)u * Tn + n] = m + logf(l);
+  }
+}
+
+// ============================================================================ cache append
+// grid (bh_count, 1 + ceil(n_chunks / 4)), block 128.
+//   blockIdx.y == 0 : ring write of the last min(n_new, W) tokens (if do_ring)
+//   blockIdx.y >= 1 : warp w summarises chunk chunk0 + 4*(y-1) + w (if do_sum)
+// Rows of a chunk come from K_new (positions >= pos) or the ring (positions < pos).
+template <typename T, int D>
+__global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __restrict__ Kn,
+                                                     const T* __restrict__ Vn,
+                                                     const float* __restrict__ eps, int n_new,
+                                                     int do_ring, int do_sum, int64_t chunk0,
+                                                     int n_chunks) {
+  const int u = blockIdx.x;
+  const int W = c.cfg.window, C = c.cfg.chunk;
+  const int64_t pos = c.pos;
+  T* rk = static_cast<T*>(c.ring_k) + (size_t)u * W * D;
+  T* rv = static_cast<T*>(c.ring_v) + (size_t)u * W * D;
+  const T* kn = Kn + (size_t)u * n_new * D;
+  const T* vn = Vn + (size_t)u * n_new * D;
+  if (blockIdx.y == 0) {
+    if (!do_ring) return;
+    const int keep = min(n_new, W);
+    const int first = n_new - keep;
+    for (int i = threadIdx.x; i < keep * D; i += blockDim.x) {
+      const int r = first + i / D, cc = i % D;
+      const size_t slot = (size_t)((pos + r) % W);
+      rk[slot * D + cc] = kn[(size_t)r * D + cc];
+      rv[slot * D + cc] = vn[(size_t)r * D + cc];
+    }
+    return;
+  }
+  if (!do_sum) return;
+  const int ci = (blockIdx.y - 1) * 4 + (threadIdx.x >> 5);
+  if (ci >= n_chunks) return;
+  const int64_t chunk = chunk0 + ci;
+  const int64_t p0 = chunk * C;
+  auto rowK = [&](int i) -> const T* {
+    const int64_t p = p0 + i;
+    return p >= pos ? kn + (size_t)(p - pos) * D : rk + (size_t)(p % W) * D;
+  };
+  auto rowV = [&](int i) -> const T* {
+    const int64_t p = p0 + i;
+    return p >= pos ? vn + (size_t)(p - pos) * D : rv + (size_t)(p % W) * D;
+  };
+  const float* e = eps ? eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr;
+  T* sk = static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D;
+  T* sv = static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D;
+  summarize_chunk_warp<T, D>(rowK, rowV, C, e, (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk,
+                             c.cfg, sk, sv);
+}
+
+// ============================================================================ decode
+// grid (bh_count, splits), block 128 (4 warps).  The visible list of query
+// n = pos-1 is the summary prefix [0, nsum) followed by the ring positions
+// [lo, n] (slot p mod W).  Split s takes entries [s*E/S, (s+1)*E/S); warp w of
+// the CTA takes every 4th entry.  Online softmax per warp, merged in smem.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) decode_kernel(eva_cache c, const T* __restrict__ Q,
+                                                     T* __restrict__ O, float* __restrict__ lse,
+                                                     float* __restrict__ ws) {
+  using LM = LaneMap<D>;
+  constexpr int CPL = LM::CPL;
+  __shared__ float sm_m[4], sm_l[4];
+  __shared__ float sm_acc[4][D];
+  const int u = blockIdx.x, S = gridDim.y, s = blockIdx.y;
+  const int W = c.cfg.window, C = c.cfg.chunk;
+  const int64_t n = c.pos - 1;
+  const Range r = mask_range(n, C, W, c.cfg.mode);
+  const int64_t E = r.nsum + (n - r.lo + 1);
+  const int64_t e0 = E * s / S, e1 = E * (s + 1) / S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool act = lane < LM::LANES;
+  const int ch0 = lane * CPL;
+  const T* sk = static_cast<const T*>(c.sum_k) + (size_t)u * c.cap_chunks * D;
+  const T* sv = static_cast<const T*>(c.sum_v) + (size_t)u * c.cap_chunks * D;
+  const T* rk = static_cast<const T*>(c.ring_k) + (size_t)u * W * D;
+  const T* rv = static_cast<const T*>(c.ring_v) + (size_t)u * W * D;
+  float q[CPL], acc[CPL];
+  if (act) load_vec<T, CPL>(Q + (size_t)u * D + ch0, q);
+#pragma unroll
+  for (int j = 0; j < CPL; ++j) {
+    q[j] = act ? q[j] * c.cfg.scale : 0.f;
+    acc[j] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  for (int64_t e = e0 + warp; e < e1; e += 4) {
+    const T *kp, *vp;
+    if (e < r.nsum) {
+      kp = sk + (size_t)e * D;
+      vp = sv + (size_t)e * D;
+    } else {
+      const int64_t p = r.lo + (e - r.nsum);
+      kp = rk + (size_t)(p % W) * D;
+      vp = rv + (size_t)(p % W) * D;
+    }
+    float k[CPL], v[CPL], part = 0.f;
+    if (act) {
+      load_vec<T, CPL>(kp + ch0, k);
+      load_vec<T, CPL>(vp + ch0, v);
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) part += q[j] * k[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) v[j] = 0.f;
+    }
+    const float sc = warp_sum(part);
+    const float mn = fmaxf(m, sc);
+    const float corr = __expf(m - mn), p = __expf(sc - mn);
+    l = l * corr + p;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) acc[j] = acc[j] * corr + p * v[j];
+    m = mn;
+  }
+  if (lane == 0) { sm_m[warp] = m; sm_l[warp] = l; }
+  if (act) {
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) sm_acc[warp][ch0 + j] = acc[j];
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  float M = fmaxf(fmaxf(sm_m[0], sm_m[1]), fmaxf(sm_m[2], sm_m[3]));
+  float f[4], L = 0.f;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    f[w] = sm_m[w] == -INFINITY ? 0.f : __expf(sm_m[w] - M);
+    L += f[w] * sm_l[w];
+  }
+  if (!act) return;
+  float out[CPL];
+#pragma unroll
+  for (int j = 0; j < CPL; ++j)
+    out[j] = f[0] * sm_acc[0][ch0 + j] + f[1] * sm_acc[1][ch0 + j] + f[2] * sm_acc[2][ch0 + j] +
+             f[3] * sm_acc[3][ch0 + j];
+  if (S == 1) {
+    const float il = 1.0f / L;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) out[j] *= il;
+    store_vec<T, CPL>(O + (size_t)u * D + ch0, out);
+    if (lse && lane == 0) lse[u] = M + logf(L);
+  } else {
+    float* p = ws + ((size_t)u * S + s) * (D + 2);
+    if (lane == 0) { p[0] = M; p[1] = L; }
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) p[2 + ch0 + j] = out[j];
+  }
+}
+
+// Merge split-K partials: one warp per unit.
+template <typename T, int D>
+__global__ void __launch_bounds__(128) decode_merge_kernel(int bh_count, int S, const float* __restrict__ ws,
+                                                           T* __restrict__ O, float* __restrict__ lse) {
+  using LM = LaneMap<D>;
+  constexpr int CPL = LM::CPL;
+  const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (u >= bh_count) return;
+  const float* p = ws + (size_t)u * S * (D + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < S; ++s) M = fmaxf(M, p[(size_t)s * (D + 2)]);
+  float L = 0.f, out[CPL];
+#pragma unroll
+  for (int j = 0; j < CPL; ++j) out[j] = 0.f;
+  for (int s = 0; s < S; ++s) {
+    const float* q = p + (size_t)s * (D + 2);
+    const float f = q[0] == -INFINITY ? 0.f : __expf(q[0] - M);
+    L += f * q[1];
+    if (lane < LM::LANES) {
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) out[j] += f * q[2 + lane * CPL + j];
+    }
+  }
+  if (lane < LM::LANES) {
+    const float il = 1.0f / L;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) out[j] *= il;
+    store_vec<T, CPL>(O + (size_t)u * D + lane * CPL, out);
+  }
+  if (lse && lane == 0) lse[u] = M + logf(L);
+}
+
+// ============================================================================ debug kernels
+__global__ void mask_ranges_kernel(int C, int W, int mode, int64_t n0, int64_t count, int64_t* lo,
+                                   int64_t* nsum) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const Range r = mask_range(n0 + i, C, W, mode);
+  lo[i] = r.lo;
+  nsum[i] = r.nsum;
+}
+
+__global__ void philox_kernel(const uint32_t* in, uint32_t* out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t* a = in + (size_t)i * 6;
+  U4 r = philox4x32_10(U4{a[0], a[1], a[2], a[3]}, a[4], a[5]);
+  out[4 * i] = r.x; out[4 * i + 1] = r.y; out[4 * i + 2] = r.z; out[4 * i + 3] = r.w;
+}
+
+__global__ void draw_eps_kernel(eva_config cfg, int nC, float* eps) {
+  // one thread per (unit, chunk, block of 4 channels)
+  const int nb = (cfg.d_head + 3) / 4;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)cfg.bh_count * nC * nb) return;
+  const int b4 = (int)(i % nb);
+  const int c = (int)((i / nb) % nC);
+  const int u = (int)(i / ((int64_t)nb * nC));
+  const float4 z = philox_normal4(cfg.seed, cfg.layer, (uint32_t)(cfg.bh_begin + u), c, b4);
+  const float zz[4] = {z.x, z.y, z.z, z.w};
+  float* e = eps + ((size_t)u * nC + c) * cfg.d_head;
+  for (int j = 0; j < 4 && 4 * b4 + j < cfg.d_head; ++j) e[4 * b4 + j] = zz[j];
+}
+
+// ============================================================================ launchers
+#define EVA_DISPATCH_D(D_, ...)                               \
+  switch (D_) {                                               \
+    case 16: { constexpr int D = 16; __VA_ARGS__; } break;    \
+    case 32: { constexpr int D = 32; __VA_ARGS__; } break;    \
+    case 64: { constexpr int D = 64; __VA_ARGS__; } break;    \
+    case 128: { constexpr int D = 128; __VA_ARGS__; } break;  \
+    default: return cudaErrorInvalidValue;                    \
+  }
+#define EVA_DISPATCH_T(dt, ...)                                                 \
+  if ((dt) == EVA_BF16) { using T = __nv_bfloat16; __VA_ARGS__; }               \
+  else { using T = float; __VA_ARGS__; }
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
+                             void* Ksum, void* Vsum, cudaStream_t s) {
+  const int nC = cfg.T / cfg.chunk;
+  if (nC == 0 || cfg.bh_count == 0) return cudaSuccess;
+  dim3 grid((nC + 3) / 4, cfg.bh_count);
+  EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head,
+      summarize_kernel<T, D><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum,
+                                                  (T*)Vsum)));
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prefill_simt(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                const void* Ksum, const void* Vsum, void* O, float* lse,
+                                cudaStream_t s) {
+  if (cfg.bh_count == 0) return cudaSuccess;
+  EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
+    constexpr int G = D >= 32 ? D / 32 : 1;
+    constexpr int QT = 128 / G;
+    dim3 grid((cfg.T + QT - 1) / QT, cfg.bh_count);
+    prefill_simt_kernel<T, D><<<grid, 128, 0, s>>>(cfg, (const T*)Q, (const T*)K, (const T*)V,
+                                                   (const T*)Ksum, (const T*)Vsum, (T*)O, lse);
+  }));
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* Vn, int n_new,
+                                const float* eps, cudaStream_t s) {
+  const int C = c.cfg.chunk, W = c.cfg.window;
+  if (c.cfg.bh_count == 0) return cudaSuccess;
+  const int64_t chunk0 = c.pos / C;                      // first chunk not yet summarised
+  const int64_t chunk_end = (c.pos + n_new) / C;         // chunks complete after the append
+  const int n_chunks = (int)std::max<int64_t>(0, chunk_end - chunk0);
+  const int ygroups = (n_chunks + 3) / 4;
+  // Writing the ring can overwrite old positions still needed by a straddling
+  // chunk only if n_new > W - C + 1; then summaries go first.
+  const bool hazard = n_new > W - C + 1 && n_chunks > 0;
+  cudaError_t err = cudaSuccess;
+  EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
+    if (!hazard) {
+      dim3 grid(c.cfg.bh_count, 1 + ygroups);
+      append_kernel<T, D><<<grid, 128, 0, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 1, 1,
+                                               chunk0, n_chunks);
+      note_launch();
+    } else {
+      dim3 g1(c.cfg.bh_count, 1 + ygroups);
+      append_kernel<T, D><<<g1, 128, 0, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 0, 1,
+                                             chunk0, n_chunks);
+      dim3 g2(c.cfg.bh_count, 1);
+      append_kernel<T, D><<<g2, 128, 0, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 1, 0,
+                                             chunk0, 0);
+      note_launch(2);
+    }
+    err = cudaGetLastError();
+  }));
+  return err;
+}
+
+int decode_splits(const eva_cache& c) {
+  const int64_t n = c.pos - 1;
+  const Range r = mask_range(n, c.cfg.chunk, c.cfg.window, c.cfg.mode);
+  const int64_t E = r.nsum + (n - r.lo + 1);
+  const int64_t target = (int64_t)num_sms() * 8;  // CTAs for ~full occupancy
+  int64_t S = (target + c.cfg.bh_count - 1) / std::max(1, c.cfg.bh_count);
+  S = std::min<int64_t>(S, std::max<int64_t>(1, E / 64));
+  S = std::max<int64_t>(1, std::min<int64_t>(S, 64));
+  return (int)S;
+}
+
+cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse, float* ws,
+                          int splits, cudaStream_t s) {
+  if (c.cfg.bh_count == 0) return cudaSuccess;
+  EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
+    dim3 grid(c.cfg.bh_count, splits);
+    decode_kernel<T, D><<<grid, 128, 0, s>>>(c, (const T*)Q, (T*)O, lse, ws);
+    note_launch();
+    if (splits > 1) {
+      decode_merge_kernel<T, D><<<(c.cfg.bh_count + 3) / 4, 128, 0, s>>>(c.cfg.bh_count, splits,
+                                                                         ws, (T*)O, lse);
+      note_launch();
+    }
+  }));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mask_ranges(const eva_config& cfg, int64_t n0, int64_t count, int64_t* lo,
+                               int64_t* nsum, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  mask_ranges_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(cfg.chunk, cfg.window, cfg.mode,
+                                                                    n0, count, lo, nsum);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_philox(const uint32_t* in, uint32_t* out, int n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  philox_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, out, n);
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_draw_eps(const eva_config& cfg, float* eps, cudaStream_t s) {
+  const int nC = cfg.T / cfg.chunk;
+  const int64_t total = (int64_t)cfg.bh_count * nC * ((cfg.d_head + 3) / 4);
+  if (total == 0) return cudaSuccess;
+  draw_eps_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(cfg, nC, eps);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace eva

@@ -1,0 +1,45 @@
+// launch.h -- internal (C++) launchers behind the C ABI in api.cu.
+// Arguments are validated by api.cu before any of these is called.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/eva.h"
+
+namespace eva {
+
+// eva_summarize: K, V [bh, T, d] -> Ksum, Vsum [bh, nC, d].
+cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
+                             void* Ksum, void* Vsum, cudaStream_t s);
+
+// SIMT prefill (fp32 parity path; any supported d, either dtype).
+cudaError_t launch_prefill_simt(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                const void* Ksum, const void* Vsum, void* O, float* lse,
+                                cudaStream_t s);
+
+// tcgen05/TMEM/TMA prefill (bf16, d in {64, 128}).  Returns cudaErrorNotSupported if the
+// shape is outside the kernel's envelope (the caller then reports EVA_ERR_UNSUPPORTED).
+bool prefill_sm100_supported(const eva_config& cfg);
+cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                 const void* Ksum, const void* Vsum, void* O, float* lse,
+                                 cudaStream_t s);
+
+// Cache append: summaries of chunks completed in [pos, pos+n_new), ring write of the
+// last min(n_new, W) tokens.
+cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* Vn, int n_new,
+                                const float* eps, cudaStream_t s);
+
+// Decode: splits chosen by the host (workspace needed when splits > 1).
+int decode_splits(const eva_cache& c);
+cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse, float* ws,
+                          int splits, cudaStream_t s);
+
+cudaError_t launch_mask_ranges(const eva_config& cfg, int64_t n0, int64_t count, int64_t* lo,
+                               int64_t* nsum, cudaStream_t s);
+cudaError_t launch_philox(const uint32_t* in, uint32_t* out, int n, cudaStream_t s);
+cudaError_t launch_draw_eps(const eva_config& cfg, float* eps, cudaStream_t s);
+
+int num_sms();
+
+}  // namespace eva

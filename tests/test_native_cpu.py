@@ -1,0 +1,125 @@
+"""CPU-side checks of libeva.so: it loads, exports every symbol include/eva.h
+declares, and its synchronous host logic (defaults, argument validation,
+capacity accounting, workspace sizing) behaves as documented.  No kernel is
+launched here (there is no GPU on the build host)."""
+import ctypes
+import math
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "eva.h")
+
+
+@pytest.fixture(scope="module")
+def N():
+    from paper_2511_00576_b200 import _native
+    return _native
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(eva_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(N):
+    names = _declared()
+    assert "eva_attn_prefill" in names and "eva_cache_append" in names
+    for nm in names:
+        assert hasattr(N.lib, nm), nm
+    assert set(names) == set(N.EXPORTS)
+
+
+def test_struct_layouts_match_header(N):
+    assert ctypes.sizeof(N.EvaConfig) == 15 * 4 + 4 + 8  # 16 x 4-byte fields (+pad) + u64
+    assert N.EvaConfig.seed.offset == 64
+    assert N.EvaCache.pos.offset == ctypes.sizeof(N.EvaConfig)
+    assert N.EvaCache.ring_k.offset == ctypes.sizeof(N.EvaConfig) + 16
+
+
+def test_config_defaults(N):
+    cfg = N.EvaConfig()
+    N.lib.eva_config_default(ctypes.byref(cfg), 8, 32, 8192, 128, 64, 256)
+    assert (cfg.B, cfg.H, cfg.bh_begin, cfg.bh_count) == (8, 32, 0, 256)
+    assert (cfg.T, cfg.d_head, cfg.chunk, cfg.window, cfg.samples) == (8192, 128, 64, 256, 1)
+    assert cfg.mode == N.EVA_WINDOW_SLIDING and cfg.dtype == N.EVA_BF16
+    assert abs(cfg.scale - 1 / math.sqrt(128)) < 1e-7
+    assert abs(cfg.lambda_ - 0.1) < 1e-7 and cfg.clip == 1.0
+    assert N.lib.eva_version().decode().startswith("flasheva-b200")
+
+
+def _cfg(N, **kw):
+    cfg = N.EvaConfig()
+    N.lib.eva_config_default(ctypes.byref(cfg), 1, 2, 64, 32, 8, 16)
+    for k, v in kw.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+FAKE = ctypes.c_void_p(0x10000)  # aligned, never dereferenced: validation fails first
+
+
+@pytest.mark.parametrize("field,value,status", [
+    ("window", 12, 1), ("chunk", 0, 1), ("T", 0, 1), ("B", 0, 1), ("bh_count", 3, 1),
+    ("bh_begin", -1, 1), ("mode", 7, 1), ("dtype", 5, 1), ("omega_mode", 2, 1),
+    ("samples", 2, 2), ("d_head", 48, 2), ("d_head", 256, 2)])
+def test_validation_rejects_bad_configs(N, field, value, status):
+    cfg = _cfg(N, **{field: value})
+    st = N.lib.eva_summarize(ctypes.byref(cfg), FAKE, FAKE, None, FAKE, FAKE, None)
+    assert st == status
+    assert len(N.lib.eva_last_error()) > 0
+    st = N.lib.eva_attn_prefill(ctypes.byref(cfg), FAKE, FAKE, FAKE, FAKE, FAKE, None, FAKE, None, 0, None)
+    assert st == status
+
+
+def test_validation_rejects_null_and_misaligned_pointers(N):
+    cfg = _cfg(N)
+    st = N.lib.eva_attn_prefill(ctypes.byref(cfg), None, FAKE, FAKE, FAKE, FAKE, None, FAKE, None, 0, None)
+    assert st == N.EVA_ERR_INVALID_ARG and b"Q" in N.lib.eva_last_error()
+    st = N.lib.eva_attn_prefill(ctypes.byref(cfg), FAKE, ctypes.c_void_p(0x10002), FAKE, FAKE, FAKE,
+                                None, FAKE, None, 0, None)
+    assert st == N.EVA_ERR_INVALID_ARG and b"aligned" in N.lib.eva_last_error()
+    st = N.lib.eva_attn_prefill(ctypes.byref(cfg), FAKE, FAKE, FAKE, FAKE, FAKE, None, FAKE, None, 0x80, None)
+    assert st == N.EVA_ERR_INVALID_ARG
+
+
+def _cache(N, pos, cap, **kw):
+    c = N.EvaCache()
+    c.cfg = _cfg(N, **kw)
+    c.pos = pos
+    c.cap_chunks = cap
+    c.ring_k = c.ring_v = c.sum_k = c.sum_v = 0x10000
+    return c
+
+
+def test_cache_capacity_and_position_logic(N):
+    c = _cache(N, 0, 2)  # C = 8: room for 2 summaries -> positions < 24
+    assert N.lib.eva_cache_append(ctypes.byref(c), FAKE, FAKE, 24, None, None) == N.EVA_ERR_CAPACITY
+    assert c.pos == 0  # unchanged on failure
+    assert N.lib.eva_cache_append(ctypes.byref(c), FAKE, FAKE, 0, None, None) == N.EVA_ERR_INVALID_ARG
+    d = _cache(N, 0, 1)
+    assert N.lib.eva_attn_decode(ctypes.byref(d), FAKE, FAKE, None, None, 0, None) == N.EVA_ERR_INVALID_ARG
+    e = _cache(N, 40, 1)  # query 39: nsum = 39//8 - 2 + 1 = 3 > cap 1
+    assert N.lib.eva_attn_decode(ctypes.byref(e), FAKE, FAKE, None, None, 0, None) == N.EVA_ERR_CAPACITY
+
+
+def test_decode_workspace_bytes(N):
+    small = _cache(N, 1, 4)  # 2 units, 1 visible entry -> a single split, no workspace
+    assert N.lib.eva_decode_workspace_bytes(ctypes.byref(small)) == 0
+    long = _cache(N, 4000, 600, bh_count=2)
+    ws = N.lib.eva_decode_workspace_bytes(ctypes.byref(long))
+    assert ws > 0 and ws % (2 * (32 + 2) * 4) == 0
+
+
+def test_product_package_does_not_import_oracle():
+    """The product path never imports oracle/ (DESIGN.md §4)."""
+    pkg = os.path.join(ROOT, "paper_2511_00576_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "eva_oracle" not in txt and "liboracle" not in txt, f

@@ -1,0 +1,347 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Tolerances (north_star): max |GPU - oracle| <= 1e-4 on the fp32
+path and <= 2e-2 on the bf16 path for O, LSE, Ksum, Vsum on unit-variance
+inputs; mask ranges and Philox words bit-exact.  Both sides consume the same
+seeded inputs (eva_inputs) and the same eps (caller-supplied, or the two
+independent Philox implementations).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import eva_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def eva(cuda_device):
+    import paper_2511_00576_b200 as eva
+    return eva
+
+
+def f64(t):
+    return t.detach().float().cpu().double().numpy()
+
+
+def oracle_eps_for(cfg, nC, d):
+    return oracle.eps_units(cfg.seed, cfg.layer, cfg.bh_begin, cfg.bh_count, nC, d)
+
+
+def run_oracle(Q, K, V, E, C, W, mode, scale):
+    ks, vs = oracle.summarize_batch(f64(K), f64(V), E, C)
+    O, lse = oracle.prefill_batch(f64(Q), f64(K), f64(V), ks, vs, C, W, mode, scale)
+    return ks, vs, O, lse
+
+
+# ----------------------------------------------------------------------------- bit-exact pieces
+def test_philox_bit_exact(eva):
+    rng = np.random.default_rng(0)
+    blocks = rng.integers(0, 2 ** 32, size=(256, 6), dtype=np.uint64).astype(np.int64)
+    blocks[0] = 0
+    blocks[1] = 0xFFFFFFFF
+    out = eva.eva_philox(torch.from_numpy(blocks)).cpu().numpy()
+    for i in range(blocks.shape[0]):
+        b = [int(x) for x in blocks[i]]
+        assert [int(x) for x in out[i]] == oracle.philox4x32_10(b[:4], b[4:])
+
+
+@pytest.mark.parametrize("d", [16, 64, 128])
+def test_draw_eps_matches_oracle(eva, d):
+    cfg = eva.make_config(2, 3, 640, d, 64, 128, bh_begin=1, bh_count=4, seed=0xABCDEF0123, layer=5)
+    e = f64(eva.eva_draw_eps(cfg))
+    ref = oracle_eps_for(cfg, 10, d)
+    assert np.max(np.abs(e - ref)) < 2e-5
+
+
+@pytest.mark.parametrize("mode", ["sliding", "block"])
+@pytest.mark.parametrize("C,W", [(1, 1), (1, 5), (4, 4), (8, 32), (64, 256), (16, 64)])
+def test_mask_ranges_bit_exact(eva, mode, C, W):
+    cfg = eva.make_config(1, 1, 1, 16, C, W, mode=mode)
+    lo, ns = eva.eva_mask_ranges(cfg, 0, 20000)
+    lo, ns = lo.cpu().numpy(), ns.cpu().numpy()
+    m = oracle.SLIDING if mode == "sliding" else oracle.BLOCK
+    for n in list(range(0, 3000)) + list(range(19000, 20000)):
+        assert (lo[n], ns[n]) == oracle.mask(n, C, W, m)
+
+
+# ----------------------------------------------------------------------------- summaries
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("d", [16, 32, 64, 128])
+@pytest.mark.parametrize("philox", [False, True])
+def test_summarize_parity(eva, dtype, d, philox):
+    B, H, T, C = 1, 3, 200, 16
+    cfg = eva.make_config(B, H, T, d, C, 32, dtype=dtype, seed=99)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=1, device="cuda")
+    nC = T // C
+    eps = None if philox else eva_inputs.eps(0, B * H, nC, d, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V, eps=eps)
+    E = oracle_eps_for(cfg, nC, d) if philox else f64(eps)
+    rk, rv = oracle.summarize_batch(f64(K), f64(V), E, C)
+    assert np.max(np.abs(f64(ks) - rk)) <= TOL[dtype]
+    assert np.max(np.abs(f64(vs) - rv)) <= TOL[dtype]
+
+
+def test_summarize_singleton_and_constant_chunks(eva):
+    """C = 1 -> (k~, beta) = (k, v) exactly; a constant chunk -> its own (k, v)."""
+    Q, K, V = eva_inputs.qkv(0, 2, 64, 64, torch.float32, seed=4, device="cuda")
+    cfg = eva.make_config(1, 2, 64, 64, 1, 4, dtype=torch.float32)
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    assert torch.equal(ks, K) and torch.max((vs - V).abs()).item() < 1e-6
+    Kc = K[:, :1].expand(2, 64, 64).contiguous()
+    Vc = V[:, :1].expand(2, 64, 64).contiguous()
+    cfg = eva.make_config(1, 2, 64, 64, 16, 32, dtype=torch.float32)
+    ks, vs = eva.eva_summarize(cfg, Kc, Vc)
+    assert torch.max((ks - Kc[:, :4]).abs()).item() < 1e-6
+    assert torch.max((vs - Vc[:, :4]).abs()).item() < 1e-5
+
+
+# ----------------------------------------------------------------------------- prefill
+CASES = [  # (B, H, T, d, C, W)
+    (1, 1, 256, 16, 16, 32),      # configs[0]
+    (1, 2, 300, 32, 8, 24),       # ragged T, W = 3C
+    (2, 1, 515, 64, 64, 128),     # configs[1] shape family, ragged tail
+    (1, 2, 700, 128, 64, 256),    # configs[2] shape family
+    (1, 1, 130, 64, 16, 16),      # W = C: a tile consumes summaries of its own rows
+    (1, 1, 40, 64, 64, 128),      # T < C: no summaries at all
+    (1, 1, 1, 128, 4, 8),         # T = 1
+    (1, 1, 96, 64, 1, 3),         # C = 1: exact causal softmax
+]
+
+
+@pytest.mark.parametrize("mode", ["sliding", "block"])
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("dtype,simt", [(torch.float32, True), (torch.bfloat16, True),
+                                        (torch.bfloat16, False)])
+def test_prefill_parity(eva, case, mode, dtype, simt):
+    B, H, T, d, C, W = case
+    cfg = eva.make_config(B, H, T, d, C, W, mode=mode, dtype=dtype, seed=7)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=2, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=simt)
+    torch.cuda.synchronize()
+    nC = T // C
+    E = oracle_eps_for(cfg, nC, d)
+    m = oracle.SLIDING if mode == "sliding" else oracle.BLOCK
+    rk, rv, rO, rl = run_oracle(Q, K, V, E, C, W, m, cfg.scale)
+    tol = TOL[dtype]
+    if nC:
+        assert np.max(np.abs(f64(ks) - rk)) <= tol
+        assert np.max(np.abs(f64(vs) - rv)) <= tol
+    err = np.max(np.abs(f64(O) - rO))
+    assert err <= tol, err
+    assert np.max(np.abs(f64(lse) - rl)) <= tol
+
+
+@pytest.mark.parametrize("dtype,simt", [(torch.float32, True), (torch.bfloat16, False)])
+def test_prefill_window_covers_sequence_is_softmax(eva, dtype, simt):
+    """W >= T reduces to exact causal softmax: compare with torch SDPA in fp64."""
+    T, d = 256, 64
+    cfg = eva.make_config(1, 2, T, d, 64, 256, dtype=dtype)
+    Q, K, V = eva_inputs.qkv(0, 2, T, d, dtype, seed=3, device="cuda")
+    O, _, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, simt=simt)
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        Q.double(), K.double(), V.double(), is_causal=True, scale=cfg.scale)
+    assert (O.double() - ref).abs().max().item() <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype,simt", [(torch.float32, True), (torch.bfloat16, False)])
+def test_prefill_summaries_provided_and_poison(eva, dtype, simt):
+    """Everything a query block must not see is poisoned with large finite values;
+    its outputs must not move (bit-exact).  Uses EVA_SUMMARIES_PROVIDED."""
+    T, d, C, W = 1024, 64, 64, 128
+    cfg = eva.make_config(1, 1, T, d, C, W, dtype=dtype)
+    Q, K, V = eva_inputs.qkv(0, 1, T, d, dtype, seed=5, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    O, lse, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, simt=simt)
+    n0, n1 = 512, 639  # one 128-query block
+    lo0, _ = oracle.mask(n0, C, W, 0)
+    _, ns1 = oracle.mask(n1, C, W, 0)
+    K2, V2, ks2, vs2 = K.clone(), V.clone(), ks.clone(), vs.clone()
+    K2[:, :lo0] = 3e4
+    V2[:, :lo0] = -3e4
+    K2[:, n1 + 1:] = 3e4
+    V2[:, n1 + 1:] = 3e4
+    ks2[:, ns1:] = 3e4
+    vs2[:, ns1:] = -3e4
+    O2, lse2, _, _ = eva.eva_attn_prefill(cfg, Q, K2, V2, Ksum=ks2, Vsum=vs2, summaries_provided=True,
+                                          simt=simt)
+    assert torch.equal(O2[:, n0:n1 + 1], O[:, n0:n1 + 1])
+    assert torch.equal(lse2[:, n0:n1 + 1], lse[:, n0:n1 + 1])
+
+
+@pytest.mark.parametrize("mode", ["sliding", "block"])
+@pytest.mark.parametrize("dtype,simt", [(torch.float32, True), (torch.bfloat16, False)])
+def test_prefill_position_probe(eva, mode, dtype, simt):
+    """q = k = 0: every logit is 0, xi = 1, k~ = 0, beta = chunk mean of v.  With
+    v_m = (1, (m mod 64)/8) (exact in bf16) each output is the mean over exactly the
+    visible set; an off-by-one in any range moves it by >= 1/8/64 > tolerance... x8."""
+    T, d, C, W = 640, 64, 16, 64
+    cfg = eva.make_config(1, 1, T, d, C, W, mode=mode, dtype=dtype)
+    Q = torch.zeros(1, T, d, dtype=dtype, device="cuda")
+    K = torch.zeros_like(Q)
+    V = torch.zeros_like(Q)
+    V[0, :, 0] = 1.0
+    V[0, :, 1] = (torch.arange(T, device="cuda", dtype=torch.float32) % 64).to(dtype) / 8.0
+    O, _, _, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=simt)
+    m = oracle.SLIDING if mode == "sliding" else oracle.BLOCK
+    Of = O.float().cpu().numpy()[0]
+    for n in range(T):
+        lo, ns = oracle.mask(n, C, W, m)
+        vals = [((c * C) % 64 + (C - 1) / 2) / 8.0 for c in range(ns)] + \
+            [(x % 64) / 8.0 for x in range(lo, n + 1)]
+        assert abs(Of[n, 0] - 1.0) < 1e-2
+        assert abs(Of[n, 1] - np.mean(vals)) <= 2e-2 * max(1.0, abs(np.mean(vals)) / 8), n
+
+
+def test_prefill_detects_beta_perturbation(eva):
+    """SPEC fault injection: a 1e-3 perturbation of one beta must fail the
+    suite: the Vsum gate (1e-4) trips, and exactly the rows that see that summary move."""
+    T, d, C, W = 512, 32, 16, 32
+    cfg = eva.make_config(1, 1, T, d, C, W, dtype=torch.float32)
+    Q, K, V = eva_inputs.qkv(0, 1, T, d, torch.float32, seed=6, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    O0, _, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, simt=True)
+    E = oracle_eps_for(cfg, T // C, d)
+    rk, rv = oracle.summarize_batch(f64(K), f64(V), E, C)
+    assert np.max(np.abs(f64(vs) - rv)) <= 1e-4
+    vs[0, 3] += 1e-3
+    assert np.max(np.abs(f64(vs) - rv)) > 1e-4  # the parity gate on Vsum now fails
+    O1, _, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, simt=True)
+    moved = (O1 != O0).any(dim=-1)[0].cpu().numpy()
+    sees = np.array([oracle.mask(n, C, W, 0)[1] > 3 for n in range(T)])
+    assert np.array_equal(moved, sees)
+
+
+@pytest.mark.parametrize("dtype,simt", [(torch.float32, True), (torch.bfloat16, False)])
+def test_sharded_equals_unsharded(eva, dtype, simt):
+    """(b,h) shards computed separately are bitwise equal to the full run (RNG keyed by global unit)."""
+    B, H, T, d, C, W = 2, 3, 384, 64, 32, 64
+    cfg = eva.make_config(B, H, T, d, C, W, dtype=dtype)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=8, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=simt)
+    for b0, cnt in ((0, 2), (2, 3), (5, 1)):
+        c2 = eva.make_config(B, H, T, d, C, W, dtype=dtype, bh_begin=b0, bh_count=cnt)
+        q, k, v = eva_inputs.qkv(b0, cnt, T, d, dtype, seed=8, device="cuda")
+        O2, lse2, ks2, vs2 = eva.eva_attn_prefill(c2, q, k, v, simt=simt)
+        assert torch.equal(O2, O[b0:b0 + cnt]) and torch.equal(lse2, lse[b0:b0 + cnt])
+        assert torch.equal(ks2, ks[b0:b0 + cnt]) and torch.equal(vs2, vs[b0:b0 + cnt])
+
+
+def test_errors_are_reported_not_silent(eva):
+    cfg = eva.make_config(1, 1, 64, 64, 16, 40)  # W % C != 0
+    Q = torch.zeros(1, 64, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(eva.EvaError, match="INVALID_ARG"):
+        eva.eva_attn_prefill(cfg, Q, Q, Q)
+    cfg = eva.make_config(1, 1, 64, 64, 16, 32, samples=4)
+    with pytest.raises(eva.EvaError, match="UNSUPPORTED"):
+        eva.eva_attn_prefill(cfg, Q, Q, Q)
+
+
+# ----------------------------------------------------------------------------- decode
+@pytest.mark.parametrize("mode", ["sliding", "block"])
+@pytest.mark.parametrize("dtype,d,C,W", [(torch.float32, 32, 8, 24), (torch.bfloat16, 128, 16, 64),
+                                         (torch.bfloat16, 64, 4, 4), (torch.float32, 16, 1, 3)])
+def test_decode_streaming_parity(eva, mode, dtype, d, C, W):
+    """Token-by-token append + decode == oracle streaming cache at every step."""
+    BH, T = 3, 150
+    cfg = eva.make_config(1, BH, 0, d, C, W, mode=mode, dtype=dtype, seed=11)
+    cap = T // C
+    cache = eva.DecodeCache(cfg, cap, device="cuda")
+    q, k, v = eva_inputs.decode_tokens(0, BH, T, d, dtype, seed=12, device="cuda")
+    m = oracle.SLIDING if mode == "sliding" else oracle.BLOCK
+    orc = [oracle.Cache(d, C, W, m, cap=cap, scale=cfg.scale) for _ in range(BH)]
+    E = oracle_eps_for(cfg, cap + 1, d)
+    worst = 0.0
+    for t in range(T):
+        cache.eva_cache_append(k[t], v[t])
+        o, lse = cache.eva_attn_decode(q[t])
+        of, lf = f64(o), f64(lse)
+        for u in range(BH):
+            assert orc[u].append(f64(k[t, u]), f64(v[t, u]), E[u, t // C]) == 0
+            ro, rl = orc[u].decode(f64(q[t, u]))
+            worst = max(worst, np.max(np.abs(of[u] - ro)), abs(lf[u] - rl))
+    assert worst <= TOL[dtype], worst
+    # the cache's summaries equal the oracle's
+    rks, rvs = orc[1].summaries()
+    n = cache.pos // C
+    assert np.max(np.abs(f64(cache.sum_k[1, :n]) - rks)) <= TOL[dtype]
+    assert np.max(np.abs(f64(cache.sum_v[1, :n]) - rvs)) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_prefill_handoff_then_decode(eva, dtype):
+    """append(n_new = T) after a prompt, then token-by-token: each decoded row equals
+    the prefill row of the extended sequence."""
+    BH, T0, G, d, C, W = 2, 1000, 70, 64, 64, 128
+    T = T0 + G
+    cfg = eva.make_config(1, BH, T, d, C, W, dtype=dtype, seed=21)
+    Q, K, V = eva_inputs.qkv(0, BH, T, d, dtype, seed=22, device="cuda")
+    O_full, lse_full, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, simt=True)
+    cache = eva.DecodeCache(cfg, T // C + 1, device="cuda")
+    cache.eva_cache_append(K[:, :T0].contiguous(), V[:, :T0].contiguous())
+    o, lse = cache.eva_attn_decode(Q[:, T0 - 1].contiguous())
+    outs = [o]
+    for t in range(T0, T):
+        cache.eva_cache_append(K[:, t].contiguous(), V[:, t].contiguous())
+        o, lse = cache.eva_attn_decode(Q[:, t].contiguous())
+        outs.append(o)
+    dec = torch.stack(outs, 1)
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    assert (dec.float() - O_full[:, T0 - 1:].float()).abs().max().item() <= tol
+
+
+def test_decode_poisoned_stale_ring_slots(eva):
+    """Stale / invisible ring slots and unused summary rows are poisoned; output unchanged."""
+    BH, d, C, W, T = 2, 64, 16, 64, 300
+    cfg = eva.make_config(1, BH, 0, d, C, W, dtype=torch.bfloat16)
+    cache = eva.DecodeCache(cfg, 32, device="cuda")
+    q, k, v = eva_inputs.decode_tokens(0, BH, T, d, torch.bfloat16, seed=13, device="cuda")
+    for t in range(T):
+        cache.eva_cache_append(k[t], v[t])
+    o, lse = cache.eva_attn_decode(q[T - 1])
+    n = T - 1
+    lo, ns = oracle.mask(n, C, W, 0)
+    for p in range(n - W + 1, lo):  # still in the ring but not visible
+        cache.ring_k[:, p % W] = 3e4
+        cache.ring_v[:, p % W] = 3e4
+    cache.sum_k[:, ns:] = 3e4
+    cache.sum_v[:, ns:] = -3e4
+    o2, lse2 = cache.eva_attn_decode(q[T - 1])
+    assert torch.equal(o, o2) and torch.equal(lse, lse2)
+
+
+def test_decode_capacity_error(eva):
+    cfg = eva.make_config(1, 1, 0, 64, 16, 32)
+    cache = eva.DecodeCache(cfg, 1, device="cuda")
+    x = torch.zeros(1, 31, 64, dtype=torch.bfloat16, device="cuda")
+    cache.eva_cache_append(x, x)
+    with pytest.raises(eva.EvaError, match="CAPACITY"):
+        cache.eva_cache_append(x[:, :1], x[:, :1])
+
+
+# ----------------------------------------------------------------------------- full-size sampled parity
+@pytest.mark.parametrize("B,H,T,d,C,W", [(1, 16, 2048, 64, 64, 128), (1, 4, 8192, 128, 64, 256)])
+def test_full_size_sampled_parity(eva, B, H, T, d, C, W):
+    """BASELINE configs[1] (full) and configs[2] (4 of its 256 units, same kernel launch
+    shape per unit) on the bf16 tensor-core path; oracle on sampled rows."""
+    cfg = eva.make_config(B, H, T, d, C, W, dtype=torch.bfloat16)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    nC = T // C
+    rng = np.random.default_rng(1)
+    for u in (0, B * H - 1):
+        E = oracle.eps(cfg.seed, cfg.layer, u, nC, d)
+        rk, rv = oracle.summarize(f64(K[u]), f64(V[u]), E, C)
+        assert np.max(np.abs(f64(ks[u]) - rk)) <= 2e-2
+        assert np.max(np.abs(f64(vs[u]) - rv)) <= 2e-2
+        rows = np.unique(np.concatenate([rng.integers(0, T, 200), [0, 1, C - 1, C, W - 1, W, T - 1]]))
+        rows, rO, rl = oracle.prefill_rows(f64(Q[u]), f64(K[u]), f64(V[u]), rk, rv, rows, C, W, 0,
+                                           cfg.scale)
+        assert np.max(np.abs(f64(O[u])[rows] - rO)) <= 2e-2
+        assert np.max(np.abs(f64(lse[u])[rows] - rl)) <= 2e-2
