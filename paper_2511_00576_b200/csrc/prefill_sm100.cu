@@ -1,11 +1,357 @@
-// prefill_sm100.cu -- tcgen05/TMEM/TMA bf16 FlashEVA prefill (placeholder until the
-// tensor-core kernel lands; the SIMT kernel serves every shape meanwhile).
+// prefill_sm100.cu -- bf16 FlashEVA chunk-causal prefill on the sm_100a tensor cores.
+//
+// Computes, for every query n of a 128-query tile (Eq.12-14, mask P:124):
+//   o_n = softmax over { s q_n.k~_c : c < nsum(n) }  U  { s q_n.k_m : lo(n) <= m <= n }
+// with the summary prefix and the local span walked as 64-key tiles.
+//
+// CTA = one (unit, 128-query tile); 6 warps, warp-specialised:
+//   warp 0      TMA producer: Q tile once, then K/V (or Ksum/Vsum) 64-row tiles into an
+//               NSTAGE-deep shared-memory ring (SWIZZLE_128B, mbarrier complete_tx)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
+//                 S_j  = Q K_j^T      (SS, M=128 N=64 K=d)  -> TMEM S buffer j%2
+//                 O   += P_j V_j      (TS, M=128 N=d K=64)   P_j read from TMEM
+//               issue order S_0, S_1, PV_0, S_2, PV_1, ... so S_{j+1} overlaps softmax j
+//   warps 2..5  softmax: thread <-> TMEM lane <-> query row.  tcgen05.ld S, apply the
+//               per-row chunk-causal mask, online max (lazy rescale: O in TMEM is only
+//               corrected when the running max grows by > 2^8), P = exp2(...) packed to
+//               bf16 and tcgen05.st back into the S buffer, arrive p_full.
+//               Epilogue: O / l -> bf16 -> swizzled smem -> TMA store; LSE.
+// TMEM (256 columns): [0,64) S/P buffer 0, [64,128) S/P buffer 1, [128,128+d) O.
+// Two CTAs fit on one SM (smem <= ~97 KB, 256 TMEM columns each).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "common.cuh"
 #include "launch.h"
+#include "sm100.cuh"
 
 namespace eva {
-bool prefill_sm100_supported(const eva_config&) { return false; }
-cudaError_t launch_prefill_sm100(const eva_config&, const void*, const void*, const void*,
-                                 const void*, const void*, void*, float*, cudaStream_t) {
+namespace {
+
+using namespace sm100;
+constexpr int BM = 128;       // queries per tile
+constexpr int BN = 64;        // keys per KV tile
+constexpr int NTHREADS = 192;
+constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TM_O = 128;
+
+template <int D, int NSTAGE>
+struct __align__(1024) Smem {
+  __nv_bfloat16 q[BM * D];               // D/64 sub-tiles [128][64], 16 KB each
+  __nv_bfloat16 k[NSTAGE][BN * D];       // D/64 sub-tiles [64][64], 8 KB each
+  __nv_bfloat16 v[NSTAGE][BN * D];
+  uint64_t q_full;
+  uint64_t k_full[NSTAGE], v_full[NSTAGE], kv_empty[NSTAGE];
+  uint64_t s_full[2], p_full[2], o_done, o_final;
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+struct TilePlan {
+  int n0, nlast, n_st, n_lt, lo0;
+  __device__ TilePlan(int qt, int T, int C, int W, int mode) {
+    n0 = qt * BM;
+    nlast = min(n0 + BM - 1, T - 1);
+    const Range rf = mask_range(n0, C, W, mode), rl = mask_range(nlast, C, W, mode);
+    n_st = (int)((rl.nsum + BN - 1) / BN);
+    lo0 = (int)rf.lo;
+    n_lt = (nlast - lo0 + 1 + BN - 1) / BN;
+  }
+  __device__ int count() const { return n_st + n_lt; }
+  __device__ bool summary(int j) const { return j < n_st; }
+  __device__ int base(int j) const { return j < n_st ? j * BN : lo0 + (j - n_st) * BN; }
+};
+
+template <int D, int NSTAGE>
+__global__ void __launch_bounds__(NTHREADS, 2)
+prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
+                     const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
+                     int T, int C, int W, int mode, float scale_log2, float* __restrict__ lse) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem<D, NSTAGE>* sm = reinterpret_cast<Smem<D, NSTAGE>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.y;
+  const TilePlan plan(blockIdx.x, T, C, W, mode);
+  const int NT = plan.count();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
+    tma_prefetch(&mKs); tma_prefetch(&mVs); tma_prefetch(&mO);
+    mbar_init(&sm->q_full, 1);
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm->k_full[s], 1);
+      mbar_init(&sm->v_full[s], 1);
+      mbar_init(&sm->kv_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm->s_full[b], 1);
+      mbar_init(&sm->p_full[b], 128);
+    }
+    mbar_init(&sm->o_done, 1);
+    mbar_init(&sm->o_final, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm->tmem_base, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
+      for (int kb = 0; kb < D / 64; ++kb)
+        tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
+      for (int j = 0; j < NT; ++j) {
+        const int s = j % NSTAGE;
+        if (j >= NSTAGE) mbar_wait(&sm->kv_empty[s], ((j / NSTAGE) - 1) & 1);
+        const bool summ = plan.summary(j);
+        const int row = plan.base(j);
+        const CUtensorMap* mk = summ ? &mKs : &mK;
+        const CUtensorMap* mv = summ ? &mVs : &mV;
+        mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb)
+          tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, row, u);
+        mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb)
+          tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, row, u);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
+      const uint32_t q_addr = smem_u32(sm->q);
+      mbar_wait(&sm->q_full, 0);
+      for (int j = 0; j <= NT; ++j) {
+        if (j < NT) {
+          const int s = j % NSTAGE;
+          mbar_wait(&sm->k_full[s], (j / NSTAGE) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(sm->k[s]);
+          const uint32_t d_tmem = tmem + (uint32_t)(j & 1) * BN;
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+            const uint64_t a = smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024);
+            const uint64_t b = smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024);
+            mma_ss(d_tmem, a, b, idesc_s, ks > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm->s_full[j & 1]);
+        }
+        if (j >= 1) {
+          const int jj = j - 1, s = jj % NSTAGE;
+          mbar_wait(&sm->p_full[jj & 1], (jj >> 1) & 1);
+          mbar_wait(&sm->v_full[s], (jj / NSTAGE) & 1);
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(sm->v[s]);
+#pragma unroll
+          for (int ks = 0; ks < BN / 16; ++ks) {
+            const uint32_t a_tmem = tmem + (uint32_t)(jj & 1) * BN + ks * 8;
+            const uint64_t b = smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024);
+            mma_ts(tmem + TM_O, a_tmem, b, idesc_o, (jj > 0 || ks > 0) ? 1u : 0u);
+          }
+          mma_commit(&sm->kv_empty[s]);
+          mma_commit(&sm->o_done);
+          if (jj == NT - 1) mma_commit(&sm->o_final);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int n = plan.n0 + r;
+    const bool valid = n < T;
+    const Range rr = mask_range(valid ? n : plan.nlast, C, W, mode);
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < NT; ++j) {
+      mbar_wait(&sm->s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[64];
+      tmem_ld32(t_lane + (uint32_t)(j & 1) * BN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(t_lane + (uint32_t)(j & 1) * BN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_wait_ld();
+      const int base = plan.base(j);
+      int vlo, vhi;
+      if (plan.summary(j)) {
+        vlo = 0;
+        vhi = (int)min((int64_t)BN, rr.nsum - base);
+      } else {
+        vlo = (int)max((int64_t)0, rr.lo - base);
+        vhi = min(BN, n - base + 1);
+      }
+      if (!valid) vhi = vlo;
+      float x[64];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        x[c] = (c >= vlo && c < vhi) ? __uint_as_float(sr[c]) * scale_log2 : -INFINITY;
+        mx = fmaxf(mx, x[c]);
+      }
+      const bool grow = mx > m_ref + 8.0f;
+      if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+        // lazy rescale of the running O (TMEM) and l; wait for PV_{j-1} first
+        const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
+        mbar_wait(&sm->o_done, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(t_lane + TM_O + cc * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+          tmem_st32(t_lane + TM_O + cc * 32, o);
+        }
+        tmem_wait_st();
+        l *= f;
+      }
+      if (grow) m_ref = mx;
+      const float mref = m_ref == -INFINITY ? 0.f : m_ref;
+      uint32_t pk[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const float p0 = ex2(x[2 * c] - mref), p1 = ex2(x[2 * c + 1] - mref);
+        l += p0 + p1;
+        pk[c] = pack_bf16(p0, p1);
+      }
+      tmem_st32(t_lane + (uint32_t)(j & 1) * BN, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm->p_full[j & 1]);
+    }
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(&sm->o_final, 0);
+    tc_fence_after();
+    const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+    uint8_t* qs = reinterpret_cast<uint8_t*>(sm->q);
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(t_lane + TM_O + cc * 32, o);
+      tmem_wait_ld();
+      const int kb = (cc * 32) / 64, c16_0 = ((cc * 32) % 64) / 8;
+      uint8_t* rowp = qs + kb * (BM * 128) + r * 128;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(o[8 * g + 0]) * inv_l, __uint_as_float(o[8 * g + 1]) * inv_l);
+        w.y = pack_bf16(__uint_as_float(o[8 * g + 2]) * inv_l, __uint_as_float(o[8 * g + 3]) * inv_l);
+        w.z = pack_bf16(__uint_as_float(o[8 * g + 4]) * inv_l, __uint_as_float(o[8 * g + 5]) * inv_l);
+        w.w = pack_bf16(__uint_as_float(o[8 * g + 6]) * inv_l, __uint_as_float(o[8 * g + 7]) * inv_l);
+        *reinterpret_cast<uint4*>(rowp + (((c16_0 + g) ^ (r & 7)) * 16)) = w;
+      }
+    }
+    if (valid && lse) lse[(size_t)u * T + n] = (m_ref + __log2f(l)) * 0.69314718055994531f;
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (warp == 2 && lane == 0) {
+      for (int kb = 0; kb < D / 64; ++kb) tma_store_3d(&mO, sm->q + kb * BM * 64, kb * 64, plan.n0, u);
+      tma_store_commit();
+      tma_store_wait_all();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 map over [units, rows, D] with a {64, box_rows, 1} box, 128-byte swizzle.
+bool make_map(CUtensorMap* m, const void* base, int units, int rows, int D, int box_rows) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)rows, (cuuint64_t)units};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)rows * D * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D, int NSTAGE>
+cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                     const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
+  const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
+  CUtensorMap mQ, mK, mV, mKs, mVs, mO;
+  bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BN) &&
+            make_map(&mV, V, BH, T, D, BN) && make_map(&mO, O, BH, T, D, BM);
+  if (nC > 0) {
+    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BN) && make_map(&mVs, Vsum, BH, nC, D, BN);
+  } else {  // never read (no summary tiles); any valid map will do
+    mKs = mK;
+    mVs = mV;
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(Smem<D, NSTAGE>) + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_sm100_kernel<D, NSTAGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((T + BM - 1) / BM, BH);
+  const float scale_log2 = cfg.scale * 1.4426950408889634f;
+  prefill_sm100_kernel<D, NSTAGE><<<grid, NTHREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, mO, T, cfg.chunk,
+                                                               cfg.window, cfg.mode, scale_log2, lse);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool prefill_sm100_supported(const eva_config& cfg) {
+  return cfg.dtype == EVA_BF16 && (cfg.d_head == 64 || cfg.d_head == 128) && encode_fn() != nullptr;
+}
+
+cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                 const void* Ksum, const void* Vsum, void* O, float* lse,
+                                 cudaStream_t s) {
+  if (cfg.bh_count == 0) return cudaSuccess;
+  if (cfg.d_head == 128) return launch_t<128, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  if (cfg.d_head == 64) return launch_t<64, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cudaErrorNotSupported;
 }
+
 }  // namespace eva
