@@ -6,10 +6,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "launch.h"
 #include "summarize.cuh"
+#include "summarize_cta.cuh"
 
 namespace eva {
 
@@ -32,6 +35,25 @@ __global__ void __launch_bounds__(128) summarize_kernel(eva_config cfg, const T*
   const float* e = eps ? eps + ((size_t)u * nC + c) * D : nullptr;
   summarize_chunk_warp<T, D>(rowK, rowV, C, e, (uint32_t)(cfg.bh_begin + u), (uint32_t)c, cfg,
                              Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D);
+}
+
+// grid: (nC, bh_count); block 128; one CTA per chunk, rows staged in shared memory.
+template <typename T, int D>
+__global__ void __launch_bounds__(SUMM_THREADS) summarize_cta_kernel(eva_config cfg, const T* __restrict__ K,
+                                                                   const T* __restrict__ V,
+                                                                   const float* __restrict__ eps,
+                                                                   T* __restrict__ Ksum,
+                                                                   T* __restrict__ Vsum) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int nC = cfg.T / cfg.chunk;
+  const int c = blockIdx.x, u = blockIdx.y, C = cfg.chunk;
+  const T* Kc = K + ((size_t)u * cfg.T + (size_t)c * C) * D;
+  const T* Vc = V + ((size_t)u * cfg.T + (size_t)c * C) * D;
+  auto rowK = [&](int i) { return Kc + (size_t)i * D; };
+  auto rowV = [&](int i) { return Vc + (size_t)i * D; };
+  const float* e = eps ? eps + ((size_t)u * nC + c) * D : nullptr;
+  summarize_chunk_cta<T, D>(rowK, rowV, C, e, (uint32_t)(cfg.bh_begin + u), (uint32_t)c, cfg,
+                            Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D, smem);
 }
 
 // ============================================================================ SIMT prefill
@@ -118,16 +140,17 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, const
 }
 
 // ============================================================================ cache append
-// grid (bh_count, 1 + ceil(n_chunks / 4)), block 128.
+// grid (bh_count, 1 + n_chunks), block 128.
 //   blockIdx.y == 0 : ring write of the last min(n_new, W) tokens (if do_ring)
-//   blockIdx.y >= 1 : warp w summarises chunk chunk0 + 4*(y-1) + w (if do_sum)
+//   blockIdx.y >= 1 : the CTA summarises chunk chunk0 + y - 1 (if do_sum)
 // Rows of a chunk come from K_new (positions >= pos) or the ring (positions < pos).
-template <typename T, int D>
+template <typename T, int D, bool CTA_SUMM>
 __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __restrict__ Kn,
                                                      const T* __restrict__ Vn,
                                                      const float* __restrict__ eps, int n_new,
                                                      int do_ring, int do_sum, int64_t chunk0,
                                                      int n_chunks) {
+  extern __shared__ __align__(16) uint8_t smem[];
   const int u = blockIdx.x;
   const int W = c.cfg.window, C = c.cfg.chunk;
   const int64_t pos = c.pos;
@@ -137,18 +160,19 @@ __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __res
   const T* vn = Vn + (size_t)u * n_new * D;
   if (blockIdx.y == 0) {
     if (!do_ring) return;
+    constexpr int VEC = 16 / sizeof(T);
     const int keep = min(n_new, W);
     const int first = n_new - keep;
-    for (int i = threadIdx.x; i < keep * D; i += blockDim.x) {
-      const int r = first + i / D, cc = i % D;
+    for (int i = threadIdx.x; i < keep * (D / VEC); i += blockDim.x) {
+      const int r = first + i / (D / VEC), cc = (i % (D / VEC)) * VEC;
       const size_t slot = (size_t)((pos + r) % W);
-      rk[slot * D + cc] = kn[(size_t)r * D + cc];
-      rv[slot * D + cc] = vn[(size_t)r * D + cc];
+      *reinterpret_cast<uint4*>(rk + slot * D + cc) = *reinterpret_cast<const uint4*>(kn + (size_t)r * D + cc);
+      *reinterpret_cast<uint4*>(rv + slot * D + cc) = *reinterpret_cast<const uint4*>(vn + (size_t)r * D + cc);
     }
     return;
   }
   if (!do_sum) return;
-  const int ci = (blockIdx.y - 1) * 4 + (threadIdx.x >> 5);
+  const int ci = CTA_SUMM ? (int)blockIdx.y - 1 : ((int)blockIdx.y - 1) * 4 + (int)(threadIdx.x >> 5);
   if (ci >= n_chunks) return;
   const int64_t chunk = chunk0 + ci;
   const int64_t p0 = chunk * C;
@@ -163,23 +187,37 @@ __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __res
   const float* e = eps ? eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr;
   T* sk = static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D;
   T* sv = static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D;
-  summarize_chunk_warp<T, D>(rowK, rowV, C, e, (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk,
-                             c.cfg, sk, sv);
+  if constexpr (CTA_SUMM)
+    summarize_chunk_cta<T, D>(rowK, rowV, C, e, (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk,
+                              c.cfg, sk, sv, smem);
+  else
+    summarize_chunk_warp<T, D>(rowK, rowV, C, e, (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk,
+                               c.cfg, sk, sv);
 }
 
 // ============================================================================ decode
 // grid (bh_count, splits), block 128 (4 warps).  The visible list of query
 // n = pos-1 is the summary prefix [0, nsum) followed by the ring positions
-// [lo, n] (slot p mod W).  Split s takes entries [s*E/S, (s+1)*E/S); warp w of
-// the CTA takes every 4th entry.  Online softmax per warp, merged in smem.
+// [lo, n] (slot p mod W, at most two contiguous ring segments).  Split s takes
+// entries [s*E/S, (s+1)*E/S).  Bandwidth layout: a row of D elements is read by a
+// group of TPR = D/VEC lanes with one 16-byte load each (VEC elements per lane);
+// a warp covers RPW = 32/TPR rows per load and UNROLL row-blocks per iteration, so
+// every lane has 2*UNROLL independent 16-byte loads in flight.  Each lane group
+// keeps its own online-softmax state (m, l, acc[VEC]); groups and warps are merged
+// at the end (shuffles, then shared memory).
 template <typename T, int D>
 __global__ void __launch_bounds__(128) decode_kernel(eva_cache c, const T* __restrict__ Q,
                                                      T* __restrict__ O, float* __restrict__ lse,
                                                      float* __restrict__ ws) {
-  using LM = LaneMap<D>;
-  constexpr int CPL = LM::CPL;
-  __shared__ float sm_m[4], sm_l[4];
-  __shared__ float sm_acc[4][D];
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int TPR = D / VEC;          // lanes per row
+  constexpr int RPW = 32 / TPR;         // rows per warp-wide load
+  constexpr int UNROLL = 4;
+  constexpr int ROWS_IT = RPW * UNROLL; // rows per warp iteration
+  constexpr int NW = 4;
+  static_assert(TPR >= 1 && TPR <= 32 && 32 % TPR == 0, "bad D/VEC");
+  __shared__ float sm_m[NW], sm_l[NW];
+  __shared__ float sm_acc[NW][D];
   const int u = blockIdx.x, S = gridDim.y, s = blockIdx.y;
   const int W = c.cfg.window, C = c.cfg.chunk;
   const int64_t n = c.pos - 1;
@@ -187,79 +225,117 @@ __global__ void __launch_bounds__(128) decode_kernel(eva_cache c, const T* __res
   const int64_t E = r.nsum + (n - r.lo + 1);
   const int64_t e0 = E * s / S, e1 = E * (s + 1) / S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool act = lane < LM::LANES;
-  const int ch0 = lane * CPL;
-  const T* sk = static_cast<const T*>(c.sum_k) + (size_t)u * c.cap_chunks * D;
-  const T* sv = static_cast<const T*>(c.sum_v) + (size_t)u * c.cap_chunks * D;
-  const T* rk = static_cast<const T*>(c.ring_k) + (size_t)u * W * D;
-  const T* rv = static_cast<const T*>(c.ring_v) + (size_t)u * W * D;
-  float q[CPL], acc[CPL];
-  if (act) load_vec<T, CPL>(Q + (size_t)u * D + ch0, q);
+  const int grp = lane / TPR, gl = lane % TPR;
+  const int ch0 = gl * VEC;
+  const T* sk = static_cast<const T*>(c.sum_k) + (size_t)u * c.cap_chunks * D + ch0;
+  const T* sv = static_cast<const T*>(c.sum_v) + (size_t)u * c.cap_chunks * D + ch0;
+  const T* rk = static_cast<const T*>(c.ring_k) + (size_t)u * W * D + ch0;
+  const T* rv = static_cast<const T*>(c.ring_v) + (size_t)u * W * D + ch0;
+  float q[VEC], acc[VEC];
+  load_vec<T, VEC>(Q + (size_t)u * D + ch0, q);
 #pragma unroll
-  for (int j = 0; j < CPL; ++j) {
-    q[j] = act ? q[j] * c.cfg.scale : 0.f;
+  for (int j = 0; j < VEC; ++j) {
+    q[j] *= c.cfg.scale;
     acc[j] = 0.f;
   }
   float m = -INFINITY, l = 0.f;
-  for (int64_t e = e0 + warp; e < e1; e += 4) {
-    const T *kp, *vp;
-    if (e < r.nsum) {
-      kp = sk + (size_t)e * D;
-      vp = sv + (size_t)e * D;
-    } else {
-      const int64_t p = r.lo + (e - r.nsum);
-      kp = rk + (size_t)(p % W) * D;
-      vp = rv + (size_t)(p % W) * D;
+  for (int64_t eb = e0 + (int64_t)warp * ROWS_IT; eb < e1; eb += (int64_t)NW * ROWS_IT) {
+    float kx[UNROLL][VEC], vx[UNROLL][VEC];
+    bool ok[UNROLL];
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i) {
+      const int64_t e = eb + i * RPW + grp;
+      ok[i] = e < e1;
+      const T *kp, *vp;
+      if (e < r.nsum) {
+        kp = sk + (size_t)e * D;
+        vp = sv + (size_t)e * D;
+      } else {
+        const int64_t slot = (r.lo + (e - r.nsum)) % W;
+        kp = rk + (size_t)slot * D;
+        vp = rv + (size_t)slot * D;
+      }
+      if (ok[i]) {
+        load_vec<T, VEC>(kp, kx[i]);
+        load_vec<T, VEC>(vp, vx[i]);
+      }
     }
-    float k[CPL], v[CPL], part = 0.f;
-    if (act) {
-      load_vec<T, CPL>(kp + ch0, k);
-      load_vec<T, CPL>(vp + ch0, v);
+    float sc[UNROLL];
+    float mx = m;
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) part += q[j] * k[j];
-    } else {
+    for (int i = 0; i < UNROLL; ++i) {
+      float d = 0.f;
+      if (ok[i]) {
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) v[j] = 0.f;
+        for (int j = 0; j < VEC; ++j) d += q[j] * kx[i][j];
+      }
+      d = group_sum<TPR>(d);
+      sc[i] = ok[i] ? d : -INFINITY;
+      mx = fmaxf(mx, sc[i]);
     }
-    const float sc = warp_sum(part);
-    const float mn = fmaxf(m, sc);
-    const float corr = __expf(m - mn), p = __expf(sc - mn);
-    l = l * corr + p;
+    if (mx == -INFINITY) continue;
+    const float corr = __expf(m - mx);
+    l *= corr;
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) acc[j] = acc[j] * corr + p * v[j];
-    m = mn;
+    for (int j = 0; j < VEC; ++j) acc[j] *= corr;
+#pragma unroll
+    for (int i = 0; i < UNROLL; ++i) {
+      const float p = __expf(sc[i] - mx);
+      l += p;
+      if (ok[i]) {
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[j] += p * vx[i][j];
+      }
+    }
+    m = mx;
+  }
+  // merge the RPW lane groups of this warp (butterfly over group ids)
+#pragma unroll
+  for (int o = TPR; o < 32; o <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float l2 = __shfl_xor_sync(0xffffffffu, l, o);
+    const float M = fmaxf(m, m2);
+    const float f1 = m == -INFINITY ? 0.f : __expf(m - M);
+    const float f2 = m2 == -INFINITY ? 0.f : __expf(m2 - M);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[j] = acc[j] * f1 + __shfl_xor_sync(0xffffffffu, acc[j], o) * f2;
+    l = l * f1 + l2 * f2;
+    m = M;
   }
   if (lane == 0) { sm_m[warp] = m; sm_l[warp] = l; }
-  if (act) {
+  if (grp == 0) {
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) sm_acc[warp][ch0 + j] = acc[j];
+    for (int j = 0; j < VEC; ++j) sm_acc[warp][ch0 + j] = acc[j];
   }
   __syncthreads();
   if (warp != 0) return;
-  float M = fmaxf(fmaxf(sm_m[0], sm_m[1]), fmaxf(sm_m[2], sm_m[3]));
-  float f[4], L = 0.f;
+  float M = -INFINITY;
 #pragma unroll
-  for (int w = 0; w < 4; ++w) {
+  for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_m[w]);
+  float f[NW], L = 0.f;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
     f[w] = sm_m[w] == -INFINITY ? 0.f : __expf(sm_m[w] - M);
     L += f[w] * sm_l[w];
   }
-  if (!act) return;
-  float out[CPL];
+  for (int ch = lane; ch < D; ch += 32) {
+    float o = 0.f;
 #pragma unroll
-  for (int j = 0; j < CPL; ++j)
-    out[j] = f[0] * sm_acc[0][ch0 + j] + f[1] * sm_acc[1][ch0 + j] + f[2] * sm_acc[2][ch0 + j] +
-             f[3] * sm_acc[3][ch0 + j];
-  if (S == 1) {
-    const float il = 1.0f / L;
-#pragma unroll
-    for (int j = 0; j < CPL; ++j) out[j] *= il;
-    store_vec<T, CPL>(O + (size_t)u * D + ch0, out);
-    if (lse && lane == 0) lse[u] = M + logf(L);
-  } else {
-    float* p = ws + ((size_t)u * S + s) * (D + 2);
-    if (lane == 0) { p[0] = M; p[1] = L; }
-#pragma unroll
-    for (int j = 0; j < CPL; ++j) p[2 + ch0 + j] = out[j];
+    for (int w = 0; w < NW; ++w) o += f[w] * sm_acc[w][ch];
+    if (S == 1) {
+      O[(size_t)u * D + ch] = Elem<T>::from_f(o / L);
+    } else {
+      ws[((size_t)u * S + s) * (D + 2) + 2 + ch] = o;
+    }
+  }
+  if (lane == 0) {
+    if (S == 1) {
+      if (lse) lse[u] = M + logf(L);
+    } else {
+      float* p = ws + ((size_t)u * S + s) * (D + 2);
+      p[0] = M;
+      p[1] = L;
+    }
   }
 }
 
@@ -352,14 +428,40 @@ int num_sms() {
   return sms;
 }
 
+constexpr size_t kSummSmemMax = 96 * 1024;
+
+// Raise the dynamic shared-memory limit of `fn` to `bytes` (once per function and size).
+cudaError_t set_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[fn];
+  if (bytes > cur) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    cur = bytes;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
                              void* Ksum, void* Vsum, cudaStream_t s) {
   const int nC = cfg.T / cfg.chunk;
   if (nC == 0 || cfg.bh_count == 0) return cudaSuccess;
-  dim3 grid((nC + 3) / 4, cfg.bh_count);
-  EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head,
-      summarize_kernel<T, D><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum,
-                                                  (T*)Vsum)));
+  cudaError_t err = cudaSuccess;
+  EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
+    const size_t sm = summ_smem_bytes(cfg.chunk, D, sizeof(T));
+    if (sm <= kSummSmemMax) {
+      err = set_smem_attr((const void*)summarize_cta_kernel<T, D>, sm);
+      if (err != cudaSuccess) return err;
+      summarize_cta_kernel<T, D><<<dim3(nC, cfg.bh_count), SUMM_THREADS, sm, s>>>(
+          cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+    } else {
+      summarize_kernel<T, D><<<dim3((nC + 3) / 4, cfg.bh_count), 128, 0, s>>>(
+          cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+    }
+  }));
   note_launch();
   return cudaGetLastError();
 }
@@ -386,24 +488,29 @@ cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* 
   const int64_t chunk0 = c.pos / C;                      // first chunk not yet summarised
   const int64_t chunk_end = (c.pos + n_new) / C;         // chunks complete after the append
   const int n_chunks = (int)std::max<int64_t>(0, chunk_end - chunk0);
-  const int ygroups = (n_chunks + 3) / 4;
   // Writing the ring can overwrite old positions still needed by a straddling
   // chunk only if n_new > W - C + 1; then summaries go first.
   const bool hazard = n_new > W - C + 1 && n_chunks > 0;
   cudaError_t err = cudaSuccess;
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
+    const size_t sm = summ_smem_bytes(C, D, sizeof(T));
+    const bool cta = sm <= kSummSmemMax;
+    auto fn = cta ? append_kernel<T, D, true> : append_kernel<T, D, false>;
+    const size_t smem = cta ? sm : 0;
+    if (cta) {
+      err = set_smem_attr((const void*)append_kernel<T, D, true>, sm);
+      if (err != cudaSuccess) return err;
+    }
+    const int ysum = cta ? n_chunks : (n_chunks + 3) / 4;
     if (!hazard) {
-      dim3 grid(c.cfg.bh_count, 1 + ygroups);
-      append_kernel<T, D><<<grid, 128, 0, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 1, 1,
-                                               chunk0, n_chunks);
+      fn<<<dim3(c.cfg.bh_count, 1 + ysum), 128, smem, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 1, 1,
+                                                          chunk0, n_chunks);
       note_launch();
     } else {
-      dim3 g1(c.cfg.bh_count, 1 + ygroups);
-      append_kernel<T, D><<<g1, 128, 0, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 0, 1,
-                                             chunk0, n_chunks);
-      dim3 g2(c.cfg.bh_count, 1);
-      append_kernel<T, D><<<g2, 128, 0, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 1, 0,
-                                             chunk0, 0);
+      fn<<<dim3(c.cfg.bh_count, 1 + ysum), 128, smem, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 0, 1,
+                                                          chunk0, n_chunks);
+      fn<<<dim3(c.cfg.bh_count, 1), 128, smem, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 1, 0,
+                                                   chunk0, 0);
       note_launch(2);
     }
     err = cudaGetLastError();

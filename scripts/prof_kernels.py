@@ -1,0 +1,45 @@
+"""Launch one hot-path kernel at a BASELINE config a few times (for ncu -k captures).
+
+    python scripts/prof_kernels.py prefill_cfg3|prefill_cfg2|summarize_cfg3|decode_cfg4 [reps]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import eva_inputs
+import paper_2511_00576_b200 as eva
+
+what = sys.argv[1]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+dev = torch.device("cuda:0")
+if what in ("prefill_cfg3", "summarize_cfg3", "prefill_cfg2"):
+    if what == "prefill_cfg2":
+        B, H, T, d, C, W = 1, 16, 2048, 64, 64, 128
+    else:
+        B, H, T, d, C, W = 8, 32, 8192, 128, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device=dev)
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    O = torch.empty_like(Q)
+    lse = torch.empty(B * H, T, device=dev)
+    for _ in range(reps):
+        if what == "summarize_cfg3":
+            eva.eva_summarize(cfg, K, V, Ksum=ks, Vsum=vs)
+        else:
+            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse)
+elif what == "decode_cfg4":
+    BH, d, C, W, ctx = 256 * 32, 128, 64, 256, 32768
+    cfg = eva.make_config(256, 32, 0, d, C, W)
+    cache = eva.DecodeCache(cfg, ctx // C + 16, device=dev)
+    for t in (cache.ring_k, cache.ring_v, cache.sum_k, cache.sum_v):
+        t.normal_()
+    cache.c.pos = ctx
+    q = torch.randn(BH, d, device=dev).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    for _ in range(reps):
+        cache.eva_cache_append(q, q)
+        cache.eva_attn_decode(q, O=o, want_lse=False)
+torch.cuda.synchronize()
+print("done", what)
