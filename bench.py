@@ -147,11 +147,13 @@ def run_ours(args, rank, world, local_rank):
     peaks = load_peaks()
     s = torch.cuda.current_stream(dev)
 
+    from paper_2511_00576_b200.parallel import max_over_ranks, shard_for
+
     wl = WORKLOAD
     B, H, T, d, C, W = (wl[k] for k in ("B", "H", "T", "d", "C", "W"))
-    BH = B * H
+    shard = shard_for(rank, world, B * world, H)   # weak scaling: B sequences per GPU
+    BH, bh0 = shard.bh_count, shard.bh_begin
     nC = T // C
-    bh0 = rank * BH
     cfg = eva.make_config(B * world, H, T, d, C, W, bh_begin=bh0, bh_count=BH, dtype=torch.bfloat16)
     Q, K, V = eva_inputs.qkv(bh0, BH, T, d, torch.bfloat16, seed=0, device=dev)
     Ksum = torch.empty(BH, nC, d, dtype=torch.bfloat16, device=dev)
@@ -198,11 +200,7 @@ def run_ours(args, rank, world, local_rank):
         step_ms = [ev[i][0].elapsed_time(ev[i][3]) for i in range(args.steps)]
         pre_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(args.steps)]
         sum_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(args.steps)]
-        total_ms = sum(step_ms)
-        if dist:
-            t = torch.tensor([total_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total_ms = float(t.item())
+        total_ms = max_over_ranks(sum(step_ms), device=dev)
 
         # ---------------- e2e through the public API with pinned host buffers
         hQ, hK, hV = (x.cpu().pin_memory() for x in (Q, K, V))
@@ -230,11 +228,7 @@ def run_ours(args, rank, world, local_rank):
             flush.zero_()
             e2e_step(e_ev[i])
         torch.cuda.synchronize()
-        e2e_ms = sum(a.elapsed_time(b) for a, b in e_ev)
-        if dist:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in e_ev), device=dev)
 
         extras = {}
         if not args.no_extras:

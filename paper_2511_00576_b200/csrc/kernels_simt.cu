@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __res
 // keeps its own online-softmax state (m, l, acc[VEC]); groups and warps are merged
 // at the end (shuffles, then shared memory).
 template <typename T, int D>
-__global__ void __launch_bounds__(128) decode_kernel(eva_cache c, const T* __restrict__ Q,
+__global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __restrict__ Q,
                                                      T* __restrict__ O, float* __restrict__ lse,
                                                      float* __restrict__ ws) {
   constexpr int VEC = 16 / sizeof(T);
@@ -222,8 +222,11 @@ __global__ void __launch_bounds__(128) decode_kernel(eva_cache c, const T* __res
   const int W = c.cfg.window, C = c.cfg.chunk;
   const int64_t n = c.pos - 1;
   const Range r = mask_range(n, C, W, c.cfg.mode);
-  const int64_t E = r.nsum + (n - r.lo + 1);
-  const int64_t e0 = E * s / S, e1 = E * (s + 1) / S;
+  // 32-bit entry indices: E <= nsum + W stays far below 2^31 for any cache that fits HBM
+  const int ns = (int)r.nsum;
+  const int E = ns + (int)(n - r.lo + 1);
+  const int e0 = (int)((int64_t)E * s / S), e1 = (int)((int64_t)E * (s + 1) / S);
+  const int slot0 = (int)(r.lo % W) - ns;  // ring slot of entry e >= ns is slot0 + e (mod W)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / TPR, gl = lane % TPR;
   const int ch0 = gl * VEC;
@@ -239,25 +242,26 @@ __global__ void __launch_bounds__(128) decode_kernel(eva_cache c, const T* __res
     acc[j] = 0.f;
   }
   float m = -INFINITY, l = 0.f;
-  for (int64_t eb = e0 + (int64_t)warp * ROWS_IT; eb < e1; eb += (int64_t)NW * ROWS_IT) {
-    float kx[UNROLL][VEC], vx[UNROLL][VEC];
+  for (int eb = e0 + warp * ROWS_IT; eb < e1; eb += NW * ROWS_IT) {
+    uint4 kx[UNROLL], vx[UNROLL];
     bool ok[UNROLL];
 #pragma unroll
     for (int i = 0; i < UNROLL; ++i) {
-      const int64_t e = eb + i * RPW + grp;
+      const int e = eb + i * RPW + grp;
       ok[i] = e < e1;
       const T *kp, *vp;
-      if (e < r.nsum) {
+      if (e < ns) {
         kp = sk + (size_t)e * D;
         vp = sv + (size_t)e * D;
       } else {
-        const int64_t slot = (r.lo + (e - r.nsum)) % W;
+        int slot = slot0 + e;
+        if (slot >= W) slot -= W;
         kp = rk + (size_t)slot * D;
         vp = rv + (size_t)slot * D;
       }
       if (ok[i]) {
-        load_vec<T, VEC>(kp, kx[i]);
-        load_vec<T, VEC>(vp, vx[i]);
+        kx[i] = ldg16_stream(kp);
+        vx[i] = ldg16_stream(vp);
       }
     }
     float sc[UNROLL];
@@ -266,8 +270,10 @@ __global__ void __launch_bounds__(128) decode_kernel(eva_cache c, const T* __res
     for (int i = 0; i < UNROLL; ++i) {
       float d = 0.f;
       if (ok[i]) {
+        float k[VEC];
+        unpack16<T>(kx[i], k);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) d += q[j] * kx[i][j];
+        for (int j = 0; j < VEC; ++j) d += q[j] * k[j];
       }
       d = group_sum<TPR>(d);
       sc[i] = ok[i] ? d : -INFINITY;
@@ -283,8 +289,10 @@ __global__ void __launch_bounds__(128) decode_kernel(eva_cache c, const T* __res
       const float p = __expf(sc[i] - mx);
       l += p;
       if (ok[i]) {
+        float v[VEC];
+        unpack16<T>(vx[i], v);
 #pragma unroll
-        for (int j = 0; j < VEC; ++j) acc[j] += p * vx[i][j];
+        for (int j = 0; j < VEC; ++j) acc[j] += p * v[j];
       }
     }
     m = mx;
