@@ -96,8 +96,13 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
                      eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
                      Vsum: Optional[torch.Tensor] = None, summaries_provided: bool = False,
                      want_lse: bool = True, simt: bool = False, O: Optional[torch.Tensor] = None,
-                     lse: Optional[torch.Tensor] = None):
-    """FlashEVA chunk-causal prefill.  Returns (O, lse, Ksum, Vsum)."""
+                     lse: Optional[torch.Tensor] = None, kernel: Optional[str] = None):
+    """FlashEVA chunk-causal prefill.  Returns (O, lse, Ksum, Vsum).
+
+    kernel: None (chosen by size), "simt", "tile" (tcgen05, one 128-query tile per CTA)
+    or "pair" (persistent tcgen05 kernel, two Q tiles per CTA sharing the K/V stream)."""
+    if kernel == "simt":
+        simt = True
     dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
     nC = T // cfg.chunk
     for t, nm in ((Q, "Q"), (K, "K"), (V, "V")):
@@ -119,6 +124,7 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
     if want_lse and lse is None:
         lse = torch.empty(bh, T, dtype=torch.float32, device=Q.device)
     flags = (N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0) | (N.EVA_PREFILL_SIMT if simt else 0)
+    flags |= {None: 0, "simt": 0, "tile": N.EVA_PREFILL_TC_TILE, "pair": N.EVA_PREFILL_TC_PAIR}[kernel]
     check(lib.eva_attn_prefill(ctypes.byref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum), _ptr(Vsum),
                                _ptr(eps), _ptr(O), _ptr(lse if want_lse else None), flags,
                                _stream(Q.device)))

@@ -129,7 +129,7 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
                             uint32_t flags, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
-  if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT))
+  if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT | EVA_PREFILL_TC_TILE | EVA_PREFILL_TC_PAIR))
     return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
   if (cfg->bh_count == 0) return ok();
   const void* p[] = {Q, K, V, O};
@@ -150,7 +150,8 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   }
   const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) &&
                   eva::prefill_sm100_supported(*cfg);
-  cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, Q, K, V, Ksum, Vsum, O, lse, s)
+  const uint32_t variant = (flags & EVA_PREFILL_TC_TILE) ? 1u : (flags & EVA_PREFILL_TC_PAIR) ? 2u : 0u;
+  cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, Q, K, V, Ksum, Vsum, O, lse, variant, s)
                      : eva::launch_prefill_simt(*cfg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cuda_status(e, tc ? "eva_attn_prefill(sm100)" : "eva_attn_prefill(simt)");
 }

@@ -140,40 +140,50 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, const
 }
 
 // ============================================================================ cache append
-// grid (bh_count, 1 + n_chunks), block 128.
-//   blockIdx.y == 0 : ring write of the last min(n_new, W) tokens (if do_ring)
-//   blockIdx.y >= 1 : the CTA summarises chunk chunk0 + y - 1 (if do_sum)
+// One launch, flat grid of 128-thread CTAs:
+//   blockIdx.x <  n_copy : ring write of the last min(n_new, W) tokens of every unit
+//                          (one 16-byte piece of K and of V per thread; if do_ring)
+//   blockIdx.x >= n_copy : CTA summarises (unit, chunk) = divmod(x - n_copy, n_chunks)
+//                          (if do_sum)
 // Rows of a chunk come from K_new (positions >= pos) or the ring (positions < pos).
 template <typename T, int D, bool CTA_SUMM>
 __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __restrict__ Kn,
                                                      const T* __restrict__ Vn,
                                                      const float* __restrict__ eps, int n_new,
-                                                     int do_ring, int do_sum, int64_t chunk0,
+                                                     int n_copy, int do_sum, int64_t chunk0,
                                                      int n_chunks) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const int u = blockIdx.x;
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int PPR = D / VEC;
   const int W = c.cfg.window, C = c.cfg.chunk;
   const int64_t pos = c.pos;
-  T* rk = static_cast<T*>(c.ring_k) + (size_t)u * W * D;
-  T* rv = static_cast<T*>(c.ring_v) + (size_t)u * W * D;
-  const T* kn = Kn + (size_t)u * n_new * D;
-  const T* vn = Vn + (size_t)u * n_new * D;
-  if (blockIdx.y == 0) {
-    if (!do_ring) return;
-    constexpr int VEC = 16 / sizeof(T);
-    const int keep = min(n_new, W);
-    const int first = n_new - keep;
-    for (int i = threadIdx.x; i < keep * (D / VEC); i += blockDim.x) {
-      const int r = first + i / (D / VEC), cc = (i % (D / VEC)) * VEC;
-      const size_t slot = (size_t)((pos + r) % W);
-      *reinterpret_cast<uint4*>(rk + slot * D + cc) = *reinterpret_cast<const uint4*>(kn + (size_t)r * D + cc);
-      *reinterpret_cast<uint4*>(rv + slot * D + cc) = *reinterpret_cast<const uint4*>(vn + (size_t)r * D + cc);
-    }
+  const int keep = min(n_new, W);
+  if ((int)blockIdx.x < n_copy) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // piece index
+    const int64_t per_unit = (int64_t)keep * PPR;
+    if (i >= per_unit * c.cfg.bh_count) return;
+    const int u = (int)(i / per_unit);
+    const int rem = (int)(i % per_unit);
+    const int r = n_new - keep + rem / PPR, cc = (rem % PPR) * VEC;
+    const size_t slot = (size_t)((pos + r) % W);
+    T* rk = static_cast<T*>(c.ring_k) + (size_t)u * W * D;
+    T* rv = static_cast<T*>(c.ring_v) + (size_t)u * W * D;
+    const T* kn = Kn + (size_t)u * n_new * D;
+    const T* vn = Vn + (size_t)u * n_new * D;
+    *reinterpret_cast<uint4*>(rk + slot * D + cc) = *reinterpret_cast<const uint4*>(kn + (size_t)r * D + cc);
+    *reinterpret_cast<uint4*>(rv + slot * D + cc) = *reinterpret_cast<const uint4*>(vn + (size_t)r * D + cc);
     return;
   }
   if (!do_sum) return;
-  const int ci = CTA_SUMM ? (int)blockIdx.y - 1 : ((int)blockIdx.y - 1) * 4 + (int)(threadIdx.x >> 5);
-  if (ci >= n_chunks) return;
+  const int x = (int)blockIdx.x - n_copy;
+  const int per = CTA_SUMM ? n_chunks : (n_chunks + 3) / 4;
+  const int u = x / per;
+  const int ci = CTA_SUMM ? x % per : (x % per) * 4 + (int)(threadIdx.x >> 5);
+  if (u >= c.cfg.bh_count || ci >= n_chunks) return;
+  const T* rk = static_cast<const T*>(c.ring_k) + (size_t)u * W * D;
+  const T* rv = static_cast<const T*>(c.ring_v) + (size_t)u * W * D;
+  const T* kn = Kn + (size_t)u * n_new * D;
+  const T* vn = Vn + (size_t)u * n_new * D;
   const int64_t chunk = chunk0 + ci;
   const int64_t p0 = chunk * C;
   auto rowK = [&](int i) -> const T* {
@@ -509,16 +519,18 @@ cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* 
       err = set_smem_attr((const void*)append_kernel<T, D, true>, sm);
       if (err != cudaSuccess) return err;
     }
-    const int ysum = cta ? n_chunks : (n_chunks + 3) / 4;
+    constexpr int VEC = 16 / sizeof(T);
+    const int64_t pieces = (int64_t)std::min(n_new, W) * (D / VEC) * c.cfg.bh_count;
+    const int n_copy = (int)((pieces + 127) / 128);
+    const int n_sum = n_chunks == 0 ? 0 : c.cfg.bh_count * (cta ? n_chunks : (n_chunks + 3) / 4);
+    const T* kn = (const T*)Kn;
+    const T* vn = (const T*)Vn;
     if (!hazard) {
-      fn<<<dim3(c.cfg.bh_count, 1 + ysum), 128, smem, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 1, 1,
-                                                          chunk0, n_chunks);
+      fn<<<n_copy + n_sum, 128, smem, s>>>(c, kn, vn, eps, n_new, n_copy, 1, chunk0, n_chunks);
       note_launch();
-    } else {
-      fn<<<dim3(c.cfg.bh_count, 1 + ysum), 128, smem, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 0, 1,
-                                                          chunk0, n_chunks);
-      fn<<<dim3(c.cfg.bh_count, 1), 128, smem, s>>>(c, (const T*)Kn, (const T*)Vn, eps, n_new, 1, 0,
-                                                   chunk0, 0);
+    } else {  // summaries first, then the ring write
+      fn<<<n_sum, 128, smem, s>>>(c, kn, vn, eps, n_new, 0, 1, chunk0, n_chunks);
+      fn<<<n_copy, 128, smem, s>>>(c, kn, vn, eps, n_new, n_copy, 0, chunk0, 0);
       note_launch(2);
     }
     err = cudaGetLastError();

@@ -21,9 +21,10 @@ cudaError_t launch_prefill_simt(const eva_config& cfg, const void* Q, const void
 // tcgen05/TMEM/TMA prefill (bf16, d in {64, 128}).  Returns cudaErrorNotSupported if the
 // shape is outside the kernel's envelope (the caller then reports EVA_ERR_UNSUPPORTED).
 bool prefill_sm100_supported(const eva_config& cfg);
+// variant: 0 = automatic, 1 = one 128-query tile per CTA, 2 = persistent pair kernel.
 cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
                                  const void* Ksum, const void* Vsum, void* O, float* lse,
-                                 cudaStream_t s);
+                                 uint32_t variant, cudaStream_t s);
 
 // Cache append: summaries of chunks completed in [pos, pos+n_new), ring write of the
 // last min(n_new, W) tokens.

@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "common.cuh"
@@ -277,6 +278,324 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// ========================================================================== pair kernel
+// Persistent variant for large problems: a CTA owns one SM and loops over work items
+// (unit, pair of adjacent 128-query tiles).  The two Q tiles share one K/V stream (the
+// union of their tile lists, loaded once through an NS-deep TMA ring), each Q tile has
+// its own softmax warpgroup and its own TMEM half (S double buffer + O):
+//   warp 0      TMA producer (Q tiles of the next item prefetched as soon as the last
+//               S MMA of the current item has consumed the old ones)
+//   warp 1      MMA issuer: per union tile j: S_t(j) for each Q tile t that needs j,
+//               then PV_t(j-1); stage released after the last PV that reads it
+//   warps 2-5   softmax + epilogue of Q tile 0;   warps 6-9   the same for Q tile 1
+// Epilogue: O / l straight from registers to global (rows are contiguous 2d-byte runs).
+constexpr int PAIR_THREADS = 320;
+constexpr uint32_t PAIR_TMEM_COLS = 512;
+
+template <int D, int NS>
+struct __align__(1024) SmemPair {
+  __nv_bfloat16 q[2][BM * D];
+  __nv_bfloat16 k[NS][BN * D];
+  __nv_bfloat16 v[NS][BN * D];
+  uint64_t q_full[2], q_empty[2];
+  uint64_t k_full[NS], v_full[NS], kv_empty[NS];
+  uint64_t s_full[2][2], p_full[2][2], o_done[2], o_final[2], o_empty[2];
+  uint32_t tmem_base;
+};
+
+struct PairPlan {
+  int n0, n_st, n_lt, lo0;
+  int nlast[2], lo_first[2], ns_last[2];
+  __device__ PairPlan(int pair, int T, int C, int W, int mode) {
+    n0 = pair * 2 * BM;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int a = n0 + t * BM;
+      if (a < T) {
+        nlast[t] = min(a + BM - 1, T - 1);
+        lo_first[t] = (int)mask_range(a, C, W, mode).lo;
+        ns_last[t] = (int)mask_range(nlast[t], C, W, mode).nsum;
+      } else {
+        nlast[t] = -1;
+        lo_first[t] = 0;
+        ns_last[t] = 0;
+      }
+    }
+    const int tl = nlast[1] >= 0 ? 1 : 0;
+    n_st = (ns_last[tl] + BN - 1) / BN;
+    lo0 = lo_first[0];
+    n_lt = (nlast[tl] - lo0 + 1 + BN - 1) / BN;
+  }
+  __device__ bool active(int t) const { return nlast[t] >= 0; }
+  __device__ int count() const { return n_st + n_lt; }
+  __device__ bool summary(int j) const { return j < n_st; }
+  __device__ int base(int j) const { return j < n_st ? j * BN : lo0 + (j - n_st) * BN; }
+  __device__ bool need(int t, int j) const {
+    if (nlast[t] < 0) return false;
+    const int b = base(j);
+    if (j < n_st) return b < ns_last[t];
+    return b <= nlast[t] && b + BN - 1 >= lo_first[t];
+  }
+  __device__ int last_need(int t) const {
+    for (int j = count() - 1; j >= 0; --j)
+      if (need(t, j)) return j;
+    return -1;
+  }
+};
+
+template <int D, int NS>
+__global__ void __launch_bounds__(PAIR_THREADS, 1)
+prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                    const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
+                    const __grid_constant__ CUtensorMap mVs, int BH, int T, int C, int W, int mode,
+                    float scale_log2, __nv_bfloat16* __restrict__ O, float* __restrict__ lse) {
+  extern __shared__ uint8_t smem_raw[];
+  SmemPair<D, NS>* sm = reinterpret_cast<SmemPair<D, NS>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ppu = (T + 2 * BM - 1) / (2 * BM);
+  const int n_items = BH * ppu;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mKs); tma_prefetch(&mVs);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&sm->q_full[t], 1);
+      mbar_init(&sm->q_empty[t], 1);
+      mbar_init(&sm->o_done[t], 1);
+      mbar_init(&sm->o_final[t], 1);
+      mbar_init(&sm->o_empty[t], 128);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&sm->s_full[t][b], 1);
+        mbar_init(&sm->p_full[t][b], 128);
+      }
+    }
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&sm->k_full[s], 1);
+      mbar_init(&sm->v_full[s], 1);
+      mbar_init(&sm->kv_empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm->tmem_base, PAIR_TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t kv = 0;
+      int qcnt[2] = {0, 0};
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int u = item / ppu;
+        const PairPlan plan(item % ppu, T, C, W, mode);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (!plan.active(t)) continue;
+          if (qcnt[t] > 0) mbar_wait(&sm->q_empty[t], (qcnt[t] - 1) & 1);
+          mbar_arrive_expect_tx(&sm->q_full[t], BM * D * 2);
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_3d(sm->q[t] + kb * BM * 64, &mQ, &sm->q_full[t], kb * 64, plan.n0 + t * BM, u);
+          ++qcnt[t];
+        }
+        const int NT = plan.count();
+        for (int j = 0; j < NT; ++j, ++kv) {
+          const int s = kv % NS;
+          if (kv >= (uint32_t)NS) mbar_wait(&sm->kv_empty[s], ((kv / NS) - 1) & 1);
+          const bool summ = plan.summary(j);
+          const int row = plan.base(j);
+          const CUtensorMap* mk = summ ? &mKs : &mK;
+          const CUtensorMap* mv = summ ? &mVs : &mV;
+          mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, row, u);
+          mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, row, u);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
+      uint32_t kv = 0;
+      int cS[2] = {0, 0}, cP[2] = {0, 0}, icnt[2] = {0, 0};
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const PairPlan plan(item % ppu, T, C, W, mode);
+        const int NT = plan.count();
+        const int last[2] = {plan.last_need(0), plan.last_need(1)};
+        bool first_pv[2] = {true, true};
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (plan.active(t)) mbar_wait(&sm->q_full[t], icnt[t] & 1);
+        auto issue_pv = [&](int jp, uint32_t kvp) {
+          const int sp = kvp % NS;
+          bool v_ready = false;
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (!plan.need(t, jp)) continue;
+            mbar_wait(&sm->p_full[t][cP[t] & 1], (cP[t] >> 1) & 1);
+            if (first_pv[t] && icnt[t] > 0) mbar_wait(&sm->o_empty[t], (icnt[t] - 1) & 1);
+            if (!v_ready) {
+              mbar_wait(&sm->v_full[sp], (kvp / NS) & 1);
+              v_ready = true;
+            }
+            tc_fence_after();
+            const uint32_t v_addr = smem_u32(sm->v[sp]);
+            const uint32_t tb = tmem + (uint32_t)t * 256;
+#pragma unroll
+            for (int ks = 0; ks < BN / 16; ++ks) {
+              const uint64_t b = smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024);
+              mma_ts(tb + TM_O, tb + (uint32_t)(cP[t] & 1) * BN + ks * 8, b, idesc_o,
+                     (!first_pv[t] || ks > 0) ? 1u : 0u);
+            }
+            mma_commit(&sm->o_done[t]);
+            if (jp == last[t]) mma_commit(&sm->o_final[t]);
+            first_pv[t] = false;
+            ++cP[t];
+          }
+          mma_commit(&sm->kv_empty[sp]);
+        };
+        for (int j = 0; j < NT; ++j, ++kv) {
+          const int s = kv % NS;
+          mbar_wait(&sm->k_full[s], (kv / NS) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(sm->k[s]);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (!plan.need(t, j)) continue;
+            const uint32_t q_addr = smem_u32(sm->q[t]);
+            const uint32_t d_tmem = tmem + (uint32_t)t * 256 + (uint32_t)(cS[t] & 1) * BN;
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+              const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+              const uint64_t a = smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024);
+              const uint64_t b = smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024);
+              mma_ss(d_tmem, a, b, idesc_s, ks > 0 ? 1u : 0u);
+            }
+            mma_commit(&sm->s_full[t][cS[t] & 1]);
+            if (j == last[t]) mma_commit(&sm->q_empty[t]);
+            ++cS[t];
+          }
+          if (j > 0) issue_pv(j - 1, kv - 1);
+        }
+        if (NT > 0) issue_pv(NT - 1, kv - 1);
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (plan.active(t)) ++icnt[t];
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int t = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t t_lane = tmem + (uint32_t)t * 256 + ((uint32_t)(quad * 32) << 16);
+    int cS = 0, icnt = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int u = item / ppu;
+      const PairPlan plan(item % ppu, T, C, W, mode);
+      if (!plan.active(t)) continue;
+      const int n = plan.n0 + t * BM + r;
+      const bool valid = n <= plan.nlast[t];
+      const Range rr = mask_range(valid ? n : plan.nlast[t], C, W, mode);
+      const int NT = plan.count();
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < NT; ++j) {
+        if (!plan.need(t, j)) continue;
+        const int b = cS & 1;
+        mbar_wait(&sm->s_full[t][b], (cS >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[64];
+        tmem_ld32(t_lane + (uint32_t)b * BN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        tmem_ld32(t_lane + (uint32_t)b * BN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        tmem_wait_ld();
+        const int base = plan.base(j);
+        int vlo, vhi;
+        if (plan.summary(j)) {
+          vlo = 0;
+          vhi = (int)min((int64_t)BN, rr.nsum - base);
+        } else {
+          vlo = (int)max((int64_t)0, rr.lo - base);
+          vhi = min(BN, n - base + 1);
+        }
+        if (!valid) vhi = vlo;
+        float x[64];
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          x[c] = (c >= vlo && c < vhi) ? __uint_as_float(sr[c]) * scale_log2 : -INFINITY;
+          mx = fmaxf(mx, x[c]);
+        }
+        const bool grow = mx > m_ref + 8.0f;
+        if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+          const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
+          mbar_wait(&sm->o_done[t], (cS - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(t_lane + TM_O + cc * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+            tmem_st32(t_lane + TM_O + cc * 32, o);
+          }
+          tmem_wait_st();
+          l *= f;
+        }
+        if (grow) m_ref = mx;
+        const float mref = m_ref == -INFINITY ? 0.f : m_ref;
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float p0 = ex2(x[2 * c] - mref), p1 = ex2(x[2 * c + 1] - mref);
+          l += p0 + p1;
+          pk[c] = pack_bf16(p0, p1);
+        }
+        tmem_st32(t_lane + (uint32_t)b * BN, pk);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm->p_full[t][b]);
+        ++cS;
+      }
+      // ---------------------------------------------------------- epilogue
+      mbar_wait(&sm->o_final[t], icnt & 1);
+      tc_fence_after();
+      const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+      uint32_t ob[D / 2];
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(t_lane + TM_O + cc * 32, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          ob[cc * 16 + i] = pack_bf16(__uint_as_float(o[2 * i]) * inv_l, __uint_as_float(o[2 * i + 1]) * inv_l);
+      }
+      tc_fence_before();
+      mbar_arrive(&sm->o_empty[t]);
+      if (valid) {
+        uint4* dst = reinterpret_cast<uint4*>(O + ((size_t)u * T + n) * D);
+#pragma unroll
+        for (int i = 0; i < D / 8; ++i)
+          dst[i] = make_uint4(ob[4 * i], ob[4 * i + 1], ob[4 * i + 2], ob[4 * i + 3]);
+        if (lse) lse[(size_t)u * T + n] = (m_ref + __log2f(l)) * 0.69314718055994531f;
+      }
+      ++icnt;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, PAIR_TMEM_COLS);
+}
+
 // ------------------------------------------------------------------ host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -339,6 +658,39 @@ cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const 
   return cudaGetLastError();
 }
 
+template <int D, int NS>
+cudaError_t launch_pair(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                        const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
+  const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
+  CUtensorMap mQ, mK, mV, mKs, mVs;
+  bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BN) &&
+            make_map(&mV, V, BH, T, D, BN);
+  if (nC > 0) {
+    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BN) && make_map(&mVs, Vsum, BH, nC, D, BN);
+  } else {
+    mKs = mK;
+    mVs = mV;
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(SmemPair<D, NS>) + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_pair_kernel<D, NS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int ppu = (T + 2 * BM - 1) / (2 * BM);
+  const int64_t items = (int64_t)BH * ppu;
+  const int grid = (int)std::min<int64_t>(items, num_sms());  // 1 CTA/SM: all CTAs co-resident
+  const float scale_log2 = cfg.scale * 1.4426950408889634f;
+  prefill_pair_kernel<D, NS><<<grid, PAIR_THREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, BH, T, cfg.chunk,
+                                                              cfg.window, cfg.mode, scale_log2,
+                                                              (__nv_bfloat16*)O, lse);
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool prefill_sm100_supported(const eva_config& cfg) {
@@ -347,10 +699,19 @@ bool prefill_sm100_supported(const eva_config& cfg) {
 
 cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
                                  const void* Ksum, const void* Vsum, void* O, float* lse,
-                                 cudaStream_t s) {
+                                 uint32_t variant, cudaStream_t s) {
   if (cfg.bh_count == 0) return cudaSuccess;
-  if (cfg.d_head == 128) return launch_t<128, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-  if (cfg.d_head == 64) return launch_t<64, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  const int64_t pairs = (int64_t)cfg.bh_count * ((cfg.T + 2 * BM - 1) / (2 * BM));
+  bool pair = pairs >= 2 * num_sms();  // enough items to keep every SM busy for 2+ rounds
+  if (variant == 1) pair = false;
+  if (variant == 2) pair = true;
+  if (pair) {
+    if (cfg.d_head == 128) return launch_pair<128, 4>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+    if (cfg.d_head == 64) return launch_pair<64, 8>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  } else {
+    if (cfg.d_head == 128) return launch_t<128, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+    if (cfg.d_head == 64) return launch_t<64, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  }
   return cudaErrorNotSupported;
 }
 

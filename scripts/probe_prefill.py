@@ -5,14 +5,16 @@ import numpy as np, torch
 import eva_inputs, oracle
 import paper_2511_00576_b200 as eva
 
+KERNEL = sys.argv[1] if len(sys.argv) > 1 else None
 def f64(t): return t.detach().float().cpu().double().numpy()
 for (B, H, T, d, C, W, mode) in [(1, 1, 128, 64, 64, 128, "sliding"), (1, 2, 515, 64, 64, 128, "sliding"),
                                  (1, 2, 700, 128, 64, 256, "sliding"), (1, 1, 130, 64, 16, 16, "block"),
-                                 (1, 1, 1, 128, 4, 8, "sliding")]:
+                                 (1, 1, 1, 128, 4, 8, "sliding"), (2, 3, 1100, 64, 32, 96, "sliding"),
+                                 (1, 3, 300, 128, 16, 32, "block"), (1, 8, 4096, 128, 64, 256, "sliding")]:
     cfg = eva.make_config(B, H, T, d, C, W, mode=mode)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=2, device="cuda")
     O1, l1, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=True)
-    O2, l2, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True)
+    O2, l2, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, kernel=KERNEL)
     torch.cuda.synchronize()
     E = oracle.eps_units(cfg.seed, 0, 0, B * H, T // C, d)
     rk, rv = oracle.summarize_batch(f64(K), f64(V), E, C)

@@ -112,18 +112,22 @@ CASES = [  # (B, H, T, d, C, W)
     (1, 1, 40, 64, 64, 128),      # T < C: no summaries at all
     (1, 1, 1, 128, 4, 8),         # T = 1
     (1, 1, 96, 64, 1, 3),         # C = 1: exact causal softmax
+    (2, 3, 1100, 64, 32, 96),     # several pair items per unit, Q tile 1 partly past T
+    (1, 3, 300, 128, 16, 32),     # last pair: Q tile 1 = rows 256..299
 ]
 
 
 @pytest.mark.parametrize("mode", ["sliding", "block"])
 @pytest.mark.parametrize("case", CASES)
-@pytest.mark.parametrize("dtype,simt", [(torch.float32, True), (torch.bfloat16, True),
-                                        (torch.bfloat16, False)])
-def test_prefill_parity(eva, case, mode, dtype, simt):
+@pytest.mark.parametrize("dtype,kernel", [(torch.float32, "simt"), (torch.bfloat16, "simt"),
+                                          (torch.bfloat16, "tile"), (torch.bfloat16, "pair")])
+def test_prefill_parity(eva, case, mode, dtype, kernel):
     B, H, T, d, C, W = case
+    if kernel in ("tile", "pair") and d not in (64, 128):
+        pytest.skip("tensor-core kernels cover d in {64, 128}; other d run the SIMT kernel")
     cfg = eva.make_config(B, H, T, d, C, W, mode=mode, dtype=dtype, seed=7)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=2, device="cuda")
-    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=simt)
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, kernel=kernel)
     torch.cuda.synchronize()
     nC = T // C
     E = oracle_eps_for(cfg, nC, d)
@@ -150,15 +154,17 @@ def test_prefill_window_covers_sequence_is_softmax(eva, dtype, simt):
     assert (O.double() - ref).abs().max().item() <= TOL[dtype]
 
 
-@pytest.mark.parametrize("dtype,simt", [(torch.float32, True), (torch.bfloat16, False)])
-def test_prefill_summaries_provided_and_poison(eva, dtype, simt):
+@pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, "tile"),
+                                               (torch.bfloat16, False, "pair")])
+def test_prefill_summaries_provided_and_poison(eva, dtype, simt, kernel):
     """Everything a query block must not see is poisoned with large finite values;
     its outputs must not move (bit-exact).  Uses EVA_SUMMARIES_PROVIDED."""
     T, d, C, W = 1024, 64, 64, 128
     cfg = eva.make_config(1, 1, T, d, C, W, dtype=dtype)
     Q, K, V = eva_inputs.qkv(0, 1, T, d, dtype, seed=5, device="cuda")
     ks, vs = eva.eva_summarize(cfg, K, V)
-    O, lse, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, simt=simt)
+    O, lse, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, simt=simt,
+                                        kernel=kernel)
     n0, n1 = 512, 639  # one 128-query block
     lo0, _ = oracle.mask(n0, C, W, 0)
     _, ns1 = oracle.mask(n1, C, W, 0)
@@ -170,7 +176,7 @@ def test_prefill_summaries_provided_and_poison(eva, dtype, simt):
     ks2[:, ns1:] = 3e4
     vs2[:, ns1:] = -3e4
     O2, lse2, _, _ = eva.eva_attn_prefill(cfg, Q, K2, V2, Ksum=ks2, Vsum=vs2, summaries_provided=True,
-                                          simt=simt)
+                                          simt=simt, kernel=kernel)
     assert torch.equal(O2[:, n0:n1 + 1], O[:, n0:n1 + 1])
     assert torch.equal(lse2[:, n0:n1 + 1], lse[:, n0:n1 + 1])
 
@@ -218,17 +224,18 @@ def test_prefill_detects_beta_perturbation(eva):
     assert np.array_equal(moved, sees)
 
 
-@pytest.mark.parametrize("dtype,simt", [(torch.float32, True), (torch.bfloat16, False)])
-def test_sharded_equals_unsharded(eva, dtype, simt):
+@pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, "tile"),
+                                               (torch.bfloat16, False, "pair")])
+def test_sharded_equals_unsharded(eva, dtype, simt, kernel):
     """(b,h) shards computed separately are bitwise equal to the full run (RNG keyed by global unit)."""
     B, H, T, d, C, W = 2, 3, 384, 64, 32, 64
     cfg = eva.make_config(B, H, T, d, C, W, dtype=dtype)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=8, device="cuda")
-    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=simt)
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=simt, kernel=kernel)
     for b0, cnt in ((0, 2), (2, 3), (5, 1)):
         c2 = eva.make_config(B, H, T, d, C, W, dtype=dtype, bh_begin=b0, bh_count=cnt)
         q, k, v = eva_inputs.qkv(b0, cnt, T, d, dtype, seed=8, device="cuda")
-        O2, lse2, ks2, vs2 = eva.eva_attn_prefill(c2, q, k, v, simt=simt)
+        O2, lse2, ks2, vs2 = eva.eva_attn_prefill(c2, q, k, v, simt=simt, kernel=kernel)
         assert torch.equal(O2, O[b0:b0 + cnt]) and torch.equal(lse2, lse[b0:b0 + cnt])
         assert torch.equal(ks2, ks[b0:b0 + cnt]) and torch.equal(vs2, vs[b0:b0 + cnt])
 
@@ -326,13 +333,14 @@ def test_decode_capacity_error(eva):
 
 
 # ----------------------------------------------------------------------------- full-size sampled parity
+@pytest.mark.parametrize("kernel", [None, "tile", "pair"])
 @pytest.mark.parametrize("B,H,T,d,C,W", [(1, 16, 2048, 64, 64, 128), (1, 4, 8192, 128, 64, 256)])
-def test_full_size_sampled_parity(eva, B, H, T, d, C, W):
+def test_full_size_sampled_parity(eva, B, H, T, d, C, W, kernel):
     """BASELINE configs[1] (full) and configs[2] (4 of its 256 units, same kernel launch
     shape per unit) on the bf16 tensor-core path; oracle on sampled rows."""
     cfg = eva.make_config(B, H, T, d, C, W, dtype=torch.bfloat16)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device="cuda")
-    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, kernel=kernel)
     nC = T // C
     rng = np.random.default_rng(1)
     for u in (0, B * H - 1):
