@@ -81,7 +81,7 @@ typedef struct {
   int32_t mode;               /* eva_window_mode */
   int32_t dtype;              /* eva_dtype */
   int32_t omega_mode;         /* eva_omega_mode */
-  float scale;                /* logit scale s on q.k and q.k~ (reading R5), e.g. 1/sqrt(d) */
+  float scale;                /* logit scale s > 0 on q.k and q.k~ (reading R5), e.g. 1/sqrt(d) */
   float lambda;               /* Eq.15 lambda, paper value 0.1                 */
   float clip;                 /* Eq.15 clip bound, paper value 1               */
   uint32_t layer;             /* RNG key component (reading R9)                         */
@@ -168,10 +168,22 @@ typedef struct {
 eva_status eva_cache_append(eva_cache* cache, const void* K_new, const void* V_new, int32_t n_new,
                             const float* eps, eva_stream_t stream);
 
+/* Prefill hand-off when the prompt's summaries already exist (e.g. Ksum/Vsum written
+ * by eva_attn_prefill): equivalent to eva_cache_append(cache, K, V, n, eps) on an empty
+ * cache (the summaries are the same function of the same chunks, R13), but copies the
+ * nC = floor(n / C) summary rows instead of recomputing them.
+ * K, V       : [bh_count, n, d] cfg.dtype -- the prompt's keys and values
+ * Ksum, Vsum : [bh_count, nC, d] cfg.dtype (may be NULL when nC == 0)
+ * Requires cache->pos == 0.  EVA_ERR_CAPACITY if nC > cap_chunks.  On success pos = n. */
+eva_status eva_cache_load(eva_cache* cache, const void* K, const void* V, const void* Ksum,
+                          const void* Vsum, int32_t n, eva_stream_t stream);
+
 /* One query per unit at position n = pos - 1 over the cache (Eq.12, one row):
  * Q, O : [bh_count, d] cfg.dtype;  lse : [bh_count] fp32 or NULL.
  * workspace : device scratch of eva_decode_workspace_bytes(cache) bytes (may be
- *             NULL when that is 0).  pos must be >= 1. */
+ *             NULL when that is 0).  It must be zero-filled before its first use; every
+ *             call leaves it zero-filled where it matters (split-K merge counters), so
+ *             one buffer serves a whole generation.  pos must be >= 1. */
 eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float* lse,
                            void* workspace, size_t workspace_bytes, eva_stream_t stream);
 size_t eva_decode_workspace_bytes(const eva_cache* cache);

@@ -5,7 +5,7 @@ thin torch binding with the same names.  Importing this package loads
 libeva.so and fails loudly if it has not been built.
 """
 from .api import (DecodeCache, EvaConfig, EvaError, eva_attn_decode, eva_attn_prefill,  # noqa: F401
-                  eva_cache_append, eva_draw_eps, eva_mask_ranges, eva_philox, eva_summarize,
+                  eva_cache_append, eva_cache_load, eva_draw_eps, eva_mask_ranges, eva_philox, eva_summarize,
                   launch_count, make_config, version)
 
 __version__ = "0.1.0"

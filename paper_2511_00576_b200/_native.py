@@ -41,9 +41,10 @@ class EvaCache(ctypes.Structure):
                 ("ring_v", ctypes.c_void_p), ("sum_k", ctypes.c_void_p), ("sum_v", ctypes.c_void_p)]
 
 
-EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache_append",
+EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache_append", "eva_cache_load",
            "eva_attn_decode", "eva_decode_workspace_bytes", "eva_mask_ranges", "eva_philox",
-           "eva_draw_eps", "eva_last_error", "eva_version", "eva_launch_count"]
+           "eva_draw_eps", "eva_last_error", "eva_version", "eva_launch_count",
+           "eva_debug_trace_prefill"]
 
 
 class EvaError(RuntimeError):
@@ -67,6 +68,7 @@ def _load():
         "eva_attn_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_uint32, P]),
         "eva_cache_append": (st, [CACHE, P, P, ctypes.c_int32, P, P]),
         "eva_attn_decode": (st, [CACHE, P, P, P, P, ctypes.c_size_t, P]),
+        "eva_cache_load": (st, [CACHE, P, P, P, P, ctypes.c_int32, P]),
         "eva_decode_workspace_bytes": (ctypes.c_size_t, [CACHE]),
         "eva_mask_ranges": (st, [CFG, ctypes.c_int64, ctypes.c_int64, P, P, P]),
         "eva_philox": (st, [P, P, ctypes.c_int32, P]),
@@ -74,6 +76,7 @@ def _load():
         "eva_last_error": (ctypes.c_char_p, []),
         "eva_version": (ctypes.c_char_p, []),
         "eva_launch_count": (ctypes.c_uint64, []),
+        "eva_debug_trace_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_int32, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

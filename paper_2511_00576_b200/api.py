@@ -15,7 +15,7 @@ import torch
 from . import _native as N
 from ._native import EvaCache, EvaConfig, EvaError, check, lib
 
-__all__ = ["make_config", "eva_summarize", "eva_attn_prefill", "eva_cache_append",
+__all__ = ["make_config", "eva_summarize", "eva_attn_prefill", "eva_cache_append", "eva_cache_load",
            "eva_attn_decode", "DecodeCache", "eva_mask_ranges", "eva_philox", "eva_draw_eps",
            "EvaConfig", "EvaError", "launch_count", "version"]
 
@@ -177,6 +177,23 @@ class DecodeCache:
 
     append = eva_cache_append
 
+    def eva_cache_load(self, K: torch.Tensor, V: torch.Tensor, Ksum: Optional[torch.Tensor] = None,
+                       Vsum: Optional[torch.Tensor] = None) -> None:
+        """Prefill hand-off into an empty cache with already-computed summaries."""
+        cfg = self.c.cfg
+        dt, bh, d = _tdtype(cfg), cfg.bh_count, cfg.d_head
+        n = K.shape[1]
+        nC = n // cfg.chunk
+        _need(K, "K", (bh, n, d), dt)
+        _need(V, "V", (bh, n, d), dt)
+        if nC:
+            _need(Ksum, "Ksum", (bh, nC, d), dt)
+            _need(Vsum, "Vsum", (bh, nC, d), dt)
+        check(lib.eva_cache_load(ctypes.byref(self.c), _ptr(K), _ptr(V), _ptr(Ksum if nC else None),
+                                 _ptr(Vsum if nC else None), n, _stream(self.device)))
+
+    load = eva_cache_load
+
     def eva_attn_decode(self, q: torch.Tensor, O: Optional[torch.Tensor] = None,
                         lse: Optional[torch.Tensor] = None, want_lse: bool = True):
         """One query per unit at position pos-1: q [bh, d] -> (o [bh, d], lse [bh])."""
@@ -188,7 +205,7 @@ class DecodeCache:
             lse = torch.empty(bh, dtype=torch.float32, device=q.device)
         nbytes = self.workspace_bytes()
         if nbytes and (self._ws is None or self._ws.numel() * 4 < nbytes):
-            self._ws = torch.empty((nbytes + 3) // 4 * 2, dtype=torch.float32, device=q.device)
+            self._ws = torch.zeros((nbytes + 3) // 4 * 2, dtype=torch.float32, device=q.device)
         ws = self._ws if nbytes else None
         check(lib.eva_attn_decode(ctypes.byref(self.c), _ptr(q), _ptr(O),
                                   _ptr(lse if want_lse else None), _ptr(ws),
@@ -219,6 +236,11 @@ def eva_cache_append(cache: "DecodeCache", K_new: torch.Tensor, V_new: torch.Ten
                      eps: Optional[torch.Tensor] = None) -> None:
     """C-ABI-named alias of DecodeCache.eva_cache_append."""
     cache.eva_cache_append(K_new, V_new, eps)
+
+
+def eva_cache_load(cache: "DecodeCache", K, V, Ksum=None, Vsum=None) -> None:
+    """C-ABI-named alias of DecodeCache.eva_cache_load."""
+    cache.eva_cache_load(K, V, Ksum, Vsum)
 
 
 def eva_attn_decode(cache: "DecodeCache", q: torch.Tensor, **kw):

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "../../include/eva.h"
+#include "../../include/eva_debug.h"
 #include "common.cuh"
 #include "launch.h"
 
@@ -67,8 +68,8 @@ eva_status check_cfg(const eva_config* cfg, bool need_T) {
   if (cfg->omega_mode != EVA_OMEGA_AS_PRINTED && cfg->omega_mode != EVA_OMEGA_SHIFTED_NOISE)
     return fail(EVA_ERR_INVALID_ARG, "omega_mode=%d", cfg->omega_mode);
   if (!std::isfinite(cfg->scale) || !std::isfinite(cfg->lambda) || !std::isfinite(cfg->clip) ||
-      cfg->clip < 0.f)
-    return fail(EVA_ERR_INVALID_ARG, "scale/lambda/clip must be finite, clip >= 0");
+      cfg->clip < 0.f || !(cfg->scale > 0.f))
+    return fail(EVA_ERR_INVALID_ARG, "scale must be finite and > 0, lambda finite, clip finite >= 0");
   if (cfg->samples != 1)
     return fail(EVA_ERR_UNSUPPORTED, "samples=%d: only S=1 makes beta query-independent (P:101)",
                 cfg->samples);
@@ -185,13 +186,40 @@ eva_status eva_cache_append(eva_cache* cache, const void* K_new, const void* V_n
   return ok();
 }
 
+eva_status eva_cache_load(eva_cache* cache, const void* K, const void* V, const void* Ksum,
+                          const void* Vsum, int32_t n, eva_stream_t stream) {
+  if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
+  eva_status st = check_cfg(&cache->cfg, false);
+  if (st != EVA_OK) return st;
+  if (n < 1) return fail(EVA_ERR_INVALID_ARG, "n=%d must be >= 1", n);
+  if (cache->pos != 0) return fail(EVA_ERR_INVALID_ARG, "eva_cache_load needs an empty cache (pos=%lld)", (long long)cache->pos);
+  const int nC = n / cache->cfg.chunk;
+  if (nC > cache->cap_chunks) return fail(EVA_ERR_CAPACITY, "%d summaries > cap %d", nC, cache->cap_chunks);
+  if (cache->cfg.bh_count > 0) {
+    const void* p[] = {K, V, cache->ring_k, cache->ring_v};
+    const char* nm[] = {"K", "V", "ring_k", "ring_v"};
+    if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+    if (nC > 0) {
+      const void* p2[] = {Ksum, Vsum, cache->sum_k, cache->sum_v};
+      const char* nm2[] = {"Ksum", "Vsum", "sum_k", "sum_v"};
+      if ((st = check_ptrs(4, p2, nm2)) != EVA_OK) return st;
+    }
+    cudaError_t e = eva::launch_cache_load(*cache, K, V, Ksum, Vsum, n, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "eva_cache_load");
+  }
+  cache->pos = n;
+  return ok();
+}
+
 size_t eva_decode_workspace_bytes(const eva_cache* cache) {
   if (!cache || cache->pos < 1 || cache->cfg.chunk < 1 || cache->cfg.window < 1 ||
       !d_supported(cache->cfg.d_head))
     return 0;
   const int S = eva::decode_splits(*cache);
   if (S <= 1) return 0;
-  return (size_t)cache->cfg.bh_count * S * (cache->cfg.d_head + 2) * sizeof(float);
+  // split partials (m, l, acc[d]) per (unit, split) + one merge counter per unit
+  return (size_t)cache->cfg.bh_count * S * (cache->cfg.d_head + 2) * sizeof(float) +
+         (size_t)cache->cfg.bh_count * sizeof(unsigned);
 }
 
 eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float* lse,
@@ -214,7 +242,7 @@ eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float
   }
   if (lse && !aligned16(lse)) return fail(EVA_ERR_INVALID_ARG, "lse is not 16-byte aligned");
   const int S = eva::decode_splits(*cache);
-  const size_t need = S > 1 ? (size_t)cache->cfg.bh_count * S * (cache->cfg.d_head + 2) * sizeof(float) : 0;
+  const size_t need = eva_decode_workspace_bytes(cache);
   if (need > 0 && (!workspace || workspace_bytes < need))
     return fail(EVA_ERR_INVALID_ARG, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
   if (workspace && !aligned16(workspace)) return fail(EVA_ERR_INVALID_ARG, "workspace is not 16-byte aligned");
@@ -246,6 +274,20 @@ eva_status eva_draw_eps(const eva_config* cfg, float* eps, eva_stream_t stream) 
   if (st != EVA_OK) return st;
   if (cfg->bh_count > 0 && cfg->T / cfg->chunk > 0 && !eps) return fail(EVA_ERR_INVALID_ARG, "eps is NULL");
   return cuda_status(eva::launch_draw_eps(*cfg, eps, (cudaStream_t)stream), "eva_draw_eps");
+}
+
+eva_status eva_debug_trace_prefill(const eva_config* cfg, const void* Q, const void* K,
+                                   const void* V, const void* Ksum, const void* Vsum, void* O,
+                                   float* lse, unsigned long long* trace, int32_t cap,
+                                   eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (cfg->dtype != EVA_BF16 || (cfg->d_head != 64 && cfg->d_head != 128))
+    return fail(EVA_ERR_UNSUPPORTED, "trace needs bf16, d in {64,128}");
+  if (!trace || cap < 1) return fail(EVA_ERR_INVALID_ARG, "trace buffer");
+  return cuda_status(eva::debug_trace_prefill(*cfg, Q, K, V, Ksum, Vsum, O, lse, trace, cap,
+                                              (cudaStream_t)stream),
+                     "eva_debug_trace_prefill");
 }
 
 const char* eva_last_error(void) { return g_err.c_str(); }

@@ -346,48 +346,81 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
       ws[((size_t)u * S + s) * (D + 2) + 2 + ch] = o;
     }
   }
+  if (S == 1) {
+    if (lane == 0 && lse) lse[u] = M + logf(L);
+    return;
+  }
   if (lane == 0) {
-    if (S == 1) {
-      if (lse) lse[u] = M + logf(L);
-    } else {
-      float* p = ws + ((size_t)u * S + s) * (D + 2);
-      p[0] = M;
-      p[1] = L;
+    float* p = ws + ((size_t)u * S + s) * (D + 2);
+    p[0] = M;
+    p[1] = L;
+  }
+  // split-K: the last CTA of this unit to finish merges the S partials (no second launch).
+  // Counters live after the partials and are left at zero for the next call.
+  unsigned* counters = reinterpret_cast<unsigned*>(ws + (size_t)gridDim.x * S * (D + 2));
+  __threadfence();
+  __syncwarp();
+  unsigned prev = 0;
+  if (lane == 0) prev = atomicAdd(&counters[u], 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != (unsigned)(S - 1)) return;
+  __threadfence();
+  const volatile float* pu = ws + (size_t)u * S * (D + 2);
+  float Mg = -INFINITY;
+  for (int k = 0; k < S; ++k) Mg = fmaxf(Mg, pu[(size_t)k * (D + 2)]);
+  float Lg = 0.f;
+  for (int k = 0; k < S; ++k) {
+    const float mk = pu[(size_t)k * (D + 2)];
+    Lg += (mk == -INFINITY ? 0.f : __expf(mk - Mg)) * pu[(size_t)k * (D + 2) + 1];
+  }
+  for (int ch = lane; ch < D; ch += 32) {
+    float o = 0.f;
+    for (int k = 0; k < S; ++k) {
+      const float mk = pu[(size_t)k * (D + 2)];
+      if (mk != -INFINITY) o += __expf(mk - Mg) * pu[(size_t)k * (D + 2) + 2 + ch];
     }
+    O[(size_t)u * D + ch] = Elem<T>::from_f(o / Lg);
+  }
+  if (lane == 0) {
+    if (lse) lse[u] = Mg + logf(Lg);
+    counters[u] = 0u;
   }
 }
 
-// Merge split-K partials: one warp per unit.
+// ============================================================================ cache load
+// Prefill hand-off with summaries already computed: one flat grid of 16-byte copies,
+//   pieces [0, n_ring)            : the last keep = min(n, W) tokens -> ring slots (p mod W)
+//   pieces [n_ring, n_ring+n_sum) : Ksum/Vsum rows [bh, nC, d] -> sum_k/sum_v rows [bh, cap, d]
 template <typename T, int D>
-__global__ void __launch_bounds__(128) decode_merge_kernel(int bh_count, int S, const float* __restrict__ ws,
-                                                           T* __restrict__ O, float* __restrict__ lse) {
-  using LM = LaneMap<D>;
-  constexpr int CPL = LM::CPL;
-  const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (u >= bh_count) return;
-  const float* p = ws + (size_t)u * S * (D + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < S; ++s) M = fmaxf(M, p[(size_t)s * (D + 2)]);
-  float L = 0.f, out[CPL];
-#pragma unroll
-  for (int j = 0; j < CPL; ++j) out[j] = 0.f;
-  for (int s = 0; s < S; ++s) {
-    const float* q = p + (size_t)s * (D + 2);
-    const float f = q[0] == -INFINITY ? 0.f : __expf(q[0] - M);
-    L += f * q[1];
-    if (lane < LM::LANES) {
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) out[j] += f * q[2 + lane * CPL + j];
-    }
+__global__ void __launch_bounds__(256) cache_load_kernel(eva_cache c, const T* __restrict__ K,
+                                                         const T* __restrict__ V,
+                                                         const T* __restrict__ Ksum,
+                                                         const T* __restrict__ Vsum, int n, int nC) {
+  constexpr int PPR = D * (int)sizeof(T) / 16;
+  const int W = c.cfg.window;
+  const int keep = min(n, W);
+  const int64_t n_ring = (int64_t)c.cfg.bh_count * keep * PPR;
+  const int64_t n_sum = (int64_t)c.cfg.bh_count * nC * PPR;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_ring) {
+    const int u = (int)(i / ((int64_t)keep * PPR));
+    const int rem = (int)(i % ((int64_t)keep * PPR));
+    const int r = n - keep + rem / PPR, p = rem % PPR;
+    const size_t slot = (size_t)((c.pos + r) % W);
+    const size_t src = ((size_t)u * n + r) * D * sizeof(T) / 16 + p;
+    const size_t dst = ((size_t)u * W + slot) * D * sizeof(T) / 16 + p;
+    reinterpret_cast<uint4*>(c.ring_k)[dst] = reinterpret_cast<const uint4*>(K)[src];
+    reinterpret_cast<uint4*>(c.ring_v)[dst] = reinterpret_cast<const uint4*>(V)[src];
+  } else if (i < n_ring + n_sum) {
+    const int64_t k = i - n_ring;
+    const int u = (int)(k / ((int64_t)nC * PPR));
+    const int rem = (int)(k % ((int64_t)nC * PPR));
+    const int row = rem / PPR, p = rem % PPR;
+    const size_t src = ((size_t)u * nC + row) * D * sizeof(T) / 16 + p;
+    const size_t dst = ((size_t)u * c.cap_chunks + row) * D * sizeof(T) / 16 + p;
+    reinterpret_cast<uint4*>(c.sum_k)[dst] = reinterpret_cast<const uint4*>(Ksum)[src];
+    reinterpret_cast<uint4*>(c.sum_v)[dst] = reinterpret_cast<const uint4*>(Vsum)[src];
   }
-  if (lane < LM::LANES) {
-    const float il = 1.0f / L;
-#pragma unroll
-    for (int j = 0; j < CPL; ++j) out[j] *= il;
-    store_vec<T, CPL>(O + (size_t)u * D + lane * CPL, out);
-  }
-  if (lse && lane == 0) lse[u] = M + logf(L);
 }
 
 // ============================================================================ debug kernels
@@ -556,11 +589,20 @@ cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse
     dim3 grid(c.cfg.bh_count, splits);
     decode_kernel<T, D><<<grid, 128, 0, s>>>(c, (const T*)Q, (T*)O, lse, ws);
     note_launch();
-    if (splits > 1) {
-      decode_merge_kernel<T, D><<<(c.cfg.bh_count + 3) / 4, 128, 0, s>>>(c.cfg.bh_count, splits,
-                                                                         ws, (T*)O, lse);
-      note_launch();
-    }
+  }));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cache_load(const eva_cache& c, const void* K, const void* V, const void* Ksum,
+                              const void* Vsum, int n, cudaStream_t s) {
+  if (c.cfg.bh_count == 0) return cudaSuccess;
+  const int nC = n / c.cfg.chunk;
+  EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
+    constexpr int PPR = D * (int)sizeof(T) / 16;
+    const int64_t pieces = (int64_t)c.cfg.bh_count * (std::min(n, c.cfg.window) + nC) * PPR;
+    cache_load_kernel<T, D><<<(unsigned)((pieces + 255) / 256), 256, 0, s>>>(
+        c, (const T*)K, (const T*)V, (const T*)Ksum, (const T*)Vsum, n, nC);
+    note_launch();
   }));
   return cudaGetLastError();
 }

@@ -26,10 +26,19 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const voi
                                  const void* Ksum, const void* Vsum, void* O, float* lse,
                                  uint32_t variant, cudaStream_t s);
 
+// Debug: run the pair kernel with CTA 0 recording a (clock64, event) timeline into trace_dev.
+cudaError_t debug_trace_prefill(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                const void* Ksum, const void* Vsum, void* O, float* lse,
+                                unsigned long long* trace_dev, int cap, cudaStream_t s);
+
 // Cache append: summaries of chunks completed in [pos, pos+n_new), ring write of the
 // last min(n_new, W) tokens.
 cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* Vn, int n_new,
                                 const float* eps, cudaStream_t s);
+
+// Prefill hand-off with provided summaries (cache.pos == 0): ring + summary copies.
+cudaError_t launch_cache_load(const eva_cache& c, const void* K, const void* V, const void* Ksum,
+                              const void* Vsum, int n, cudaStream_t s);
 
 // Decode: splits chosen by the host (workspace needed when splits > 1).
 int decode_splits(const eva_cache& c);

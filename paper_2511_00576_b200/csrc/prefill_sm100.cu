@@ -60,6 +60,67 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+
+// One softmax step of a 64-key tile for this thread's query row (thread <-> TMEM lane).
+// S (fp32, raw q.k) is read from TMEM, columns outside [vlo, vhi) are masked, the running
+// max m_ref (log2 units) is raised lazily (O and l are only rescaled when the tile max
+// exceeds m_ref by more than 8, i.e. p <= 2^8), and P = exp2(s*scale_log2 - m_ref) is
+// written back to the same TMEM columns as packed bf16 (the A operand of the PV MMA).
+// wait_o() must make the previous PV of this Q tile complete before O is rescaled.
+// Requires scale_log2 > 0 (validated by the C ABI), so max and scaling commute.
+template <int D, typename WaitO>
+__device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, int vlo, int vhi,
+                                             float scale_log2, float& m_ref, float& l,
+                                             const WaitO& wait_o) {
+  uint32_t sr[64];
+  tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+  tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+  tmem_wait_ld();
+  const bool full = vlo <= 0 && vhi >= 64;
+  if (!__all_sync(0xffffffffu, full)) {
+#pragma unroll
+    for (int c = 0; c < 64; ++c)
+      if (c < vlo || c >= vhi) sr[c] = 0xff800000u;  // -inf
+  }
+  float mx = __uint_as_float(sr[0]);
+#pragma unroll
+  for (int c = 1; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
+  mx *= scale_log2;
+  const bool grow = mx > m_ref + 8.0f;
+  if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+    const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
+    wait_o();
+    tc_fence_after();
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(o_addr + cc * 32, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+      tmem_st32(o_addr + cc * 32, o);
+    }
+    tmem_wait_st();
+    l *= f;
+  }
+  if (grow) m_ref = mx;
+  const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
+  uint32_t pk[32];
+  float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg));
+    const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg));
+    l0 += p0;
+    l1 += p1;
+    pk[c] = pack_bf16(p0, p1);
+  }
+  l += l0 + l1;
+  tmem_st32(s_addr, pk);
+  tmem_wait_st();
+  tc_fence_before();
+}
+
 struct TilePlan {
   int n0, nlast, n_st, n_lt, lo0;
   __device__ TilePlan(int qt, int T, int C, int W, int mode) {
@@ -115,19 +176,24 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
 
+  // Producer and MMA roles run on whole warps (warp-uniform control flow keeps every
+  // descriptor and coordinate in uniform registers); one elected lane issues.
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
+    if (elect_one()) {
       mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
       for (int kb = 0; kb < D / 64; ++kb)
         tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
-      for (int j = 0; j < NT; ++j) {
-        const int s = j % NSTAGE;
-        if (j >= NSTAGE) mbar_wait(&sm->kv_empty[s], ((j / NSTAGE) - 1) & 1);
-        const bool summ = plan.summary(j);
-        const int row = plan.base(j);
-        const CUtensorMap* mk = summ ? &mKs : &mK;
-        const CUtensorMap* mv = summ ? &mVs : &mV;
+    }
+    __syncwarp();
+    for (int j = 0; j < NT; ++j) {
+      const int s = j % NSTAGE;
+      if (j >= NSTAGE) mbar_wait(&sm->kv_empty[s], ((j / NSTAGE) - 1) & 1);
+      const bool summ = plan.summary(j);
+      const int row = plan.base(j);
+      const CUtensorMap* mk = summ ? &mKs : &mK;
+      const CUtensorMap* mv = summ ? &mVs : &mV;
+      if (elect_one()) {
         mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
         for (int kb = 0; kb < D / 64; ++kb)
           tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, row, u);
@@ -135,21 +201,22 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         for (int kb = 0; kb < D / 64; ++kb)
           tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, row, u);
       }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
-      const uint32_t q_addr = smem_u32(sm->q);
-      mbar_wait(&sm->q_full, 0);
-      for (int j = 0; j <= NT; ++j) {
-        if (j < NT) {
-          const int s = j % NSTAGE;
-          mbar_wait(&sm->k_full[s], (j / NSTAGE) & 1);
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(sm->k[s]);
-          const uint32_t d_tmem = tmem + (uint32_t)(j & 1) * BN;
+    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
+    const uint32_t q_addr = smem_u32(sm->q);
+    mbar_wait(&sm->q_full, 0);
+    for (int j = 0; j <= NT; ++j) {
+      if (j < NT) {
+        const int s = j % NSTAGE;
+        mbar_wait(&sm->k_full[s], (j / NSTAGE) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sm->k[s]);
+        const uint32_t d_tmem = tmem + (uint32_t)(j & 1) * BN;
+        if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < D / 16; ++ks) {
             const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
@@ -159,12 +226,15 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
           }
           mma_commit(&sm->s_full[j & 1]);
         }
-        if (j >= 1) {
-          const int jj = j - 1, s = jj % NSTAGE;
-          mbar_wait(&sm->p_full[jj & 1], (jj >> 1) & 1);
-          mbar_wait(&sm->v_full[s], (jj / NSTAGE) & 1);
-          tc_fence_after();
-          const uint32_t v_addr = smem_u32(sm->v[s]);
+        __syncwarp();
+      }
+      if (j >= 1) {
+        const int jj = j - 1, s = jj % NSTAGE;
+        mbar_wait(&sm->p_full[jj & 1], (jj >> 1) & 1);
+        mbar_wait(&sm->v_full[s], (jj / NSTAGE) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sm->v[s]);
+        if (elect_one()) {
 #pragma unroll
           for (int ks = 0; ks < BN / 16; ++ks) {
             const uint32_t a_tmem = tmem + (uint32_t)(jj & 1) * BN + ks * 8;
@@ -175,6 +245,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
           mma_commit(&sm->o_done);
           if (jj == NT - 1) mma_commit(&sm->o_final);
         }
+        __syncwarp();
       }
     }
   } else {
@@ -189,10 +260,6 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     for (int j = 0; j < NT; ++j) {
       mbar_wait(&sm->s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[64];
-      tmem_ld32(t_lane + (uint32_t)(j & 1) * BN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(t_lane + (uint32_t)(j & 1) * BN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_wait_ld();
       const int base = plan.base(j);
       int vlo, vhi;
       if (plan.summary(j)) {
@@ -203,43 +270,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         vhi = min(BN, n - base + 1);
       }
       if (!valid) vhi = vlo;
-      float x[64];
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        x[c] = (c >= vlo && c < vhi) ? __uint_as_float(sr[c]) * scale_log2 : -INFINITY;
-        mx = fmaxf(mx, x[c]);
-      }
-      const bool grow = mx > m_ref + 8.0f;
-      if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
-        // lazy rescale of the running O (TMEM) and l; wait for PV_{j-1} first
-        const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
-        mbar_wait(&sm->o_done, (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
-          uint32_t o[32];
-          tmem_ld32(t_lane + TM_O + cc * 32, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-          tmem_st32(t_lane + TM_O + cc * 32, o);
-        }
-        tmem_wait_st();
-        l *= f;
-      }
-      if (grow) m_ref = mx;
-      const float mref = m_ref == -INFINITY ? 0.f : m_ref;
-      uint32_t pk[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const float p0 = ex2(x[2 * c] - mref), p1 = ex2(x[2 * c + 1] - mref);
-        l += p0 + p1;
-        pk[c] = pack_bf16(p0, p1);
-      }
-      tmem_st32(t_lane + (uint32_t)(j & 1) * BN, pk);
-      tmem_wait_st();
-      tc_fence_before();
+      softmax_tile<D>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
+                      [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
       mbar_arrive(&sm->p_full[j & 1]);
     }
     // ------------------------------------------------------------ epilogue
@@ -289,8 +321,49 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
 //               then PV_t(j-1); stage released after the last PV that reads it
 //   warps 2-5   softmax + epilogue of Q tile 0;   warps 6-9   the same for Q tile 1
 // Epilogue: O / l straight from registers to global (rows are contiguous 2d-byte runs).
-constexpr int PAIR_THREADS = 320;
+constexpr int PAIR_THREADS = 352;  // + warp 10: Q-tile loader
 constexpr uint32_t PAIR_TMEM_COLS = 512;
+
+// Debug timeline (eva_debug_trace_prefill): CTA 0 records (clock64 << 24 | code) events in
+// per-role shared-memory logs (no atomics: role r appends to its own slice), copied to
+// global memory at exit.  code = kind << 20 | t << 16 | j.  kinds: 1 producer issued tile j,
+// 2 MMA issued S_t(j), 3 MMA issued PV_t(j), 4 softmax t got S(j), 5 softmax t released
+// P(j), 6 epilogue t done, 7 producer slot free for tile j, 8 MMA got k_full(j),
+// 9 MMA got p_full_t(j).
+__device__ unsigned long long* g_trace = nullptr;
+__device__ int g_trace_n = 0;
+__device__ int g_trace_cap = 0;
+constexpr int TRACE_ROLES = 4, TRACE_PER_ROLE = 384;
+struct TraceLog {
+  unsigned long long ev[TRACE_ROLES][TRACE_PER_ROLE];
+  int n[TRACE_ROLES];
+};
+template <bool TRACE>
+__device__ __forceinline__ void trace(TraceLog* log, int role, int kind, int t, int j) {
+  if constexpr (TRACE) {
+    if (blockIdx.x == 0) {
+      const int i = log->n[role];
+      if (i < TRACE_PER_ROLE)
+        log->ev[role][i] = ((unsigned long long)clock64() << 24) | ((unsigned)kind << 20) |
+                           ((unsigned)t << 16) | ((unsigned)j & 0xffff);
+      log->n[role] = i + 1;
+    }
+  }
+}
+template <bool TRACE>
+__device__ __forceinline__ void trace_flush(TraceLog* log) {
+  if constexpr (TRACE) {
+    if (blockIdx.x == 0 && g_trace) {
+      for (int r = 0; r < TRACE_ROLES; ++r) {
+        const int n = min(log->n[r], TRACE_PER_ROLE);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          const int k = r * TRACE_PER_ROLE + i;
+          if (k < g_trace_cap) g_trace[k] = log->ev[r][i];
+        }
+      }
+    }
+  }
+}
 
 template <int D, int NS>
 struct __align__(1024) SmemPair {
@@ -343,7 +416,7 @@ struct PairPlan {
   }
 };
 
-template <int D, int NS>
+template <int D, int NS, bool TRACE>
 __global__ void __launch_bounds__(PAIR_THREADS, 1)
 prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
@@ -352,8 +425,10 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
   extern __shared__ uint8_t smem_raw[];
   SmemPair<D, NS>* sm = reinterpret_cast<SmemPair<D, NS>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  TraceLog* tlog = reinterpret_cast<TraceLog*>(sm + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ppu = (T + 2 * BM - 1) / (2 * BM);
+  if (TRACE && threadIdx.x < TRACE_ROLES) tlog->n[threadIdx.x] = 0;
   const int n_items = BH * ppu;
 
   if (warp == 0 && lane == 0) {
@@ -386,30 +461,21 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
   const uint32_t tmem = sm->tmem_base;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t kv = 0;
-      int qcnt[2] = {0, 0};
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const int u = item / ppu;
-        const PairPlan plan(item % ppu, T, C, W, mode);
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (!plan.active(t)) continue;
-          if (qcnt[t] > 0) mbar_wait(&sm->q_empty[t], (qcnt[t] - 1) & 1);
-          mbar_arrive_expect_tx(&sm->q_full[t], BM * D * 2);
-          for (int kb = 0; kb < D / 64; ++kb)
-            tma_load_3d(sm->q[t] + kb * BM * 64, &mQ, &sm->q_full[t], kb * 64, plan.n0 + t * BM, u);
-          ++qcnt[t];
-        }
-        const int NT = plan.count();
-        for (int j = 0; j < NT; ++j, ++kv) {
-          const int s = kv % NS;
-          if (kv >= (uint32_t)NS) mbar_wait(&sm->kv_empty[s], ((kv / NS) - 1) & 1);
-          const bool summ = plan.summary(j);
-          const int row = plan.base(j);
-          const CUtensorMap* mk = summ ? &mKs : &mK;
-          const CUtensorMap* mv = summ ? &mVs : &mV;
+    // ------------------------------------------------------------ TMA producer (whole warp)
+    uint32_t kv = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int u = item / ppu;
+      const PairPlan plan(item % ppu, T, C, W, mode);
+      const int NT = plan.count();
+      for (int j = 0; j < NT; ++j, ++kv) {
+        const int s = kv % NS;
+        if (kv >= (uint32_t)NS) mbar_wait(&sm->kv_empty[s], ((kv / NS) - 1) & 1);
+        if (lane == 0) trace<TRACE>(tlog, 0, 7, 0, kv);
+        const bool summ = plan.summary(j);
+        const int row = plan.base(j);
+        const CUtensorMap* mk = summ ? &mKs : &mK;
+        const CUtensorMap* mv = summ ? &mVs : &mV;
+        if (elect_one()) {
           mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
           for (int kb = 0; kb < D / 64; ++kb)
             tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, row, u);
@@ -417,61 +483,95 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
           for (int kb = 0; kb < D / 64; ++kb)
             tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, row, u);
         }
+        __syncwarp();
+        if (lane == 0) trace<TRACE>(tlog, 0, 1, 0, kv);
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ Q-tile loader (whole warp)
+    // Separate from the K/V producer so the ring keeps streaming the next item's tiles
+    // while this warp waits for the current item's last S MMA to release a Q buffer.
+    int qcnt0 = 0, qcnt1 = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int u = item / ppu;
+      const PairPlan plan(item % ppu, T, C, W, mode);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (!plan.active(t)) continue;
+        int& qc = t ? qcnt1 : qcnt0;
+        if (qc > 0) mbar_wait(&sm->q_empty[t], (qc - 1) & 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&sm->q_full[t], BM * D * 2);
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_3d(sm->q[t] + kb * BM * 64, &mQ, &sm->q_full[t], kb * 64, plan.n0 + t * BM, u);
+        }
+        __syncwarp();
+        ++qc;
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
-      uint32_t kv = 0;
-      int cS[2] = {0, 0}, cP[2] = {0, 0}, icnt[2] = {0, 0};
-      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-        const PairPlan plan(item % ppu, T, C, W, mode);
-        const int NT = plan.count();
-        const int last[2] = {plan.last_need(0), plan.last_need(1)};
-        bool first_pv[2] = {true, true};
+    // ------------------------------------------------------------ MMA issuer (whole warp)
+    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
+    uint32_t kv = 0;
+    int cS0 = 0, cS1 = 0, cP0 = 0, cP1 = 0, icnt0 = 0, icnt1 = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const PairPlan plan(item % ppu, T, C, W, mode);
+      const int NT = plan.count();
+      const int last0 = plan.last_need(0), last1 = plan.last_need(1);
+      bool first0 = true, first1 = true;
+      if (plan.active(0)) mbar_wait(&sm->q_full[0], icnt0 & 1);
+      if (plan.active(1)) mbar_wait(&sm->q_full[1], icnt1 & 1);
+      auto issue_pv = [&](int jp, uint32_t kvp) {
+        const int sp = kvp % NS;
+        bool v_ready = false;
 #pragma unroll
-        for (int t = 0; t < 2; ++t)
-          if (plan.active(t)) mbar_wait(&sm->q_full[t], icnt[t] & 1);
-        auto issue_pv = [&](int jp, uint32_t kvp) {
-          const int sp = kvp % NS;
-          bool v_ready = false;
-#pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            if (!plan.need(t, jp)) continue;
-            mbar_wait(&sm->p_full[t][cP[t] & 1], (cP[t] >> 1) & 1);
-            if (first_pv[t] && icnt[t] > 0) mbar_wait(&sm->o_empty[t], (icnt[t] - 1) & 1);
-            if (!v_ready) {
-              mbar_wait(&sm->v_full[sp], (kvp / NS) & 1);
-              v_ready = true;
-            }
-            tc_fence_after();
-            const uint32_t v_addr = smem_u32(sm->v[sp]);
-            const uint32_t tb = tmem + (uint32_t)t * 256;
+        for (int t = 0; t < 2; ++t) {
+          if (!plan.need(t, jp)) continue;
+          int& cP = t ? cP1 : cP0;
+          bool& first = t ? first1 : first0;
+          const int icnt = t ? icnt1 : icnt0;
+          mbar_wait(&sm->p_full[t][cP & 1], (cP >> 1) & 1);
+          if (lane == 0) trace<TRACE>(tlog, 1, 9, t, kvp);
+          if (first && icnt > 0) mbar_wait(&sm->o_empty[t], (icnt - 1) & 1);
+          if (!v_ready) {
+            mbar_wait(&sm->v_full[sp], (kvp / NS) & 1);
+            v_ready = true;
+          }
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(sm->v[sp]);
+          const uint32_t tb = tmem + (uint32_t)t * 256;
+          if (elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < BN / 16; ++ks) {
               const uint64_t b = smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024);
-              mma_ts(tb + TM_O, tb + (uint32_t)(cP[t] & 1) * BN + ks * 8, b, idesc_o,
-                     (!first_pv[t] || ks > 0) ? 1u : 0u);
+              mma_ts(tb + TM_O, tb + (uint32_t)(cP & 1) * BN + ks * 8, b, idesc_o,
+                     (!first || ks > 0) ? 1u : 0u);
             }
             mma_commit(&sm->o_done[t]);
-            if (jp == last[t]) mma_commit(&sm->o_final[t]);
-            first_pv[t] = false;
-            ++cP[t];
+            if (jp == (t ? last1 : last0)) mma_commit(&sm->o_final[t]);
           }
-          mma_commit(&sm->kv_empty[sp]);
-        };
-        for (int j = 0; j < NT; ++j, ++kv) {
-          const int s = kv % NS;
-          mbar_wait(&sm->k_full[s], (kv / NS) & 1);
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(sm->k[s]);
+          __syncwarp();
+          if (lane == 0) trace<TRACE>(tlog, 1, 3, t, kvp);
+          first = false;
+          ++cP;
+        }
+        if (elect_one()) mma_commit(&sm->kv_empty[sp]);
+        __syncwarp();
+      };
+      for (int j = 0; j < NT; ++j, ++kv) {
+        const int s = kv % NS;
+        mbar_wait(&sm->k_full[s], (kv / NS) & 1);
+        if (lane == 0) trace<TRACE>(tlog, 1, 8, 0, kv);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sm->k[s]);
 #pragma unroll
-          for (int t = 0; t < 2; ++t) {
-            if (!plan.need(t, j)) continue;
-            const uint32_t q_addr = smem_u32(sm->q[t]);
-            const uint32_t d_tmem = tmem + (uint32_t)t * 256 + (uint32_t)(cS[t] & 1) * BN;
+        for (int t = 0; t < 2; ++t) {
+          if (!plan.need(t, j)) continue;
+          int& cS = t ? cS1 : cS0;
+          const uint32_t q_addr = smem_u32(sm->q[t]);
+          const uint32_t d_tmem = tmem + (uint32_t)t * 256 + (uint32_t)(cS & 1) * BN;
+          if (elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < D / 16; ++ks) {
               const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
@@ -479,17 +579,18 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
               const uint64_t b = smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024);
               mma_ss(d_tmem, a, b, idesc_s, ks > 0 ? 1u : 0u);
             }
-            mma_commit(&sm->s_full[t][cS[t] & 1]);
-            if (j == last[t]) mma_commit(&sm->q_empty[t]);
-            ++cS[t];
+            mma_commit(&sm->s_full[t][cS & 1]);
+            if (j == (t ? last1 : last0)) mma_commit(&sm->q_empty[t]);
           }
-          if (j > 0) issue_pv(j - 1, kv - 1);
+          __syncwarp();
+          if (lane == 0) trace<TRACE>(tlog, 1, 2, t, kv);
+          ++cS;
         }
-        if (NT > 0) issue_pv(NT - 1, kv - 1);
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-          if (plan.active(t)) ++icnt[t];
+        if (j > 0) issue_pv(j - 1, kv - 1);
       }
+      if (NT > 0) issue_pv(NT - 1, kv - 1);
+      if (plan.active(0)) ++icnt0;
+      if (plan.active(1)) ++icnt1;
     }
   } else {
     // ------------------------------------------------------------ softmax warpgroups
@@ -511,11 +612,8 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
         if (!plan.need(t, j)) continue;
         const int b = cS & 1;
         mbar_wait(&sm->s_full[t][b], (cS >> 1) & 1);
+        if (r == 0) trace<TRACE>(tlog, 2 + t, 4, t, cS);
         tc_fence_after();
-        uint32_t sr[64];
-        tmem_ld32(t_lane + (uint32_t)b * BN, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        tmem_ld32(t_lane + (uint32_t)b * BN + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        tmem_wait_ld();
         const int base = plan.base(j);
         int vlo, vhi;
         if (plan.summary(j)) {
@@ -526,43 +624,10 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
           vhi = min(BN, n - base + 1);
         }
         if (!valid) vhi = vlo;
-        float x[64];
-        float mx = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          x[c] = (c >= vlo && c < vhi) ? __uint_as_float(sr[c]) * scale_log2 : -INFINITY;
-          mx = fmaxf(mx, x[c]);
-        }
-        const bool grow = mx > m_ref + 8.0f;
-        if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
-          const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
-          mbar_wait(&sm->o_done[t], (cS - 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int cc = 0; cc < D / 32; ++cc) {
-            uint32_t o[32];
-            tmem_ld32(t_lane + TM_O + cc * 32, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-            tmem_st32(t_lane + TM_O + cc * 32, o);
-          }
-          tmem_wait_st();
-          l *= f;
-        }
-        if (grow) m_ref = mx;
-        const float mref = m_ref == -INFINITY ? 0.f : m_ref;
-        uint32_t pk[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float p0 = ex2(x[2 * c] - mref), p1 = ex2(x[2 * c + 1] - mref);
-          l += p0 + p1;
-          pk[c] = pack_bf16(p0, p1);
-        }
-        tmem_st32(t_lane + (uint32_t)b * BN, pk);
-        tmem_wait_st();
-        tc_fence_before();
+        softmax_tile<D>(t_lane + (uint32_t)b * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
+                        [&] { mbar_wait(&sm->o_done[t], (cS - 1) & 1); });
         mbar_arrive(&sm->p_full[t][b]);
+        if (r == 0) trace<TRACE>(tlog, 2 + t, 5, t, cS);
         ++cS;
       }
       // ---------------------------------------------------------- epilogue
@@ -588,11 +653,13 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
           dst[i] = make_uint4(ob[4 * i], ob[4 * i + 1], ob[4 * i + 2], ob[4 * i + 3]);
         if (lse) lse[(size_t)u * T + n] = (m_ref + __log2f(l)) * 0.69314718055994531f;
       }
+      if (r == 0) trace<TRACE>(tlog, 2 + t, 6, t, icnt);
       ++icnt;
     }
   }
   tc_fence_before();
   __syncthreads();
+  trace_flush<TRACE>(tlog);
   if (warp == 1) tmem_dealloc(tmem, PAIR_TMEM_COLS);
 }
 
@@ -658,7 +725,7 @@ cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const 
   return cudaGetLastError();
 }
 
-template <int D, int NS>
+template <int D, int NS, bool TRACE = false>
 cudaError_t launch_pair(const eva_config& cfg, const void* Q, const void* K, const void* V,
                         const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
   const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
@@ -672,10 +739,10 @@ cudaError_t launch_pair(const eva_config& cfg, const void* Q, const void* K, con
     mVs = mV;
   }
   if (!ok) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(SmemPair<D, NS>) + 1024;
+  const size_t smem = sizeof(SmemPair<D, NS>) + 1024 + (TRACE ? sizeof(TraceLog) : 0);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_pair_kernel<D, NS>,
+    cudaError_t e = cudaFuncSetAttribute(prefill_pair_kernel<D, NS, TRACE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -684,7 +751,7 @@ cudaError_t launch_pair(const eva_config& cfg, const void* Q, const void* K, con
   const int64_t items = (int64_t)BH * ppu;
   const int grid = (int)std::min<int64_t>(items, num_sms());  // 1 CTA/SM: all CTAs co-resident
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  prefill_pair_kernel<D, NS><<<grid, PAIR_THREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, BH, T, cfg.chunk,
+  prefill_pair_kernel<D, NS, TRACE><<<grid, PAIR_THREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, BH, T, cfg.chunk,
                                                               cfg.window, cfg.mode, scale_log2,
                                                               (__nv_bfloat16*)O, lse);
   note_launch();
@@ -692,6 +759,19 @@ cudaError_t launch_pair(const eva_config& cfg, const void* Q, const void* K, con
 }
 
 }  // namespace
+
+cudaError_t debug_trace_prefill(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                const void* Ksum, const void* Vsum, void* O, float* lse,
+                                unsigned long long* trace_dev, int cap, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(g_trace, &trace_dev, sizeof(trace_dev), 0, cudaMemcpyHostToDevice, s);
+  const int zero = 0;
+  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(g_trace_n, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(g_trace_cap, &cap, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  if (cfg.d_head == 128) return launch_pair<128, 4, true>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  if (cfg.d_head == 64) return launch_pair<64, 8, true>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  return cudaErrorNotSupported;
+}
 
 bool prefill_sm100_supported(const eva_config& cfg) {
   return cfg.dtype == EVA_BF16 && (cfg.d_head == 64 || cfg.d_head == 128) && encode_fn() != nullptr;
@@ -706,7 +786,7 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const voi
   if (variant == 1) pair = false;
   if (variant == 2) pair = true;
   if (pair) {
-    if (cfg.d_head == 128) return launch_pair<128, 4>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+    if (cfg.d_head == 128) return launch_pair<128, 5>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
     if (cfg.d_head == 64) return launch_pair<64, 8>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
   } else {
     if (cfg.d_head == 128) return launch_t<128, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);

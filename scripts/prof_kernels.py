@@ -28,7 +28,8 @@ if what in ("prefill_cfg3", "summarize_cfg3", "prefill_cfg2"):
         if what == "summarize_cfg3":
             eva.eva_summarize(cfg, K, V, Ksum=ks, Vsum=vs)
         else:
-            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse)
+            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse,
+                                 kernel=os.environ.get("EVA_PROF_KERNEL") or None)
 elif what == "decode_cfg4":
     BH, d, C, W, ctx = 256 * 32, 128, 64, 256, 32768
     cfg = eva.make_config(256, 32, 0, d, C, W)

@@ -10,7 +10,8 @@ import re
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "eva.h")
+HEADERS = [os.path.join(ROOT, "include", h) for h in sorted(os.listdir(os.path.join(ROOT, "include")))
+           if h.endswith(".h")]
 
 
 @pytest.fixture(scope="module")
@@ -20,7 +21,7 @@ def N():
 
 
 def _declared():
-    src = open(HEADER).read()
+    src = "\n".join(open(h).read() for h in HEADERS)
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(eva_[a-z_]+)\s*\(", src)))
 
@@ -111,7 +112,8 @@ def test_decode_workspace_bytes(N):
     assert N.lib.eva_decode_workspace_bytes(ctypes.byref(small)) == 0
     long = _cache(N, 4000, 600, bh_count=2)
     ws = N.lib.eva_decode_workspace_bytes(ctypes.byref(long))
-    assert ws > 0 and ws % (2 * (32 + 2) * 4) == 0
+    # (m, l, acc[d]) per (unit, split) + one merge counter per unit
+    assert ws > 0 and (ws - 2 * 4) % (2 * (32 + 2) * 4) == 0
 
 
 def test_product_package_does_not_import_oracle():

@@ -303,6 +303,55 @@ def test_prefill_handoff_then_decode(eva, dtype):
     assert (dec.float() - O_full[:, T0 - 1:].float()).abs().max().item() <= tol
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_cache_load_equals_append(eva, dtype):
+    """eva_cache_load with the prefill's summaries == eva_cache_append(n_new = T): same ring,
+    same summaries (bitwise), and the decode continues identically."""
+    BH, T, d, C, W = 3, 777, 64, 32, 96
+    cfg = eva.make_config(1, BH, T, d, C, W, dtype=dtype, seed=31)
+    Q, K, V = eva_inputs.qkv(0, BH, T, d, dtype, seed=32, device="cuda")
+    _, _, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=True)
+    a = eva.DecodeCache(cfg, T // C + 4, device="cuda")
+    b = eva.DecodeCache(cfg, T // C + 4, device="cuda")
+    a.eva_cache_append(K, V)
+    b.eva_cache_load(K, V, ks, vs)
+    assert a.pos == b.pos == T
+    assert torch.equal(a.ring_k, b.ring_k) and torch.equal(a.ring_v, b.ring_v)
+    nC = T // C
+    assert torch.equal(a.sum_k[:, :nC], b.sum_k[:, :nC]) and torch.equal(a.sum_v[:, :nC], b.sum_v[:, :nC])
+    q, k, v = eva_inputs.decode_tokens(0, BH, 80, d, dtype, seed=33, device="cuda")
+    for t in range(80):
+        a.eva_cache_append(k[t], v[t])
+        b.eva_cache_append(k[t], v[t])
+        oa, la = a.eva_attn_decode(q[t])
+        ob, lb = b.eva_attn_decode(q[t])
+        assert torch.equal(oa, ob) and torch.equal(la, lb)
+
+
+@pytest.mark.parametrize("BH,ctx", [(1, 5000), (2, 20000), (64, 3000)])
+def test_decode_split_k_parity(eva, BH, ctx):
+    """Long compressed contexts at small batch use split-K with the in-kernel last-CTA merge;
+    the cache (filled through eva_cache_load) decodes like the oracle row."""
+    d, C, W = 128, 64, 256
+    T = ctx
+    cfg = eva.make_config(1, BH, T, d, C, W, dtype=torch.bfloat16, seed=41)
+    Q, K, V = eva_inputs.qkv(0, BH, T, d, torch.bfloat16, seed=42, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    cache = eva.DecodeCache(cfg, T // C + 2, device="cuda")
+    cache.eva_cache_load(K[:, :T - 1].contiguous(), V[:, :T - 1].contiguous(), ks[:, :(T - 1) // C].contiguous(),
+                         vs[:, :(T - 1) // C].contiguous())
+    cache.eva_cache_append(K[:, T - 1].contiguous(), V[:, T - 1].contiguous())
+    assert cache.workspace_bytes() > 0 or BH * 8 >= 148 * 8
+    for rep in range(2):  # the merge counters must be left at zero
+        o, lse = cache.eva_attn_decode(Q[:, T - 1].contiguous())
+        for u in range(BH):
+            E = oracle.eps(cfg.seed, cfg.layer, u, T // C, d)
+            rk, rv = oracle.summarize(f64(K[u]), f64(V[u]), E, C)
+            _, rO, rl = oracle.prefill_rows(f64(Q[u]), f64(K[u]), f64(V[u]), rk, rv, [T - 1], C, W, 0, cfg.scale)
+            assert np.max(np.abs(f64(o[u]) - rO[0])) <= 2e-2
+            assert abs(float(lse[u]) - rl[0]) <= 2e-2
+
+
 def test_decode_poisoned_stale_ring_slots(eva):
     """Stale / invisible ring slots and unused summary rows are poisoned; output unchanged."""
     BH, d, C, W, T = 2, 64, 16, 64, 300
