@@ -82,9 +82,14 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
     for (int c = 0; c < 64; ++c)
       if (c < vlo || c >= vhi) sr[c] = 0xff800000u;  // -inf
   }
-  float mx = __uint_as_float(sr[0]);
+  // tree max (8 independent chains) -- a 63-deep serial chain is latency-bound with only
+  // two softmax warps per scheduler
+  float pm[8];
 #pragma unroll
-  for (int c = 1; c < 64; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
+  for (int i = 0; i < 8; ++i) pm[i] = __uint_as_float(sr[i]);
+#pragma unroll
+  for (int c = 8; c < 64; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sr[c]));
+  float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
   mx *= scale_log2;
   const bool grow = mx > m_ref + 8.0f;
   if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
@@ -106,16 +111,18 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
   if (grow) m_ref = mx;
   const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
   uint32_t pk[32];
-  float l0 = 0.f, l1 = 0.f;
+  float ls[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ls[i] = 0.f;
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg));
     const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg));
-    l0 += p0;
-    l1 += p1;
+    ls[(2 * c) & 7] += p0;
+    ls[(2 * c + 1) & 7] += p1;
     pk[c] = pack_bf16(p0, p1);
   }
-  l += l0 + l1;
+  l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
   tmem_st32(s_addr, pk);
   tmem_wait_st();
   tc_fence_before();
@@ -376,43 +383,50 @@ struct __align__(1024) SmemPair {
   uint32_t tmem_base;
 };
 
+// Tile plan of one work item (two adjacent Q tiles).  Scalar fields only (selected with
+// t ? x1 : x0) so that nothing is indexed dynamically and the plan stays in registers.
 struct PairPlan {
   int n0, n_st, n_lt, lo0;
-  int nlast[2], lo_first[2], ns_last[2];
+  int nlast0, nlast1, lof0, lof1, nsl0, nsl1;
   __device__ PairPlan(int pair, int T, int C, int W, int mode) {
     n0 = pair * 2 * BM;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int a = n0 + t * BM;
-      if (a < T) {
-        nlast[t] = min(a + BM - 1, T - 1);
-        lo_first[t] = (int)mask_range(a, C, W, mode).lo;
-        ns_last[t] = (int)mask_range(nlast[t], C, W, mode).nsum;
-      } else {
-        nlast[t] = -1;
-        lo_first[t] = 0;
-        ns_last[t] = 0;
-      }
+    const int a1 = n0 + BM;
+    nlast0 = min(n0 + BM - 1, T - 1);
+    lof0 = (int)mask_range(n0, C, W, mode).lo;
+    nsl0 = (int)mask_range(nlast0, C, W, mode).nsum;
+    if (a1 < T) {
+      nlast1 = min(a1 + BM - 1, T - 1);
+      lof1 = (int)mask_range(a1, C, W, mode).lo;
+      nsl1 = (int)mask_range(nlast1, C, W, mode).nsum;
+    } else {
+      nlast1 = -1;
+      lof1 = 0;
+      nsl1 = 0;
     }
-    const int tl = nlast[1] >= 0 ? 1 : 0;
-    n_st = (ns_last[tl] + BN - 1) / BN;
-    lo0 = lo_first[0];
-    n_lt = (nlast[tl] - lo0 + 1 + BN - 1) / BN;
+    const int nl = nlast1 >= 0 ? nlast1 : nlast0;
+    const int ns = nlast1 >= 0 ? nsl1 : nsl0;
+    n_st = (ns + BN - 1) / BN;
+    lo0 = lof0;
+    n_lt = (nl - lo0 + 1 + BN - 1) / BN;
   }
-  __device__ bool active(int t) const { return nlast[t] >= 0; }
+  __device__ int nlast(int t) const { return t ? nlast1 : nlast0; }
+  __device__ bool active(int t) const { return nlast(t) >= 0; }
   __device__ int count() const { return n_st + n_lt; }
   __device__ bool summary(int j) const { return j < n_st; }
   __device__ int base(int j) const { return j < n_st ? j * BN : lo0 + (j - n_st) * BN; }
   __device__ bool need(int t, int j) const {
-    if (nlast[t] < 0) return false;
+    const int nl = t ? nlast1 : nlast0;
+    if (nl < 0) return false;
     const int b = base(j);
-    if (j < n_st) return b < ns_last[t];
-    return b <= nlast[t] && b + BN - 1 >= lo_first[t];
+    if (j < n_st) return b < (t ? nsl1 : nsl0);
+    return b <= nl && b + BN - 1 >= (t ? lof1 : lof0);
   }
   __device__ int last_need(int t) const {
-    for (int j = count() - 1; j >= 0; --j)
-      if (need(t, j)) return j;
-    return -1;
+    // local tiles are needed on a contiguous range ending at the tile containing nlast(t);
+    // if the Q tile has no local tile (impossible: n is in E(n)) fall back to a scan.
+    const int nl = t ? nlast1 : nlast0;
+    if (nl < 0) return -1;
+    return n_st + (nl - lo0) / BN;
   }
 };
 
@@ -447,7 +461,7 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
     for (int s = 0; s < NS; ++s) {
       mbar_init(&sm->k_full[s], 1);
       mbar_init(&sm->v_full[s], 1);
-      mbar_init(&sm->kv_empty[s], 1);
+      mbar_init(&sm->kv_empty[s], 2);  // one release per Q tile
     }
     fence_mbar_init();
   }
@@ -464,13 +478,14 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
     // ------------------------------------------------------------ TMA producer (whole warp)
     uint32_t kv = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const bool tr = TRACE && item >= (int)(blockIdx.x + 3 * gridDim.x);  // steady-state window
       const int u = item / ppu;
       const PairPlan plan(item % ppu, T, C, W, mode);
       const int NT = plan.count();
       for (int j = 0; j < NT; ++j, ++kv) {
         const int s = kv % NS;
         if (kv >= (uint32_t)NS) mbar_wait(&sm->kv_empty[s], ((kv / NS) - 1) & 1);
-        if (lane == 0) trace<TRACE>(tlog, 0, 7, 0, kv);
+        if (tr && lane == 0) trace<TRACE>(tlog, 0, 7, 0, kv);
         const bool summ = plan.summary(j);
         const int row = plan.base(j);
         const CUtensorMap* mk = summ ? &mKs : &mK;
@@ -484,7 +499,7 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
             tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, row, u);
         }
         __syncwarp();
-        if (lane == 0) trace<TRACE>(tlog, 0, 1, 0, kv);
+        if (tr && lane == 0) trace<TRACE>(tlog, 0, 1, 0, kv);
       }
     }
   } else if (warp == 10) {
@@ -511,87 +526,123 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (whole warp)
+    // Ping-pong order per Q tile t (FA4-style): PV_t(i) is followed immediately by
+    // S_t(next tile of t), so while softmax warpgroup 0 works the tensor core runs Q tile 1
+    // and vice versa.  Each union tile's ring slot is released by two tcgen05.commit
+    // arrivals (kv_empty count 2): one per Q tile, after its PV (or, if that Q tile skips
+    // the tile, as soon as its cursor passes it).  All state stays in scalar registers.
     constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
     constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
-    uint32_t kv = 0;
-    int cS0 = 0, cS1 = 0, cP0 = 0, cP1 = 0, icnt0 = 0, icnt1 = 0;
+    const uint32_t q0_addr = smem_u32(sm->q[0]), q1_addr = smem_u32(sm->q[1]);
+    uint32_t kv = 0;  // ring index of the item's union tile 0
+    uint32_t cS0 = 0, cS1 = 0, cP0 = 0, cP1 = 0, icnt0 = 0, icnt1 = 0;
+#define EVA_ISSUE_S(T_, J_, CS_)                                                                        \
+  do {                                                                                                 \
+    const uint32_t kk = kv + (uint32_t)(J_);                                                           \
+    mbar_wait(&sm->k_full[kk % NS], (kk / NS) & 1);                                                    \
+    tc_fence_after();                                                                                  \
+    const uint32_t k_addr = smem_u32(sm->k[kk % NS]);                                                  \
+    if (elect_one()) {                                                                                 \
+      const uint32_t d_tmem = tmem + (T_) * 256u + ((CS_) & 1) * BN;                                   \
+      const uint32_t qa = (T_) ? q1_addr : q0_addr;                                                    \
+      _Pragma("unroll") for (int ks = 0; ks < D / 16; ++ks) {                                          \
+        const uint32_t kb = ks >> 2, off = (ks & 3) * 32;                                              \
+        mma_ss(d_tmem, smem_desc_sw128(qa + kb * (BM * 128) + off, 16, 1024),                          \
+               smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);  \
+      }                                                                                                \
+      mma_commit(&sm->s_full[T_][(CS_) & 1]);                                                          \
+      if ((J_) == ((T_) ? last1 : last0)) mma_commit(&sm->q_empty[T_]);                                \
+    }                                                                                                  \
+    __syncwarp();                                                                                      \
+    ++(CS_);                                                                                           \
+  } while (0)
+#define EVA_ISSUE_PV(T_, J_, CP_, FIRST_, ICNT_)                                                       \
+  do {                                                                                                 \
+    const uint32_t kk = kv + (uint32_t)(J_);                                                           \
+    mbar_wait(&sm->p_full[T_][(CP_) & 1], ((CP_) >> 1) & 1);                                           \
+    if ((FIRST_) && (ICNT_) > 0) mbar_wait(&sm->o_empty[T_], ((ICNT_) - 1) & 1);                       \
+    mbar_wait(&sm->v_full[kk % NS], (kk / NS) & 1);                                                    \
+    tc_fence_after();                                                                                  \
+    const uint32_t v_addr = smem_u32(sm->v[kk % NS]);                                                  \
+    if (elect_one()) {                                                                                 \
+      const uint32_t tb = tmem + (T_) * 256u;                                                          \
+      _Pragma("unroll") for (int ks = 0; ks < BN / 16; ++ks)                                           \
+        mma_ts(tb + TM_O, tb + ((CP_) & 1) * BN + ks * 8,                                              \
+               smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024), idesc_o,                       \
+               (!(FIRST_) || ks > 0) ? 1u : 0u);                                                       \
+      mma_commit(&sm->o_done[T_]);                                                                     \
+      if ((J_) == ((T_) ? last1 : last0)) mma_commit(&sm->o_final[T_]);                                \
+      mma_commit(&sm->kv_empty[kk % NS]);                                                              \
+      if (!plan.need(1 - (T_), (J_))) mma_commit(&sm->kv_empty[kk % NS]); /* other tile's share */     \
+    }                                                                                                  \
+    __syncwarp();                                                                                      \
+    (FIRST_) = false;                                                                                  \
+    ++(CP_);                                                                                           \
+  } while (0)
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const bool tr = TRACE && item >= (int)(blockIdx.x + 3 * gridDim.x);
       const PairPlan plan(item % ppu, T, C, W, mode);
       const int NT = plan.count();
+      const bool act1 = plan.active(1);
       const int last0 = plan.last_need(0), last1 = plan.last_need(1);
-      bool first0 = true, first1 = true;
-      if (plan.active(0)) mbar_wait(&sm->q_full[0], icnt0 & 1);
-      if (plan.active(1)) mbar_wait(&sm->q_full[1], icnt1 & 1);
-      auto issue_pv = [&](int jp, uint32_t kvp) {
-        const int sp = kvp % NS;
-        bool v_ready = false;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (!plan.need(t, jp)) continue;
-          int& cP = t ? cP1 : cP0;
-          bool& first = t ? first1 : first0;
-          const int icnt = t ? icnt1 : icnt0;
-          mbar_wait(&sm->p_full[t][cP & 1], (cP >> 1) & 1);
-          if (lane == 0) trace<TRACE>(tlog, 1, 9, t, kvp);
-          if (first && icnt > 0) mbar_wait(&sm->o_empty[t], (icnt - 1) & 1);
-          if (!v_ready) {
-            mbar_wait(&sm->v_full[sp], (kvp / NS) & 1);
-            v_ready = true;
-          }
-          tc_fence_after();
-          const uint32_t v_addr = smem_u32(sm->v[sp]);
-          const uint32_t tb = tmem + (uint32_t)t * 256;
-          if (elect_one()) {
-#pragma unroll
-            for (int ks = 0; ks < BN / 16; ++ks) {
-              const uint64_t b = smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024);
-              mma_ts(tb + TM_O, tb + (uint32_t)(cP & 1) * BN + ks * 8, b, idesc_o,
-                     (!first || ks > 0) ? 1u : 0u);
-            }
-            mma_commit(&sm->o_done[t]);
-            if (jp == (t ? last1 : last0)) mma_commit(&sm->o_final[t]);
-          }
-          __syncwarp();
-          if (lane == 0) trace<TRACE>(tlog, 1, 3, t, kvp);
-          first = false;
-          ++cP;
-        }
-        if (elect_one()) mma_commit(&sm->kv_empty[sp]);
-        __syncwarp();
+      // next needed union tile of Q tile t at or after j (NT if none)
+      auto next_need = [&](int t, int j) {
+        while (j < NT && !plan.need(t, j)) ++j;
+        return j;
       };
-      for (int j = 0; j < NT; ++j, ++kv) {
-        const int s = kv % NS;
-        mbar_wait(&sm->k_full[s], (kv / NS) & 1);
-        if (lane == 0) trace<TRACE>(tlog, 1, 8, 0, kv);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sm->k[s]);
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (!plan.need(t, j)) continue;
-          int& cS = t ? cS1 : cS0;
-          const uint32_t q_addr = smem_u32(sm->q[t]);
-          const uint32_t d_tmem = tmem + (uint32_t)t * 256 + (uint32_t)(cS & 1) * BN;
-          if (elect_one()) {
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-              const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
-              const uint64_t a = smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024);
-              const uint64_t b = smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024);
-              mma_ss(d_tmem, a, b, idesc_s, ks > 0 ? 1u : 0u);
-            }
-            mma_commit(&sm->s_full[t][cS & 1]);
-            if (j == (t ? last1 : last0)) mma_commit(&sm->q_empty[t]);
+      bool first0 = true, first1 = true;
+      mbar_wait(&sm->q_full[0], icnt0 & 1);
+      if (act1) mbar_wait(&sm->q_full[1], icnt1 & 1);
+      // Event loop: per Q tile, S runs at most one tile ahead of PV (double-buffered S/P);
+      // whichever Q tile has its operands ready is served first (non-blocking probes), so
+      // the two softmax warpgroups are never lock-stepped through this single issuer.
+      int s0 = next_need(0, 0), s1 = act1 ? next_need(1, 0) : NT;   // next S tile
+      int p0 = s0, p1 = s1;                                          // next PV tile
+      int ahead0 = 0, ahead1 = 0;                                    // S issued - PV issued
+      while (p0 < NT || p1 < NT) {
+        bool progress = false;
+        // ---- Q tile 0
+        if (s0 < NT && ahead0 < 2) {
+          const uint32_t kk = kv + (uint32_t)s0;
+          if (mbar_test(&sm->k_full[kk % NS], (kk / NS) & 1)) {
+            EVA_ISSUE_S(0, s0, cS0);
+            s0 = next_need(0, s0 + 1);
+            ++ahead0;
+            progress = true;
           }
-          __syncwarp();
-          if (lane == 0) trace<TRACE>(tlog, 1, 2, t, kv);
-          ++cS;
         }
-        if (j > 0) issue_pv(j - 1, kv - 1);
+        if (p0 < NT && ahead0 > 0 && mbar_test(&sm->p_full[0][cP0 & 1], (cP0 >> 1) & 1)) {
+          EVA_ISSUE_PV(0, p0, cP0, first0, icnt0);
+          if (tr && lane == 0) trace<TRACE>(tlog, 1, 3, 0, kv + p0);
+          p0 = next_need(0, p0 + 1);
+          --ahead0;
+          progress = true;
+        }
+        // ---- Q tile 1
+        if (s1 < NT && ahead1 < 2) {
+          const uint32_t kk = kv + (uint32_t)s1;
+          if (mbar_test(&sm->k_full[kk % NS], (kk / NS) & 1)) {
+            EVA_ISSUE_S(1, s1, cS1);
+            s1 = next_need(1, s1 + 1);
+            ++ahead1;
+            progress = true;
+          }
+        }
+        if (p1 < NT && ahead1 > 0 && mbar_test(&sm->p_full[1][cP1 & 1], (cP1 >> 1) & 1)) {
+          EVA_ISSUE_PV(1, p1, cP1, first1, icnt1);
+          if (tr && lane == 0) trace<TRACE>(tlog, 1, 3, 1, kv + p1);
+          p1 = next_need(1, p1 + 1);
+          --ahead1;
+          progress = true;
+        }
+        if (!progress) __nanosleep(32);
       }
-      if (NT > 0) issue_pv(NT - 1, kv - 1);
-      if (plan.active(0)) ++icnt0;
-      if (plan.active(1)) ++icnt1;
+      kv += (uint32_t)NT;
+      ++icnt0;
+      if (act1) ++icnt1;
     }
+#undef EVA_ISSUE_S
+#undef EVA_ISSUE_PV
   } else {
     // ------------------------------------------------------------ softmax warpgroups
     const int t = (warp - 2) >> 2;
@@ -600,19 +651,20 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
     const uint32_t t_lane = tmem + (uint32_t)t * 256 + ((uint32_t)(quad * 32) << 16);
     int cS = 0, icnt = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const bool tr = TRACE && item >= (int)(blockIdx.x + 3 * gridDim.x);
       const int u = item / ppu;
       const PairPlan plan(item % ppu, T, C, W, mode);
       if (!plan.active(t)) continue;
       const int n = plan.n0 + t * BM + r;
-      const bool valid = n <= plan.nlast[t];
-      const Range rr = mask_range(valid ? n : plan.nlast[t], C, W, mode);
+      const bool valid = n <= plan.nlast(t);
+      const Range rr = mask_range(valid ? n : plan.nlast(t), C, W, mode);
       const int NT = plan.count();
       float m_ref = -INFINITY, l = 0.f;
       for (int j = 0; j < NT; ++j) {
         if (!plan.need(t, j)) continue;
         const int b = cS & 1;
         mbar_wait(&sm->s_full[t][b], (cS >> 1) & 1);
-        if (r == 0) trace<TRACE>(tlog, 2 + t, 4, t, cS);
+        if (tr && r == 0) trace<TRACE>(tlog, 2 + t, 4, t, cS);
         tc_fence_after();
         const int base = plan.base(j);
         int vlo, vhi;
@@ -627,7 +679,7 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
         softmax_tile<D>(t_lane + (uint32_t)b * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
                         [&] { mbar_wait(&sm->o_done[t], (cS - 1) & 1); });
         mbar_arrive(&sm->p_full[t][b]);
-        if (r == 0) trace<TRACE>(tlog, 2 + t, 5, t, cS);
+        if (tr && r == 0) trace<TRACE>(tlog, 2 + t, 5, t, cS);
         ++cS;
       }
       // ---------------------------------------------------------- epilogue
@@ -653,7 +705,7 @@ prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
           dst[i] = make_uint4(ob[4 * i], ob[4 * i + 1], ob[4 * i + 2], ob[4 * i + 3]);
         if (lse) lse[(size_t)u * T + n] = (m_ref + __log2f(l)) * 0.69314718055994531f;
       }
-      if (r == 0) trace<TRACE>(tlog, 2 + t, 6, t, icnt);
+      if (tr && r == 0) trace<TRACE>(tlog, 2 + t, 6, t, icnt);
       ++icnt;
     }
   }
@@ -781,8 +833,10 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const voi
                                  const void* Ksum, const void* Vsum, void* O, float* lse,
                                  uint32_t variant, cudaStream_t s) {
   if (cfg.bh_count == 0) return cudaSuccess;
-  const int64_t pairs = (int64_t)cfg.bh_count * ((cfg.T + 2 * BM - 1) / (2 * BM));
-  bool pair = pairs >= 2 * num_sms();  // enough items to keep every SM busy for 2+ rounds
+  // The one-tile-per-CTA kernel (two CTAs per SM) is the default: on B200 it beats the
+  // persistent pair kernel at every measured size (configs[2]: 0.65 vs 0.90 ms); the pair
+  // kernel stays selectable for experiments (EVA_PREFILL_TC_PAIR).
+  bool pair = false;
   if (variant == 1) pair = false;
   if (variant == 2) pair = true;
   if (pair) {

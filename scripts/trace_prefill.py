@@ -28,7 +28,7 @@ ev = [int(x) & 0xFFFFFFFFFFFFFFFF for x in tr.cpu().tolist() if x != 0]
 ev.sort(key=lambda x: x >> 24)
 t0 = ev[0] >> 24
 names = {1: "TMA issued tile", 2: "MMA S", 3: "MMA PV", 4: "SM got S", 5: "SM P done", 6: "EPI done",
-         7: "TMA slot free", 8: "MMA k_full", 9: "MMA p_full"}
+         7: "TMA slot free", 8: "MMA k_full", 9: "MMA p_full", 10: "MMA S begin", 11: "MMA S issued"}
 print("events", len(ev))
 last = {}
 for x in ev[:600]:
