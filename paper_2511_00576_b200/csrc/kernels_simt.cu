@@ -56,6 +56,165 @@ __global__ void __launch_bounds__(SUMM_THREADS) summarize_cta_kernel(eva_config 
                             Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D, smem);
 }
 
+// Register-resident variant (the default when C <= 32 * 128 * 16 / (D * sizeof(T))):
+// one CTA (4 warps) per chunk; a row is read by TPR = D*sizeof(T)/16 lanes with one 16-byte
+// load each, a warp covers RPW = 32/TPR rows per load and warp w owns the row slots
+// w*RPW + 4*RPW*i.  Every K and V piece of the chunk is loaded up front (up to 2*NI
+// 16-byte loads in flight per lane) and kept in registers: column sums -> k~ (smem merge
+// of the 4 warps), Eq.15 -> omega, per-row log-xi logits (group shuffles), per-warp
+// online softmax of the rows -> partial (m, l, acc), merged across warps in smem.
+template <typename T, int D, int NI, typename RowK, typename RowV>
+__device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV& rowV, int C,
+                                                    const float* eps_c, uint32_t bh_global,
+                                                    uint32_t chunk, const eva_config& cfg,
+                                                    T* ksum_out, T* vsum_out) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int TPR = D / VEC;
+  constexpr int RPW = 32 / TPR;
+  __shared__ float sh_sum[4][D];
+  __shared__ float sh_om[D];
+  __shared__ float sh_m[4], sh_l[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / TPR, gl = lane % TPR, ch0 = gl * VEC;
+  uint4 kx[NI], vx[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    if (r < C) {
+      kx[i] = ldg16_stream(rowK(r) + ch0);
+      vx[i] = ldg16_stream(rowV(r) + ch0);
+    }
+  }
+  // column sums
+  float cs[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) cs[j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    if (r < C) {
+      float k[VEC];
+      unpack16<T>(kx[i], k);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) cs[j] += k[j];
+    }
+  }
+#pragma unroll
+  for (int o = TPR; o < 32; o <<= 1)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], o);
+  if (grp == 0) {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) sh_sum[warp][ch0 + j] = cs[j];
+  }
+  __syncthreads();
+  // k~ and omega (Eq.15); one Philox block per 4 channels
+  if (threadIdx.x < D / 4) {
+    const int q = threadIdx.x;
+    float e[4];
+    if (eps_c) {
+      const float* ep = eps_c + 4 * q;
+      e[0] = ep[0]; e[1] = ep[1]; e[2] = ep[2]; e[3] = ep[3];
+    } else {
+      const float4 z = philox_normal4(cfg.seed, cfg.layer, bh_global, chunk, (uint32_t)q);
+      e[0] = z.x; e[1] = z.y; e[2] = z.z; e[3] = z.w;
+    }
+    T* ko = ksum_out + 4 * q;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int ch = 4 * q + j;
+      const float kt = (sh_sum[0][ch] + sh_sum[1][ch] + sh_sum[2][ch] + sh_sum[3][ch]) * (1.0f / (float)C);
+      sh_om[ch] = omega_of(kt, e[j], cfg);
+      ko[j] = Elem<T>::from_f(kt);
+    }
+  }
+  __syncthreads();
+  float om[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) om[j] = sh_om[ch0 + j];
+  // logits a_r = omega . k_r - |k_r|^2 / 2 and the warp's online softmax over its rows
+  float a[NI];
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    float part = 0.f;
+    if (r < C) {
+      float k[VEC];
+      unpack16<T>(kx[i], k);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) part += k[j] * (om[j] - 0.5f * k[j]);
+    }
+    part = group_sum<TPR>(part);
+    a[i] = r < C ? part : -INFINITY;
+    m = fmaxf(m, a[i]);
+  }
+#pragma unroll
+  for (int o = TPR; o < 32; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  float l = 0.f, acc[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    if (r < C) {
+      const float p = __expf(a[i] - m);
+      l += p;
+      float v[VEC];
+      unpack16<T>(vx[i], v);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc[j] += p * v[j];
+    }
+  }
+#pragma unroll
+  for (int o = TPR; o < 32; o <<= 1) {
+    l += __shfl_xor_sync(0xffffffffu, l, o);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+  }
+  if (lane == 0) { sh_m[warp] = m; sh_l[warp] = l; }
+  __syncthreads();  // sh_sum is free again: reuse it for the partial accumulators
+  if (grp == 0) {
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) sh_sum[warp][ch0 + j] = acc[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const int ch = threadIdx.x;
+    float M = fmaxf(fmaxf(sh_m[0], sh_m[1]), fmaxf(sh_m[2], sh_m[3]));
+    float L = 0.f, o = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float f = sh_m[w] == -INFINITY ? 0.f : __expf(sh_m[w] - M);
+      L += f * sh_l[w];
+      o += f * sh_sum[w][ch];
+    }
+    vsum_out[ch] = Elem<T>::from_f(o / L);
+  }
+}
+
+
+template <typename T, int D, int NI>
+__global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, const T* __restrict__ K,
+                                                           const T* __restrict__ V,
+                                                           const float* __restrict__ eps,
+                                                           T* __restrict__ Ksum, T* __restrict__ Vsum) {
+  const int C = cfg.chunk, nC = cfg.T / C;
+  const int c = blockIdx.x, u = blockIdx.y;
+  const T* Kc = K + ((size_t)u * cfg.T + (size_t)c * C) * D;
+  const T* Vc = V + ((size_t)u * cfg.T + (size_t)c * C) * D;
+  summarize_chunk_reg<T, D, NI>([&](int r) { return Kc + (size_t)r * D; }, [&](int r) { return Vc + (size_t)r * D; },
+                                C, eps ? eps + ((size_t)u * nC + c) * D : nullptr,
+                                (uint32_t)(cfg.bh_begin + u), (uint32_t)c, cfg,
+                                Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D);
+}
+
+// Rows per lane slot of the register summariser for (C, D, T); > 8 means "too large".
+template <typename T, int D>
+constexpr int summ_reg_ni(int C) {
+  return (C + 4 * (32 / (D * (int)sizeof(T) / 16)) - 1) / (4 * (32 / (D * (int)sizeof(T) / 16)));
+}
+
 // ============================================================================ SIMT prefill
 // One CTA = one unit x QT queries.  G threads cooperate on one query (thread gi
 // owns channels gi, gi+G, ... -> conflict-free smem reads); key/value tiles of
@@ -146,7 +305,7 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, const
 //   blockIdx.x >= n_copy : CTA summarises (unit, chunk) = divmod(x - n_copy, n_chunks)
 //                          (if do_sum)
 // Rows of a chunk come from K_new (positions >= pos) or the ring (positions < pos).
-template <typename T, int D, bool CTA_SUMM>
+template <typename T, int D, int SUMM>  // SUMM: 0 warp, 1 staged CTA, 2/4/8 register NI
 __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __restrict__ Kn,
                                                      const T* __restrict__ Vn,
                                                      const float* __restrict__ eps, int n_new,
@@ -176,6 +335,7 @@ __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __res
   }
   if (!do_sum) return;
   const int x = (int)blockIdx.x - n_copy;
+  constexpr bool CTA_SUMM = SUMM != 0;
   const int per = CTA_SUMM ? n_chunks : (n_chunks + 3) / 4;
   const int u = x / per;
   const int ci = CTA_SUMM ? x % per : (x % per) * 4 + (int)(threadIdx.x >> 5);
@@ -197,7 +357,10 @@ __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __res
   const float* e = eps ? eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr;
   T* sk = static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D;
   T* sv = static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D;
-  if constexpr (CTA_SUMM)
+  if constexpr (SUMM >= 2)
+    summarize_chunk_reg<T, D, (SUMM >= 2 ? SUMM : 2)>(rowK, rowV, C, e, (uint32_t)(c.cfg.bh_begin + u),
+                                                       (uint32_t)chunk, c.cfg, sk, sv);
+  else if constexpr (SUMM == 1)
     summarize_chunk_cta<T, D>(rowK, rowV, C, e, (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk,
                               c.cfg, sk, sv, smem);
   else
@@ -503,7 +666,16 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
   cudaError_t err = cudaSuccess;
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
     const size_t sm = summ_smem_bytes(cfg.chunk, D, sizeof(T));
-    if (sm <= kSummSmemMax) {
+    const int ni = summ_reg_ni<T, D>(cfg.chunk);  // row slots per lane
+    if (ni <= 8) {
+      const dim3 grid(nC, cfg.bh_count);
+      if (ni <= 2)
+        summarize_reg_kernel<T, D, 2><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+      else if (ni <= 4)
+        summarize_reg_kernel<T, D, 4><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+      else
+        summarize_reg_kernel<T, D, 8><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+    } else if (sm <= kSummSmemMax) {
       err = set_smem_attr((const void*)summarize_cta_kernel<T, D>, sm);
       if (err != cudaSuccess) return err;
       summarize_cta_kernel<T, D><<<dim3(nC, cfg.bh_count), SUMM_THREADS, sm, s>>>(
@@ -545,11 +717,13 @@ cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* 
   cudaError_t err = cudaSuccess;
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     const size_t sm = summ_smem_bytes(C, D, sizeof(T));
-    const bool cta = sm <= kSummSmemMax;
-    auto fn = cta ? append_kernel<T, D, true> : append_kernel<T, D, false>;
-    const size_t smem = cta ? sm : 0;
-    if (cta) {
-      err = set_smem_attr((const void*)append_kernel<T, D, true>, sm);
+    const int ni = summ_reg_ni<T, D>(C);
+    const bool cta = ni <= 8 || sm <= kSummSmemMax;
+    auto fn = ni <= 2 ? append_kernel<T, D, 2> : ni <= 4 ? append_kernel<T, D, 4> : ni <= 8 ? append_kernel<T, D, 8>
+            : sm <= kSummSmemMax ? append_kernel<T, D, 1> : append_kernel<T, D, 0>;
+    const size_t smem = (ni > 8 && sm <= kSummSmemMax) ? sm : 0;
+    if (smem) {
+      err = set_smem_attr((const void*)append_kernel<T, D, 1>, sm);
       if (err != cudaSuccess) return err;
     }
     constexpr int VEC = 16 / sizeof(T);

@@ -32,32 +32,43 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
 
+// Stage the chunk's C key rows and C value rows into kv_smem ([C][D] K then [C][D] V)
+// with cp.async; the caller commits / waits the group.
 template <typename T, int D, typename RowK, typename RowV>
-__device__ __forceinline__ void summarize_chunk_cta(const RowK& rowK, const RowV& rowV, int C,
-                                                    const float* eps_c, uint32_t bh_global,
-                                                    uint32_t chunk, const eva_config& cfg,
-                                                    T* ksum_out, T* vsum_out, uint8_t* smem) {
+__device__ __forceinline__ void summarize_stage(const RowK& rowK, const RowV& rowV, int C, T* kv_smem) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int TPR = D / VEC;
+  T* Ks = kv_smem;
+  T* Vs = Ks + (size_t)C * D;
+  for (int i = threadIdx.x; i < C * TPR; i += SUMM_THREADS) {
+    const int r = i / TPR, p = i % TPR;
+    cp_async16(Ks + (size_t)r * D + p * VEC, rowK(r) + p * VEC);
+    cp_async16(Vs + (size_t)r * D + p * VEC, rowV(r) + p * VEC);
+  }
+}
+
+// Compute (k~, beta^) of a staged chunk.  work: scratch of summ_work_bytes(C, D) bytes.
+__host__ __device__ constexpr size_t summ_work_bytes(int C, int D) {
+  return (size_t)C * 4 + (size_t)D * 4 + (size_t)SUMM_THREADS * 16 * 4 + 64;
+}
+template <typename T, int D>
+__device__ __forceinline__ void summarize_compute(const T* kv_smem, int C, const float* eps_c,
+                                                  uint32_t bh_global, uint32_t chunk,
+                                                  const eva_config& cfg, T* ksum_out, T* vsum_out,
+                                                  uint8_t* work) {
   constexpr int VEC = 16 / sizeof(T);          // elements per 16-byte piece
   constexpr int TPR = D / VEC;                 // pieces (threads) per row
   constexpr int G = SUMM_THREADS / TPR;        // row groups
   static_assert(TPR >= 1 && TPR <= 32 && SUMM_THREADS % TPR == 0, "bad D");
-  T* Ks = reinterpret_cast<T*>(smem);
-  T* Vs = Ks + (size_t)C * D;
-  float* a = reinterpret_cast<float*>(Vs + (size_t)C * D);
+  const T* Ks = kv_smem;
+  const T* Vs = Ks + (size_t)C * D;
+  float* a = reinterpret_cast<float*>(work);
   float* om = a + C;
   float* part = om + D;  // [G][D]
   float* stat = part + G * D;
   const int tid = threadIdx.x;
   const int pc = tid % TPR, g = tid / TPR;
   const int ch0 = pc * VEC;
-
-  for (int i = tid; i < C * TPR; i += SUMM_THREADS) {
-    const int r = i / TPR, p = i % TPR;
-    cp_async16(Ks + (size_t)r * D + p * VEC, rowK(r) + p * VEC);
-    cp_async16(Vs + (size_t)r * D + p * VEC, rowV(r) + p * VEC);
-  }
-  cp_async_wait_all();
-  __syncthreads();
 
   // k~: column mean
   {
@@ -143,6 +154,19 @@ __device__ __forceinline__ void summarize_chunk_cta(const RowK& rowK, const RowV
     for (int gg = 0; gg < G; ++gg) s += part[gg * D + tid];
     vsum_out[tid] = Elem<T>::from_f(s * stat[0]);
   }
+}
+
+template <typename T, int D, typename RowK, typename RowV>
+__device__ __forceinline__ void summarize_chunk_cta(const RowK& rowK, const RowV& rowV, int C,
+                                                    const float* eps_c, uint32_t bh_global,
+                                                    uint32_t chunk, const eva_config& cfg,
+                                                    T* ksum_out, T* vsum_out, uint8_t* smem) {
+  T* kv = reinterpret_cast<T*>(smem);
+  summarize_stage<T, D>(rowK, rowV, C, kv);
+  cp_async_wait_all();
+  __syncthreads();
+  summarize_compute<T, D>(kv, C, eps_c, bh_global, chunk, cfg, ksum_out, vsum_out,
+                          smem + (size_t)2 * C * D * sizeof(T));
 }
 
 }  // namespace eva
