@@ -5,7 +5,7 @@ timeout 1200 python -m pytest tests -q -m gpu --timeout 300 -x 2>&1 | tail -5
 python bench.py --steps 50 --warmup 5 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu-baseline --quick > /dev/null 2>&1
-for k in prefill_cfg3:prefill decode_cfg4:decode_kernel summarize_cfg3:summarize prefill_cfg2:prefill; do
+for k in prefill_cfg3:prefill_sm100_kernel decode_cfg4:decode_kernel summarize_cfg3:summarize prefill_cfg2:prefill_sm100_kernel; do
   w=${k%%:*}; pat=${k##*:}
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$pat -s 1 -c 1 -o gpurun_out/prof_${w}_${TAG} -f \
       python scripts/prof_kernels.py $w 2 > gpurun_out/ncu_${w}.log 2>&1
