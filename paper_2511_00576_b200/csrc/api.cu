@@ -130,7 +130,8 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
                             uint32_t flags, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
-  if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT | EVA_PREFILL_TC_TILE | EVA_PREFILL_TC_PAIR))
+  if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT | EVA_PREFILL_TC_TILE | EVA_PREFILL_TC_PAIR |
+                EVA_PREFILL_TC_WIDE))
     return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
   if (cfg->bh_count == 0) return ok();
   const void* p[] = {Q, K, V, O};
@@ -151,7 +152,8 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   }
   const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) &&
                   eva::prefill_sm100_supported(*cfg);
-  const uint32_t variant = (flags & EVA_PREFILL_TC_TILE) ? 1u : (flags & EVA_PREFILL_TC_PAIR) ? 2u : 0u;
+  const uint32_t variant = (flags & EVA_PREFILL_TC_TILE) ? 1u : (flags & EVA_PREFILL_TC_PAIR) ? 2u
+                          : (flags & EVA_PREFILL_TC_WIDE) ? 3u : 0u;
   cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, Q, K, V, Ksum, Vsum, O, lse, variant, s)
                      : eva::launch_prefill_simt(*cfg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cuda_status(e, tc ? "eva_attn_prefill(sm100)" : "eva_attn_prefill(simt)");
@@ -285,6 +287,9 @@ eva_status eva_debug_trace_prefill(const eva_config* cfg, const void* Q, const v
   if (cfg->dtype != EVA_BF16 || (cfg->d_head != 64 && cfg->d_head != 128))
     return fail(EVA_ERR_UNSUPPORTED, "trace needs bf16, d in {64,128}");
   if (!trace || cap < 1) return fail(EVA_ERR_INVALID_ARG, "trace buffer");
+  if (cap < 0x10000)  // small buffers: the tile kernel's 4-CTA timeline (4 x 3 x 48 entries)
+    return cuda_status(eva::debug_trace_tile(*cfg, Q, K, V, Ksum, Vsum, O, lse, trace, (cudaStream_t)stream),
+                       "eva_debug_trace_prefill(tile)");
   return cuda_status(eva::debug_trace_prefill(*cfg, Q, K, V, Ksum, Vsum, O, lse, trace, cap,
                                               (cudaStream_t)stream),
                      "eva_debug_trace_prefill");

@@ -31,6 +31,10 @@ cudaError_t debug_trace_prefill(const eva_config& cfg, const void* Q, const void
                                 const void* Ksum, const void* Vsum, void* O, float* lse,
                                 unsigned long long* trace_dev, int cap, cudaStream_t s);
 
+cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                             const void* Ksum, const void* Vsum, void* O, float* lse,
+                             unsigned long long* trace_dev, cudaStream_t s);
+
 // Cache append: summaries of chunks completed in [pos, pos+n_new), ring write of the
 // last min(n_new, W) tokens.
 cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* Vn, int n_new,

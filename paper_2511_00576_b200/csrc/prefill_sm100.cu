@@ -45,7 +45,9 @@ struct __align__(1024) Smem {
   __nv_bfloat16 k[NSTAGE][BN * D];       // D/64 sub-tiles [64][64], 8 KB each
   __nv_bfloat16 v[NSTAGE][BN * D];
   uint64_t q_full;
-  uint64_t k_full[NSTAGE], v_full[NSTAGE], kv_empty[NSTAGE];
+  // K and V slots are released separately: a K slot as soon as its S MMA completed, a V
+  // slot after its PV MMA, so the next K tiles stream in one softmax period earlier.
+  uint64_t k_full[NSTAGE], v_full[NSTAGE], k_empty[NSTAGE], v_empty[NSTAGE];
   uint64_t s_full[2], p_full[2], o_done, o_final;
   uint32_t tmem_base;
 };
@@ -143,7 +145,35 @@ struct TilePlan {
   __device__ int base(int j) const { return j < n_st ? j * BN : lo0 + (j - n_st) * BN; }
 };
 
-template <int D, int NSTAGE>
+
+// Debug timeline of the tile kernel (eva_debug_trace_prefill with variant 1): CTAs with
+// linear id in {0, 1, 150, 151} log (globaltimer-free) clock64 events per role in shared
+// memory and flush them to g_trace2 at exit.  Roles: 0 producer, 1 MMA, 2 softmax (warp 2
+// lane 0).  kinds: 1 start, 2 Q arrived (MMA), 3 k_full(j) (MMA), 4 S(j) issued, 5 P(j)
+// received (MMA), 6 PV(j) issued, 7 softmax got S(j), 8 softmax P(j) done, 9 o_final
+// (epilogue start), 10 epilogue done, 11 producer slot free (j), 12 producer issued (j).
+__device__ unsigned long long* g_trace2 = nullptr;
+constexpr int TT_ROLES = 3, TT_PER_ROLE = 48, TT_SLOTS = 4;
+struct TileTrace {
+  unsigned long long ev[TT_ROLES][TT_PER_ROLE];
+  int n[TT_ROLES];
+};
+__device__ __forceinline__ int tt_slot() {
+  const int id = blockIdx.y * gridDim.x + blockIdx.x;
+  return id == 0 ? 0 : id == 1 ? 1 : id == 150 ? 2 : id == 151 ? 3 : -1;
+}
+template <bool TRACE>
+__device__ __forceinline__ void tt(TileTrace* tl, int role, int kind, int j) {
+  if constexpr (TRACE) {
+    if (tt_slot() >= 0) {
+      const int i = tl->n[role];
+      if (i < TT_PER_ROLE) tl->ev[role][i] = ((unsigned long long)clock64() << 24) | ((unsigned)kind << 16) | (unsigned)(j & 0xffff);
+      tl->n[role] = i + 1;
+    }
+  }
+}
+
+template <int D, int NSTAGE, bool TRACE = false>
 __global__ void __launch_bounds__(NTHREADS, 2)
 prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
@@ -156,6 +186,9 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   const int u = blockIdx.y;
   const TilePlan plan(blockIdx.x, T, C, W, mode);
   const int NT = plan.count();
+  __shared__ TileTrace tlog_s;
+  TileTrace* tl = &tlog_s;
+  if (TRACE && threadIdx.x < TT_ROLES) tl->n[threadIdx.x] = 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
@@ -164,7 +197,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&sm->k_full[s], 1);
       mbar_init(&sm->v_full[s], 1);
-      mbar_init(&sm->kv_empty[s], 1);
+      mbar_init(&sm->k_empty[s], 1);
+      mbar_init(&sm->v_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm->s_full[b], 1);
@@ -182,6 +216,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
+  if (threadIdx.x == 0) tt<TRACE>(tl, 0, 1, 0);
 
   // Producer and MMA roles run on whole warps (warp-uniform control flow keeps every
   // descriptor and coordinate in uniform registers); one elected lane issues.
@@ -191,24 +226,48 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
       for (int kb = 0; kb < D / 64; ++kb)
         tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
+      // The ring holds only NSTAGE tiles; pull every later K/V tile of this CTA into L2 now
+      // so its TMA load later on is an L2 hit instead of a full DRAM round trip.
+      for (int j = NSTAGE; j < NT; ++j) {
+        const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
+        const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
+        for (int kb = 0; kb < D / 64; ++kb) {
+          tma_prefetch_l2_3d(mk, kb * 64, plan.base(j), u);
+          tma_prefetch_l2_3d(mv, kb * 64, plan.base(j), u);
+        }
+      }
     }
     __syncwarp();
-    for (int j = 0; j < NT; ++j) {
+    // Issue order K(0), K(1), V(0), K(2), V(1), ...: K(j+1) waits only for S(j+1-NSTAGE)
+    // to finish reading its slot, V(j) for PV(j-NSTAGE).
+    auto load_k = [&](int j) {
       const int s = j % NSTAGE;
-      if (j >= NSTAGE) mbar_wait(&sm->kv_empty[s], ((j / NSTAGE) - 1) & 1);
-      const bool summ = plan.summary(j);
-      const int row = plan.base(j);
-      const CUtensorMap* mk = summ ? &mKs : &mK;
-      const CUtensorMap* mv = summ ? &mVs : &mV;
+      if (j >= NSTAGE) mbar_wait(&sm->k_empty[s], ((j / NSTAGE) - 1) & 1);
+      if (lane == 0) tt<TRACE>(tl, 0, 11, j);
+      const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
       if (elect_one()) {
         mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
         for (int kb = 0; kb < D / 64; ++kb)
-          tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, row, u);
-        mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
-        for (int kb = 0; kb < D / 64; ++kb)
-          tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, row, u);
+          tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, plan.base(j), u);
       }
       __syncwarp();
+      if (lane == 0) tt<TRACE>(tl, 0, 12, j);
+    };
+    auto load_v = [&](int j) {
+      const int s = j % NSTAGE;
+      if (j >= NSTAGE) mbar_wait(&sm->v_empty[s], ((j / NSTAGE) - 1) & 1);
+      const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb)
+          tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, plan.base(j), u);
+      }
+      __syncwarp();
+    };
+    load_k(0);
+    for (int j = 0; j < NT; ++j) {
+      if (j + 1 < NT) load_k(j + 1);
+      load_v(j);
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -216,10 +275,12 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
     const uint32_t q_addr = smem_u32(sm->q);
     mbar_wait(&sm->q_full, 0);
+    if (lane == 0) tt<TRACE>(tl, 1, 2, 0);
     for (int j = 0; j <= NT; ++j) {
       if (j < NT) {
         const int s = j % NSTAGE;
         mbar_wait(&sm->k_full[s], (j / NSTAGE) & 1);
+        if (lane == 0) tt<TRACE>(tl, 1, 3, j);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sm->k[s]);
         const uint32_t d_tmem = tmem + (uint32_t)(j & 1) * BN;
@@ -232,12 +293,15 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
             mma_ss(d_tmem, a, b, idesc_s, ks > 0 ? 1u : 0u);
           }
           mma_commit(&sm->s_full[j & 1]);
+          mma_commit(&sm->k_empty[s]);
         }
         __syncwarp();
+        if (lane == 0) tt<TRACE>(tl, 1, 4, j);
       }
       if (j >= 1) {
         const int jj = j - 1, s = jj % NSTAGE;
         mbar_wait(&sm->p_full[jj & 1], (jj >> 1) & 1);
+        if (lane == 0) tt<TRACE>(tl, 1, 5, jj);
         mbar_wait(&sm->v_full[s], (jj / NSTAGE) & 1);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sm->v[s]);
@@ -248,11 +312,12 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
             const uint64_t b = smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024);
             mma_ts(tmem + TM_O, a_tmem, b, idesc_o, (jj > 0 || ks > 0) ? 1u : 0u);
           }
-          mma_commit(&sm->kv_empty[s]);
+          mma_commit(&sm->v_empty[s]);
           mma_commit(&sm->o_done);
           if (jj == NT - 1) mma_commit(&sm->o_final);
         }
         __syncwarp();
+        if (lane == 0) tt<TRACE>(tl, 1, 6, jj);
       }
     }
   } else {
@@ -264,8 +329,10 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     const Range rr = mask_range(valid ? n : plan.nlast, C, W, mode);
     const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
     float m_ref = -INFINITY, l = 0.f;
+    const bool tw = warp == 2 && lane == 0;
     for (int j = 0; j < NT; ++j) {
       mbar_wait(&sm->s_full[j & 1], (j >> 1) & 1);
+      if (tw) tt<TRACE>(tl, 2, 7, j);
       tc_fence_after();
       const int base = plan.base(j);
       int vlo, vhi;
@@ -280,8 +347,300 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       softmax_tile<D>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
                       [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
       mbar_arrive(&sm->p_full[j & 1]);
+      if (tw) tt<TRACE>(tl, 2, 8, j);
     }
     // ------------------------------------------------------------ epilogue
+    mbar_wait(&sm->o_final, 0);
+    if (tw) tt<TRACE>(tl, 2, 9, 0);
+    tc_fence_after();
+    const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+    uint8_t* qs = reinterpret_cast<uint8_t*>(sm->q);
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(t_lane + TM_O + cc * 32, o);
+      tmem_wait_ld();
+      const int kb = (cc * 32) / 64, c16_0 = ((cc * 32) % 64) / 8;
+      uint8_t* rowp = qs + kb * (BM * 128) + r * 128;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(o[8 * g + 0]) * inv_l, __uint_as_float(o[8 * g + 1]) * inv_l);
+        w.y = pack_bf16(__uint_as_float(o[8 * g + 2]) * inv_l, __uint_as_float(o[8 * g + 3]) * inv_l);
+        w.z = pack_bf16(__uint_as_float(o[8 * g + 4]) * inv_l, __uint_as_float(o[8 * g + 5]) * inv_l);
+        w.w = pack_bf16(__uint_as_float(o[8 * g + 6]) * inv_l, __uint_as_float(o[8 * g + 7]) * inv_l);
+        *reinterpret_cast<uint4*>(rowp + (((c16_0 + g) ^ (r & 7)) * 16)) = w;
+      }
+    }
+    if (valid && lse) lse[(size_t)u * T + n] = (m_ref + __log2f(l)) * 0.69314718055994531f;
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (warp == 2 && lane == 0) {
+      for (int kb = 0; kb < D / 64; ++kb) tma_store_3d(&mO, sm->q + kb * BM * 64, kb * 64, plan.n0, u);
+      tma_store_commit();
+      tma_store_wait_all();
+      tt<TRACE>(tl, 2, 10, 0);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (TRACE) {
+    const int slot = tt_slot();
+    if (slot >= 0 && g_trace2) {
+      for (int i = threadIdx.x; i < TT_ROLES * TT_PER_ROLE; i += blockDim.x) {
+        const int r = i / TT_PER_ROLE, k = i % TT_PER_ROLE;
+        g_trace2[(size_t)slot * TT_ROLES * TT_PER_ROLE + i] = k < tl->n[r] ? tl->ev[r][k] : 0ull;
+      }
+    }
+  }
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// ========================================================================== wide-tile kernel
+// One 128-query tile per CTA (two CTAs per SM) walking 128-key tiles: the S MMA is
+// M=128 x N=128 (full tensor rate; N=64 SS MMAs are shared-memory bound at 48 instead of
+// 32 cycles per K-step).  TMEM (256 columns): S/P [0,128) single-buffered, O [128,128+d).
+// Per tile the MMA warp issues PV(j-1) then S(j), so when softmax sees S(j) complete,
+// PV(j-1) has completed too and O may be rescaled without another barrier.  K and V have
+// separate slot rings (NSK, NSV) released by the S and the PV MMA respectively.
+constexpr int BNW = 128;
+
+struct WidePlan {
+  int n0, nlast, n_st, n_lt, lo0;
+  __device__ WidePlan(int qt, int T, int C, int W, int mode) {
+    n0 = qt * BM;
+    nlast = min(n0 + BM - 1, T - 1);
+    const Range rf = mask_range(n0, C, W, mode), rl = mask_range(nlast, C, W, mode);
+    n_st = (int)((rl.nsum + BNW - 1) / BNW);
+    lo0 = (int)rf.lo;
+    n_lt = (nlast - lo0 + 1 + BNW - 1) / BNW;
+  }
+  __device__ int count() const { return n_st + n_lt; }
+  __device__ bool summary(int j) const { return j < n_st; }
+  __device__ int base(int j) const { return j < n_st ? j * BNW : lo0 + (j - n_st) * BNW; }
+};
+
+template <int D, int NSK, int NSV>
+struct __align__(1024) SmemWide {
+  __nv_bfloat16 q[BM * D];           // D/64 sub-tiles [128][64]
+  __nv_bfloat16 k[NSK][BNW * D];     // D/64 sub-tiles [128][64]
+  __nv_bfloat16 v[NSV][BNW * D];
+  uint64_t q_full, k_full[NSK], k_empty[NSK], v_full[NSV], v_empty[NSV];
+  uint64_t s_full, p_full, o_final;
+  uint32_t tmem_base;
+};
+
+// Softmax step on a 128-column S tile (see softmax_tile): pass 1 loads all 128 columns and
+// finds the row max, pass 2 writes P (bf16 pairs) in place and stores it to TMEM [0,64).
+// The previous PV has completed whenever this runs (issue order), so no wait is needed
+// before rescaling O.
+template <int D>
+__device__ __forceinline__ void softmax_tile128(uint32_t s_addr, uint32_t o_addr, int vlo, int vhi,
+                                                float scale_log2, float& m_ref, float& l) {
+  // pass 1: row max over the 128 columns, 32 at a time (keeps register use low)
+  const bool full = __all_sync(0xffffffffu, vlo <= 0 && vhi >= 128);
+  float pm[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) pm[i] = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t sr[32];
+    tmem_ld32(s_addr + 32 * q, sr);
+    tmem_wait_ld();
+    if (!full) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (32 * q + c < vlo || 32 * q + c >= vhi) sr[c] = 0xff800000u;
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sr[c]));
+  }
+  float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+  mx *= scale_log2;
+  const bool grow = mx > m_ref + 8.0f;
+  if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+    const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(o_addr + cc * 32, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+      tmem_st32(o_addr + cc * 32, o);
+    }
+    tmem_wait_st();
+    l *= f;
+  }
+  if (grow) m_ref = mx;
+  const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
+  // pass 2: P = exp2(s*scale - m) as bf16 pairs; chunk q (S columns 32q..32q+31) lands in
+  // P columns 16q..16q+15, which only overwrite S columns already consumed
+  float ls[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ls[i] = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t sr[32];
+    tmem_ld32(s_addr + 32 * q, sr);
+    tmem_wait_ld();
+    if (!full) {
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (32 * q + c < vlo || 32 * q + c >= vhi) sr[c] = 0xff800000u;
+    }
+    uint32_t pk[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg));
+      const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg));
+      ls[(2 * c) & 7] += p0;
+      ls[(2 * c + 1) & 7] += p1;
+      pk[c] = pack_bf16(p0, p1);
+    }
+    tmem_st16(s_addr + 16 * q, pk);
+  }
+  l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+  tmem_wait_st();
+  tc_fence_before();
+}
+
+template <int D, int NSK, int NSV>
+__global__ void __launch_bounds__(NTHREADS, 2)
+prefill_wide_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                    const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
+                    const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
+                    int T, int C, int W, int mode, float scale_log2, float* __restrict__ lse) {
+  extern __shared__ uint8_t smem_raw[];
+  SmemWide<D, NSK, NSV>* sm = reinterpret_cast<SmemWide<D, NSK, NSV>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.y;
+  const WidePlan plan(blockIdx.x, T, C, W, mode);
+  const int NT = plan.count();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
+    tma_prefetch(&mKs); tma_prefetch(&mVs); tma_prefetch(&mO);
+    mbar_init(&sm->q_full, 1);
+    for (int s = 0; s < NSK; ++s) { mbar_init(&sm->k_full[s], 1); mbar_init(&sm->k_empty[s], 1); }
+    for (int s = 0; s < NSV; ++s) { mbar_init(&sm->v_full[s], 1); mbar_init(&sm->v_empty[s], 1); }
+    mbar_init(&sm->s_full, 1);
+    mbar_init(&sm->p_full, 128);
+    mbar_init(&sm->o_final, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm->tmem_base, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
+      for (int kb = 0; kb < D / 64; ++kb)
+        tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
+      for (int j = 1; j < NT; ++j) {  // later tiles: warm L2 (the rings hold only NSK/NSV)
+        const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
+        const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
+        for (int kb = 0; kb < D / 64; ++kb) {
+          tma_prefetch_l2_3d(mk, kb * 64, plan.base(j), u);
+          tma_prefetch_l2_3d(mv, kb * 64, plan.base(j), u);
+        }
+      }
+    }
+    __syncwarp();
+    auto load = [&](bool is_k, int j) {
+      const int s = is_k ? j % NSK : j % NSV;
+      const int ns = is_k ? NSK : NSV;
+      uint64_t* empty = is_k ? &sm->k_empty[s] : &sm->v_empty[s];
+      uint64_t* full = is_k ? &sm->k_full[s] : &sm->v_full[s];
+      __nv_bfloat16* dst = is_k ? sm->k[s] : sm->v[s];
+      if (j >= ns) mbar_wait(empty, ((j / ns) - 1) & 1);
+      const CUtensorMap* m = plan.summary(j) ? (is_k ? &mKs : &mVs) : (is_k ? &mK : &mV);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(full, BNW * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb) tma_load_3d(dst + kb * BNW * 64, m, full, kb * 64, plan.base(j), u);
+      }
+      __syncwarp();
+    };
+    // K(j) is consumed by S(j), V(j) by PV(j) one softmax later: K runs one tile ahead.
+    load(true, 0);
+    for (int j = 0; j < NT; ++j) {
+      load(false, j);
+      if (j + 1 < NT) load(true, j + 1);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BNW, false);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
+    const uint32_t q_addr = smem_u32(sm->q);
+    mbar_wait(&sm->q_full, 0);
+    for (int j = 0; j <= NT; ++j) {
+      if (j >= 1) {  // PV(j-1)
+        const int jj = j - 1, s = jj % NSV;
+        mbar_wait(&sm->p_full, jj & 1);
+        mbar_wait(&sm->v_full[s], (jj / NSV) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sm->v[s]);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < BNW / 16; ++ks)
+            mma_ts(tmem + TM_O, tmem + ks * 8, smem_desc_sw128(v_addr + ks * 16 * 128, BNW * 128, 1024),
+                   idesc_o, (jj > 0 || ks > 0) ? 1u : 0u);
+          mma_commit(&sm->v_empty[s]);
+          if (jj == NT - 1) mma_commit(&sm->o_final);
+        }
+        __syncwarp();
+      }
+      if (j < NT) {  // S(j)
+        const int s = j % NSK;
+        mbar_wait(&sm->k_full[s], (j / NSK) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sm->k[s]);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+            mma_ss(tmem, smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024),
+                   smem_desc_sw128(k_addr + kb * (BNW * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm->s_full);
+          mma_commit(&sm->k_empty[s]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax warps + epilogue
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int n = plan.n0 + r;
+    const bool valid = n < T;
+    const Range rr = mask_range(valid ? n : plan.nlast, C, W, mode);
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < NT; ++j) {
+      mbar_wait(&sm->s_full, j & 1);
+      tc_fence_after();
+      const int base = plan.base(j);
+      int vlo, vhi;
+      if (plan.summary(j)) {
+        vlo = 0;
+        vhi = (int)min((int64_t)BNW, rr.nsum - base);
+      } else {
+        vlo = (int)max((int64_t)0, rr.lo - base);
+        vhi = min(BNW, n - base + 1);
+      }
+      if (!valid) vhi = vlo;
+      softmax_tile128<D>(t_lane, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l);
+      mbar_arrive(&sm->p_full);
+    }
     mbar_wait(&sm->o_final, 0);
     tc_fence_after();
     const float inv_l = l > 0.f ? 1.0f / l : 0.f;
@@ -747,7 +1106,7 @@ bool make_map(CUtensorMap* m, const void* base, int units, int rows, int D, int 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, int NSTAGE>
+template <int D, int NSTAGE, bool TRACE = false>
 cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const void* V,
                      const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
   const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
@@ -764,14 +1123,44 @@ cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const 
   const size_t smem = sizeof(Smem<D, NSTAGE>) + 1024;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_sm100_kernel<D, NSTAGE>,
+    cudaError_t e = cudaFuncSetAttribute(prefill_sm100_kernel<D, NSTAGE, TRACE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid((T + BM - 1) / BM, BH);
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  prefill_sm100_kernel<D, NSTAGE><<<grid, NTHREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, mO, T, cfg.chunk,
+  prefill_sm100_kernel<D, NSTAGE, TRACE><<<grid, NTHREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, mO, T, cfg.chunk,
+                                                               cfg.window, cfg.mode, scale_log2, lse);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int D, int NSK, int NSV>
+cudaError_t launch_wide(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                        const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
+  const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
+  CUtensorMap mQ, mK, mV, mKs, mVs, mO;
+  bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BNW) &&
+            make_map(&mV, V, BH, T, D, BNW) && make_map(&mO, O, BH, T, D, BM);
+  if (nC > 0) {
+    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BNW) && make_map(&mVs, Vsum, BH, nC, D, BNW);
+  } else {
+    mKs = mK;
+    mVs = mV;
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(SmemWide<D, NSK, NSV>) + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_wide_kernel<D, NSK, NSV>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((T + BM - 1) / BM, BH);
+  const float scale_log2 = cfg.scale * 1.4426950408889634f;
+  prefill_wide_kernel<D, NSK, NSV><<<grid, NTHREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, mO, T, cfg.chunk,
                                                                cfg.window, cfg.mode, scale_log2, lse);
   note_launch();
   return cudaGetLastError();
@@ -825,6 +1214,16 @@ cudaError_t debug_trace_prefill(const eva_config& cfg, const void* Q, const void
   return cudaErrorNotSupported;
 }
 
+cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                             const void* Ksum, const void* Vsum, void* O, float* lse,
+                             unsigned long long* trace_dev, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(g_trace2, &trace_dev, sizeof(trace_dev), 0, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  if (cfg.d_head == 128) return launch_t<128, 2, true>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  if (cfg.d_head == 64) return launch_t<64, 3, true>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  return cudaErrorNotSupported;
+}
+
 bool prefill_sm100_supported(const eva_config& cfg) {
   return cfg.dtype == EVA_BF16 && (cfg.d_head == 64 || cfg.d_head == 128) && encode_fn() != nullptr;
 }
@@ -839,6 +1238,10 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const voi
   bool pair = false;
   if (variant == 1) pair = false;
   if (variant == 2) pair = true;
+  if (variant == 3) {
+    if (cfg.d_head == 128) return launch_wide<128, 1, 1>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+    if (cfg.d_head == 64) return launch_wide<64, 2, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  }
   if (pair) {
     if (cfg.d_head == 128) return launch_pair<128, 5>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
     if (cfg.d_head == 64) return launch_pair<64, 8>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);

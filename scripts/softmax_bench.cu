@@ -1,0 +1,84 @@
+// softmax_bench.cu -- cycles per softmax_tile() call (the prefill's per-tile softmax step),
+// 4 warps (one per TMEM lane quadrant), 1 or 2 CTAs per SM.  Dev tool.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../paper_2511_00576_b200/csrc/prefill_sm100.cu"
+namespace eva { void note_launch(int) {} int num_sms() { return 148; } }
+
+namespace eva { namespace {
+// MMA load: warp 4 issues PV-shaped TS MMAs (M128 N128 K16, A = TMEM cols [64,96), B = smem,
+// accumulate into TMEM cols [128,256)) back to back while the softmax warps run.
+template <int D, int MMA>
+__global__ void __launch_bounds__(160, 2) sm_bench(int iters, int full, unsigned long long* out, float* sink) {
+  __shared__ uint32_t tbase;
+  __shared__ __align__(1024) uint8_t bsm[16384];
+  __shared__ volatile int stop;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) { stop = 0; mbar_init(&bar, 1); fence_mbar_init(); }
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) reinterpret_cast<uint32_t*>(bsm)[i] = 0x3c003c00u;
+  fence_proxy_async_smem();
+  if (warp == 0) { tmem_alloc(&tbase, 256); tmem_relinquish(); }
+  tc_fence_before(); __syncthreads(); tc_fence_after();
+  if (warp == 4) {
+    if (MMA) {
+      const uint32_t idesc = idesc_bf16_f32(128, 128, true);
+      while (!stop) {
+        if (elect_one()) {
+          for (int ks = 0; ks < 4; ++ks)
+            mma_ts(tbase + 128, tbase + 64 + ks * 8, smem_desc_sw128(smem_u32(bsm) + ks * 2048, 8192, 1024), idesc, 1);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(&bar);
+      __syncwarp();
+      mbar_wait(&bar, 0);
+    }
+    tc_fence_before(); __syncthreads();
+    if (warp == 0) tmem_dealloc(tbase, 256);
+    return;
+  }
+  const uint32_t t_lane = tbase + ((uint32_t)(warp * 32) << 16);
+  // fill S with small values
+  uint32_t init[32];
+  for (int i = 0; i < 32; ++i) init[i] = __float_as_uint(0.01f * ((i * 7 + lane) % 13));
+  tmem_st32(t_lane, init); tmem_st32(t_lane + 32, init); tmem_wait_st();
+  float m = -INFINITY, l = 0.f;
+  __syncwarp();
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    const int vlo = full ? 0 : (lane & 7), vhi = full ? 64 : 60;
+    softmax_tile<D>(t_lane, t_lane + 128, vlo, vhi, 0.18f, m, l, [] {});
+    // restore S (softmax overwrote the first 32 columns with P)
+    tmem_st32(t_lane, init); tmem_wait_st();
+  }
+  unsigned long long t1 = clock64();
+  if (lane == 0) out[blockIdx.x * 4 + warp] = t1 - t0;
+  if (l == 12345.f) sink[0] = m;
+  __syncwarp();
+  asm volatile("bar.sync 1, 128;");
+  if (threadIdx.x == 0) stop = 1;
+  tc_fence_before(); __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+}}
+
+int main() {
+  unsigned long long* d; float* sink;
+  cudaMalloc(&d, 296 * 4 * 8); cudaMalloc(&sink, 4);
+  for (int mma = 0; mma < 2; ++mma)
+  for (int full = 1; full >= 0; --full)
+    for (int grid : {148, 296}) {
+      const int iters = 2000;
+      if (mma) eva::sm_bench<128, 1><<<grid, 160>>>(iters, full, d, sink);
+      else eva::sm_bench<128, 0><<<grid, 160>>>(iters, full, d, sink);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
+      unsigned long long h[296 * 4];
+      cudaMemcpy(h, d, grid * 4 * 8, cudaMemcpyDeviceToHost);
+      double s = 0; for (int i = 0; i < grid * 4; ++i) s += h[i];
+      printf("softmax_tile (%s tile) %d CTA/SM%s: %.0f cycles per call (incl. a 32-col TMEM restore)\n",
+             full ? "unmasked" : "masked", grid / 148, mma ? " + PV MMA stream" : "", s / (grid * 4) / iters);
+    }
+  return 0;
+}

@@ -1,0 +1,29 @@
+"""Time the tensor-core prefill variants at configs[2]'s per-GPU shape (dev tool)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import eva_inputs
+import paper_2511_00576_b200 as eva
+shapes = [(8, 32, 8192, 128, 64, 256), (1, 16, 2048, 64, 64, 128)]
+for (B, H, T, d, C, W) in shapes:
+    cfg = eva.make_config(B, H, T, d, C, W)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    O = torch.empty_like(Q)
+    flush = torch.empty(512 << 18, device="cuda")
+    for kern in sys.argv[1:] or ["tile", "pair"]:
+        for _ in range(3):
+            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, kernel=kern)
+        ts = []
+        for _ in range(10):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, kernel=kern)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ts.sort()
+        nC = T // C
+        gb = B * H * (4 * T * d * 2 + 2 * nC * d * 2 + 4 * T) / 1e9
+        print(f"T={T} d={d} {kern}: median {ts[5]*1e3:.1f} us  min {ts[0]*1e3:.1f} us  -> {gb / (ts[5] / 1e3):.0f} GB/s")

@@ -1,0 +1,36 @@
+"""Timeline of 4 CTAs of the one-tile-per-CTA prefill kernel (dev tool).
+    python scripts/trace_tile.py B H T d C W"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import eva_inputs
+import paper_2511_00576_b200 as eva
+from paper_2511_00576_b200 import _native as N
+
+B, H, T, d, C, W = (int(x) for x in sys.argv[1:7]) if len(sys.argv) > 6 else (1, 16, 2048, 64, 64, 128)
+cfg = eva.make_config(B, H, T, d, C, W)
+Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device="cuda")
+ks, vs = eva.eva_summarize(cfg, K, V)
+O = torch.empty_like(Q)
+lse = torch.empty(B * H, T, device="cuda")
+tr = torch.zeros(4 * 3 * 48, dtype=torch.int64, device="cuda")
+P = lambda t: ctypes.c_void_p(t.data_ptr())
+st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+flush = torch.empty(512 << 18, device="cuda")
+for _ in range(3):
+    flush.zero_()
+    N.check(N.lib.eva_debug_trace_prefill(ctypes.byref(cfg), P(Q), P(K), P(V), P(ks), P(vs), P(O), P(lse), P(tr), 1000, st))
+torch.cuda.synchronize()
+names = {1: "start", 2: "MMA: Q arrived", 3: "MMA: K(j) arrived", 4: "MMA: S(j) issued", 5: "MMA: P(j) seen",
+         6: "MMA: PV(j) issued", 7: "SM: got S(j)", 8: "SM: P(j) done", 9: "EPI: O final", 10: "EPI: stored",
+         11: "TMA: slot free(j)", 12: "TMA: issued(j)"}
+v = [int(x) & 0xFFFFFFFFFFFFFFFF for x in tr.cpu().tolist()]
+for slot in range(4):
+    ev = [x for x in v[slot * 144:(slot + 1) * 144] if x]
+    if not ev:
+        continue
+    ev.sort(key=lambda x: x >> 24)
+    t0 = ev[0] >> 24
+    print(f"=== CTA slot {slot}: {len(ev)} events, span {(ev[-1] >> 24) - t0} cycles")
+    for x in ev:
+        print(f"  {(x >> 24) - t0:7d}  {names.get((x >> 16) & 0xff, '?'):20s} j={x & 0xffff}")

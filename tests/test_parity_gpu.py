@@ -120,10 +120,11 @@ CASES = [  # (B, H, T, d, C, W)
 @pytest.mark.parametrize("mode", ["sliding", "block"])
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("dtype,kernel", [(torch.float32, "simt"), (torch.bfloat16, "simt"),
-                                          (torch.bfloat16, "tile"), (torch.bfloat16, "pair")])
+                                          (torch.bfloat16, "tile"), (torch.bfloat16, "pair"),
+                                          (torch.bfloat16, "wide")])
 def test_prefill_parity(eva, case, mode, dtype, kernel):
     B, H, T, d, C, W = case
-    if kernel in ("tile", "pair") and d not in (64, 128):
+    if kernel in ("tile", "pair", "wide") and d not in (64, 128):
         pytest.skip("tensor-core kernels cover d in {64, 128}; other d run the SIMT kernel")
     cfg = eva.make_config(B, H, T, d, C, W, mode=mode, dtype=dtype, seed=7)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=2, device="cuda")
@@ -155,7 +156,7 @@ def test_prefill_window_covers_sequence_is_softmax(eva, dtype, simt):
 
 
 @pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, "tile"),
-                                               (torch.bfloat16, False, "pair")])
+                                               (torch.bfloat16, False, "pair"), (torch.bfloat16, False, "wide")])
 def test_prefill_summaries_provided_and_poison(eva, dtype, simt, kernel):
     """Everything a query block must not see is poisoned with large finite values;
     its outputs must not move (bit-exact).  Uses EVA_SUMMARIES_PROVIDED."""
@@ -225,7 +226,7 @@ def test_prefill_detects_beta_perturbation(eva):
 
 
 @pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, "tile"),
-                                               (torch.bfloat16, False, "pair")])
+                                               (torch.bfloat16, False, "pair"), (torch.bfloat16, False, "wide")])
 def test_sharded_equals_unsharded(eva, dtype, simt, kernel):
     """(b,h) shards computed separately are bitwise equal to the full run (RNG keyed by global unit)."""
     B, H, T, d, C, W = 2, 3, 384, 64, 32, 64
@@ -382,7 +383,7 @@ def test_decode_capacity_error(eva):
 
 
 # ----------------------------------------------------------------------------- full-size sampled parity
-@pytest.mark.parametrize("kernel", [None, "tile", "pair"])
+@pytest.mark.parametrize("kernel", [None, "tile", "pair", "wide"])
 @pytest.mark.parametrize("B,H,T,d,C,W", [(1, 16, 2048, 64, 64, 128), (1, 4, 8192, 128, 64, 256)])
 def test_full_size_sampled_parity(eva, B, H, T, d, C, W, kernel):
     """BASELINE configs[1] (full) and configs[2] (4 of its 256 units, same kernel launch
