@@ -403,3 +403,27 @@ def test_full_size_sampled_parity(eva, B, H, T, d, C, W, kernel):
                                            cfg.scale)
         assert np.max(np.abs(f64(O[u])[rows] - rO)) <= 2e-2
         assert np.max(np.abs(f64(lse[u])[rows] - rl)) <= 2e-2
+
+
+# ----------------------------------------------------------------------------- configs[4] sweep shapes
+@pytest.mark.parametrize("T,C,W", [(4096, 32, 128), (16384, 32, 512), (32768, 128, 128), (65536, 64, 512),
+                                   (131072, 128, 512)])
+def test_long_context_sweep_sampled_parity(eva, T, C, W):
+    """BASELINE configs[4] shapes (H=32, d=128 per unit; 2 units run, same launch shape per
+    unit): summaries of sampled chunks and outputs of sampled rows vs the oracle."""
+    d, units = 128, 2
+    cfg = eva.make_config(1, units, T, d, C, W, dtype=torch.bfloat16, seed=5)
+    Q, K, V = eva_inputs.qkv(0, units, T, d, torch.bfloat16, seed=9, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    nC = T // C
+    rng = np.random.default_rng(T + C + W)
+    for u in range(units):
+        E = oracle.eps(cfg.seed, cfg.layer, u, nC, d)
+        Kf, Vf = f64(K[u]), f64(V[u])
+        rk, rv = oracle.summarize(Kf, Vf, E, C)
+        assert np.max(np.abs(f64(ks[u]) - rk)) <= 2e-2
+        assert np.max(np.abs(f64(vs[u]) - rv)) <= 2e-2
+        rows = np.unique(np.concatenate([rng.integers(0, T, 48), [0, W - 1, W, T // 2, T - 1]]))
+        rows, rO, rl = oracle.prefill_rows(f64(Q[u]), Kf, Vf, rk, rv, rows, C, W, 0, cfg.scale)
+        assert np.max(np.abs(f64(O[u])[rows] - rO)) <= 2e-2
+        assert np.max(np.abs(f64(lse[u])[rows] - rl)) <= 2e-2
