@@ -125,6 +125,7 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
  *              EVA_PREFILL_TC_TILE    -- force the one-tile-per-CTA tensor-core kernel;
  *              EVA_PREFILL_TC_PAIR    -- force the persistent two-tile tensor-core kernel;
  *              EVA_PREFILL_TC_WIDE    -- force the 128-key-tile tensor-core kernel;
+ *              EVA_PREFILL_TC_SPLIT   -- force the split-softmax (8 softmax warps) kernel;
  *              0                      -- compute summaries, then attend (kernel chosen
  *                                        by problem size).
  * bf16 runs the tcgen05/TMEM/TMA kernel for d in {64, 128} (requires 16-byte
@@ -134,6 +135,7 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
 #define EVA_PREFILL_TC_TILE 8u
 #define EVA_PREFILL_TC_PAIR 16u
 #define EVA_PREFILL_TC_WIDE 32u
+#define EVA_PREFILL_TC_SPLIT 64u
 eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K, const void* V,
                             void* Ksum, void* Vsum, const float* eps, void* O, float* lse,
                             uint32_t flags, eva_stream_t stream);

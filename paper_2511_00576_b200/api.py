@@ -125,7 +125,7 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
         lse = torch.empty(bh, T, dtype=torch.float32, device=Q.device)
     flags = (N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0) | (N.EVA_PREFILL_SIMT if simt else 0)
     flags |= {None: 0, "simt": 0, "tile": N.EVA_PREFILL_TC_TILE, "pair": N.EVA_PREFILL_TC_PAIR,
-              "wide": N.EVA_PREFILL_TC_WIDE}[kernel]
+              "wide": N.EVA_PREFILL_TC_WIDE, "split": N.EVA_PREFILL_TC_SPLIT}[kernel]
     check(lib.eva_attn_prefill(ctypes.byref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum), _ptr(Vsum),
                                _ptr(eps), _ptr(O), _ptr(lse if want_lse else None), flags,
                                _stream(Q.device)))

@@ -131,7 +131,7 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
   if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT | EVA_PREFILL_TC_TILE | EVA_PREFILL_TC_PAIR |
-                EVA_PREFILL_TC_WIDE))
+                EVA_PREFILL_TC_WIDE | EVA_PREFILL_TC_SPLIT))
     return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
   if (cfg->bh_count == 0) return ok();
   const void* p[] = {Q, K, V, O};
@@ -153,7 +153,7 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) &&
                   eva::prefill_sm100_supported(*cfg);
   const uint32_t variant = (flags & EVA_PREFILL_TC_TILE) ? 1u : (flags & EVA_PREFILL_TC_PAIR) ? 2u
-                          : (flags & EVA_PREFILL_TC_WIDE) ? 3u : 0u;
+                          : (flags & EVA_PREFILL_TC_WIDE) ? 3u : (flags & EVA_PREFILL_TC_SPLIT) ? 4u : 0u;
   cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, Q, K, V, Ksum, Vsum, O, lse, variant, s)
                      : eva::launch_prefill_simt(*cfg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cuda_status(e, tc ? "eva_attn_prefill(sm100)" : "eva_attn_prefill(simt)");

@@ -396,6 +396,271 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// ========================================================================== split-softmax kernel
+// The tile kernel with 8 softmax warps: warps 2..5 own columns [0,32) of every 64-key S tile,
+// warps 6..9 columns [32,64), of the same 128 rows (warp w and w+4 share TMEM lane quadrant
+// w%4).  The two halves exchange their partial row max through shared memory (a 64-thread
+// named barrier per quadrant, double-buffered), so per-warp softmax work and latency halve.
+// Register budget: 2 CTAs x 320 threads per SM (<= 102 registers per thread).
+constexpr int NTHREADS2 = 320;
+
+template <int D, int NSTAGE>
+struct __align__(1024) Smem2 {
+  __nv_bfloat16 q[BM * D];
+  __nv_bfloat16 k[NSTAGE][BN * D];
+  __nv_bfloat16 v[NSTAGE][BN * D];
+  float xmax[2][2][BM];  // [tile parity][half][row]
+  float xsum[2][BM];
+  uint64_t q_full;
+  uint64_t k_full[NSTAGE], v_full[NSTAGE], k_empty[NSTAGE], v_empty[NSTAGE];
+  uint64_t s_full[2], p_full[2], o_done, o_final;
+  uint32_t tmem_base;
+};
+
+template <int D, int NSTAGE>
+__global__ void __launch_bounds__(NTHREADS2, 2)
+prefill_split_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
+                     const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
+                     int T, int C, int W, int mode, float scale_log2, float* __restrict__ lse) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem2<D, NSTAGE>* sm = reinterpret_cast<Smem2<D, NSTAGE>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.y;
+  const TilePlan plan(blockIdx.x, T, C, W, mode);
+  const int NT = plan.count();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
+    tma_prefetch(&mKs); tma_prefetch(&mVs); tma_prefetch(&mO);
+    mbar_init(&sm->q_full, 1);
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm->k_full[s], 1);
+      mbar_init(&sm->v_full[s], 1);
+      mbar_init(&sm->k_empty[s], 1);
+      mbar_init(&sm->v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm->s_full[b], 1);
+      mbar_init(&sm->p_full[b], 256);
+    }
+    mbar_init(&sm->o_done, 1);
+    mbar_init(&sm->o_final, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm->tmem_base, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
+      for (int kb = 0; kb < D / 64; ++kb)
+        tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
+      for (int j = NSTAGE; j < NT; ++j) {
+        const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
+        const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
+        for (int kb = 0; kb < D / 64; ++kb) {
+          tma_prefetch_l2_3d(mk, kb * 64, plan.base(j), u);
+          tma_prefetch_l2_3d(mv, kb * 64, plan.base(j), u);
+        }
+      }
+    }
+    __syncwarp();
+    auto load_k = [&](int j) {
+      const int s = j % NSTAGE;
+      if (j >= NSTAGE) mbar_wait(&sm->k_empty[s], ((j / NSTAGE) - 1) & 1);
+      const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb)
+          tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, plan.base(j), u);
+      }
+      __syncwarp();
+    };
+    auto load_v = [&](int j) {
+      const int s = j % NSTAGE;
+      if (j >= NSTAGE) mbar_wait(&sm->v_empty[s], ((j / NSTAGE) - 1) & 1);
+      const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb)
+          tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, plan.base(j), u);
+      }
+      __syncwarp();
+    };
+    load_k(0);
+    for (int j = 0; j < NT; ++j) {
+      if (j + 1 < NT) load_k(j + 1);
+      load_v(j);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
+    const uint32_t q_addr = smem_u32(sm->q);
+    mbar_wait(&sm->q_full, 0);
+    for (int j = 0; j <= NT; ++j) {
+      if (j < NT) {
+        const int s = j % NSTAGE;
+        mbar_wait(&sm->k_full[s], (j / NSTAGE) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sm->k[s]);
+        const uint32_t d_tmem = tmem + (uint32_t)(j & 1) * BN;
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+            mma_ss(d_tmem, smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024),
+                   smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm->s_full[j & 1]);
+          mma_commit(&sm->k_empty[s]);
+        }
+        __syncwarp();
+      }
+      if (j >= 1) {
+        const int jj = j - 1, s = jj % NSTAGE;
+        mbar_wait(&sm->p_full[jj & 1], (jj >> 1) & 1);
+        mbar_wait(&sm->v_full[s], (jj / NSTAGE) & 1);
+        tc_fence_after();
+        const uint32_t v_addr = smem_u32(sm->v[s]);
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < BN / 16; ++ks)
+            mma_ts(tmem + TM_O, tmem + (uint32_t)(jj & 1) * BN + ks * 8,
+                   smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024), idesc_o, (jj > 0 || ks > 0) ? 1u : 0u);
+          mma_commit(&sm->v_empty[s]);
+          mma_commit(&sm->o_done);
+          if (jj == NT - 1) mma_commit(&sm->o_final);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax halves + epilogue
+    const int h = (warp - 2) >> 2;          // column half: 0 -> [0,32), 1 -> [32,64)
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int n = plan.n0 + r;
+    const bool valid = n < T;
+    const Range rr = mask_range(valid ? n : plan.nlast, C, W, mode);
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    constexpr int DH = D / 2;               // O columns owned by this half
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < NT; ++j) {
+      const int b = j & 1;
+      mbar_wait(&sm->s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const int base = plan.base(j) + 32 * h;
+      int vlo, vhi;
+      if (plan.summary(j)) {
+        vlo = 0;
+        vhi = (int)min((int64_t)32, rr.nsum - base);
+      } else {
+        vlo = (int)max((int64_t)0, rr.lo - base);
+        vhi = min(32, n - base + 1);
+      }
+      if (!valid) vhi = vlo;
+      uint32_t sr[32];
+      tmem_ld32(t_lane + (uint32_t)b * BN + 32 * h, sr);
+      tmem_wait_ld();
+      if (!__all_sync(0xffffffffu, vlo <= 0 && vhi >= 32)) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (c < vlo || c >= vhi) sr[c] = 0xff800000u;
+      }
+      float pm[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pm[i] = __uint_as_float(sr[i]);
+#pragma unroll
+      for (int c = 4; c < 32; ++c) pm[c & 3] = fmaxf(pm[c & 3], __uint_as_float(sr[c]));
+      const float pmx = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
+      sm->xmax[b][h][r] = pmx;
+      named_bar_sync(2 + quad, 64);
+      const float mx = fmaxf(pmx, sm->xmax[b][1 - h][r]) * scale_log2;
+      const bool grow = mx > m_ref + 8.0f;
+      if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+        const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
+        mbar_wait(&sm->o_done, (j - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int cc = 0; cc < DH / 32; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(t_lane + TM_O + h * DH + cc * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+          tmem_st32(t_lane + TM_O + h * DH + cc * 32, o);
+        }
+        tmem_wait_st();
+        l *= f;
+      }
+      if (grow) m_ref = mx;
+      const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
+      uint32_t pk[16];
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg));
+        const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg));
+        ls[(2 * c) & 3] += p0;
+        ls[(2 * c + 1) & 3] += p1;
+        pk[c] = pack_bf16(p0, p1);
+      }
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      tmem_st16(t_lane + (uint32_t)b * BN + 16 * h, pk);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm->p_full[b]);
+    }
+    // ------------------------------------------------------------ epilogue
+    sm->xsum[h][r] = l;
+    mbar_wait(&sm->o_final, 0);
+    tc_fence_after();
+    named_bar_sync(2 + quad, 64);
+    const float lt = sm->xsum[0][r] + sm->xsum[1][r];
+    const float inv_l = lt > 0.f ? 1.0f / lt : 0.f;
+    uint8_t* qs = reinterpret_cast<uint8_t*>(sm->q);
+#pragma unroll
+    for (int cc = 0; cc < DH / 32; ++cc) {
+      uint32_t o[32];
+      const int col = h * DH + cc * 32;
+      tmem_ld32(t_lane + TM_O + col, o);
+      tmem_wait_ld();
+      const int kb = col / 64, c16_0 = (col % 64) / 8;
+      uint8_t* rowp = qs + kb * (BM * 128) + r * 128;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        uint4 w;
+        w.x = pack_bf16(__uint_as_float(o[8 * g + 0]) * inv_l, __uint_as_float(o[8 * g + 1]) * inv_l);
+        w.y = pack_bf16(__uint_as_float(o[8 * g + 2]) * inv_l, __uint_as_float(o[8 * g + 3]) * inv_l);
+        w.z = pack_bf16(__uint_as_float(o[8 * g + 4]) * inv_l, __uint_as_float(o[8 * g + 5]) * inv_l);
+        w.w = pack_bf16(__uint_as_float(o[8 * g + 6]) * inv_l, __uint_as_float(o[8 * g + 7]) * inv_l);
+        *reinterpret_cast<uint4*>(rowp + (((c16_0 + g) ^ (r & 7)) * 16)) = w;
+      }
+    }
+    if (h == 0 && valid && lse) lse[(size_t)u * T + n] = (m_ref + __log2f(lt)) * 0.69314718055994531f;
+    fence_proxy_async_smem();
+    named_bar_sync(1, 256);
+    if (warp == 2 && lane == 0) {
+      for (int kb = 0; kb < D / 64; ++kb) tma_store_3d(&mO, sm->q + kb * BM * 64, kb * 64, plan.n0, u);
+      tma_store_commit();
+      tma_store_wait_all();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
 // ========================================================================== wide-tile kernel
 // One 128-query tile per CTA (two CTAs per SM) walking 128-key tiles: the S MMA is
 // M=128 x N=128 (full tensor rate; N=64 SS MMAs are shared-memory bound at 48 instead of
@@ -1136,6 +1401,36 @@ cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const 
   return cudaGetLastError();
 }
 
+template <int D, int NSTAGE>
+cudaError_t launch_split(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                         const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
+  const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
+  CUtensorMap mQ, mK, mV, mKs, mVs, mO;
+  bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BN) &&
+            make_map(&mV, V, BH, T, D, BN) && make_map(&mO, O, BH, T, D, BM);
+  if (nC > 0) {
+    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BN) && make_map(&mVs, Vsum, BH, nC, D, BN);
+  } else {
+    mKs = mK;
+    mVs = mV;
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(Smem2<D, NSTAGE>) + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_split_kernel<D, NSTAGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((T + BM - 1) / BM, BH);
+  const float scale_log2 = cfg.scale * 1.4426950408889634f;
+  prefill_split_kernel<D, NSTAGE><<<grid, NTHREADS2, smem, s>>>(mQ, mK, mV, mKs, mVs, mO, T, cfg.chunk,
+                                                               cfg.window, cfg.mode, scale_log2, lse);
+  note_launch();
+  return cudaGetLastError();
+}
+
 template <int D, int NSK, int NSV>
 cudaError_t launch_wide(const eva_config& cfg, const void* Q, const void* K, const void* V,
                         const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
@@ -1238,6 +1533,10 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const voi
   bool pair = false;
   if (variant == 1) pair = false;
   if (variant == 2) pair = true;
+  if (variant == 4) {
+    if (cfg.d_head == 128) return launch_split<128, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+    if (cfg.d_head == 64) return launch_split<64, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  }
   if (variant == 3) {
     if (cfg.d_head == 128) return launch_wide<128, 1, 1>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
     if (cfg.d_head == 64) return launch_wide<64, 2, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);

@@ -11,7 +11,7 @@ for (B, H, T, d, C, W) in shapes:
     ks, vs = eva.eva_summarize(cfg, K, V)
     O = torch.empty_like(Q)
     flush = torch.empty(512 << 18, device="cuda")
-    for kern in sys.argv[1:] or ["tile", "pair"]:
+    for kern in sys.argv[1:] or ["tile", "split"]:
         for _ in range(3):
             eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, kernel=kern)
         ts = []
