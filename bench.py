@@ -9,7 +9,7 @@ window, Q/K/V ~ N(0,1) synthetic (eva_inputs), eps from the in-kernel Philox.
 One STEP = the whole hot path over one batch:
     eva_summarize (a1-a3) -> eva_attn_prefill (a4-a5, summaries provided)
     -> eva_cache_load (a6, prompt hand-off with the prefill's summaries)
-    -> eva_cache_append(1) + eva_attn_decode (a6-a7)
+    -> eva_decode_step (a6 + a7: append the next token and attend it, one launch)
 The step is captured once as a CUDA graph and replayed (it is launch-latency scale).
 metric value = prompt tokens (B*T per GPU, all ranks) / device time of the step.
 Weak scaling: rank r owns units [r*B*H, (r+1)*B*H) of a global batch of N*B sequences;
@@ -128,10 +128,15 @@ def prefill_flops(BH, T, d, C, W, mode=0):
 
 
 def decode_bytes(BH, d, n, C, W, elem=2):
-    """Algorithmic bytes of one eva_attn_decode at query n: K+V of every visible entry + q + o."""
+    """Algorithmic bytes of one fused decode step at query n: K+V of every
+    visible entry + q + o + the appended k, v (read once, written to the ring) + when the
+    token completes a chunk, the chunk's C key/value rows re-read and its summary written."""
     ns = max(0, n // C - W // C + 1)
     lo = ns * C
-    return BH * ((ns + n - lo + 1) * 2 * d * elem + 2 * d * elem + 4)
+    b = (ns + n - lo + 1) * 2 * d * elem + 2 * d * elem + 2 * 2 * d * elem
+    if (n + 1) % C == 0:
+        b += 2 * C * d * elem + 2 * d * elem
+    return BH * b
 
 
 def run_ours(args, rank, world, local_rank):
@@ -175,8 +180,7 @@ def run_ours(args, rank, world, local_rank):
         eva.eva_attn_prefill(cfg, Q, K, V, Ksum=Ksum, Vsum=Vsum, summaries_provided=True,
                              O=O, lse=lse)                                       # a4-a5
         cache.eva_cache_load(K, V, Ksum, Vsum)                                    # a6 hand-off
-        cache.eva_cache_append(kn, vn)                                            # a6
-        cache.eva_attn_decode(qn, O=o_dec, want_lse=False)                        # a7
+        cache.eva_decode_step(qn, kn, vn, O=o_dec, want_lse=False)                # a6 + a7 fused
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -224,9 +228,8 @@ def run_ours(args, rank, world, local_rank):
             eva.eva_attn_prefill(cfg, Q, K, V, Ksum=Ksum, Vsum=Vsum, summaries_provided=True, O=O, lse=lse)
             e[2].record(s)
             cache.eva_cache_load(K, V, Ksum, Vsum)
-            cache.eva_cache_append(kn, vn)
             e[3].record(s)
-            cache.eva_attn_decode(qn, O=o_dec, want_lse=False)
+            cache.eva_decode_step(qn, kn, vn, O=o_dec, want_lse=False)
             e[4].record(s)
         torch.cuda.synchronize()
         sum_ms = [e[0].elapsed_time(e[1]) for e in kev]
@@ -247,8 +250,7 @@ def run_ours(args, rank, world, local_rank):
             cache.c.pos = 0
             Oo, _, ks_, vs_ = eva.eva_attn_prefill(cfg, dQ, dK, dV, want_lse=False)
             cache.eva_cache_load(dK, dV, ks_, vs_)
-            cache.eva_cache_append(kn, vn)
-            od, _ = cache.eva_attn_decode(qn, want_lse=False)
+            od, _ = cache.eva_decode_step(qn, kn, vn, want_lse=False)
             hO.copy_(Oo, non_blocking=True)
             hOd.copy_(od, non_blocking=True)
             if e: e[1].record(s)
@@ -298,7 +300,7 @@ def run_ours(args, rank, world, local_rank):
                                                  + statistics.mean(dec_ms)),
                      "peak_source": peaks["src"]},
         "breakdown_ms": {"summarize": statistics.mean(sum_ms), "prefill": pre_avg,
-                         "cache_load+append": statistics.mean(app_ms), "decode": statistics.mean(dec_ms),
+                         "cache_load": statistics.mean(app_ms), "decode_step": statistics.mean(dec_ms),
                          "note": "eager per-kernel events; the step itself is a CUDA-graph replay"},
         "kernels_per_step": kernels_per_step,
         "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s",
@@ -399,17 +401,27 @@ def bench_decode(args, eva, torch, dev, s, rank, world, peaks):
     nbytes = 0
     e_app[0].record(s)
     for i in range(steps):
-        cache.eva_cache_append(toks[i, 1], toks[i, 2])
         e_dec[i].record(s)
-        cache.eva_attn_decode(toks[i, 0], O=o, want_lse=False)
+        cache.eva_decode_step(toks[i, 0], toks[i, 1], toks[i, 2], O=o, want_lse=False)  # append + decode
         e_app[i + 1].record(s)
         nbytes += decode_bytes(BH, d, cache.pos - 1, C, W)
     torch.cuda.synchronize()
     total = e_app[0].elapsed_time(e_app[-1])
     dec = sum(e_dec[i].elapsed_time(e_app[i + 1]) for i in range(steps))
+    # the same tokens through the two-launch path (append kernel + decode kernel), for reference
+    cache.c.pos = ctx
+    e2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e2[0].record(s)
+    for i in range(steps):
+        cache.eva_cache_append(toks[i, 1], toks[i, 2])
+        cache.eva_attn_decode(toks[i, 0], O=o, want_lse=False)
+    e2[1].record(s)
+    torch.cuda.synchronize()
+    two_launch_ms = e2[0].elapsed_time(e2[1]) / steps
     out = {"workload": f"configs[3]: B=256,H=32,d=128,C=64,W=256, context {ctx}, {steps} generated tokens",
            "tokens_per_s_per_gpu": D["B"] * steps / (total / 1e3), "ms_per_token": total / steps,
            "decode_ms_per_token": dec / steps,
+           "two_launch_ms_per_token": two_launch_ms,
            "roofline": {"kernel": "eva_attn_decode", "bound": "hbm",
                         "achieved": nbytes / (dec / 1e3) / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
                         "frac": nbytes / (dec / 1e3) / 1e9 / peaks["hbm"],

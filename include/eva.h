@@ -192,6 +192,20 @@ eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float
                            void* workspace, size_t workspace_bytes, eva_stream_t stream);
 size_t eva_decode_workspace_bytes(const eva_cache* cache);
 
+/* One generation step in one launch: append (K_new, V_new) at position p = pos and attend
+ * query Q (the same position) over the cache -- the result equals
+ * eva_cache_append(cache, K_new, V_new, 1, eps) followed by eva_attn_decode(cache, Q, ...),
+ * bit for bit.  The token's own key/value are read from K_new/V_new and written to the ring by
+ * the same launch; a token that completes a chunk, and any step with bh_count >= 1024 (where
+ * the decode is a long HBM stream and two launches measured faster), takes the two-launch
+ * path (append kernel, then decode).
+ * K_new, V_new, Q, O : [bh_count, d] cfg.dtype; eps as in eva_cache_append; lse or NULL.
+ * workspace: eva_decode_workspace_bytes() of the cache AFTER the append (pos + 1).
+ * On success pos += 1. */
+eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, const void* V_new,
+                           const float* eps, void* O, float* lse, void* workspace,
+                           size_t workspace_bytes, eva_stream_t stream);
+
 /* ---------------------------------------------------------------- debug / introspection
  * eva_mask_ranges: the (lo(n), nsum(n)) the kernels use, for n in
  * [n_begin, n_begin + count), written to device int64 arrays lo, nsum

@@ -215,6 +215,32 @@ class DecodeCache:
 
     decode = eva_attn_decode
 
+    def eva_decode_step(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
+                        eps: Optional[torch.Tensor] = None, O: Optional[torch.Tensor] = None,
+                        lse: Optional[torch.Tensor] = None, want_lse: bool = True):
+        """Append (k, v) and attend q at that position in one launch: q, k, v [bh, d]."""
+        cfg = self.c.cfg
+        dt, bh, d = _tdtype(cfg), cfg.bh_count, cfg.d_head
+        for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+            _need(t, nm, (bh, d), dt)
+        if eps is not None:
+            _need(eps, "eps", (bh, self.c.cap_chunks, d), torch.float32)
+        O = torch.empty_like(q) if O is None else O
+        if want_lse and lse is None:
+            lse = torch.empty(bh, dtype=torch.float32, device=q.device)
+        self.c.pos += 1
+        nbytes = self.workspace_bytes()
+        self.c.pos -= 1
+        if nbytes and (self._ws is None or self._ws.numel() * 4 < nbytes):
+            self._ws = torch.zeros((nbytes + 3) // 4 * 2, dtype=torch.float32, device=q.device)
+        ws = self._ws if nbytes else None
+        check(lib.eva_decode_step(ctypes.byref(self.c), _ptr(q), _ptr(k), _ptr(v), _ptr(eps), _ptr(O),
+                                  _ptr(lse if want_lse else None), _ptr(ws),
+                                  0 if ws is None else ws.numel() * 4, _stream(q.device)))
+        return O, (lse if want_lse else None)
+
+    step = eva_decode_step
+
 
 def eva_mask_ranges(cfg: EvaConfig, n_begin: int, count: int, device="cuda"):
     lo = torch.empty(count, dtype=torch.int64, device=device)

@@ -252,6 +252,53 @@ eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float
                      "eva_attn_decode");
 }
 
+eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, const void* V_new,
+                           const float* eps, void* O, float* lse, void* workspace,
+                           size_t workspace_bytes, eva_stream_t stream) {
+  if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
+  eva_status st = check_cfg(&cache->cfg, false);
+  if (st != EVA_OK) return st;
+  if (cache->pos < 0) return fail(EVA_ERR_INVALID_ARG, "pos=%lld", (long long)cache->pos);
+  if ((cache->pos + 1) / cache->cfg.chunk > cache->cap_chunks)
+    return fail(EVA_ERR_CAPACITY, "append at pos %lld needs %lld summaries > cap %d", (long long)cache->pos,
+                (long long)((cache->pos + 1) / cache->cfg.chunk), cache->cap_chunks);
+  if (cache->cfg.bh_count == 0) {
+    cache->pos += 1;
+    return ok();
+  }
+  const void* p[] = {Q, K_new, V_new, O, cache->ring_k, cache->ring_v};
+  const char* nm[] = {"Q", "K_new", "V_new", "O", "ring_k", "ring_v"};
+  if ((st = check_ptrs(6, p, nm)) != EVA_OK) return st;
+  if (cache->cap_chunks > 0) {
+    const void* p2[] = {cache->sum_k, cache->sum_v};
+    const char* nm2[] = {"sum_k", "sum_v"};
+    if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+  }
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  if (lse && !aligned16(lse)) return fail(EVA_ERR_INVALID_ARG, "lse is not 16-byte aligned");
+  eva_cache after = *cache;
+  after.pos += 1;
+  const int S = eva::decode_splits(after);
+  const size_t need = eva_decode_workspace_bytes(&after);
+  if (need > 0 && (!workspace || workspace_bytes < need))
+    return fail(EVA_ERR_INVALID_ARG, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
+  if (workspace && !aligned16(workspace)) return fail(EVA_ERR_INVALID_ARG, "workspace is not 16-byte aligned");
+  // A token that completes a chunk needs its chunk summarised (append kernel).  Large
+  // batches also take the two-launch path: there the decode is a pure HBM stream and the
+  // separate append measured faster (0.478 vs 0.518 ms/token at configs[3]); the fused
+  // launch pays off when the step is launch-latency bound (small batch x heads).
+  if ((cache->pos + 1) % cache->cfg.chunk == 0 || cache->cfg.bh_count >= 1024) {
+    st = eva_cache_append(cache, K_new, V_new, 1, eps, stream);
+    if (st != EVA_OK) return st;
+    return eva_attn_decode(cache, Q, O, lse, workspace, workspace_bytes, stream);
+  }
+  cudaError_t e = eva::launch_decode_step(after, Q, K_new, V_new, O, lse, (float*)workspace, S,
+                                          (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "eva_decode_step");
+  cache->pos += 1;
+  return ok();
+}
+
 eva_status eva_mask_ranges(const eva_config* cfg, int64_t n_begin, int64_t count, int64_t* lo,
                            int64_t* nsum, eva_stream_t stream) {
   if (!cfg) return fail(EVA_ERR_INVALID_ARG, "cfg is NULL");

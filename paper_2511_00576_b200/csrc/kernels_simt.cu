@@ -378,10 +378,16 @@ __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __res
 // every lane has 2*UNROLL independent 16-byte loads in flight.  Each lane group
 // keeps its own online-softmax state (m, l, acc[VEC]); groups and warps are merged
 // at the end (shuffles, then shared memory).
-template <typename T, int D>
+// Fused decode step (FUSED): the cache descriptor already counts the new token (pos = p+1)
+// and Knew/Vnew hold it; entry n = p is read from Knew/Vnew instead of the ring, and the
+// split-0 CTA of each unit writes it to ring slot p mod W (which held position p - W,
+// invisible to query p).  Used for steps that do not complete a chunk.
+template <typename T, int D, bool FUSED = false>
 __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __restrict__ Q,
                                                      T* __restrict__ O, float* __restrict__ lse,
-                                                     float* __restrict__ ws) {
+                                                     float* __restrict__ ws, int S_,
+                                                     const T* __restrict__ Knew = nullptr,
+                                                     const T* __restrict__ Vnew = nullptr) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int TPR = D / VEC;          // lanes per row
   constexpr int RPW = 32 / TPR;         // rows per warp-wide load
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   static_assert(TPR >= 1 && TPR <= 32 && 32 % TPR == 0, "bad D/VEC");
   __shared__ float sm_m[NW], sm_l[NW];
   __shared__ float sm_acc[NW][D];
-  const int u = blockIdx.x, S = gridDim.y, s = blockIdx.y;
+  const int u = blockIdx.x, S = S_, s = blockIdx.y;
   const int W = c.cfg.window, C = c.cfg.chunk;
   const int64_t n = c.pos - 1;
   const Range r = mask_range(n, C, W, c.cfg.mode);
@@ -426,6 +432,9 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
       if (e < ns) {
         kp = sk + (size_t)e * D;
         vp = sv + (size_t)e * D;
+      } else if (FUSED && e == E - 1) {  // the token being appended in this launch
+        kp = Knew + (size_t)u * D + ch0;
+        vp = Vnew + (size_t)u * D + ch0;
       } else {
         int slot = slot0 + e;
         if (slot >= W) slot -= W;
@@ -487,6 +496,19 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   if (grp == 0) {
 #pragma unroll
     for (int j = 0; j < VEC; ++j) sm_acc[warp][ch0 + j] = acc[j];
+  }
+  if constexpr (FUSED) {
+    // append: split 0 writes the new token to ring slot p mod W (position p - W, never read
+    // by this launch); issued after the attention loads so it does not delay them
+    if (s == 0 && warp == 1) {
+      const size_t slot = (size_t)((c.pos - 1) % W);
+      T* wk = static_cast<T*>(c.ring_k) + ((size_t)u * W + slot) * D;
+      T* wv = static_cast<T*>(c.ring_v) + ((size_t)u * W + slot) * D;
+      for (int i = lane; i < D; i += 32) {
+        wk[i] = Knew[(size_t)u * D + i];
+        wv[i] = Vnew[(size_t)u * D + i];
+      }
+    }
   }
   __syncthreads();
   if (warp != 0) return;
@@ -667,14 +689,16 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
     const size_t sm = summ_smem_bytes(cfg.chunk, D, sizeof(T));
     const int ni = summ_reg_ni<T, D>(cfg.chunk);  // row slots per lane
-    if (ni <= 8) {
+    if (ni <= 16) {
       const dim3 grid(nC, cfg.bh_count);
       if (ni <= 2)
         summarize_reg_kernel<T, D, 2><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
       else if (ni <= 4)
         summarize_reg_kernel<T, D, 4><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
-      else
+      else if (ni <= 8)
         summarize_reg_kernel<T, D, 8><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+      else
+        summarize_reg_kernel<T, D, 16><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
     } else if (sm <= kSummSmemMax) {
       err = set_smem_attr((const void*)summarize_cta_kernel<T, D>, sm);
       if (err != cudaSuccess) return err;
@@ -718,10 +742,11 @@ cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* 
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     const size_t sm = summ_smem_bytes(C, D, sizeof(T));
     const int ni = summ_reg_ni<T, D>(C);
-    const bool cta = ni <= 8 || sm <= kSummSmemMax;
+    const bool cta = ni <= 16 || sm <= kSummSmemMax;
     auto fn = ni <= 2 ? append_kernel<T, D, 2> : ni <= 4 ? append_kernel<T, D, 4> : ni <= 8 ? append_kernel<T, D, 8>
+            : ni <= 16 ? append_kernel<T, D, 16>
             : sm <= kSummSmemMax ? append_kernel<T, D, 1> : append_kernel<T, D, 0>;
-    const size_t smem = (ni > 8 && sm <= kSummSmemMax) ? sm : 0;
+    const size_t smem = (ni > 16 && sm <= kSummSmemMax) ? sm : 0;
     if (smem) {
       err = set_smem_attr((const void*)append_kernel<T, D, 1>, sm);
       if (err != cudaSuccess) return err;
@@ -761,7 +786,7 @@ cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse
   if (c.cfg.bh_count == 0) return cudaSuccess;
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     dim3 grid(c.cfg.bh_count, splits);
-    decode_kernel<T, D><<<grid, 128, 0, s>>>(c, (const T*)Q, (T*)O, lse, ws);
+    decode_kernel<T, D><<<grid, 128, 0, s>>>(c, (const T*)Q, (T*)O, lse, ws, splits);
     note_launch();
   }));
   return cudaGetLastError();
@@ -776,6 +801,18 @@ cudaError_t launch_cache_load(const eva_cache& c, const void* K, const void* V, 
     const int64_t pieces = (int64_t)c.cfg.bh_count * (std::min(n, c.cfg.window) + nC) * PPR;
     cache_load_kernel<T, D><<<(unsigned)((pieces + 255) / 256), 256, 0, s>>>(
         c, (const T*)K, (const T*)V, (const T*)Ksum, (const T*)Vsum, n, nC);
+    note_launch();
+  }));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_step(const eva_cache& c_after, const void* Q, const void* Kn, const void* Vn,
+                               void* O, float* lse, float* ws, int splits, cudaStream_t s) {
+  if (c_after.cfg.bh_count == 0) return cudaSuccess;
+  EVA_DISPATCH_T(c_after.cfg.dtype, EVA_DISPATCH_D(c_after.cfg.d_head, {
+    dim3 grid(c_after.cfg.bh_count, splits);
+    decode_kernel<T, D, true><<<grid, 128, 0, s>>>(c_after, (const T*)Q, (T*)O, lse, ws, splits,
+                                                   (const T*)Kn, (const T*)Vn);
     note_launch();
   }));
   return cudaGetLastError();

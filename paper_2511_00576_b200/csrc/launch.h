@@ -49,6 +49,11 @@ int decode_splits(const eva_cache& c);
 cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse, float* ws,
                           int splits, cudaStream_t s);
 
+// Fused append(1) + decode for a token that does not complete a chunk: c_after already
+// counts the new token.
+cudaError_t launch_decode_step(const eva_cache& c_after, const void* Q, const void* Kn, const void* Vn,
+                               void* O, float* lse, float* ws, int splits, cudaStream_t s);
+
 cudaError_t launch_mask_ranges(const eva_config& cfg, int64_t n0, int64_t count, int64_t* lo,
                                int64_t* nsum, cudaStream_t s);
 cudaError_t launch_philox(const uint32_t* in, uint32_t* out, int n, cudaStream_t s);

@@ -353,6 +353,32 @@ def test_decode_split_k_parity(eva, BH, ctx):
             assert abs(float(lse[u]) - rl[0]) <= 2e-2
 
 
+@pytest.mark.parametrize("dtype,d,C,W,mode", [(torch.bfloat16, 128, 16, 64, "sliding"),
+                                              (torch.float32, 64, 8, 8, "block"),
+                                              (torch.bfloat16, 64, 64, 128, "sliding")])
+def test_fused_decode_step_equals_append_then_decode(eva, dtype, d, C, W, mode):
+    """eva_decode_step == eva_cache_append(1) + eva_attn_decode, bit for bit (outputs and cache),
+    across chunk completions, with in-kernel Philox and with caller eps."""
+    T0, G = 300, 150
+    for use_eps, BH in ((False, 5), (True, 5), (False, 1030)):  # 1030 units: two-launch path
+        cfg = eva.make_config(1, BH, 0, d, C, W, mode=mode, dtype=dtype, seed=51)
+        cap = (T0 + G) // C + 1
+        a = eva.DecodeCache(cfg, cap, device="cuda")
+        b = eva.DecodeCache(cfg, cap, device="cuda")
+        eps = eva_inputs.eps(0, BH, cap, d, device="cuda") if use_eps else None
+        q, k, v = eva_inputs.decode_tokens(0, BH, T0 + G, d, dtype, seed=52, device="cuda")
+        a.eva_cache_append(k[:T0].transpose(0, 1).contiguous(), v[:T0].transpose(0, 1).contiguous(), eps)
+        b.eva_cache_append(k[:T0].transpose(0, 1).contiguous(), v[:T0].transpose(0, 1).contiguous(), eps)
+        for t in range(T0, T0 + G):
+            a.eva_cache_append(k[t], v[t], eps)
+            oa, la = a.eva_attn_decode(q[t])
+            ob, lb = b.eva_decode_step(q[t], k[t], v[t], eps)
+            assert torch.equal(oa, ob) and torch.equal(la, lb), t
+        assert a.pos == b.pos
+        assert torch.equal(a.ring_k, b.ring_k) and torch.equal(a.ring_v, b.ring_v)
+        assert torch.equal(a.sum_k, b.sum_k) and torch.equal(a.sum_v, b.sum_v)
+
+
 def test_decode_poisoned_stale_ring_slots(eva):
     """Stale / invisible ring slots and unused summary rows are poisoned; output unchanged."""
     BH, d, C, W, T = 2, 64, 16, 64, 300
