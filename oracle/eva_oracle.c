@@ -378,3 +378,151 @@ EXPORT double oracle_cache_decode(const oracle_cache* s, const double* q, double
   free(logit);
   return mx + log(z);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Backward of the prefill (NEXT row 1: the paper's training path,    */
+/* P:253 "forward and backward pass").  For L = sum_n dO_n . o_n it returns  */
+/* dQ, dK, dV of one unit, written out step by step from the forward:       */
+/*  attention (Eq.12): P_nx = softmax_x(s q_n.key_x), D_n = dO_n . o_n,      */
+/*    dS_nx = P_nx (dO_n . val_x - D_n); dq_n = s sum_x dS_nx key_x;         */
+/*    local x = m: dk_m += s dS_nm q_n, dv_m += P_nm dO_n;                   */
+/*    summary x = c: dk~_c += s dS_nc q_n, dbeta_c += P_nc dO_n.             */
+/*  summaries (Eq.9, Eq.10, Eq.15), chunk c with rows i:           */
+/*    w_i = softmax_i(a_i), a_i = omega.k_i - |k_i|^2/2, beta = sum w_i v_i:  */
+/*    dv_i += w_i dbeta; da_i = w_i (dbeta.v_i - dbeta.beta);                */
+/*    dk_i += da_i (omega - k_i); domega = sum_i da_i k_i;                    */
+/*    omega = lambda clip(k~ + eps): dk~ += lambda [|k~+eps| <= clip] domega  */
+/*    (as printed; the shifted reading omega = k~ + lambda clip(eps) gives    */
+/*    dk~ += domega); k~ = mean k_i: dk_i += dk~ / C.                         */
+/* eps is a constant.  Q, K, V, dO, dQ, dK, dV: [T, d]; eps [nC, d].          */
+/* ------------------------------------------------------------------------ */
+EXPORT void oracle_backward(int T, int d, int C, int W, int mode, double scale, double lambda,
+                            double clipv, int omega_mode, const double* Q, const double* K,
+                            const double* V, const double* eps, const double* dO, double* dQ,
+                            double* dK, double* dV) {
+  const int nC = T / C;
+  const size_t nd = (size_t)(nC > 0 ? nC : 1) * d;
+  double* kt = (double*)calloc(nd, sizeof(double));
+  double* bt = (double*)calloc(nd, sizeof(double));
+  double* om = (double*)calloc(nd, sizeof(double));
+  double* dkt = (double*)calloc(nd, sizeof(double));
+  double* dbt = (double*)calloc(nd, sizeof(double));
+  double* logit = (double*)malloc(sizeof(double) * ((size_t)T + nC + 1));
+  double* o = (double*)malloc(sizeof(double) * d);
+  if (nC > 0) oracle_summarize(T, d, C, K, V, eps, lambda, clipv, omega_mode, kt, bt, om);
+  memset(dQ, 0, sizeof(double) * (size_t)T * d);
+  memset(dK, 0, sizeof(double) * (size_t)T * d);
+  memset(dV, 0, sizeof(double) * (size_t)T * d);
+  for (int n = 0; n < T; ++n) {
+    int64_t lo, ns;
+    oracle_mask(n, C, W, mode, &lo, &ns);
+    const double* q = Q + (size_t)n * d;
+    const double* g = dO + (size_t)n * d;
+    int cnt = 0;
+    double mx = -INFINITY;
+    for (int64_t c = 0; c < ns; ++c, ++cnt) {
+      double t = 0.0;
+      for (int j = 0; j < d; ++j) t += q[j] * kt[(size_t)c * d + j];
+      logit[cnt] = scale * t;
+      if (logit[cnt] > mx) mx = logit[cnt];
+    }
+    for (int64_t m = lo; m <= n; ++m, ++cnt) {
+      double t = 0.0;
+      for (int j = 0; j < d; ++j) t += q[j] * K[(size_t)m * d + j];
+      logit[cnt] = scale * t;
+      if (logit[cnt] > mx) mx = logit[cnt];
+    }
+    double z = 0.0;
+    for (int i = 0; i < cnt; ++i) z += exp(logit[i] - mx);
+    for (int i = 0; i < cnt; ++i) logit[i] = exp(logit[i] - mx) / z; /* now P */
+    for (int j = 0; j < d; ++j) o[j] = 0.0;
+    int i = 0;
+    for (int64_t c = 0; c < ns; ++c, ++i)
+      for (int j = 0; j < d; ++j) o[j] += logit[i] * bt[(size_t)c * d + j];
+    for (int64_t m = lo; m <= n; ++m, ++i)
+      for (int j = 0; j < d; ++j) o[j] += logit[i] * V[(size_t)m * d + j];
+    double Dn = 0.0;
+    for (int j = 0; j < d; ++j) Dn += g[j] * o[j];
+    i = 0;
+    for (int64_t c = 0; c < ns; ++c, ++i) {
+      double dp = 0.0;
+      for (int j = 0; j < d; ++j) dp += g[j] * bt[(size_t)c * d + j];
+      const double dS = logit[i] * (dp - Dn);
+      for (int j = 0; j < d; ++j) {
+        dQ[(size_t)n * d + j] += scale * dS * kt[(size_t)c * d + j];
+        dkt[(size_t)c * d + j] += scale * dS * q[j];
+        dbt[(size_t)c * d + j] += logit[i] * g[j];
+      }
+    }
+    for (int64_t m = lo; m <= n; ++m, ++i) {
+      double dp = 0.0;
+      for (int j = 0; j < d; ++j) dp += g[j] * V[(size_t)m * d + j];
+      const double dS = logit[i] * (dp - Dn);
+      for (int j = 0; j < d; ++j) {
+        dQ[(size_t)n * d + j] += scale * dS * K[(size_t)m * d + j];
+        dK[(size_t)m * d + j] += scale * dS * q[j];
+        dV[(size_t)m * d + j] += logit[i] * g[j];
+      }
+    }
+  }
+  /* through the summaries */
+  double* a = (double*)malloc(sizeof(double) * (C > 0 ? C : 1));
+  double* dom = (double*)malloc(sizeof(double) * d);
+  for (int c = 0; c < nC; ++c) {
+    const double* Kc = K + (size_t)c * C * d;
+    const double* Vc = V + (size_t)c * C * d;
+    const double* w_om = om + (size_t)c * d;
+    const double* db = dbt + (size_t)c * d;
+    const double* be = bt + (size_t)c * d;
+    double amax = -INFINITY;
+    for (int r = 0; r < C; ++r) {
+      double dot = 0.0, nrm = 0.0;
+      for (int j = 0; j < d; ++j) {
+        dot += w_om[j] * Kc[(size_t)r * d + j];
+        nrm += Kc[(size_t)r * d + j] * Kc[(size_t)r * d + j];
+      }
+      a[r] = dot - 0.5 * nrm;
+      if (a[r] > amax) amax = a[r];
+    }
+    double zz = 0.0;
+    for (int r = 0; r < C; ++r) zz += exp(a[r] - amax);
+    double dbb = 0.0;
+    for (int j = 0; j < d; ++j) dbb += db[j] * be[j];
+    for (int j = 0; j < d; ++j) dom[j] = 0.0;
+    for (int r = 0; r < C; ++r) {
+      const double w = exp(a[r] - amax) / zz;
+      double dbv = 0.0;
+      for (int j = 0; j < d; ++j) dbv += db[j] * Vc[(size_t)r * d + j];
+      const double da = w * (dbv - dbb);
+      for (int j = 0; j < d; ++j) {
+        dV[((size_t)c * C + r) * d + j] += w * db[j];
+        dK[((size_t)c * C + r) * d + j] += da * (w_om[j] - Kc[(size_t)r * d + j]);
+        dom[j] += da * Kc[(size_t)r * d + j];
+      }
+    }
+    for (int j = 0; j < d; ++j) {
+      double dk_t = dkt[(size_t)c * d + j];
+      if (omega_mode == 0) {
+        const double x = kt[(size_t)c * d + j] + eps[(size_t)c * d + j];
+        if (x >= -clipv && x <= clipv) dk_t += lambda * dom[j];
+      } else {
+        dk_t += dom[j];
+      }
+      for (int r = 0; r < C; ++r) dK[((size_t)c * C + r) * d + j] += dk_t / (double)C;
+    }
+  }
+  free(a); free(dom); free(kt); free(bt); free(om); free(dkt); free(dbt); free(logit); free(o);
+}
+
+EXPORT void oracle_backward_batch(int BH, int T, int d, int C, int W, int mode, double scale,
+                                  double lambda, double clipv, int omega_mode, const double* Q,
+                                  const double* K, const double* V, const double* eps,
+                                  const double* dO, double* dQ, double* dK, double* dV) {
+  const int nC = T / C;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int u = 0; u < BH; ++u) {
+    const size_t off = (size_t)u * T * d;
+    oracle_backward(T, d, C, W, mode, scale, lambda, clipv, omega_mode, Q + off, K + off, V + off,
+                    eps + (size_t)u * nC * d, dO + off, dQ + off, dK + off, dV + off);
+  }
+}
