@@ -206,6 +206,26 @@ eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, c
                            const float* eps, void* O, float* lse, void* workspace,
                            size_t workspace_bytes, eva_stream_t stream);
 
+/* ---------------------------------------------------------------- backward (training)
+ * eva_attn_backward: gradient of the prefill (the paper
+ * trains FlashEVA models with it).  For L = sum_n dO_n . o_n it
+ * writes dQ, dK, dV, differentiating through the attention (Eq.12-14) AND the
+ * chunk summaries (k~ = chunk mean, omega = Eq.15, beta^ = Eq.9/10); eps is a
+ * constant; d clip/dx = 1 on the closed range [-clip, clip] (R14).
+ * Q, K, V, O, dO, dQ, dK, dV : [bh_count, T, d] cfg.dtype
+ * Ksum, Vsum : [bh_count, nC, d] cfg.dtype -- the summaries the forward used
+ * O, lse     : the forward's output and natural-log lse ([bh_count, T] fp32)
+ * eps        : as in eva_summarize (NULL = the in-kernel Philox draws); must be
+ *              what the forward used.
+ * workspace  : device scratch of eva_backward_workspace_bytes(cfg) bytes, 256-byte
+ *              aligned; no initialisation needed (fp32 D, dQ, dK, dV accumulators).
+ * Arithmetic is fp32 (SIMT kernels); three kernels are enqueued on stream. */
+size_t eva_backward_workspace_bytes(const eva_config* cfg);
+eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K, const void* V,
+                             const void* Ksum, const void* Vsum, const void* O, const float* lse,
+                             const void* dO, const float* eps, void* dQ, void* dK, void* dV,
+                             void* workspace, size_t workspace_bytes, eva_stream_t stream);
+
 /* ---------------------------------------------------------------- debug / introspection
  * eva_mask_ranges: the (lo(n), nsum(n)) the kernels use, for n in
  * [n_begin, n_begin + count), written to device int64 arrays lo, nsum

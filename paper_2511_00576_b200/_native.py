@@ -46,7 +46,8 @@ class EvaCache(ctypes.Structure):
 EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache_append", "eva_cache_load",
            "eva_attn_decode", "eva_decode_workspace_bytes", "eva_mask_ranges", "eva_philox",
            "eva_draw_eps", "eva_last_error", "eva_version", "eva_launch_count",
-           "eva_debug_trace_prefill", "eva_decode_step"]
+           "eva_debug_trace_prefill", "eva_decode_step", "eva_backward_workspace_bytes",
+           "eva_attn_backward"]
 
 
 class EvaError(RuntimeError):
@@ -73,6 +74,8 @@ def _load():
         "eva_cache_load": (st, [CACHE, P, P, P, P, ctypes.c_int32, P]),
         "eva_decode_step": (st, [CACHE, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "eva_decode_workspace_bytes": (ctypes.c_size_t, [CACHE]),
+        "eva_backward_workspace_bytes": (ctypes.c_size_t, [CFG]),
+        "eva_attn_backward": (st, [CFG] + [P] * 13 + [ctypes.c_size_t, P]),
         "eva_mask_ranges": (st, [CFG, ctypes.c_int64, ctypes.c_int64, P, P, P]),
         "eva_philox": (st, [P, P, ctypes.c_int32, P]),
         "eva_draw_eps": (st, [CFG, P, P]),

@@ -17,7 +17,8 @@ from ._native import EvaCache, EvaConfig, EvaError, check, lib
 
 __all__ = ["make_config", "eva_summarize", "eva_attn_prefill", "eva_cache_append", "eva_cache_load",
            "eva_attn_decode", "DecodeCache", "eva_mask_ranges", "eva_philox", "eva_draw_eps",
-           "EvaConfig", "EvaError", "launch_count", "version"]
+           "EvaConfig", "EvaError", "launch_count", "version", "eva_attn_backward",
+           "eva_backward_workspace_bytes"]
 
 _DT = {torch.float32: N.EVA_F32, torch.bfloat16: N.EVA_BF16}
 _MODE = {"sliding": N.EVA_WINDOW_SLIDING, "block": N.EVA_WINDOW_BLOCK}
@@ -130,6 +131,44 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
                                _ptr(eps), _ptr(O), _ptr(lse if want_lse else None), flags,
                                _stream(Q.device)))
     return O, (lse if want_lse else None), Ksum, Vsum
+
+
+def eva_backward_workspace_bytes(cfg: EvaConfig) -> int:
+    return int(lib.eva_backward_workspace_bytes(ctypes.byref(cfg)))
+
+
+def eva_attn_backward(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
+                      Ksum: torch.Tensor, Vsum: torch.Tensor, O: torch.Tensor, lse: torch.Tensor,
+                      dO: torch.Tensor, *, eps: Optional[torch.Tensor] = None,
+                      workspace: Optional[torch.Tensor] = None, dQ: Optional[torch.Tensor] = None,
+                      dK: Optional[torch.Tensor] = None, dV: Optional[torch.Tensor] = None):
+    """Gradient of the prefill for L = sum(dO * O).  Returns (dQ, dK, dV).
+
+    Ksum/Vsum/O/lse/eps are what eva_attn_prefill used and produced.  workspace: a
+    uint8 CUDA tensor of at least eva_backward_workspace_bytes(cfg) bytes (allocated
+    here when None)."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    nC = T // cfg.chunk
+    for t, nm in ((Q, "Q"), (K, "K"), (V, "V"), (O, "O"), (dO, "dO")):
+        _need(t, nm, (bh, T, d), dt)
+    _need(lse, "lse", (bh, T), torch.float32)
+    if nC:
+        _need(Ksum, "Ksum", (bh, nC, d), dt)
+        _need(Vsum, "Vsum", (bh, nC, d), dt)
+    if eps is not None:
+        _need(eps, "eps", (bh, nC, d), torch.float32)
+    dQ = torch.empty_like(Q) if dQ is None else dQ
+    dK = torch.empty_like(K) if dK is None else dK
+    dV = torch.empty_like(V) if dV is None else dV
+    for t, nm in ((dQ, "dQ"), (dK, "dK"), (dV, "dV")):
+        _need(t, nm, (bh, T, d), dt)
+    nbytes = eva_backward_workspace_bytes(cfg)
+    if workspace is None:
+        workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=Q.device)
+    check(lib.eva_attn_backward(ctypes.byref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum), _ptr(Vsum),
+                                _ptr(O), _ptr(lse), _ptr(dO), _ptr(eps), _ptr(dQ), _ptr(dK), _ptr(dV),
+                                _ptr(workspace), workspace.numel(), _stream(Q.device)))
+    return dQ, dK, dV
 
 
 class DecodeCache:

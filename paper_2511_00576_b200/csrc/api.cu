@@ -299,6 +299,37 @@ eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, c
   return ok();
 }
 
+size_t eva_backward_workspace_bytes(const eva_config* cfg) {
+  if (check_cfg(cfg, true) != EVA_OK) return 0;
+  return eva::backward_workspace_bytes(*cfg);
+}
+
+eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K, const void* V,
+                             const void* Ksum, const void* Vsum, const void* O, const float* lse,
+                             const void* dO, const float* eps, void* dQ, void* dK, void* dV,
+                             void* workspace, size_t workspace_bytes, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (cfg->bh_count == 0) return ok();
+  const void* p[] = {Q, K, V, O, lse, dO, dQ, dK, dV, workspace};
+  const char* nm[] = {"Q", "K", "V", "O", "lse", "dO", "dQ", "dK", "dV", "workspace"};
+  if ((st = check_ptrs(10, p, nm)) != EVA_OK) return st;
+  if (cfg->T / cfg->chunk > 0) {
+    const void* p2[] = {Ksum, Vsum};
+    const char* nm2[] = {"Ksum", "Vsum"};
+    if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+  }
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255u) != 0)
+    return fail(EVA_ERR_INVALID_ARG, "workspace is not 256-byte aligned");
+  const size_t need = eva::backward_workspace_bytes(*cfg);
+  if (workspace_bytes < need)
+    return fail(EVA_ERR_INVALID_ARG, "workspace_bytes %zu < %zu", workspace_bytes, need);
+  return cuda_status(eva::launch_backward(*cfg, Q, K, V, Ksum, Vsum, O, lse, dO, eps, dQ, dK, dV,
+                                          workspace, (cudaStream_t)stream),
+                     "eva_attn_backward");
+}
+
 eva_status eva_mask_ranges(const eva_config* cfg, int64_t n_begin, int64_t count, int64_t* lo,
                            int64_t* nsum, eva_stream_t stream) {
   if (!cfg) return fail(EVA_ERR_INVALID_ARG, "cfg is NULL");

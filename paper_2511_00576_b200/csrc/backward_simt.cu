@@ -1,0 +1,569 @@
+// backward_simt.cu -- gradient of the FlashEVA prefill (the paper
+// trains with it: "forward and backward pass").  For L = sum_n dO_n . o_n:
+//
+//   attention (Eq.12-14), P_nx = exp(s q_n.key_x - lse_n):
+//     D_n = dO_n . o_n,  dS_nx = P_nx (dO_n . val_x - D_n)
+//     dq_n = s sum_x dS_nx key_x
+//     local key m   : dk_m += s sum_n dS_nm q_n,   dv_m += sum_n P_nm dO_n
+//     summary key c : dk~_c = s sum_n dS_nc q_n,   dbeta_c = sum_n P_nc dO_n
+//   summaries (Eq.9, Eq.10, Eq.15), chunk c with rows i:
+//     w_i = softmax_i(omega.k_i - |k_i|^2/2),  beta = sum_i w_i v_i
+//     dv_i += w_i dbeta;  da_i = w_i (dbeta.v_i - dbeta.beta)
+//     dk_i += da_i (omega - k_i);  domega = sum_i da_i k_i
+//     dk~ += (d omega / d k~) domega   (lambda [|k~+eps| <= clip] as printed, 1 shifted)
+//     dk_i += dk~ / C                  (k~ = mean of the chunk's keys)
+//
+// Three kernels (fp32 arithmetic, cfg.dtype I/O, fp32 workspace):
+//   bwd_prep      : D_n = dO_n . o_n; zero the dQ and summary-gradient accumulators.
+//   bwd_main      : key-tile-major.  A CTA owns one tile of 64 keys (locals of one tile,
+//                   or 64 summaries), keeps its dK/dV in registers and walks the query
+//                   tiles that see it (locals: the next W + 64 queries; summaries: a
+//                   segment of the queries after the window -- split across CTAs and
+//                   combined with fp32 atomics).  Per 64x64 pair: S = Q K^T and
+//                   dP = dO V^T as a register-tiled SIMT product from shared memory,
+//                   P / dS elementwise, dV += P^T dO, dK += dS^T Q, and dQ += dS K
+//                   added to the fp32 accumulator with red.global.add.
+//   bwd_finalize  : one CTA per chunk: the summary chain rule above, then dQ, dK, dV
+//                   of the chunk's rows are written in cfg.dtype (tail rows are copied).
+// This is the parity-grade first version of the row (SIMT fp32 math); the tcgen05
+// version is future work.
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace eva {
+
+namespace {
+
+constexpr int BT = 64;        // keys per tile, queries per tile
+constexpr int BWD_THREADS = 256;
+
+// Last query that sees local key m (inverse of mask_range: lo(n) <= m).
+__host__ __device__ __forceinline__ int64_t local_qhi(int64_t m, int C, int W, int mode) {
+  if (mode == EVA_WINDOW_SLIDING) return (m / C + W / C) * (int64_t)C - 1;
+  return (m / W + 1) * (int64_t)W - 1;
+}
+// First query that sees summary c (c < nsum(n)).
+__host__ __device__ __forceinline__ int64_t summary_qlo(int64_t c, int C, int W, int mode) {
+  if (mode == EVA_WINDOW_SLIDING) return (c + W / C) * (int64_t)C;
+  return (c / (W / C) + 1) * (int64_t)W;
+}
+
+struct BwdWs {
+  float* D;    // [bh, T]
+  float* dQ;   // [bh, T, d]
+  float* dK;   // [bh, T, d]  local-attention part
+  float* dV;   // [bh, T, d]
+  float* dKs;  // [bh, nC, d] d k~ from the attention
+  float* dVs;  // [bh, nC, d] d beta
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+BwdWs carve(const eva_config& cfg, void* base) {
+  const size_t BH = (size_t)cfg.bh_count, T = (size_t)cfg.T, d = (size_t)cfg.d_head;
+  const size_t nC = (size_t)(cfg.T / cfg.chunk);
+  char* p = static_cast<char*>(base);
+  BwdWs w;
+  w.D = reinterpret_cast<float*>(p);   p += align256(BH * T * 4);
+  w.dQ = reinterpret_cast<float*>(p);  p += align256(BH * T * d * 4);
+  w.dK = reinterpret_cast<float*>(p);  p += align256(BH * T * d * 4);
+  w.dV = reinterpret_cast<float*>(p);  p += align256(BH * T * d * 4);
+  w.dKs = reinterpret_cast<float*>(p); p += align256(BH * nC * d * 4);
+  w.dVs = reinterpret_cast<float*>(p);
+  return w;
+}
+
+// Query tiles per summary work item (balances the summary CTAs against the local ones).
+constexpr int kSumSegTiles = 8;
+
+struct ItemPlan {
+  int n_sum_items, n_local_items;
+};
+
+__host__ __device__ __forceinline__ int n_qtiles(int T) { return (T + BT - 1) / BT; }
+
+// Summary tile s covers chunks [64 s, 64 s + 64); its query tiles start at the one holding
+// the first query that sees chunk 64 s.
+__host__ __device__ __forceinline__ int sum_tile_qt0(int s, int T, int C, int W, int mode) {
+  const int64_t q = summary_qlo((int64_t)s * BT, C, W, mode);
+  return q >= T ? n_qtiles(T) : (int)(q / BT);
+}
+__host__ __device__ __forceinline__ int sum_tile_segs(int s, int T, int C, int W, int mode) {
+  const int nq = n_qtiles(T) - sum_tile_qt0(s, T, C, W, mode);
+  return (nq + kSumSegTiles - 1) / kSumSegTiles;
+}
+
+ItemPlan plan_items(const eva_config& cfg) {
+  const int T = cfg.T, C = cfg.chunk, W = cfg.window, nC = T / C;
+  ItemPlan p{0, n_qtiles(T)};
+  for (int s = 0; s * BT < nC; ++s) p.n_sum_items += sum_tile_segs(s, T, C, W, cfg.mode);
+  return p;
+}
+
+// ------------------------------------------------------------------ bwd_prep
+template <typename T, int D>
+__global__ void __launch_bounds__(128) bwd_prep_kernel(eva_config cfg, const T* __restrict__ O,
+                                                       const T* __restrict__ dO, BwdWs ws) {
+  const int Tn = cfg.T, nC = Tn / cfg.chunk;
+  const int u = blockIdx.y;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = blockIdx.x * 4 + warp;
+  if (n >= Tn) return;
+  const size_t row = (size_t)u * Tn + n;
+  float s = 0.f;
+  for (int j = lane; j < D; j += 32) {
+    s += Elem<T>::to_f(O[row * D + j]) * Elem<T>::to_f(dO[row * D + j]);
+    ws.dQ[row * D + j] = 0.f;
+  }
+  s = warp_sum(s);
+  if (lane == 0) ws.D[row] = s;
+  if (n < nC) {
+    const size_t srow = (size_t)u * nC + n;
+    for (int j = lane; j < D; j += 32) {
+      ws.dKs[srow * D + j] = 0.f;
+      ws.dVs[srow * D + j] = 0.f;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ bwd_main
+template <int D>
+struct MainSmem {
+  float Ks[BT][D + 1], Vs[BT][D + 1], Qs[BT][D + 1], dOs[BT][D + 1];
+  float Ps[BT][BT + 1], dSs[BT][BT + 1];
+  float lse2[BT], Dd[BT];
+  int rlo[BT], rns[BT];
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(BWD_THREADS, 1)
+    bwd_main_kernel(eva_config cfg, const T* __restrict__ Q, const T* __restrict__ K,
+                    const T* __restrict__ V, const T* __restrict__ Ksum, const T* __restrict__ Vsum,
+                    const T* __restrict__ dO, const float* __restrict__ lse, BwdWs ws, int n_sum_items) {
+  constexpr int CE = D / 16;  // channels per thread in the [64 x D] products (D >= 16)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MainSmem<D>& sm = *reinterpret_cast<MainSmem<D>*>(smem_raw);
+  const int Tn = cfg.T, C = cfg.chunk, W = cfg.window, mode = cfg.mode, nC = Tn / C;
+  const int u = blockIdx.y;
+  const int tid = threadIdx.x;
+  const float scale = cfg.scale;
+  const float sl2 = scale * 1.4426950408889634f;
+
+  // ---- decode the work item
+  bool is_sum;
+  int k0, nk, qt_begin, qt_end;
+  {
+    int item = blockIdx.x;
+    if (item < n_sum_items) {
+      is_sum = true;
+      int s = 0;
+      for (;; ++s) {
+        const int ns = sum_tile_segs(s, Tn, C, W, mode);
+        if (item < ns) break;
+        item -= ns;
+      }
+      k0 = s * BT;
+      nk = min(BT, nC - k0);
+      const int qt0 = sum_tile_qt0(s, Tn, C, W, mode);
+      qt_begin = qt0 + item * kSumSegTiles;
+      qt_end = min(n_qtiles(Tn), qt_begin + kSumSegTiles);
+    } else {
+      is_sum = false;
+      const int t = item - n_sum_items;
+      k0 = t * BT;
+      nk = min(BT, Tn - k0);
+      qt_begin = t;
+      const int64_t qhi = min((int64_t)Tn - 1, local_qhi(k0 + nk - 1, C, W, mode));
+      qt_end = (int)(qhi / BT) + 1;
+    }
+  }
+  const T* kb = is_sum ? Ksum + (size_t)u * nC * D : K + (size_t)u * Tn * D;
+  const T* vb = is_sum ? Vsum + (size_t)u * nC * D : V + (size_t)u * Tn * D;
+  for (int i = tid; i < BT * D; i += BWD_THREADS) {
+    const int r = i / D, c = i % D;
+    const bool ok = r < nk;
+    sm.Ks[r][c] = ok ? Elem<T>::to_f(kb[(size_t)(k0 + r) * D + c]) : 0.f;
+    sm.Vs[r][c] = ok ? Elem<T>::to_f(vb[(size_t)(k0 + r) * D + c]) : 0.f;
+  }
+
+  const int ty = tid / 16, tx = tid % 16;  // S/dP block: rows ty*4+a, cols tx+16b
+  float dk[4][CE], dv[4][CE];
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+#pragma unroll
+    for (int e = 0; e < CE; ++e) dk[b][e] = dv[b][e] = 0.f;
+
+  const T* qb = Q + (size_t)u * Tn * D;
+  const T* gb = dO + (size_t)u * Tn * D;
+  for (int qt = qt_begin; qt < qt_end; ++qt) {
+    const int n0 = qt * BT;
+    __syncthreads();  // previous tile's readers are done (and the K/V tile is staged)
+    for (int i = tid; i < BT * D; i += BWD_THREADS) {
+      const int r = i / D, c = i % D;
+      const bool ok = n0 + r < Tn;
+      sm.Qs[r][c] = ok ? Elem<T>::to_f(qb[(size_t)(n0 + r) * D + c]) : 0.f;
+      sm.dOs[r][c] = ok ? Elem<T>::to_f(gb[(size_t)(n0 + r) * D + c]) : 0.f;
+    }
+    if (tid < BT) {
+      const int64_t n = (int64_t)n0 + tid;
+      if (n < Tn) {
+        const Range rg = mask_range(n, C, W, mode);
+        sm.rlo[tid] = (int)rg.lo;
+        sm.rns[tid] = (int)rg.nsum;
+        sm.lse2[tid] = lse[(size_t)u * Tn + n] * 1.4426950408889634f;
+        sm.Dd[tid] = ws.D[(size_t)u * Tn + n];
+      } else {
+        sm.rlo[tid] = 1 << 30;  // nothing visible
+        sm.rns[tid] = 0;
+        sm.lse2[tid] = 0.f;
+        sm.Dd[tid] = 0.f;
+      }
+    }
+    __syncthreads();
+
+    // S = Q K^T and dP = dO V^T for rows ty*4+a, cols tx+16b
+    {
+      float s[4][4], dp[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) s[a][b] = dp[a][b] = 0.f;
+#pragma unroll 4
+      for (int k = 0; k < D; ++k) {
+        float qa[4], ga[4], kk[4], vv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          qa[a] = sm.Qs[ty * 4 + a][k];
+          ga[a] = sm.dOs[ty * 4 + a][k];
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          kk[b] = sm.Ks[tx + 16 * b][k];
+          vv[b] = sm.Vs[tx + 16 * b][k];
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            s[a][b] = fmaf(qa[a], kk[b], s[a][b]);
+            dp[a][b] = fmaf(ga[a], vv[b], dp[a][b]);
+          }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = ty * 4 + a;
+        const int n = n0 + i;
+        const int lo = sm.rlo[i], ns = sm.rns[i];
+        const float l2 = sm.lse2[i], Dn = sm.Dd[i];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int j = tx + 16 * b;
+          const int x = k0 + j;
+          const bool vis = j < nk && (is_sum ? (x < ns) : (x >= lo && x <= n));
+          const float p = vis ? exp2f(fmaf(s[a][b], sl2, -l2)) : 0.f;
+          sm.Ps[i][j] = p;
+          sm.dSs[i][j] = p * (dp[a][b] - Dn);
+        }
+      }
+    }
+    __syncthreads();
+
+    // dV += P^T dO, dK += dS^T Q: keys ty*4+b, channels tx+16e
+#pragma unroll 2
+    for (int i = 0; i < BT; ++i) {
+      float pb[4], db[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        pb[b] = sm.Ps[i][ty * 4 + b];
+        db[b] = sm.dSs[i][ty * 4 + b];
+      }
+#pragma unroll
+      for (int e = 0; e < CE; ++e) {
+        const float g = sm.dOs[i][tx + 16 * e], q = sm.Qs[i][tx + 16 * e];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          dv[b][e] = fmaf(pb[b], g, dv[b][e]);
+          dk[b][e] = fmaf(db[b], q, dk[b][e]);
+        }
+      }
+    }
+
+    // dQ += s dS K: rows ty*4+a, channels tx+16e
+    {
+      float dq[4][CE];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int e = 0; e < CE; ++e) dq[a][e] = 0.f;
+#pragma unroll 2
+      for (int j = 0; j < BT; ++j) {
+        float da[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) da[a] = sm.dSs[ty * 4 + a][j];
+#pragma unroll
+        for (int e = 0; e < CE; ++e) {
+          const float kv = sm.Ks[j][tx + 16 * e];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) dq[a][e] = fmaf(da[a], kv, dq[a][e]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int n = n0 + ty * 4 + a;
+        if (n < Tn) {
+          float* dst = ws.dQ + ((size_t)u * Tn + n) * D;
+#pragma unroll
+          for (int e = 0; e < CE; ++e) atomicAdd(dst + tx + 16 * e, scale * dq[a][e]);
+        }
+      }
+    }
+  }
+
+  // write the key tile's gradients
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int r = ty * 4 + b;
+    if (r >= nk) continue;
+    if (is_sum) {
+      float* dks = ws.dKs + ((size_t)u * nC + k0 + r) * D;
+      float* dvs = ws.dVs + ((size_t)u * nC + k0 + r) * D;
+#pragma unroll
+      for (int e = 0; e < CE; ++e) {
+        atomicAdd(dks + tx + 16 * e, scale * dk[b][e]);
+        atomicAdd(dvs + tx + 16 * e, dv[b][e]);
+      }
+    } else {
+      float* dkl = ws.dK + ((size_t)u * Tn + k0 + r) * D;
+      float* dvl = ws.dV + ((size_t)u * Tn + k0 + r) * D;
+#pragma unroll
+      for (int e = 0; e < CE; ++e) {
+        dkl[tx + 16 * e] = scale * dk[b][e];
+        dvl[tx + 16 * e] = dv[b][e];
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ bwd_finalize
+// Block x < nC: chunk x (summary chain rule + output of its C rows); x >= nC: tail rows
+// [nC*C + (x-nC)*C, ...) that belong to no complete chunk (copy-out only).
+template <typename T, int D>
+__global__ void __launch_bounds__(128) bwd_finalize_kernel(eva_config cfg, const T* __restrict__ K,
+                                                           const T* __restrict__ V,
+                                                           const float* __restrict__ eps, BwdWs ws,
+                                                           T* __restrict__ dQ, T* __restrict__ dK,
+                                                           T* __restrict__ dV) {
+  constexpr int CH = (D + 31) / 32;
+  const int Tn = cfg.T, C = cfg.chunk, nC = Tn / C;
+  const int u = blockIdx.y;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int bx = blockIdx.x;
+  const int r0 = bx * C;
+  const int r1 = min(Tn, r0 + C);
+  const size_t ub = (size_t)u * Tn;
+  if (bx >= nC) {
+    for (int r = r0 + warp; r < r1; r += 4) {
+      const size_t o = (ub + r) * D;
+      for (int j = lane; j < D; j += 32) {
+        dQ[o + j] = Elem<T>::from_f(ws.dQ[o + j]);
+        dK[o + j] = Elem<T>::from_f(ws.dK[o + j]);
+        dV[o + j] = Elem<T>::from_f(ws.dV[o + j]);
+      }
+    }
+    return;
+  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* part = reinterpret_cast<float*>(smem_raw);  // [4][D]
+  float* kt = part + 4 * D;
+  float* om = kt + D;
+  float* beta = om + D;
+  float* dbeta = beta + D;
+  float* dkt = dbeta + D;
+  float* stat = dkt + D;  // [8]
+  float* w = stat + 8;    // [C]
+  float* da = w + C;      // [C]
+  const int c = bx;
+  const T* Kc = K + (ub + r0) * D;
+  const T* Vc = V + (ub + r0) * D;
+  const size_t srow = ((size_t)u * nC + c) * D;
+
+  // k~ = mean of the chunk's keys
+  float acc[CH];
+#pragma unroll
+  for (int e = 0; e < CH; ++e) acc[e] = 0.f;
+  for (int r = warp; r < C; r += 4)
+#pragma unroll
+    for (int e = 0; e < CH; ++e)
+      if (lane + 32 * e < D) acc[e] += Elem<T>::to_f(Kc[(size_t)r * D + lane + 32 * e]);
+#pragma unroll
+  for (int e = 0; e < CH; ++e)
+    if (lane + 32 * e < D) part[warp * D + lane + 32 * e] = acc[e];
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const int j = threadIdx.x;
+    const float s = part[j] + part[D + j] + part[2 * D + j] + part[3 * D + j];
+    const float k_t = s * (1.0f / (float)C);
+    const uint32_t bh = (uint32_t)(cfg.bh_begin + u);
+    const float e = eps ? eps[((size_t)u * nC + c) * D + j]
+                        : philox_normal1(cfg.seed, cfg.layer, bh, (uint32_t)c, (uint32_t)j);
+    kt[j] = k_t;
+    om[j] = omega_of(k_t, e, cfg);
+    dbeta[j] = ws.dVs[srow + j];
+    // d omega / d k~ (Eq.15 as printed: lambda inside the clip range, inclusive)
+    float g;
+    if (cfg.omega_mode == EVA_OMEGA_AS_PRINTED) {
+      const float x = k_t + e;
+      g = (x >= -cfg.clip && x <= cfg.clip) ? cfg.lambda : 0.f;
+    } else {
+      g = 1.f;
+    }
+    dkt[j] = g;  // factor for now; the gradient is assembled below
+  }
+  __syncthreads();
+  // a_i = omega . k_i - |k_i|^2 / 2
+  for (int r = warp; r < C; r += 4) {
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      const int j = lane + 32 * e;
+      if (j < D) {
+        const float k = Elem<T>::to_f(Kc[(size_t)r * D + j]);
+        s += k * (om[j] - 0.5f * k);
+      }
+    }
+    s = warp_sum(s);
+    if (lane == 0) w[r] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float m = -INFINITY;
+    for (int r = lane; r < C; r += 32) m = fmaxf(m, w[r]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float z = 0.f;
+    for (int r = lane; r < C; r += 32) z += __expf(w[r] - m);
+    z = warp_sum(z);
+    const float iz = 1.f / z;
+    for (int r = lane; r < C; r += 32) w[r] = __expf(w[r] - m) * iz;
+  }
+  __syncthreads();
+  // beta = sum_i w_i v_i
+#pragma unroll
+  for (int e = 0; e < CH; ++e) acc[e] = 0.f;
+  for (int r = warp; r < C; r += 4) {
+    const float wr = w[r];
+#pragma unroll
+    for (int e = 0; e < CH; ++e)
+      if (lane + 32 * e < D) acc[e] += wr * Elem<T>::to_f(Vc[(size_t)r * D + lane + 32 * e]);
+  }
+#pragma unroll
+  for (int e = 0; e < CH; ++e)
+    if (lane + 32 * e < D) part[warp * D + lane + 32 * e] = acc[e];
+  __syncthreads();
+  if (warp == 0) {
+    float s = 0.f;
+    for (int j = lane; j < D; j += 32) {
+      const float b = part[j] + part[D + j] + part[2 * D + j] + part[3 * D + j];
+      beta[j] = b;
+      s += b * dbeta[j];
+    }
+    s = warp_sum(s);
+    if (lane == 0) stat[0] = s;  // dbeta . beta
+  }
+  __syncthreads();
+  // da_i = w_i (dbeta . v_i - dbeta . beta); domega = sum_i da_i k_i
+  const float dbb = stat[0];
+#pragma unroll
+  for (int e = 0; e < CH; ++e) acc[e] = 0.f;
+  for (int r = warp; r < C; r += 4) {
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      const int j = lane + 32 * e;
+      if (j < D) s += dbeta[j] * Elem<T>::to_f(Vc[(size_t)r * D + j]);
+    }
+    s = warp_sum(s);
+    const float d_a = w[r] * (s - dbb);
+    if (lane == 0) da[r] = d_a;
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      const int j = lane + 32 * e;
+      if (j < D) acc[e] += d_a * Elem<T>::to_f(Kc[(size_t)r * D + j]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < CH; ++e)
+    if (lane + 32 * e < D) part[warp * D + lane + 32 * e] = acc[e];
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const int j = threadIdx.x;
+    const float dom = part[j] + part[D + j] + part[2 * D + j] + part[3 * D + j];
+    dkt[j] = (ws.dKs[srow + j] + dkt[j] * dom) * (1.0f / (float)C);  // d k~ / C
+  }
+  __syncthreads();
+  // rows of the chunk
+  for (int r = warp; r < C; r += 4) {
+    const size_t o = (ub + r0 + r) * D;
+    const float wr = w[r], dar = da[r];
+    for (int j = lane; j < D; j += 32) {
+      const float k = Elem<T>::to_f(Kc[(size_t)r * D + j]);
+      dQ[o + j] = Elem<T>::from_f(ws.dQ[o + j]);
+      dV[o + j] = Elem<T>::from_f(ws.dV[o + j] + wr * dbeta[j]);
+      dK[o + j] = Elem<T>::from_f(ws.dK[o + j] + dar * (om[j] - k) + dkt[j]);
+    }
+  }
+}
+
+#define BWD_DISPATCH_D(D_, ...)                               \
+  switch (D_) {                                               \
+    case 16: { constexpr int D = 16; __VA_ARGS__; } break;    \
+    case 32: { constexpr int D = 32; __VA_ARGS__; } break;    \
+    case 64: { constexpr int D = 64; __VA_ARGS__; } break;    \
+    case 128: { constexpr int D = 128; __VA_ARGS__; } break;  \
+    default: return cudaErrorInvalidValue;                    \
+  }
+#define BWD_DISPATCH_T(dt, ...)                                                 \
+  if ((dt) == EVA_BF16) { using T = __nv_bfloat16; __VA_ARGS__; }               \
+  else { using T = float; __VA_ARGS__; }
+
+}  // namespace
+
+size_t backward_workspace_bytes(const eva_config& cfg) {
+  const size_t BH = (size_t)cfg.bh_count, T = (size_t)cfg.T, d = (size_t)cfg.d_head;
+  const size_t nC = (size_t)(cfg.T / cfg.chunk);
+  return align256(BH * T * 4) + 3 * align256(BH * T * d * 4) + 2 * align256(BH * nC * d * 4);
+}
+
+cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                            const void* Ksum, const void* Vsum, const void* O, const float* lse,
+                            const void* dO, const float* eps, void* dQ, void* dK, void* dV,
+                            void* workspace, cudaStream_t s) {
+  const BwdWs ws = carve(cfg, workspace);
+  const int Tn = cfg.T, C = cfg.chunk, nC = Tn / C;
+  const ItemPlan plan = plan_items(cfg);
+  cudaError_t err = cudaSuccess;
+  BWD_DISPATCH_T(cfg.dtype, BWD_DISPATCH_D(cfg.d_head, {
+    bwd_prep_kernel<T, D><<<dim3((Tn + 3) / 4, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)O,
+                                                                         (const T*)dO, ws);
+    const size_t sm = sizeof(MainSmem<D>);
+    err = set_smem_attr((const void*)bwd_main_kernel<T, D>, sm);
+    if (err != cudaSuccess) return err;
+    bwd_main_kernel<T, D><<<dim3(plan.n_sum_items + plan.n_local_items, cfg.bh_count),
+                            BWD_THREADS, sm, s>>>(cfg, (const T*)Q, (const T*)K, (const T*)V,
+                                                  (const T*)Ksum, (const T*)Vsum, (const T*)dO,
+                                                  lse, ws, plan.n_sum_items);
+    const int n_tail = (Tn - nC * C + C - 1) / C;
+    const size_t fsm = (size_t)(9 * D + 8 + 2 * C) * sizeof(float);
+    err = set_smem_attr((const void*)bwd_finalize_kernel<T, D>, fsm);
+    if (err != cudaSuccess) return err;
+    bwd_finalize_kernel<T, D><<<dim3(nC + n_tail, cfg.bh_count), 128, fsm, s>>>(
+        cfg, (const T*)K, (const T*)V, eps, ws, (T*)dQ, (T*)dK, (T*)dV);
+    note_launch(3);
+    err = cudaGetLastError();
+  }));
+  return err;
+}
+
+}  // namespace eva

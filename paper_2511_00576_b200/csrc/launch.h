@@ -59,6 +59,15 @@ cudaError_t launch_mask_ranges(const eva_config& cfg, int64_t n0, int64_t count,
 cudaError_t launch_philox(const uint32_t* in, uint32_t* out, int n, cudaStream_t s);
 cudaError_t launch_draw_eps(const eva_config& cfg, float* eps, cudaStream_t s);
 
+// Backward of the prefill (backward_simt.cu): dQ, dK, dV of L = sum(dO * O).
+size_t backward_workspace_bytes(const eva_config& cfg);
+cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                            const void* Ksum, const void* Vsum, const void* O, const float* lse,
+                            const void* dO, const float* eps, void* dQ, void* dK, void* dV,
+                            void* workspace, cudaStream_t s);
+
 int num_sms();
+// Raise a kernel's dynamic shared-memory limit (once per function and size).
+cudaError_t set_smem_attr(const void* fn, size_t bytes);
 
 }  // namespace eva

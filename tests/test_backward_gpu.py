@@ -1,0 +1,141 @@
+"""GPU parity of eva_attn_backward (NEXT row 1) against the fp64 oracle (oracle.backward).
+
+The oracle's gradient is pinned in tests/test_oracle_backward.py (finite
+differences, autograd of the direct form, causal-softmax special cases).
+Tolerance: gradients are sums over many queries, so the bound is
+relative to the largest reference gradient:
+    max |GPU - oracle| <= tol * max(1, max |oracle|),  tol = 1e-4 fp32, 2e-2 bf16.
+"""
+import numpy as np
+import pytest
+import torch
+
+import eva_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def eva(cuda_device):
+    import paper_2511_00576_b200 as eva
+    return eva
+
+
+def f64(t):
+    return t.detach().float().cpu().double().numpy()
+
+
+def _check(name, got, ref, tol):
+    bound = tol * max(1.0, float(np.max(np.abs(ref))) if ref.size else 1.0)
+    err = float(np.max(np.abs(got - ref))) if ref.size else 0.0
+    assert err <= bound, f"{name}: max err {err:.3e} > {bound:.3e}"
+
+
+CASES = [  # (B, H, T, d, C, W)
+    (1, 1, 256, 16, 16, 32),      # configs[0]
+    (1, 2, 300, 32, 8, 24),       # ragged T, W = 3C
+    (2, 1, 515, 64, 64, 128),     # configs[1] shape family, ragged tail
+    (1, 2, 700, 128, 64, 256),    # configs[2] shape family
+    (1, 1, 130, 64, 16, 16),      # W = C
+    (1, 1, 40, 64, 64, 128),      # T < C: no summaries
+    (1, 1, 1, 128, 4, 8),         # T = 1
+    (1, 1, 96, 64, 1, 3),         # C = 1: exact causal softmax gradients
+    (1, 1, 1500, 32, 4, 8),       # 375 chunks: several summary tiles and segments
+]
+
+
+@pytest.mark.parametrize("mode", ["sliding", "block"])
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_backward_parity(eva, case, mode, dtype):
+    B, H, T, d, C, W = case
+    cfg = eva.make_config(B, H, T, d, C, W, mode=mode, dtype=dtype, seed=11)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=3, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, dtype, seed=4, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    dQ, dK, dV = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO)
+    torch.cuda.synchronize()
+    nC = T // C
+    E = oracle.eps_units(cfg.seed, cfg.layer, cfg.bh_begin, cfg.bh_count, nC, d)
+    m = oracle.SLIDING if mode == "sliding" else oracle.BLOCK
+    rq, rk, rv = oracle.backward_batch(f64(Q), f64(K), f64(V), E, f64(dO), C, W, m, cfg.scale)
+    tol = TOL[dtype]
+    _check("dQ", f64(dQ), rq, tol)
+    _check("dK", f64(dK), rk, tol)
+    _check("dV", f64(dV), rv, tol)
+
+
+@pytest.mark.parametrize("omega_mode", [0, 1])
+def test_backward_caller_eps_and_omega_readings(eva, omega_mode):
+    B, H, T, d, C, W = 1, 2, 384, 64, 16, 64
+    cfg = eva.make_config(B, H, T, d, C, W, dtype=torch.float32, omega_mode=omega_mode, seed=1)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.float32, seed=5, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.float32, seed=6, device="cuda")
+    nC = T // C
+    E = eva_inputs.eps(0, B * H, nC, d, seed=8, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, eps=E)
+    dQ, dK, dV = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO, eps=E)
+    torch.cuda.synchronize()
+    om = omega_mode
+    rq, rk, rv = oracle.backward_batch(f64(Q), f64(K), f64(V), f64(E), f64(dO), C, W,
+                                       oracle.SLIDING, cfg.scale, omega_mode=om)
+    _check("dQ", f64(dQ), rq, 1e-4)
+    _check("dK", f64(dK), rk, 1e-4)
+    _check("dV", f64(dV), rv, 1e-4)
+
+
+def test_backward_sharded_equals_unsharded(eva):
+    """A (b, h) shard computes exactly its slice (Philox keyed by the global unit)."""
+    B, H, T, d, C, W = 2, 2, 256, 64, 16, 32
+    full = eva.make_config(B, H, T, d, C, W, dtype=torch.float32, seed=2)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.float32, seed=9, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.float32, seed=10, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(full, Q, K, V)
+    g = eva.eva_attn_backward(full, Q, K, V, ks, vs, O, lse, dO)
+    sh = eva.make_config(B, H, T, d, C, W, dtype=torch.float32, seed=2, bh_begin=1, bh_count=2)
+    sl = slice(1, 3)
+    gs = eva.eva_attn_backward(sh, Q[sl].contiguous(), K[sl].contiguous(), V[sl].contiguous(),
+                               ks[sl].contiguous(), vs[sl].contiguous(), O[sl].contiguous(),
+                               lse[sl].contiguous(), dO[sl].contiguous())
+    torch.cuda.synchronize()
+    for a, b in zip(g, gs):
+        assert torch.allclose(a[sl], b, rtol=0, atol=1e-5)
+
+
+def test_backward_workspace_reuse_is_stateless(eva):
+    """A dirty workspace gives the same result (the kernels initialise what they accumulate)."""
+    B, H, T, d, C, W = 1, 2, 200, 32, 8, 16
+    cfg = eva.make_config(B, H, T, d, C, W, dtype=torch.float32, seed=4)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.float32, seed=12, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.float32, seed=13, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    ws = torch.full((eva.eva_backward_workspace_bytes(cfg),), 0x7F, dtype=torch.uint8, device="cuda")
+    a = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO, workspace=ws)
+    a = [t.clone() for t in a]
+    b = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO, workspace=ws)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert torch.allclose(x, y, rtol=0, atol=1e-6)
+    with pytest.raises(eva.EvaError):
+        eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO, workspace=ws[:1024])
+
+
+@pytest.mark.parametrize("B,H,T,d,C,W", [(1, 4, 4096, 128, 64, 256), (2, 2, 2048, 64, 64, 128)])
+def test_backward_full_size_family(eva, B, H, T, d, C, W):
+    """configs[1]/[2] head dims and chunking at T in the thousands, bf16 through the
+    tensor-core forward, all elements against the oracle."""
+    cfg = eva.make_config(B, H, T, d, C, W, dtype=torch.bfloat16, seed=21)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=22, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.bfloat16, seed=23, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    dQ, dK, dV = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO)
+    torch.cuda.synchronize()
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, T // C, d)
+    rq, rk, rv = oracle.backward_batch(f64(Q), f64(K), f64(V), E, f64(dO), C, W, oracle.SLIDING,
+                                       cfg.scale)
+    _check("dQ", f64(dQ), rq, 2e-2)
+    _check("dK", f64(dK), rk, 2e-2)
+    _check("dV", f64(dV), rv, 2e-2)

@@ -125,3 +125,31 @@ def test_product_package_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "eva_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_backward_workspace_and_validation(N):
+    cfg = _cfg(N)  # bh 2, T 64, d 32, C 8 -> nC 8
+    ws = N.lib.eva_backward_workspace_bytes(ctypes.byref(cfg))
+
+    def a256(x):
+        return (x + 255) // 256 * 256
+    # fp32: D [bh,T], dQ/dK/dV [bh,T,d], d k~ / d beta [bh,nC,d]
+    assert ws == a256(2 * 64 * 4) + 3 * a256(2 * 64 * 32 * 4) + 2 * a256(2 * 8 * 32 * 4)
+    args = [FAKE] * 13  # Q K V Ksum Vsum O lse dO eps dQ dK dV workspace
+    bw = N.lib.eva_attn_backward
+    # a NULL gradient output is rejected with its name
+    a = list(args)
+    a[10] = None  # dK
+    assert bw(ctypes.byref(cfg), *a, ws, None) == N.EVA_ERR_INVALID_ARG
+    assert b"dK" in N.lib.eva_last_error()
+    # too small a workspace
+    assert bw(ctypes.byref(cfg), *args, ws - 1, None) == N.EVA_ERR_INVALID_ARG
+    assert b"workspace_bytes" in N.lib.eva_last_error()
+    # a workspace that is 16- but not 256-byte aligned
+    a = list(args)
+    a[12] = ctypes.c_void_p(0x10010)
+    assert bw(ctypes.byref(cfg), *a, ws, None) == N.EVA_ERR_INVALID_ARG
+    assert b"256-byte" in N.lib.eva_last_error()
+    bad = _cfg(N, samples=2)
+    assert bw(ctypes.byref(bad), *args, ws, None) == N.EVA_ERR_UNSUPPORTED
+    assert N.lib.eva_backward_workspace_bytes(ctypes.byref(bad)) == 0
