@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/eva.h"
 
 namespace eva {
@@ -144,6 +146,35 @@ __device__ __forceinline__ float omega_of(float kt, float e, const eva_config& c
   if (cfg.omega_mode == EVA_OMEGA_AS_PRINTED)
     return cfg.lambda * fminf(fmaxf(kt + e, -cfg.clip), cfg.clip);
   return kt + cfg.lambda * fminf(fmaxf(e, -cfg.clip), cfg.clip);
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels of the hot path are launched with programmatic stream serialisation: the next
+// kernel on the stream may be scheduled as soon as every CTA of this one has executed
+// pdl_trigger(), and it runs its prologue (barrier init, TMEM alloc, descriptor prefetch)
+// while this one drains.  pdl_wait() blocks until the previous grid has COMPLETED and its
+// memory is visible, so every kernel calls it before its first global-memory access --
+// the overlap is launch latency and prologue only, never data.  Both are no-ops when the
+// launch carried no programmatic dependency.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...);
 }
 
 // Launch counter (eva_launch_count): incremented on the host per enqueue.

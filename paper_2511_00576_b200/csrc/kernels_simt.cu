@@ -199,6 +199,8 @@ __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, cons
                                                            const T* __restrict__ V,
                                                            const float* __restrict__ eps,
                                                            T* __restrict__ Ksum, T* __restrict__ Vsum) {
+  pdl_wait();
+  pdl_trigger();
   const int C = cfg.chunk, nC = cfg.T / C;
   const int c = blockIdx.x, u = blockIdx.y;
   const T* Kc = K + ((size_t)u * cfg.T + (size_t)c * C) * D;
@@ -397,6 +399,8 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   static_assert(TPR >= 1 && TPR <= 32 && 32 % TPR == 0, "bad D/VEC");
   __shared__ float sm_m[NW], sm_l[NW];
   __shared__ float sm_acc[NW][D];
+  pdl_wait();
+  pdl_trigger();
   const int u = blockIdx.x, S = S_, s = blockIdx.y;
   const int W = c.cfg.window, C = c.cfg.chunk;
   const int64_t n = c.pos - 1;
@@ -581,6 +585,8 @@ __global__ void __launch_bounds__(256) cache_load_kernel(eva_cache c, const T* _
                                                          const T* __restrict__ V,
                                                          const T* __restrict__ Ksum,
                                                          const T* __restrict__ Vsum, int n, int nC) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int PPR = D * (int)sizeof(T) / 16;
   const int W = c.cfg.window;
   const int keep = min(n, W);
@@ -692,13 +698,14 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
     if (ni <= 16) {
       const dim3 grid(nC, cfg.bh_count);
       if (ni <= 2)
-        summarize_reg_kernel<T, D, 2><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+        err = launch_pdl(summarize_reg_kernel<T, D, 2>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
       else if (ni <= 4)
-        summarize_reg_kernel<T, D, 4><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+        err = launch_pdl(summarize_reg_kernel<T, D, 4>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
       else if (ni <= 8)
-        summarize_reg_kernel<T, D, 8><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+        err = launch_pdl(summarize_reg_kernel<T, D, 8>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
       else
-        summarize_reg_kernel<T, D, 16><<<grid, 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+        err = launch_pdl(summarize_reg_kernel<T, D, 16>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+      if (err != cudaSuccess) return err;
     } else if (sm <= kSummSmemMax) {
       err = set_smem_attr((const void*)summarize_cta_kernel<T, D>, sm);
       if (err != cudaSuccess) return err;
@@ -786,7 +793,9 @@ cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse
   if (c.cfg.bh_count == 0) return cudaSuccess;
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     dim3 grid(c.cfg.bh_count, splits);
-    decode_kernel<T, D><<<grid, 128, 0, s>>>(c, (const T*)Q, (T*)O, lse, ws, splits);
+    cudaError_t e = launch_pdl(decode_kernel<T, D, false>, grid, dim3(128), 0, s, c, (const T*)Q, (T*)O, lse, ws,
+                               splits, (const T*)nullptr, (const T*)nullptr);
+    if (e != cudaSuccess) return e;
     note_launch();
   }));
   return cudaGetLastError();
@@ -799,8 +808,9 @@ cudaError_t launch_cache_load(const eva_cache& c, const void* K, const void* V, 
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     constexpr int PPR = D * (int)sizeof(T) / 16;
     const int64_t pieces = (int64_t)c.cfg.bh_count * (std::min(n, c.cfg.window) + nC) * PPR;
-    cache_load_kernel<T, D><<<(unsigned)((pieces + 255) / 256), 256, 0, s>>>(
-        c, (const T*)K, (const T*)V, (const T*)Ksum, (const T*)Vsum, n, nC);
+    cudaError_t e = launch_pdl(cache_load_kernel<T, D>, dim3((unsigned)((pieces + 255) / 256)), dim3(256), 0, s,
+                               c, (const T*)K, (const T*)V, (const T*)Ksum, (const T*)Vsum, n, nC);
+    if (e != cudaSuccess) return e;
     note_launch();
   }));
   return cudaGetLastError();
@@ -811,8 +821,9 @@ cudaError_t launch_decode_step(const eva_cache& c_after, const void* Q, const vo
   if (c_after.cfg.bh_count == 0) return cudaSuccess;
   EVA_DISPATCH_T(c_after.cfg.dtype, EVA_DISPATCH_D(c_after.cfg.d_head, {
     dim3 grid(c_after.cfg.bh_count, splits);
-    decode_kernel<T, D, true><<<grid, 128, 0, s>>>(c_after, (const T*)Q, (T*)O, lse, ws, splits,
-                                                   (const T*)Kn, (const T*)Vn);
+    cudaError_t e = launch_pdl(decode_kernel<T, D, true>, grid, dim3(128), 0, s, c_after, (const T*)Q, (T*)O, lse,
+                               ws, splits, (const T*)Kn, (const T*)Vn);
+    if (e != cudaSuccess) return e;
     note_launch();
   }));
   return cudaGetLastError();

@@ -216,6 +216,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
+  pdl_wait();  // inputs of the previous kernel (summaries) are complete from here on
+  pdl_trigger();
   if (threadIdx.x == 0) tt<TRACE>(tl, 0, 1, 0);
 
   // Producer and MMA roles run on whole warps (warp-uniform control flow keeps every
@@ -1395,8 +1397,9 @@ cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const 
   }
   dim3 grid((T + BM - 1) / BM, BH);
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  prefill_sm100_kernel<D, NSTAGE, TRACE><<<grid, NTHREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, mO, T, cfg.chunk,
-                                                               cfg.window, cfg.mode, scale_log2, lse);
+  cudaError_t e = launch_pdl(prefill_sm100_kernel<D, NSTAGE, TRACE>, grid, dim3(NTHREADS), smem, s, mQ, mK, mV,
+                             mKs, mVs, mO, T, cfg.chunk, cfg.window, cfg.mode, scale_log2, lse);
+  if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
 }
