@@ -12,9 +12,11 @@
  * Conventions shared by every entry point
  * ---------------------------------------
  *  - All tensor pointers are DEVICE pointers (cudaMalloc / torch CUDA memory)
- *    owned by the caller.  The library allocates no device memory and keeps
- *    no global state except a thread-local error string and a cache of the
- *    device attributes it queried.
+ *    owned by the caller, except the h* arguments of eva_attn_prefill_host
+ *    (host memory).  The library allocates no device memory and keeps no
+ *    global state except a thread-local error string and a cache of the
+ *    device attributes it queried; the streams and events of the host-copy
+ *    pipeline live in an explicit eva_pipeline object.
  *  - Layout: row-major, contiguous.  A "unit" is one (batch, head) pair with
  *    global flattened index u = b*H + h.  Per-unit tensors are [units, rows, d].
  *    Every call works on units [bh_begin, bh_begin + bh_count): tensor
@@ -205,6 +207,39 @@ size_t eva_decode_workspace_bytes(const eva_cache* cache);
 eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, const void* V_new,
                            const float* eps, void* O, float* lse, void* workspace,
                            size_t workspace_bytes, eva_stream_t stream);
+
+/* ---------------------------------------------------------------- host-buffer prefill
+ * eva_attn_prefill_host: eva_attn_prefill on inputs and outputs in HOST memory, with the
+ * host<->device copies overlapped with the kernels (the end-to-end path of a caller whose
+ * prompt is on the host).  The units [0, bh_count) are cut into n_slices contiguous slices
+ * (each unit's summaries and attention depend on that unit only, P:101 S = 1, so slices
+ * are independent); on three streams
+ *     copy-in  : H2D of slice i's Q, K, V                     (pipe's h2d stream)
+ *     compute  : eva_attn_prefill(slice i, flags)             (`stream`)
+ *     copy-out : D2H of slice i's O (and lse)                 (pipe's d2h stream)
+ * so slice i's H2D overlaps slice i-1's kernels and slice i-2's D2H.  Both side streams
+ * fork from and join back into `stream` (the call is stream-ordered and CUDA-graph
+ * capturable).  Results are bitwise equal to one eva_attn_prefill over all units.
+ * hQ, hK, hV : host [bh_count, T, d] cfg.dtype (pinned for true asynchrony; pageable
+ *              memory works but serialises the copies)
+ * hO         : host [bh_count, T, d] cfg.dtype (out);  hlse : host [bh_count, T] fp32 or NULL
+ * dQ, dK, dV, dO : device staging [bh_count, T, d] cfg.dtype, caller-owned; on completion
+ *              dK, dV hold the prompt (for eva_cache_load) and dO the output
+ * dKsum, dVsum : device [bh_count, nC, d] (out: the summaries, for eva_cache_load)
+ * dlse       : device [bh_count, T] fp32, required when hlse != NULL, else may be NULL
+ * eps, flags : as in eva_attn_prefill (EVA_SUMMARIES_PROVIDED is rejected: summaries are
+ *              always computed here from the copied K, V)
+ * n_slices   : 1 .. eva_pipeline max_slices (clamped to bh_count)
+ * The host buffers must stay valid until `stream` reaches the end of the call. */
+typedef struct eva_pipeline eva_pipeline;
+/* Creates the two side streams and 2*max_slices+2 events the copy pipeline uses. */
+eva_status eva_pipeline_create(int32_t max_slices, eva_pipeline** out);
+void eva_pipeline_destroy(eva_pipeline* pipe);
+eva_status eva_attn_prefill_host(eva_pipeline* pipe, const eva_config* cfg, const void* hQ,
+                                 const void* hK, const void* hV, void* hO, float* hlse, void* dQ,
+                                 void* dK, void* dV, void* dKsum, void* dVsum, void* dO, float* dlse,
+                                 const float* eps, uint32_t flags, int32_t n_slices,
+                                 eva_stream_t stream);
 
 /* ---------------------------------------------------------------- backward (training)
  * eva_attn_backward: gradient of the prefill (the paper

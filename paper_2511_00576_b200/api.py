@@ -18,7 +18,7 @@ from ._native import EvaCache, EvaConfig, EvaError, check, lib
 __all__ = ["make_config", "eva_summarize", "eva_attn_prefill", "eva_cache_append", "eva_cache_load",
            "eva_attn_decode", "DecodeCache", "eva_mask_ranges", "eva_philox", "eva_draw_eps",
            "EvaConfig", "EvaError", "launch_count", "version", "eva_attn_backward",
-           "eva_backward_workspace_bytes"]
+           "eva_backward_workspace_bytes", "HostPrefill", "eva_attn_prefill_host"]
 
 _DT = {torch.float32: N.EVA_F32, torch.bfloat16: N.EVA_BF16}
 _MODE = {"sliding": N.EVA_WINDOW_SLIDING, "block": N.EVA_WINDOW_BLOCK}
@@ -131,6 +131,59 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
                                _ptr(eps), _ptr(O), _ptr(lse if want_lse else None), flags,
                                _stream(Q.device)))
     return O, (lse if want_lse else None), Ksum, Vsum
+
+
+class HostPrefill:
+    """eva_attn_prefill_host with its pipeline (2 side streams + events) and the device
+    staging buffers it copies through (torch-owned, reused across calls).
+
+    After a call, .Q/.K/.V/.O/.Ksum/.Vsum are the device copies (for eva_cache_load)."""
+
+    def __init__(self, cfg: EvaConfig, max_slices: int = 8, device="cuda", want_lse: bool = False):
+        dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+        nC = T // cfg.chunk
+        self.cfg, self.device = cfg, torch.device(device)
+        self.Q, self.K, self.V, self.O = (torch.empty(bh, T, d, dtype=dt, device=device) for _ in range(4))
+        self.Ksum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=device)[:, :nC]
+        self.Vsum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=device)[:, :nC]
+        self.lse = torch.empty(bh, T, dtype=torch.float32, device=device) if want_lse else None
+        self.max_slices = max_slices
+        h = ctypes.c_void_p()
+        check(lib.eva_pipeline_create(max_slices, ctypes.byref(h)))
+        self._pipe = h
+
+    def __del__(self):
+        if getattr(self, "_pipe", None) is not None and self._pipe.value:
+            lib.eva_pipeline_destroy(self._pipe)
+            self._pipe = None
+
+    def __call__(self, hQ: torch.Tensor, hK: torch.Tensor, hV: torch.Tensor, hO: torch.Tensor,
+                 hlse: Optional[torch.Tensor] = None, eps: Optional[torch.Tensor] = None,
+                 n_slices: Optional[int] = None, kernel: Optional[str] = None):
+        cfg = self.cfg
+        dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+        for t, nm in ((hQ, "hQ"), (hK, "hK"), (hV, "hV"), (hO, "hO")):
+            if t.is_cuda or not t.is_contiguous() or t.dtype != dt or tuple(t.shape) != (bh, T, d):
+                raise ValueError(f"{nm} must be a contiguous host tensor [{bh}, {T}, {d}] of {dt}")
+        if hlse is not None:
+            if self.lse is None:
+                raise ValueError("HostPrefill(want_lse=True) is needed for hlse")
+            if hlse.is_cuda or tuple(hlse.shape) != (bh, T) or hlse.dtype != torch.float32:
+                raise ValueError("hlse must be a host fp32 tensor [bh, T]")
+        if eps is not None:
+            _need(eps, "eps", (bh, T // cfg.chunk, d), torch.float32)
+        flags = {None: 0, "simt": N.EVA_PREFILL_SIMT, "tile": N.EVA_PREFILL_TC_TILE}[kernel]
+        check(lib.eva_attn_prefill_host(self._pipe, ctypes.byref(cfg), _ptr(hQ), _ptr(hK), _ptr(hV),
+                                        _ptr(hO), _ptr(hlse), _ptr(self.Q), _ptr(self.K), _ptr(self.V),
+                                        _ptr(self.Ksum), _ptr(self.Vsum), _ptr(self.O), _ptr(self.lse),
+                                        _ptr(eps), flags, n_slices or self.max_slices,
+                                        _stream(self.device)))
+        return hO
+
+
+def eva_attn_prefill_host(cfg: EvaConfig, hQ, hK, hV, hO, **kw):
+    """One-shot eva_attn_prefill_host (allocates a HostPrefill; keep one for repeated calls)."""
+    return HostPrefill(cfg, device=kw.pop("device", "cuda"))(hQ, hK, hV, hO, **kw)
 
 
 def eva_backward_workspace_bytes(cfg: EvaConfig) -> int:

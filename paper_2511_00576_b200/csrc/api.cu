@@ -7,6 +7,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "../../include/eva.h"
 #include "../../include/eva_debug.h"
@@ -297,6 +299,138 @@ eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, c
   if (e != cudaSuccess) return cuda_status(e, "eva_decode_step");
   cache->pos += 1;
   return ok();
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ host-copy pipeline
+struct eva_pipeline {
+  int max_slices = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  std::vector<cudaEvent_t> in, done;  // per slice: H2D complete, kernels complete
+};
+
+namespace {
+void pipeline_free(eva_pipeline* p) {
+  if (!p) return;
+  for (cudaEvent_t e : p->in) if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->done) if (e) cudaEventDestroy(e);
+  if (p->fork) cudaEventDestroy(p->fork);
+  if (p->join) cudaEventDestroy(p->join);
+  if (p->h2d) cudaStreamDestroy(p->h2d);
+  if (p->d2h) cudaStreamDestroy(p->d2h);
+  delete p;
+}
+}  // namespace
+
+extern "C" {
+
+eva_status eva_pipeline_create(int32_t max_slices, eva_pipeline** out) {
+  if (!out) return fail(EVA_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (max_slices < 1 || max_slices > 4096) return fail(EVA_ERR_INVALID_ARG, "max_slices=%d", max_slices);
+  eva_pipeline* p = new eva_pipeline;
+  p->max_slices = max_slices;
+  p->in.assign(max_slices, nullptr);
+  p->done.assign(max_slices, nullptr);
+  cudaError_t e = cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->join, cudaEventDisableTiming);
+  for (int i = 0; i < max_slices && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&p->in[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->done[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    pipeline_free(p);
+    return cuda_status(e, "eva_pipeline_create");
+  }
+  *out = p;
+  return ok();
+}
+
+void eva_pipeline_destroy(eva_pipeline* pipe) { pipeline_free(pipe); }
+
+eva_status eva_attn_prefill_host(eva_pipeline* pipe, const eva_config* cfg, const void* hQ,
+                                 const void* hK, const void* hV, void* hO, float* hlse, void* dQ,
+                                 void* dK, void* dV, void* dKsum, void* dVsum, void* dO, float* dlse,
+                                 const float* eps, uint32_t flags, int32_t n_slices,
+                                 eva_stream_t stream) {
+  if (!pipe) return fail(EVA_ERR_INVALID_ARG, "pipe is NULL");
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (flags & EVA_SUMMARIES_PROVIDED)
+    return fail(EVA_ERR_INVALID_ARG, "eva_attn_prefill_host always computes the summaries");
+  if (n_slices < 1 || n_slices > pipe->max_slices)
+    return fail(EVA_ERR_INVALID_ARG, "n_slices=%d outside [1, %d]", n_slices, pipe->max_slices);
+  if (cfg->bh_count == 0) return ok();
+  const void* hp[] = {hQ, hK, hV, hO};
+  const char* hn[] = {"hQ", "hK", "hV", "hO"};
+  for (int i = 0; i < 4; ++i)
+    if (!hp[i]) return fail(EVA_ERR_INVALID_ARG, "%s is NULL", hn[i]);
+  if (hlse && !dlse) return fail(EVA_ERR_INVALID_ARG, "hlse needs the device staging dlse");
+  const int units = cfg->bh_count;
+  const int ns = std::min(n_slices, units);
+  const int per = (units + ns - 1) / ns;
+  const size_t elem = cfg->dtype == EVA_BF16 ? 2 : 4;
+  const size_t row_b = (size_t)cfg->T * cfg->d_head * elem;             // one unit of Q/K/V/O
+  const size_t sum_b = (size_t)(cfg->T / cfg->chunk) * cfg->d_head * elem;  // one unit of Ksum
+  const size_t lse_b = (size_t)cfg->T * sizeof(float);
+  // Validate every slice before enqueueing anything (nothing is enqueued on error).
+  for (int u0 = 0; u0 < units; u0 += per) {
+    eva_config sub = *cfg;
+    sub.bh_begin = cfg->bh_begin + u0;
+    sub.bh_count = std::min(per, units - u0);
+    const void* p[] = {(char*)dQ + u0 * row_b, (char*)dK + u0 * row_b, (char*)dV + u0 * row_b,
+                       (char*)dO + u0 * row_b};
+    const char* nm[] = {"dQ", "dK", "dV", "dO"};
+    if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+    if (sum_b) {
+      const void* p2[] = {(char*)dKsum + u0 * sum_b, (char*)dVsum + u0 * sum_b};
+      const char* nm2[] = {"dKsum", "dVsum"};
+      if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+    }
+    if (dlse && !aligned16((char*)dlse + u0 * lse_b))
+      return fail(EVA_ERR_INVALID_ARG, "dlse slice is not 16-byte aligned");
+  }
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t eps_b = (size_t)(cfg->T / cfg->chunk) * cfg->d_head * sizeof(float);
+  cudaError_t e = cudaEventRecord(pipe->fork, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(pipe->h2d, pipe->fork, 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(pipe->d2h, pipe->fork, 0);
+  if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill_host(fork)");
+  int i = 0;
+  for (int u0 = 0; u0 < units; u0 += per, ++i) {
+    const int cnt = std::min(per, units - u0);
+    const size_t off = u0 * row_b, nb = cnt * row_b;
+    e = cudaMemcpyAsync((char*)dQ + off, (const char*)hQ + off, nb, cudaMemcpyHostToDevice, pipe->h2d);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((char*)dK + off, (const char*)hK + off, nb, cudaMemcpyHostToDevice, pipe->h2d);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((char*)dV + off, (const char*)hV + off, nb, cudaMemcpyHostToDevice, pipe->h2d);
+    if (e == cudaSuccess) e = cudaEventRecord(pipe->in[i], pipe->h2d);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, pipe->in[i], 0);
+    if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill_host(h2d)");
+    eva_config sub = *cfg;
+    sub.bh_begin = cfg->bh_begin + u0;
+    sub.bh_count = cnt;
+    st = eva_attn_prefill(&sub, (char*)dQ + off, (char*)dK + off, (char*)dV + off,
+                          (char*)dKsum + u0 * sum_b, (char*)dVsum + u0 * sum_b,
+                          eps ? (const float*)((const char*)eps + u0 * eps_b) : nullptr,
+                          (char*)dO + off, dlse ? (float*)((char*)dlse + u0 * lse_b) : nullptr, flags,
+                          stream);
+    if (st != EVA_OK) return st;
+    e = cudaEventRecord(pipe->done[i], s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(pipe->d2h, pipe->done[i], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync((char*)hO + off, (char*)dO + off, nb, cudaMemcpyDeviceToHost, pipe->d2h);
+    if (e == cudaSuccess && hlse)
+      e = cudaMemcpyAsync((char*)hlse + u0 * lse_b, (char*)dlse + u0 * lse_b, cnt * lse_b,
+                          cudaMemcpyDeviceToHost, pipe->d2h);
+    if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill_host(d2h)");
+  }
+  e = cudaEventRecord(pipe->join, pipe->d2h);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, pipe->join, 0);
+  return cuda_status(e, "eva_attn_prefill_host(join)");
 }
 
 size_t eva_backward_workspace_bytes(const eva_config* cfg) {

@@ -153,3 +153,16 @@ def test_backward_workspace_and_validation(N):
     bad = _cfg(N, samples=2)
     assert bw(ctypes.byref(bad), *args, ws, None) == N.EVA_ERR_UNSUPPORTED
     assert N.lib.eva_backward_workspace_bytes(ctypes.byref(bad)) == 0
+
+
+def test_host_pipeline_validation(N):
+    """eva_pipeline_create / eva_attn_prefill_host argument checks (synchronous, no launch)."""
+    h = ctypes.c_void_p()
+    assert N.lib.eva_pipeline_create(0, ctypes.byref(h)) == N.EVA_ERR_INVALID_ARG
+    cfg = N.EvaConfig()
+    N.lib.eva_config_default(ctypes.byref(cfg), 1, 2, 64, 64, 16, 32)
+    buf = (ctypes.c_uint8 * 64)()
+    P = ctypes.cast(buf, ctypes.c_void_p)
+    args = [P] * 4 + [None] + [P] * 6 + [None, None]
+    assert N.lib.eva_attn_prefill_host(None, ctypes.byref(cfg), *args, 0, 1, None) == N.EVA_ERR_INVALID_ARG
+    assert b"pipe" in N.lib.eva_last_error()

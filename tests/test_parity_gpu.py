@@ -241,6 +241,27 @@ def test_sharded_equals_unsharded(eva, dtype, simt, kernel):
         assert torch.equal(ks2, ks[b0:b0 + cnt]) and torch.equal(vs2, vs[b0:b0 + cnt])
 
 
+@pytest.mark.parametrize("dtype,kernel,n_slices", [(torch.bfloat16, None, 1), (torch.bfloat16, None, 4),
+                                                    (torch.bfloat16, None, 7), (torch.float32, "simt", 3)])
+def test_prefill_host_pipeline_equals_device_call(eva, dtype, kernel, n_slices):
+    """eva_attn_prefill_host (H2D / kernels / D2H pipelined over unit slices) is bitwise
+    equal to one eva_attn_prefill over all units, and leaves the device copies in place."""
+    B, H, T, d, C, W = 2, 3, 320, 64, 32, 64
+    cfg = eva.make_config(B, H, T, d, C, W, bh_begin=0, dtype=dtype)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=12, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, simt=kernel == "simt")
+    hQ, hK, hV = (x.cpu().pin_memory() for x in (Q, K, V))
+    hO = torch.full((B * H, T, d), float("nan"), dtype=dtype).pin_memory()
+    hl = torch.full((B * H, T), float("nan")).pin_memory()
+    hp = eva.HostPrefill(cfg, max_slices=8, device="cuda", want_lse=True)
+    hp(hQ, hK, hV, hO, hlse=hl, n_slices=n_slices, kernel=kernel)
+    torch.cuda.synchronize()
+    assert torch.equal(hO, O.cpu()) and torch.equal(hl, lse.cpu())
+    assert torch.equal(hp.Ksum, ks) and torch.equal(hp.Vsum, vs) and torch.equal(hp.K, K)
+    with pytest.raises(eva.EvaError, match="INVALID_ARG"):
+        hp(hQ, hK, hV, hO, n_slices=9)
+
+
 def test_errors_are_reported_not_silent(eva):
     cfg = eva.make_config(1, 1, 64, 64, 16, 40)  # W % C != 0
     Q = torch.zeros(1, 64, 64, dtype=torch.bfloat16, device="cuda")
