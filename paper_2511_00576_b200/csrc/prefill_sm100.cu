@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -130,6 +131,114 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
   tc_fence_before();
 }
 
+// ---- packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two lanes per issue slot)
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ float f2lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float f2hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x for x <= 0 on the FMA/ALU pipes (the MUFU pipe does 16 ex2 per clock per SM, a quarter of
+// what the softmax would need to keep pace with the tensor core at d = 64): x = n + f with
+// n = rint(x) via the 1.5*2^23 shifter, 2^f on [-1/2, 1/2] by a degree-3 polynomial (relative
+// error 7.5e-5, far below the bf16 rounding of P), and n added to the exponent field.  x is
+// clamped at -126 so that -inf (masked columns) gives a value below 2^-125 instead of garbage.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
+  const float lo = fmaxf(f2lo(x), -126.f), hi = fmaxf(f2hi(x), -126.f);
+  const uint64_t xc = f2pack(lo, hi);
+  const uint64_t SH = f2pack(12582912.f, 12582912.f), NSH = f2pack(-12582912.f, -12582912.f);
+  const uint64_t j = fadd2(xc, SH);                    // low mantissa bits hold rint(x)
+  const uint64_t f = ffma2(fadd2(j, NSH), f2pack(-1.f, -1.f), xc);  // x - rint(x), exact
+  uint64_t p = ffma2(f2pack(0.055171627551317215f, 0.055171627551317215f), f,
+                     f2pack(0.24261116981506348f, 0.24261116981506348f));
+  p = ffma2(p, f, f2pack(0.6932610273361206f, 0.6932610273361206f));
+  p = ffma2(p, f, f2pack(0.9999280571937561f, 0.9999280571937561f));
+  const uint32_t rlo = (uint32_t)p + ((uint32_t)j << 23);
+  const uint32_t rhi = (uint32_t)(p >> 32) + ((uint32_t)(j >> 32) << 23);
+  return (uint64_t)rlo | ((uint64_t)rhi << 32);
+}
+
+// softmax_tile with packed fp32x2 arithmetic and EMU of every 8 column pairs exponentiated by
+// exp2_poly2 instead of MUFU.EX2 (FA4-style split of the exponentials between the MUFU and
+// FMA pipes).  Same contract and results up to the exp2 approximation (both are far below
+// the bf16 rounding of P).
+template <int D, int EMU, typename WaitO>
+__device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, int vlo, int vhi,
+                                              float scale_log2, float& m_ref, float& l,
+                                              const WaitO& wait_o) {
+  uint32_t sr[64];
+  tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+  tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+  tmem_wait_ld();
+  const bool full = vlo <= 0 && vhi >= 64;
+  if (!__all_sync(0xffffffffu, full)) {
+#pragma unroll
+    for (int c = 0; c < 64; ++c)
+      if (c < vlo || c >= vhi) sr[c] = 0xff800000u;  // -inf
+  }
+  float pm[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) pm[i] = __uint_as_float(sr[i]);
+#pragma unroll
+  for (int c = 8; c < 64; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sr[c]));
+  float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+  mx *= scale_log2;
+  const bool grow = mx > m_ref + 8.0f;
+  if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
+    const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
+    wait_o();
+    tc_fence_after();
+    const uint64_t f2 = f2pack(f, f);
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(o_addr + cc * 32, o);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const uint64_t v = ffma2(f2pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), f2, 0ull);
+        o[i] = (uint32_t)v;
+        o[i + 1] = (uint32_t)(v >> 32);
+      }
+      tmem_st32(o_addr + cc * 32, o);
+    }
+    tmem_wait_st();
+    l *= f;
+  }
+  if (grow) m_ref = mx;
+  const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
+  const uint64_t sc2 = f2pack(scale_log2, scale_log2), ng2 = f2pack(neg, neg);
+  uint32_t pk[32];
+  uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const uint64_t x = ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2, ng2);
+    uint64_t p;
+    if ((c & 7) < EMU) {
+      p = exp2_poly2(x);
+    } else {
+      p = f2pack(ex2(f2lo(x)), ex2(f2hi(x)));
+    }
+    ls[c & 3] = fadd2(ls[c & 3], p);
+    pk[c] = pack_bf16(f2lo(p), f2hi(p));
+  }
+  const uint64_t s2 = fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3]));
+  l += f2lo(s2) + f2hi(s2);
+  tmem_st32(s_addr, pk);
+  tmem_wait_st();
+  tc_fence_before();
+}
+
 struct TilePlan {
   int n0, nlast, n_st, n_lt, lo0;
   __device__ TilePlan(int qt, int T, int C, int W, int mode) {
@@ -173,7 +282,7 @@ __device__ __forceinline__ void tt(TileTrace* tl, int role, int kind, int j) {
   }
 }
 
-template <int D, int NSTAGE, bool TRACE = false>
+template <int D, int NSTAGE, bool TRACE = false, int SMX = -1>
 __global__ void __launch_bounds__(NTHREADS, 2)
 prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
@@ -228,8 +337,12 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
       for (int kb = 0; kb < D / 64; ++kb)
         tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
+    }
+    __syncwarp();
+    auto prefetch_rest = [&] {
       // The ring holds only NSTAGE tiles; pull every later K/V tile of this CTA into L2 now
       // so its TMA load later on is an L2 hit instead of a full DRAM round trip.
+      if (elect_one()) {
       for (int j = NSTAGE; j < NT; ++j) {
         const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
         const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
@@ -238,8 +351,9 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
           tma_prefetch_l2_3d(mv, kb * 64, plan.base(j), u);
         }
       }
-    }
-    __syncwarp();
+      }
+      __syncwarp();
+    };
     // Issue order K(0), K(1), V(0), K(2), V(1), ...: K(j+1) waits only for S(j+1-NSTAGE)
     // to finish reading its slot, V(j) for PV(j-NSTAGE).
     auto load_k = [&](int j) {
@@ -267,7 +381,10 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       __syncwarp();
     };
     load_k(0);
-    for (int j = 0; j < NT; ++j) {
+    if (NT > 1) load_k(1);
+    load_v(0);
+    prefetch_rest();  // after the first tiles: they are on the critical path
+    for (int j = 1; j < NT; ++j) {
       if (j + 1 < NT) load_k(j + 1);
       load_v(j);
     }
@@ -346,8 +463,12 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         vhi = min(BN, n - base + 1);
       }
       if (!valid) vhi = vlo;
-      softmax_tile<D>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
-                      [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
+      if constexpr (SMX < 0)
+        softmax_tile<D>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
+                        [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
+      else
+        softmax_tile2<D, SMX>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
+                              [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
       mbar_arrive(&sm->p_full[j & 1]);
       if (tw) tt<TRACE>(tl, 2, 8, j);
     }
@@ -466,6 +587,10 @@ prefill_split_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
       for (int kb = 0; kb < D / 64; ++kb)
         tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
+    }
+    __syncwarp();
+    auto prefetch_rest = [&] {
+      if (elect_one()) {
       for (int j = NSTAGE; j < NT; ++j) {
         const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
         const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
@@ -474,8 +599,9 @@ prefill_split_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
           tma_prefetch_l2_3d(mv, kb * 64, plan.base(j), u);
         }
       }
-    }
-    __syncwarp();
+      }
+      __syncwarp();
+    };
     auto load_k = [&](int j) {
       const int s = j % NSTAGE;
       if (j >= NSTAGE) mbar_wait(&sm->k_empty[s], ((j / NSTAGE) - 1) & 1);
@@ -499,7 +625,10 @@ prefill_split_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       __syncwarp();
     };
     load_k(0);
-    for (int j = 0; j < NT; ++j) {
+    if (NT > 1) load_k(1);
+    load_v(0);
+    prefetch_rest();  // after the first tiles: they are on the critical path
+    for (int j = 1; j < NT; ++j) {
       if (j + 1 < NT) load_k(j + 1);
       load_v(j);
     }
@@ -1373,9 +1502,29 @@ bool make_map(CUtensorMap* m, const void* base, int units, int rows, int D, int 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int D, int NSTAGE, bool TRACE = false>
+// Softmax exponential split of the tile kernel: -1 = all MUFU.EX2 (softmax_tile), k >= 0 =
+// softmax_tile2 with k of every 8 column pairs on the FMA pipe.  EVA_SOFTMAX_EMU overrides
+// the default (tuning knob, read once).
+int softmax_emu() {
+  static const int v = [] {
+    const char* e = getenv("EVA_SOFTMAX_EMU");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+
+template <int D, int NSTAGE, bool TRACE = false, int SMX = -1>
 cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const void* V,
                      const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
+  if constexpr (!TRACE && SMX == -1) {
+    switch (softmax_emu()) {
+      case 0: return launch_t<D, NSTAGE, false, 0>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+      case 1: return launch_t<D, NSTAGE, false, 1>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+      case 2: return launch_t<D, NSTAGE, false, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+      case 3: return launch_t<D, NSTAGE, false, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+      default: break;
+    }
+  }
   const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
   CUtensorMap mQ, mK, mV, mKs, mVs, mO;
   bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BN) &&
@@ -1390,14 +1539,14 @@ cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const 
   const size_t smem = sizeof(Smem<D, NSTAGE>) + 1024;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_sm100_kernel<D, NSTAGE, TRACE>,
+    cudaError_t e = cudaFuncSetAttribute(prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grid((T + BM - 1) / BM, BH);
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  cudaError_t e = launch_pdl(prefill_sm100_kernel<D, NSTAGE, TRACE>, grid, dim3(NTHREADS), smem, s, mQ, mK, mV,
+  cudaError_t e = launch_pdl(prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>, grid, dim3(NTHREADS), smem, s, mQ, mK, mV,
                              mKs, mVs, mO, T, cfg.chunk, cfg.window, cfg.mode, scale_log2, lse);
   if (e != cudaSuccess) return e;
   note_launch();

@@ -8,7 +8,7 @@ namespace eva { void note_launch(int) {} int num_sms() { return 148; } }
 namespace eva { namespace {
 // MMA load: warp 4 issues PV-shaped TS MMAs (M128 N128 K16, A = TMEM cols [64,96), B = smem,
 // accumulate into TMEM cols [128,256)) back to back while the softmax warps run.
-template <int D, int MMA>
+template <int D, int MMA, int VAR>
 __global__ void __launch_bounds__(160, 2) sm_bench(int iters, int full, unsigned long long* out, float* sink) {
   __shared__ uint32_t tbase;
   __shared__ __align__(1024) uint8_t bsm[16384];
@@ -40,17 +40,28 @@ __global__ void __launch_bounds__(160, 2) sm_bench(int iters, int full, unsigned
   }
   const uint32_t t_lane = tbase + ((uint32_t)(warp * 32) << 16);
   // fill S with small values
-  uint32_t init[32];
-  for (int i = 0; i < 32; ++i) init[i] = __float_as_uint(0.01f * ((i * 7 + lane) % 13));
-  tmem_st32(t_lane, init); tmem_st32(t_lane + 32, init); tmem_wait_st();
+  __shared__ __align__(16) uint32_t init_s[4][32][32];  // [warp][lane][col]: restore source
+  {
+    uint32_t init[32];
+    for (int i = 0; i < 32; ++i) init[i] = __float_as_uint(0.01f * ((i * 7 + lane) % 13));
+    for (int i = 0; i < 32; ++i) init_s[warp][lane][i] = init[i];
+    tmem_st32(t_lane, init); tmem_st32(t_lane + 32, init); tmem_wait_st();
+  }
   float m = -INFINITY, l = 0.f;
   __syncwarp();
   unsigned long long t0 = clock64();
   for (int it = 0; it < iters; ++it) {
     const int vlo = full ? 0 : (lane & 7), vhi = full ? 64 : 60;
-    softmax_tile<D>(t_lane, t_lane + 128, vlo, vhi, 0.18f, m, l, [] {});
+    if constexpr (VAR < 0) softmax_tile<D>(t_lane, t_lane + 128, vlo, vhi, 0.18f, m, l, [] {});
+    else softmax_tile2<D, VAR>(t_lane, t_lane + 128, vlo, vhi, 0.18f, m, l, [] {});
     // restore S (softmax overwrote the first 32 columns with P)
-    tmem_st32(t_lane, init); tmem_wait_st();
+    {
+      uint32_t init[32];
+      const uint4* src = reinterpret_cast<const uint4*>(init_s[warp][lane]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(&init[4 * i]) = src[i];
+      tmem_st32(t_lane, init); tmem_wait_st();
+    }
   }
   unsigned long long t1 = clock64();
   if (lane == 0) out[blockIdx.x * 4 + warp] = t1 - t0;
@@ -63,22 +74,32 @@ __global__ void __launch_bounds__(160, 2) sm_bench(int iters, int full, unsigned
 }
 }}
 
-int main() {
-  unsigned long long* d; float* sink;
-  cudaMalloc(&d, 296 * 4 * 8); cudaMalloc(&sink, 4);
+template <int VAR>
+void run(const char* name, unsigned long long* d, float* sink) {
   for (int mma = 0; mma < 2; ++mma)
   for (int full = 1; full >= 0; --full)
     for (int grid : {148, 296}) {
       const int iters = 2000;
-      if (mma) eva::sm_bench<128, 1><<<grid, 160>>>(iters, full, d, sink);
-      else eva::sm_bench<128, 0><<<grid, 160>>>(iters, full, d, sink);
+      if (mma) eva::sm_bench<128, 1, VAR><<<grid, 160>>>(iters, full, d, sink);
+      else eva::sm_bench<128, 0, VAR><<<grid, 160>>>(iters, full, d, sink);
       cudaError_t e = cudaDeviceSynchronize();
-      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
+      if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
       unsigned long long h[296 * 4];
       cudaMemcpy(h, d, grid * 4 * 8, cudaMemcpyDeviceToHost);
       double s = 0; for (int i = 0; i < grid * 4; ++i) s += h[i];
-      printf("softmax_tile (%s tile) %d CTA/SM%s: %.0f cycles per call (incl. a 32-col TMEM restore)\n",
+      printf("%-22s (%s tile) %d CTA/SM%s: %.0f cycles per call (incl. a 32-col TMEM restore)\n", name,
              full ? "unmasked" : "masked", grid / 148, mma ? " + PV MMA stream" : "", s / (grid * 4) / iters);
     }
+}
+
+int main() {
+  unsigned long long* d; float* sink;
+  cudaMalloc(&d, 296 * 4 * 8); cudaMalloc(&sink, 4);
+  run<-1>("softmax_tile", d, sink);
+  run<0>("softmax_tile2 emu 0/8", d, sink);
+  run<1>("softmax_tile2 emu 1/8", d, sink);
+  run<2>("softmax_tile2 emu 2/8", d, sink);
+  run<3>("softmax_tile2 emu 3/8", d, sink);
+  run<4>("softmax_tile2 emu 4/8", d, sink);
   return 0;
 }
