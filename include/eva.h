@@ -142,6 +142,35 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
                             void* Ksum, void* Vsum, const float* eps, void* O, float* lse,
                             uint32_t flags, eva_stream_t stream);
 
+/* ---------------------------------------------------------------- query-range prefill
+ * The building blocks of a sequence-sharded (context-parallel) prefill (SURVEY §8(f) NEXT
+ * row 2; the paper positions EVA against ring attention): a rank that owns positions
+ * [q0, q1) needs only its own keys/values, a halo of the window before q0, and the chunk
+ * summaries of the whole prefix (summaries are per-chunk, query-independent).
+ *
+ * eva_summarize_range: eva_summarize for rows that start at absolute position chunk0 * C:
+ * K, V : [bh_count, cfg.T, d] with row r = position chunk0*C + r; Ksum, Vsum : [bh_count,
+ * floor(cfg.T / C), d], row c = absolute chunk chunk0 + c (whose random draw it uses; eps,
+ * if given, is [bh_count, floor(cfg.T / C), d] for those chunks).  chunk0 >= 0. */
+eva_status eva_summarize_range(const eva_config* cfg, int32_t chunk0, const void* K, const void* V,
+                               const float* eps, void* Ksum, void* Vsum, eva_stream_t stream);
+
+/* eva_attn_prefill_range: eva_attn_prefill (summaries provided) for the queries at absolute
+ * positions [q0, q0 + n_q) only.
+ * Q, O : [bh_count, n_q, d]        row i = position q0 + i
+ * K, V : [bh_count, n_kv, d]       row r = position k0 + r
+ * Ksum, Vsum : [bh_count, n_sum, d] row c = chunk c (absolute, from 0)
+ * lse : [bh_count, n_q] fp32 or NULL.  cfg.T is not used.
+ * Requires k0 <= lo(q0) (the window of the first query is present: a halo of at most W - 1
+ * rows before q0), k0 + n_kv >= q0 + n_q, and n_sum >= nsum(q0 + n_q - 1); otherwise
+ * EVA_ERR_INVALID_ARG.  flags: 0 or EVA_PREFILL_SIMT.  When q0 is a multiple of 128 the rows
+ * are bitwise equal to the same rows of a whole-sequence eva_attn_prefill (same tiles, same
+ * kernel); otherwise equal up to fp32 summation order. */
+eva_status eva_attn_prefill_range(const eva_config* cfg, int64_t q0, int32_t n_q, int64_t k0,
+                                  int32_t n_kv, const void* Q, const void* K, const void* V,
+                                  const void* Ksum, const void* Vsum, int32_t n_sum, void* O,
+                                  float* lse, uint32_t flags, eva_stream_t stream);
+
 /* ---------------------------------------------------------------- decode cache
  * Compressed decode cache ("cache of (compressed) past
  * context"): a ring of the last W tokens plus one summary per

@@ -18,7 +18,8 @@ from ._native import EvaCache, EvaConfig, EvaError, check, lib
 __all__ = ["make_config", "eva_summarize", "eva_attn_prefill", "eva_cache_append", "eva_cache_load",
            "eva_attn_decode", "DecodeCache", "eva_mask_ranges", "eva_philox", "eva_draw_eps",
            "EvaConfig", "EvaError", "launch_count", "version", "eva_attn_backward",
-           "eva_backward_workspace_bytes", "HostPrefill", "eva_attn_prefill_host"]
+           "eva_backward_workspace_bytes", "HostPrefill", "eva_attn_prefill_host",
+           "eva_summarize_range", "eva_attn_prefill_range"]
 
 _DT = {torch.float32: N.EVA_F32, torch.bfloat16: N.EVA_BF16}
 _MODE = {"sliding": N.EVA_WINDOW_SLIDING, "block": N.EVA_WINDOW_BLOCK}
@@ -131,6 +132,50 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
                                _ptr(eps), _ptr(O), _ptr(lse if want_lse else None), flags,
                                _stream(Q.device)))
     return O, (lse if want_lse else None), Ksum, Vsum
+
+
+def eva_summarize_range(cfg: EvaConfig, chunk0: int, K: torch.Tensor, V: torch.Tensor,
+                        eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
+                        Vsum: Optional[torch.Tensor] = None):
+    """Summaries of the complete chunks of rows that start at absolute chunk `chunk0`
+    (K, V [bh, cfg.T, d]) -> Ksum, Vsum [bh, cfg.T // C, d] for chunks chunk0 + c."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    nC = T // cfg.chunk
+    _need(K, "K", (bh, T, d), dt)
+    _need(V, "V", (bh, T, d), dt)
+    if eps is not None:
+        _need(eps, "eps", (bh, nC, d), torch.float32)
+    Ksum = torch.empty(bh, nC, d, dtype=dt, device=K.device) if Ksum is None else Ksum
+    Vsum = torch.empty(bh, nC, d, dtype=dt, device=K.device) if Vsum is None else Vsum
+    check(lib.eva_summarize_range(ctypes.byref(cfg), chunk0, _ptr(K), _ptr(V), _ptr(eps), _ptr(Ksum),
+                                  _ptr(Vsum), _stream(K.device)))
+    return Ksum, Vsum
+
+
+def eva_attn_prefill_range(cfg: EvaConfig, q0: int, k0: int, Q: torch.Tensor, K: torch.Tensor,
+                           V: torch.Tensor, Ksum: torch.Tensor, Vsum: torch.Tensor, *,
+                           want_lse: bool = True, simt: bool = False,
+                           O: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None):
+    """Prefill of the queries at positions [q0, q0 + Q.shape[1]) given keys/values for
+    positions [k0, k0 + K.shape[1]) and the summaries of chunks [0, Ksum.shape[1]).
+    Returns (O, lse)."""
+    dt, bh, d = _tdtype(cfg), cfg.bh_count, cfg.d_head
+    nq, nkv, ns = Q.shape[1], K.shape[1], Ksum.shape[1]
+    _need(Q, "Q", (bh, nq, d), dt)
+    _need(K, "K", (bh, nkv, d), dt)
+    _need(V, "V", (bh, nkv, d), dt)
+    if ns:
+        _need(Ksum, "Ksum", (bh, ns, d), dt)
+        _need(Vsum, "Vsum", (bh, ns, d), dt)
+    O = torch.empty_like(Q) if O is None else O
+    _need(O, "O", (bh, nq, d), dt)
+    if want_lse and lse is None:
+        lse = torch.empty(bh, nq, dtype=torch.float32, device=Q.device)
+    check(lib.eva_attn_prefill_range(ctypes.byref(cfg), q0, nq, k0, nkv, _ptr(Q), _ptr(K), _ptr(V),
+                                     _ptr(Ksum if ns else None), _ptr(Vsum if ns else None), ns, _ptr(O),
+                                     _ptr(lse if want_lse else None), N.EVA_PREFILL_SIMT if simt else 0,
+                                     _stream(Q.device)))
+    return O, (lse if want_lse else None)
 
 
 class HostPrefill:

@@ -156,9 +156,69 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
                   eva::prefill_sm100_supported(*cfg);
   const uint32_t variant = (flags & EVA_PREFILL_TC_TILE) ? 1u : (flags & EVA_PREFILL_TC_PAIR) ? 2u
                           : (flags & EVA_PREFILL_TC_WIDE) ? 3u : (flags & EVA_PREFILL_TC_SPLIT) ? 4u : 0u;
-  cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, Q, K, V, Ksum, Vsum, O, lse, variant, s)
-                     : eva::launch_prefill_simt(*cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  const eva::PrefillRange rg = eva::full_range(*cfg);
+  cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, variant, s)
+                     : eva::launch_prefill_simt(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cuda_status(e, tc ? "eva_attn_prefill(sm100)" : "eva_attn_prefill(simt)");
+}
+
+eva_status eva_summarize_range(const eva_config* cfg, int32_t chunk0, const void* K, const void* V,
+                               const float* eps, void* Ksum, void* Vsum, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (chunk0 < 0) return fail(EVA_ERR_INVALID_ARG, "chunk0=%d must be >= 0", chunk0);
+  if (cfg->bh_count == 0 || cfg->T / cfg->chunk == 0) return ok();
+  const void* p[] = {K, V, Ksum, Vsum};
+  const char* nm[] = {"K", "V", "Ksum", "Vsum"};
+  if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  return cuda_status(eva::launch_summarize(*cfg, K, V, eps, Ksum, Vsum, (cudaStream_t)stream, chunk0),
+                     "eva_summarize_range");
+}
+
+eva_status eva_attn_prefill_range(const eva_config* cfg, int64_t q0, int32_t n_q, int64_t k0,
+                                  int32_t n_kv, const void* Q, const void* K, const void* V,
+                                  const void* Ksum, const void* Vsum, int32_t n_sum, void* O,
+                                  float* lse, uint32_t flags, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, false);
+  if (st != EVA_OK) return st;
+  if (flags & ~EVA_PREFILL_SIMT) return fail(EVA_ERR_INVALID_ARG, "flags 0x%x: only EVA_PREFILL_SIMT", flags);
+  if (q0 < 0 || n_q < 0 || k0 < 0 || n_kv < 0 || n_sum < 0)
+    return fail(EVA_ERR_INVALID_ARG, "q0=%lld n_q=%d k0=%lld n_kv=%d n_sum=%d must be >= 0",
+                (long long)q0, n_q, (long long)k0, n_kv, n_sum);
+  if (cfg->bh_count == 0 || n_q == 0) return ok();
+  const int C = cfg->chunk, W = cfg->window;
+  const eva::Range rf = eva::mask_range(q0, C, W, cfg->mode);
+  const eva::Range rl = eva::mask_range(q0 + n_q - 1, C, W, cfg->mode);
+  if (k0 > rf.lo)
+    return fail(EVA_ERR_INVALID_ARG, "k0=%lld > lo(q0)=%lld: the window halo of the first query is missing",
+                (long long)k0, (long long)rf.lo);
+  if (k0 + n_kv < q0 + n_q)
+    return fail(EVA_ERR_INVALID_ARG, "keys end at %lld < last query + 1 = %lld", (long long)(k0 + n_kv),
+                (long long)(q0 + n_q));
+  if (n_sum < rl.nsum)
+    return fail(EVA_ERR_INVALID_ARG, "n_sum=%d < nsum(last query)=%lld", n_sum, (long long)rl.nsum);
+  const void* p[] = {Q, K, V, O};
+  const char* nm[] = {"Q", "K", "V", "O"};
+  if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+  if (n_sum > 0) {
+    const void* p2[] = {Ksum, Vsum};
+    const char* nm2[] = {"Ksum", "Vsum"};
+    if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+  }
+  if (lse && !aligned16(lse)) return fail(EVA_ERR_INVALID_ARG, "lse is not 16-byte aligned");
+  eva::PrefillRange rg;
+  rg.q0 = q0;
+  rg.nq = n_q;
+  rg.pad0 = 0;
+  rg.k0 = k0;
+  rg.nkv = n_kv;
+  rg.nsl = n_sum;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) && eva::prefill_sm100_supported(*cfg);
+  cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, 1u, s)
+                     : eva::launch_prefill_simt(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+  return cuda_status(e, tc ? "eva_attn_prefill_range(sm100)" : "eva_attn_prefill_range(simt)");
 }
 
 eva_status eva_cache_append(eva_cache* cache, const void* K_new, const void* V_new, int32_t n_new,

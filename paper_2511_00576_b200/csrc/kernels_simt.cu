@@ -22,7 +22,7 @@ template <typename T, int D>
 __global__ void __launch_bounds__(128) summarize_kernel(eva_config cfg, const T* __restrict__ K,
                                                         const T* __restrict__ V,
                                                         const float* __restrict__ eps,
-                                                        T* __restrict__ Ksum, T* __restrict__ Vsum) {
+                                                        T* __restrict__ Ksum, T* __restrict__ Vsum, int c0) {
   const int nC = cfg.T / cfg.chunk;
   const int c = blockIdx.x * 4 + (threadIdx.x >> 5);
   const int u = blockIdx.y;
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(128) summarize_kernel(eva_config cfg, const T*
   auto rowK = [&](int i) { return Kc + (size_t)i * D; };
   auto rowV = [&](int i) { return Vc + (size_t)i * D; };
   const float* e = eps ? eps + ((size_t)u * nC + c) * D : nullptr;
-  summarize_chunk_warp<T, D>(rowK, rowV, C, e, (uint32_t)(cfg.bh_begin + u), (uint32_t)c, cfg,
+  summarize_chunk_warp<T, D>(rowK, rowV, C, e, (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
                              Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D);
 }
 
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(SUMM_THREADS) summarize_cta_kernel(eva_config 
                                                                    const T* __restrict__ V,
                                                                    const float* __restrict__ eps,
                                                                    T* __restrict__ Ksum,
-                                                                   T* __restrict__ Vsum) {
+                                                                   T* __restrict__ Vsum, int c0) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int nC = cfg.T / cfg.chunk;
   const int c = blockIdx.x, u = blockIdx.y, C = cfg.chunk;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(SUMM_THREADS) summarize_cta_kernel(eva_config 
   auto rowK = [&](int i) { return Kc + (size_t)i * D; };
   auto rowV = [&](int i) { return Vc + (size_t)i * D; };
   const float* e = eps ? eps + ((size_t)u * nC + c) * D : nullptr;
-  summarize_chunk_cta<T, D>(rowK, rowV, C, e, (uint32_t)(cfg.bh_begin + u), (uint32_t)c, cfg,
+  summarize_chunk_cta<T, D>(rowK, rowV, C, e, (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
                             Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D, smem);
 }
 
@@ -198,7 +198,7 @@ template <typename T, int D, int NI>
 __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, const T* __restrict__ K,
                                                            const T* __restrict__ V,
                                                            const float* __restrict__ eps,
-                                                           T* __restrict__ Ksum, T* __restrict__ Vsum) {
+                                                           T* __restrict__ Ksum, T* __restrict__ Vsum, int c0) {
   pdl_wait();
   pdl_trigger();
   const int C = cfg.chunk, nC = cfg.T / C;
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, cons
   const T* Vc = V + ((size_t)u * cfg.T + (size_t)c * C) * D;
   summarize_chunk_reg<T, D, NI>([&](int r) { return Kc + (size_t)r * D; }, [&](int r) { return Vc + (size_t)r * D; },
                                 C, eps ? eps + ((size_t)u * nC + c) * D : nullptr,
-                                (uint32_t)(cfg.bh_begin + u), (uint32_t)c, cfg,
+                                (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
                                 Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D);
 }
 
@@ -224,7 +224,8 @@ constexpr int summ_reg_ni(int C) {
 // order: the summary prefix [0, nsum(n_last)) and the local span
 // [lo(n_first), n_last]; each query applies its own (lo, nsum) (P:124 mask).
 template <typename T, int D>
-__global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, const T* __restrict__ Q,
+__global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, PrefillRange rg,
+                                                           const T* __restrict__ Q,
                                                            const T* __restrict__ K,
                                                            const T* __restrict__ V,
                                                            const T* __restrict__ Ksum,
@@ -237,20 +238,22 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, const
   __shared__ float Ks[KT][D];
   __shared__ float Vs[KT][D];
 
-  const int Tn = cfg.T, C = cfg.chunk, W = cfg.window;
-  const int nC = Tn / C;
+  // Absolute positions: query row i is position q0 + i, key/value row r is position k0 + r,
+  // summary row c is chunk c (rows per unit: nq, nkv, nsl).
+  const int C = cfg.chunk, W = cfg.window;
+  const int64_t q0 = rg.q0, k0 = rg.k0, qend = rg.q0 + rg.nq;
   const int u = blockIdx.y;
-  const int n0 = blockIdx.x * QT;
+  const int64_t n0 = q0 + (int64_t)blockIdx.x * QT;
   const int tid = threadIdx.x, qi = tid / G, gi = tid % G;
-  const int64_t n = (int64_t)n0 + qi;
-  const bool valid = n < Tn;
-  const int64_t nlast = min((int64_t)n0 + QT - 1, (int64_t)Tn - 1);
+  const int64_t n = n0 + qi;
+  const bool valid = n < qend;
+  const int64_t nlast = min(n0 + QT - 1, qend - 1);
   const Range rme = mask_range(valid ? n : nlast, C, W, cfg.mode);
   const Range rfirst = mask_range(n0, C, W, cfg.mode);
   const Range rlast = mask_range(nlast, C, W, cfg.mode);
 
   float q[CH], acc[CH];
-  const T* qp = Q + ((size_t)u * Tn + (size_t)(valid ? n : nlast)) * D;
+  const T* qp = Q + ((size_t)u * rg.nq + (size_t)((valid ? n : nlast) - q0)) * D;
 #pragma unroll
   for (int j = 0; j < CH; ++j) {
     q[j] = Elem<T>::to_f(qp[j * G + gi]) * cfg.scale;
@@ -259,8 +262,9 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, const
   float m = -INFINITY, l = 0.f;
 
   for (int seg = 0; seg < 2; ++seg) {
-    const T* kb = seg == 0 ? Ksum + (size_t)u * nC * D : K + (size_t)u * Tn * D;
-    const T* vb = seg == 0 ? Vsum + (size_t)u * nC * D : V + (size_t)u * Tn * D;
+    // kb/vb indexed by absolute position (local segment) or chunk (summary segment)
+    const T* kb = seg == 0 ? Ksum + (size_t)u * rg.nsl * D : K + ((size_t)u * rg.nkv - k0) * D;
+    const T* vb = seg == 0 ? Vsum + (size_t)u * rg.nsl * D : V + ((size_t)u * rg.nkv - k0) * D;
     const int64_t beg = seg == 0 ? 0 : rfirst.lo;
     const int64_t end = seg == 0 ? rlast.nsum : nlast + 1;
     for (int64_t t0 = beg; t0 < end; t0 += KT) {
@@ -293,10 +297,10 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, const
   }
   if (valid) {
     const float il = 1.0f / l;
-    T* op = O + ((size_t)u * Tn + (size_t)n) * D;
+    T* op = O + ((size_t)u * rg.nq + (size_t)(n - q0)) * D;
 #pragma unroll
     for (int j = 0; j < CH; ++j) op[j * G + gi] = Elem<T>::from_f(acc[j] * il);
-    if (lse && gi == 0) lse[(size_t)u * Tn + n] = m + logf(l);
+    if (lse && gi == 0) lse[(size_t)u * rg.nq + (n - q0)] = m + logf(l);
   }
 }
 
@@ -688,7 +692,7 @@ cudaError_t set_smem_attr(const void* fn, size_t bytes) {
 }
 
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
-                             void* Ksum, void* Vsum, cudaStream_t s) {
+                             void* Ksum, void* Vsum, cudaStream_t s, int c0) {
   const int nC = cfg.T / cfg.chunk;
   if (nC == 0 || cfg.bh_count == 0) return cudaSuccess;
   cudaError_t err = cudaSuccess;
@@ -698,37 +702,37 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
     if (ni <= 16) {
       const dim3 grid(nC, cfg.bh_count);
       if (ni <= 2)
-        err = launch_pdl(summarize_reg_kernel<T, D, 2>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+        err = launch_pdl(summarize_reg_kernel<T, D, 2>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
       else if (ni <= 4)
-        err = launch_pdl(summarize_reg_kernel<T, D, 4>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+        err = launch_pdl(summarize_reg_kernel<T, D, 4>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
       else if (ni <= 8)
-        err = launch_pdl(summarize_reg_kernel<T, D, 8>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+        err = launch_pdl(summarize_reg_kernel<T, D, 8>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
       else
-        err = launch_pdl(summarize_reg_kernel<T, D, 16>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+        err = launch_pdl(summarize_reg_kernel<T, D, 16>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
       if (err != cudaSuccess) return err;
     } else if (sm <= kSummSmemMax) {
       err = set_smem_attr((const void*)summarize_cta_kernel<T, D>, sm);
       if (err != cudaSuccess) return err;
       summarize_cta_kernel<T, D><<<dim3(nC, cfg.bh_count), SUMM_THREADS, sm, s>>>(
-          cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+          cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
     } else {
       summarize_kernel<T, D><<<dim3((nC + 3) / 4, cfg.bh_count), 128, 0, s>>>(
-          cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum);
+          cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
     }
   }));
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_prefill_simt(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                                const void* Ksum, const void* Vsum, void* O, float* lse,
-                                cudaStream_t s) {
-  if (cfg.bh_count == 0) return cudaSuccess;
+cudaError_t launch_prefill_simt(const eva_config& cfg, const PrefillRange& rg, const void* Q,
+                                const void* K, const void* V, const void* Ksum, const void* Vsum,
+                                void* O, float* lse, cudaStream_t s) {
+  if (cfg.bh_count == 0 || rg.nq == 0) return cudaSuccess;
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
     constexpr int G = D >= 32 ? D / 32 : 1;
     constexpr int QT = 128 / G;
-    dim3 grid((cfg.T + QT - 1) / QT, cfg.bh_count);
-    prefill_simt_kernel<T, D><<<grid, 128, 0, s>>>(cfg, (const T*)Q, (const T*)K, (const T*)V,
+    dim3 grid((rg.nq + QT - 1) / QT, cfg.bh_count);
+    prefill_simt_kernel<T, D><<<grid, 128, 0, s>>>(cfg, rg, (const T*)Q, (const T*)K, (const T*)V,
                                                    (const T*)Ksum, (const T*)Vsum, (T*)O, lse);
   }));
   note_launch();

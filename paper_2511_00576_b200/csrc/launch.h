@@ -9,22 +9,37 @@
 
 namespace eva {
 
-// eva_summarize: K, V [bh, T, d] -> Ksum, Vsum [bh, nC, d].
+// eva_summarize: K, V [bh, T, d] -> Ksum, Vsum [bh, nC, d].  c0: absolute index of the first
+// chunk (row 0 is position c0 * C; keys the random draws).
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
-                             void* Ksum, void* Vsum, cudaStream_t s);
+                             void* Ksum, void* Vsum, cudaStream_t s, int c0 = 0);
+
+// Row ranges of one prefill call: query rows are absolute positions [q0, q0 + nq), key/value
+// rows [k0, k0 + nkv), summary rows chunks [0, nsl).  The whole-sequence call is
+// {0, T, 0, T, T / C}.
+struct PrefillRange {
+  int64_t q0;
+  int32_t nq;
+  int32_t pad0;
+  int64_t k0;
+  int32_t nkv;
+  int32_t nsl;
+};
+inline PrefillRange full_range(const eva_config& c) { return {0, c.T, 0, 0, c.T, c.T / c.chunk}; }
 
 // SIMT prefill (fp32 parity path; any supported d, either dtype).
-cudaError_t launch_prefill_simt(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                                const void* Ksum, const void* Vsum, void* O, float* lse,
-                                cudaStream_t s);
+cudaError_t launch_prefill_simt(const eva_config& cfg, const PrefillRange& rg, const void* Q,
+                                const void* K, const void* V, const void* Ksum, const void* Vsum,
+                                void* O, float* lse, cudaStream_t s);
 
 // tcgen05/TMEM/TMA prefill (bf16, d in {64, 128}).  Returns cudaErrorNotSupported if the
 // shape is outside the kernel's envelope (the caller then reports EVA_ERR_UNSUPPORTED).
 bool prefill_sm100_supported(const eva_config& cfg);
 // variant: 0 = automatic, 1 = one 128-query tile per CTA, 2 = persistent pair kernel.
-cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                                 const void* Ksum, const void* Vsum, void* O, float* lse,
-                                 uint32_t variant, cudaStream_t s);
+// A range other than full_range(cfg) always runs the one-tile-per-CTA kernel.
+cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, const void* Q,
+                                 const void* K, const void* V, const void* Ksum, const void* Vsum,
+                                 void* O, float* lse, uint32_t variant, cudaStream_t s);
 
 // Debug: run the pair kernel with CTA 0 recording a (clock64, event) timeline into trace_dev.
 cudaError_t debug_trace_prefill(const eva_config& cfg, const void* Q, const void* K, const void* V,

@@ -254,6 +254,27 @@ struct TilePlan {
   __device__ int base(int j) const { return j < n_st ? j * BN : lo0 + (j - n_st) * BN; }
 };
 
+// TilePlan of a query-range call (eva_attn_prefill_range): query tile qt covers absolute
+// positions [q0 + qt*BM, ...), local key tiles start at lo(n0) (absolute); row() maps a
+// tile base to the TMA row of its tensor (key rows are stored from position k0).
+struct RangePlan {
+  int64_t n0, nlast, lo0, k0;
+  int n_st, n_lt;
+  __device__ RangePlan(int qt, const PrefillRange& rg, int C, int W, int mode) {
+    n0 = rg.q0 + (int64_t)qt * BM;
+    nlast = min(n0 + BM - 1, rg.q0 + rg.nq - 1);
+    const Range rf = mask_range(n0, C, W, mode), rl = mask_range(nlast, C, W, mode);
+    n_st = (int)((rl.nsum + BN - 1) / BN);
+    lo0 = rf.lo;
+    k0 = rg.k0;
+    n_lt = (int)((nlast - lo0 + 1 + BN - 1) / BN);
+  }
+  __device__ int count() const { return n_st + n_lt; }
+  __device__ bool summary(int j) const { return j < n_st; }
+  __device__ int64_t base(int j) const { return j < n_st ? (int64_t)j * BN : lo0 + (int64_t)(j - n_st) * BN; }
+  __device__ int row(int j) const { return j < n_st ? j * BN : (int)(lo0 - k0) + (j - n_st) * BN; }
+};
+
 
 // Debug timeline of the tile kernel (eva_debug_trace_prefill with variant 1): CTAs with
 // linear id in {0, 1, 150, 151} log (globaltimer-free) clock64 events per role in shared
@@ -287,13 +308,15 @@ __global__ void __launch_bounds__(NTHREADS, 2)
 prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
                      const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
-                     int T, int C, int W, int mode, float scale_log2, float* __restrict__ lse) {
+                     const PrefillRange rg, int C, int W, int mode, float scale_log2,
+                     float* __restrict__ lse) {
   extern __shared__ uint8_t smem_raw[];
   Smem<D, NSTAGE>* sm = reinterpret_cast<Smem<D, NSTAGE>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.y;
-  const TilePlan plan(blockIdx.x, T, C, W, mode);
+  const RangePlan plan(blockIdx.x, rg, C, W, mode);
+  const int qrow = blockIdx.x * BM;  // TMA row of this query tile in Q / O
   const int NT = plan.count();
   __shared__ TileTrace tlog_s;
   TileTrace* tl = &tlog_s;
@@ -336,7 +359,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     if (elect_one()) {
       mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
       for (int kb = 0; kb < D / 64; ++kb)
-        tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
+        tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, qrow, u);
     }
     __syncwarp();
     auto prefetch_rest = [&] {
@@ -347,8 +370,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
         const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
         for (int kb = 0; kb < D / 64; ++kb) {
-          tma_prefetch_l2_3d(mk, kb * 64, plan.base(j), u);
-          tma_prefetch_l2_3d(mv, kb * 64, plan.base(j), u);
+          tma_prefetch_l2_3d(mk, kb * 64, plan.row(j), u);
+          tma_prefetch_l2_3d(mv, kb * 64, plan.row(j), u);
         }
       }
       }
@@ -364,7 +387,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       if (elect_one()) {
         mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
         for (int kb = 0; kb < D / 64; ++kb)
-          tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, plan.base(j), u);
+          tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, plan.row(j), u);
       }
       __syncwarp();
       if (lane == 0) tt<TRACE>(tl, 0, 12, j);
@@ -376,7 +399,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       if (elect_one()) {
         mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
         for (int kb = 0; kb < D / 64; ++kb)
-          tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, plan.base(j), u);
+          tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, plan.row(j), u);
       }
       __syncwarp();
     };
@@ -443,8 +466,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     // ------------------------------------------------------------ softmax warps
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
-    const int n = plan.n0 + r;
-    const bool valid = n < T;
+    const int64_t n = plan.n0 + r;
+    const bool valid = n < rg.q0 + rg.nq;
     const Range rr = mask_range(valid ? n : plan.nlast, C, W, mode);
     const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
     float m_ref = -INFINITY, l = 0.f;
@@ -453,14 +476,14 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       mbar_wait(&sm->s_full[j & 1], (j >> 1) & 1);
       if (tw) tt<TRACE>(tl, 2, 7, j);
       tc_fence_after();
-      const int base = plan.base(j);
+      const int64_t base = plan.base(j);
       int vlo, vhi;
       if (plan.summary(j)) {
         vlo = 0;
         vhi = (int)min((int64_t)BN, rr.nsum - base);
       } else {
         vlo = (int)max((int64_t)0, rr.lo - base);
-        vhi = min(BN, n - base + 1);
+        vhi = (int)min((int64_t)BN, n - base + 1);
       }
       if (!valid) vhi = vlo;
       if constexpr (SMX < 0)
@@ -495,11 +518,11 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         *reinterpret_cast<uint4*>(rowp + (((c16_0 + g) ^ (r & 7)) * 16)) = w;
       }
     }
-    if (valid && lse) lse[(size_t)u * T + n] = (m_ref + __log2f(l)) * 0.69314718055994531f;
+    if (valid && lse) lse[(size_t)u * rg.nq + (size_t)(n - rg.q0)] = (m_ref + __log2f(l)) * 0.69314718055994531f;
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (warp == 2 && lane == 0) {
-      for (int kb = 0; kb < D / 64; ++kb) tma_store_3d(&mO, sm->q + kb * BM * 64, kb * 64, plan.n0, u);
+      for (int kb = 0; kb < D / 64; ++kb) tma_store_3d(&mO, sm->q + kb * BM * 64, kb * 64, qrow, u);
       tma_store_commit();
       tma_store_wait_all();
       tt<TRACE>(tl, 2, 10, 0);
@@ -1514,21 +1537,23 @@ int softmax_emu() {
 }
 
 template <int D, int NSTAGE, bool TRACE = false, int SMX = -1>
-cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                     const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
+cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* Q, const void* K,
+                     const void* V, const void* Ksum, const void* Vsum, void* O, float* lse,
+                     cudaStream_t s) {
   if constexpr (!TRACE && SMX == -1) {
     switch (softmax_emu()) {
-      case 0: return launch_t<D, NSTAGE, false, 0>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-      case 1: return launch_t<D, NSTAGE, false, 1>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-      case 2: return launch_t<D, NSTAGE, false, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-      case 3: return launch_t<D, NSTAGE, false, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+      case 0: return launch_t<D, NSTAGE, false, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+      case 1: return launch_t<D, NSTAGE, false, 1>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+      case 2: return launch_t<D, NSTAGE, false, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+      case 3: return launch_t<D, NSTAGE, false, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
       default: break;
     }
   }
-  const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
+  const int BH = cfg.bh_count, nC = rg.nsl;
+  if (rg.nq == 0) return cudaSuccess;
   CUtensorMap mQ, mK, mV, mKs, mVs, mO;
-  bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BN) &&
-            make_map(&mV, V, BH, T, D, BN) && make_map(&mO, O, BH, T, D, BM);
+  bool ok = make_map(&mQ, Q, BH, rg.nq, D, BM) && make_map(&mK, K, BH, rg.nkv, D, BN) &&
+            make_map(&mV, V, BH, rg.nkv, D, BN) && make_map(&mO, O, BH, rg.nq, D, BM);
   if (nC > 0) {
     ok = ok && make_map(&mKs, Ksum, BH, nC, D, BN) && make_map(&mVs, Vsum, BH, nC, D, BN);
   } else {  // never read (no summary tiles); any valid map will do
@@ -1544,10 +1569,10 @@ cudaError_t launch_t(const eva_config& cfg, const void* Q, const void* K, const 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid((T + BM - 1) / BM, BH);
+  dim3 grid((rg.nq + BM - 1) / BM, BH);
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
   cudaError_t e = launch_pdl(prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>, grid, dim3(NTHREADS), smem, s, mQ, mK, mV,
-                             mKs, mVs, mO, T, cfg.chunk, cfg.window, cfg.mode, scale_log2, lse);
+                             mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2, lse);
   if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
@@ -1666,8 +1691,9 @@ cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K
                              unsigned long long* trace_dev, cudaStream_t s) {
   cudaError_t e = cudaMemcpyToSymbolAsync(g_trace2, &trace_dev, sizeof(trace_dev), 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
-  if (cfg.d_head == 128) return launch_t<128, 2, true>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-  if (cfg.d_head == 64) return launch_t<64, 3, true>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+  const PrefillRange rg = full_range(cfg);
+  if (cfg.d_head == 128) return launch_t<128, 2, true>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+  if (cfg.d_head == 64) return launch_t<64, 3, true>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cudaErrorNotSupported;
 }
 
@@ -1675,10 +1701,13 @@ bool prefill_sm100_supported(const eva_config& cfg) {
   return cfg.dtype == EVA_BF16 && (cfg.d_head == 64 || cfg.d_head == 128) && encode_fn() != nullptr;
 }
 
-cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                                 const void* Ksum, const void* Vsum, void* O, float* lse,
-                                 uint32_t variant, cudaStream_t s) {
+cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, const void* Q,
+                                 const void* K, const void* V, const void* Ksum, const void* Vsum,
+                                 void* O, float* lse, uint32_t variant, cudaStream_t s) {
   if (cfg.bh_count == 0) return cudaSuccess;
+  const PrefillRange full = full_range(cfg);
+  if (rg.q0 != full.q0 || rg.nq != full.nq || rg.k0 != full.k0 || rg.nkv != full.nkv || rg.nsl != full.nsl)
+    variant = 1;  // query-range calls: the one-tile-per-CTA kernel only
   // The one-tile-per-CTA kernel (two CTAs per SM) is the default: on B200 it beats the
   // persistent pair kernel at every measured size (configs[2]: 0.65 vs 0.90 ms); the pair
   // kernel stays selectable for experiments (EVA_PREFILL_TC_PAIR).
@@ -1697,8 +1726,8 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const void* Q, const voi
     if (cfg.d_head == 128) return launch_pair<128, 5>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
     if (cfg.d_head == 64) return launch_pair<64, 8>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
   } else {
-    if (cfg.d_head == 128) return launch_t<128, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-    if (cfg.d_head == 64) return launch_t<64, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
+    if (cfg.d_head == 128) return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+    if (cfg.d_head == 64) return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   }
   return cudaErrorNotSupported;
 }
