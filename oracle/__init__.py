@@ -28,6 +28,7 @@ _lib = None
 
 SLIDING = 0
 BLOCK = 1
+NONCAUSAL = 2
 
 
 def build(force: bool = False) -> str:
@@ -56,6 +57,7 @@ def _L():
         lib.oracle_prefill.argtypes = [i, i, i, i, i, d_, D, D, D, D, D, D, D]
         lib.oracle_summarize_batch.argtypes = [i, i, i, i, D, D, D, d_, d_, i, D, D]
         lib.oracle_prefill_batch.argtypes = [i, i, i, i, i, i, d_, D, D, D, D, D, D, D]
+        lib.oracle_prefill_ext_batch.argtypes = [i, i, i, i, i, i, d_, d_, D, D, D, D, D, D, D]
         lib.oracle_prefill_rows.argtypes = [i, i, i, i, i, d_, D, D, D, D, D, i, I64, D, D]
         lib.oracle_backward.argtypes = [i, i, i, i, i, d_, d_, d_, i, D, D, D, D, D, D, D, D]
         lib.oracle_backward_batch.argtypes = [i, i, i, i, i, i, d_, d_, d_, i, D, D, D, D, D, D, D, D]
@@ -168,6 +170,22 @@ def prefill_batch(Q, K, V, Ksum, Vsum, C: int, W: int, mode: int = SLIDING, scal
     lse = np.zeros((BH, T))
     _L().oracle_prefill_batch(BH, T, d, C, W, mode, scale, _dp(Q), _dp(K), _dp(V), _dp(ks),
                               _dp(vs), _dp(O), _dp(lse))
+    return O, lse
+
+
+def prefill_ext_batch(Q, K, V, Ksum, Vsum, C: int, W: int, mode: int = SLIDING, scale: float = 1.0,
+                      bias: float = 0.0):
+    """oracle_prefill_ext over [BH, T, d]: mode 0/1 causal, 2 non-causal (R15); bias added to
+    every summary logit (R16).  Returns O [BH, T, d], lse [BH, T]."""
+    Q, K, V = _f64(Q), _f64(K), _f64(V)
+    BH, T, d = Q.shape
+    nC = T // C
+    ks = _f64(Ksum) if nC else np.zeros((BH, 1, d))
+    vs = _f64(Vsum) if nC else np.zeros((BH, 1, d))
+    O = np.zeros((BH, T, d))
+    lse = np.zeros((BH, T))
+    _L().oracle_prefill_ext_batch(BH, T, d, C, W, mode, scale, bias, _dp(Q), _dp(K), _dp(V), _dp(ks),
+                                  _dp(vs), _dp(O), _dp(lse))
     return O, lse
 
 

@@ -207,6 +207,91 @@ EXPORT void oracle_prefill(int T, int d, int C, int W, int mode, double scale, c
 }
 
 /* ------------------------------------------------------------------------ */
+/* Prefill variants (R15, R16).            */
+/*  mode 0 / 1: the causal partitions of oracle_mask (sliding / block-local). */
+/*  mode 2 (non-causal, "In the non-causal setting ..."; the original   */
+/*    EVA): E(n) = n's whole block of W positions [lo, min(lo+W, T)) with     */
+/*    lo = floor(n/W)*W, and the summaries of every complete chunk outside    */
+/*    that block, before AND after it: c < lo/C or c >= (lo+W)/C.             */
+/*  bias: added to every summary logit (R16; bias = ln C counts each summary  */
+/*    as the C tokens it stands for -- the |P_c| factor Eq.10 omits).   */
+/* Summaries are visible as two ranges [0, s1) and [s2, nC).                   */
+/* ------------------------------------------------------------------------ */
+static void visible_set(int64_t n, int T, int C, int W, int mode, int64_t* lo, int64_t* hi,
+                        int64_t* s1, int64_t* s2) {
+  const int64_t nC = T / C;
+  if (mode == 2) {
+    *lo = (n / W) * W;
+    *hi = *lo + W < T ? *lo + W : T;
+    *s1 = *lo / C;
+    *s2 = (*lo + W) / C;
+    if (*s2 > nC) *s2 = nC;
+  } else {
+    int64_t ns;
+    oracle_mask(n, C, W, mode, lo, &ns);
+    *hi = n + 1;
+    *s1 = ns;
+    *s2 = nC;
+  }
+}
+
+EXPORT void oracle_prefill_ext(int T, int d, int C, int W, int mode, double scale, double bias,
+                               const double* Q, const double* K, const double* V,
+                               const double* Ksum, const double* Vsum, double* O,
+                               double* lse /* may be NULL */) {
+  const int64_t nC = T / C;
+  double* logit = (double*)malloc(sizeof(double) * ((size_t)T + (size_t)nC + 1));
+  for (int n = 0; n < T; ++n) {
+    int64_t lo, hi, s1, s2;
+    visible_set(n, T, C, W, mode, &lo, &hi, &s1, &s2);
+    const double* q = Q + (size_t)n * d;
+    int cnt = 0;
+    double mx = -INFINITY;
+    for (int64_t c = 0; c < nC; ++c) {
+      if (!(c < s1 || c >= s2)) continue;
+      double s = 0.0;
+      for (int j = 0; j < d; ++j) s += q[j] * Ksum[(size_t)c * d + j];
+      logit[cnt] = scale * s + bias;
+      if (logit[cnt] > mx) mx = logit[cnt];
+      ++cnt;
+    }
+    for (int64_t m = lo; m < hi; ++m) {
+      double s = 0.0;
+      for (int j = 0; j < d; ++j) s += q[j] * K[(size_t)m * d + j];
+      logit[cnt] = scale * s;
+      if (logit[cnt] > mx) mx = logit[cnt];
+      ++cnt;
+    }
+    double z = 0.0;
+    for (int i = 0; i < cnt; ++i) z += exp(logit[i] - mx);
+    double* o = O + (size_t)n * d;
+    for (int j = 0; j < d; ++j) {
+      double acc = 0.0;
+      int i = 0;
+      for (int64_t c = 0; c < nC; ++c) {
+        if (!(c < s1 || c >= s2)) continue;
+        acc += exp(logit[i++] - mx) * Vsum[(size_t)c * d + j];
+      }
+      for (int64_t m = lo; m < hi; ++m) acc += exp(logit[i++] - mx) * V[(size_t)m * d + j];
+      o[j] = acc / z;
+    }
+    if (lse) lse[n] = mx + log(z);
+  }
+  free(logit);
+}
+
+EXPORT void oracle_prefill_ext_batch(int BH, int T, int d, int C, int W, int mode, double scale,
+                                     double bias, const double* Q, const double* K, const double* V,
+                                     const double* Ksum, const double* Vsum, double* O, double* lse) {
+  const int nC = T / C;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int u = 0; u < BH; ++u)
+    oracle_prefill_ext(T, d, C, W, mode, scale, bias, Q + (size_t)u * T * d, K + (size_t)u * T * d,
+                       V + (size_t)u * T * d, Ksum + (size_t)u * nC * d, Vsum + (size_t)u * nC * d,
+                       O + (size_t)u * T * d, lse ? lse + (size_t)u * T : NULL);
+}
+
+/* ------------------------------------------------------------------------ */
 /* Batched drivers: the same per-unit functions over BH units.  The loop is   */
 /* over independent units only (no change to any unit's arithmetic).          */
 /* ------------------------------------------------------------------------ */

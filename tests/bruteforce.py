@@ -33,6 +33,19 @@ def partition_sets(n: int, C: int, W: int, mode: str):
     elif mode == "block":
         b = math.ceil(p / W)
         E = list(range((b - 1) * W + 1, p + 1))
+    elif mode.startswith("noncausal:"):
+        # non-causal EVA (R15): E(p) = p's whole block of width W (future
+        # positions of the block included); every position outside it, before AND after, is
+        # grouped left to right into chunks of exactly C (the caller's T is a multiple of C).
+        T = int(mode.split(":")[1])
+        b = math.ceil(p / W)
+        E = list(range((b - 1) * W + 1, min(b * W, T) + 1))
+        earlier = list(range(1, min(E)))
+        later = list(range(max(E) + 1, T + 1))
+        assert len(earlier) % C == 0 and len(later) % C == 0
+        chunks = [earlier[i:i + C] for i in range(0, len(earlier), C)] + \
+                 [later[i:i + C] for i in range(0, len(later), C)]
+        return [x - 1 for x in E], [[x - 1 for x in ch] for ch in chunks]
     else:
         raise ValueError(mode)
     earlier = list(range(1, min(E)))
@@ -52,8 +65,11 @@ def summary_direct(Kc, Vc, eps_c, lam=0.1, clip=1.0):
     return kt, omega, beta
 
 
-def eva_direct(Q, K, V, E_eps, C: int, W: int, mode: str, scale: float = 1.0, lam=0.1, clip=1.0):
-    """EVA output of one unit, every query by explicit sets.  Returns O [T, d]."""
+def eva_direct(Q, K, V, E_eps, C: int, W: int, mode: str, scale: float = 1.0, lam=0.1, clip=1.0,
+               multiplicity: float = 1.0):
+    """EVA output of one unit, every query by explicit sets.  Returns O [T, d].
+    multiplicity: each chunk's Z-term exp(q.k~_c) counts this many times (1 = Eq.10 as
+    printed; C = the |P_c| tokens the chunk replaces, R16)."""
     Q = np.asarray(Q, dtype=np.float64)
     K = np.asarray(K, dtype=np.float64)
     V = np.asarray(V, dtype=np.float64)
@@ -67,10 +83,11 @@ def eva_direct(Q, K, V, E_eps, C: int, W: int, mode: str, scale: float = 1.0, la
             w = math.exp(scale * float(Q[n] @ K[m]))
             Z += w
             num += w * V[m]
-        for c, members in enumerate(chunks):
+        for members in chunks:
+            c = members[0] // C
             assert members == list(range(c * C, c * C + C))
             kt, _, beta = summary_direct(K[members], V[members], E_eps[c], lam, clip)
-            w = math.exp(scale * float(Q[n] @ kt))
+            w = multiplicity * math.exp(scale * float(Q[n] @ kt))
             Z += w
             num += w * beta
         O[n] = num / Z
@@ -87,4 +104,16 @@ def exact_causal_softmax(Q, K, V, scale=1.0):
     for n in range(T):
         w = np.array([math.exp(scale * float(Q[n] @ K[m])) for m in range(n + 1)])
         O[n] = (w[:, None] * V[: n + 1]).sum(axis=0) / w.sum()
+    return O
+
+
+def exact_softmax(Q, K, V, scale=1.0):
+    """Eq.1 without the causal restriction (every query sees every key), two loops."""
+    Q = np.asarray(Q, dtype=np.float64)
+    K = np.asarray(K, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    O = np.zeros((Q.shape[0], V.shape[1]))
+    for n in range(Q.shape[0]):
+        w = np.array([math.exp(scale * float(Q[n] @ K[m])) for m in range(K.shape[0])])
+        O[n] = (w[:, None] * V).sum(axis=0) / w.sum()
     return O
