@@ -65,7 +65,13 @@ typedef enum { EVA_F32 = 0, EVA_BF16 = 1 } eva_dtype;
  *   BLOCK (original EVA's non-overlapping local blocks of width W):
  *       lo(n) = floor(n/W)*W,                    nsum(n) = lo(n)/C
  * Query n attends to locals m in [lo(n), n] and to summaries c < nsum(n). */
-typedef enum { EVA_WINDOW_SLIDING = 0, EVA_WINDOW_BLOCK = 1 } eva_window_mode;
+typedef enum { EVA_WINDOW_SLIDING = 0, EVA_WINDOW_BLOCK = 1, EVA_NONCAUSAL = 2 } eva_window_mode;
+/* EVA_NONCAUSAL (prefill only; "In the non-causal setting ..."; reading R15):
+ *   E(n) = n's whole block [lo, min(lo + W, T)), lo = floor(n/W)*W (later positions of the
+ *   block included), plus the summaries of EVERY complete chunk outside that block, before
+ *   and after it: c < lo/C or c >= (lo + W)/C.  Requires T % C == 0 (every position is a
+ *   local or inside exactly one summarised chunk).  Decode, cache, backward and the
+ *   query-range prefill are causal by construction and return EVA_ERR_UNSUPPORTED. */
 
 /* Proposal of Eq.15, reading R3:
  *   AS_PRINTED:     omega_c = lambda * clip(k~_c + eps_c, -clip, clip)   (default)
@@ -88,11 +94,15 @@ typedef struct {
   float clip;                 /* Eq.15 clip bound, paper value 1               */
   uint32_t layer;             /* RNG key component (reading R9)                         */
   uint64_t seed;              /* RNG key when eps == NULL (reading R9)                  */
+  float summary_bias;         /* added to every summary logit s q.k~_c (natural-log units):
+                                 0 = Eq.10 as printed (reading R4); ln C counts each
+                                 summary as the C tokens it replaces (reading R16) */
+  int32_t reserved;           /* must be 0 */
 } eva_config;
 
 /* Fill *cfg with the paper's defaults for (B, H, T, d, C, W):
  * full shard, S = 1, sliding, scale = 1/sqrt(d), lambda = 0.1, clip = 1,
- * omega as printed, seed = 1234, layer = 0, dtype bf16. */
+ * omega as printed, seed = 1234, layer = 0, dtype bf16, summary_bias = 0. */
 void eva_config_default(eva_config* cfg, int32_t B, int32_t H, int32_t T, int32_t d,
                         int32_t chunk, int32_t window);
 

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libeva.so")
 
 EVA_OK, EVA_ERR_INVALID_ARG, EVA_ERR_UNSUPPORTED, EVA_ERR_CAPACITY, EVA_ERR_CUDA = range(5)
 EVA_F32, EVA_BF16 = 0, 1
-EVA_WINDOW_SLIDING, EVA_WINDOW_BLOCK = 0, 1
+EVA_WINDOW_SLIDING, EVA_WINDOW_BLOCK, EVA_NONCAUSAL = 0, 1, 2
 EVA_OMEGA_AS_PRINTED, EVA_OMEGA_SHIFTED_NOISE = 0, 1
 EVA_SUMMARIES_PROVIDED = 1
 EVA_PREFILL_SIMT = 4
@@ -34,7 +34,8 @@ class EvaConfig(ctypes.Structure):
                 ("samples", ctypes.c_int32), ("mode", ctypes.c_int32),
                 ("dtype", ctypes.c_int32), ("omega_mode", ctypes.c_int32),
                 ("scale", ctypes.c_float), ("lambda_", ctypes.c_float), ("clip", ctypes.c_float),
-                ("layer", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
+                ("layer", ctypes.c_uint32), ("seed", ctypes.c_uint64),
+                ("summary_bias", ctypes.c_float), ("reserved", ctypes.c_int32)]
 
 
 class EvaCache(ctypes.Structure):

@@ -22,7 +22,7 @@ __all__ = ["make_config", "eva_summarize", "eva_attn_prefill", "eva_cache_append
            "eva_summarize_range", "eva_attn_prefill_range"]
 
 _DT = {torch.float32: N.EVA_F32, torch.bfloat16: N.EVA_BF16}
-_MODE = {"sliding": N.EVA_WINDOW_SLIDING, "block": N.EVA_WINDOW_BLOCK}
+_MODE = {"sliding": N.EVA_WINDOW_SLIDING, "block": N.EVA_WINDOW_BLOCK, "noncausal": N.EVA_NONCAUSAL}
 
 
 def version() -> str:
@@ -37,7 +37,8 @@ def launch_count() -> int:
 def make_config(B: int, H: int, T: int, d: int, chunk: int, window: int, *, bh_begin: int = 0,
                 bh_count: Optional[int] = None, mode: str = "sliding", dtype=torch.bfloat16,
                 scale: Optional[float] = None, lam: float = 0.1, clip: float = 1.0,
-                seed: int = 1234, layer: int = 0, omega_mode: int = 0, samples: int = 1) -> EvaConfig:
+                seed: int = 1234, layer: int = 0, omega_mode: int = 0, samples: int = 1,
+                summary_bias: float = 0.0) -> EvaConfig:
     cfg = EvaConfig()
     lib.eva_config_default(ctypes.byref(cfg), B, H, T, d, chunk, window)
     cfg.bh_begin = bh_begin
@@ -51,6 +52,7 @@ def make_config(B: int, H: int, T: int, d: int, chunk: int, window: int, *, bh_b
     cfg.layer = layer
     cfg.omega_mode = omega_mode
     cfg.samples = samples
+    cfg.summary_bias = summary_bias
     return cfg
 
 

@@ -154,7 +154,7 @@ def cp_prefill(cfg, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, shards: L
     sub = api.make_config(cfg.B, cfg.H, n, cfg.d_head, cfg.chunk, cfg.window, bh_begin=cfg.bh_begin,
                           bh_count=cfg.bh_count, mode=cfg.mode, dtype=api._tdtype(cfg), scale=cfg.scale,
                           lam=cfg.lambda_, clip=cfg.clip, seed=cfg.seed, layer=cfg.layer,
-                          omega_mode=cfg.omega_mode)
+                          omega_mode=cfg.omega_mode, summary_bias=cfg.summary_bias)
     Ks, Vs = api.eva_summarize_range(sub, me.q0 // cfg.chunk, K, V)                   # (1)
     Ks_all, Vs_all, Kh, Vh = exchange(Ks, Vs, K, V, shards, rank, cfg.chunk, group)             # (2)
     Kc = torch.cat([Kh, K], dim=1) if Kh.shape[1] else K

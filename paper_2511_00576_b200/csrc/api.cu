@@ -63,8 +63,10 @@ eva_status check_cfg(const eva_config* cfg, bool need_T) {
   if (cfg->window % cfg->chunk != 0)
     return fail(EVA_ERR_INVALID_ARG, "window %d is not a multiple of chunk %d (S:211)", cfg->window,
                 cfg->chunk);
-  if (cfg->mode != EVA_WINDOW_SLIDING && cfg->mode != EVA_WINDOW_BLOCK)
+  if (cfg->mode != EVA_WINDOW_SLIDING && cfg->mode != EVA_WINDOW_BLOCK && cfg->mode != EVA_NONCAUSAL)
     return fail(EVA_ERR_INVALID_ARG, "mode=%d", cfg->mode);
+  if (!std::isfinite(cfg->summary_bias) || cfg->reserved != 0)
+    return fail(EVA_ERR_INVALID_ARG, "summary_bias must be finite and reserved 0");
   if (cfg->dtype != EVA_F32 && cfg->dtype != EVA_BF16)
     return fail(EVA_ERR_INVALID_ARG, "dtype=%d", cfg->dtype);
   if (cfg->omega_mode != EVA_OMEGA_AS_PRINTED && cfg->omega_mode != EVA_OMEGA_SHIFTED_NOISE)
@@ -77,6 +79,13 @@ eva_status check_cfg(const eva_config* cfg, bool need_T) {
                 cfg->samples);
   if (!d_supported(cfg->d_head))
     return fail(EVA_ERR_UNSUPPORTED, "d_head=%d not in {16,32,64,128}", cfg->d_head);
+  return EVA_OK;
+}
+
+// Decode, cache, backward and the query-range prefill are causal by construction (R15).
+eva_status check_causal(const eva_config* cfg, const char* what) {
+  if (cfg->mode == EVA_NONCAUSAL)
+    return fail(EVA_ERR_UNSUPPORTED, "%s is causal; EVA_NONCAUSAL applies to the prefill only", what);
   return EVA_OK;
 }
 
@@ -112,6 +121,8 @@ void eva_config_default(eva_config* cfg, int32_t B, int32_t H, int32_t T, int32_
   cfg->clip = 1.0f;
   cfg->layer = 0;
   cfg->seed = 1234;
+  cfg->summary_bias = 0.f;
+  cfg->reserved = 0;
 }
 
 eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, const float* eps,
@@ -135,6 +146,9 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT | EVA_PREFILL_TC_TILE | EVA_PREFILL_TC_PAIR |
                 EVA_PREFILL_TC_WIDE | EVA_PREFILL_TC_SPLIT))
     return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  if (cfg->mode == EVA_NONCAUSAL && cfg->T % cfg->chunk != 0)
+    return fail(EVA_ERR_INVALID_ARG, "non-causal prefill needs T %% C == 0 (T=%d, C=%d; reading R15)", cfg->T,
+                cfg->chunk);
   if (cfg->bh_count == 0) return ok();
   const void* p[] = {Q, K, V, O};
   const char* nm[] = {"Q", "K", "V", "O"};
@@ -182,6 +196,7 @@ eva_status eva_attn_prefill_range(const eva_config* cfg, int64_t q0, int32_t n_q
                                   float* lse, uint32_t flags, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, false);
   if (st != EVA_OK) return st;
+  if ((st = check_causal(cfg, "eva_attn_prefill_range")) != EVA_OK) return st;
   if (flags & ~EVA_PREFILL_SIMT) return fail(EVA_ERR_INVALID_ARG, "flags 0x%x: only EVA_PREFILL_SIMT", flags);
   if (q0 < 0 || n_q < 0 || k0 < 0 || n_kv < 0 || n_sum < 0)
     return fail(EVA_ERR_INVALID_ARG, "q0=%lld n_q=%d k0=%lld n_kv=%d n_sum=%d must be >= 0",
@@ -226,6 +241,7 @@ eva_status eva_cache_append(eva_cache* cache, const void* K_new, const void* V_n
   if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
   eva_status st = check_cfg(&cache->cfg, false);
   if (st != EVA_OK) return st;
+  if ((st = check_causal(&cache->cfg, "the decode cache")) != EVA_OK) return st;
   if (n_new < 1) return fail(EVA_ERR_INVALID_ARG, "n_new=%d must be >= 1", n_new);
   if (cache->pos < 0 || cache->cap_chunks < 0)
     return fail(EVA_ERR_INVALID_ARG, "pos=%lld cap_chunks=%d", (long long)cache->pos, cache->cap_chunks);
@@ -255,6 +271,7 @@ eva_status eva_cache_load(eva_cache* cache, const void* K, const void* V, const 
   if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
   eva_status st = check_cfg(&cache->cfg, false);
   if (st != EVA_OK) return st;
+  if ((st = check_causal(&cache->cfg, "the decode cache")) != EVA_OK) return st;
   if (n < 1) return fail(EVA_ERR_INVALID_ARG, "n=%d must be >= 1", n);
   if (cache->pos != 0) return fail(EVA_ERR_INVALID_ARG, "eva_cache_load needs an empty cache (pos=%lld)", (long long)cache->pos);
   const int nC = n / cache->cfg.chunk;
@@ -291,6 +308,7 @@ eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float
   if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
   eva_status st = check_cfg(&cache->cfg, false);
   if (st != EVA_OK) return st;
+  if ((st = check_causal(&cache->cfg, "the decode cache")) != EVA_OK) return st;
   if (cache->pos < 1) return fail(EVA_ERR_INVALID_ARG, "decode needs pos >= 1 (pos=%lld)", (long long)cache->pos);
   if (cache->cfg.bh_count == 0) return ok();
   const void* p[] = {Q, O, cache->ring_k, cache->ring_v};
@@ -320,6 +338,7 @@ eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, c
   if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
   eva_status st = check_cfg(&cache->cfg, false);
   if (st != EVA_OK) return st;
+  if ((st = check_causal(&cache->cfg, "the decode cache")) != EVA_OK) return st;
   if (cache->pos < 0) return fail(EVA_ERR_INVALID_ARG, "pos=%lld", (long long)cache->pos);
   if ((cache->pos + 1) / cache->cfg.chunk > cache->cap_chunks)
     return fail(EVA_ERR_CAPACITY, "append at pos %lld needs %lld summaries > cap %d", (long long)cache->pos,
@@ -504,6 +523,9 @@ eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K
                              void* workspace, size_t workspace_bytes, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
+  if ((st = check_causal(cfg, "eva_attn_backward")) != EVA_OK) return st;
+  if (cfg->summary_bias != 0.f)
+    return fail(EVA_ERR_UNSUPPORTED, "eva_attn_backward: summary_bias != 0 is not implemented");
   if (cfg->bh_count == 0) return ok();
   const void* p[] = {Q, K, V, O, lse, dO, dQ, dK, dV, workspace};
   const char* nm[] = {"Q", "K", "V", "O", "lse", "dO", "dQ", "dK", "dV", "workspace"};

@@ -99,6 +99,26 @@ __host__ __device__ __forceinline__ Range mask_range(int64_t n, int C, int W, in
   return r;
 }
 
+// Visible set of query n in a sequence of T positions, every mode (R7, R15): locals
+// [lo, hi) and summaries [0, s1) U [s2, nC).  Causal modes: hi = n + 1, s2 = "never".
+struct Vis { int64_t lo, hi, s1, s2; };
+__host__ __device__ __forceinline__ Vis visible_set(int64_t n, int C, int W, int mode, int64_t T) {
+  Vis v;
+  if (mode == EVA_NONCAUSAL) {
+    v.lo = (n / W) * W;
+    v.hi = v.lo + W < T ? v.lo + W : T;
+    v.s1 = v.lo / C;
+    v.s2 = (v.lo + W) / C;
+  } else {
+    const Range r = mask_range(n, C, W, mode);
+    v.lo = r.lo;
+    v.hi = n + 1;
+    v.s1 = r.nsum;
+    v.s2 = INT64_MAX;
+  }
+  return v;
+}
+
 // ---------------------------------------------------------------- Philox4x32-10 (reading R9)
 struct U4 { uint32_t x, y, z, w; };
 __host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {

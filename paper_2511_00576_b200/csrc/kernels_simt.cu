@@ -248,9 +248,10 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, Prefi
   const int64_t n = n0 + qi;
   const bool valid = n < qend;
   const int64_t nlast = min(n0 + QT - 1, qend - 1);
-  const Range rme = mask_range(valid ? n : nlast, C, W, cfg.mode);
-  const Range rfirst = mask_range(n0, C, W, cfg.mode);
-  const Range rlast = mask_range(nlast, C, W, cfg.mode);
+  const Vis vme = visible_set(valid ? n : nlast, C, W, cfg.mode, qend);
+  const Vis vfirst = visible_set(n0, C, W, cfg.mode, qend);
+  const Vis vlast = visible_set(nlast, C, W, cfg.mode, qend);
+  const bool noncausal = cfg.mode == EVA_NONCAUSAL;
 
   float q[CH], acc[CH];
   const T* qp = Q + ((size_t)u * rg.nq + (size_t)((valid ? n : nlast) - q0)) * D;
@@ -265,8 +266,9 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, Prefi
     // kb/vb indexed by absolute position (local segment) or chunk (summary segment)
     const T* kb = seg == 0 ? Ksum + (size_t)u * rg.nsl * D : K + ((size_t)u * rg.nkv - k0) * D;
     const T* vb = seg == 0 ? Vsum + (size_t)u * rg.nsl * D : V + ((size_t)u * rg.nkv - k0) * D;
-    const int64_t beg = seg == 0 ? 0 : rfirst.lo;
-    const int64_t end = seg == 0 ? rlast.nsum : nlast + 1;
+    const int64_t beg = seg == 0 ? 0 : vfirst.lo;
+    const int64_t end = seg == 0 ? (noncausal ? (int64_t)rg.nsl : vlast.s1) : vlast.hi;
+    const float bias = seg == 0 ? cfg.summary_bias : 0.f;
     for (int64_t t0 = beg; t0 < end; t0 += KT) {
       const int nk = (int)min((int64_t)KT, end - t0);
       __syncthreads();
@@ -280,9 +282,9 @@ __global__ void __launch_bounds__(128) prefill_simt_kernel(eva_config cfg, Prefi
         float s = 0.f;
 #pragma unroll
         for (int c2 = 0; c2 < CH; ++c2) s += q[c2] * Ks[j][c2 * G + gi];
-        s = group_sum<G>(s);
+        s = group_sum<G>(s) + bias;
         const int64_t t = t0 + j;
-        const bool vis = valid && (seg == 0 ? (t < rme.nsum) : (t >= rme.lo && t <= n));
+        const bool vis = valid && (seg == 0 ? (t < vme.s1 || t >= vme.s2) : (t >= vme.lo && t < vme.hi));
         if (vis) {
           const float mn = fmaxf(m, s);
           const float corr = __expf(m - mn);
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
         for (int j = 0; j < VEC; ++j) d += q[j] * k[j];
       }
       d = group_sum<TPR>(d);
-      sc[i] = ok[i] ? d : -INFINITY;
+      sc[i] = ok[i] ? (eb + i * RPW + grp < ns ? d + c.cfg.summary_bias : d) : -INFINITY;
       mx = fmaxf(mx, sc[i]);
     }
     if (mx == -INFINITY) continue;

@@ -71,19 +71,21 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // written back to the same TMEM columns as packed bf16 (the A operand of the PV MMA).
 // wait_o() must make the previous PV of this Q tile complete before O is rescaled.
 // Requires scale_log2 > 0 (validated by the C ABI), so max and scaling commute.
+// Columns [xlo, xhi) are masked too (the non-causal mode's own-block summaries, R15), and
+// bias2 (log2 units) is added to every logit of the tile (summary_bias on summary tiles, R16).
 template <int D, typename WaitO>
-__device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, int vlo, int vhi,
-                                             float scale_log2, float& m_ref, float& l,
-                                             const WaitO& wait_o) {
+__device__ __forceinline__ void softmax_tile_mx(uint32_t s_addr, uint32_t o_addr, int vlo, int vhi,
+                                                int xlo, int xhi, float bias2, float scale_log2,
+                                                float& m_ref, float& l, const WaitO& wait_o) {
   uint32_t sr[64];
   tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
   tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
   tmem_wait_ld();
-  const bool full = vlo <= 0 && vhi >= 64;
+  const bool full = vlo <= 0 && vhi >= 64 && (xhi <= 0 || xlo >= 64 || xlo >= xhi);
   if (!__all_sync(0xffffffffu, full)) {
 #pragma unroll
     for (int c = 0; c < 64; ++c)
-      if (c < vlo || c >= vhi) sr[c] = 0xff800000u;  // -inf
+      if (c < vlo || c >= vhi || (c >= xlo && c < xhi)) sr[c] = 0xff800000u;  // -inf
   }
   // tree max (8 independent chains) -- a 63-deep serial chain is latency-bound with only
   // two softmax warps per scheduler
@@ -93,7 +95,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
 #pragma unroll
   for (int c = 8; c < 64; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sr[c]));
   float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
-  mx *= scale_log2;
+  mx = mx * scale_log2 + bias2;
   const bool grow = mx > m_ref + 8.0f;
   if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
     const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
@@ -112,7 +114,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
     l *= f;
   }
   if (grow) m_ref = mx;
-  const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
+  const float neg = (m_ref == -INFINITY ? 0.f : -m_ref) + bias2;
   uint32_t pk[32];
   float ls[8];
 #pragma unroll
@@ -129,6 +131,13 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
   tmem_st32(s_addr, pk);
   tmem_wait_st();
   tc_fence_before();
+}
+
+template <int D, typename WaitO>
+__device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, int vlo, int vhi,
+                                             float scale_log2, float& m_ref, float& l,
+                                             const WaitO& wait_o) {
+  softmax_tile_mx<D>(s_addr, o_addr, vlo, vhi, 0, 0, 0.f, scale_log2, m_ref, l, wait_o);
 }
 
 // ---- packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two lanes per issue slot)
@@ -174,17 +183,17 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
 // the bf16 rounding of P).
 template <int D, int EMU, typename WaitO>
 __device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, int vlo, int vhi,
-                                              float scale_log2, float& m_ref, float& l,
-                                              const WaitO& wait_o) {
+                                              int xlo, int xhi, float bias2, float scale_log2,
+                                              float& m_ref, float& l, const WaitO& wait_o) {
   uint32_t sr[64];
   tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
   tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
   tmem_wait_ld();
-  const bool full = vlo <= 0 && vhi >= 64;
+  const bool full = vlo <= 0 && vhi >= 64 && (xhi <= 0 || xlo >= 64 || xlo >= xhi);
   if (!__all_sync(0xffffffffu, full)) {
 #pragma unroll
     for (int c = 0; c < 64; ++c)
-      if (c < vlo || c >= vhi) sr[c] = 0xff800000u;  // -inf
+      if (c < vlo || c >= vhi || (c >= xlo && c < xhi)) sr[c] = 0xff800000u;  // -inf
   }
   float pm[8];
 #pragma unroll
@@ -192,7 +201,7 @@ __device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, 
 #pragma unroll
   for (int c = 8; c < 64; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sr[c]));
   float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
-  mx *= scale_log2;
+  mx = mx * scale_log2 + bias2;
   const bool grow = mx > m_ref + 8.0f;
   if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
     const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
@@ -216,7 +225,7 @@ __device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, 
     l *= f;
   }
   if (grow) m_ref = mx;
-  const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
+  const float neg = (m_ref == -INFINITY ? 0.f : -m_ref) + bias2;
   const uint64_t sc2 = f2pack(scale_log2, scale_log2), ng2 = f2pack(neg, neg);
   uint32_t pk[32];
   uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
@@ -261,13 +270,16 @@ struct RangePlan {
   int64_t n0, nlast, lo0, k0;
   int n_st, n_lt;
   __device__ RangePlan(int qt, const PrefillRange& rg, int C, int W, int mode) {
+    const int64_t qend = rg.q0 + rg.nq;
     n0 = rg.q0 + (int64_t)qt * BM;
-    nlast = min(n0 + BM - 1, rg.q0 + rg.nq - 1);
-    const Range rf = mask_range(n0, C, W, mode), rl = mask_range(nlast, C, W, mode);
-    n_st = (int)((rl.nsum + BN - 1) / BN);
-    lo0 = rf.lo;
+    nlast = min(n0 + BM - 1, qend - 1);
+    const Vis vf = visible_set(n0, C, W, mode, qend), vl = visible_set(nlast, C, W, mode, qend);
+    // causal: summary prefix [0, nsum(n_last)); non-causal: every summary (rows mask their
+    // own block's chunks)
+    n_st = (int)(((mode == EVA_NONCAUSAL ? (int64_t)rg.nsl : vl.s1) + BN - 1) / BN);
+    lo0 = vf.lo;
     k0 = rg.k0;
-    n_lt = (int)((nlast - lo0 + 1 + BN - 1) / BN);
+    n_lt = (int)((vl.hi - lo0 + BN - 1) / BN);
   }
   __device__ int count() const { return n_st + n_lt; }
   __device__ bool summary(int j) const { return j < n_st; }
@@ -309,7 +321,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
                      const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
                      const PrefillRange rg, int C, int W, int mode, float scale_log2,
-                     float* __restrict__ lse) {
+                     float bias_log2, float* __restrict__ lse) {
   extern __shared__ uint8_t smem_raw[];
   Smem<D, NSTAGE>* sm = reinterpret_cast<Smem<D, NSTAGE>*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -468,7 +480,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     const int r = quad * 32 + lane;
     const int64_t n = plan.n0 + r;
     const bool valid = n < rg.q0 + rg.nq;
-    const Range rr = mask_range(valid ? n : plan.nlast, C, W, mode);
+    const Vis rr = visible_set(valid ? n : plan.nlast, C, W, mode, rg.q0 + rg.nq);
     const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
     float m_ref = -INFINITY, l = 0.f;
     const bool tw = warp == 2 && lane == 0;
@@ -477,21 +489,29 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       if (tw) tt<TRACE>(tl, 2, 7, j);
       tc_fence_after();
       const int64_t base = plan.base(j);
-      int vlo, vhi;
+      int vlo, vhi, xlo = 0, xhi = 0;
+      float bias2 = 0.f;
       if (plan.summary(j)) {
         vlo = 0;
-        vhi = (int)min((int64_t)BN, rr.nsum - base);
+        if (mode == EVA_NONCAUSAL) {  // every summary except those of the row's own block
+          vhi = (int)min((int64_t)BN, (int64_t)rg.nsl - base);
+          xlo = (int)max((int64_t)-1, min((int64_t)BN, rr.s1 - base));
+          xhi = (int)max((int64_t)-1, min((int64_t)BN, rr.s2 - base));
+        } else {
+          vhi = (int)min((int64_t)BN, rr.s1 - base);
+        }
+        bias2 = bias_log2;
       } else {
         vlo = (int)max((int64_t)0, rr.lo - base);
-        vhi = (int)min((int64_t)BN, n - base + 1);
+        vhi = (int)min((int64_t)BN, rr.hi - base);
       }
       if (!valid) vhi = vlo;
       if constexpr (SMX < 0)
-        softmax_tile<D>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
-                        [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
+        softmax_tile_mx<D>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, xlo, xhi, bias2,
+                           scale_log2, m_ref, l, [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
       else
-        softmax_tile2<D, SMX>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
-                              [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
+        softmax_tile2<D, SMX>(t_lane + (uint32_t)(j & 1) * BN, t_lane + TM_O, vlo, vhi, xlo, xhi, bias2,
+                              scale_log2, m_ref, l, [&] { mbar_wait(&sm->o_done, (j - 1) & 1); });
       mbar_arrive(&sm->p_full[j & 1]);
       if (tw) tt<TRACE>(tl, 2, 8, j);
     }
@@ -1572,7 +1592,8 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
   dim3 grid((rg.nq + BM - 1) / BM, BH);
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
   cudaError_t e = launch_pdl(prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>, grid, dim3(NTHREADS), smem, s, mQ, mK, mV,
-                             mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2, lse);
+                             mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
+                             cfg.summary_bias * 1.4426950408889634f, lse);
   if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
@@ -1708,6 +1729,7 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, 
   const PrefillRange full = full_range(cfg);
   if (rg.q0 != full.q0 || rg.nq != full.nq || rg.k0 != full.k0 || rg.nkv != full.nkv || rg.nsl != full.nsl)
     variant = 1;  // query-range calls: the one-tile-per-CTA kernel only
+  if (cfg.mode == EVA_NONCAUSAL || cfg.summary_bias != 0.f) variant = 1;  // variants: tile kernel only
   // The one-tile-per-CTA kernel (two CTAs per SM) is the default: on B200 it beats the
   // persistent pair kernel at every measured size (configs[2]: 0.65 vs 0.90 ms); the pair
   // kernel stays selectable for experiments (EVA_PREFILL_TC_PAIR).

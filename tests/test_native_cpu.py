@@ -35,8 +35,9 @@ def test_exports_every_declared_symbol(N):
 
 
 def test_struct_layouts_match_header(N):
-    assert ctypes.sizeof(N.EvaConfig) == 15 * 4 + 4 + 8  # 16 x 4-byte fields (+pad) + u64
+    assert ctypes.sizeof(N.EvaConfig) == 16 * 4 + 8 + 2 * 4  # 16 x 4-byte fields + u64 + bias, reserved
     assert N.EvaConfig.seed.offset == 64
+    assert N.EvaConfig.summary_bias.offset == 72
     assert N.EvaCache.pos.offset == ctypes.sizeof(N.EvaConfig)
     assert N.EvaCache.ring_k.offset == ctypes.sizeof(N.EvaConfig) + 16
 
@@ -166,3 +167,29 @@ def test_host_pipeline_validation(N):
     args = [P] * 4 + [None] + [P] * 6 + [None, None]
     assert N.lib.eva_attn_prefill_host(None, ctypes.byref(cfg), *args, 0, 1, None) == N.EVA_ERR_INVALID_ARG
     assert b"pipe" in N.lib.eva_last_error()
+
+
+def test_noncausal_and_bias_validation(N):
+    """Mode EVA_NONCAUSAL: prefill needs T % C == 0; decode/cache/backward/range refuse it
+    (EVA_ERR_UNSUPPORTED); a non-finite summary_bias or a nonzero reserved field is invalid."""
+    buf = (ctypes.c_uint8 * 4096)()
+    P = ctypes.cast(buf, ctypes.c_void_p)
+    cfg = N.EvaConfig()
+    N.lib.eva_config_default(ctypes.byref(cfg), 1, 1, 70, 64, 16, 32)
+    assert cfg.summary_bias == 0.0 and cfg.reserved == 0
+    cfg.mode = N.EVA_NONCAUSAL
+    assert N.lib.eva_attn_prefill(ctypes.byref(cfg), P, P, P, P, P, None, P, None, 0, None) == N.EVA_ERR_INVALID_ARG
+    assert b"T % C" in N.lib.eva_last_error()
+    cache = N.EvaCache()
+    cache.cfg = cfg
+    cache.cap_chunks = 4
+    cache.ring_k = cache.ring_v = cache.sum_k = cache.sum_v = ctypes.addressof(buf)
+    assert N.lib.eva_cache_append(ctypes.byref(cache), P, P, 1, None, None) == N.EVA_ERR_UNSUPPORTED
+    assert N.lib.eva_attn_prefill_range(ctypes.byref(cfg), 0, 0, 0, 0, P, P, P, P, P, 0, P, None, 0,
+                                        None) == N.EVA_ERR_UNSUPPORTED
+    cfg.mode = N.EVA_WINDOW_SLIDING
+    cfg.summary_bias = float("inf")
+    assert N.lib.eva_summarize(ctypes.byref(cfg), P, P, None, P, P, None) == N.EVA_ERR_INVALID_ARG
+    cfg.summary_bias = 0.0
+    cfg.reserved = 1
+    assert N.lib.eva_summarize(ctypes.byref(cfg), P, P, None, P, P, None) == N.EVA_ERR_INVALID_ARG
