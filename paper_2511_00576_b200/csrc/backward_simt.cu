@@ -28,6 +28,7 @@
 // This is the parity-grade first version of the row (SIMT fp32 math); the tcgen05
 // version is future work.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -528,6 +529,15 @@ __global__ void __launch_bounds__(128) bwd_finalize_kernel(eva_config cfg, const
   if ((dt) == EVA_BF16) { using T = __nv_bfloat16; __VA_ARGS__; }               \
   else { using T = float; __VA_ARGS__; }
 
+// EVA_BACKWARD_SIMT=1 forces the SIMT main pass for bf16, d = 128 (parity cross-check knob).
+bool backward_force_simt() {
+  static const bool v = [] {
+    const char* e = getenv("EVA_BACKWARD_SIMT");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+
 }  // namespace
 
 size_t backward_workspace_bytes(const eva_config& cfg) {
@@ -547,13 +557,19 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
   BWD_DISPATCH_T(cfg.dtype, BWD_DISPATCH_D(cfg.d_head, {
     bwd_prep_kernel<T, D><<<dim3((Tn + 3) / 4, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)O,
                                                                          (const T*)dO, ws);
-    const size_t sm = sizeof(MainSmem<D>);
-    err = set_smem_attr((const void*)bwd_main_kernel<T, D>, sm);
-    if (err != cudaSuccess) return err;
-    bwd_main_kernel<T, D><<<dim3(plan.n_sum_items + plan.n_local_items, cfg.bh_count),
-                            BWD_THREADS, sm, s>>>(cfg, (const T*)Q, (const T*)K, (const T*)V,
-                                                  (const T*)Ksum, (const T*)Vsum, (const T*)dO,
-                                                  lse, ws, plan.n_sum_items);
+    if (D == 128 && cfg.dtype == EVA_BF16 && backward_sm100_supported(cfg) && !backward_force_simt()) {
+      err = launch_backward_main_sm100(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws.D, ws.dQ, ws.dK, ws.dV,
+                                       ws.dKs, ws.dVs, s);
+      if (err != cudaSuccess) return err;
+    } else {
+      const size_t sm = sizeof(MainSmem<D>);
+      err = set_smem_attr((const void*)bwd_main_kernel<T, D>, sm);
+      if (err != cudaSuccess) return err;
+      bwd_main_kernel<T, D><<<dim3(plan.n_sum_items + plan.n_local_items, cfg.bh_count),
+                              BWD_THREADS, sm, s>>>(cfg, (const T*)Q, (const T*)K, (const T*)V,
+                                                    (const T*)Ksum, (const T*)Vsum, (const T*)dO,
+                                                    lse, ws, plan.n_sum_items);
+    }
     const int n_tail = (Tn - nC * C + C - 1) / C;
     const size_t fsm = (size_t)(9 * D + 8 + 2 * C) * sizeof(float);
     err = set_smem_attr((const void*)bwd_finalize_kernel<T, D>, fsm);

@@ -1,0 +1,430 @@
+// backward_sm100.cu -- tensor-core (tcgen05/TMEM/TMA) main pass of the FlashEVA prefill
+// backward (the paper trains with it), bf16, d = 128.
+//
+// It replaces bwd_main_kernel of backward_simt.cu for that case and keeps its contract: the
+// prep kernel has written D_n = dO_n . o_n and zeroed the fp32 accumulators, and the finalize
+// kernel applies the summary chain rule (k~ = chunk mean, Eq.15 omega, log-xi softmax).
+//
+// Work item = one unit x one tile of 128 keys (local keys, or 128 summaries k~_c / beta_c
+// with a segment of the query tiles that see them); the CTA walks its 64-query tiles:
+//     S^T  = K Q_i^T                (SS, M=128 keys, N=64 queries, K=d)     TMEM [0,64)
+//     dP^T = V dO_i^T               (SS)                                    TMEM [64,128)
+//     P^T  = exp2(s S^T log2e - lse2),  dS^T = P^T (dP^T - D)   (thread <-> key row; mask)
+//            P^T, dS^T bf16 back into TMEM (A operands), dS^T also into smem (swizzled)
+//     dV  += P^T dO_i               (TS, M=128, N=d, K=64)                   TMEM [256,384)
+//     dK  += dS^T Q_i               (TS)                                    TMEM [384,512)
+//     dQ_i^T = K^T dS^T             (SS, A = K tile MN-major, B = dS^T MN-major; M=d, N=64)
+//            -> fp32 red.global.add into the dQ accumulator (thread <-> channel)
+// Warps: 0 TMA producer (K/V once, Q_i/dO_i through a 2-stage ring), 1 TMEM allocator +
+// single-thread MMA issuer, 2-5 softmax/dS + dQ epilogue + dK/dV write-out.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "launch.h"
+#include "sm100.cuh"
+
+namespace eva {
+namespace {
+
+using namespace sm100;
+constexpr int BK = 128;  // keys per work item (MMA M)
+constexpr int BQ = 64;   // queries per step (MMA N)
+constexpr int NSQ = 2;   // Q / dO ring stages
+constexpr int SEG = 8;   // query tiles per summary work item
+constexpr int BWD_TC_THREADS = 192;
+constexpr uint32_t TM_S = 0, TM_DP = 64, TM_DQ = 128, TM_DV = 256, TM_DK = 384;
+
+template <int D>
+struct __align__(1024) BwdSm {
+  __nv_bfloat16 k[BK * D];        // D/64 sub-tiles [128 keys][64 ch], 16 KB each
+  __nv_bfloat16 v[BK * D];
+  __nv_bfloat16 q[NSQ][BQ * D];   // D/64 sub-tiles [64 queries][64 ch], 8 KB each
+  __nv_bfloat16 dO[NSQ][BQ * D];
+  __nv_bfloat16 ds[BK * BQ];      // dS^T [128 keys][64 queries], 128-byte swizzled rows
+  float dqs[2][BQ * D];           // dQ_i staging [64 queries][d] fp32 for the bulk reduce-add
+  float lse2[2][BQ], Dq[2][BQ];
+  uint64_t kv_full, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free, acc_done;
+  uint32_t tmem_base;
+};
+
+struct BwdWsT {
+  float *D, *dQ, *dK, *dV, *dKs, *dVs;
+};
+
+// Inverse maps of the causal mask (same formulas as backward_simt.cu)
+__host__ __device__ __forceinline__ int64_t qhi_of_key(int64_t m, int C, int W, int mode) {
+  if (mode == EVA_WINDOW_SLIDING) return (m / C + W / C) * (int64_t)C - 1;
+  return (m / W + 1) * (int64_t)W - 1;
+}
+__host__ __device__ __forceinline__ int64_t qlo_of_summary(int64_t c, int C, int W, int mode) {
+  if (mode == EVA_WINDOW_SLIDING) return (c + W / C) * (int64_t)C;
+  return (c / (W / C) + 1) * (int64_t)W;
+}
+__host__ __device__ __forceinline__ int nqt(int T) { return (T + BQ - 1) / BQ; }
+__host__ __device__ __forceinline__ int sum_qt0(int s, int T, int C, int W, int mode) {
+  const int64_t q = qlo_of_summary((int64_t)s * BK, C, W, mode);
+  return q >= T ? nqt(T) : (int)(q / BQ);
+}
+__host__ __device__ __forceinline__ int sum_segs(int s, int T, int C, int W, int mode) {
+  return (nqt(T) - sum_qt0(s, T, C, W, mode) + SEG - 1) / SEG;
+}
+
+// Bulk (non-tensor) reduce-add of `bytes` contiguous fp32 from shared to global memory,
+// performed by the TMA unit at L2 (one instruction per 64 x d tile instead of 64 x d REDs).
+__device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const float* ssrc, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int D>
+__global__ void __launch_bounds__(BWD_TC_THREADS, 1)
+bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
+                      const __grid_constant__ CUtensorMap mKs, const __grid_constant__ CUtensorMap mVs,
+                      const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mdO,
+                      int T, int C, int W, int mode, float scale, const float* __restrict__ lse,
+                      BwdWsT ws, int n_sum_items) {
+  extern __shared__ uint8_t smem_raw[];
+  BwdSm<D>* sm = reinterpret_cast<BwdSm<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.y;
+  const int nC = T / C;
+
+  // ---- work item (identical on every thread)
+  bool is_sum;
+  int k0, nk, qt_begin, qt_end;
+  {
+    int item = blockIdx.x;
+    if (item < n_sum_items) {
+      is_sum = true;
+      int s = 0;
+      for (;; ++s) {
+        const int ns = sum_segs(s, T, C, W, mode);
+        if (item < ns) break;
+        item -= ns;
+      }
+      k0 = s * BK;
+      nk = min(BK, nC - k0);
+      qt_begin = sum_qt0(s, T, C, W, mode) + item * SEG;
+      qt_end = min(nqt(T), qt_begin + SEG);
+    } else {
+      is_sum = false;
+      k0 = (item - n_sum_items) * BK;
+      nk = min(BK, T - k0);
+      qt_begin = k0 / BQ;
+      const int64_t qhi = min((int64_t)T - 1, qhi_of_key(k0 + nk - 1, C, W, mode));
+      qt_end = (int)(qhi / BQ) + 1;
+    }
+  }
+  const int nsteps = max(0, qt_end - qt_begin);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mKs); tma_prefetch(&mVs);
+    tma_prefetch(&mQ); tma_prefetch(&mdO);
+    mbar_init(&sm->kv_full, 1);
+    for (int s = 0; s < NSQ; ++s) {
+      mbar_init(&sm->q_full[s], 1);
+      mbar_init(&sm->q_empty[s], 1);
+    }
+    mbar_init(&sm->s_full, 1);
+    mbar_init(&sm->p_full, 128);
+    mbar_init(&sm->st_free, 1);
+    mbar_init(&sm->dq_full, 1);
+    mbar_init(&sm->dq_free, 128);
+    mbar_init(&sm->acc_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm->tmem_base, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm->tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (nsteps > 0) {
+      if (elect_one()) {
+        const CUtensorMap* mk = is_sum ? &mKs : &mK;
+        const CUtensorMap* mv = is_sum ? &mVs : &mV;
+        mbar_arrive_expect_tx(&sm->kv_full, 2 * BK * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb) {
+          tma_load_3d(sm->k + kb * BK * 64, mk, &sm->kv_full, kb * 64, k0, u);
+          tma_load_3d(sm->v + kb * BK * 64, mv, &sm->kv_full, kb * 64, k0, u);
+        }
+      }
+      __syncwarp();
+      for (int i = 0; i < nsteps; ++i) {
+        const int s = i % NSQ;
+        if (i >= NSQ) mbar_wait(&sm->q_empty[s], ((i / NSQ) - 1) & 1);
+        if (elect_one()) {
+          const int n0 = (qt_begin + i) * BQ;
+          mbar_arrive_expect_tx(&sm->q_full[s], 2 * BQ * D * 2);
+          for (int kb = 0; kb < D / 64; ++kb) {
+            tma_load_3d(sm->q[s] + kb * BQ * 64, &mQ, &sm->q_full[s], kb * 64, n0, u);
+            tma_load_3d(sm->dO[s] + kb * BQ * 64, &mdO, &sm->q_full[s], kb * 64, n0, u);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16_f32(BK, BQ, false);        // S^T, dP^T
+    constexpr uint32_t idesc_g = idesc_bf16_f32(BK, D, true);          // dV, dK (B MN-major)
+    constexpr uint32_t idesc_q = idesc_bf16_f32_ab(D, BQ, true, true); // dQ^T (A, B MN-major)
+    const uint32_t k_addr = smem_u32(sm->k), v_addr = smem_u32(sm->v), ds_addr = smem_u32(sm->ds);
+    if (nsteps > 0) mbar_wait(&sm->kv_full, 0);
+    for (int i = 0; i < nsteps; ++i) {
+      const int s = i % NSQ;
+      const uint32_t q_addr = smem_u32(sm->q[s]), do_addr = smem_u32(sm->dO[s]);
+      mbar_wait(&sm->q_full[s], (i / NSQ) & 1);
+      if (i > 0) mbar_wait(&sm->st_free, (i - 1) & 1);  // dV/dK of the last step read P^T, dS^T
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+          mma_ss(tmem + TM_S, smem_desc_sw128(k_addr + kb * (BK * 128) + off, 16, 1024),
+                 smem_desc_sw128(q_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+          mma_ss(tmem + TM_DP, smem_desc_sw128(v_addr + kb * (BK * 128) + off, 16, 1024),
+                 smem_desc_sw128(do_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm->s_full);
+      }
+      __syncwarp();
+      mbar_wait(&sm->p_full, i & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) {
+          const uint32_t acc = (i > 0 || ks > 0) ? 1u : 0u;
+          mma_ts(tmem + TM_DV, tmem + TM_S + ks * 8, smem_desc_sw128(do_addr + ks * 16 * 128, BQ * 128, 1024),
+                 idesc_g, acc);
+          mma_ts(tmem + TM_DK, tmem + TM_DP + ks * 8, smem_desc_sw128(q_addr + ks * 16 * 128, BQ * 128, 1024),
+                 idesc_g, acc);
+        }
+        mma_commit(&sm->q_empty[s]);
+        mma_commit(&sm->st_free);
+        if (i == nsteps - 1) mma_commit(&sm->acc_done);
+      }
+      __syncwarp();
+      if (i > 0) mbar_wait(&sm->dq_free, (i - 1) & 1);  // the epilogue has read the last dQ^T
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < BK / 16; ++ks)
+          mma_ss(tmem + TM_DQ, smem_desc_sw128(k_addr + ks * 16 * 128, BK * 128, 1024),
+                 smem_desc_sw128(ds_addr + ks * 16 * 128, BQ * 128, 1024), idesc_q, ks > 0 ? 1u : 0u);
+        mma_commit(&sm->dq_full);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / dS / epilogues
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;        // key row of this thread (and dQ^T channel)
+    const int tc = (warp - 2) * 32 + lane;  // 0..127 among the compute warps
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    const int64_t m = (int64_t)k0 + r;
+    int64_t vq_lo = 1, vq_hi = 0;  // queries [vq_lo, vq_hi] see this key
+    if (r < nk) {
+      if (is_sum) {
+        vq_lo = qlo_of_summary(m, C, W, mode);
+        vq_hi = T - 1;
+      } else {
+        vq_lo = m;
+        vq_hi = min((int64_t)T - 1, qhi_of_key(m, C, W, mode));
+      }
+    }
+    const float sl2 = scale * 1.4426950408889634f;
+    uint8_t* dsrow = reinterpret_cast<uint8_t*>(sm->ds) + r * 128;
+    // lse / D of the next query tile are fetched one step ahead (registers of threads < 64)
+    float nx_l = 0.f, nx_d = 0.f;
+    auto fetch = [&](int i) {
+      const int n = (qt_begin + i) * BQ + tc;
+      if (tc < BQ && i < nsteps && n < T) {
+        nx_l = lse[(size_t)u * T + n] * 1.4426950408889634f;
+        nx_d = ws.D[(size_t)u * T + n];
+      } else {
+        nx_l = nx_d = 0.f;
+      }
+    };
+    fetch(0);
+    for (int i = 0; i < nsteps; ++i) {
+      const int n0 = (qt_begin + i) * BQ;
+      const int b = i & 1;
+      if (tc < BQ) {
+        sm->lse2[b][tc] = nx_l;
+        sm->Dq[b][tc] = nx_d;
+      }
+      fetch(i + 1);
+      named_bar_sync(1, 128);
+      mbar_wait(&sm->s_full, i & 1);
+      tc_fence_after();
+      uint32_t sr[64], dr[64];
+      tmem_ld32(t_lane + TM_S, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+      tmem_ld32(t_lane + TM_S + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+      tmem_ld32(t_lane + TM_DP, *reinterpret_cast<uint32_t(*)[32]>(&dr[0]));
+      tmem_ld32(t_lane + TM_DP + 32, *reinterpret_cast<uint32_t(*)[32]>(&dr[32]));
+      tmem_wait_ld();
+      const int vlo = (int)max((int64_t)0, min((int64_t)BQ, vq_lo - n0));
+      const int vhi = (int)max((int64_t)0, min((int64_t)BQ, vq_hi + 1 - n0));
+      uint32_t pk[32], dk[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        float p[2], g[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = 2 * c + e;
+          const bool vis = j >= vlo && j < vhi;
+          p[e] = vis ? exp2f(fmaf(__uint_as_float(sr[j]), sl2, -sm->lse2[b][j])) : 0.f;
+          g[e] = p[e] * (__uint_as_float(dr[j]) - sm->Dq[b][j]);
+        }
+        pk[c] = pack2(p[0], p[1]);
+        dk[c] = pack2(g[0], g[1]);
+      }
+      tmem_st32(t_lane + TM_S, pk);
+      tmem_st32(t_lane + TM_DP, dk);
+      // dS^T row r into shared memory (128-byte swizzled rows: the dQ MMA's B operand)
+#pragma unroll
+      for (int c16 = 0; c16 < 8; ++c16) {
+        uint4 w4;
+        w4.x = dk[4 * c16 + 0];
+        w4.y = dk[4 * c16 + 1];
+        w4.z = dk[4 * c16 + 2];
+        w4.w = dk[4 * c16 + 3];
+        *reinterpret_cast<uint4*>(dsrow + ((c16 ^ (r & 7)) * 16)) = w4;
+      }
+      fence_proxy_async_smem();
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&sm->p_full);
+      // dQ_i^T -> fp32 accumulator (thread <-> channel r)
+      mbar_wait(&sm->dq_full, i & 1);
+      tc_fence_after();
+      uint32_t qv[64];
+      tmem_ld32(t_lane + TM_DQ, *reinterpret_cast<uint32_t(*)[32]>(&qv[0]));
+      tmem_ld32(t_lane + TM_DQ + 32, *reinterpret_cast<uint32_t(*)[32]>(&qv[32]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&sm->dq_free);
+      // stage dQ_i [64 queries][d] (thread <-> column r) and reduce-add it into the fp32
+      // accumulator with one bulk TMA operation; staging is double-buffered, so only the
+      // reduce of step i-2 must have finished reading buffer b
+      if (tc == 0) bulk_wait_read_le1();
+      named_bar_sync(1, 128);
+      float* st = sm->dqs[b] + r;
+#pragma unroll
+      for (int j = 0; j < BQ; ++j) st[j * D] = scale * __uint_as_float(qv[j]);
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (tc == 0) {
+        const int nv = min(BQ, T - n0);
+        bulk_reduce_add_f32(ws.dQ + ((size_t)u * T + n0) * D, sm->dqs[b], (uint32_t)(nv * D * 4));
+        tma_store_commit();
+      }
+    }
+    if (tc == 0) tma_store_wait_all();
+    // ---- dK, dV of this key tile
+    if (nsteps > 0) {
+      mbar_wait(&sm->acc_done, 0);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t kv[32], vv[32];
+      if (nsteps > 0) {
+        tmem_ld32(t_lane + TM_DK + cc * 32, kv);
+        tmem_ld32(t_lane + TM_DV + cc * 32, vv);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) kv[e] = vv[e] = 0u;
+      }
+      if (r < nk) {
+        if (is_sum) {
+          float* dks = ws.dKs + ((size_t)u * nC + m) * D + cc * 32;
+          float* dvs = ws.dVs + ((size_t)u * nC + m) * D + cc * 32;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            atomicAdd(dks + e, scale * __uint_as_float(kv[e]));
+            atomicAdd(dvs + e, __uint_as_float(vv[e]));
+          }
+        } else {
+          float4* dkl = reinterpret_cast<float4*>(ws.dK + ((size_t)u * T + m) * D + cc * 32);
+          float4* dvl = reinterpret_cast<float4*>(ws.dV + ((size_t)u * T + m) * D + cc * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            dkl[e] = make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
+                                 scale * __uint_as_float(kv[4 * e + 2]), scale * __uint_as_float(kv[4 * e + 3]));
+            dvl[e] = make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
+                                 __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3]));
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace
+
+bool backward_sm100_supported(const eva_config& cfg) {
+  CUtensorMap probe;
+  static const bool have_tma = make_tma_map_bf16(&probe, reinterpret_cast<void*>(0x1000), 1, 128, 128, 64);
+  return cfg.dtype == EVA_BF16 && cfg.d_head == 128 && have_tma;
+}
+
+cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                       const void* Ksum, const void* Vsum, const void* dO, const float* lse,
+                                       float* wsD, float* wsdQ, float* wsdK, float* wsdV, float* wsdKs,
+                                       float* wsdVs, cudaStream_t s) {
+  constexpr int D = 128;
+  const int BH = cfg.bh_count, T = cfg.T, C = cfg.chunk, W = cfg.window, nC = T / C;
+  CUtensorMap mK, mV, mKs, mVs, mQ, mdO;
+  bool ok = make_tma_map_bf16(&mK, K, BH, T, D, BK) && make_tma_map_bf16(&mV, V, BH, T, D, BK) &&
+            make_tma_map_bf16(&mQ, Q, BH, T, D, BQ) && make_tma_map_bf16(&mdO, dO, BH, T, D, BQ);
+  if (nC > 0) {
+    ok = ok && make_tma_map_bf16(&mKs, Ksum, BH, nC, D, BK) && make_tma_map_bf16(&mVs, Vsum, BH, nC, D, BK);
+  } else {
+    mKs = mK;
+    mVs = mV;
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  int n_sum_items = 0;
+  for (int st = 0; st * BK < nC; ++st) n_sum_items += sum_segs(st, T, C, W, cfg.mode);
+  const int n_local_items = (T + BK - 1) / BK;
+  const size_t smem = sizeof(BwdSm<D>) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(bwd_main_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  BwdWsT ws{wsD, wsdQ, wsdK, wsdV, wsdKs, wsdVs};
+  bwd_main_sm100_kernel<D><<<dim3(n_sum_items + n_local_items, BH), BWD_TC_THREADS, smem, s>>>(
+      mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale, lse, ws, n_sum_items);
+  return cudaGetLastError();
+}
+
+}  // namespace eva

@@ -1,6 +1,7 @@
 // launch.h -- internal (C++) launchers behind the C ABI in api.cu.
 // Arguments are validated by api.cu before any of these is called.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -81,7 +82,17 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
                             const void* dO, const float* eps, void* dQ, void* dK, void* dV,
                             void* workspace, cudaStream_t s);
 
+// Tensor-core main pass of the backward (backward_sm100.cu): bf16, d = 128.
+bool backward_sm100_supported(const eva_config& cfg);
+cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                       const void* Ksum, const void* Vsum, const void* dO, const float* lse,
+                                       float* wsD, float* wsdQ, float* wsdK, float* wsdV, float* wsdKs,
+                                       float* wsdVs, cudaStream_t s);
+
 int num_sms();
+// 3-D bf16 TMA map over [units, rows, D] with a {64, box_rows, 1} box and 128-byte swizzle
+// (prefill_sm100.cu); false if the driver entry point is unavailable.
+bool make_tma_map_bf16(CUtensorMap* m, const void* base, int units, int rows, int D, int box_rows);
 // Raise a kernel's dynamic shared-memory limit (once per function and size).
 cudaError_t set_smem_attr(const void* fn, size_t bytes);
 

@@ -1694,6 +1694,10 @@ cudaError_t launch_pair(const eva_config& cfg, const void* Q, const void* K, con
 
 }  // namespace
 
+bool make_tma_map_bf16(CUtensorMap* m, const void* base, int units, int rows, int D, int box_rows) {
+  return make_map(m, base, units, rows, D, box_rows);
+}
+
 cudaError_t debug_trace_prefill(const eva_config& cfg, const void* Q, const void* K, const void* V,
                                 const void* Ksum, const void* Vsum, void* O, float* lse,
                                 unsigned long long* trace_dev, int cap, cudaStream_t s) {

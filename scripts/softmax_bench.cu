@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(160, 2) sm_bench(int iters, int full, unsigned
   for (int it = 0; it < iters; ++it) {
     const int vlo = full ? 0 : (lane & 7), vhi = full ? 64 : 60;
     if constexpr (VAR < 0) softmax_tile<D>(t_lane, t_lane + 128, vlo, vhi, 0.18f, m, l, [] {});
-    else softmax_tile2<D, VAR>(t_lane, t_lane + 128, vlo, vhi, 0.18f, m, l, [] {});
+    else softmax_tile2<D, VAR>(t_lane, t_lane + 128, vlo, vhi, 0, 0, 0.f, 0.18f, m, l, [] {});
     // restore S (softmax overwrote the first 32 columns with P)
     {
       uint32_t init[32];

@@ -44,6 +44,7 @@ CASES = [  # (B, H, T, d, C, W)
     (1, 1, 1, 128, 4, 8),         # T = 1
     (1, 1, 96, 64, 1, 3),         # C = 1: exact causal softmax gradients
     (1, 1, 1500, 32, 4, 8),       # 375 chunks: several summary tiles and segments
+    (1, 1, 2200, 128, 8, 16),     # bf16 tensor-core main pass: 3 summary key tiles, ragged tail
 ]
 
 
