@@ -517,6 +517,218 @@ __global__ void __launch_bounds__(128) bwd_finalize_kernel(eva_config cfg, const
   }
 }
 
+// Register-resident finalize (bf16 with 16-byte rows, C <= 8 rows per lane slot): the same
+// chain rule as bwd_finalize_kernel with the chunk's K and V rows loaded once into registers
+// (lane mapping of summarize_chunk_reg: a row is read by TPR = D*2/16 lanes, warp w owns row
+// slots w*RPW + 4*RPW*i) and every reduction done with group shuffles + one smem merge.
+template <typename T, int D, int NI>
+__global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, const T* __restrict__ K,
+                                                               const T* __restrict__ V,
+                                                               const float* __restrict__ eps, BwdWs ws,
+                                                               T* __restrict__ dQ, T* __restrict__ dK,
+                                                               T* __restrict__ dV) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int TPR = D / VEC;
+  constexpr int RPW = 32 / TPR;
+  __shared__ float sh_red[4][D];
+  __shared__ float sh_om[D], sh_g[D], sh_db[D], sh_dkt[D];
+  __shared__ float sh_w[8];
+  const int Tn = cfg.T, C = cfg.chunk, nC = Tn / C;
+  const int u = blockIdx.y, c = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / TPR, gl = lane % TPR, ch0 = gl * VEC;
+  const size_t ub = (size_t)u * Tn;
+  if (c >= nC) {  // tail rows that belong to no complete chunk: copy-out only
+    const int r0 = c * C, r1 = min(Tn, r0 + C);
+    for (int r = r0 + warp; r < r1; r += 4) {
+      const size_t o = (ub + r) * D;
+      for (int j = lane; j < D; j += 32) {
+        dQ[o + j] = Elem<T>::from_f(ws.dQ[o + j]);
+        dK[o + j] = Elem<T>::from_f(ws.dK[o + j]);
+        dV[o + j] = Elem<T>::from_f(ws.dV[o + j]);
+      }
+    }
+    return;
+  }
+  const T* Kc = K + (ub + (size_t)c * C) * D;
+  const T* Vc = V + (ub + (size_t)c * C) * D;
+  const size_t srow = ((size_t)u * nC + c) * D;
+  uint4 kx[NI], vx[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    if (r < C) {
+      kx[i] = ldg16_stream(Kc + (size_t)r * D + ch0);
+      vx[i] = ldg16_stream(Vc + (size_t)r * D + ch0);
+    } else {  // unused slots: zeros (they enter sums with weight 0)
+      kx[i] = make_uint4(0u, 0u, 0u, 0u);
+      vx[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+  // the 4 warps' partial column sums over their rows, merged through sh_red
+  auto merge_cols = [&](float (&acc)[VEC]) {
+#pragma unroll
+    for (int o = TPR; o < 32; o <<= 1)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    if (grp == 0) {
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) sh_red[warp][ch0 + j] = acc[j];
+    }
+  };
+  float acc[VEC];
+  // ---- k~ = mean of the chunk's keys; omega (Eq.15) and d omega / d k~
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    if (r < C) {
+      float k[VEC];
+      unpack16<T>(kx[i], k);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc[j] += k[j];
+    }
+  }
+  merge_cols(acc);
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const int j = threadIdx.x;
+    const float kt = (sh_red[0][j] + sh_red[1][j] + sh_red[2][j] + sh_red[3][j]) * (1.0f / (float)C);
+    const uint32_t bh = (uint32_t)(cfg.bh_begin + u);
+    const float e = eps ? eps[srow + j] : philox_normal1(cfg.seed, cfg.layer, bh, (uint32_t)c, (uint32_t)j);
+    sh_om[j] = omega_of(kt, e, cfg);
+    if (cfg.omega_mode == EVA_OMEGA_AS_PRINTED) {
+      const float x = kt + e;
+      sh_g[j] = (x >= -cfg.clip && x <= cfg.clip) ? cfg.lambda : 0.f;
+    } else {
+      sh_g[j] = 1.f;
+    }
+    sh_db[j] = ws.dVs[srow + j];
+  }
+  __syncthreads();
+  float om[VEC], db[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    om[j] = sh_om[ch0 + j];
+    db[j] = sh_db[ch0 + j];
+  }
+  // ---- a_i = omega . k_i - |k_i|^2 / 2, w = softmax(a) over the chunk
+  float w[NI];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    float part = 0.f;
+    if (r < C) {
+      float k[VEC];
+      unpack16<T>(kx[i], k);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) part += k[j] * (om[j] - 0.5f * k[j]);
+    }
+    part = group_sum<TPR>(part);
+    w[i] = r < C ? part : -INFINITY;
+    mx = fmaxf(mx, w[i]);
+  }
+#pragma unroll
+  for (int o = TPR; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) sh_w[warp] = mx;
+  __syncthreads();
+  const float M = fmaxf(fmaxf(sh_w[0], sh_w[1]), fmaxf(sh_w[2], sh_w[3]));
+  float z = 0.f;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    w[i] = r < C ? __expf(w[i] - M) : 0.f;
+    if (gl == 0) z += w[i];
+  }
+  z = warp_sum(z);
+  if (lane == 0) sh_w[4 + warp] = z;
+  __syncthreads();
+  const float iz = 1.f / (sh_w[4] + sh_w[5] + sh_w[6] + sh_w[7]);
+  // ---- beta = sum_i w_i v_i; s_i = dbeta . v_i
+  float sdv[NI];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    w[i] *= iz;
+    float v[VEC];
+    unpack16<T>(vx[i], v);
+    float part = 0.f;
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      acc[j] += w[i] * v[j];
+      part += db[j] * v[j];
+    }
+    sdv[i] = group_sum<TPR>(part);
+  }
+  merge_cols(acc);
+  __syncthreads();
+  // dbeta . beta (thread ch < D holds beta[ch] * dbeta[ch]; warp sums + smem)
+  float bb = 0.f;
+  if (threadIdx.x < D) {
+    const int j = threadIdx.x;
+    bb = (sh_red[0][j] + sh_red[1][j] + sh_red[2][j] + sh_red[3][j]) * sh_db[j];
+  }
+  bb = warp_sum(bb);
+  __syncthreads();  // everyone has read sh_red (beta); sh_w[0..3] is free
+  if (lane == 0) sh_w[warp] = bb;
+  __syncthreads();
+  const float dbb = sh_w[0] + sh_w[1] + sh_w[2] + sh_w[3];
+  // ---- da_i = w_i (dbeta . v_i - dbeta . beta); d omega = sum_i da_i k_i
+  float da[NI];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    da[i] = w[i] * (sdv[i] - dbb);
+    float k[VEC];
+    unpack16<T>(kx[i], k);
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) acc[j] += da[i] * k[j];
+  }
+  merge_cols(acc);
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const int j = threadIdx.x;
+    const float dom = sh_red[0][j] + sh_red[1][j] + sh_red[2][j] + sh_red[3][j];
+    sh_dkt[j] = (ws.dKs[srow + j] + sh_g[j] * dom) * (1.0f / (float)C);  // d k~ / C
+  }
+  __syncthreads();
+  // ---- the chunk's rows
+  float dkt[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) dkt[j] = sh_dkt[ch0 + j];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int r = warp * RPW + 4 * RPW * i + grp;
+    if (r >= C) continue;
+    const size_t o = (ub + (size_t)c * C + r) * D + ch0;
+    float k[VEC], q[VEC], gk[VEC], gv[VEC];
+    unpack16<T>(kx[i], k);
+#pragma unroll
+    for (int j = 0; j < VEC; j += 4) {
+      const float4 a = *reinterpret_cast<const float4*>(ws.dQ + o + j);
+      const float4 b = *reinterpret_cast<const float4*>(ws.dK + o + j);
+      const float4 e = *reinterpret_cast<const float4*>(ws.dV + o + j);
+      q[j] = a.x; q[j + 1] = a.y; q[j + 2] = a.z; q[j + 3] = a.w;
+      gk[j] = b.x; gk[j + 1] = b.y; gk[j + 2] = b.z; gk[j + 3] = b.w;
+      gv[j] = e.x; gv[j + 1] = e.y; gv[j + 2] = e.z; gv[j + 3] = e.w;
+    }
+    T oq[VEC], ok[VEC], ov[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      oq[j] = Elem<T>::from_f(q[j]);
+      ov[j] = Elem<T>::from_f(gv[j] + w[i] * db[j]);
+      ok[j] = Elem<T>::from_f(gk[j] + da[i] * (om[j] - k[j]) + dkt[j]);
+    }
+    *reinterpret_cast<uint4*>(dQ + o) = *reinterpret_cast<const uint4*>(oq);
+    *reinterpret_cast<uint4*>(dK + o) = *reinterpret_cast<const uint4*>(ok);
+    *reinterpret_cast<uint4*>(dV + o) = *reinterpret_cast<const uint4*>(ov);
+  }
+}
+
 #define BWD_DISPATCH_D(D_, ...)                               \
   switch (D_) {                                               \
     case 16: { constexpr int D = 16; __VA_ARGS__; } break;    \
@@ -571,11 +783,20 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
                                                     lse, ws, plan.n_sum_items);
     }
     const int n_tail = (Tn - nC * C + C - 1) / C;
-    const size_t fsm = (size_t)(9 * D + 8 + 2 * C) * sizeof(float);
-    err = set_smem_attr((const void*)bwd_finalize_kernel<T, D>, fsm);
-    if (err != cudaSuccess) return err;
-    bwd_finalize_kernel<T, D><<<dim3(nC + n_tail, cfg.bh_count), 128, fsm, s>>>(
-        cfg, (const T*)K, (const T*)V, eps, ws, (T*)dQ, (T*)dK, (T*)dV);
+    constexpr int RPW = 32 / (D * (int)sizeof(T) / 16 > 32 ? 32 : D * (int)sizeof(T) / 16);
+    const int ni = (C + 4 * RPW - 1) / (4 * RPW);
+    if (sizeof(T) == 2 && D * sizeof(T) >= 64 && ni <= 8 && !backward_force_simt()) {
+      auto fn = ni <= 2 ? bwd_finalize_reg_kernel<T, D, 2> : ni <= 4 ? bwd_finalize_reg_kernel<T, D, 4>
+                                                                     : bwd_finalize_reg_kernel<T, D, 8>;
+      fn<<<dim3(nC + n_tail, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, ws, (T*)dQ,
+                                                         (T*)dK, (T*)dV);
+    } else {
+      const size_t fsm = (size_t)(9 * D + 8 + 2 * C) * sizeof(float);
+      err = set_smem_attr((const void*)bwd_finalize_kernel<T, D>, fsm);
+      if (err != cudaSuccess) return err;
+      bwd_finalize_kernel<T, D><<<dim3(nC + n_tail, cfg.bh_count), 128, fsm, s>>>(
+          cfg, (const T*)K, (const T*)V, eps, ws, (T*)dQ, (T*)dK, (T*)dV);
+    }
     note_launch(3);
     err = cudaGetLastError();
   }));

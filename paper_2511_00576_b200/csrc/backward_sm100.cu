@@ -35,7 +35,7 @@ constexpr int BK = 128;  // keys per work item (MMA M)
 constexpr int BQ = 64;   // queries per step (MMA N)
 constexpr int NSQ = 2;   // Q / dO ring stages
 constexpr int SEG = 8;   // query tiles per summary work item
-constexpr int BWD_TC_THREADS = 192;
+constexpr int BWD_TC_THREADS = 320;
 constexpr uint32_t TM_S = 0, TM_DP = 64, TM_DQ = 128, TM_DV = 256, TM_DK = 384;
 
 template <int D>
@@ -44,10 +44,11 @@ struct __align__(1024) BwdSm {
   __nv_bfloat16 v[BK * D];
   __nv_bfloat16 q[NSQ][BQ * D];   // D/64 sub-tiles [64 queries][64 ch], 8 KB each
   __nv_bfloat16 dO[NSQ][BQ * D];
-  __nv_bfloat16 ds[BK * BQ];      // dS^T [128 keys][64 queries], 128-byte swizzled rows
-  float dqs[2][BQ * D];           // dQ_i staging [64 queries][d] fp32 for the bulk reduce-add
+  __nv_bfloat16 ds[2][BK * BQ];   // dS^T [128 keys][64 queries], 128-byte swizzled rows, x2
+  float dqs[BQ * D];              // dQ_i staging [64 queries][d] fp32 for the bulk reduce-add
   float lse2[2][BQ], Dq[2][BQ];
-  uint64_t kv_full, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free, acc_done;
+  uint64_t kv_full, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free, ds_free[2],
+      acc_done;
   uint32_t tmem_base;
 };
 
@@ -80,13 +81,31 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const float* ss
                "r"(smem_u32(ssrc)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
 
+// 10 warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2-5 softmax / dS (thread <-> key
+// row), 6-9 dQ epilogue (thread <-> channel).  Per step i the MMA warp issues S(i), dP(i),
+// then dQ(i-1) (its dS buffer was written during step i-1), then -- after the softmax of
+// step i -- dV(i), dK(i); so the softmax of step i+1 overlaps dQ(i) and its epilogue.
 template <int D>
 __global__ void __launch_bounds__(BWD_TC_THREADS, 1)
 bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
@@ -141,6 +160,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     mbar_init(&sm->st_free, 1);
     mbar_init(&sm->dq_full, 1);
     mbar_init(&sm->dq_free, 128);
+    mbar_init(&sm->ds_free[0], 1);
+    mbar_init(&sm->ds_free[1], 1);
     mbar_init(&sm->acc_done, 1);
     fence_mbar_init();
   }
@@ -185,13 +206,27 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     constexpr uint32_t idesc_s = idesc_bf16_f32(BK, BQ, false);        // S^T, dP^T
     constexpr uint32_t idesc_g = idesc_bf16_f32(BK, D, true);          // dV, dK (B MN-major)
     constexpr uint32_t idesc_q = idesc_bf16_f32_ab(D, BQ, true, true); // dQ^T (A, B MN-major)
-    const uint32_t k_addr = smem_u32(sm->k), v_addr = smem_u32(sm->v), ds_addr = smem_u32(sm->ds);
+    const uint32_t k_addr = smem_u32(sm->k), v_addr = smem_u32(sm->v);
+    auto issue_dq = [&](int j) {  // dQ(j)^T = K^T dS^T(j)
+      if (j > 0) mbar_wait(&sm->dq_free, (j - 1) & 1);  // the epilogue has read dQ(j-1)
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t ds_addr = smem_u32(sm->ds[j & 1]);
+#pragma unroll
+        for (int ks = 0; ks < BK / 16; ++ks)
+          mma_ss(tmem + TM_DQ, smem_desc_sw128(k_addr + ks * 16 * 128, BK * 128, 1024),
+                 smem_desc_sw128(ds_addr + ks * 16 * 128, BQ * 128, 1024), idesc_q, ks > 0 ? 1u : 0u);
+        mma_commit(&sm->dq_full);
+        mma_commit(&sm->ds_free[j & 1]);
+      }
+      __syncwarp();
+    };
     if (nsteps > 0) mbar_wait(&sm->kv_full, 0);
     for (int i = 0; i < nsteps; ++i) {
       const int s = i % NSQ;
       const uint32_t q_addr = smem_u32(sm->q[s]), do_addr = smem_u32(sm->dO[s]);
       mbar_wait(&sm->q_full[s], (i / NSQ) & 1);
-      if (i > 0) mbar_wait(&sm->st_free, (i - 1) & 1);  // dV/dK of the last step read P^T, dS^T
+      if (i > 0) mbar_wait(&sm->st_free, (i - 1) & 1);  // dV/dK(i-1) have read P^T, dS^T
       tc_fence_after();
       if (elect_one()) {
 #pragma unroll
@@ -209,6 +244,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         mma_commit(&sm->s_full);
       }
       __syncwarp();
+      if (i > 0) issue_dq(i - 1);
       mbar_wait(&sm->p_full, i & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -225,22 +261,13 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         if (i == nsteps - 1) mma_commit(&sm->acc_done);
       }
       __syncwarp();
-      if (i > 0) mbar_wait(&sm->dq_free, (i - 1) & 1);  // the epilogue has read the last dQ^T
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < BK / 16; ++ks)
-          mma_ss(tmem + TM_DQ, smem_desc_sw128(k_addr + ks * 16 * 128, BK * 128, 1024),
-                 smem_desc_sw128(ds_addr + ks * 16 * 128, BQ * 128, 1024), idesc_q, ks > 0 ? 1u : 0u);
-        mma_commit(&sm->dq_full);
-      }
-      __syncwarp();
     }
-  } else {
-    // ------------------------------------------------------------ softmax / dS / epilogues
+    if (nsteps > 0) issue_dq(nsteps - 1);
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ softmax / dS (thread <-> key row)
     const int quad = warp & 3;
-    const int r = quad * 32 + lane;        // key row of this thread (and dQ^T channel)
-    const int tc = (warp - 2) * 32 + lane;  // 0..127 among the compute warps
+    const int r = quad * 32 + lane;
+    const int tc = (warp - 2) * 32 + lane;  // 0..127 among these warps
     const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
     const int64_t m = (int64_t)k0 + r;
     int64_t vq_lo = 1, vq_hi = 0;  // queries [vq_lo, vq_hi] see this key
@@ -254,7 +281,6 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       }
     }
     const float sl2 = scale * 1.4426950408889634f;
-    uint8_t* dsrow = reinterpret_cast<uint8_t*>(sm->ds) + r * 128;
     // lse / D of the next query tile are fetched one step ahead (registers of threads < 64)
     float nx_l = 0.f, nx_d = 0.f;
     auto fetch = [&](int i) {
@@ -277,71 +303,49 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       fetch(i + 1);
       named_bar_sync(1, 128);
       mbar_wait(&sm->s_full, i & 1);
+      if (i >= 2) mbar_wait(&sm->ds_free[b], ((i >> 1) - 1) & 1);  // dQ(i-2) has read ds[b]
       tc_fence_after();
-      uint32_t sr[64], dr[64];
-      tmem_ld32(t_lane + TM_S, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-      tmem_ld32(t_lane + TM_S + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-      tmem_ld32(t_lane + TM_DP, *reinterpret_cast<uint32_t(*)[32]>(&dr[0]));
-      tmem_ld32(t_lane + TM_DP + 32, *reinterpret_cast<uint32_t(*)[32]>(&dr[32]));
-      tmem_wait_ld();
       const int vlo = (int)max((int64_t)0, min((int64_t)BQ, vq_lo - n0));
       const int vhi = (int)max((int64_t)0, min((int64_t)BQ, vq_hi + 1 - n0));
-      uint32_t pk[32], dk[32];
+      uint8_t* dsrow = reinterpret_cast<uint8_t*>(sm->ds[b]) + r * 128;
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        float p[2], g[2];
+      for (int h = 0; h < 2; ++h) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(t_lane + TM_S + 32 * h, sr);
+        tmem_ld32(t_lane + TM_DP + 32 * h, dr);
+        tmem_wait_ld();
+        uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = 2 * c + e;
-          const bool vis = j >= vlo && j < vhi;
-          p[e] = vis ? exp2f(fmaf(__uint_as_float(sr[j]), sl2, -sm->lse2[b][j])) : 0.f;
-          g[e] = p[e] * (__uint_as_float(dr[j]) - sm->Dq[b][j]);
+        for (int c = 0; c < 16; ++c) {
+          float p[2], g[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int jj = 2 * c + e, j = 32 * h + jj;
+            const bool vis = j >= vlo && j < vhi;
+            p[e] = vis ? ex2f(fmaf(__uint_as_float(sr[jj]), sl2, -sm->lse2[b][j])) : 0.f;
+            g[e] = p[e] * (__uint_as_float(dr[jj]) - sm->Dq[b][j]);
+          }
+          pk[c] = pack2(p[0], p[1]);
+          dk[c] = pack2(g[0], g[1]);
         }
-        pk[c] = pack2(p[0], p[1]);
-        dk[c] = pack2(g[0], g[1]);
-      }
-      tmem_st32(t_lane + TM_S, pk);
-      tmem_st32(t_lane + TM_DP, dk);
-      // dS^T row r into shared memory (128-byte swizzled rows: the dQ MMA's B operand)
+        tmem_st16(t_lane + TM_S + 16 * h, pk);
+        tmem_st16(t_lane + TM_DP + 16 * h, dk);
 #pragma unroll
-      for (int c16 = 0; c16 < 8; ++c16) {
-        uint4 w4;
-        w4.x = dk[4 * c16 + 0];
-        w4.y = dk[4 * c16 + 1];
-        w4.z = dk[4 * c16 + 2];
-        w4.w = dk[4 * c16 + 3];
-        *reinterpret_cast<uint4*>(dsrow + ((c16 ^ (r & 7)) * 16)) = w4;
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int c16 = 4 * h + c4;
+          uint4 w4;
+          w4.x = dk[4 * c4 + 0];
+          w4.y = dk[4 * c4 + 1];
+          w4.z = dk[4 * c4 + 2];
+          w4.w = dk[4 * c4 + 3];
+          *reinterpret_cast<uint4*>(dsrow + ((c16 ^ (r & 7)) * 16)) = w4;
+        }
       }
       fence_proxy_async_smem();
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&sm->p_full);
-      // dQ_i^T -> fp32 accumulator (thread <-> channel r)
-      mbar_wait(&sm->dq_full, i & 1);
-      tc_fence_after();
-      uint32_t qv[64];
-      tmem_ld32(t_lane + TM_DQ, *reinterpret_cast<uint32_t(*)[32]>(&qv[0]));
-      tmem_ld32(t_lane + TM_DQ + 32, *reinterpret_cast<uint32_t(*)[32]>(&qv[32]));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&sm->dq_free);
-      // stage dQ_i [64 queries][d] (thread <-> column r) and reduce-add it into the fp32
-      // accumulator with one bulk TMA operation; staging is double-buffered, so only the
-      // reduce of step i-2 must have finished reading buffer b
-      if (tc == 0) bulk_wait_read_le1();
-      named_bar_sync(1, 128);
-      float* st = sm->dqs[b] + r;
-#pragma unroll
-      for (int j = 0; j < BQ; ++j) st[j * D] = scale * __uint_as_float(qv[j]);
-      fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (tc == 0) {
-        const int nv = min(BQ, T - n0);
-        bulk_reduce_add_f32(ws.dQ + ((size_t)u * T + n0) * D, sm->dqs[b], (uint32_t)(nv * D * 4));
-        tma_store_commit();
-      }
     }
-    if (tc == 0) tma_store_wait_all();
     // ---- dK, dV of this key tile
     if (nsteps > 0) {
       mbar_wait(&sm->acc_done, 0);
@@ -380,6 +384,38 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         }
       }
     }
+  } else {
+    // ------------------------------------------------------------ dQ epilogue (thread <-> channel)
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;          // channel
+    const int et = (warp - 6) * 32 + lane;   // 0..127 among these warps
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    for (int i = 0; i < nsteps; ++i) {
+      const int n0 = (qt_begin + i) * BQ;
+      mbar_wait(&sm->dq_full, i & 1);
+      tc_fence_after();
+      uint32_t qv[64];
+      tmem_ld32(t_lane + TM_DQ, *reinterpret_cast<uint32_t(*)[32]>(&qv[0]));
+      tmem_ld32(t_lane + TM_DQ + 32, *reinterpret_cast<uint32_t(*)[32]>(&qv[32]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&sm->dq_free);
+      // stage dQ_i [64 queries][d] and reduce-add it into the fp32 accumulator with one
+      // bulk TMA operation (the previous reduce must have finished reading the staging)
+      if (et == 0) bulk_wait_read_all();
+      named_bar_sync(2, 128);
+      float* st = sm->dqs + r;
+#pragma unroll
+      for (int j = 0; j < BQ; ++j) st[j * D] = scale * __uint_as_float(qv[j]);
+      fence_proxy_async_smem();
+      named_bar_sync(2, 128);
+      if (et == 0) {
+        const int nv = min(BQ, T - n0);
+        bulk_reduce_add_f32(ws.dQ + ((size_t)u * T + n0) * D, sm->dqs, (uint32_t)(nv * D * 4));
+        tma_store_commit();
+      }
+    }
+    if (et == 0) tma_store_wait_all();
   }
   tc_fence_before();
   __syncthreads();

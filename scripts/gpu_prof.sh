@@ -10,4 +10,6 @@ for k in prefill_cfg3:prefill_sm100_kernel decode_cfg4:decode_kernel summarize_c
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$pat -s 1 -c 1 -o gpurun_out/prof_${w}_${TAG} -f \
       python scripts/prof_kernels.py $w 2 > gpurun_out/ncu_${w}.log 2>&1
 done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:bwd_main_sm100 -s 1 -c 1 -o gpurun_out/prof_bwd_main_${TAG} -f \
+    python scripts/prof_backward.py > gpurun_out/ncu_bwd.log 2>&1
 ls gpurun_out
