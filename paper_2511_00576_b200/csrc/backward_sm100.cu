@@ -33,7 +33,7 @@ namespace {
 using namespace sm100;
 constexpr int BK = 128;  // keys per work item (MMA M)
 constexpr int BQ = 64;   // queries per step (MMA N)
-constexpr int NSQ = 2;   // Q / dO ring stages
+constexpr int NSQ = 3;   // Q / dO ring stages
 constexpr int SEG = 8;   // query tiles per summary work item
 constexpr int BWD_TC_THREADS = 320;
 constexpr uint32_t TM_S = 0, TM_DP = 64, TM_DQ = 128, TM_DV = 256, TM_DK = 384;
@@ -47,8 +47,8 @@ struct __align__(1024) BwdSm {
   __nv_bfloat16 ds[2][BK * BQ];   // dS^T [128 keys][64 queries], 128-byte swizzled rows, x2
   float dqs[BQ * D];              // dQ_i staging [64 queries][d] fp32 for the bulk reduce-add
   float lse2[2][BQ], Dq[2][BQ];
-  uint64_t kv_full, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free, ds_free[2],
-      acc_done;
+  uint64_t kv_full, kv_empty, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free,
+      ds_free[2], acc_done, acc_free;
   uint32_t tmem_base;
 };
 
@@ -102,55 +102,68 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "memory");
 }
 
-// 10 warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2-5 softmax / dS (thread <-> key
-// row), 6-9 dQ epilogue (thread <-> channel).  Per step i the MMA warp issues S(i), dP(i),
-// then dQ(i-1) (its dS buffer was written during step i-1), then -- after the softmax of
-// step i -- dV(i), dK(i); so the softmax of step i+1 overlaps dQ(i) and its epilogue.
+struct Item {
+  bool is_sum;
+  int u, k0, nk, qt_begin, nsteps;
+};
+
+// Work item w of the linearised (unit, item) list: items [0, n_sum_items) of a unit are
+// summary tiles of 128 summaries x SEG query tiles, the rest local tiles of 128 keys.
+__device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum_items, int T, int C, int W,
+                                            int mode) {
+  Item it;
+  it.u = w / items_per_unit;
+  int item = w % items_per_unit;
+  const int nC = T / C;
+  int qt_end;
+  if (item < n_sum_items) {
+    it.is_sum = true;
+    int s = 0;
+    for (;; ++s) {
+      const int ns = sum_segs(s, T, C, W, mode);
+      if (item < ns) break;
+      item -= ns;
+    }
+    it.k0 = s * BK;
+    it.nk = min(BK, nC - it.k0);
+    it.qt_begin = sum_qt0(s, T, C, W, mode) + item * SEG;
+    qt_end = min(nqt(T), it.qt_begin + SEG);
+  } else {
+    it.is_sum = false;
+    it.k0 = (item - n_sum_items) * BK;
+    it.nk = min(BK, T - it.k0);
+    it.qt_begin = it.k0 / BQ;
+    const int64_t qhi = min((int64_t)T - 1, qhi_of_key(it.k0 + it.nk - 1, C, W, mode));
+    qt_end = (int)(qhi / BQ) + 1;
+  }
+  it.nsteps = max(0, qt_end - it.qt_begin);
+  return it;
+}
+
+// Persistent: one CTA per SM walks work items w = blockIdx.x, + gridDim.x, ...  10 warps:
+// 0 TMA producer, 1 TMEM allocator + MMA issuer, 2-5 softmax / dS (thread <-> key row) and
+// the item's dK/dV write-out, 6-9 dQ epilogue (thread <-> channel).  Ring stages and barrier
+// phases follow a step counter g that runs across items.  Per step the MMA warp issues S(g),
+// dP(g), then dQ(g-1) (its dS buffer was written one step earlier), then -- after the
+// softmax -- dV(g), dK(g); so the softmax of step g+1 overlaps dQ(g) and its epilogue, and
+// the next item's K/V load and first MMAs overlap this item's dK/dV write-out.
 template <int D>
 __global__ void __launch_bounds__(BWD_TC_THREADS, 1)
 bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
                       const __grid_constant__ CUtensorMap mKs, const __grid_constant__ CUtensorMap mVs,
                       const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mdO,
                       int T, int C, int W, int mode, float scale, const float* __restrict__ lse,
-                      BwdWsT ws, int n_sum_items) {
+                      BwdWsT ws, int n_sum_items, int items_per_unit, int n_items) {
   extern __shared__ uint8_t smem_raw[];
   BwdSm<D>* sm = reinterpret_cast<BwdSm<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.y;
   const int nC = T / C;
-
-  // ---- work item (identical on every thread)
-  bool is_sum;
-  int k0, nk, qt_begin, qt_end;
-  {
-    int item = blockIdx.x;
-    if (item < n_sum_items) {
-      is_sum = true;
-      int s = 0;
-      for (;; ++s) {
-        const int ns = sum_segs(s, T, C, W, mode);
-        if (item < ns) break;
-        item -= ns;
-      }
-      k0 = s * BK;
-      nk = min(BK, nC - k0);
-      qt_begin = sum_qt0(s, T, C, W, mode) + item * SEG;
-      qt_end = min(nqt(T), qt_begin + SEG);
-    } else {
-      is_sum = false;
-      k0 = (item - n_sum_items) * BK;
-      nk = min(BK, T - k0);
-      qt_begin = k0 / BQ;
-      const int64_t qhi = min((int64_t)T - 1, qhi_of_key(k0 + nk - 1, C, W, mode));
-      qt_end = (int)(qhi / BQ) + 1;
-    }
-  }
-  const int nsteps = max(0, qt_end - qt_begin);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mKs); tma_prefetch(&mVs);
     tma_prefetch(&mQ); tma_prefetch(&mdO);
     mbar_init(&sm->kv_full, 1);
+    mbar_init(&sm->kv_empty, 1);
     for (int s = 0; s < NSQ; ++s) {
       mbar_init(&sm->q_full[s], 1);
       mbar_init(&sm->q_empty[s], 1);
@@ -163,6 +176,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     mbar_init(&sm->ds_free[0], 1);
     mbar_init(&sm->ds_free[1], 1);
     mbar_init(&sm->acc_done, 1);
+    mbar_init(&sm->acc_free, 128);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -173,33 +187,44 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
+  auto item_of = [&](int w) { return decode_item(w, items_per_unit, n_sum_items, T, C, W, mode); };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (nsteps > 0) {
+    int g = 0, kcount = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const Item it = item_of(w);
+      if (it.nsteps == 0) continue;
+      if (kcount > 0) mbar_wait(&sm->kv_empty, (kcount - 1) & 1);  // last item's dQ MMA is done
       if (elect_one()) {
-        const CUtensorMap* mk = is_sum ? &mKs : &mK;
-        const CUtensorMap* mv = is_sum ? &mVs : &mV;
+        const CUtensorMap* mk = it.is_sum ? &mKs : &mK;
+        const CUtensorMap* mv = it.is_sum ? &mVs : &mV;
         mbar_arrive_expect_tx(&sm->kv_full, 2 * BK * D * 2);
         for (int kb = 0; kb < D / 64; ++kb) {
-          tma_load_3d(sm->k + kb * BK * 64, mk, &sm->kv_full, kb * 64, k0, u);
-          tma_load_3d(sm->v + kb * BK * 64, mv, &sm->kv_full, kb * 64, k0, u);
+          tma_load_3d(sm->k + kb * BK * 64, mk, &sm->kv_full, kb * 64, it.k0, it.u);
+          tma_load_3d(sm->v + kb * BK * 64, mv, &sm->kv_full, kb * 64, it.k0, it.u);
         }
+        for (int i = NSQ; i < it.nsteps; ++i)  // later Q / dO tiles of the item into L2
+          for (int kb = 0; kb < D / 64; ++kb) {
+            tma_prefetch_l2_3d(&mQ, kb * 64, (it.qt_begin + i) * BQ, it.u);
+            tma_prefetch_l2_3d(&mdO, kb * 64, (it.qt_begin + i) * BQ, it.u);
+          }
       }
       __syncwarp();
-      for (int i = 0; i < nsteps; ++i) {
-        const int s = i % NSQ;
-        if (i >= NSQ) mbar_wait(&sm->q_empty[s], ((i / NSQ) - 1) & 1);
+      for (int i = 0; i < it.nsteps; ++i, ++g) {
+        const int s = g % NSQ;
+        if (g >= NSQ) mbar_wait(&sm->q_empty[s], ((g / NSQ) - 1) & 1);
         if (elect_one()) {
-          const int n0 = (qt_begin + i) * BQ;
+          const int n0 = (it.qt_begin + i) * BQ;
           mbar_arrive_expect_tx(&sm->q_full[s], 2 * BQ * D * 2);
           for (int kb = 0; kb < D / 64; ++kb) {
-            tma_load_3d(sm->q[s] + kb * BQ * 64, &mQ, &sm->q_full[s], kb * 64, n0, u);
-            tma_load_3d(sm->dO[s] + kb * BQ * 64, &mdO, &sm->q_full[s], kb * 64, n0, u);
+            tma_load_3d(sm->q[s] + kb * BQ * 64, &mQ, &sm->q_full[s], kb * 64, n0, it.u);
+            tma_load_3d(sm->dO[s] + kb * BQ * 64, &mdO, &sm->q_full[s], kb * 64, n0, it.u);
           }
         }
         __syncwarp();
       }
+      ++kcount;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -207,7 +232,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     constexpr uint32_t idesc_g = idesc_bf16_f32(BK, D, true);          // dV, dK (B MN-major)
     constexpr uint32_t idesc_q = idesc_bf16_f32_ab(D, BQ, true, true); // dQ^T (A, B MN-major)
     const uint32_t k_addr = smem_u32(sm->k), v_addr = smem_u32(sm->v);
-    auto issue_dq = [&](int j) {  // dQ(j)^T = K^T dS^T(j)
+    auto issue_dq = [&](int j) {  // dQ(j)^T = K^T dS^T(j), global step j
       if (j > 0) mbar_wait(&sm->dq_free, (j - 1) & 1);  // the epilogue has read dQ(j-1)
       tc_fence_after();
       if (elect_one()) {
@@ -221,168 +246,173 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       }
       __syncwarp();
     };
-    if (nsteps > 0) mbar_wait(&sm->kv_full, 0);
-    for (int i = 0; i < nsteps; ++i) {
-      const int s = i % NSQ;
-      const uint32_t q_addr = smem_u32(sm->q[s]), do_addr = smem_u32(sm->dO[s]);
-      mbar_wait(&sm->q_full[s], (i / NSQ) & 1);
-      if (i > 0) mbar_wait(&sm->st_free, (i - 1) & 1);  // dV/dK(i-1) have read P^T, dS^T
-      tc_fence_after();
-      if (elect_one()) {
+    int g = 0, kcount = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const Item it = item_of(w);
+      if (it.nsteps == 0) continue;
+      mbar_wait(&sm->kv_full, kcount & 1);
+      for (int i = 0; i < it.nsteps; ++i, ++g) {
+        const int s = g % NSQ;
+        const uint32_t q_addr = smem_u32(sm->q[s]), do_addr = smem_u32(sm->dO[s]);
+        mbar_wait(&sm->q_full[s], (g / NSQ) & 1);
+        if (g > 0) mbar_wait(&sm->st_free, (g - 1) & 1);  // dV/dK(g-1) have read P^T, dS^T
+        tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
-          mma_ss(tmem + TM_S, smem_desc_sw128(k_addr + kb * (BK * 128) + off, 16, 1024),
-                 smem_desc_sw128(q_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
-        }
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+            mma_ss(tmem + TM_S, smem_desc_sw128(k_addr + kb * (BK * 128) + off, 16, 1024),
+                   smem_desc_sw128(q_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+          }
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {
-          const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
-          mma_ss(tmem + TM_DP, smem_desc_sw128(v_addr + kb * (BK * 128) + off, 16, 1024),
-                 smem_desc_sw128(do_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+            mma_ss(tmem + TM_DP, smem_desc_sw128(v_addr + kb * (BK * 128) + off, 16, 1024),
+                   smem_desc_sw128(do_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+          }
+          mma_commit(&sm->s_full);
         }
-        mma_commit(&sm->s_full);
+        __syncwarp();
+        if (i > 0) issue_dq(g - 1);
+        mbar_wait(&sm->p_full, g & 1);
+        if (i == 0 && kcount > 0) mbar_wait(&sm->acc_free, (kcount - 1) & 1);  // dK/dV drained
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < BQ / 16; ++ks) {
+            const uint32_t acc = (i > 0 || ks > 0) ? 1u : 0u;
+            mma_ts(tmem + TM_DV, tmem + TM_S + ks * 8, smem_desc_sw128(do_addr + ks * 16 * 128, BQ * 128, 1024),
+                   idesc_g, acc);
+            mma_ts(tmem + TM_DK, tmem + TM_DP + ks * 8, smem_desc_sw128(q_addr + ks * 16 * 128, BQ * 128, 1024),
+                   idesc_g, acc);
+          }
+          mma_commit(&sm->q_empty[s]);
+          mma_commit(&sm->st_free);
+          if (i == it.nsteps - 1) mma_commit(&sm->acc_done);
+        }
+        __syncwarp();
       }
+      issue_dq(g - 1);
+      if (elect_one()) mma_commit(&sm->kv_empty);  // K/V smem free once this dQ completes
       __syncwarp();
-      if (i > 0) issue_dq(i - 1);
-      mbar_wait(&sm->p_full, i & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) {
-          const uint32_t acc = (i > 0 || ks > 0) ? 1u : 0u;
-          mma_ts(tmem + TM_DV, tmem + TM_S + ks * 8, smem_desc_sw128(do_addr + ks * 16 * 128, BQ * 128, 1024),
-                 idesc_g, acc);
-          mma_ts(tmem + TM_DK, tmem + TM_DP + ks * 8, smem_desc_sw128(q_addr + ks * 16 * 128, BQ * 128, 1024),
-                 idesc_g, acc);
-        }
-        mma_commit(&sm->q_empty[s]);
-        mma_commit(&sm->st_free);
-        if (i == nsteps - 1) mma_commit(&sm->acc_done);
-      }
-      __syncwarp();
+      ++kcount;
     }
-    if (nsteps > 0) issue_dq(nsteps - 1);
   } else if (warp < 6) {
     // ------------------------------------------------------------ softmax / dS (thread <-> key row)
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const int tc = (warp - 2) * 32 + lane;  // 0..127 among these warps
     const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
-    const int64_t m = (int64_t)k0 + r;
-    int64_t vq_lo = 1, vq_hi = 0;  // queries [vq_lo, vq_hi] see this key
-    if (r < nk) {
-      if (is_sum) {
-        vq_lo = qlo_of_summary(m, C, W, mode);
-        vq_hi = T - 1;
-      } else {
-        vq_lo = m;
-        vq_hi = min((int64_t)T - 1, qhi_of_key(m, C, W, mode));
-      }
-    }
     const float sl2 = scale * 1.4426950408889634f;
-    // lse / D of the next query tile are fetched one step ahead (registers of threads < 64)
-    float nx_l = 0.f, nx_d = 0.f;
-    auto fetch = [&](int i) {
-      const int n = (qt_begin + i) * BQ + tc;
-      if (tc < BQ && i < nsteps && n < T) {
-        nx_l = lse[(size_t)u * T + n] * 1.4426950408889634f;
-        nx_d = ws.D[(size_t)u * T + n];
-      } else {
-        nx_l = nx_d = 0.f;
+    int g = 0, kcount = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const Item it = item_of(w);
+      if (it.nsteps == 0) {  // a local tile no query sees cannot occur; summaries need no zeros
+        continue;
       }
-    };
-    fetch(0);
-    for (int i = 0; i < nsteps; ++i) {
-      const int n0 = (qt_begin + i) * BQ;
-      const int b = i & 1;
-      if (tc < BQ) {
-        sm->lse2[b][tc] = nx_l;
-        sm->Dq[b][tc] = nx_d;
+      const int u = it.u;
+      const int64_t m = (int64_t)it.k0 + r;
+      int64_t vq_lo = 1, vq_hi = 0;  // queries [vq_lo, vq_hi] see this key
+      if (r < it.nk) {
+        if (it.is_sum) {
+          vq_lo = qlo_of_summary(m, C, W, mode);
+          vq_hi = T - 1;
+        } else {
+          vq_lo = m;
+          vq_hi = min((int64_t)T - 1, qhi_of_key(m, C, W, mode));
+        }
       }
-      fetch(i + 1);
-      named_bar_sync(1, 128);
-      mbar_wait(&sm->s_full, i & 1);
-      if (i >= 2) mbar_wait(&sm->ds_free[b], ((i >> 1) - 1) & 1);  // dQ(i-2) has read ds[b]
-      tc_fence_after();
-      const int vlo = (int)max((int64_t)0, min((int64_t)BQ, vq_lo - n0));
-      const int vhi = (int)max((int64_t)0, min((int64_t)BQ, vq_hi + 1 - n0));
-      uint8_t* dsrow = reinterpret_cast<uint8_t*>(sm->ds[b]) + r * 128;
+      for (int i = 0; i < it.nsteps; ++i, ++g) {
+        const int n0 = (it.qt_begin + i) * BQ;
+        const int b = g & 1;
+        if (tc < BQ) {
+          const int n = n0 + tc;
+          sm->lse2[b][tc] = n < T ? lse[(size_t)u * T + n] * 1.4426950408889634f : 0.f;
+          sm->Dq[b][tc] = n < T ? ws.D[(size_t)u * T + n] : 0.f;
+        }
+        named_bar_sync(1, 128);
+        mbar_wait(&sm->s_full, g & 1);
+        if (g >= 2) mbar_wait(&sm->ds_free[b], ((g >> 1) - 1) & 1);  // dQ(g-2) has read ds[b]
+        tc_fence_after();
+        const int vlo = (int)max((int64_t)0, min((int64_t)BQ, vq_lo - n0));
+        const int vhi = (int)max((int64_t)0, min((int64_t)BQ, vq_hi + 1 - n0));
+        const float* lse2 = sm->lse2[b];
+        const float* Dq = sm->Dq[b];
+        uint8_t* dsrow = reinterpret_cast<uint8_t*>(sm->ds[b]) + r * 128;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(t_lane + TM_S + 32 * h, sr);
-        tmem_ld32(t_lane + TM_DP + 32 * h, dr);
-        tmem_wait_ld();
-        uint32_t pk[16], dk[16];
+        for (int h = 0; h < 2; ++h) {
+          uint32_t sr[32], dr[32];
+          tmem_ld32(t_lane + TM_S + 32 * h, sr);
+          tmem_ld32(t_lane + TM_DP + 32 * h, dr);
+          tmem_wait_ld();
+          uint32_t pk[16], dk[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float p[2], g[2];
+          for (int c = 0; c < 16; ++c) {
+            float p[2], gg[2];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int jj = 2 * c + e, j = 32 * h + jj;
-            const bool vis = j >= vlo && j < vhi;
-            p[e] = vis ? ex2f(fmaf(__uint_as_float(sr[jj]), sl2, -sm->lse2[b][j])) : 0.f;
-            g[e] = p[e] * (__uint_as_float(dr[jj]) - sm->Dq[b][j]);
+            for (int e = 0; e < 2; ++e) {
+              const int jj = 2 * c + e, j = 32 * h + jj;
+              const bool vis = j >= vlo && j < vhi;
+              p[e] = vis ? ex2f(fmaf(__uint_as_float(sr[jj]), sl2, -lse2[j])) : 0.f;
+              gg[e] = p[e] * (__uint_as_float(dr[jj]) - Dq[j]);
+            }
+            pk[c] = pack2(p[0], p[1]);
+            dk[c] = pack2(gg[0], gg[1]);
           }
-          pk[c] = pack2(p[0], p[1]);
-          dk[c] = pack2(g[0], g[1]);
-        }
-        tmem_st16(t_lane + TM_S + 16 * h, pk);
-        tmem_st16(t_lane + TM_DP + 16 * h, dk);
+          tmem_st16(t_lane + TM_S + 16 * h, pk);
+          tmem_st16(t_lane + TM_DP + 16 * h, dk);
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          const int c16 = 4 * h + c4;
-          uint4 w4;
-          w4.x = dk[4 * c4 + 0];
-          w4.y = dk[4 * c4 + 1];
-          w4.z = dk[4 * c4 + 2];
-          w4.w = dk[4 * c4 + 3];
-          *reinterpret_cast<uint4*>(dsrow + ((c16 ^ (r & 7)) * 16)) = w4;
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const int c16 = 4 * h + c4;
+            uint4 w4;
+            w4.x = dk[4 * c4 + 0];
+            w4.y = dk[4 * c4 + 1];
+            w4.z = dk[4 * c4 + 2];
+            w4.w = dk[4 * c4 + 3];
+            *reinterpret_cast<uint4*>(dsrow + ((c16 ^ (r & 7)) * 16)) = w4;
+          }
         }
+        fence_proxy_async_smem();
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&sm->p_full);
       }
-      fence_proxy_async_smem();
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&sm->p_full);
-    }
-    // ---- dK, dV of this key tile
-    if (nsteps > 0) {
-      mbar_wait(&sm->acc_done, 0);
+      // ---- dK, dV of this key tile: drain TMEM, release it, then write to global
+      mbar_wait(&sm->acc_done, kcount & 1);
       tc_fence_after();
-    }
 #pragma unroll 1
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t kv[32], vv[32];
-      if (nsteps > 0) {
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t kv[32], vv[32];
         tmem_ld32(t_lane + TM_DK + cc * 32, kv);
         tmem_ld32(t_lane + TM_DV + cc * 32, vv);
         tmem_wait_ld();
-      } else {
+        if (cc == D / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&sm->acc_free);
+        }
+        if (r < it.nk) {
+          if (it.is_sum) {
+            float* dks = ws.dKs + ((size_t)u * nC + m) * D + cc * 32;
+            float* dvs = ws.dVs + ((size_t)u * nC + m) * D + cc * 32;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) kv[e] = vv[e] = 0u;
-      }
-      if (r < nk) {
-        if (is_sum) {
-          float* dks = ws.dKs + ((size_t)u * nC + m) * D + cc * 32;
-          float* dvs = ws.dVs + ((size_t)u * nC + m) * D + cc * 32;
+            for (int e = 0; e < 32; ++e) {
+              atomicAdd(dks + e, scale * __uint_as_float(kv[e]));
+              atomicAdd(dvs + e, __uint_as_float(vv[e]));
+            }
+          } else {
+            float4* dkl = reinterpret_cast<float4*>(ws.dK + ((size_t)u * T + m) * D + cc * 32);
+            float4* dvl = reinterpret_cast<float4*>(ws.dV + ((size_t)u * T + m) * D + cc * 32);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            atomicAdd(dks + e, scale * __uint_as_float(kv[e]));
-            atomicAdd(dvs + e, __uint_as_float(vv[e]));
-          }
-        } else {
-          float4* dkl = reinterpret_cast<float4*>(ws.dK + ((size_t)u * T + m) * D + cc * 32);
-          float4* dvl = reinterpret_cast<float4*>(ws.dV + ((size_t)u * T + m) * D + cc * 32);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            dkl[e] = make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
-                                 scale * __uint_as_float(kv[4 * e + 2]), scale * __uint_as_float(kv[4 * e + 3]));
-            dvl[e] = make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
-                                 __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3]));
+            for (int e = 0; e < 8; ++e) {
+              dkl[e] = make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
+                                   scale * __uint_as_float(kv[4 * e + 2]), scale * __uint_as_float(kv[4 * e + 3]));
+              dvl[e] = make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
+                                   __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3]));
+            }
           }
         }
       }
+      ++kcount;
     }
   } else {
     // ------------------------------------------------------------ dQ epilogue (thread <-> channel)
@@ -390,32 +420,37 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     const int r = quad * 32 + lane;          // channel
     const int et = (warp - 6) * 32 + lane;   // 0..127 among these warps
     const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
-    for (int i = 0; i < nsteps; ++i) {
-      const int n0 = (qt_begin + i) * BQ;
-      mbar_wait(&sm->dq_full, i & 1);
-      tc_fence_after();
-      uint32_t qv[64];
-      tmem_ld32(t_lane + TM_DQ, *reinterpret_cast<uint32_t(*)[32]>(&qv[0]));
-      tmem_ld32(t_lane + TM_DQ + 32, *reinterpret_cast<uint32_t(*)[32]>(&qv[32]));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&sm->dq_free);
-      // stage dQ_i [64 queries][d] and reduce-add it into the fp32 accumulator with one
-      // bulk TMA operation (the previous reduce must have finished reading the staging)
-      if (et == 0) bulk_wait_read_all();
-      named_bar_sync(2, 128);
-      float* st = sm->dqs + r;
+    int g = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+      const Item it = item_of(w);
+      for (int i = 0; i < it.nsteps; ++i, ++g) {
+        const int n0 = (it.qt_begin + i) * BQ;
+        mbar_wait(&sm->dq_full, g & 1);
+        tc_fence_after();
+        uint32_t qv[64];
+        tmem_ld32(t_lane + TM_DQ, *reinterpret_cast<uint32_t(*)[32]>(&qv[0]));
+        tmem_ld32(t_lane + TM_DQ + 32, *reinterpret_cast<uint32_t(*)[32]>(&qv[32]));
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&sm->dq_free);
+        // stage dQ [64 queries][d] and reduce-add it into the fp32 accumulator with one bulk
+        // TMA operation (the previous reduce must have finished reading the staging buffer)
+        if (et == 0) bulk_wait_read_all();
+        named_bar_sync(2, 128);
+        float* st = sm->dqs + r;
 #pragma unroll
-      for (int j = 0; j < BQ; ++j) st[j * D] = scale * __uint_as_float(qv[j]);
-      fence_proxy_async_smem();
-      named_bar_sync(2, 128);
-      if (et == 0) {
-        const int nv = min(BQ, T - n0);
-        bulk_reduce_add_f32(ws.dQ + ((size_t)u * T + n0) * D, sm->dqs, (uint32_t)(nv * D * 4));
-        tma_store_commit();
+        for (int j = 0; j < BQ; ++j) st[j * D] = scale * __uint_as_float(qv[j]);
+        fence_proxy_async_smem();
+        named_bar_sync(2, 128);
+        if (et == 0) {
+          const int nv = min(BQ, T - n0);
+          bulk_reduce_add_f32(ws.dQ + ((size_t)it.u * T + n0) * D, sm->dqs, (uint32_t)(nv * D * 4));
+          tma_store_commit();
+        }
       }
     }
-    if (et == 0) tma_store_wait_all();
+    if (et == 0) bulk_wait_read_all();  // smem may be released once read; the global
+                                         // reduction completes asynchronously before grid end
   }
   tc_fence_before();
   __syncthreads();
@@ -458,8 +493,11 @@ cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, con
     attr = true;
   }
   BwdWsT ws{wsD, wsdQ, wsdK, wsdV, wsdKs, wsdVs};
-  bwd_main_sm100_kernel<D><<<dim3(n_sum_items + n_local_items, BH), BWD_TC_THREADS, smem, s>>>(
-      mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale, lse, ws, n_sum_items);
+  const int items_per_unit = n_sum_items + n_local_items;
+  const int n_items = items_per_unit * BH;
+  const int grid = std::max(1, std::min(n_items, num_sms()));
+  bwd_main_sm100_kernel<D><<<grid, BWD_TC_THREADS, smem, s>>>(
+      mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale, lse, ws, n_sum_items, items_per_unit, n_items);
   return cudaGetLastError();
 }
 

@@ -18,7 +18,10 @@ def dram_bytes(rep):
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         i = hdr.index(k)
         tot += float(r[i].replace(",", "")) * UNIT[units[i]]
-    return tot, float(r[hdr.index("gpu__time_duration.sum")].replace(",", "")), r[hdr.index("Kernel Name")].split("(")[0]
+    ti = hdr.index("gpu__time_duration.sum")
+    t_us = float(r[ti].replace(",", "")) * {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                                           "nsecond": 1e-3, "second": 1e6}.get(units[ti], 1.0)
+    return tot, t_us, r[hdr.index("Kernel Name")].split("(")[0]
 
 
 def main():
