@@ -40,15 +40,22 @@ constexpr int NTHREADS = 192;
 constexpr uint32_t TMEM_COLS = 256;
 constexpr uint32_t TM_O = 128;
 
+// NSTAGE < 10: NSTAGE K and NSTAGE V slots.  NSTAGE = 10*NSK + NSV: separate ring depths
+// (a deeper K ring lets the next K tiles stream in earlier; K is consumed one softmax period
+// before V).  Deep-ring layouts are sized to fill the SM with two CTAs, so they are used
+// without the 1 KB alignment pad (the dynamic window is 1 KB aligned; checked in-kernel).
 template <int D, int NSTAGE>
 struct __align__(1024) Smem {
+  static constexpr int NSK = NSTAGE >= 10 ? NSTAGE / 10 : NSTAGE;
+  static constexpr int NSV = NSTAGE >= 10 ? NSTAGE % 10 : NSTAGE;
+  static constexpr size_t PAD = NSTAGE >= 10 ? 0 : 1024;
   __nv_bfloat16 q[BM * D];               // D/64 sub-tiles [128][64], 16 KB each
-  __nv_bfloat16 k[NSTAGE][BN * D];       // D/64 sub-tiles [64][64], 8 KB each
-  __nv_bfloat16 v[NSTAGE][BN * D];
+  __nv_bfloat16 k[NSK][BN * D];          // D/64 sub-tiles [64][64], 8 KB each
+  __nv_bfloat16 v[NSV][BN * D];
   uint64_t q_full;
   // K and V slots are released separately: a K slot as soon as its S MMA completed, a V
   // slot after its PV MMA, so the next K tiles stream in one softmax period earlier.
-  uint64_t k_full[NSTAGE], v_full[NSTAGE], k_empty[NSTAGE], v_empty[NSTAGE];
+  uint64_t k_full[NSK], v_full[NSV], k_empty[NSK], v_empty[NSV];
   uint64_t s_full[2], p_full[2], o_done, o_final;
   uint32_t tmem_base;
 };
@@ -323,25 +330,34 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
                      const PrefillRange rg, int C, int W, int mode, float scale_log2,
                      float bias_log2, float* __restrict__ lse) {
   extern __shared__ uint8_t smem_raw[];
-  Smem<D, NSTAGE>* sm = reinterpret_cast<Smem<D, NSTAGE>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  using SM = Smem<D, NSTAGE>;
+  constexpr int NSK = SM::NSK, NSV = SM::NSV;
+  if constexpr (SM::PAD == 0) {
+    if ((reinterpret_cast<uintptr_t>(smem_raw) & 1023) != 0) __trap();
+  }
+  SM* sm = reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.y;
   const RangePlan plan(blockIdx.x, rg, C, W, mode);
   const int qrow = blockIdx.x * BM;  // TMA row of this query tile in Q / O
   const int NT = plan.count();
-  __shared__ TileTrace tlog_s;
-  TileTrace* tl = &tlog_s;
-  if (TRACE && threadIdx.x < TT_ROLES) tl->n[threadIdx.x] = 0;
+  TileTrace* tl = nullptr;
+  if constexpr (TRACE) {
+    __shared__ TileTrace tlog_s;
+    tl = &tlog_s;
+    if (threadIdx.x < TT_ROLES) tl->n[threadIdx.x] = 0;
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
     tma_prefetch(&mKs); tma_prefetch(&mVs); tma_prefetch(&mO);
     mbar_init(&sm->q_full, 1);
-    for (int s = 0; s < NSTAGE; ++s) {
+    for (int s = 0; s < NSK; ++s) {
       mbar_init(&sm->k_full[s], 1);
-      mbar_init(&sm->v_full[s], 1);
       mbar_init(&sm->k_empty[s], 1);
+    }
+    for (int s = 0; s < NSV; ++s) {
+      mbar_init(&sm->v_full[s], 1);
       mbar_init(&sm->v_empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -378,7 +394,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       // The ring holds only NSTAGE tiles; pull every later K/V tile of this CTA into L2 now
       // so its TMA load later on is an L2 hit instead of a full DRAM round trip.
       if (elect_one()) {
-      for (int j = NSTAGE; j < NT; ++j) {
+      for (int j = NSV < NSK ? NSV : NSK; j < NT; ++j) {
         const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
         const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
         for (int kb = 0; kb < D / 64; ++kb) {
@@ -392,8 +408,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     // Issue order K(0), K(1), V(0), K(2), V(1), ...: K(j+1) waits only for S(j+1-NSTAGE)
     // to finish reading its slot, V(j) for PV(j-NSTAGE).
     auto load_k = [&](int j) {
-      const int s = j % NSTAGE;
-      if (j >= NSTAGE) mbar_wait(&sm->k_empty[s], ((j / NSTAGE) - 1) & 1);
+      const int s = j % NSK;
+      if (j >= NSK) mbar_wait(&sm->k_empty[s], ((j / NSK) - 1) & 1);
       if (lane == 0) tt<TRACE>(tl, 0, 11, j);
       const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
       if (elect_one()) {
@@ -405,8 +421,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       if (lane == 0) tt<TRACE>(tl, 0, 12, j);
     };
     auto load_v = [&](int j) {
-      const int s = j % NSTAGE;
-      if (j >= NSTAGE) mbar_wait(&sm->v_empty[s], ((j / NSTAGE) - 1) & 1);
+      const int s = j % NSV;
+      if (j >= NSV) mbar_wait(&sm->v_empty[s], ((j / NSV) - 1) & 1);
       const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
       if (elect_one()) {
         mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
@@ -432,8 +448,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     if (lane == 0) tt<TRACE>(tl, 1, 2, 0);
     for (int j = 0; j <= NT; ++j) {
       if (j < NT) {
-        const int s = j % NSTAGE;
-        mbar_wait(&sm->k_full[s], (j / NSTAGE) & 1);
+        const int s = j % NSK;
+        mbar_wait(&sm->k_full[s], (j / NSK) & 1);
         if (lane == 0) tt<TRACE>(tl, 1, 3, j);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sm->k[s]);
@@ -453,10 +469,10 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         if (lane == 0) tt<TRACE>(tl, 1, 4, j);
       }
       if (j >= 1) {
-        const int jj = j - 1, s = jj % NSTAGE;
+        const int jj = j - 1, s = jj % NSV;
         mbar_wait(&sm->p_full[jj & 1], (jj >> 1) & 1);
         if (lane == 0) tt<TRACE>(tl, 1, 5, jj);
-        mbar_wait(&sm->v_full[s], (jj / NSTAGE) & 1);
+        mbar_wait(&sm->v_full[s], (jj / NSV) & 1);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sm->v[s]);
         if (elect_one()) {
@@ -1581,7 +1597,7 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
     mVs = mV;
   }
   if (!ok) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(Smem<D, NSTAGE>) + 1024;
+  const size_t smem = sizeof(Smem<D, NSTAGE>) + Smem<D, NSTAGE>::PAD;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>,
@@ -1752,8 +1768,19 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, 
     if (cfg.d_head == 128) return launch_pair<128, 5>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
     if (cfg.d_head == 64) return launch_pair<64, 8>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
   } else {
-    if (cfg.d_head == 128) return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-    if (cfg.d_head == 64) return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+    // ring depths of the tile kernel (EVA_PREFILL_RING overrides: "2"/"32" at d=128, "3"/"54" at d=64)
+    static const int ring = [] {
+      const char* e = getenv("EVA_PREFILL_RING");
+      return e ? atoi(e) : 0;
+    }();
+    if (cfg.d_head == 128) {
+      if (ring == 32) return launch_t<128, 32>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+      return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+    }
+    if (cfg.d_head == 64) {
+      if (ring == 54) return launch_t<64, 54>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+      return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+    }
   }
   return cudaErrorNotSupported;
 }
