@@ -138,6 +138,7 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
  *              EVA_PREFILL_TC_PAIR    -- force the persistent two-tile tensor-core kernel;
  *              EVA_PREFILL_TC_WIDE    -- force the 128-key-tile tensor-core kernel;
  *              EVA_PREFILL_TC_SPLIT   -- force the split-softmax (8 softmax warps) kernel;
+ *              EVA_PREFILL_OVERLAP    -- see below;
  *              0                      -- compute summaries, then attend (kernel chosen
  *                                        by problem size).
  * bf16 runs the tcgen05/TMEM/TMA kernel for d in {64, 128} (requires 16-byte
@@ -148,6 +149,13 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
 #define EVA_PREFILL_TC_PAIR 16u
 #define EVA_PREFILL_TC_WIDE 32u
 #define EVA_PREFILL_TC_SPLIT 64u
+/* EVA_PREFILL_OVERLAP (with EVA_SUMMARIES_PROVIDED, tensor-core path): the caller asserts that
+ * the launch immediately before this one on `stream` is the eva_summarize that writes Ksum/Vsum
+ * and that Q, K, V were complete before that launch.  The prefill then starts its local-window
+ * tiles while that kernel finishes (programmatic dependent launch) and waits for it only before
+ * reading the summaries (measured neutral to slower on B200 -- DESIGN.md §11 -- so off by
+ * default). */
+#define EVA_PREFILL_OVERLAP 128u
 eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K, const void* V,
                             void* Ksum, void* Vsum, const float* eps, void* O, float* lse,
                             uint32_t flags, eva_stream_t stream);

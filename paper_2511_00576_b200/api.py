@@ -100,7 +100,8 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
                      eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
                      Vsum: Optional[torch.Tensor] = None, summaries_provided: bool = False,
                      want_lse: bool = True, simt: bool = False, O: Optional[torch.Tensor] = None,
-                     lse: Optional[torch.Tensor] = None, kernel: Optional[str] = None):
+                     lse: Optional[torch.Tensor] = None, kernel: Optional[str] = None,
+                     overlap: bool = False):
     """FlashEVA chunk-causal prefill.  Returns (O, lse, Ksum, Vsum).
 
     kernel: None (chosen by size), "simt", "tile" (tcgen05, one 128-query tile per CTA)
@@ -130,6 +131,8 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
     flags = (N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0) | (N.EVA_PREFILL_SIMT if simt else 0)
     flags |= {None: 0, "simt": 0, "tile": N.EVA_PREFILL_TC_TILE, "pair": N.EVA_PREFILL_TC_PAIR,
               "wide": N.EVA_PREFILL_TC_WIDE, "split": N.EVA_PREFILL_TC_SPLIT}[kernel]
+    if overlap:  # the previous launch on this stream is the eva_summarize writing Ksum/Vsum
+        flags |= N.EVA_PREFILL_OVERLAP
     check(lib.eva_attn_prefill(ctypes.byref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum), _ptr(Vsum),
                                _ptr(eps), _ptr(O), _ptr(lse if want_lse else None), flags,
                                _stream(Q.device)))

@@ -288,10 +288,20 @@ struct RangePlan {
     k0 = rg.k0;
     n_lt = (int)((vl.hi - lo0 + BN - 1) / BN);
   }
+  // Tile order: local tiles first, then the summary tiles (sum_first = 0) -- the local span
+  // depends only on the inputs, so with EVA_PREFILL_OVERLAP it runs while the summarize
+  // kernel is still finishing -- or summaries first (sum_first = 1).
+  int sum_first = 0;
   __device__ int count() const { return n_st + n_lt; }
-  __device__ bool summary(int j) const { return j < n_st; }
-  __device__ int64_t base(int j) const { return j < n_st ? (int64_t)j * BN : lo0 + (int64_t)(j - n_st) * BN; }
-  __device__ int row(int j) const { return j < n_st ? j * BN : (int)(lo0 - k0) + (j - n_st) * BN; }
+  __device__ bool summary(int j) const { return sum_first ? j < n_st : j >= n_lt; }
+  __device__ int64_t base(int j) const {
+    if (sum_first) return j < n_st ? (int64_t)j * BN : lo0 + (int64_t)(j - n_st) * BN;
+    return j >= n_lt ? (int64_t)(j - n_lt) * BN : lo0 + (int64_t)j * BN;
+  }
+  __device__ int row(int j) const {
+    if (sum_first) return j < n_st ? j * BN : (int)(lo0 - k0) + (j - n_st) * BN;
+    return j >= n_lt ? (j - n_lt) * BN : (int)(lo0 - k0) + j * BN;
+  }
 };
 
 
@@ -328,7 +338,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
                      const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
                      const PrefillRange rg, int C, int W, int mode, float scale_log2,
-                     float bias_log2, float* __restrict__ lse) {
+                     float bias_log2, float* __restrict__ lse, int overlap, int overlap_order_sum_first) {
   extern __shared__ uint8_t smem_raw[];
   using SM = Smem<D, NSTAGE>;
   constexpr int NSK = SM::NSK, NSV = SM::NSV;
@@ -338,7 +348,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   SM* sm = reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.y;
-  const RangePlan plan(blockIdx.x, rg, C, W, mode);
+  RangePlan plan(blockIdx.x, rg, C, W, mode);
+  plan.sum_first = overlap ? 0 : (overlap_order_sum_first ? 1 : 0);
   const int qrow = blockIdx.x * BM;  // TMA row of this query tile in Q / O
   const int NT = plan.count();
   TileTrace* tl = nullptr;
@@ -376,7 +387,11 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
-  pdl_wait();  // inputs of the previous kernel (summaries) are complete from here on
+  // PDL: by default every thread waits for the previous grid here.  With `overlap` (the
+  // previous grid is the eva_summarize producing Ksum/Vsum and Q, K, V were complete before
+  // it) only the producer waits, right before its first summary-tile access, so the local
+  // tiles (processed first) overlap the summarize kernel's tail.
+  if (!overlap) pdl_wait();
   pdl_trigger();
   if (threadIdx.x == 0) tt<TRACE>(tl, 0, 1, 0);
 
@@ -390,11 +405,20 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, qrow, u);
     }
     __syncwarp();
+    bool waited = !overlap;
+    auto wait_summaries = [&](int j) {
+      if (!waited && plan.summary(j)) {
+        pdl_wait();
+        waited = true;
+      }
+    };
     auto prefetch_rest = [&] {
       // The ring holds only NSTAGE tiles; pull every later K/V tile of this CTA into L2 now
-      // so its TMA load later on is an L2 hit instead of a full DRAM round trip.
+      // so its TMA load later on is an L2 hit instead of a full DRAM round trip (summary
+      // tiles only once they are known to be complete).
       if (elect_one()) {
       for (int j = NSV < NSK ? NSV : NSK; j < NT; ++j) {
+        if (!waited && plan.summary(j)) break;
         const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
         const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
         for (int kb = 0; kb < D / 64; ++kb) {
@@ -411,6 +435,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       const int s = j % NSK;
       if (j >= NSK) mbar_wait(&sm->k_empty[s], ((j / NSK) - 1) & 1);
       if (lane == 0) tt<TRACE>(tl, 0, 11, j);
+      wait_summaries(j);
       const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
       if (elect_one()) {
         mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
@@ -423,6 +448,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     auto load_v = [&](int j) {
       const int s = j % NSV;
       if (j >= NSV) mbar_wait(&sm->v_empty[s], ((j / NSV) - 1) & 1);
+      wait_summaries(j);
       const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
       if (elect_one()) {
         mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
@@ -560,7 +586,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     if (warp == 2 && lane == 0) {
       for (int kb = 0; kb < D / 64; ++kb) tma_store_3d(&mO, sm->q + kb * BM * 64, kb * 64, qrow, u);
       tma_store_commit();
-      tma_store_wait_all();
+      tma_store_wait_read();
       tt<TRACE>(tl, 2, 10, 0);
     }
   }
@@ -1572,16 +1598,26 @@ int softmax_emu() {
   return v;
 }
 
+// Tile order when not overlapping the summarize kernel: summary tiles first (measured 613 vs
+// 629 us at configs[2]); EVA_PREFILL_SUMFIRST=0 selects local-first for measurements.
+int tile_sum_first() {
+  static const int v = [] {
+    const char* e = getenv("EVA_PREFILL_SUMFIRST");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <int D, int NSTAGE, bool TRACE = false, int SMX = -1>
 cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* Q, const void* K,
                      const void* V, const void* Ksum, const void* Vsum, void* O, float* lse,
-                     cudaStream_t s) {
+                     cudaStream_t s, bool overlap = false) {
   if constexpr (!TRACE && SMX == -1) {
     switch (softmax_emu()) {
-      case 0: return launch_t<D, NSTAGE, false, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-      case 1: return launch_t<D, NSTAGE, false, 1>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-      case 2: return launch_t<D, NSTAGE, false, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-      case 3: return launch_t<D, NSTAGE, false, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+      case 0: return launch_t<D, NSTAGE, false, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
+      case 1: return launch_t<D, NSTAGE, false, 1>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
+      case 2: return launch_t<D, NSTAGE, false, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
+      case 3: return launch_t<D, NSTAGE, false, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
       default: break;
     }
   }
@@ -1609,7 +1645,7 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
   cudaError_t e = launch_pdl(prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>, grid, dim3(NTHREADS), smem, s, mQ, mK, mV,
                              mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
-                             cfg.summary_bias * 1.4426950408889634f, lse);
+                             cfg.summary_bias * 1.4426950408889634f, lse, overlap ? 1 : 0, tile_sum_first());
   if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
@@ -1746,6 +1782,8 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, 
                                  const void* K, const void* V, const void* Ksum, const void* Vsum,
                                  void* O, float* lse, uint32_t variant, cudaStream_t s) {
   if (cfg.bh_count == 0) return cudaSuccess;
+  const bool overlap = (variant & 0x100u) != 0;  // EVA_PREFILL_OVERLAP
+  variant &= 0xffu;
   const PrefillRange full = full_range(cfg);
   if (rg.q0 != full.q0 || rg.nq != full.nq || rg.k0 != full.k0 || rg.nkv != full.nkv || rg.nsl != full.nsl)
     variant = 1;  // query-range calls: the one-tile-per-CTA kernel only
@@ -1774,12 +1812,12 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, 
       return e ? atoi(e) : 0;
     }();
     if (cfg.d_head == 128) {
-      if (ring == 32) return launch_t<128, 32>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-      return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+      if (ring == 32) return launch_t<128, 32>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
+      return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
     }
     if (cfg.d_head == 64) {
-      if (ring == 54) return launch_t<64, 54>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-      return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+      if (ring == 54) return launch_t<64, 54>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
+      return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
     }
   }
   return cudaErrorNotSupported;

@@ -262,6 +262,40 @@ def test_prefill_host_pipeline_equals_device_call(eva, dtype, kernel, n_slices):
         hp(hQ, hK, hV, hO, n_slices=9)
 
 
+@pytest.mark.parametrize("d", [64, 128])
+def test_prefill_overlap_flag_equals_plain_call(eva, d):
+    """EVA_PREFILL_OVERLAP (prefill launched right after the eva_summarize producing its
+    summaries, local tiles started before that kernel completes) gives the same bits as the
+    plain call, eagerly and inside a CUDA graph."""
+    B, H, T, C, W = 2, 4, 1536, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=14, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    O, lse, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True)
+    ks2, vs2 = torch.zeros_like(ks), torch.zeros_like(vs)
+    O2, lse2 = torch.zeros_like(O), torch.zeros_like(lse)
+    for _ in range(3):
+        ks2.zero_(); vs2.zero_()
+        eva.eva_summarize(cfg, K, V, Ksum=ks2, Vsum=vs2)
+        eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks2, Vsum=vs2, summaries_provided=True, O=O2, lse=lse2,
+                             overlap=True)
+        torch.cuda.synchronize()
+        assert torch.equal(O2, O) and torch.equal(lse2, lse)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g):
+            eva.eva_summarize(cfg, K, V, Ksum=ks2, Vsum=vs2)
+            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks2, Vsum=vs2, summaries_provided=True, O=O2,
+                                 lse=lse2, overlap=True)
+    for _ in range(3):
+        ks2.zero_(); vs2.zero_(); O2.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(O2, O) and torch.equal(lse2, lse)
+
+
 def test_errors_are_reported_not_silent(eva):
     cfg = eva.make_config(1, 1, 64, 64, 16, 40)  # W % C != 0
     Q = torch.zeros(1, 64, 64, dtype=torch.bfloat16, device="cuda")
