@@ -769,7 +769,7 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
   BWD_DISPATCH_T(cfg.dtype, BWD_DISPATCH_D(cfg.d_head, {
     bwd_prep_kernel<T, D><<<dim3((Tn + 3) / 4, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)O,
                                                                          (const T*)dO, ws);
-    if (D == 128 && cfg.dtype == EVA_BF16 && backward_sm100_supported(cfg) && !backward_force_simt()) {
+    if ((D == 128 || D == 64) && cfg.dtype == EVA_BF16 && backward_sm100_supported(cfg) && !backward_force_simt()) {
       err = launch_backward_main_sm100(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws.D, ws.dQ, ws.dK, ws.dV,
                                        ws.dKs, ws.dVs, s);
       if (err != cudaSuccess) return err;

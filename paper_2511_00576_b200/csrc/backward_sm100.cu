@@ -32,20 +32,36 @@ namespace {
 
 using namespace sm100;
 constexpr int BK = 128;  // keys per work item (MMA M)
-constexpr int BQ = 64;   // queries per step (MMA N)
-constexpr int NSQ = 3;   // Q / dO ring stages
 constexpr int SEG = 8;   // query tiles per summary work item
 constexpr int BWD_TC_THREADS = 320;
-constexpr uint32_t TM_S = 0, TM_DP = 64, TM_DQ = 128, TM_DV = 256, TM_DK = 384;
+
+// Tiling per head dim.  d = 128: 64-query steps, dQ computed transposed (dQ^T = K^T dS^T,
+// M = d = 128); d = 64: 128-query steps, dQ = dS K (M = 128 queries).  TMEM columns:
+// S^T, dP^T (BQ each), dQ, dV, dK.
+template <int D> struct BwdT;
+template <> struct BwdT<128> {
+  static constexpr int BQ = 64, NSQ = 3;
+  static constexpr bool DQT = true;
+  static constexpr uint32_t TM_S = 0, TM_DP = 64, TM_DQ = 128, TM_DV = 256, TM_DK = 384;
+  static constexpr int DQS_FLOATS = BQ * 128;  // staging [64 queries][128] (column writes)
+};
+template <> struct BwdT<64> {
+  static constexpr int BQ = 128, NSQ = 2;
+  static constexpr bool DQT = false;
+  static constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256, TM_DV = 320, TM_DK = 384;
+  static constexpr int DQS_FLOATS = BQ * 68;   // staging rows padded to 68 floats (row writes)
+};
 
 template <int D>
 struct __align__(1024) BwdSm {
+  static constexpr int BQ = BwdT<D>::BQ, NSQ = BwdT<D>::NSQ;
   __nv_bfloat16 k[BK * D];        // D/64 sub-tiles [128 keys][64 ch], 16 KB each
   __nv_bfloat16 v[BK * D];
-  __nv_bfloat16 q[NSQ][BQ * D];   // D/64 sub-tiles [64 queries][64 ch], 8 KB each
+  __nv_bfloat16 q[NSQ][BQ * D];   // D/64 sub-tiles [BQ queries][64 ch]
   __nv_bfloat16 dO[NSQ][BQ * D];
-  __nv_bfloat16 ds[2][BK * BQ];   // dS^T [128 keys][64 queries], 128-byte swizzled rows, x2
-  float dqs[BQ * D];              // dQ_i staging [64 queries][d] fp32 for the bulk reduce-add
+  __nv_bfloat16 ds[2][BK * BQ];   // dS^T [128 keys][BQ queries]: BQ/64 sub-tiles of 128-byte
+                                  // swizzled rows, double-buffered
+  float dqs[BwdT<D>::DQS_FLOATS]; // dQ staging (fp32) for the bulk reduce-add
   float lse2[2][BQ], Dq[2][BQ];
   uint64_t kv_full, kv_empty, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free,
       ds_free[2], acc_done, acc_free;
@@ -65,13 +81,15 @@ __host__ __device__ __forceinline__ int64_t qlo_of_summary(int64_t c, int C, int
   if (mode == EVA_WINDOW_SLIDING) return (c + W / C) * (int64_t)C;
   return (c / (W / C) + 1) * (int64_t)W;
 }
-__host__ __device__ __forceinline__ int nqt(int T) { return (T + BQ - 1) / BQ; }
+template <int BQ> __host__ __device__ __forceinline__ int nqt(int T) { return (T + BQ - 1) / BQ; }
+template <int BQ>
 __host__ __device__ __forceinline__ int sum_qt0(int s, int T, int C, int W, int mode) {
   const int64_t q = qlo_of_summary((int64_t)s * BK, C, W, mode);
-  return q >= T ? nqt(T) : (int)(q / BQ);
+  return q >= T ? nqt<BQ>(T) : (int)(q / BQ);
 }
+template <int BQ>
 __host__ __device__ __forceinline__ int sum_segs(int s, int T, int C, int W, int mode) {
-  return (nqt(T) - sum_qt0(s, T, C, W, mode) + SEG - 1) / SEG;
+  return (nqt<BQ>(T) - sum_qt0<BQ>(s, T, C, W, mode) + SEG - 1) / SEG;
 }
 
 // Bulk (non-tensor) reduce-add of `bytes` contiguous fp32 from shared to global memory,
@@ -109,6 +127,7 @@ struct Item {
 
 // Work item w of the linearised (unit, item) list: items [0, n_sum_items) of a unit are
 // summary tiles of 128 summaries x SEG query tiles, the rest local tiles of 128 keys.
+template <int BQ>
 __device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum_items, int T, int C, int W,
                                             int mode) {
   Item it;
@@ -120,14 +139,14 @@ __device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum
     it.is_sum = true;
     int s = 0;
     for (;; ++s) {
-      const int ns = sum_segs(s, T, C, W, mode);
+      const int ns = sum_segs<BQ>(s, T, C, W, mode);
       if (item < ns) break;
       item -= ns;
     }
     it.k0 = s * BK;
     it.nk = min(BK, nC - it.k0);
-    it.qt_begin = sum_qt0(s, T, C, W, mode) + item * SEG;
-    qt_end = min(nqt(T), it.qt_begin + SEG);
+    it.qt_begin = sum_qt0<BQ>(s, T, C, W, mode) + item * SEG;
+    qt_end = min(nqt<BQ>(T), it.qt_begin + SEG);
   } else {
     it.is_sum = false;
     it.k0 = (item - n_sum_items) * BK;
@@ -154,6 +173,10 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
                       const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mdO,
                       int T, int C, int W, int mode, float scale, const float* __restrict__ lse,
                       BwdWsT ws, int n_sum_items, int items_per_unit, int n_items) {
+  using TT = BwdT<D>;
+  constexpr int BQ = TT::BQ, NSQ = TT::NSQ;
+  constexpr uint32_t TM_S = TT::TM_S, TM_DP = TT::TM_DP, TM_DQ = TT::TM_DQ, TM_DV = TT::TM_DV,
+                     TM_DK = TT::TM_DK;
   extern __shared__ uint8_t smem_raw[];
   BwdSm<D>* sm = reinterpret_cast<BwdSm<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -187,7 +210,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
-  auto item_of = [&](int w) { return decode_item(w, items_per_unit, n_sum_items, T, C, W, mode); };
+  auto item_of = [&](int w) { return decode_item<BQ>(w, items_per_unit, n_sum_items, T, C, W, mode); };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -230,17 +253,21 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t idesc_s = idesc_bf16_f32(BK, BQ, false);        // S^T, dP^T
     constexpr uint32_t idesc_g = idesc_bf16_f32(BK, D, true);          // dV, dK (B MN-major)
-    constexpr uint32_t idesc_q = idesc_bf16_f32_ab(D, BQ, true, true); // dQ^T (A, B MN-major)
+    // dQ: d = 128 -> dQ^T = K^T dS^T (M = d, N = BQ); d = 64 -> dQ = dS K (M = BQ, N = d);
+    // A and B both MN-major, two 64-wide atoms along M 16 KB apart (LBO)
+    constexpr uint32_t idesc_q = TT::DQT ? idesc_bf16_f32_ab(D, BQ, true, true)
+                                         : idesc_bf16_f32_ab(BQ, D, true, true);
     const uint32_t k_addr = smem_u32(sm->k), v_addr = smem_u32(sm->v);
     auto issue_dq = [&](int j) {  // dQ(j)^T = K^T dS^T(j), global step j
       if (j > 0) mbar_wait(&sm->dq_free, (j - 1) & 1);  // the epilogue has read dQ(j-1)
       tc_fence_after();
       if (elect_one()) {
         const uint32_t ds_addr = smem_u32(sm->ds[j & 1]);
+        const uint32_t a_addr = TT::DQT ? k_addr : ds_addr, b_addr = TT::DQT ? ds_addr : k_addr;
 #pragma unroll
         for (int ks = 0; ks < BK / 16; ++ks)
-          mma_ss(tmem + TM_DQ, smem_desc_sw128(k_addr + ks * 16 * 128, BK * 128, 1024),
-                 smem_desc_sw128(ds_addr + ks * 16 * 128, BQ * 128, 1024), idesc_q, ks > 0 ? 1u : 0u);
+          mma_ss(tmem + TM_DQ, smem_desc_sw128(a_addr + ks * 16 * 128, BK * 128, 1024),
+                 smem_desc_sw128(b_addr + ks * 16 * 128, BK * 128, 1024), idesc_q, ks > 0 ? 1u : 0u);
         mma_commit(&sm->dq_full);
         mma_commit(&sm->ds_free[j & 1]);
       }
@@ -340,7 +367,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         const float* Dq = sm->Dq[b];
         uint8_t* dsrow = reinterpret_cast<uint8_t*>(sm->ds[b]) + r * 128;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < BQ / 32; ++h) {
           uint32_t sr[32], dr[32];
           tmem_ld32(t_lane + TM_S + 32 * h, sr);
           tmem_ld32(t_lane + TM_DP + 32 * h, dr);
@@ -363,13 +390,14 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
           tmem_st16(t_lane + TM_DP + 16 * h, dk);
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
-            const int c16 = 4 * h + c4;
+            const int q16 = 4 * h + c4;           // 16-byte chunk of the row (8 queries)
+            const int sub = q16 >> 3, c16 = q16 & 7;  // 64-query sub-tile, chunk within it
             uint4 w4;
             w4.x = dk[4 * c4 + 0];
             w4.y = dk[4 * c4 + 1];
             w4.z = dk[4 * c4 + 2];
             w4.w = dk[4 * c4 + 3];
-            *reinterpret_cast<uint4*>(dsrow + ((c16 ^ (r & 7)) * 16)) = w4;
+            *reinterpret_cast<uint4*>(dsrow + sub * (BK * 128) + ((c16 ^ (r & 7)) * 16)) = w4;
           }
         }
         fence_proxy_async_smem();
@@ -433,6 +461,23 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&sm->dq_free);
+        if constexpr (!TT::DQT) {
+          // d = 64: thread <-> query row n0 + r; its 64 channels go to a padded staging row
+          // and are reduce-added by this thread's own 256-byte bulk operation
+          bulk_wait_read_all();  // this thread's previous reduce has read its staging row
+          float* st = sm->dqs + r * 68;
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            *reinterpret_cast<float4*>(st + 4 * e) =
+                make_float4(scale * __uint_as_float(qv[4 * e]), scale * __uint_as_float(qv[4 * e + 1]),
+                            scale * __uint_as_float(qv[4 * e + 2]), scale * __uint_as_float(qv[4 * e + 3]));
+          fence_proxy_async_smem();
+          if (n0 + r < T) {
+            bulk_reduce_add_f32(ws.dQ + ((size_t)it.u * T + n0 + r) * D, st, (uint32_t)(D * 4));
+            tma_store_commit();
+          }
+          continue;
+        }
         // stage dQ [64 queries][d] and reduce-add it into the fp32 accumulator with one bulk
         // TMA operation (the previous reduce must have finished reading the staging buffer)
         if (et == 0) bulk_wait_read_all();
@@ -449,8 +494,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         }
       }
     }
-    if (et == 0) bulk_wait_read_all();  // smem may be released once read; the global
-                                         // reduction completes asynchronously before grid end
+    if (et == 0 || !TT::DQT) bulk_wait_read_all();  // smem may be released once read; the
+                                         // global reduction completes asynchronously before grid end
   }
   tc_fence_before();
   __syncthreads();
@@ -462,14 +507,15 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
 bool backward_sm100_supported(const eva_config& cfg) {
   CUtensorMap probe;
   static const bool have_tma = make_tma_map_bf16(&probe, reinterpret_cast<void*>(0x1000), 1, 128, 128, 64);
-  return cfg.dtype == EVA_BF16 && cfg.d_head == 128 && have_tma;
+  return cfg.dtype == EVA_BF16 && (cfg.d_head == 128 || cfg.d_head == 64) && have_tma;
 }
 
-cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                                       const void* Ksum, const void* Vsum, const void* dO, const float* lse,
-                                       float* wsD, float* wsdQ, float* wsdK, float* wsdV, float* wsdKs,
-                                       float* wsdVs, cudaStream_t s) {
-  constexpr int D = 128;
+namespace {
+template <int D>
+cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                            const void* Ksum, const void* Vsum, const void* dO, const float* lse,
+                            const BwdWsT& ws, cudaStream_t s) {
+  constexpr int BQ = BwdT<D>::BQ;
   const int BH = cfg.bh_count, T = cfg.T, C = cfg.chunk, W = cfg.window, nC = T / C;
   CUtensorMap mK, mV, mKs, mVs, mQ, mdO;
   bool ok = make_tma_map_bf16(&mK, K, BH, T, D, BK) && make_tma_map_bf16(&mV, V, BH, T, D, BK) &&
@@ -482,7 +528,7 @@ cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, con
   }
   if (!ok) return cudaErrorInvalidValue;
   int n_sum_items = 0;
-  for (int st = 0; st * BK < nC; ++st) n_sum_items += sum_segs(st, T, C, W, cfg.mode);
+  for (int st = 0; st * BK < nC; ++st) n_sum_items += sum_segs<BQ>(st, T, C, W, cfg.mode);
   const int n_local_items = (T + BK - 1) / BK;
   const size_t smem = sizeof(BwdSm<D>) + 1024;
   static bool attr = false;
@@ -492,13 +538,23 @@ cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, con
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  BwdWsT ws{wsD, wsdQ, wsdK, wsdV, wsdKs, wsdVs};
   const int items_per_unit = n_sum_items + n_local_items;
   const int n_items = items_per_unit * BH;
   const int grid = std::max(1, std::min(n_items, num_sms()));
   bwd_main_sm100_kernel<D><<<grid, BWD_TC_THREADS, smem, s>>>(
       mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale, lse, ws, n_sum_items, items_per_unit, n_items);
   return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                       const void* Ksum, const void* Vsum, const void* dO, const float* lse,
+                                       float* wsD, float* wsdQ, float* wsdK, float* wsdV, float* wsdKs,
+                                       float* wsdVs, cudaStream_t s) {
+  const BwdWsT ws{wsD, wsdQ, wsdK, wsdV, wsdKs, wsdVs};
+  if (cfg.d_head == 128) return launch_bwd_main<128>(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws, s);
+  if (cfg.d_head == 64) return launch_bwd_main<64>(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws, s);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace eva
