@@ -22,6 +22,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "launch.h"
@@ -40,14 +42,20 @@ constexpr int BWD_TC_THREADS = 320;
 // S^T, dP^T (BQ each), dQ, dV, dK.
 template <int D> struct BwdT;
 template <> struct BwdT<128> {
-  static constexpr int BQ = 64, NSQ = 3;
+  static constexpr int BQ = 64, NSQ = 3, PBUF = 1;
   static constexpr bool DQT = true;
+  // P^T and dS^T go to shared memory (the dV/dK MMAs read them from there), so S^T/dP^T in
+  // TMEM are free as soon as the softmax warps have loaded them: the next step's S/dP MMAs
+  // run during this step's softmax.
+  static constexpr bool PSMEM = true;
   static constexpr uint32_t TM_S = 0, TM_DP = 64, TM_DQ = 128, TM_DV = 256, TM_DK = 384;
-  static constexpr int DQS_FLOATS = BQ * 128;  // staging [64 queries][128] (column writes)
+  static constexpr int DQS_FLOATS = 32 * 128;  // staging [32 queries][128] (column writes),
+                                               // the 64-query dQ tile in two halves
 };
 template <> struct BwdT<64> {
-  static constexpr int BQ = 128, NSQ = 2;
+  static constexpr int BQ = 128, NSQ = 2, PBUF = 1;
   static constexpr bool DQT = false;
+  static constexpr bool PSMEM = false;  // P^T, dS^T back into TMEM (TS MMAs)
   static constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256, TM_DV = 320, TM_DK = 384;
   static constexpr int DQS_FLOATS = BQ * 68;   // staging rows padded to 68 floats (row writes)
 };
@@ -62,9 +70,10 @@ struct __align__(1024) BwdSm {
   __nv_bfloat16 ds[2][BK * BQ];   // dS^T [128 keys][BQ queries]: BQ/64 sub-tiles of 128-byte
                                   // swizzled rows, double-buffered
   float dqs[BwdT<D>::DQS_FLOATS]; // dQ staging (fp32) for the bulk reduce-add
-  float lse2[2][BQ], Dq[2][BQ];
+  __nv_bfloat16 p[BwdT<D>::PBUF][BwdT<D>::PSMEM ? BK * BQ : 8];  // P^T [128 keys][BQ] (PSMEM)
+  float lse2[NSQ][BQ], Dq[NSQ][BQ];  // per Q/dO ring slot, loaded by the producer warp
   uint64_t kv_full, kv_empty, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free,
-      ds_free[2], acc_done, acc_free;
+      ds_free[2], acc_done, acc_free, s_free, p_free[BwdT<D>::PBUF];
   uint32_t tmem_base;
 };
 
@@ -100,6 +109,17 @@ __device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const float* ss
                : "memory");
 }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// 16-byte shared-memory load through the shared window (the arrays live in dynamic shared
+// memory reached by a generic pointer, which the compiler would otherwise load with
+// generic, serialised LD instructions)
+__device__ __forceinline__ float4 lds4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
@@ -166,13 +186,26 @@ __device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum
 // dP(g), then dQ(g-1) (its dS buffer was written one step earlier), then -- after the
 // softmax -- dV(g), dK(g); so the softmax of step g+1 overlaps dQ(g) and its epilogue, and
 // the next item's K/V load and first MMAs overlap this item's dK/dV write-out.
-template <int D>
+__device__ long long g_bwd_trs[5][48];  // debug timeline (EVA_BWD_TRACE)
+__device__ int g_bwd_trn[5];
+
+template <int D, bool TRACE>
 __global__ void __launch_bounds__(BWD_TC_THREADS, 1)
 bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
                       const __grid_constant__ CUtensorMap mKs, const __grid_constant__ CUtensorMap mVs,
                       const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mdO,
                       int T, int C, int W, int mode, float scale, const float* __restrict__ lse,
-                      BwdWsT ws, int n_sum_items, int items_per_unit, int n_items) {
+                      BwdWsT ws, int n_sum_items, int items_per_unit, int n_items, int trace) {
+  // debug timeline (EVA_BWD_TRACE=1): CTA 0 records clock64 per role and prints it at exit
+  constexpr int TRN = 48;
+  auto TR = [&](int role, int code) {
+    if constexpr (TRACE) {
+      if (trace && blockIdx.x == 0) {
+        const int k = atomicAdd(&g_bwd_trn[role], 1);
+        if (k < TRN) g_bwd_trs[role][k] = (clock64() << 8) | code;
+      }
+    }
+  };
   using TT = BwdT<D>;
   constexpr int BQ = TT::BQ, NSQ = TT::NSQ;
   constexpr uint32_t TM_S = TT::TM_S, TM_DP = TT::TM_DP, TM_DQ = TT::TM_DQ, TM_DV = TT::TM_DV,
@@ -188,7 +221,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     mbar_init(&sm->kv_full, 1);
     mbar_init(&sm->kv_empty, 1);
     for (int s = 0; s < NSQ; ++s) {
-      mbar_init(&sm->q_full[s], 1);
+      mbar_init(&sm->q_full[s], 1 + 32);  // the TMA expect_tx + the producer lanes' lse/D stores
       mbar_init(&sm->q_empty[s], 1);
     }
     mbar_init(&sm->s_full, 1);
@@ -200,6 +233,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     mbar_init(&sm->ds_free[1], 1);
     mbar_init(&sm->acc_done, 1);
     mbar_init(&sm->acc_free, 128);
+    mbar_init(&sm->s_free, 128);
+    for (int k = 0; k < BwdT<D>::PBUF; ++k) mbar_init(&sm->p_free[k], 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -220,6 +255,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       if (it.nsteps == 0) continue;
       if (kcount > 0) mbar_wait(&sm->kv_empty, (kcount - 1) & 1);  // last item's dQ MMA is done
       if (elect_one()) {
+        TR(0, 9);
         const CUtensorMap* mk = it.is_sum ? &mKs : &mK;
         const CUtensorMap* mv = it.is_sum ? &mVs : &mV;
         mbar_arrive_expect_tx(&sm->kv_full, 2 * BK * D * 2);
@@ -232,13 +268,41 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
             tma_prefetch_l2_3d(&mQ, kb * 64, (it.qt_begin + i) * BQ, it.u);
             tma_prefetch_l2_3d(&mdO, kb * 64, (it.qt_begin + i) * BQ, it.u);
           }
+        // the NEXT item's K/V and first Q/dO tiles into L2: its K/V load can only start once
+        // this item's last dQ MMA is done, so it must not be a DRAM round trip
+        if (w + (int)gridDim.x < n_items) {
+          const Item nx = item_of(w + gridDim.x);
+          const CUtensorMap* nk = nx.is_sum ? &mKs : &mK;
+          const CUtensorMap* nv = nx.is_sum ? &mVs : &mV;
+          for (int kb = 0; kb < D / 64; ++kb) {
+            tma_prefetch_l2_3d(nk, kb * 64, nx.k0, nx.u);
+            tma_prefetch_l2_3d(nv, kb * 64, nx.k0, nx.u);
+            for (int i = 0; i < NSQ && i < nx.nsteps; ++i) {
+              tma_prefetch_l2_3d(&mQ, kb * 64, (nx.qt_begin + i) * BQ, nx.u);
+              tma_prefetch_l2_3d(&mdO, kb * 64, (nx.qt_begin + i) * BQ, nx.u);
+            }
+          }
+        }
       }
       __syncwarp();
       for (int i = 0; i < it.nsteps; ++i, ++g) {
         const int s = g % NSQ;
+        // lse (log2 units) and D of the step's queries: loaded into registers first, so their
+        // latency overlaps the wait for the ring slot
+        float lv[BQ / 32], dvv[BQ / 32];
+        {
+          const int n0 = (it.qt_begin + i) * BQ;
+#pragma unroll
+          for (int k = 0; k < BQ / 32; ++k) {
+            const int n = n0 + lane + 32 * k;
+            lv[k] = n < T ? lse[(size_t)it.u * T + n] * 1.4426950408889634f : 0.f;
+            dvv[k] = n < T ? ws.D[(size_t)it.u * T + n] : 0.f;
+          }
+        }
         if (g >= NSQ) mbar_wait(&sm->q_empty[s], ((g / NSQ) - 1) & 1);
         if (elect_one()) {
           const int n0 = (it.qt_begin + i) * BQ;
+          TR(0, 1);
           mbar_arrive_expect_tx(&sm->q_full[s], 2 * BQ * D * 2);
           for (int kb = 0; kb < D / 64; ++kb) {
             tma_load_3d(sm->q[s] + kb * BQ * 64, &mQ, &sm->q_full[s], kb * 64, n0, it.u);
@@ -246,6 +310,12 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
           }
         }
         __syncwarp();
+#pragma unroll
+        for (int k = 0; k < BQ / 32; ++k) {  // lse / D into the slot, then arrive
+          sm->lse2[s][lane + 32 * k] = lv[k];
+          sm->Dq[s][lane + 32 * k] = dvv[k];
+        }
+        mbar_arrive(&sm->q_full[s]);
       }
       ++kcount;
     }
@@ -273,6 +343,75 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       }
       __syncwarp();
     };
+    auto issue_s = [&](int g) {  // S^T(g) = K Q^T, dP^T(g) = V dO^T
+      const int s = g % NSQ;
+      const uint32_t q_addr = smem_u32(sm->q[s]), do_addr = smem_u32(sm->dO[s]);
+      if (elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+          mma_ss(tmem + TM_S, smem_desc_sw128(k_addr + kb * (BK * 128) + off, 16, 1024),
+                 smem_desc_sw128(q_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+          mma_ss(tmem + TM_DP, smem_desc_sw128(v_addr + kb * (BK * 128) + off, 16, 1024),
+                 smem_desc_sw128(do_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+        }
+        mma_commit(&sm->s_full);
+      }
+      __syncwarp();
+    };
+    if constexpr (TT::PSMEM) {
+      // dV(j), dK(j) from P^T / dS^T in shared memory, then dQ(j)
+      auto grad_step = [&](int j, int ij, int kc, bool last) {
+        const int s = j % NSQ;
+        const uint32_t q_addr = smem_u32(sm->q[s]), do_addr = smem_u32(sm->dO[s]);
+        const uint32_t p_addr = smem_u32(sm->p[j % TT::PBUF]), ds_addr = smem_u32(sm->ds[j & 1]);
+        mbar_wait(&sm->p_full, j & 1);
+        if (ij == 0 && kc > 0) mbar_wait(&sm->acc_free, (kc - 1) & 1);  // dK/dV drained
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < BQ / 16; ++ks) {
+            const uint32_t acc = (ij > 0 || ks > 0) ? 1u : 0u;
+            const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+            mma_ss(tmem + TM_DV, smem_desc_sw128(p_addr + kb * (BK * 128) + off, 16, 1024),
+                   smem_desc_sw128(do_addr + ks * 16 * 128, BQ * 128, 1024), idesc_g, acc);
+            mma_ss(tmem + TM_DK, smem_desc_sw128(ds_addr + kb * (BK * 128) + off, 16, 1024),
+                   smem_desc_sw128(q_addr + ks * 16 * 128, BQ * 128, 1024), idesc_g, acc);
+          }
+          mma_commit(&sm->q_empty[s]);
+          mma_commit(&sm->p_free[j % TT::PBUF]);
+          if (last) mma_commit(&sm->acc_done);
+        }
+        __syncwarp();
+        issue_dq(j);
+      };
+      int g = 0, kcount = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+        const Item it = item_of(w);
+        if (it.nsteps == 0) continue;
+        mbar_wait(&sm->kv_full, kcount & 1);
+        if (lane == 0) TR(1, 10);
+        for (int i = 0; i < it.nsteps; ++i, ++g) {
+          mbar_wait(&sm->q_full[g % NSQ], (g / NSQ) & 1);
+          if (g > 0) mbar_wait(&sm->s_free, (g - 1) & 1);  // softmax has loaded S/dP(g-1)
+          tc_fence_after();
+          if (lane == 0) TR(1, 2);
+          issue_s(g);
+          if (lane == 0) TR(1, 3);
+          if (i > 0) grad_step(g - 1, i - 1, kcount, false);
+          if (lane == 0) TR(1, 4);
+        }
+        grad_step(g - 1, it.nsteps - 1, kcount, true);
+        if (lane == 0) TR(1, 5);
+        if (elect_one()) mma_commit(&sm->kv_empty);  // K/V smem free once this dQ completes
+        __syncwarp();
+        ++kcount;
+      }
+    } else {
     int g = 0, kcount = 0;
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
       const Item it = item_of(w);
@@ -324,6 +463,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       __syncwarp();
       ++kcount;
     }
+    }
   } else if (warp < 6) {
     // ------------------------------------------------------------ softmax / dS (thread <-> key row)
     const int quad = warp & 3;
@@ -352,20 +492,65 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       for (int i = 0; i < it.nsteps; ++i, ++g) {
         const int n0 = (it.qt_begin + i) * BQ;
         const int b = g & 1;
-        if (tc < BQ) {
-          const int n = n0 + tc;
-          sm->lse2[b][tc] = n < T ? lse[(size_t)u * T + n] * 1.4426950408889634f : 0.f;
-          sm->Dq[b][tc] = n < T ? ws.D[(size_t)u * T + n] : 0.f;
-        }
-        named_bar_sync(1, 128);
         mbar_wait(&sm->s_full, g & 1);
-        if (g >= 2) mbar_wait(&sm->ds_free[b], ((g >> 1) - 1) & 1);  // dQ(g-2) has read ds[b]
-        tc_fence_after();
+        mbar_wait(&sm->q_full[g % NSQ], (g / NSQ) & 1);  // the producer's lse/D stores
+        if (tc == 0) TR(2, 6);
         const int vlo = (int)max((int64_t)0, min((int64_t)BQ, vq_lo - n0));
         const int vhi = (int)max((int64_t)0, min((int64_t)BQ, vq_hi + 1 - n0));
-        const float* lse2 = sm->lse2[b];
-        const float* Dq = sm->Dq[b];
+        const float* lse2 = sm->lse2[g % NSQ];
+        const float* Dq = sm->Dq[g % NSQ];
         uint8_t* dsrow = reinterpret_cast<uint8_t*>(sm->ds[b]) + r * 128;
+        if constexpr (TT::PSMEM) {
+          // load S^T / dP^T, release TMEM at once (the next step's MMAs may overwrite it),
+          // then P^T and dS^T into shared memory as K-major A operands of the dV/dK MMAs
+          tc_fence_after();
+          uint32_t sr[BQ], dr[BQ];
+#pragma unroll
+          for (int h = 0; h < BQ / 32; ++h) {
+            tmem_ld32(t_lane + TM_S + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * h]));
+            tmem_ld32(t_lane + TM_DP + 32 * h, *reinterpret_cast<uint32_t(*)[32]>(&dr[32 * h]));
+          }
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(&sm->s_free);
+          constexpr int PB = TT::PBUF;
+          if (g >= PB) mbar_wait(&sm->p_free[g % PB], ((g / PB) - 1) & 1);  // dV(g-PB) read it
+          if (g >= 2) mbar_wait(&sm->ds_free[b], ((g >> 1) - 1) & 1);      // dK/dQ(g-2) read ds[b]
+          uint8_t* prow = reinterpret_cast<uint8_t*>(sm->p[g % PB]) + r * 128;
+#pragma unroll
+          for (int c16 = 0; c16 < BQ / 8; ++c16) {
+            uint32_t pk[4], dk[4];
+            float lv[8], dv[8];
+            *reinterpret_cast<float4*>(&lv[0]) = lds4(lse2 + 8 * c16);
+            *reinterpret_cast<float4*>(&lv[4]) = lds4(lse2 + 8 * c16 + 4);
+            *reinterpret_cast<float4*>(&dv[0]) = lds4(Dq + 8 * c16);
+            *reinterpret_cast<float4*>(&dv[4]) = lds4(Dq + 8 * c16 + 4);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              float pp[2], gg[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int jj = 2 * c + e, j = 8 * c16 + jj;
+                const bool vis = j >= vlo && j < vhi;
+                pp[e] = vis ? ex2f(fmaf(__uint_as_float(sr[j]), sl2, -lv[jj])) : 0.f;
+                gg[e] = pp[e] * (__uint_as_float(dr[j]) - dv[jj]);
+              }
+              pk[c] = pack2(pp[0], pp[1]);
+              dk[c] = pack2(gg[0], gg[1]);
+            }
+            const int sub = c16 >> 3, cc = c16 & 7;
+            const uint32_t off = sub * (BK * 128) + ((cc ^ (r & 7)) * 16);
+            *reinterpret_cast<uint4*>(prow + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(dsrow + off) = make_uint4(dk[0], dk[1], dk[2], dk[3]);
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&sm->p_full);
+          if (tc == 0) TR(2, 7);
+          continue;
+        }
+        if (g >= 2) mbar_wait(&sm->ds_free[b], ((g >> 1) - 1) & 1);  // dQ(g-2) has read ds[b]
+        tc_fence_after();
+        float2 lnext = make_float2(0.f, 0.f), dnext = make_float2(0.f, 0.f);
 #pragma unroll
         for (int h = 0; h < BQ / 32; ++h) {
           uint32_t sr[32], dr[32];
@@ -376,12 +561,23 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             float p[2], gg[2];
+            float2 lv2, dv2;
+            if ((c & 1) == 0) {
+              const float4 l4 = lds4(lse2 + 32 * h + 2 * c), d4 = lds4(Dq + 32 * h + 2 * c);
+              lv2 = make_float2(l4.x, l4.y);
+              dv2 = make_float2(d4.x, d4.y);
+              lnext = make_float2(l4.z, l4.w);
+              dnext = make_float2(d4.z, d4.w);
+            } else {
+              lv2 = lnext;
+              dv2 = dnext;
+            }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
               const int jj = 2 * c + e, j = 32 * h + jj;
               const bool vis = j >= vlo && j < vhi;
-              p[e] = vis ? ex2f(fmaf(__uint_as_float(sr[jj]), sl2, -lse2[j])) : 0.f;
-              gg[e] = p[e] * (__uint_as_float(dr[jj]) - Dq[j]);
+              p[e] = vis ? ex2f(fmaf(__uint_as_float(sr[jj]), sl2, -(e ? lv2.y : lv2.x))) : 0.f;
+              gg[e] = p[e] * (__uint_as_float(dr[jj]) - (e ? dv2.y : dv2.x));
             }
             pk[c] = pack2(p[0], p[1]);
             dk[c] = pack2(gg[0], gg[1]);
@@ -407,6 +603,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       }
       // ---- dK, dV of this key tile: drain TMEM, release it, then write to global
       mbar_wait(&sm->acc_done, kcount & 1);
+      if (tc == 0) TR(2, 11);
       tc_fence_after();
 #pragma unroll 1
       for (int cc = 0; cc < D / 32; ++cc) {
@@ -420,12 +617,17 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         }
         if (r < it.nk) {
           if (it.is_sum) {
-            float* dks = ws.dKs + ((size_t)u * nC + m) * D + cc * 32;
-            float* dvs = ws.dVs + ((size_t)u * nC + m) * D + cc * 32;
+            // summary tiles are split into query segments over several CTAs: vector
+            // reductions (red.global.add.v4.f32) into the fp32 accumulators
+            float4* dks = reinterpret_cast<float4*>(ws.dKs + ((size_t)u * nC + m) * D + cc * 32);
+            float4* dvs = reinterpret_cast<float4*>(ws.dVs + ((size_t)u * nC + m) * D + cc * 32);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              atomicAdd(dks + e, scale * __uint_as_float(kv[e]));
-              atomicAdd(dvs + e, __uint_as_float(vv[e]));
+            for (int e = 0; e < 8; ++e) {
+              atomicAdd(dks + e, make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
+                                             scale * __uint_as_float(kv[4 * e + 2]),
+                                             scale * __uint_as_float(kv[4 * e + 3])));
+              atomicAdd(dvs + e, make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
+                                             __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3])));
             }
           } else {
             float4* dkl = reinterpret_cast<float4*>(ws.dK + ((size_t)u * T + m) * D + cc * 32);
@@ -440,6 +642,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
           }
         }
       }
+      if (tc == 0) TR(2, 12);
       ++kcount;
     }
   } else {
@@ -454,6 +657,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       for (int i = 0; i < it.nsteps; ++i, ++g) {
         const int n0 = (it.qt_begin + i) * BQ;
         mbar_wait(&sm->dq_full, g & 1);
+        if (r == 0) TR(3, 8);
         tc_fence_after();
         uint32_t qv[64];
         tmem_ld32(t_lane + TM_DQ, *reinterpret_cast<uint32_t(*)[32]>(&qv[0]));
@@ -480,17 +684,24 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         }
         // stage dQ [64 queries][d] and reduce-add it into the fp32 accumulator with one bulk
         // TMA operation (the previous reduce must have finished reading the staging buffer)
-        if (et == 0) bulk_wait_read_all();
-        named_bar_sync(2, 128);
-        float* st = sm->dqs + r;
+        // two halves of 32 queries through a [32][d] staging buffer
 #pragma unroll
-        for (int j = 0; j < BQ; ++j) st[j * D] = scale * __uint_as_float(qv[j]);
-        fence_proxy_async_smem();
-        named_bar_sync(2, 128);
-        if (et == 0) {
-          const int nv = min(BQ, T - n0);
-          bulk_reduce_add_f32(ws.dQ + ((size_t)it.u * T + n0) * D, sm->dqs, (uint32_t)(nv * D * 4));
-          tma_store_commit();
+        for (int hf = 0; hf < 2; ++hf) {
+          if (et == 0) bulk_wait_read_all();
+          named_bar_sync(2, 128);
+          float* st = sm->dqs + r;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) st[j * D] = scale * __uint_as_float(qv[32 * hf + j]);
+          fence_proxy_async_smem();
+          named_bar_sync(2, 128);
+          if (et == 0) {
+            const int nv = min(32, T - n0 - 32 * hf);
+            if (nv > 0) {
+              bulk_reduce_add_f32(ws.dQ + ((size_t)it.u * T + n0 + 32 * hf) * D, sm->dqs,
+                                  (uint32_t)(nv * D * 4));
+              tma_store_commit();
+            }
+          }
         }
       }
     }
@@ -500,6 +711,14 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
+  if (TRACE && trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    long long t0 = g_bwd_trs[1][0] >> 8;
+    for (int role = 0; role < 4; ++role) {
+      for (int k = 0; k < min(g_bwd_trn[role], TRN); ++k)
+        printf("TR role=%d ev=%d t=%lld\n", role, (int)(g_bwd_trs[role][k] & 0xff), (g_bwd_trs[role][k] >> 8) - t0);
+      g_bwd_trn[role] = 0;
+    }
+  }
 }
 
 }  // namespace
@@ -531,18 +750,19 @@ cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K,
   for (int st = 0; st * BK < nC; ++st) n_sum_items += sum_segs<BQ>(st, T, C, W, cfg.mode);
   const int n_local_items = (T + BK - 1) / BK;
   const size_t smem = sizeof(BwdSm<D>) + 1024;
+  static const bool trace = getenv("EVA_BWD_TRACE") != nullptr;  // debug timeline of CTA 0
+  auto kern = trace ? bwd_main_sm100_kernel<D, true> : bwd_main_sm100_kernel<D, false>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(bwd_main_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int items_per_unit = n_sum_items + n_local_items;
   const int n_items = items_per_unit * BH;
   const int grid = std::max(1, std::min(n_items, num_sms()));
-  bwd_main_sm100_kernel<D><<<grid, BWD_TC_THREADS, smem, s>>>(
-      mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale, lse, ws, n_sum_items, items_per_unit, n_items);
+  kern<<<grid, BWD_TC_THREADS, smem, s>>>(mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale, lse, ws,
+                                          n_sum_items, items_per_unit, n_items, trace ? 1 : 0);
   return cudaGetLastError();
 }
 }  // namespace
