@@ -34,7 +34,7 @@ namespace {
 
 using namespace sm100;
 constexpr int BK = 128;  // keys per work item (MMA M)
-constexpr int SEG = 8;   // query tiles per summary work item
+// query tiles per summary work item: chosen per launch (bwd_seg_for), 8 .. 32
 constexpr int BWD_TC_THREADS = 320;
 
 // Tiling per head dim.  d = 128: 64-query steps, dQ computed transposed (dQ^T = K^T dS^T,
@@ -97,7 +97,7 @@ __host__ __device__ __forceinline__ int sum_qt0(int s, int T, int C, int W, int 
   return q >= T ? nqt<BQ>(T) : (int)(q / BQ);
 }
 template <int BQ>
-__host__ __device__ __forceinline__ int sum_segs(int s, int T, int C, int W, int mode) {
+__host__ __device__ __forceinline__ int sum_segs(int s, int T, int C, int W, int mode, int SEG) {
   return (nqt<BQ>(T) - sum_qt0<BQ>(s, T, C, W, mode) + SEG - 1) / SEG;
 }
 
@@ -149,7 +149,7 @@ struct Item {
 // summary tiles of 128 summaries x SEG query tiles, the rest local tiles of 128 keys.
 template <int BQ>
 __device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum_items, int T, int C, int W,
-                                            int mode) {
+                                            int mode, int SEG) {
   Item it;
   it.u = w / items_per_unit;
   int item = w % items_per_unit;
@@ -159,7 +159,7 @@ __device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum
     it.is_sum = true;
     int s = 0;
     for (;; ++s) {
-      const int ns = sum_segs<BQ>(s, T, C, W, mode);
+      const int ns = sum_segs<BQ>(s, T, C, W, mode, SEG);
       if (item < ns) break;
       item -= ns;
     }
@@ -195,7 +195,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
                       const __grid_constant__ CUtensorMap mKs, const __grid_constant__ CUtensorMap mVs,
                       const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mdO,
                       int T, int C, int W, int mode, float scale, const float* __restrict__ lse,
-                      BwdWsT ws, int n_sum_items, int items_per_unit, int n_items, int trace) {
+                      BwdWsT ws, int n_sum_items, int items_per_unit, int n_items, int seg, int trace) {
   // debug timeline (EVA_BWD_TRACE=1): CTA 0 records clock64 per role and prints it at exit
   constexpr int TRN = 48;
   auto TR = [&](int role, int code) {
@@ -245,7 +245,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
-  auto item_of = [&](int w) { return decode_item<BQ>(w, items_per_unit, n_sum_items, T, C, W, mode); };
+  auto item_of = [&](int w) { return decode_item<BQ>(w, items_per_unit, n_sum_items, T, C, W, mode, seg); };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -601,48 +601,6 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         tc_fence_before();
         mbar_arrive(&sm->p_full);
       }
-      // ---- dK, dV of this key tile: drain TMEM, release it, then write to global
-      mbar_wait(&sm->acc_done, kcount & 1);
-      if (tc == 0) TR(2, 11);
-      tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t kv[32], vv[32];
-        tmem_ld32(t_lane + TM_DK + cc * 32, kv);
-        tmem_ld32(t_lane + TM_DV + cc * 32, vv);
-        tmem_wait_ld();
-        if (cc == D / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&sm->acc_free);
-        }
-        if (r < it.nk) {
-          if (it.is_sum) {
-            // summary tiles are split into query segments over several CTAs: vector
-            // reductions (red.global.add.v4.f32) into the fp32 accumulators
-            float4* dks = reinterpret_cast<float4*>(ws.dKs + ((size_t)u * nC + m) * D + cc * 32);
-            float4* dvs = reinterpret_cast<float4*>(ws.dVs + ((size_t)u * nC + m) * D + cc * 32);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              atomicAdd(dks + e, make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
-                                             scale * __uint_as_float(kv[4 * e + 2]),
-                                             scale * __uint_as_float(kv[4 * e + 3])));
-              atomicAdd(dvs + e, make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
-                                             __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3])));
-            }
-          } else {
-            float4* dkl = reinterpret_cast<float4*>(ws.dK + ((size_t)u * T + m) * D + cc * 32);
-            float4* dvl = reinterpret_cast<float4*>(ws.dV + ((size_t)u * T + m) * D + cc * 32);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              dkl[e] = make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
-                                   scale * __uint_as_float(kv[4 * e + 2]), scale * __uint_as_float(kv[4 * e + 3]));
-              dvl[e] = make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
-                                   __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3]));
-            }
-          }
-        }
-      }
-      if (tc == 0) TR(2, 12);
       ++kcount;
     }
   } else {
@@ -651,7 +609,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     const int r = quad * 32 + lane;          // channel
     const int et = (warp - 6) * 32 + lane;   // 0..127 among these warps
     const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
-    int g = 0;
+    int g = 0, kcount = 0;
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
       const Item it = item_of(w);
       for (int i = 0; i < it.nsteps; ++i, ++g) {
@@ -704,6 +662,51 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
           }
         }
       }
+      // ---- dK, dV of this key tile (here, so the softmax warps go straight on to the next
+      // item): drain TMEM, release it, then write to global
+      if (it.nsteps == 0) continue;
+      const int64_t m = (int64_t)it.k0 + r;
+      mbar_wait(&sm->acc_done, kcount & 1);
+      if (et == 0) TR(3, 11);
+      tc_fence_after();
+#pragma unroll 1
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t kv[32], vv[32];
+        tmem_ld32(t_lane + TM_DK + cc * 32, kv);
+        tmem_ld32(t_lane + TM_DV + cc * 32, vv);
+        tmem_wait_ld();
+        if (cc == D / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&sm->acc_free);
+        }
+        if (r < it.nk) {
+          if (it.is_sum) {
+            // summary tiles are split into query segments over several CTAs: vector
+            // reductions (red.global.add.v4.f32) into the fp32 accumulators
+            float4* dks = reinterpret_cast<float4*>(ws.dKs + ((size_t)it.u * nC + m) * D + cc * 32);
+            float4* dvs = reinterpret_cast<float4*>(ws.dVs + ((size_t)it.u * nC + m) * D + cc * 32);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              atomicAdd(dks + e, make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
+                                             scale * __uint_as_float(kv[4 * e + 2]),
+                                             scale * __uint_as_float(kv[4 * e + 3])));
+              atomicAdd(dvs + e, make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
+                                             __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3])));
+            }
+          } else {
+            float4* dkl = reinterpret_cast<float4*>(ws.dK + ((size_t)it.u * T + m) * D + cc * 32);
+            float4* dvl = reinterpret_cast<float4*>(ws.dV + ((size_t)it.u * T + m) * D + cc * 32);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              dkl[e] = make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
+                                   scale * __uint_as_float(kv[4 * e + 2]), scale * __uint_as_float(kv[4 * e + 3]));
+              dvl[e] = make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
+                                   __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3]));
+            }
+          }
+        }
+      }
+      ++kcount;
     }
     if (et == 0 || !TT::DQT) bulk_wait_read_all();  // smem may be released once read; the
                                          // global reduction completes asynchronously before grid end
@@ -746,9 +749,17 @@ cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K,
     mVs = mV;
   }
   if (!ok) return cudaErrorInvalidValue;
-  int n_sum_items = 0;
-  for (int st = 0; st * BK < nC; ++st) n_sum_items += sum_segs<BQ>(st, T, C, W, cfg.mode);
+  // Summary tiles are cut into segments of `seg` query tiles (one work item each; their
+  // dK~/dbeta partials meet in fp32 reductions).  Long segments cost fewer item switches and
+  // reductions; short ones keep small problems parallel: the longest seg (<= 32) that still
+  // leaves >= 4 work items per SM.
   const int n_local_items = (T + BK - 1) / BK;
+  int seg = 32, n_sum_items = 0;
+  for (;; seg /= 2) {
+    n_sum_items = 0;
+    for (int st = 0; st * BK < nC; ++st) n_sum_items += sum_segs<BQ>(st, T, C, W, cfg.mode, seg);
+    if (seg <= 4 || (int64_t)(n_sum_items + n_local_items) * BH >= 4 * num_sms()) break;
+  }
   const size_t smem = sizeof(BwdSm<D>) + 1024;
   static const bool trace = getenv("EVA_BWD_TRACE") != nullptr;  // debug timeline of CTA 0
   auto kern = trace ? bwd_main_sm100_kernel<D, true> : bwd_main_sm100_kernel<D, false>;
@@ -762,7 +773,7 @@ cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K,
   const int n_items = items_per_unit * BH;
   const int grid = std::max(1, std::min(n_items, num_sms()));
   kern<<<grid, BWD_TC_THREADS, smem, s>>>(mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale, lse, ws,
-                                          n_sum_items, items_per_unit, n_items, trace ? 1 : 0);
+                                          n_sum_items, items_per_unit, n_items, seg, trace ? 1 : 0);
   return cudaGetLastError();
 }
 }  // namespace
