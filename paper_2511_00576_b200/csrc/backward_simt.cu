@@ -25,8 +25,8 @@
 //                   added to the fp32 accumulator with red.global.add.
 //   bwd_finalize  : one CTA per chunk: the summary chain rule above, then dQ, dK, dV
 //                   of the chunk's rows are written in cfg.dtype (tail rows are copied).
-// This is the parity-grade first version of the row (SIMT fp32 math); the tcgen05
-// version is future work.
+// bf16 with d in {64, 128} replaces bwd_main with the tcgen05 main pass of
+// backward_sm100.cu; the SIMT main pass serves fp32 and the other head dims.
 #include <algorithm>
 #include <cstdlib>
 
