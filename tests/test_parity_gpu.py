@@ -265,8 +265,9 @@ def test_prefill_host_pipeline_equals_device_call(eva, dtype, kernel, n_slices):
 @pytest.mark.parametrize("d", [64, 128])
 def test_prefill_overlap_flag_equals_plain_call(eva, d):
     """EVA_PREFILL_OVERLAP (prefill launched right after the eva_summarize producing its
-    summaries, local tiles started before that kernel completes) gives the same bits as the
-    plain call, eagerly and inside a CUDA graph."""
+    summaries, local tiles started before that kernel completes): deterministic (the same bits
+    eagerly, repeatedly and inside a CUDA graph) and equal to the plain call up to the tile
+    order (the plain call walks the summary tiles first)."""
     B, H, T, C, W = 2, 4, 1536, 64, 256
     cfg = eva.make_config(B, H, T, d, C, W)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=14, device="cuda")
@@ -274,13 +275,18 @@ def test_prefill_overlap_flag_equals_plain_call(eva, d):
     O, lse, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True)
     ks2, vs2 = torch.zeros_like(ks), torch.zeros_like(vs)
     O2, lse2 = torch.zeros_like(O), torch.zeros_like(lse)
+    ref = None
     for _ in range(3):
         ks2.zero_(); vs2.zero_()
         eva.eva_summarize(cfg, K, V, Ksum=ks2, Vsum=vs2)
         eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks2, Vsum=vs2, summaries_provided=True, O=O2, lse=lse2,
                              overlap=True)
         torch.cuda.synchronize()
-        assert torch.equal(O2, O) and torch.equal(lse2, lse)
+        if ref is None:
+            ref = (O2.clone(), lse2.clone())
+            assert (O2.float() - O.float()).abs().max().item() <= 2e-2
+            assert (lse2 - lse).abs().max().item() <= 1e-3
+        assert torch.equal(O2, ref[0]) and torch.equal(lse2, ref[1])
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
@@ -293,7 +299,7 @@ def test_prefill_overlap_flag_equals_plain_call(eva, d):
         ks2.zero_(); vs2.zero_(); O2.zero_()
         g.replay()
         torch.cuda.synchronize()
-        assert torch.equal(O2, O) and torch.equal(lse2, lse)
+        assert torch.equal(O2, ref[0]) and torch.equal(lse2, ref[1])
 
 
 def test_errors_are_reported_not_silent(eva):
