@@ -139,6 +139,7 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
  *              EVA_PREFILL_TC_WIDE    -- force the 128-key-tile tensor-core kernel;
  *              EVA_PREFILL_TC_SPLIT   -- force the split-softmax (8 softmax warps) kernel;
  *              EVA_PREFILL_OVERLAP    -- see below;
+ *              EVA_PREFILL_TC_PERSIST -- force the persistent tile kernel (see below);
  *              0                      -- compute summaries, then attend (kernel chosen
  *                                        by problem size).
  * bf16 runs the tcgen05/TMEM/TMA kernel for d in {64, 128} (requires 16-byte
@@ -156,6 +157,10 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
  * reading the summaries (measured neutral to slower on B200 -- DESIGN.md §11 -- so off by
  * default). */
 #define EVA_PREFILL_OVERLAP 128u
+/* EVA_PREFILL_TC_PERSIST: the persistent form of the one-tile-per-CTA tensor-core kernel (two
+ * CTAs per SM loop over the query tiles; the next tile's loads and first MMAs overlap the
+ * current tile's epilogue). */
+#define EVA_PREFILL_TC_PERSIST 256u
 eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K, const void* V,
                             void* Ksum, void* Vsum, const float* eps, void* O, float* lse,
                             uint32_t flags, eva_stream_t stream);

@@ -22,6 +22,7 @@ EVA_PREFILL_TC_PAIR = 16
 EVA_PREFILL_TC_WIDE = 32
 EVA_PREFILL_TC_SPLIT = 64
 EVA_PREFILL_OVERLAP = 128
+EVA_PREFILL_TC_PERSIST = 256
 
 _STATUS = {0: "EVA_OK", 1: "EVA_ERR_INVALID_ARG", 2: "EVA_ERR_UNSUPPORTED", 3: "EVA_ERR_CAPACITY",
            4: "EVA_ERR_CUDA"}

@@ -130,7 +130,8 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
         lse = torch.empty(bh, T, dtype=torch.float32, device=Q.device)
     flags = (N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0) | (N.EVA_PREFILL_SIMT if simt else 0)
     flags |= {None: 0, "simt": 0, "tile": N.EVA_PREFILL_TC_TILE, "pair": N.EVA_PREFILL_TC_PAIR,
-              "wide": N.EVA_PREFILL_TC_WIDE, "split": N.EVA_PREFILL_TC_SPLIT}[kernel]
+              "wide": N.EVA_PREFILL_TC_WIDE, "split": N.EVA_PREFILL_TC_SPLIT,
+              "persist": N.EVA_PREFILL_TC_PERSIST}[kernel]
     if overlap:  # the previous launch on this stream is the eva_summarize writing Ksum/Vsum
         flags |= N.EVA_PREFILL_OVERLAP
     check(lib.eva_attn_prefill(ctypes.byref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum), _ptr(Vsum),

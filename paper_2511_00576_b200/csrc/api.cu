@@ -144,7 +144,7 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
   if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT | EVA_PREFILL_TC_TILE | EVA_PREFILL_TC_PAIR |
-                EVA_PREFILL_TC_WIDE | EVA_PREFILL_TC_SPLIT | EVA_PREFILL_OVERLAP))
+                EVA_PREFILL_TC_WIDE | EVA_PREFILL_TC_SPLIT | EVA_PREFILL_OVERLAP | EVA_PREFILL_TC_PERSIST))
     return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
   if (cfg->mode == EVA_NONCAUSAL && cfg->T % cfg->chunk != 0)
     return fail(EVA_ERR_INVALID_ARG, "non-causal prefill needs T %% C == 0 (T=%d, C=%d; reading R15)", cfg->T,
@@ -169,7 +169,8 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) &&
                   eva::prefill_sm100_supported(*cfg);
   uint32_t variant = (flags & EVA_PREFILL_TC_TILE) ? 1u : (flags & EVA_PREFILL_TC_PAIR) ? 2u
-                    : (flags & EVA_PREFILL_TC_WIDE) ? 3u : (flags & EVA_PREFILL_TC_SPLIT) ? 4u : 0u;
+                    : (flags & EVA_PREFILL_TC_WIDE) ? 3u : (flags & EVA_PREFILL_TC_SPLIT) ? 4u
+                    : (flags & EVA_PREFILL_TC_PERSIST) ? 5u : 0u;
   // EVA_PREFILL_OVERLAP: the summarize kernel is the previous grid and Q, K, V predate it,
   // so the prefill may start its local tiles before the summaries are complete.  Measured
   // neutral at configs[1] (the two kernels' CTAs do not co-reside) and 2-7 % slower at

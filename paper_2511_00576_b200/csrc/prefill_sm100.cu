@@ -604,6 +604,254 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// ========================================================================== persistent tile kernel
+// The one-tile-per-CTA kernel made persistent: two CTAs per SM walk the (unit, query tile)
+// items w = blockIdx.x, + gridDim.x, ...  Ring indices and barrier phases run on global
+// counters across items, so the next item's Q (released by the last S MMA of the current
+// item), K/V tiles and first S MMAs stream in while the current item finishes; O is drained
+// from TMEM by the softmax warps (o_free releases it for the next item's first PV) and
+// written straight from registers (no smem staging, so Q's buffer is never shared).
+template <int D, int NSTAGE>
+struct __align__(1024) SmemP {
+  static constexpr int NSK = NSTAGE >= 10 ? NSTAGE / 10 : NSTAGE;
+  static constexpr int NSV = NSTAGE >= 10 ? NSTAGE % 10 : NSTAGE;
+  __nv_bfloat16 q[BM * D];
+  __nv_bfloat16 k[NSK][BN * D];
+  __nv_bfloat16 v[NSV][BN * D];
+  uint64_t q_full, q_empty;
+  uint64_t k_full[NSK], v_full[NSV], k_empty[NSK], v_empty[NSV];
+  uint64_t s_full[2], p_full[2], o_done, o_final, o_free;
+  uint32_t tmem_base;
+};
+
+template <int D, int NSTAGE>
+__global__ void __launch_bounds__(NTHREADS, 2)
+prefill_persist_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
+                       const __grid_constant__ CUtensorMap mVs, const PrefillRange rg, int C, int W, int mode,
+                       float scale_log2, float bias_log2, float* __restrict__ lse, __nv_bfloat16* __restrict__ O,
+                       int n_qt, int n_items) {
+  extern __shared__ uint8_t smem_raw[];
+  using SM = SmemP<D, NSTAGE>;
+  constexpr int NSK = SM::NSK, NSV = SM::NSV;
+  SM* sm = reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto plan_of = [&](int w) {
+    RangePlan p(w % n_qt, rg, C, W, mode);
+    p.sum_first = 1;
+    return p;
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
+    tma_prefetch(&mKs); tma_prefetch(&mVs);
+    mbar_init(&sm->q_full, 1);
+    mbar_init(&sm->q_empty, 1);
+    for (int s = 0; s < NSK; ++s) {
+      mbar_init(&sm->k_full[s], 1);
+      mbar_init(&sm->k_empty[s], 1);
+    }
+    for (int s = 0; s < NSV; ++s) {
+      mbar_init(&sm->v_full[s], 1);
+      mbar_init(&sm->v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm->s_full[b], 1);
+      mbar_init(&sm->p_full[b], 128);
+    }
+    mbar_init(&sm->o_done, 1);
+    mbar_init(&sm->o_final, 1);
+    mbar_init(&sm->o_free, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(&sm->tmem_base, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm->tmem_base;
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    int tk = 0, tv = 0, ic = 0;  // global K tile, V tile and item counters
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ic) {
+      const RangePlan plan = plan_of(w);
+      const int u = w / n_qt, qrow = (w % n_qt) * BM, NT = plan.count();
+      if (ic > 0) mbar_wait(&sm->q_empty, (ic - 1) & 1);  // the last item's S MMAs are done
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb) tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, qrow, u);
+        for (int j = 2; j < NT; ++j) {
+          const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
+          const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
+          for (int kb = 0; kb < D / 64; ++kb) {
+            tma_prefetch_l2_3d(mk, kb * 64, plan.row(j), u);
+            tma_prefetch_l2_3d(mv, kb * 64, plan.row(j), u);
+          }
+        }
+      }
+      __syncwarp();
+      auto load_k = [&](int j) {
+        const int t = tk + j, s = t % NSK;
+        if (t >= NSK) mbar_wait(&sm->k_empty[s], ((t / NSK) - 1) & 1);
+        const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, plan.row(j), u);
+        }
+        __syncwarp();
+      };
+      auto load_v = [&](int j) {
+        const int t = tv + j, s = t % NSV;
+        if (t >= NSV) mbar_wait(&sm->v_empty[s], ((t / NSV) - 1) & 1);
+        const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, plan.row(j), u);
+        }
+        __syncwarp();
+      };
+      load_k(0);
+      for (int j = 0; j < NT; ++j) {
+        if (j + 1 < NT) load_k(j + 1);
+        load_v(j);
+      }
+      tk += NT;
+      tv += NT;
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
+    const uint32_t q_addr = smem_u32(sm->q);
+    int t0 = 0, ic = 0;  // global tile counter at the item start, item counter
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ic) {
+      const int NT = plan_of(w).count();
+      mbar_wait(&sm->q_full, ic & 1);
+      for (int j = 0; j <= NT; ++j) {
+        if (j < NT) {
+          const int t = t0 + j, s = t % NSK;
+          mbar_wait(&sm->k_full[s], (t / NSK) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(sm->k[s]);
+          const uint32_t d_tmem = tmem + (uint32_t)(t & 1) * BN;
+          if (elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < D / 16; ++ks) {
+              const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
+              mma_ss(d_tmem, smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024),
+                     smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
+            }
+            mma_commit(&sm->s_full[t & 1]);
+            mma_commit(&sm->k_empty[s]);
+            if (j == NT - 1) mma_commit(&sm->q_empty);  // Q is read by the S MMAs only
+          }
+          __syncwarp();
+        }
+        if (j >= 1) {
+          const int jj = j - 1, t = t0 + jj, s = t % NSV;
+          mbar_wait(&sm->p_full[t & 1], (t >> 1) & 1);
+          if (jj == 0 && ic > 0) mbar_wait(&sm->o_free, (ic - 1) & 1);  // last item's O drained
+          mbar_wait(&sm->v_full[s], (t / NSV) & 1);
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(sm->v[s]);
+          if (elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < BN / 16; ++ks) {
+              const uint32_t a_tmem = tmem + (uint32_t)(t & 1) * BN + ks * 8;
+              mma_ts(tmem + TM_O, a_tmem, smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024), idesc_o,
+                     (jj > 0 || ks > 0) ? 1u : 0u);
+            }
+            mma_commit(&sm->v_empty[s]);
+            mma_commit(&sm->o_done);
+            if (jj == NT - 1) mma_commit(&sm->o_final);
+          }
+          __syncwarp();
+        }
+      }
+      t0 += NT;
+    }
+  } else {
+    // ------------------------------------------------------------ softmax + epilogue warps
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    const int64_t qend = rg.q0 + rg.nq;
+    int t0 = 0, ic = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ic) {
+      const RangePlan plan = plan_of(w);
+      const int u = w / n_qt, NT = plan.count();
+      const int64_t n = plan.n0 + r;
+      const bool valid = n < qend;
+      const Vis rr = visible_set(valid ? n : plan.nlast, C, W, mode, qend);
+      float m_ref = -INFINITY, l = 0.f;
+      for (int j = 0; j < NT; ++j) {
+        const int t = t0 + j;
+        mbar_wait(&sm->s_full[t & 1], (t >> 1) & 1);
+        tc_fence_after();
+        const int64_t base = plan.base(j);
+        int vlo, vhi, xlo = 0, xhi = 0;
+        float bias2 = 0.f;
+        if (plan.summary(j)) {
+          vlo = 0;
+          if (mode == EVA_NONCAUSAL) {
+            vhi = (int)min((int64_t)BN, (int64_t)rg.nsl - base);
+            xlo = (int)max((int64_t)-1, min((int64_t)BN, rr.s1 - base));
+            xhi = (int)max((int64_t)-1, min((int64_t)BN, rr.s2 - base));
+          } else {
+            vhi = (int)min((int64_t)BN, rr.s1 - base);
+          }
+          bias2 = bias_log2;
+        } else {
+          vlo = (int)max((int64_t)0, rr.lo - base);
+          vhi = (int)min((int64_t)BN, rr.hi - base);
+        }
+        if (!valid) vhi = vlo;
+        softmax_tile_mx<D>(t_lane + (uint32_t)(t & 1) * BN, t_lane + TM_O, vlo, vhi, xlo, xhi, bias2, scale_log2,
+                           m_ref, l, [&] { mbar_wait(&sm->o_done, (t - 1) & 1); });
+        mbar_arrive(&sm->p_full[t & 1]);
+      }
+      // ---- epilogue: O / l straight from TMEM to global (this thread's row), lse
+      mbar_wait(&sm->o_final, ic & 1);
+      tc_fence_after();
+      const float inv_l = l > 0.f ? 1.0f / l : 0.f;
+      __nv_bfloat16* orow = O + ((size_t)u * rg.nq + (size_t)(valid ? n - rg.q0 : 0)) * D;
+#pragma unroll
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t o[32];
+        tmem_ld32(t_lane + TM_O + cc * 32, o);
+        tmem_wait_ld();
+        if (cc == D / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&sm->o_free);
+        }
+        if (valid) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint4 w4;
+            w4.x = pack_bf16(__uint_as_float(o[8 * g + 0]) * inv_l, __uint_as_float(o[8 * g + 1]) * inv_l);
+            w4.y = pack_bf16(__uint_as_float(o[8 * g + 2]) * inv_l, __uint_as_float(o[8 * g + 3]) * inv_l);
+            w4.z = pack_bf16(__uint_as_float(o[8 * g + 4]) * inv_l, __uint_as_float(o[8 * g + 5]) * inv_l);
+            w4.w = pack_bf16(__uint_as_float(o[8 * g + 6]) * inv_l, __uint_as_float(o[8 * g + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = w4;
+          }
+        }
+      }
+      if (valid && lse) lse[(size_t)u * rg.nq + (size_t)(n - rg.q0)] = (m_ref + __log2f(l)) * 0.69314718055994531f;
+      t0 += NT;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+}
+
 // ========================================================================== split-softmax kernel
 // The tile kernel with 8 softmax warps: warps 2..5 own columns [0,32) of every 64-key S tile,
 // warps 6..9 columns [32,64), of the same 128 rows (warp w and w+4 share TMEM lane quadrant
@@ -1652,6 +1900,42 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
 }
 
 template <int D, int NSTAGE>
+cudaError_t launch_persist(const eva_config& cfg, const PrefillRange& rg, const void* Q, const void* K,
+                           const void* V, const void* Ksum, const void* Vsum, void* O, float* lse,
+                           cudaStream_t s) {
+  const int BH = cfg.bh_count, nC = rg.nsl;
+  if (rg.nq == 0) return cudaSuccess;
+  CUtensorMap mQ, mK, mV, mKs, mVs;
+  bool ok = make_map(&mQ, Q, BH, rg.nq, D, BM) && make_map(&mK, K, BH, rg.nkv, D, BN) &&
+            make_map(&mV, V, BH, rg.nkv, D, BN);
+  if (nC > 0) {
+    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BN) && make_map(&mVs, Vsum, BH, nC, D, BN);
+  } else {
+    mKs = mK;
+    mVs = mV;
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(SmemP<D, NSTAGE>) + 1024;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_persist_kernel<D, NSTAGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int n_qt = (rg.nq + BM - 1) / BM;
+  const int n_items = n_qt * BH;
+  const int grid = std::max(1, std::min(n_items, 2 * num_sms()));
+  const float scale_log2 = cfg.scale * 1.4426950408889634f;
+  cudaError_t e = launch_pdl(prefill_persist_kernel<D, NSTAGE>, dim3(grid), dim3(NTHREADS), smem, s, mQ, mK, mV,
+                             mKs, mVs, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
+                             cfg.summary_bias * 1.4426950408889634f, lse, (__nv_bfloat16*)O, n_qt, n_items);
+  if (e != cudaSuccess) return e;
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <int D, int NSTAGE>
 cudaError_t launch_split(const eva_config& cfg, const void* Q, const void* K, const void* V,
                          const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
   const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
@@ -1794,6 +2078,10 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, 
   bool pair = false;
   if (variant == 1) pair = false;
   if (variant == 2) pair = true;
+  if (variant == 5) {
+    if (cfg.d_head == 128) return launch_persist<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+    if (cfg.d_head == 64) return launch_persist<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+  }
   if (variant == 4) {
     if (cfg.d_head == 128) return launch_split<128, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
     if (cfg.d_head == 64) return launch_split<64, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);

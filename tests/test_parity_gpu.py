@@ -121,10 +121,10 @@ CASES = [  # (B, H, T, d, C, W)
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("dtype,kernel", [(torch.float32, "simt"), (torch.bfloat16, "simt"),
                                           (torch.bfloat16, "tile"), (torch.bfloat16, "pair"),
-                                          (torch.bfloat16, "wide")])
+                                          (torch.bfloat16, "wide"), (torch.bfloat16, "persist")])
 def test_prefill_parity(eva, case, mode, dtype, kernel):
     B, H, T, d, C, W = case
-    if kernel in ("tile", "pair", "wide") and d not in (64, 128):
+    if kernel in ("tile", "pair", "wide", "persist") and d not in (64, 128):
         pytest.skip("tensor-core kernels cover d in {64, 128}; other d run the SIMT kernel")
     cfg = eva.make_config(B, H, T, d, C, W, mode=mode, dtype=dtype, seed=7)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=2, device="cuda")
@@ -226,7 +226,8 @@ def test_prefill_detects_beta_perturbation(eva):
 
 
 @pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, "tile"),
-                                               (torch.bfloat16, False, "pair"), (torch.bfloat16, False, "wide")])
+                                               (torch.bfloat16, False, "pair"), (torch.bfloat16, False, "wide"),
+                                               (torch.bfloat16, False, "persist")])
 def test_sharded_equals_unsharded(eva, dtype, simt, kernel):
     """(b,h) shards computed separately are bitwise equal to the full run (RNG keyed by global unit)."""
     B, H, T, d, C, W = 2, 3, 384, 64, 32, 64
@@ -514,3 +515,16 @@ def test_long_context_sweep_sampled_parity(eva, T, C, W):
         rows, rO, rl = oracle.prefill_rows(f64(Q[u]), Kf, Vf, rk, rv, rows, C, W, 0, cfg.scale)
         assert np.max(np.abs(f64(O[u])[rows] - rO)) <= 2e-2
         assert np.max(np.abs(f64(lse[u])[rows] - rl)) <= 2e-2
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_persistent_prefill_equals_tile_kernel(eva, d):
+    """The persistent tile kernel walks the same tiles in the same order as the
+    one-tile-per-CTA kernel: bitwise equal results (many items per CTA, ragged tail)."""
+    B, H, T, C, W = 4, 40, 1000, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=31, device="cuda")
+    O1, l1, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, kernel="tile")
+    O2, l2, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, kernel="persist")
+    torch.cuda.synchronize()
+    assert torch.equal(O1, O2) and torch.equal(l1, l2)
