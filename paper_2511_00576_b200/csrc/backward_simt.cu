@@ -104,27 +104,51 @@ ItemPlan plan_items(const eva_config& cfg) {
 }
 
 // ------------------------------------------------------------------ bwd_prep
+// A row is read by TPR = D*sizeof(T)/16 lanes with one 16-byte load of O and of dO each
+// (RPW = 32/TPR rows per warp, 4 warps per CTA); every lane zeroes its VEC fp32 accumulator
+// entries with 16-byte stores.  Needs D*sizeof(T) >= 16 (d >= 8 bf16 / 4 fp32).
 template <typename T, int D>
 __global__ void __launch_bounds__(128) bwd_prep_kernel(eva_config cfg, const T* __restrict__ O,
                                                        const T* __restrict__ dO, BwdWs ws) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int TPR = D / VEC < 32 ? D / VEC : 32;
+  constexpr int RPW = 32 / TPR;
+  constexpr int PER = D / (TPR * VEC);  // 16-byte pieces per lane and row
   const int Tn = cfg.T, nC = Tn / cfg.chunk;
   const int u = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int n = blockIdx.x * 4 + warp;
-  if (n >= Tn) return;
-  const size_t row = (size_t)u * Tn + n;
+  const int grp = lane / TPR, gl = lane % TPR;
+  const int n = (blockIdx.x * 4 + warp) * RPW + grp;
+  const bool ok = n < Tn;
+  const size_t row = (size_t)u * Tn + (ok ? n : 0);
   float s = 0.f;
-  for (int j = lane; j < D; j += 32) {
-    s += Elem<T>::to_f(O[row * D + j]) * Elem<T>::to_f(dO[row * D + j]);
-    ws.dQ[row * D + j] = 0.f;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int ch = (k * TPR + gl) * VEC;
+    if (ok) {
+      float a[VEC], b[VEC];
+      unpack16<T>(ldg16_stream(O + row * D + ch), a);
+      unpack16<T>(ldg16_stream(dO + row * D + ch), b);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) s += a[j] * b[j];
+      float4* q = reinterpret_cast<float4*>(ws.dQ + row * D + ch);
+#pragma unroll
+      for (int j = 0; j < VEC / 4; ++j) q[j] = z;
+    }
   }
-  s = warp_sum(s);
-  if (lane == 0) ws.D[row] = s;
-  if (n < nC) {
+  s = group_sum<TPR>(s);
+  if (ok && gl == 0) ws.D[row] = s;
+  if (ok && n < nC) {
     const size_t srow = (size_t)u * nC + n;
-    for (int j = lane; j < D; j += 32) {
-      ws.dKs[srow * D + j] = 0.f;
-      ws.dVs[srow * D + j] = 0.f;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int ch = (k * TPR + gl) * VEC;
+#pragma unroll
+      for (int j = 0; j < VEC / 4; ++j) {
+        reinterpret_cast<float4*>(ws.dKs + srow * D + ch)[j] = z;
+        reinterpret_cast<float4*>(ws.dVs + srow * D + ch)[j] = z;
+      }
     }
   }
 }
@@ -767,8 +791,13 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
   const ItemPlan plan = plan_items(cfg);
   cudaError_t err = cudaSuccess;
   BWD_DISPATCH_T(cfg.dtype, BWD_DISPATCH_D(cfg.d_head, {
-    bwd_prep_kernel<T, D><<<dim3((Tn + 3) / 4, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)O,
-                                                                         (const T*)dO, ws);
+    {
+      constexpr int VEC = 16 / sizeof(T);
+      constexpr int RPW = 32 / (D / VEC < 32 ? D / VEC : 32);
+      const int rows_per_cta = 4 * RPW;
+      bwd_prep_kernel<T, D><<<dim3((Tn + rows_per_cta - 1) / rows_per_cta, cfg.bh_count), 128, 0, s>>>(
+          cfg, (const T*)O, (const T*)dO, ws);
+    }
     if ((D == 128 || D == 64) && cfg.dtype == EVA_BF16 && backward_sm100_supported(cfg) && !backward_force_simt()) {
       err = launch_backward_main_sm100(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws.D, ws.dQ, ws.dK, ws.dV,
                                        ws.dKs, ws.dVs, s);
