@@ -84,7 +84,7 @@ def test_validation_rejects_null_and_misaligned_pointers(N):
     st = N.lib.eva_attn_prefill(ctypes.byref(cfg), FAKE, ctypes.c_void_p(0x10002), FAKE, FAKE, FAKE,
                                 None, FAKE, None, 0, None)
     assert st == N.EVA_ERR_INVALID_ARG and b"aligned" in N.lib.eva_last_error()
-    st = N.lib.eva_attn_prefill(ctypes.byref(cfg), FAKE, FAKE, FAKE, FAKE, FAKE, None, FAKE, None, 0x80, None)
+    st = N.lib.eva_attn_prefill(ctypes.byref(cfg), FAKE, FAKE, FAKE, FAKE, FAKE, None, FAKE, None, 0x4000, None)
     assert st == N.EVA_ERR_INVALID_ARG
 
 
