@@ -178,6 +178,19 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
 eva_status eva_summarize_range(const eva_config* cfg, int32_t chunk0, const void* K, const void* V,
                                const float* eps, void* Ksum, void* Vsum, eva_stream_t stream);
 
+/* eva_summarize_range_bcast: eva_summarize_range fused with the context-parallel all-gather:
+ * the summaries of absolute chunks [chunk0, chunk0 + floor(T/C)) are computed once and stored
+ * to rows chunk0 + c of EVERY destination pair (dst_ksum[i], dst_vsum[i]), i < n_dst, each a
+ * [bh_count, dst_rows, d] cfg.dtype buffer -- typically every rank's copy of the global
+ * summary list reached through NVLink peer pointers (symmetric memory), so the exchange rides
+ * on the summarising kernel's own stores.  dst_ksum / dst_vsum are DEVICE arrays of n_dst
+ * device addresses (0 <= n_dst <= 64); dst_rows >= chunk0 + floor(T/C).  The caller orders
+ * the destinations' readers after this kernel on every rank (e.g. a symmetric-memory barrier).
+ * EVA_ERR_UNSUPPORTED if a chunk exceeds the register summariser (C > 256 at d = 128 bf16). */
+eva_status eva_summarize_range_bcast(const eva_config* cfg, int32_t chunk0, const void* K, const void* V,
+                                     const float* eps, const uint64_t* dst_ksum, const uint64_t* dst_vsum,
+                                     int32_t n_dst, int32_t dst_rows, eva_stream_t stream);
+
 /* eva_attn_prefill_range: eva_attn_prefill (summaries provided) for the queries at absolute
  * positions [q0, q0 + n_q) only.
  * Q, O : [bh_count, n_q, d]        row i = position q0 + i

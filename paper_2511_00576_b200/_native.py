@@ -51,7 +51,7 @@ EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache
            "eva_draw_eps", "eva_last_error", "eva_version", "eva_launch_count",
            "eva_debug_trace_prefill", "eva_decode_step", "eva_backward_workspace_bytes",
            "eva_attn_backward", "eva_pipeline_create", "eva_pipeline_destroy", "eva_attn_prefill_host",
-           "eva_summarize_range", "eva_attn_prefill_range"]
+           "eva_summarize_range", "eva_attn_prefill_range", "eva_summarize_range_bcast"]
 
 
 class EvaError(RuntimeError):
@@ -88,6 +88,7 @@ def _load():
         "eva_launch_count": (ctypes.c_uint64, []),
         "eva_debug_trace_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_int32, P]),
         "eva_summarize_range": (st, [CFG, ctypes.c_int32, P, P, P, P, P, P]),
+        "eva_summarize_range_bcast": (st, [CFG, ctypes.c_int32, P, P, P, P, P, ctypes.c_int32, ctypes.c_int32, P]),
         "eva_attn_prefill_range": (st, [CFG, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, ctypes.c_int32,
                                         P, P, P, P, P, ctypes.c_int32, P, P, ctypes.c_uint32, P]),
         "eva_pipeline_create": (st, [ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]),

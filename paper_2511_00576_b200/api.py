@@ -19,7 +19,7 @@ __all__ = ["make_config", "eva_summarize", "eva_attn_prefill", "eva_cache_append
            "eva_attn_decode", "DecodeCache", "eva_mask_ranges", "eva_philox", "eva_draw_eps",
            "EvaConfig", "EvaError", "launch_count", "version", "eva_attn_backward",
            "eva_backward_workspace_bytes", "HostPrefill", "eva_attn_prefill_host",
-           "eva_summarize_range", "eva_attn_prefill_range"]
+           "eva_summarize_range", "eva_attn_prefill_range", "eva_summarize_range_bcast"]
 
 _DT = {torch.float32: N.EVA_F32, torch.bfloat16: N.EVA_BF16}
 _MODE = {"sliding": N.EVA_WINDOW_SLIDING, "block": N.EVA_WINDOW_BLOCK, "noncausal": N.EVA_NONCAUSAL}
@@ -156,6 +156,25 @@ def eva_summarize_range(cfg: EvaConfig, chunk0: int, K: torch.Tensor, V: torch.T
     check(lib.eva_summarize_range(ctypes.byref(cfg), chunk0, _ptr(K), _ptr(V), _ptr(eps), _ptr(Ksum),
                                   _ptr(Vsum), _stream(K.device)))
     return Ksum, Vsum
+
+
+def eva_summarize_range_bcast(cfg: EvaConfig, chunk0: int, K: torch.Tensor, V: torch.Tensor,
+                              dst_ksum_ptrs: torch.Tensor, dst_vsum_ptrs: torch.Tensor, dst_rows: int,
+                              eps: Optional[torch.Tensor] = None) -> None:
+    """Summaries of chunks [chunk0, chunk0 + cfg.T // C) stored to row chunk0 + c of every
+    destination: dst_*_ptrs are int64 CUDA tensors of device addresses of [bh, dst_rows, d]
+    buffers (e.g. symmetric-memory peer pointers)."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    _need(K, "K", (bh, T, d), dt)
+    _need(V, "V", (bh, T, d), dt)
+    n = dst_ksum_ptrs.numel()
+    for t, nm in ((dst_ksum_ptrs, "dst_ksum_ptrs"), (dst_vsum_ptrs, "dst_vsum_ptrs")):
+        _need(t, nm, (n,), torch.int64)
+    if eps is not None:
+        _need(eps, "eps", (bh, T // cfg.chunk, d), torch.float32)
+    check(lib.eva_summarize_range_bcast(ctypes.byref(cfg), chunk0, _ptr(K), _ptr(V), _ptr(eps),
+                                        _ptr(dst_ksum_ptrs), _ptr(dst_vsum_ptrs), n, dst_rows,
+                                        _stream(K.device)))
 
 
 def eva_attn_prefill_range(cfg: EvaConfig, q0: int, k0: int, Q: torch.Tensor, K: torch.Tensor,

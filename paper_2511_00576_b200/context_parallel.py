@@ -100,8 +100,8 @@ def seq_shards(T: int, world: int, C: int, W: int, mode: int = EVA_WINDOW_SLIDIN
 
 
 def exchange(Ksum: torch.Tensor, Vsum: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
-             shards: List[SeqShard], rank: int, C: int,
-             group=None) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
+             shards: List[SeqShard], rank: int, C: int, group=None,
+             summaries: bool = True) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]:
     """The one exchange step.  Ksum/Vsum [bh, c_r, d]: this rank's chunk summaries; K/V
     [bh, q1 - q0, d]: its keys/values.  Returns (Ksum_all, Vsum_all) [bh, sum c_r, d] (every
     rank's summaries in chunk order) and the halo (K_halo, V_halo) [bh, q0 - k0, d] received
@@ -114,15 +114,17 @@ def exchange(Ksum: torch.Tensor, Vsum: torch.Tensor, K: torch.Tensor, V: torch.T
     if Ksum.shape[1] != counts[rank]:
         raise ValueError(f"rank {rank} has {Ksum.shape[1]} summaries, expected {counts[rank]}")
     mx = max(max(counts), 1)
-    # (2a) all-gather of the summaries (padded to the largest count)
-    send = torch.zeros(2, bh, mx, d, dtype=Ksum.dtype, device=Ksum.device)
-    send[0, :, :counts[rank]] = Ksum
-    send[1, :, :counts[rank]] = Vsum
-    recv = torch.empty((world * 2,) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
-    recv = recv.view((world,) + tuple(send.shape))
-    Ksum_all = torch.cat([recv[r, 0, :, :counts[r]] for r in range(world)], dim=1).contiguous()
-    Vsum_all = torch.cat([recv[r, 1, :, :counts[r]] for r in range(world)], dim=1).contiguous()
+    Ksum_all = Vsum_all = None
+    if summaries:
+        # (2a) all-gather of the summaries (padded to the largest count)
+        send = torch.zeros(2, bh, mx, d, dtype=Ksum.dtype, device=Ksum.device)
+        send[0, :, :counts[rank]] = Ksum
+        send[1, :, :counts[rank]] = Vsum
+        recv = torch.empty((world * 2,) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
+        dist.all_gather_into_tensor(recv, send, group=group)
+        recv = recv.view((world,) + tuple(send.shape))
+        Ksum_all = torch.cat([recv[r, 0, :, :counts[r]] for r in range(world)], dim=1).contiguous()
+        Vsum_all = torch.cat([recv[r, 1, :, :counts[r]] for r in range(world)], dim=1).contiguous()
     # (2b) halo from the previous rank, to the next rank
     ops = []
     nxt = shards[rank + 1] if rank + 1 < world else None
@@ -140,16 +142,65 @@ def exchange(Ksum: torch.Tensor, Vsum: torch.Tensor, K: torch.Tensor, V: torch.T
     return Ksum_all, Vsum_all, halo_in[:, :hl], halo_in[:, hl:]
 
 
+class PeerSummaries:
+    """The global summary list as symmetric memory: every rank holds [2, bh, n_chunks, d]
+    (K~ and beta^) and knows every peer's address, so eva_summarize_range_bcast stores each
+    rank's summaries straight into all ranks' copies over NVLink (the summarise and the
+    all-gather are one kernel); a device-side barrier then orders the readers."""
+
+    def __init__(self, bh: int, n_chunks: int, d: int, dtype, device, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.buf = symm.empty((2, bh, max(n_chunks, 1), d), dtype=dtype, device=device)
+        gname = (group or dist.group.WORLD).group_name
+        self.handle = symm.rendezvous(self.buf, gname)
+        half = bh * max(n_chunks, 1) * d * self.buf.element_size()
+        ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        self.ptr_k = torch.tensor(ptrs, dtype=torch.int64, device=device)
+        self.ptr_v = torch.tensor([p + half for p in ptrs], dtype=torch.int64, device=device)
+        self.n_chunks = n_chunks
+
+    def barrier(self):
+        self.handle.barrier(channel=0)
+
+
+def exchange_p2p(cfg, K: torch.Tensor, V: torch.Tensor, shards: List[SeqShard], rank: int,
+                 peers: PeerSummaries, group=None):
+    """The exchange with the summary all-gather fused into the summarising kernel (NVLink
+    stores into every rank's symmetric buffer); the halo still moves by NCCL send/recv."""
+    me = shards[rank]
+    sub = api.make_config(cfg.B, cfg.H, me.q1 - me.q0, cfg.d_head, cfg.chunk, cfg.window,
+                          bh_begin=cfg.bh_begin, bh_count=cfg.bh_count, mode=cfg.mode,
+                          dtype=api._tdtype(cfg), scale=cfg.scale, lam=cfg.lambda_, clip=cfg.clip,
+                          seed=cfg.seed, layer=cfg.layer, omega_mode=cfg.omega_mode,
+                          summary_bias=cfg.summary_bias)
+    api.eva_summarize_range_bcast(sub, me.q0 // cfg.chunk, K, V, peers.ptr_k, peers.ptr_v,
+                                  peers.n_chunks)
+    peers.barrier()  # every rank's summaries have landed in every copy
+    _, _, Kh, Vh = exchange(K.new_zeros(K.shape[0], (me.q1 - me.q0) // cfg.chunk, K.shape[2]),
+                            V.new_zeros(V.shape[0], (me.q1 - me.q0) // cfg.chunk, V.shape[2]),
+                            K, V, shards, rank, cfg.chunk, group, summaries=False)
+    return peers.buf[0, :, :peers.n_chunks], peers.buf[1, :, :peers.n_chunks], Kh, Vh
+
+
 def _peer(r: int, group) -> int:
     import torch.distributed as dist
     return r if group is None else dist.get_global_rank(group, r)
 
 
 def cp_prefill(cfg, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, shards: List[SeqShard],
-               rank: int, group=None, simt: bool = False, want_lse: bool = True):
+               rank: int, group=None, simt: bool = False, want_lse: bool = True,
+               peers: Optional[PeerSummaries] = None):
     """Context-parallel prefill on this rank: Q/K/V [bh, q1 - q0, d] of this rank's shard of
-    a sequence of cfg.T positions.  Returns (O, lse) for the shard."""
+    a sequence of cfg.T positions.  Returns (O, lse) for the shard.  With `peers` (symmetric
+    memory for T // C summaries) the summary all-gather is fused into the summarising kernel."""
     me = shards[rank]
+    if peers is not None:
+        Ks_all, Vs_all, Kh, Vh = exchange_p2p(cfg, K, V, shards, rank, peers, group)
+        Kc = torch.cat([Kh, K], dim=1) if Kh.shape[1] else K
+        Vc = torch.cat([Vh, V], dim=1) if Vh.shape[1] else V
+        return api.eva_attn_prefill_range(cfg, me.q0, me.k0, Q, Kc, Vc, Ks_all.contiguous(),
+                                          Vs_all.contiguous(), want_lse=want_lse, simt=simt)
     n = me.q1 - me.q0
     sub = api.make_config(cfg.B, cfg.H, n, cfg.d_head, cfg.chunk, cfg.window, bh_begin=cfg.bh_begin,
                           bh_count=cfg.bh_count, mode=cfg.mode, dtype=api._tdtype(cfg), scale=cfg.scale,

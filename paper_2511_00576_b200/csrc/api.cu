@@ -196,6 +196,30 @@ eva_status eva_summarize_range(const eva_config* cfg, int32_t chunk0, const void
                      "eva_summarize_range");
 }
 
+eva_status eva_summarize_range_bcast(const eva_config* cfg, int32_t chunk0, const void* K, const void* V,
+                                     const float* eps, const uint64_t* dst_ksum, const uint64_t* dst_vsum,
+                                     int32_t n_dst, int32_t dst_rows, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (chunk0 < 0) return fail(EVA_ERR_INVALID_ARG, "chunk0=%d must be >= 0", chunk0);
+  if (n_dst < 0 || n_dst > 64) return fail(EVA_ERR_INVALID_ARG, "n_dst=%d outside [0, 64]", n_dst);
+  const int nC = cfg->T / cfg->chunk;
+  if (dst_rows < chunk0 + nC)
+    return fail(EVA_ERR_INVALID_ARG, "dst_rows=%d < chunk0 + T/C = %d", dst_rows, chunk0 + nC);
+  if (cfg->bh_count == 0 || nC == 0 || n_dst == 0) return ok();
+  const void* p[] = {K, V, dst_ksum, dst_vsum};
+  const char* nm[] = {"K", "V", "dst_ksum", "dst_vsum"};
+  if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  cudaError_t e = eva::launch_summarize_bcast(*cfg, chunk0, K, V, eps,
+                                              reinterpret_cast<const unsigned long long*>(dst_ksum),
+                                              reinterpret_cast<const unsigned long long*>(dst_vsum), n_dst,
+                                              dst_rows, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(EVA_ERR_UNSUPPORTED, "chunk %d too large for the broadcasting summariser", cfg->chunk);
+  return cuda_status(e, "eva_summarize_range_bcast");
+}
+
 eva_status eva_attn_prefill_range(const eva_config* cfg, int64_t q0, int32_t n_q, int64_t k0,
                                   int32_t n_kv, const void* Q, const void* K, const void* V,
                                   const void* Ksum, const void* Vsum, int32_t n_sum, void* O,

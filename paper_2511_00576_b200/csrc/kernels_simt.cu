@@ -211,6 +211,39 @@ __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, cons
                                 Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D);
 }
 
+// Summaries broadcast to n_dst destination buffers (context parallelism: every rank's copy
+// of the global summary list, reached through NVLink peer pointers): the summary of chunk
+// c0 + c is computed once into shared memory and stored to row (c0 + c) of unit u of each
+// destination [units, dst_rows, D] -- the compute and the all-gather in one kernel.
+template <typename T, int D, int NI>
+__global__ void __launch_bounds__(128) summarize_bcast_kernel(eva_config cfg, const T* __restrict__ K,
+                                                             const T* __restrict__ V,
+                                                             const float* __restrict__ eps,
+                                                             const unsigned long long* __restrict__ dst_k,
+                                                             const unsigned long long* __restrict__ dst_v,
+                                                             int n_dst, int dst_rows, int c0) {
+  __shared__ __align__(16) T sk[D];
+  __shared__ __align__(16) T sv[D];
+  pdl_wait();
+  pdl_trigger();
+  const int C = cfg.chunk, nC = cfg.T / C;
+  const int c = blockIdx.x, u = blockIdx.y;
+  const T* Kc = K + ((size_t)u * cfg.T + (size_t)c * C) * D;
+  const T* Vc = V + ((size_t)u * cfg.T + (size_t)c * C) * D;
+  summarize_chunk_reg<T, D, NI>([&](int r) { return Kc + (size_t)r * D; }, [&](int r) { return Vc + (size_t)r * D; },
+                                C, eps ? eps + ((size_t)u * nC + c) * D : nullptr,
+                                (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg, sk, sv);
+  __syncthreads();
+  constexpr int PCS = D * (int)sizeof(T) / 16;  // 16-byte pieces per row
+  const size_t row = ((size_t)u * dst_rows + (size_t)(c0 + c)) * D;
+  for (int i = threadIdx.x; i < n_dst * PCS * 2; i += blockDim.x) {
+    const int which = i / (n_dst * PCS), rest = i % (n_dst * PCS), dst = rest / PCS, pc = rest % PCS;
+    const uint4 val = reinterpret_cast<const uint4*>(which ? sv : sk)[pc];
+    T* base = reinterpret_cast<T*>(which ? dst_v[dst] : dst_k[dst]);
+    reinterpret_cast<uint4*>(base + row)[pc] = val;
+  }
+}
+
 // Rows per lane slot of the register summariser for (C, D, T); > 8 means "too large".
 template <typename T, int D>
 constexpr int summ_reg_ni(int C) {
@@ -723,6 +756,35 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
     }
   }));
   note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_summarize_bcast(const eva_config& cfg, int c0, const void* K, const void* V,
+                                   const float* eps, const unsigned long long* dst_k,
+                                   const unsigned long long* dst_v, int n_dst, int dst_rows, cudaStream_t s) {
+  const int nC = cfg.T / cfg.chunk;
+  if (nC == 0 || cfg.bh_count == 0 || n_dst == 0) return cudaSuccess;
+  cudaError_t err = cudaErrorNotSupported;
+  EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
+    const int ni = summ_reg_ni<T, D>(cfg.chunk);
+    if (ni <= 16) {
+      const dim3 grid(nC, cfg.bh_count);
+      if (ni <= 2)
+        err = launch_pdl(summarize_bcast_kernel<T, D, 2>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps,
+                         dst_k, dst_v, n_dst, dst_rows, c0);
+      else if (ni <= 4)
+        err = launch_pdl(summarize_bcast_kernel<T, D, 4>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps,
+                         dst_k, dst_v, n_dst, dst_rows, c0);
+      else if (ni <= 8)
+        err = launch_pdl(summarize_bcast_kernel<T, D, 8>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps,
+                         dst_k, dst_v, n_dst, dst_rows, c0);
+      else
+        err = launch_pdl(summarize_bcast_kernel<T, D, 16>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps,
+                         dst_k, dst_v, n_dst, dst_rows, c0);
+      if (err == cudaSuccess) note_launch();
+    }
+  }));
+  if (err != cudaSuccess) return err;
   return cudaGetLastError();
 }
 

@@ -15,6 +15,13 @@ namespace eva {
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
                              void* Ksum, void* Vsum, cudaStream_t s, int c0 = 0);
 
+// Summaries of the chunks of rows [c0*C, ...) stored to row c0 + c of every destination
+// [bh, dst_rows, D] buffer (dst_k/dst_v: device arrays of n_dst base addresses).  Returns
+// cudaErrorNotSupported when the chunk does not fit the register summariser (C too large).
+cudaError_t launch_summarize_bcast(const eva_config& cfg, int c0, const void* K, const void* V,
+                                   const float* eps, const unsigned long long* dst_k,
+                                   const unsigned long long* dst_v, int n_dst, int dst_rows, cudaStream_t s);
+
 // Row ranges of one prefill call: query rows are absolute positions [q0, q0 + nq), key/value
 // rows [k0, k0 + nkv), summary rows chunks [0, nsl).  The whole-sequence call is
 // {0, T, 0, T, T / C}.

@@ -184,3 +184,70 @@ def test_prefill_range_validation(cuda_device):
         eva.eva_attn_prefill_range(cfg, 512, 320, Q, K[:, :300].contiguous(), K[:, :300].contiguous(), S, S)
     with pytest.raises(eva.EvaError, match="n_sum"):
         eva.eva_attn_prefill_range(cfg, 512, 320, Q, K, K, S[:, :2].contiguous(), S[:, :2].contiguous())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,d", [(torch.bfloat16, 128), (torch.float32, 64)])
+def test_summarize_bcast_writes_every_destination(cuda_device, dtype, d):
+    """The fused summarise + all-gather kernel: three emulated ranks each summarise their shard
+    and store it into all three destination buffers (stand-ins for NVLink peer buffers);
+    every buffer ends up bitwise equal to the single-call summaries."""
+    import paper_2511_00576_b200 as eva
+    cp = _cp()
+    B, H, T, C, W = 1, 3, 1536, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W, dtype=dtype)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=41, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    nC = T // C
+    bufs = [torch.full((2, B * H, nC, d), float("nan"), dtype=dtype, device="cuda") for _ in range(3)]
+    pk = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    pv = torch.tensor([b[1].data_ptr() for b in bufs], dtype=torch.int64, device="cuda")
+    for s in cp.seq_shards(T, 3, C, W):
+        sub = eva.make_config(B, H, s.q1 - s.q0, d, C, W, dtype=dtype)
+        eva.eva_summarize_range_bcast(sub, s.q0 // C, K[:, s.q0:s.q1].contiguous(), V[:, s.q0:s.q1].contiguous(),
+                                      pk, pv, nC)
+    torch.cuda.synchronize()
+    for b in bufs:
+        assert torch.equal(b[0], ks) and torch.equal(b[1], vs)
+    with pytest.raises(eva.EvaError, match="INVALID_ARG"):   # destination rows too few
+        eva.eva_summarize_range_bcast(cfg, 0, K, V, pk, pv, nC - 1)
+
+
+def _symm_cp_worker(q):
+    """One process, world size 1, NCCL + symmetric memory: the P2P exchange path end to end."""
+    import paper_2511_00576_b200 as eva
+    cp = _cp()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        B, H, T, d, C, W = 1, 2, 1024, 128, 64, 256
+        cfg = eva.make_config(B, H, T, d, C, W)
+        Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=42, device="cuda")
+        O, lse, _, _ = eva.eva_attn_prefill(cfg, Q, K, V)
+        try:
+            peers = cp.PeerSummaries(B * H, T // C, d, torch.bfloat16, "cuda")
+        except Exception as e:  # symmetric memory unavailable on this box
+            q.put(("skip", repr(e)[:200]))
+            return
+        sh = cp.seq_shards(T, 1, C, W)
+        O2, lse2 = cp.cp_prefill(cfg, Q, K, V, sh, 0, peers=peers)
+        torch.cuda.synchronize()
+        q.put(("ok", bool(torch.equal(O2, O) and torch.equal(lse2, lse))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_cp_prefill_symmetric_memory_world1(cuda_device):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_symm_cp_worker, args=(q,))
+    p.start()
+    p.join(timeout=300)
+    assert p.exitcode == 0
+    kind, val = q.get(timeout=5)
+    if kind == "skip":
+        pytest.skip(f"symmetric memory unavailable: {val}")
+    assert val is True
