@@ -30,8 +30,10 @@ def alg(BH, T, d, C, W):
 
 def main():
     out = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
-    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                        "MEASURED_PEAKS.json")))
+    pp = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    # measured peaks when the driver wrote them, else the fallback of B200_PROFILING.md
+    peaks = json.load(open(pp)) if os.path.exists(pp) else {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0,
+                                                            "source": "fallback"}
     H, d, tokens = 32, 128, 131072
     flush = torch.empty(512 << 18, device="cuda")
     rows = []

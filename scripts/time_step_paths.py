@@ -1,0 +1,47 @@
+"""Which branch of the configs[1] step graph is critical: time CUDA graphs of the step's
+sub-paths (dev tool)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import eva_inputs
+import paper_2511_00576_b200 as eva
+B, H, T, d, C, W = 1, 16, 2048, 64, 64, 128
+cfg = eva.make_config(B, H, T, d, C, W)
+Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device="cuda")
+ks, vs = eva.eva_summarize(cfg, K, V)
+O = torch.empty_like(Q); lse = torch.empty(B * H, T, device="cuda")
+qn, kn, vn = (x[0] for x in eva_inputs.decode_tokens(0, B * H, 1, d, torch.bfloat16, seed=1, device="cuda"))
+cache = eva.DecodeCache(cfg, T // C + 2, device="cuda")
+od = torch.empty(B * H, d, dtype=torch.bfloat16, device="cuda")
+flush = torch.empty(512 << 18, device="cuda")
+s = torch.cuda.current_stream()
+side = torch.cuda.Stream()
+def summ(): eva.eva_summarize(cfg, K, V, Ksum=ks, Vsum=vs)
+def pre(): eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse)
+def hand():
+    cache.c.pos = 0
+    cache.eva_cache_load(K, V, ks, vs)
+    cache.eva_decode_step(qn, kn, vn, O=od, want_lse=False)
+def full():
+    summ()
+    side.wait_stream(s)
+    with torch.cuda.stream(side):
+        hand()
+    pre()
+    s.wait_stream(side)
+paths = {"summarize": summ, "prefill": pre, "summarize+prefill": lambda: (summ(), pre()),
+         "handoff+decode": hand, "summarize+handoff+decode": lambda: (summ(), hand()), "full step": full}
+for name, fn in paths.items():
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    ts = []
+    for _ in range(30):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); g.replay(); b.record(); torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e3)
+    ts.sort()
+    print(f"{name:28s} median {ts[15]:.1f} us  min {ts[0]:.1f} us")
