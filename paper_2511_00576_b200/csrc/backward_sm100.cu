@@ -72,7 +72,7 @@ struct __align__(1024) BwdSm {
   float dqs[BwdT<D>::DQS_FLOATS]; // dQ staging (fp32) for the bulk reduce-add
   __nv_bfloat16 p[BwdT<D>::PBUF][BwdT<D>::PSMEM ? BK * BQ : 8];  // P^T [128 keys][BQ] (PSMEM)
   float lse2[NSQ][BQ], Dq[NSQ][BQ];  // per Q/dO ring slot, loaded by the producer warp
-  uint64_t kv_full, kv_empty, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free,
+  uint64_t k_full, v_full, k_free, v_free, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free,
       ds_free[2], acc_done, acc_free, s_free, p_free[BwdT<D>::PBUF];
   uint32_t tmem_base;
 };
@@ -186,7 +186,7 @@ __device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum
 // dP(g), then dQ(g-1) (its dS buffer was written one step earlier), then -- after the
 // softmax -- dV(g), dK(g); so the softmax of step g+1 overlaps dQ(g) and its epilogue, and
 // the next item's K/V load and first MMAs overlap this item's dK/dV write-out.
-__device__ long long g_bwd_trs[5][48];  // debug timeline (EVA_BWD_TRACE)
+__device__ long long g_bwd_trs[5][512];  // debug timeline (EVA_BWD_TRACE)
 __device__ int g_bwd_trn[5];
 
 template <int D, bool TRACE>
@@ -197,7 +197,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
                       int T, int C, int W, int mode, float scale, const float* __restrict__ lse,
                       BwdWsT ws, int n_sum_items, int items_per_unit, int n_items, int seg, int trace) {
   // debug timeline (EVA_BWD_TRACE=1): CTA 0 records clock64 per role and prints it at exit
-  constexpr int TRN = 48;
+  constexpr int TRN = 512;
   auto TR = [&](int role, int code) {
     if constexpr (TRACE) {
       if (trace && blockIdx.x == 0) {
@@ -218,8 +218,10 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mKs); tma_prefetch(&mVs);
     tma_prefetch(&mQ); tma_prefetch(&mdO);
-    mbar_init(&sm->kv_full, 1);
-    mbar_init(&sm->kv_empty, 1);
+    mbar_init(&sm->k_full, 1);
+    mbar_init(&sm->v_full, 1);
+    mbar_init(&sm->k_free, 1);
+    mbar_init(&sm->v_free, 1);
     for (int s = 0; s < NSQ; ++s) {
       mbar_init(&sm->q_full[s], 1 + 32);  // the TMA expect_tx + the producer lanes' lse/D stores
       mbar_init(&sm->q_empty[s], 1);
@@ -253,55 +255,22 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
       const Item it = item_of(w);
       if (it.nsteps == 0) continue;
-      if (kcount > 0) mbar_wait(&sm->kv_empty, (kcount - 1) & 1);  // last item's dQ MMA is done
-      if (elect_one()) {
-        TR(0, 9);
-        const CUtensorMap* mk = it.is_sum ? &mKs : &mK;
-        const CUtensorMap* mv = it.is_sum ? &mVs : &mV;
-        mbar_arrive_expect_tx(&sm->kv_full, 2 * BK * D * 2);
-        for (int kb = 0; kb < D / 64; ++kb) {
-          tma_load_3d(sm->k + kb * BK * 64, mk, &sm->kv_full, kb * 64, it.k0, it.u);
-          tma_load_3d(sm->v + kb * BK * 64, mv, &sm->kv_full, kb * 64, it.k0, it.u);
-        }
-        for (int i = NSQ; i < it.nsteps; ++i)  // later Q / dO tiles of the item into L2
-          for (int kb = 0; kb < D / 64; ++kb) {
-            tma_prefetch_l2_3d(&mQ, kb * 64, (it.qt_begin + i) * BQ, it.u);
-            tma_prefetch_l2_3d(&mdO, kb * 64, (it.qt_begin + i) * BQ, it.u);
-          }
-        // the NEXT item's K/V and first Q/dO tiles into L2: its K/V load can only start once
-        // this item's last dQ MMA is done, so it must not be a DRAM round trip
-        if (w + (int)gridDim.x < n_items) {
-          const Item nx = item_of(w + gridDim.x);
-          const CUtensorMap* nk = nx.is_sum ? &mKs : &mK;
-          const CUtensorMap* nv = nx.is_sum ? &mVs : &mV;
-          for (int kb = 0; kb < D / 64; ++kb) {
-            tma_prefetch_l2_3d(nk, kb * 64, nx.k0, nx.u);
-            tma_prefetch_l2_3d(nv, kb * 64, nx.k0, nx.u);
-            for (int i = 0; i < NSQ && i < nx.nsteps; ++i) {
-              tma_prefetch_l2_3d(&mQ, kb * 64, (nx.qt_begin + i) * BQ, nx.u);
-              tma_prefetch_l2_3d(&mdO, kb * 64, (nx.qt_begin + i) * BQ, nx.u);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      for (int i = 0; i < it.nsteps; ++i, ++g) {
+      const CUtensorMap* mk = it.is_sum ? &mKs : &mK;
+      const CUtensorMap* mv = it.is_sum ? &mVs : &mV;
+      auto issue_q = [&](int i) {  // Q / dO tiles and lse / D of step i into its ring slot
         const int s = g % NSQ;
         // lse (log2 units) and D of the step's queries: loaded into registers first, so their
         // latency overlaps the wait for the ring slot
         float lv[BQ / 32], dvv[BQ / 32];
-        {
-          const int n0 = (it.qt_begin + i) * BQ;
+        const int n0 = (it.qt_begin + i) * BQ;
 #pragma unroll
-          for (int k = 0; k < BQ / 32; ++k) {
-            const int n = n0 + lane + 32 * k;
-            lv[k] = n < T ? lse[(size_t)it.u * T + n] * 1.4426950408889634f : 0.f;
-            dvv[k] = n < T ? ws.D[(size_t)it.u * T + n] : 0.f;
-          }
+        for (int k = 0; k < BQ / 32; ++k) {
+          const int n = n0 + lane + 32 * k;
+          lv[k] = n < T ? lse[(size_t)it.u * T + n] * 1.4426950408889634f : 0.f;
+          dvv[k] = n < T ? ws.D[(size_t)it.u * T + n] : 0.f;
         }
         if (g >= NSQ) mbar_wait(&sm->q_empty[s], ((g / NSQ) - 1) & 1);
         if (elect_one()) {
-          const int n0 = (it.qt_begin + i) * BQ;
           TR(0, 1);
           mbar_arrive_expect_tx(&sm->q_full[s], 2 * BQ * D * 2);
           for (int kb = 0; kb < D / 64; ++kb) {
@@ -316,7 +285,40 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
           sm->Dq[s][lane + 32 * k] = dvv[k];
         }
         mbar_arrive(&sm->q_full[s]);
+        ++g;
+      };
+      // V is free once the last item's last dP MMA is done, K only after its last dQ MMA:
+      // V first, then the first Q/dO slots, then K
+      if (kcount > 0) mbar_wait(&sm->v_free, (kcount - 1) & 1);
+      if (elect_one()) {
+        TR(0, 9);
+        mbar_arrive_expect_tx(&sm->v_full, BK * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb) tma_load_3d(sm->v + kb * BK * 64, mv, &sm->v_full, kb * 64, it.k0, it.u);
       }
+      __syncwarp();
+      const int npre = it.nsteps < NSQ ? it.nsteps : NSQ;
+      for (int i = 0; i < npre; ++i) issue_q(i);
+      if (kcount > 0) mbar_wait(&sm->k_free, (kcount - 1) & 1);
+      if (elect_one()) {
+        mbar_arrive_expect_tx(&sm->k_full, BK * D * 2);
+        for (int kb = 0; kb < D / 64; ++kb) tma_load_3d(sm->k + kb * BK * 64, mk, &sm->k_full, kb * 64, it.k0, it.u);
+      }
+      __syncwarp();
+      for (int i = npre; i < it.nsteps; ++i) issue_q(i);
+      // the NEXT item's K/V into L2 now -- about NSQ steps before this item ends (its loads can
+      // only start once this item's last dP / dQ MMAs are done); earlier prefetches are evicted
+      // by the traffic in between.  (No bulk L2 prefetch of later Q/dO tiles: the burst would
+      // queue in front of the ring's own loads in the SM's TMA unit.)
+      if (w + (int)gridDim.x < n_items && elect_one()) {
+        const Item nx = item_of(w + gridDim.x);
+        const CUtensorMap* nk = nx.is_sum ? &mKs : &mK;
+        const CUtensorMap* nv = nx.is_sum ? &mVs : &mV;
+        for (int kb = 0; kb < D / 64; ++kb) {
+          tma_prefetch_l2_3d(nk, kb * 64, nx.k0, nx.u);
+          tma_prefetch_l2_3d(nv, kb * 64, nx.k0, nx.u);
+        }
+      }
+      __syncwarp();
       ++kcount;
     }
   } else if (warp == 1) {
@@ -393,7 +395,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
         const Item it = item_of(w);
         if (it.nsteps == 0) continue;
-        mbar_wait(&sm->kv_full, kcount & 1);
+        mbar_wait(&sm->k_full, kcount & 1);
+        mbar_wait(&sm->v_full, kcount & 1);
         if (lane == 0) TR(1, 10);
         for (int i = 0; i < it.nsteps; ++i, ++g) {
           mbar_wait(&sm->q_full[g % NSQ], (g / NSQ) & 1);
@@ -401,13 +404,17 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
           tc_fence_after();
           if (lane == 0) TR(1, 2);
           issue_s(g);
+          if (i == it.nsteps - 1) {  // the item's last dP has been issued: V is free after it
+            if (elect_one()) mma_commit(&sm->v_free);
+            __syncwarp();
+          }
           if (lane == 0) TR(1, 3);
           if (i > 0) grad_step(g - 1, i - 1, kcount, false);
           if (lane == 0) TR(1, 4);
         }
         grad_step(g - 1, it.nsteps - 1, kcount, true);
         if (lane == 0) TR(1, 5);
-        if (elect_one()) mma_commit(&sm->kv_empty);  // K/V smem free once this dQ completes
+        if (elect_one()) mma_commit(&sm->k_free);  // K smem free once this dQ completes
         __syncwarp();
         ++kcount;
       }
@@ -416,7 +423,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
       const Item it = item_of(w);
       if (it.nsteps == 0) continue;
-      mbar_wait(&sm->kv_full, kcount & 1);
+      mbar_wait(&sm->k_full, kcount & 1);
+      mbar_wait(&sm->v_full, kcount & 1);
       for (int i = 0; i < it.nsteps; ++i, ++g) {
         const int s = g % NSQ;
         const uint32_t q_addr = smem_u32(sm->q[s]), do_addr = smem_u32(sm->dO[s]);
@@ -437,6 +445,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
                    smem_desc_sw128(do_addr + kb * (BQ * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
           }
           mma_commit(&sm->s_full);
+          if (i == it.nsteps - 1) mma_commit(&sm->v_free);  // V is free after the last dP
         }
         __syncwarp();
         if (i > 0) issue_dq(g - 1);
@@ -459,7 +468,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         __syncwarp();
       }
       issue_dq(g - 1);
-      if (elect_one()) mma_commit(&sm->kv_empty);  // K/V smem free once this dQ completes
+      if (elect_one()) mma_commit(&sm->k_free);  // K smem free once this dQ completes
       __syncwarp();
       ++kcount;
     }
@@ -640,9 +649,9 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
           }
           continue;
         }
-        // stage dQ [64 queries][d] and reduce-add it into the fp32 accumulator with one bulk
-        // TMA operation (the previous reduce must have finished reading the staging buffer)
-        // two halves of 32 queries through a [32][d] staging buffer
+        // stage dQ [64 queries][d] and reduce-add it into the fp32 accumulator with bulk TMA
+        // operations, in two halves of 32 queries through a [32][d] staging buffer (the
+        // previous reduce must have finished reading it)
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           if (et == 0) bulk_wait_read_all();
