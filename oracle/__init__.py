@@ -61,6 +61,9 @@ def _L():
         lib.oracle_prefill_rows.argtypes = [i, i, i, i, i, d_, D, D, D, D, D, i, I64, D, D]
         lib.oracle_backward.argtypes = [i, i, i, i, i, d_, d_, d_, i, D, D, D, D, D, D, D, D]
         lib.oracle_backward_batch.argtypes = [i, i, i, i, i, i, d_, d_, d_, i, D, D, D, D, D, D, D, D]
+        lib.oracle_backward_ext.argtypes = [i, i, i, i, i, d_, d_, d_, d_, i, D, D, D, D, D, D, D, D]
+        lib.oracle_backward_ext_batch.argtypes = [i, i, i, i, i, i, d_, d_, d_, d_, i, D, D, D, D, D,
+                                                  D, D, D]
         lib.oracle_cache_new.argtypes = [i, i, i, i, i, d_, d_, d_, i]
         lib.oracle_cache_new.restype = ctypes.c_void_p
         lib.oracle_cache_free.argtypes = [ctypes.c_void_p]
@@ -207,27 +210,29 @@ def prefill_rows(Q, K, V, Ksum, Vsum, rows, C: int, W: int, mode: int = SLIDING,
 
 
 def backward(Q, K, V, eps_, dO, C: int, W: int, mode: int = SLIDING, scale: float = 1.0,
-             lam: float = 0.1, clip: float = 1.0, omega_mode: int = 0):
-    """Gradients (dQ, dK, dV) of L = sum(dO * O) for one unit (oracle_backward)."""
+             lam: float = 0.1, clip: float = 1.0, omega_mode: int = 0, bias: float = 0.0):
+    """Gradients (dQ, dK, dV) of L = sum(dO * O) for one unit (oracle_backward_ext; any mode,
+    including NONCAUSAL, and the summary-logit bias of R16)."""
     Q, K, V, dO = _f64(Q), _f64(K), _f64(V), _f64(dO)
     T, d = Q.shape
     nC = T // C
     E = _f64(eps_).reshape(nC, d) if nC else np.zeros((1, d))
     dQ, dK, dV = np.zeros((T, d)), np.zeros((T, d)), np.zeros((T, d))
-    _L().oracle_backward(T, d, C, W, mode, scale, lam, clip, omega_mode, _dp(Q), _dp(K), _dp(V),
-                         _dp(E), _dp(dO), _dp(dQ), _dp(dK), _dp(dV))
+    _L().oracle_backward_ext(T, d, C, W, mode, scale, bias, lam, clip, omega_mode, _dp(Q), _dp(K),
+                             _dp(V), _dp(E), _dp(dO), _dp(dQ), _dp(dK), _dp(dV))
     return dQ, dK, dV
 
 
 def backward_batch(Q, K, V, E, dO, C: int, W: int, mode: int = SLIDING, scale: float = 1.0,
-                   lam: float = 0.1, clip: float = 1.0, omega_mode: int = 0):
+                   lam: float = 0.1, clip: float = 1.0, omega_mode: int = 0, bias: float = 0.0):
     Q, K, V, dO = _f64(Q), _f64(K), _f64(V), _f64(dO)
     BH, T, d = Q.shape
     nC = T // C
     E = _f64(E) if nC else np.zeros((BH, 1, d))
     dQ, dK, dV = np.zeros_like(Q), np.zeros_like(Q), np.zeros_like(Q)
-    _L().oracle_backward_batch(BH, T, d, C, W, mode, scale, lam, clip, omega_mode, _dp(Q), _dp(K),
-                               _dp(V), _dp(E), _dp(dO), _dp(dQ), _dp(dK), _dp(dV))
+    _L().oracle_backward_ext_batch(BH, T, d, C, W, mode, scale, bias, lam, clip, omega_mode,
+                                   _dp(Q), _dp(K), _dp(V), _dp(E), _dp(dO), _dp(dQ), _dp(dK),
+                                   _dp(dV))
     return dQ, dK, dV
 
 

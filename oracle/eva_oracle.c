@@ -481,10 +481,13 @@ EXPORT double oracle_cache_decode(const oracle_cache* s, const double* q, double
 /*    dk~ += domega); k~ = mean k_i: dk_i += dk~ / C.                         */
 /* eps is a constant.  Q, K, V, dO, dQ, dK, dV: [T, d]; eps [nC, d].          */
 /* ------------------------------------------------------------------------ */
-EXPORT void oracle_backward(int T, int d, int C, int W, int mode, double scale, double lambda,
-                            double clipv, int omega_mode, const double* Q, const double* K,
-                            const double* V, const double* eps, const double* dO, double* dQ,
-                            double* dK, double* dV) {
+/* The variants (DESIGN R15, R16) change only the visible sets and the summary logits:    */
+/* summary c visible iff c < s1 or c >= s2, locals [lo, hi) (visible_set), and the summary  */
+/* logit is s q.k~_c + bias.  The bias is a constant, so dS / dk~ / dbeta keep their form.  */
+EXPORT void oracle_backward_ext(int T, int d, int C, int W, int mode, double scale, double bias,
+                                double lambda, double clipv, int omega_mode, const double* Q,
+                                const double* K, const double* V, const double* eps,
+                                const double* dO, double* dQ, double* dK, double* dV) {
   const int nC = T / C;
   const size_t nd = (size_t)(nC > 0 ? nC : 1) * d;
   double* kt = (double*)calloc(nd, sizeof(double));
@@ -499,19 +502,21 @@ EXPORT void oracle_backward(int T, int d, int C, int W, int mode, double scale, 
   memset(dK, 0, sizeof(double) * (size_t)T * d);
   memset(dV, 0, sizeof(double) * (size_t)T * d);
   for (int n = 0; n < T; ++n) {
-    int64_t lo, ns;
-    oracle_mask(n, C, W, mode, &lo, &ns);
+    int64_t lo, hi, s1, s2;
+    visible_set(n, T, C, W, mode, &lo, &hi, &s1, &s2);
     const double* q = Q + (size_t)n * d;
     const double* g = dO + (size_t)n * d;
     int cnt = 0;
     double mx = -INFINITY;
-    for (int64_t c = 0; c < ns; ++c, ++cnt) {
+    for (int64_t c = 0; c < nC; ++c) {
+      if (!(c < s1 || c >= s2)) continue;
       double t = 0.0;
       for (int j = 0; j < d; ++j) t += q[j] * kt[(size_t)c * d + j];
-      logit[cnt] = scale * t;
+      logit[cnt] = scale * t + bias;
       if (logit[cnt] > mx) mx = logit[cnt];
+      ++cnt;
     }
-    for (int64_t m = lo; m <= n; ++m, ++cnt) {
+    for (int64_t m = lo; m < hi; ++m, ++cnt) {
       double t = 0.0;
       for (int j = 0; j < d; ++j) t += q[j] * K[(size_t)m * d + j];
       logit[cnt] = scale * t;
@@ -522,14 +527,18 @@ EXPORT void oracle_backward(int T, int d, int C, int W, int mode, double scale, 
     for (int i = 0; i < cnt; ++i) logit[i] = exp(logit[i] - mx) / z; /* now P */
     for (int j = 0; j < d; ++j) o[j] = 0.0;
     int i = 0;
-    for (int64_t c = 0; c < ns; ++c, ++i)
+    for (int64_t c = 0; c < nC; ++c) {
+      if (!(c < s1 || c >= s2)) continue;
       for (int j = 0; j < d; ++j) o[j] += logit[i] * bt[(size_t)c * d + j];
-    for (int64_t m = lo; m <= n; ++m, ++i)
+      ++i;
+    }
+    for (int64_t m = lo; m < hi; ++m, ++i)
       for (int j = 0; j < d; ++j) o[j] += logit[i] * V[(size_t)m * d + j];
     double Dn = 0.0;
     for (int j = 0; j < d; ++j) Dn += g[j] * o[j];
     i = 0;
-    for (int64_t c = 0; c < ns; ++c, ++i) {
+    for (int64_t c = 0; c < nC; ++c) {
+      if (!(c < s1 || c >= s2)) continue;
       double dp = 0.0;
       for (int j = 0; j < d; ++j) dp += g[j] * bt[(size_t)c * d + j];
       const double dS = logit[i] * (dp - Dn);
@@ -538,8 +547,9 @@ EXPORT void oracle_backward(int T, int d, int C, int W, int mode, double scale, 
         dkt[(size_t)c * d + j] += scale * dS * q[j];
         dbt[(size_t)c * d + j] += logit[i] * g[j];
       }
+      ++i;
     }
-    for (int64_t m = lo; m <= n; ++m, ++i) {
+    for (int64_t m = lo; m < hi; ++m, ++i) {
       double dp = 0.0;
       for (int j = 0; j < d; ++j) dp += g[j] * V[(size_t)m * d + j];
       const double dS = logit[i] * (dp - Dn);
@@ -599,15 +609,32 @@ EXPORT void oracle_backward(int T, int d, int C, int W, int mode, double scale, 
   free(a); free(dom); free(kt); free(bt); free(om); free(dkt); free(dbt); free(logit); free(o);
 }
 
-EXPORT void oracle_backward_batch(int BH, int T, int d, int C, int W, int mode, double scale,
-                                  double lambda, double clipv, int omega_mode, const double* Q,
-                                  const double* K, const double* V, const double* eps,
-                                  const double* dO, double* dQ, double* dK, double* dV) {
+EXPORT void oracle_backward(int T, int d, int C, int W, int mode, double scale, double lambda,
+                            double clipv, int omega_mode, const double* Q, const double* K,
+                            const double* V, const double* eps, const double* dO, double* dQ,
+                            double* dK, double* dV) {
+  oracle_backward_ext(T, d, C, W, mode, scale, 0.0, lambda, clipv, omega_mode, Q, K, V, eps, dO,
+                      dQ, dK, dV);
+}
+
+EXPORT void oracle_backward_ext_batch(int BH, int T, int d, int C, int W, int mode, double scale,
+                                      double bias, double lambda, double clipv, int omega_mode,
+                                      const double* Q, const double* K, const double* V,
+                                      const double* eps, const double* dO, double* dQ,
+                                      double* dK, double* dV) {
   const int nC = T / C;
 #pragma omp parallel for schedule(dynamic, 1)
   for (int u = 0; u < BH; ++u) {
     const size_t off = (size_t)u * T * d;
-    oracle_backward(T, d, C, W, mode, scale, lambda, clipv, omega_mode, Q + off, K + off, V + off,
-                    eps + (size_t)u * nC * d, dO + off, dQ + off, dK + off, dV + off);
+    oracle_backward_ext(T, d, C, W, mode, scale, bias, lambda, clipv, omega_mode, Q + off, K + off,
+                        V + off, eps + (size_t)u * nC * d, dO + off, dQ + off, dK + off, dV + off);
   }
+}
+
+EXPORT void oracle_backward_batch(int BH, int T, int d, int C, int W, int mode, double scale,
+                                  double lambda, double clipv, int omega_mode, const double* Q,
+                                  const double* K, const double* V, const double* eps,
+                                  const double* dO, double* dQ, double* dK, double* dV) {
+  oracle_backward_ext_batch(BH, T, d, C, W, mode, scale, 0.0, lambda, clipv, omega_mode, Q, K, V,
+                            eps, dO, dQ, dK, dV);
 }

@@ -63,25 +63,29 @@ def test_backward_matches_finite_differences(mode, omega_mode):
         np.testing.assert_allclose(dX, num, rtol=0, atol=2e-7)
 
 
-def _torch_direct(Q, K, V, E, C, W, mode, scale, lam=0.1, clip=1.0):
-    """EVA by explicit sets and the linear-domain Eq.9/Eq.10 mixture, in torch."""
+def _torch_direct(Q, K, V, E, C, W, mode, scale, lam=0.1, clip=1.0, multiplicity=1.0):
+    """EVA by explicit sets and the linear-domain Eq.9/Eq.10 mixture, in torch.
+    mode: oracle.SLIDING / oracle.BLOCK or a bruteforce.partition_sets name ("noncausal:T");
+    multiplicity: the weight of each chunk's Z-term (R16: bias = ln multiplicity)."""
     T = Q.shape[0]
     rows = []
+    names = {oracle.SLIDING: "sliding", oracle.BLOCK: "block"}
     for n in range(T):
-        Eset, chunks = partition_sets(n, C, W, "sliding" if mode == oracle.SLIDING else "block")
+        Eset, chunks = partition_sets(n, C, W, names.get(mode, mode))
         num = torch.zeros(V.shape[1], dtype=torch.float64)
         Z = torch.zeros((), dtype=torch.float64)
         for m in Eset:
             w = torch.exp(scale * (Q[n] * K[m]).sum())
             Z = Z + w
             num = num + w * V[m]
-        for c, members in enumerate(chunks):
+        for members in chunks:
+            c = members[0] // C  # the chunk's own index (non-causal lists skip the block)
             Kc, Vc = K[members], V[members]
             kt = Kc.sum(0) / len(members)
             om = lam * torch.clamp(kt + E[c], -clip, clip)
             xi = torch.exp((Kc * om).sum(1) - 0.5 * (Kc * Kc).sum(1))
             beta = (xi[:, None] * Vc).sum(0) / xi.sum()
-            w = torch.exp(scale * (Q[n] * kt).sum())
+            w = multiplicity * torch.exp(scale * (Q[n] * kt).sum())
             Z = Z + w
             num = num + w * beta
         rows.append(num / Z)
@@ -142,3 +146,79 @@ def test_backward_linear_in_dO_and_batch_driver():
     c = oracle.backward(Q[0], K[0], V[0], E[0], 2 * G[0] - G2, C, W)
     for x, y, z in zip(a, b, c):
         np.testing.assert_allclose(z, 2 * x - y, rtol=0, atol=1e-12)
+
+
+# ---- the variants (NEXT row 3 backward): non-causal partition (R15), summary bias (R16)
+
+def _loss_ext(Q, K, V, E, G, C, W, mode, scale, bias):
+    ks, vs = oracle.summarize(K, V, E, C)
+    O, _ = oracle.prefill_ext_batch(Q[None], K[None], V[None], ks[None], vs[None], C, W, mode,
+                                    scale, bias)
+    return float((O[0] * G).sum())
+
+
+@pytest.mark.parametrize("mode,bias", [(oracle.NONCAUSAL, 0.0), (oracle.NONCAUSAL, 0.9),
+                                       (oracle.SLIDING, math.log(2.0)), (oracle.BLOCK, -0.4)])
+def test_variant_backward_matches_finite_differences(mode, bias):
+    """Every element of dQ, dK, dV against central differences of the forward oracle
+    (summarize + oracle_prefill_ext, itself pinned in test_oracle_variants.py)."""
+    T, d, C, W, scale = 16, 4, 2, 4, 0.7
+    Q, K, V, E, G = _inputs(T, d, C, 31 + mode)
+    dQ, dK, dV = oracle.backward(Q, K, V, E, G, C, W, mode, scale, bias=bias)
+    h = 1e-6
+    for X, dX in ((Q, dQ), (K, dK), (V, dV)):
+        num = np.zeros_like(X)
+        for idx in np.ndindex(*X.shape):
+            x0 = X[idx]
+            X[idx] = x0 + h
+            lp = _loss_ext(Q, K, V, E, G, C, W, mode, scale, bias)
+            X[idx] = x0 - h
+            lm = _loss_ext(Q, K, V, E, G, C, W, mode, scale, bias)
+            X[idx] = x0
+            num[idx] = (lp - lm) / (2 * h)
+        np.testing.assert_allclose(dX, num, rtol=0, atol=2e-7)
+
+
+@pytest.mark.parametrize("C,W,T,mult", [(2, 4, 16, 1.0), (3, 6, 18, 3.0), (2, 6, 12, 1.0)])
+def test_noncausal_backward_matches_autograd_of_direct_form(C, W, T, mult):
+    """Explicit non-causal sets (own block incl. future, chunks before AND after) with the
+    chunk multiplicity as a Z weight; the oracle takes bias = ln(multiplicity)."""
+    d, scale = 5, 0.5
+    Q, K, V, E, G = _inputs(T, d, C, 200 + C + W + T, scale_kv=0.6)
+    tq, tk, tv = (torch.tensor(x, requires_grad=True) for x in (Q, K, V))
+    O = _torch_direct(tq, tk, tv, torch.tensor(E), C, W, f"noncausal:{T}", scale,
+                      multiplicity=mult)
+    (O * torch.tensor(G)).sum().backward()
+    got = oracle.backward(Q, K, V, E, G, C, W, oracle.NONCAUSAL, scale, bias=math.log(mult))
+    for g, w in zip(got, (tq.grad, tk.grad, tv.grad)):
+        np.testing.assert_allclose(g, w.numpy(), rtol=0, atol=1e-11)
+
+
+@pytest.mark.parametrize("mode", [oracle.SLIDING, oracle.BLOCK])
+def test_bias_backward_matches_autograd_with_multiplicity(mode):
+    C, W, d, scale = 4, 8, 4, 0.6
+    T = 3 * W + 3
+    Q, K, V, E, G = _inputs(T, d, C, 300 + mode, scale_kv=0.6)
+    tq, tk, tv = (torch.tensor(x, requires_grad=True) for x in (Q, K, V))
+    O = _torch_direct(tq, tk, tv, torch.tensor(E), C, W, mode, scale, multiplicity=C)
+    (O * torch.tensor(G)).sum().backward()
+    got = oracle.backward(Q, K, V, E, G, C, W, mode, scale, bias=math.log(C))
+    for g, w in zip(got, (tq.grad, tk.grad, tv.grad)):
+        np.testing.assert_allclose(g, w.numpy(), rtol=0, atol=1e-11)
+
+
+def _full_softmax_grads(Q, K, V, G, scale):
+    tq, tk, tv = (torch.tensor(x, requires_grad=True) for x in (Q, K, V))
+    (torch.softmax(scale * tq @ tk.T, -1) @ tv * torch.tensor(G)).sum().backward()
+    return tq.grad.numpy(), tk.grad.numpy(), tv.grad.numpy()
+
+
+@pytest.mark.parametrize("C,W,T", [(1, 3, 12), (4, 64, 40), (8, 32, 32)])
+def test_noncausal_special_cases_are_full_softmax(C, W, T):
+    """Non-causal with C = 1 (every token outside the block is its own summary) or W >= T
+    (one block, no summaries) is textbook bidirectional softmax attention (Eq.1)."""
+    d, scale = 6, 0.8
+    Q, K, V, E, G = _inputs(T, d, C, 9 * C + T)
+    got = oracle.backward(Q, K, V, E, G, C, W, oracle.NONCAUSAL, scale)
+    for g, w in zip(got, _full_softmax_grads(Q, K, V, G, scale)):
+        np.testing.assert_allclose(g, w, rtol=0, atol=1e-12)
