@@ -70,8 +70,9 @@ typedef enum { EVA_WINDOW_SLIDING = 0, EVA_WINDOW_BLOCK = 1, EVA_NONCAUSAL = 2 }
  *   E(n) = n's whole block [lo, min(lo + W, T)), lo = floor(n/W)*W (later positions of the
  *   block included), plus the summaries of EVERY complete chunk outside that block, before
  *   and after it: c < lo/C or c >= (lo + W)/C.  Requires T % C == 0 (every position is a
- *   local or inside exactly one summarised chunk).  Decode, cache, backward and the
- *   query-range prefill are causal by construction and return EVA_ERR_UNSUPPORTED. */
+ *   local or inside exactly one summarised chunk).  Prefill and its backward take it;
+ *   decode, cache and the query-range prefill are causal by construction and return
+ *   EVA_ERR_UNSUPPORTED. */
 
 /* Proposal of Eq.15, reading R3:
  *   AS_PRINTED:     omega_c = lambda * clip(k~_c + eps_c, -clip, clip)   (default)
@@ -312,6 +313,9 @@ eva_status eva_attn_prefill_host(eva_pipeline* pipe, const eva_config* cfg, cons
  * writes dQ, dK, dV, differentiating through the attention (Eq.12-14) AND the
  * chunk summaries (k~ = chunk mean, omega = Eq.15, beta^ = Eq.9/10); eps is a
  * constant; d clip/dx = 1 on the closed range [-clip, clip] (R14).
+ * Every cfg.mode (incl. EVA_NONCAUSAL, T % chunk == 0) and cfg.summary_bias (R16: a
+ * constant added to the summary logits, so the summary P carries it and dS keeps its form)
+ * are supported; the forward must have used the same cfg.
  * Q, K, V, O, dO, dQ, dK, dV : [bh_count, T, d] cfg.dtype
  * Ksum, Vsum : [bh_count, nC, d] cfg.dtype -- the summaries the forward used
  * O, lse     : the forward's output and natural-log lse ([bh_count, T] fp32)

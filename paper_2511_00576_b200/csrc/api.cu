@@ -82,7 +82,7 @@ eva_status check_cfg(const eva_config* cfg, bool need_T) {
   return EVA_OK;
 }
 
-// Decode, cache, backward and the query-range prefill are causal by construction (R15).
+// Decode, cache and the query-range prefill are causal by construction (R15).
 eva_status check_causal(const eva_config* cfg, const char* what) {
   if (cfg->mode == EVA_NONCAUSAL)
     return fail(EVA_ERR_UNSUPPORTED, "%s is causal; EVA_NONCAUSAL applies to the prefill only", what);
@@ -553,9 +553,9 @@ eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K
                              void* workspace, size_t workspace_bytes, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
-  if ((st = check_causal(cfg, "eva_attn_backward")) != EVA_OK) return st;
-  if (cfg->summary_bias != 0.f)
-    return fail(EVA_ERR_UNSUPPORTED, "eva_attn_backward: summary_bias != 0 is not implemented");
+  if (cfg->mode == EVA_NONCAUSAL && cfg->T % cfg->chunk != 0)
+    return fail(EVA_ERR_INVALID_ARG, "EVA_NONCAUSAL needs T %% chunk == 0 (T=%d chunk=%d)", cfg->T,
+                cfg->chunk);
   if (cfg->bh_count == 0) return ok();
   const void* p[] = {Q, K, V, O, lse, dO, dQ, dK, dV, workspace};
   const char* nm[] = {"Q", "K", "V", "O", "lse", "dO", "dQ", "dK", "dV", "workspace"};

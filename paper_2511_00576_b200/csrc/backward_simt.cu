@@ -40,13 +40,20 @@ namespace {
 constexpr int BT = 64;        // keys per tile, queries per tile
 constexpr int BWD_THREADS = 256;
 
-// Last query that sees local key m (inverse of mask_range: lo(n) <= m).
+// Queries that see local key m: [local_qlo, local_qhi] (inverse of visible_set).  Causal:
+// from m itself to the last query whose window still starts at or before m; non-causal
+// (R15): m's whole block of W.
+__host__ __device__ __forceinline__ int64_t local_qlo(int64_t m, int W, int mode) {
+  return mode == EVA_NONCAUSAL ? (m / W) * (int64_t)W : m;
+}
 __host__ __device__ __forceinline__ int64_t local_qhi(int64_t m, int C, int W, int mode) {
   if (mode == EVA_WINDOW_SLIDING) return (m / C + W / C) * (int64_t)C - 1;
   return (m / W + 1) * (int64_t)W - 1;
 }
-// First query that sees summary c (c < nsum(n)).
+// First query that sees summary c: causal c < nsum(n); non-causal every query outside the
+// block holding chunk c sees it, so the query walk starts at 0 (the block is masked).
 __host__ __device__ __forceinline__ int64_t summary_qlo(int64_t c, int C, int W, int mode) {
+  if (mode == EVA_NONCAUSAL) return 0;
   if (mode == EVA_WINDOW_SLIDING) return (c + W / C) * (int64_t)C;
   return (c / (W / C) + 1) * (int64_t)W;
 }
@@ -159,7 +166,7 @@ struct MainSmem {
   float Ks[BT][D + 1], Vs[BT][D + 1], Qs[BT][D + 1], dOs[BT][D + 1];
   float Ps[BT][BT + 1], dSs[BT][BT + 1];
   float lse2[BT], Dd[BT];
-  int rlo[BT], rns[BT];
+  int rlo[BT], rhi[BT], rs1[BT], rs2[BT];
 };
 
 template <typename T, int D>
@@ -175,6 +182,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
   const int tid = threadIdx.x;
   const float scale = cfg.scale;
   const float sl2 = scale * 1.4426950408889634f;
+  const float bias2 = cfg.summary_bias * 1.4426950408889634f;
 
   // ---- decode the work item
   bool is_sum;
@@ -199,7 +207,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
       const int t = item - n_sum_items;
       k0 = t * BT;
       nk = min(BT, Tn - k0);
-      qt_begin = t;
+      qt_begin = (int)(local_qlo(k0, W, mode) / BT);
       const int64_t qhi = min((int64_t)Tn - 1, local_qhi(k0 + nk - 1, C, W, mode));
       qt_end = (int)(qhi / BT) + 1;
     }
@@ -234,14 +242,20 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
     if (tid < BT) {
       const int64_t n = (int64_t)n0 + tid;
       if (n < Tn) {
-        const Range rg = mask_range(n, C, W, mode);
-        sm.rlo[tid] = (int)rg.lo;
-        sm.rns[tid] = (int)rg.nsum;
-        sm.lse2[tid] = lse[(size_t)u * Tn + n] * 1.4426950408889634f;
+        const Vis vs = visible_set(n, C, W, mode, Tn);
+        sm.rlo[tid] = (int)vs.lo;
+        sm.rhi[tid] = (int)vs.hi;
+        sm.rs1[tid] = (int)vs.s1;
+        sm.rs2[tid] = (int)min(vs.s2, (int64_t)nC);
+        // P = exp2(s S log2e + bias log2e - lse log2e) for summary keys (R16): the bias
+        // is folded into the per-row constant
+        sm.lse2[tid] = lse[(size_t)u * Tn + n] * 1.4426950408889634f - (is_sum ? bias2 : 0.f);
         sm.Dd[tid] = ws.D[(size_t)u * Tn + n];
       } else {
         sm.rlo[tid] = 1 << 30;  // nothing visible
-        sm.rns[tid] = 0;
+        sm.rhi[tid] = 0;
+        sm.rs1[tid] = 0;
+        sm.rs2[tid] = 1 << 30;
         sm.lse2[tid] = 0.f;
         sm.Dd[tid] = 0.f;
       }
@@ -279,14 +293,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1)
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int i = ty * 4 + a;
-        const int n = n0 + i;
-        const int lo = sm.rlo[i], ns = sm.rns[i];
+        const int lo = sm.rlo[i], hi = sm.rhi[i], s1 = sm.rs1[i], s2 = sm.rs2[i];
         const float l2 = sm.lse2[i], Dn = sm.Dd[i];
 #pragma unroll
         for (int b = 0; b < 4; ++b) {
           const int j = tx + 16 * b;
           const int x = k0 + j;
-          const bool vis = j < nk && (is_sum ? (x < ns) : (x >= lo && x <= n));
+          const bool vis = j < nk && (is_sum ? (x < s1 || x >= s2) : (x >= lo && x < hi));
           const float p = vis ? exp2f(fmaf(s[a][b], sl2, -l2)) : 0.f;
           sm.Ps[i][j] = p;
           sm.dSs[i][j] = p * (dp[a][b] - Dn);

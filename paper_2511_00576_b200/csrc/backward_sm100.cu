@@ -81,14 +81,26 @@ struct BwdWsT {
   float *D, *dQ, *dK, *dV, *dKs, *dVs;
 };
 
-// Inverse maps of the causal mask (same formulas as backward_simt.cu)
+// Inverse maps of the mask (same formulas as backward_simt.cu): queries [qlo_of_key,
+// qhi_of_key] see local key m; summary c is seen from qlo_of_summary on -- for the
+// non-causal partition (R15) by every query outside the block of W holding chunk c.
+__host__ __device__ __forceinline__ int64_t qlo_of_key(int64_t m, int W, int mode) {
+  return mode == EVA_NONCAUSAL ? (m / W) * (int64_t)W : m;
+}
 __host__ __device__ __forceinline__ int64_t qhi_of_key(int64_t m, int C, int W, int mode) {
   if (mode == EVA_WINDOW_SLIDING) return (m / C + W / C) * (int64_t)C - 1;
   return (m / W + 1) * (int64_t)W - 1;
 }
 __host__ __device__ __forceinline__ int64_t qlo_of_summary(int64_t c, int C, int W, int mode) {
+  if (mode == EVA_NONCAUSAL) return 0;
   if (mode == EVA_WINDOW_SLIDING) return (c + W / C) * (int64_t)C;
   return (c / (W / C) + 1) * (int64_t)W;
+}
+// Bits [a, b) of a 32-column group (empty when b <= a).
+__device__ __forceinline__ uint32_t range_bits(int a, int b) {
+  a = min(max(a, 0), 32);
+  b = min(max(b, 0), 32);
+  return (uint32_t)(((1ull << b) - 1ull) & ~((1ull << a) - 1ull));
 }
 template <int BQ> __host__ __device__ __forceinline__ int nqt(int T) { return (T + BQ - 1) / BQ; }
 template <int BQ>
@@ -171,7 +183,7 @@ __device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum
     it.is_sum = false;
     it.k0 = (item - n_sum_items) * BK;
     it.nk = min(BK, T - it.k0);
-    it.qt_begin = it.k0 / BQ;
+    it.qt_begin = (int)(qlo_of_key(it.k0, W, mode) / BQ);
     const int64_t qhi = min((int64_t)T - 1, qhi_of_key(it.k0 + it.nk - 1, C, W, mode));
     qt_end = (int)(qhi / BQ) + 1;
   }
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(BWD_TC_THREADS, 1)
 bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
                       const __grid_constant__ CUtensorMap mKs, const __grid_constant__ CUtensorMap mVs,
                       const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mdO,
-                      int T, int C, int W, int mode, float scale, const float* __restrict__ lse,
+                      int T, int C, int W, int mode, float scale, float bias2, const float* __restrict__ lse,
                       BwdWsT ws, int n_sum_items, int items_per_unit, int n_items, int seg, int trace) {
   // debug timeline (EVA_BWD_TRACE=1): CTA 0 records clock64 per role and prints it at exit
   constexpr int TRN = 512;
@@ -266,7 +278,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
 #pragma unroll
         for (int k = 0; k < BQ / 32; ++k) {
           const int n = n0 + lane + 32 * k;
-          lv[k] = n < T ? lse[(size_t)it.u * T + n] * 1.4426950408889634f : 0.f;
+          // summary keys carry the logit bias (R16), folded into the row constant
+          lv[k] = n < T ? lse[(size_t)it.u * T + n] * 1.4426950408889634f - (it.is_sum ? bias2 : 0.f) : 0.f;
           dvv[k] = n < T ? ws.D[(size_t)it.u * T + n] : 0.f;
         }
         if (g >= NSQ) mbar_wait(&sm->q_empty[s], ((g / NSQ) - 1) & 1);
@@ -488,13 +501,19 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       }
       const int u = it.u;
       const int64_t m = (int64_t)it.k0 + r;
-      int64_t vq_lo = 1, vq_hi = 0;  // queries [vq_lo, vq_hi] see this key
+      // queries [vq_lo, vq_hi] minus [xq_lo, xq_hi] see this key; the excluded range is the
+      // block holding a summary's chunk under the non-causal partition
+      int64_t vq_lo = 1, vq_hi = 0, xq_lo = 1, xq_hi = 0;
       if (r < it.nk) {
         if (it.is_sum) {
           vq_lo = qlo_of_summary(m, C, W, mode);
           vq_hi = T - 1;
+          if (mode == EVA_NONCAUSAL) {
+            xq_lo = (m * C / W) * (int64_t)W;
+            xq_hi = xq_lo + W - 1;
+          }
         } else {
-          vq_lo = m;
+          vq_lo = qlo_of_key(m, W, mode);
           vq_hi = min((int64_t)T - 1, qhi_of_key(m, C, W, mode));
         }
       }
@@ -504,8 +523,16 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         mbar_wait(&sm->s_full, g & 1);
         mbar_wait(&sm->q_full[g % NSQ], (g / NSQ) & 1);  // the producer's lse/D stores
         if (tc == 0) TR(2, 6);
-        const int vlo = (int)max((int64_t)0, min((int64_t)BQ, vq_lo - n0));
-        const int vhi = (int)max((int64_t)0, min((int64_t)BQ, vq_hi + 1 - n0));
+        uint32_t vb[BQ / 32];  // visibility of the step's queries, one bit per column
+        {
+          const int vlo = (int)max((int64_t)-1, min((int64_t)BQ, vq_lo - n0));
+          const int vhi = (int)max((int64_t)-1, min((int64_t)BQ, vq_hi + 1 - n0));
+          const int xlo = (int)max((int64_t)-1, min((int64_t)BQ, xq_lo - n0));
+          const int xhi = (int)max((int64_t)-1, min((int64_t)BQ, xq_hi + 1 - n0));
+#pragma unroll
+          for (int h = 0; h < BQ / 32; ++h)
+            vb[h] = range_bits(vlo - 32 * h, vhi - 32 * h) & ~range_bits(xlo - 32 * h, xhi - 32 * h);
+        }
         const float* lse2 = sm->lse2[g % NSQ];
         const float* Dq = sm->Dq[g % NSQ];
         uint8_t* dsrow = reinterpret_cast<uint8_t*>(sm->ds[b]) + r * 128;
@@ -540,7 +567,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int jj = 2 * c + e, j = 8 * c16 + jj;
-                const bool vis = j >= vlo && j < vhi;
+                const bool vis = (vb[j >> 5] >> (j & 31)) & 1u;
                 pp[e] = vis ? ex2f(fmaf(__uint_as_float(sr[j]), sl2, -lv[jj])) : 0.f;
                 gg[e] = pp[e] * (__uint_as_float(dr[j]) - dv[jj]);
               }
@@ -583,8 +610,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
             }
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int jj = 2 * c + e, j = 32 * h + jj;
-              const bool vis = j >= vlo && j < vhi;
+              const int jj = 2 * c + e;
+              const bool vis = (vb[h] >> jj) & 1u;
               p[e] = vis ? ex2f(fmaf(__uint_as_float(sr[jj]), sl2, -(e ? lv2.y : lv2.x))) : 0.f;
               gg[e] = p[e] * (__uint_as_float(dr[jj]) - (e ? dv2.y : dv2.x));
             }
@@ -781,7 +808,8 @@ cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K,
   const int items_per_unit = n_sum_items + n_local_items;
   const int n_items = items_per_unit * BH;
   const int grid = std::max(1, std::min(n_items, num_sms()));
-  kern<<<grid, BWD_TC_THREADS, smem, s>>>(mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale, lse, ws,
+  kern<<<grid, BWD_TC_THREADS, smem, s>>>(mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale,
+                                   cfg.summary_bias * 1.4426950408889634f, lse, ws,
                                           n_sum_items, items_per_unit, n_items, seg, trace ? 1 : 0);
   return cudaGetLastError();
 }

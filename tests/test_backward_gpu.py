@@ -140,3 +140,57 @@ def test_backward_full_size_family(eva, B, H, T, d, C, W):
     _check("dQ", f64(dQ), rq, 2e-2)
     _check("dK", f64(dK), rk, 2e-2)
     _check("dV", f64(dV), rv, 2e-2)
+
+
+# ---- the variants (NEXT row 3): non-causal partition (R15) and the summary-logit bias (R16)
+VARIANT_CASES = [  # (B, H, T, d, C, W), T % C == 0 for the non-causal partition
+    (1, 1, 256, 16, 16, 32),
+    (1, 2, 312, 32, 8, 24),       # W = 3C, last block ragged (312 % 24 = 0, 312 % 64 != 0)
+    (2, 1, 576, 64, 64, 128),     # last block half full
+    (1, 2, 704, 128, 64, 256),
+    (1, 1, 128, 64, 16, 16),      # W = C
+    (1, 1, 96, 64, 1, 3),         # C = 1: exact bidirectional softmax gradients
+    (1, 1, 2200, 128, 8, 16),     # 275 chunks: 3 summary key tiles on the tensor-core pass
+    (1, 1, 40, 64, 8, 64),        # W > T: one block, no summary visible
+]
+
+
+@pytest.mark.parametrize("mode,bias", [("noncausal", 0.0), ("noncausal", "lnC"),
+                                       ("sliding", "lnC"), ("block", -0.5)])
+@pytest.mark.parametrize("case", VARIANT_CASES)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_backward_variant_parity(eva, case, mode, bias, dtype):
+    B, H, T, d, C, W = case
+    b = float(np.log(C)) if bias == "lnC" else bias
+    cfg = eva.make_config(B, H, T, d, C, W, mode=mode, dtype=dtype, seed=17, summary_bias=b)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=21, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, dtype, seed=22, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    dQ, dK, dV = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO)
+    torch.cuda.synchronize()
+    E = oracle.eps_units(cfg.seed, cfg.layer, cfg.bh_begin, cfg.bh_count, T // C, d)
+    m = {"sliding": oracle.SLIDING, "block": oracle.BLOCK, "noncausal": oracle.NONCAUSAL}[mode]
+    rq, rk, rv = oracle.backward_batch(f64(Q), f64(K), f64(V), E, f64(dO), C, W, m, cfg.scale,
+                                       bias=b)
+    tol = TOL[dtype]
+    _check("dQ", f64(dQ), rq, tol)
+    _check("dK", f64(dK), rk, tol)
+    _check("dV", f64(dV), rv, tol)
+
+
+def test_backward_noncausal_large_sampled(eva):
+    """configs[2]-like rows (d = 128, C = 64, W = 256) at T = 4096 under the non-causal
+    partition with bias ln C, tensor-core pass; the oracle runs on 2 units."""
+    B, H, T, d, C, W = 1, 2, 4096, 128, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W, mode="noncausal", seed=5, summary_bias=float(np.log(C)))
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=23, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.bfloat16, seed=24, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    dQ, dK, dV = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO)
+    torch.cuda.synchronize()
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, T // C, d)
+    rq, rk, rv = oracle.backward_batch(f64(Q), f64(K), f64(V), E, f64(dO), C, W, oracle.NONCAUSAL,
+                                       cfg.scale, bias=float(np.log(C)))
+    _check("dQ", f64(dQ), rq, 2e-2)
+    _check("dK", f64(dK), rk, 2e-2)
+    _check("dV", f64(dV), rv, 2e-2)

@@ -170,7 +170,7 @@ def test_host_pipeline_validation(N):
 
 
 def test_noncausal_and_bias_validation(N):
-    """Mode EVA_NONCAUSAL: prefill needs T % C == 0; decode/cache/backward/range refuse it
+    """Mode EVA_NONCAUSAL: prefill and backward need T % C == 0; decode/cache/range refuse it
     (EVA_ERR_UNSUPPORTED); a non-finite summary_bias or a nonzero reserved field is invalid."""
     buf = (ctypes.c_uint8 * 4096)()
     P = ctypes.cast(buf, ctypes.c_void_p)
@@ -187,6 +187,10 @@ def test_noncausal_and_bias_validation(N):
     assert N.lib.eva_cache_append(ctypes.byref(cache), P, P, 1, None, None) == N.EVA_ERR_UNSUPPORTED
     assert N.lib.eva_attn_prefill_range(ctypes.byref(cfg), 0, 0, 0, 0, P, P, P, P, P, 0, P, None, 0,
                                         None) == N.EVA_ERR_UNSUPPORTED
+    # the backward takes the non-causal partition, with the prefill's T % C rule
+    assert N.lib.eva_attn_backward(ctypes.byref(cfg), P, P, P, P, P, P, P, P, None, P, P, P, P, 1 << 30,
+                                   None) == N.EVA_ERR_INVALID_ARG
+    assert b"T % chunk" in N.lib.eva_last_error()
     cfg.mode = N.EVA_WINDOW_SLIDING
     cfg.summary_bias = float("inf")
     assert N.lib.eva_summarize(ctypes.byref(cfg), P, P, None, P, P, None) == N.EVA_ERR_INVALID_ARG

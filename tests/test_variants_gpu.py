@@ -130,8 +130,6 @@ def test_noncausal_refused_by_causal_entry_points(eva):
     S = torch.zeros(1, 4, d, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(eva.EvaError, match="UNSUPPORTED"):
         eva.eva_attn_prefill_range(cfgT, 0, 0, Q, Q, Q, S, S)
-    with pytest.raises(eva.EvaError, match="UNSUPPORTED"):
-        eva.eva_attn_backward(cfgT, Q, Q, Q, S, S, Q, torch.zeros(1, 64, device="cuda"), Q)
     bad = eva.make_config(1, 1, 70, d, 16, 32, mode="noncausal")   # T % C != 0
     Q70 = torch.zeros(1, 70, d, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(eva.EvaError, match="INVALID_ARG"):
