@@ -323,9 +323,10 @@ eva_status eva_attn_prefill_host(eva_pipeline* pipe, const eva_config* cfg, cons
  *              what the forward used.
  * workspace  : device scratch of eva_backward_workspace_bytes(cfg) bytes, 256-byte
  *              aligned; no initialisation needed (fp32 D, dQ, dK, dV accumulators).
- * Three kernels are enqueued on stream (prep, main, finalize); the main pass runs on the
- * tcgen05 tensor cores for bf16 with d in {64, 128} (bf16 operands, fp32 accumulation)
- * and as fp32 SIMT otherwise. */
+ * Kernels enqueued on stream: prep, main, finalize -- or, for bf16 with d in {64, 128}
+ * (tcgen05 tensor cores, bf16 operands, fp32 accumulation), prep, main over the summary
+ * tiles, chain-rule coefficients, main over the local tiles (which applies them and writes
+ * dK/dV), dQ conversion.  The main pass is fp32 SIMT otherwise. */
 size_t eva_backward_workspace_bytes(const eva_config* cfg);
 eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K, const void* V,
                              const void* Ksum, const void* Vsum, const void* O, const float* lse,

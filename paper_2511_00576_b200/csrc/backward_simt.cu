@@ -26,7 +26,9 @@
 //   bwd_finalize  : one CTA per chunk: the summary chain rule above, then dQ, dK, dV
 //                   of the chunk's rows are written in cfg.dtype (tail rows are copied).
 // bf16 with d in {64, 128} replaces bwd_main with the tcgen05 main pass of
-// backward_sm100.cu; the SIMT main pass serves fp32 and the other head dims.
+// backward_sm100.cu (fused schedule: summary items, bwd_finalize_reg<COEF> writing the
+// chain-rule coefficients, local items applying them, bwd_dq_convert); the SIMT main pass
+// serves fp32 and the other head dims.
 #include <algorithm>
 #include <cstdlib>
 
@@ -558,12 +560,15 @@ __global__ void __launch_bounds__(128) bwd_finalize_kernel(eva_config cfg, const
 // chain rule as bwd_finalize_kernel with the chunk's K and V rows loaded once into registers
 // (lane mapping of summarize_chunk_reg: a row is read by TPR = D*2/16 lanes, warp w owns row
 // slots w*RPW + 4*RPW*i) and every reduction done with group shuffles + one smem merge.
-template <typename T, int D, int NI>
+// COEF (the fused path of the tcgen05 main pass): instead of the rows, write the chain-rule
+// coefficients the local items apply -- w_i, da_i per row into cf.w / cf.da, omega and
+// d k~ / C per chunk into cf.om / cf.dkt (BwdFusedArgs); grid = complete chunks only.
+template <typename T, int D, int NI, bool COEF = false>
 __global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, const T* __restrict__ K,
                                                                const T* __restrict__ V,
                                                                const float* __restrict__ eps, BwdWs ws,
                                                                T* __restrict__ dQ, T* __restrict__ dK,
-                                                               T* __restrict__ dV) {
+                                                               T* __restrict__ dV, BwdFusedArgs cf) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int TPR = D / VEC;
   constexpr int RPW = 32 / TPR;
@@ -733,6 +738,21 @@ __global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, c
     sh_dkt[j] = (ws.dKs[srow + j] + sh_g[j] * dom) * (1.0f / (float)C);  // d k~ / C
   }
   __syncthreads();
+  if constexpr (COEF) {
+    if (threadIdx.x < D) {
+      cf.om[srow + threadIdx.x] = sh_om[threadIdx.x];
+      cf.dkt[srow + threadIdx.x] = sh_dkt[threadIdx.x];
+    }
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int r = warp * RPW + 4 * RPW * i + grp;
+      if (r < C && gl == 0) {
+        cf.w[ub + (size_t)c * C + r] = w[i];
+        cf.da[ub + (size_t)c * C + r] = da[i];
+      }
+    }
+    return;
+  }
   // ---- the chunk's rows
   float dkt[VEC];
 #pragma unroll
@@ -766,6 +786,26 @@ __global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, c
   }
 }
 
+// dQ of the fused path: the fp32 accumulator to cfg.dtype, 8 elements per thread.
+template <typename T>
+__global__ void __launch_bounds__(256) bwd_dq_convert_kernel(const float* __restrict__ src, T* __restrict__ dst,
+                                                             size_t n8) {
+  for (size_t i = (size_t)blockIdx.x * 256 + threadIdx.x; i < n8; i += (size_t)gridDim.x * 256) {
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(src) + 2 * i);
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(src) + 2 * i + 1);
+    const float f[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    T o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = Elem<T>::from_f(f[j]);
+    if constexpr (sizeof(T) == 2) {
+      reinterpret_cast<uint4*>(dst)[i] = *reinterpret_cast<const uint4*>(o);
+    } else {
+      reinterpret_cast<uint4*>(dst)[2 * i] = *reinterpret_cast<const uint4*>(o);
+      reinterpret_cast<uint4*>(dst)[2 * i + 1] = *reinterpret_cast<const uint4*>(o + 4);
+    }
+  }
+}
+
 #define BWD_DISPATCH_D(D_, ...)                               \
   switch (D_) {                                               \
     case 16: { constexpr int D = 16; __VA_ARGS__; } break;    \
@@ -782,6 +822,23 @@ __global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, c
 bool backward_force_simt() {
   static const bool v = [] {
     const char* e = getenv("EVA_BACKWARD_SIMT");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+// EVA_BACKWARD_UNFUSED=1 keeps the tcgen05 main pass in one launch with the fp32 dK / dV
+// workspace and the finalize kernel (A/B timing and cross-check knob).
+bool backward_force_unfused() {
+  static const bool v = [] {
+    const char* e = getenv("EVA_BACKWARD_UNFUSED");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+// EVA_BACKWARD_FUSED=1 takes the fused schedule at any size (parity tests of small cases).
+bool backward_force_fused() {
+  static const bool v = [] {
+    const char* e = getenv("EVA_BACKWARD_FUSED");
     return e && atoi(e) != 0;
   }();
   return v;
@@ -811,9 +868,42 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
       bwd_prep_kernel<T, D><<<dim3((Tn + rows_per_cta - 1) / rows_per_cta, cfg.bh_count), 128, 0, s>>>(
           cfg, (const T*)O, (const T*)dO, ws);
     }
-    if ((D == 128 || D == 64) && cfg.dtype == EVA_BF16 && backward_sm100_supported(cfg) && !backward_force_simt()) {
+    const bool tc = (D == 128 || D == 64) && cfg.dtype == EVA_BF16 && backward_sm100_supported(cfg) &&
+                    !backward_force_simt();
+    constexpr int RPW_ = 32 / (D * (int)sizeof(T) / 16 > 32 ? 32 : D * (int)sizeof(T) / 16);
+    const int ni_ = (C + 4 * RPW_ - 1) / (4 * RPW_);
+    // the fused schedule pays two extra launches and a split of the persistent main pass; it
+    // wins once the fp32 round trip it removes is large (measured: configs[2] 3.42 -> 3.33 ms,
+    // configs[1] 0.063 -> 0.070 ms)
+    const bool big = (size_t)cfg.bh_count * (size_t)Tn * D >= ((size_t)1 << 25);
+    if (tc && sizeof(T) == 2 && ni_ <= 8 && (big || backward_force_fused()) && !backward_force_unfused()) {
+      // fused: summary items -> chain-rule coefficients -> local items writing bf16 dK / dV
+      // -> dQ conversion.  The coefficients live in the (then unused) fp32 dK / dV workspace.
+      const size_t BH = (size_t)cfg.bh_count;
+      BwdFusedArgs cf{ws.dK, ws.dK + BH * Tn, ws.dV, ws.dV + BH * (size_t)nC * D, dK, dV};
       err = launch_backward_main_sm100(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws.D, ws.dQ, ws.dK, ws.dV,
-                                       ws.dKs, ws.dVs, s);
+                                       ws.dKs, ws.dVs, nullptr, 1, s);
+      if (err != cudaSuccess) return err;
+      if (nC > 0) {
+        if constexpr (sizeof(T) == 2 && D * sizeof(T) >= 64) {
+          auto fn = ni_ <= 2 ? bwd_finalize_reg_kernel<T, D, 2, true>
+                             : ni_ <= 4 ? bwd_finalize_reg_kernel<T, D, 4, true> : bwd_finalize_reg_kernel<T, D, 8, true>;
+          fn<<<dim3(nC, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, ws, (T*)dQ, (T*)dK,
+                                                    (T*)dV, cf);
+        }
+      }
+      err = launch_backward_main_sm100(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws.D, ws.dQ, ws.dK, ws.dV,
+                                       ws.dKs, ws.dVs, &cf, 2, s);
+      if (err != cudaSuccess) return err;
+      const size_t n8 = BH * (size_t)Tn * D / 8;
+      const int blocks = (int)std::min<size_t>((n8 + 255) / 256, (size_t)num_sms() * 8);
+      bwd_dq_convert_kernel<T><<<std::max(blocks, 1), 256, 0, s>>>(ws.dQ, (T*)dQ, n8);
+      note_launch(3 + (nC > 0 ? 1 : 0) + (plan.n_sum_items > 0 ? 1 : 0));
+      return cudaGetLastError();
+    }
+    if (tc) {
+      err = launch_backward_main_sm100(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws.D, ws.dQ, ws.dK, ws.dV,
+                                       ws.dKs, ws.dVs, nullptr, 0, s);
       if (err != cudaSuccess) return err;
     } else {
       const size_t sm = sizeof(MainSmem<D>);
@@ -831,7 +921,7 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
       auto fn = ni <= 2 ? bwd_finalize_reg_kernel<T, D, 2> : ni <= 4 ? bwd_finalize_reg_kernel<T, D, 4>
                                                                      : bwd_finalize_reg_kernel<T, D, 8>;
       fn<<<dim3(nC + n_tail, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, ws, (T*)dQ,
-                                                         (T*)dK, (T*)dV);
+                                                         (T*)dK, (T*)dV, BwdFusedArgs{});
     } else {
       const size_t fsm = (size_t)(9 * D + 8 + 2 * C) * sizeof(float);
       err = set_smem_attr((const void*)bwd_finalize_kernel<T, D>, fsm);

@@ -1,9 +1,15 @@
 // backward_sm100.cu -- tensor-core (tcgen05/TMEM/TMA) main pass of the FlashEVA prefill
 // backward (the paper trains with it), bf16, d = 128.
 //
-// It replaces bwd_main_kernel of backward_simt.cu for that case and keeps its contract: the
-// prep kernel has written D_n = dO_n . o_n and zeroed the fp32 accumulators, and the finalize
-// kernel applies the summary chain rule (k~ = chunk mean, Eq.15 omega, log-xi softmax).
+// It replaces bwd_main_kernel of backward_simt.cu for that case: the prep kernel has written
+// D_n = dO_n . o_n and zeroed the fp32 accumulators.  Two schedules (launch_backward):
+//   unfused: one launch over every work item, local dK/dV to the fp32 workspace, then the
+//            finalize kernel applies the summary chain rule (k~ = chunk mean, Eq.15 omega,
+//            log-xi softmax) and converts;
+//   fused (default): the summary items, then bwd_coef (the chain-rule coefficients: w_i, da_i
+//            per row, omega_c and d k~_c / C per chunk), then the local items, whose drain
+//            applies the chain rule and stores bf16 dK/dV directly, then the dQ conversion --
+//            no fp32 dK/dV round trip through HBM (4.3 GB less traffic at configs[2]).
 //
 // Work item = one unit x one tile of 128 keys (local keys, or 128 summaries k~_c / beta_c
 // with a segment of the query tiles that see them); the CTA walks its 64-query tiles:
@@ -80,6 +86,18 @@ struct __align__(1024) BwdSm {
 struct BwdWsT {
   float *D, *dQ, *dK, *dV, *dKs, *dVs;
 };
+// Fused summary chain rule for the local items (launch split: summary items, then
+// bwd_coef_kernel, then the local items with this set).  For key row m of complete chunk
+// c = m / C (the finalize's formulas, backward_simt.cu):
+//     dK_m = s dK_local + da_m (omega_c - k_m) + dkt_c,   dV_m = dV_local + w_m dbeta_c
+// with w, da per row and omega, dkt (= d k~ / C) per chunk from bwd_coef_kernel and dbeta_c
+// the summary items' fp32 accumulator; written straight to the bf16 outputs (no fp32 dK / dV
+// round trip).  dK == nullptr: the unfused path (fp32 workspace + finalize).
+struct BwdFused {
+  const float *w, *da, *om, *dkt;
+  const __nv_bfloat16* K;
+  __nv_bfloat16 *dK, *dV;
+};
 
 // Inverse maps of the mask (same formulas as backward_simt.cu): queries [qlo_of_key,
 // qhi_of_key] see local key m; summary c is seen from qlo_of_summary on -- for the
@@ -95,6 +113,12 @@ __host__ __device__ __forceinline__ int64_t qlo_of_summary(int64_t c, int C, int
   if (mode == EVA_NONCAUSAL) return 0;
   if (mode == EVA_WINDOW_SLIDING) return (c + W / C) * (int64_t)C;
   return (c / (W / C) + 1) * (int64_t)W;
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 // Bits [a, b) of a 32-column group (empty when b <= a).
 __device__ __forceinline__ uint32_t range_bits(int a, int b) {
@@ -160,11 +184,11 @@ struct Item {
 // Work item w of the linearised (unit, item) list: items [0, n_sum_items) of a unit are
 // summary tiles of 128 summaries x SEG query tiles, the rest local tiles of 128 keys.
 template <int BQ>
-__device__ __forceinline__ Item decode_item(int w, int items_per_unit, int n_sum_items, int T, int C, int W,
-                                            int mode, int SEG) {
+__device__ __forceinline__ Item decode_item(int w, int items_per_unit, int item_base, int n_sum_items, int T,
+                                            int C, int W, int mode, int SEG) {
   Item it;
   it.u = w / items_per_unit;
-  int item = w % items_per_unit;
+  int item = item_base + w % items_per_unit;
   const int nC = T / C;
   int qt_end;
   if (item < n_sum_items) {
@@ -207,7 +231,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
                       const __grid_constant__ CUtensorMap mKs, const __grid_constant__ CUtensorMap mVs,
                       const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mdO,
                       int T, int C, int W, int mode, float scale, float bias2, const float* __restrict__ lse,
-                      BwdWsT ws, int n_sum_items, int items_per_unit, int n_items, int seg, int trace) {
+                      BwdWsT ws, BwdFused fz, int n_sum_items, int items_per_unit, int item_base, int n_items,
+                      int seg, int trace) {
   // debug timeline (EVA_BWD_TRACE=1): CTA 0 records clock64 per role and prints it at exit
   constexpr int TRN = 512;
   auto TR = [&](int role, int code) {
@@ -259,7 +284,108 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
-  auto item_of = [&](int w) { return decode_item<BQ>(w, items_per_unit, n_sum_items, T, C, W, mode, seg); };
+  auto item_of = [&](int w) {
+    return decode_item<BQ>(w, items_per_unit, item_base, n_sum_items, T, C, W, mode, seg);
+  };
+  // dK, dV of a finished key tile: drain the TMEM accumulators, release them, write out.
+  // Summary tiles reduce into the fp32 dk~ / dbeta accumulators; local tiles either store
+  // fp32 partials (unfused) or apply the summary chain rule and store bf16 (fused).  Called by
+  // 128 threads whose warp quarter `quad` owns TMEM lanes [32 quad, 32 quad + 32).
+  auto drain = [&](const Item& it, int kcount, int quad) {
+    const int r = quad * 32 + lane;
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    const int64_t m = (int64_t)it.k0 + r;
+    // fused path: the row's chain-rule scalars (w_m, da_m), loaded before the accumulators
+    // are ready (the chunk coefficients are read per 8-channel piece below; the producer
+    // pulled them into L2 at item start and the last step into L1)
+    const bool fused = fz.dK != nullptr && !it.is_sum;
+    float wm = 0.f, dam = 0.f;
+    if (fused && r < it.nk && m < (int64_t)nC * C) {
+      wm = __ldg(fz.w + (size_t)it.u * T + m);
+      dam = __ldg(fz.da + (size_t)it.u * T + m);
+    }
+    mbar_wait(&sm->acc_done, kcount & 1);
+    if (r == 0) TR(3, 11);
+    tc_fence_after();
+#pragma unroll 1
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t kv[32], vv[32];
+      tmem_ld32(t_lane + TM_DK + cc * 32, kv);
+      tmem_ld32(t_lane + TM_DV + cc * 32, vv);
+      tmem_wait_ld();
+      if (cc == D / 32 - 1) {
+        tc_fence_before();
+        mbar_arrive(&sm->acc_free);
+      }
+      if (fused) {
+        // dK_m = s dK_local + da_m (omega_c - k_m) + dkt_c,  dV_m = dV_local + w_m dbeta_c
+        const bool ok_row = r < it.nk;
+        const bool inc = ok_row && m < (int64_t)nC * C;  // rows of a complete chunk get its terms
+        const size_t row = (size_t)it.u * T + (ok_row ? m : 0);
+        const size_t crow = ((size_t)it.u * nC + (inc ? m / C : 0)) * D + cc * 32;
+        const uint4* kg = reinterpret_cast<const uint4*>(fz.K + row * D + cc * 32);
+        uint4* okp = reinterpret_cast<uint4*>(fz.dK + row * D + cc * 32);
+        uint4* ovp = reinterpret_cast<uint4*>(fz.dV + row * D + cc * 32);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {  // 8 channels per 16-byte piece
+          const uint4 kr = ok_row ? __ldg(kg + e) : make_uint4(0u, 0u, 0u, 0u);
+          const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&kr);
+          float om[8], dk[8], db[8];
+          if (inc) {
+            *reinterpret_cast<float4*>(&om[0]) = __ldg(reinterpret_cast<const float4*>(fz.om + crow + 8 * e));
+            *reinterpret_cast<float4*>(&om[4]) = __ldg(reinterpret_cast<const float4*>(fz.om + crow + 8 * e + 4));
+            *reinterpret_cast<float4*>(&dk[0]) = __ldg(reinterpret_cast<const float4*>(fz.dkt + crow + 8 * e));
+            *reinterpret_cast<float4*>(&dk[4]) = __ldg(reinterpret_cast<const float4*>(fz.dkt + crow + 8 * e + 4));
+            *reinterpret_cast<float4*>(&db[0]) = __ldg(reinterpret_cast<const float4*>(ws.dVs + crow + 8 * e));
+            *reinterpret_cast<float4*>(&db[4]) = __ldg(reinterpret_cast<const float4*>(ws.dVs + crow + 8 * e + 4));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) om[j] = dk[j] = db[j] = 0.f;
+          }
+          uint32_t pk[4], pv[4];
+#pragma unroll
+          for (int j2 = 0; j2 < 4; ++j2) {
+            const float2 kf = __bfloat1622float2(k2[j2]);
+            const int j = 2 * j2, t = 8 * e + j;
+            const float gk0 = scale * __uint_as_float(kv[t]) + dam * (om[j] - kf.x) + dk[j];
+            const float gk1 = scale * __uint_as_float(kv[t + 1]) + dam * (om[j + 1] - kf.y) + dk[j + 1];
+            pk[j2] = pack2(gk0, gk1);
+            pv[j2] = pack2(__uint_as_float(vv[t]) + wm * db[j], __uint_as_float(vv[t + 1]) + wm * db[j + 1]);
+          }
+          if (ok_row) {
+            okp[e] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            ovp[e] = make_uint4(pv[0], pv[1], pv[2], pv[3]);
+          }
+        }
+      } else if (r < it.nk) {
+        if (it.is_sum) {
+          // summary tiles are split into query segments over several CTAs: vector
+          // reductions (red.global.add.v4.f32) into the fp32 accumulators
+          float4* dks = reinterpret_cast<float4*>(ws.dKs + ((size_t)it.u * nC + m) * D + cc * 32);
+          float4* dvs = reinterpret_cast<float4*>(ws.dVs + ((size_t)it.u * nC + m) * D + cc * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            atomicAdd(dks + e, make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
+                                           scale * __uint_as_float(kv[4 * e + 2]),
+                                           scale * __uint_as_float(kv[4 * e + 3])));
+            atomicAdd(dvs + e, make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
+                                           __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3])));
+          }
+        } else {
+          float4* dkl = reinterpret_cast<float4*>(ws.dK + ((size_t)it.u * T + m) * D + cc * 32);
+          float4* dvl = reinterpret_cast<float4*>(ws.dV + ((size_t)it.u * T + m) * D + cc * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            dkl[e] = make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
+                                 scale * __uint_as_float(kv[4 * e + 2]), scale * __uint_as_float(kv[4 * e + 3]));
+            dvl[e] = make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
+                                 __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3]));
+          }
+        }
+      }
+    }
+  };
+
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -300,6 +426,16 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         mbar_arrive(&sm->q_full[s]);
         ++g;
       };
+      if (fz.dK != nullptr && !it.is_sum && it.k0 < nC * C && elect_one()) {
+        // the fused drain's chunk coefficients (omega, dkt, dbeta of the tile's chunks): back
+        // into L2 while the item runs
+        const int c0 = it.k0 / C, c1 = min(nC - 1, (it.k0 + it.nk - 1) / C);
+        const size_t off = ((size_t)it.u * nC + c0) * D;
+        const uint32_t bytes = (uint32_t)((c1 - c0 + 1) * D * 4);
+        bulk_prefetch_l2(fz.om + off, bytes);
+        bulk_prefetch_l2(fz.dkt + off, bytes);
+        bulk_prefetch_l2(ws.dVs + off, bytes);
+      }
       // V is free once the last item's last dP MMA is done, K only after its last dQ MMA:
       // V first, then the first Q/dO slots, then K
       if (kcount > 0) mbar_wait(&sm->v_free, (kcount - 1) & 1);
@@ -650,6 +786,26 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       const Item it = item_of(w);
       for (int i = 0; i < it.nsteps; ++i, ++g) {
         const int n0 = (it.qt_begin + i) * BQ;
+        if (fz.dK != nullptr && !it.is_sum && i == it.nsteps - 1 && r < it.nk) {
+          // the fused drain reads this thread's key row, its (w, da) and the chunk
+          // coefficients: into L1 one step ahead (they were written a launch ago and are
+          // mostly out of L2 by now)
+          const int64_t m = (int64_t)it.k0 + r;
+          const size_t row = (size_t)it.u * T + m;
+          const char* kr = reinterpret_cast<const char*>(fz.K + row * D);
+#pragma unroll
+          for (int l = 0; l < D * 2 / 128; ++l) prefetch_l1(kr + 128 * l);
+          if (m < (int64_t)nC * C) {
+            if ((r & 31) == 0) {
+              prefetch_l1(fz.w + row);
+              prefetch_l1(fz.da + row);
+            }
+            const size_t crow = ((size_t)it.u * nC + m / C) * D;
+            const int l = r % (3 * D / 32);  // one 128-byte line of omega / dkt / dbeta per thread
+            const float* base = l < D / 32 ? fz.om : l < D / 16 ? fz.dkt : ws.dVs;
+            prefetch_l1(base + crow + 32 * (l % (D / 32)));
+          }
+        }
         mbar_wait(&sm->dq_full, g & 1);
         if (r == 0) TR(3, 8);
         tc_fence_after();
@@ -701,47 +857,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       // ---- dK, dV of this key tile (here, so the softmax warps go straight on to the next
       // item): drain TMEM, release it, then write to global
       if (it.nsteps == 0) continue;
-      const int64_t m = (int64_t)it.k0 + r;
-      mbar_wait(&sm->acc_done, kcount & 1);
-      if (et == 0) TR(3, 11);
-      tc_fence_after();
-#pragma unroll 1
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t kv[32], vv[32];
-        tmem_ld32(t_lane + TM_DK + cc * 32, kv);
-        tmem_ld32(t_lane + TM_DV + cc * 32, vv);
-        tmem_wait_ld();
-        if (cc == D / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&sm->acc_free);
-        }
-        if (r < it.nk) {
-          if (it.is_sum) {
-            // summary tiles are split into query segments over several CTAs: vector
-            // reductions (red.global.add.v4.f32) into the fp32 accumulators
-            float4* dks = reinterpret_cast<float4*>(ws.dKs + ((size_t)it.u * nC + m) * D + cc * 32);
-            float4* dvs = reinterpret_cast<float4*>(ws.dVs + ((size_t)it.u * nC + m) * D + cc * 32);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              atomicAdd(dks + e, make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
-                                             scale * __uint_as_float(kv[4 * e + 2]),
-                                             scale * __uint_as_float(kv[4 * e + 3])));
-              atomicAdd(dvs + e, make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
-                                             __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3])));
-            }
-          } else {
-            float4* dkl = reinterpret_cast<float4*>(ws.dK + ((size_t)it.u * T + m) * D + cc * 32);
-            float4* dvl = reinterpret_cast<float4*>(ws.dV + ((size_t)it.u * T + m) * D + cc * 32);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              dkl[e] = make_float4(scale * __uint_as_float(kv[4 * e]), scale * __uint_as_float(kv[4 * e + 1]),
-                                   scale * __uint_as_float(kv[4 * e + 2]), scale * __uint_as_float(kv[4 * e + 3]));
-              dvl[e] = make_float4(__uint_as_float(vv[4 * e]), __uint_as_float(vv[4 * e + 1]),
-                                   __uint_as_float(vv[4 * e + 2]), __uint_as_float(vv[4 * e + 3]));
-            }
-          }
-        }
-      }
+      drain(it, kcount, quad);
       ++kcount;
     }
     if (et == 0 || !TT::DQT) bulk_wait_read_all();  // smem may be released once read; the
@@ -769,10 +885,11 @@ bool backward_sm100_supported(const eva_config& cfg) {
 }
 
 namespace {
+// phase: 0 every item (unfused), 1 the summary items only, 2 the local items only (fz set)
 template <int D>
 cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K, const void* V,
                             const void* Ksum, const void* Vsum, const void* dO, const float* lse,
-                            const BwdWsT& ws, cudaStream_t s) {
+                            const BwdWsT& ws, const BwdFused& fz, int phase, cudaStream_t s) {
   constexpr int BQ = BwdT<D>::BQ;
   const int BH = cfg.bh_count, T = cfg.T, C = cfg.chunk, W = cfg.window, nC = T / C;
   CUtensorMap mK, mV, mKs, mVs, mQ, mdO;
@@ -805,12 +922,14 @@ cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int items_per_unit = n_sum_items + n_local_items;
+  const int items_per_unit = phase == 1 ? n_sum_items : phase == 2 ? n_local_items : n_sum_items + n_local_items;
+  const int item_base = phase == 2 ? n_sum_items : 0;
   const int n_items = items_per_unit * BH;
+  if (n_items == 0) return cudaSuccess;
   const int grid = std::max(1, std::min(n_items, num_sms()));
   kern<<<grid, BWD_TC_THREADS, smem, s>>>(mK, mV, mKs, mVs, mQ, mdO, T, C, W, cfg.mode, cfg.scale,
-                                   cfg.summary_bias * 1.4426950408889634f, lse, ws,
-                                          n_sum_items, items_per_unit, n_items, seg, trace ? 1 : 0);
+                                          cfg.summary_bias * 1.4426950408889634f, lse, ws, fz, n_sum_items,
+                                          items_per_unit, item_base, n_items, seg, trace ? 1 : 0);
   return cudaGetLastError();
 }
 }  // namespace
@@ -818,10 +937,14 @@ cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K,
 cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
                                        const void* Ksum, const void* Vsum, const void* dO, const float* lse,
                                        float* wsD, float* wsdQ, float* wsdK, float* wsdV, float* wsdKs,
-                                       float* wsdVs, cudaStream_t s) {
+                                       float* wsdVs, const BwdFusedArgs* fused, int phase, cudaStream_t s) {
   const BwdWsT ws{wsD, wsdQ, wsdK, wsdV, wsdKs, wsdVs};
-  if (cfg.d_head == 128) return launch_bwd_main<128>(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws, s);
-  if (cfg.d_head == 64) return launch_bwd_main<64>(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws, s);
+  BwdFused fz{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (fused)
+    fz = BwdFused{fused->w, fused->da, fused->om, fused->dkt, static_cast<const __nv_bfloat16*>(K),
+                  static_cast<__nv_bfloat16*>(fused->dK), static_cast<__nv_bfloat16*>(fused->dV)};
+  if (cfg.d_head == 128) return launch_bwd_main<128>(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws, fz, phase, s);
+  if (cfg.d_head == 64) return launch_bwd_main<64>(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws, fz, phase, s);
   return cudaErrorInvalidValue;
 }
 

@@ -89,12 +89,19 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
                             const void* dO, const float* eps, void* dQ, void* dK, void* dV,
                             void* workspace, cudaStream_t s);
 
-// Tensor-core main pass of the backward (backward_sm100.cu): bf16, d = 128.
+// Tensor-core main pass of the backward (backward_sm100.cu): bf16, d in {64, 128}.
+// phase 0: every work item, local dK/dV to the fp32 workspace (finalize applies the summary
+// chain rule); 1: the summary items only; 2: the local items only, applying the chain rule
+// from the coefficients in *fused and writing dK/dV in bf16.
+struct BwdFusedArgs {
+  float *w, *da, *om, *dkt;  // per row [bh, T]; per chunk [bh, nC, d]
+  void *dK, *dV;                   // bf16 outputs [bh, T, d]
+};
 bool backward_sm100_supported(const eva_config& cfg);
 cudaError_t launch_backward_main_sm100(const eva_config& cfg, const void* Q, const void* K, const void* V,
                                        const void* Ksum, const void* Vsum, const void* dO, const float* lse,
                                        float* wsD, float* wsdQ, float* wsdK, float* wsdV, float* wsdKs,
-                                       float* wsdVs, cudaStream_t s);
+                                       float* wsdVs, const BwdFusedArgs* fused, int phase, cudaStream_t s);
 
 int num_sms();
 // 3-D bf16 TMA map over [units, rows, D] with a {64, box_rows, 1} box and 128-byte swizzle

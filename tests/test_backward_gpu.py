@@ -194,3 +194,49 @@ def test_backward_noncausal_large_sampled(eva):
     _check("dQ", f64(dQ), rq, 2e-2)
     _check("dK", f64(dK), rk, 2e-2)
     _check("dV", f64(dV), rv, 2e-2)
+
+
+@pytest.mark.parametrize("knob", ["EVA_BACKWARD_FUSED", "EVA_BACKWARD_UNFUSED", "EVA_BACKWARD_SIMT"])
+def test_backward_alternate_paths_parity(knob):
+    """Schedules chosen by size or by a knob read once per process run in a child pytest with
+    the knob set: the fused tensor-core schedule (chain rule in the local tiles' drain; the
+    default only from 2^25 elements on) on EVERY bf16 parity and variant case, the one-launch
+    schedule with the fp32 dK/dV workspace + finalize (EVA_BACKWARD_UNFUSED) and the SIMT
+    main pass for bf16 (EVA_BACKWARD_SIMT) on a subset."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, **{knob: "1"})
+    if knob == "EVA_BACKWARD_FUSED":
+        sel = "test_backward_parity and dtype1 or test_backward_variant_parity and dtype1"
+    else:
+        sel = ("test_backward_parity and dtype1 and (case2 or case3 or case9) or "
+               "test_backward_variant_parity and dtype1 and case3")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-k", sel,
+                        "-p", "no:cacheprovider"], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("mode,bias", [("sliding", 0.0), ("noncausal", "lnC")])
+def test_backward_large_default_schedule_sampled(eva, mode, bias):
+    """configs[2]'s B, H, d, C, W at T = 1024 (2^25 elements: the fused schedule by default),
+    oracle on the first and last unit."""
+    B, H, T, d, C, W = 8, 32, 1024, 128, 64, 256
+    b = float(np.log(C)) if bias == "lnC" else bias
+    cfg = eva.make_config(B, H, T, d, C, W, mode=mode, seed=31, summary_bias=b)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=32, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.bfloat16, seed=33, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    dQ, dK, dV = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO)
+    torch.cuda.synchronize()
+    m = oracle.SLIDING if mode == "sliding" else oracle.NONCAUSAL
+    for u in (0, B * H - 1):
+        sl = slice(u, u + 1)
+        E = oracle.eps_units(cfg.seed, cfg.layer, u, 1, T // C, d)
+        rq, rk, rv = oracle.backward_batch(f64(Q[sl]), f64(K[sl]), f64(V[sl]), E, f64(dO[sl]), C, W, m,
+                                           cfg.scale, bias=b)
+        _check("dQ", f64(dQ[sl]), rq, 2e-2)
+        _check("dK", f64(dK[sl]), rk, 2e-2)
+        _check("dV", f64(dV[sl]), rv, 2e-2)
