@@ -427,7 +427,9 @@ def bench_prefill_large(args, eva, torch, dev, s, rank, world, peaks):
 
 def bench_backward(args, eva, torch, dev, s, rank, world, peaks, L):
     """eva_attn_backward (NEXT row 1) at a per-GPU shape (configs[2] or configs[1]): prep +
-    tcgen05 main pass + summary chain-rule finalize.  Algorithmic flops: 10d per visible
+    tcgen05 main pass + summary chain rule (configs[2]: the fused schedule -- summary tiles,
+    coefficients, local tiles applying them, dQ conversion; configs[1]: one main launch +
+    finalize, the size rule in backward_simt.cu).  Algorithmic flops: 10d per visible
     (query, key) pair (S recompute, dP, dV, dK, dQ); algorithmic bytes: Q, K, V, O, dO, lse
     read + dQ, dK, dV written once.  L2 is flushed before every rep (configs[1] fits in it)."""
     import eva_inputs
@@ -456,7 +458,8 @@ def bench_backward(args, eva, torch, dev, s, rank, world, peaks, L):
     flops = prefill_flops(BH, T, d, C, W) * 10 // 4
     nbytes = BH * T * d * 2 * 8 + BH * T * 4
     out = {"workload": f"B={L['B']},H={L['H']},T={T},d={d},C={C},W={W} bf16 per GPU, eva_attn_backward "
-                       "(prep + tcgen05 main + finalize)",
+                       + ("(fused: prep, tcgen05 summary tiles, chain-rule coefficients, tcgen05 local tiles, dQ convert)"
+                          if BH * T * d >= (1 << 25) else "(prep + tcgen05 main + finalize)"),
            "ms": ms, "tokens_per_s_per_gpu": L["B"] * T / (ms / 1e3),
            "roofline": {"bound": "tensor", "achieved": flops / (ms / 1e3) / 1e12, "peak": peaks["bf16"],
                         "unit": "TFLOP/s", "frac": flops / (ms / 1e3) / 1e12 / peaks["bf16"],

@@ -47,8 +47,12 @@ constexpr int BWD_TC_THREADS = 320;
 // M = d = 128); d = 64: 128-query steps, dQ = dS K (M = 128 queries).  TMEM columns:
 // S^T, dP^T (BQ each), dQ, dV, dK.
 template <int D> struct BwdT;
+// NK: K tile buffers -- 2 lets the next work item's K load run under the current item.
+// Measured at configs[2] (fused schedule): d = 128 with NK = 2 has room only for a 2-slot
+// Q/dO ring and is slower (3.42 vs 3.33 ms), so it keeps NSQ = 3, NK = 1; d = 64 takes
+// NK = 2 (neutral at configs[1]).
 template <> struct BwdT<128> {
-  static constexpr int BQ = 64, NSQ = 3, PBUF = 1;
+  static constexpr int BQ = 64, NSQ = 3, PBUF = 1, NK = 1;
   static constexpr bool DQT = true;
   // P^T and dS^T go to shared memory (the dV/dK MMAs read them from there), so S^T/dP^T in
   // TMEM are free as soon as the softmax warps have loaded them: the next step's S/dP MMAs
@@ -59,7 +63,7 @@ template <> struct BwdT<128> {
                                                // the 64-query dQ tile in two halves
 };
 template <> struct BwdT<64> {
-  static constexpr int BQ = 128, NSQ = 2, PBUF = 1;
+  static constexpr int BQ = 128, NSQ = 2, PBUF = 1, NK = 2;
   static constexpr bool DQT = false;
   static constexpr bool PSMEM = false;  // P^T, dS^T back into TMEM (TS MMAs)
   static constexpr uint32_t TM_S = 0, TM_DP = 128, TM_DQ = 256, TM_DV = 320, TM_DK = 384;
@@ -69,7 +73,7 @@ template <> struct BwdT<64> {
 template <int D>
 struct __align__(1024) BwdSm {
   static constexpr int BQ = BwdT<D>::BQ, NSQ = BwdT<D>::NSQ;
-  __nv_bfloat16 k[BK * D];        // D/64 sub-tiles [128 keys][64 ch], 16 KB each
+  __nv_bfloat16 k[BwdT<D>::NK][BK * D];  // D/64 sub-tiles [128 keys][64 ch], 16 KB each
   __nv_bfloat16 v[BK * D];
   __nv_bfloat16 q[NSQ][BQ * D];   // D/64 sub-tiles [BQ queries][64 ch]
   __nv_bfloat16 dO[NSQ][BQ * D];
@@ -78,7 +82,7 @@ struct __align__(1024) BwdSm {
   float dqs[BwdT<D>::DQS_FLOATS]; // dQ staging (fp32) for the bulk reduce-add
   __nv_bfloat16 p[BwdT<D>::PBUF][BwdT<D>::PSMEM ? BK * BQ : 8];  // P^T [128 keys][BQ] (PSMEM)
   float lse2[NSQ][BQ], Dq[NSQ][BQ];  // per Q/dO ring slot, loaded by the producer warp
-  uint64_t k_full, v_full, k_free, v_free, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free,
+  uint64_t k_full[BwdT<D>::NK], v_full, k_free[BwdT<D>::NK], v_free, q_full[NSQ], q_empty[NSQ], s_full, p_full, st_free, dq_full, dq_free,
       ds_free[2], acc_done, acc_free, s_free, p_free[BwdT<D>::PBUF];
   uint32_t tmem_base;
 };
@@ -255,9 +259,11 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mKs); tma_prefetch(&mVs);
     tma_prefetch(&mQ); tma_prefetch(&mdO);
-    mbar_init(&sm->k_full, 1);
+    for (int b = 0; b < TT::NK; ++b) {
+      mbar_init(&sm->k_full[b], 1);
+      mbar_init(&sm->k_free[b], 1);
+    }
     mbar_init(&sm->v_full, 1);
-    mbar_init(&sm->k_free, 1);
     mbar_init(&sm->v_free, 1);
     for (int s = 0; s < NSQ; ++s) {
       mbar_init(&sm->q_full[s], 1 + 32);  // the TMA expect_tx + the producer lanes' lse/D stores
@@ -437,7 +443,22 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         bulk_prefetch_l2(ws.dVs + off, bytes);
       }
       // V is free once the last item's last dP MMA is done, K only after its last dQ MMA:
-      // V first, then the first Q/dO slots, then K
+      // K of this item (slot kcount % NK); with NK = 2 its slot was freed an item ago, so it
+      // goes first and loads under the current item's tail
+      constexpr int NK = TT::NK;
+      const int kslot = kcount % NK;
+      auto issue_k = [&] {
+        if (kcount >= NK) mbar_wait(&sm->k_free[kslot], ((kcount / NK) - 1) & 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&sm->k_full[kslot], BK * D * 2);
+          for (int kb = 0; kb < D / 64; ++kb)
+            tma_load_3d(sm->k[kslot] + kb * BK * 64, mk, &sm->k_full[kslot], kb * 64, it.k0, it.u);
+        }
+        __syncwarp();
+      };
+      if (NK > 1) issue_k();
+      // V (free once the last item's last dP is done), then the first Q/dO slots (then K when
+      // single-buffered: free only after the last item's last dQ)
       if (kcount > 0) mbar_wait(&sm->v_free, (kcount - 1) & 1);
       if (elect_one()) {
         TR(0, 9);
@@ -447,12 +468,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       __syncwarp();
       const int npre = it.nsteps < NSQ ? it.nsteps : NSQ;
       for (int i = 0; i < npre; ++i) issue_q(i);
-      if (kcount > 0) mbar_wait(&sm->k_free, (kcount - 1) & 1);
-      if (elect_one()) {
-        mbar_arrive_expect_tx(&sm->k_full, BK * D * 2);
-        for (int kb = 0; kb < D / 64; ++kb) tma_load_3d(sm->k + kb * BK * 64, mk, &sm->k_full, kb * 64, it.k0, it.u);
-      }
-      __syncwarp();
+      if (NK == 1) issue_k();
       for (int i = npre; i < it.nsteps; ++i) issue_q(i);
       // the NEXT item's K/V into L2 now -- about NSQ steps before this item ends (its loads can
       // only start once this item's last dP / dQ MMAs are done); earlier prefetches are evicted
@@ -478,7 +494,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     // A and B both MN-major, two 64-wide atoms along M 16 KB apart (LBO)
     constexpr uint32_t idesc_q = TT::DQT ? idesc_bf16_f32_ab(D, BQ, true, true)
                                          : idesc_bf16_f32_ab(BQ, D, true, true);
-    const uint32_t k_addr = smem_u32(sm->k), v_addr = smem_u32(sm->v);
+    uint32_t k_addr = smem_u32(sm->k[0]);  // the current item's K slot (set per item)
+    const uint32_t v_addr = smem_u32(sm->v);
     auto issue_dq = [&](int j) {  // dQ(j)^T = K^T dS^T(j), global step j
       if (j > 0) mbar_wait(&sm->dq_free, (j - 1) & 1);  // the epilogue has read dQ(j-1)
       tc_fence_after();
@@ -544,7 +561,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
       for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
         const Item it = item_of(w);
         if (it.nsteps == 0) continue;
-        mbar_wait(&sm->k_full, kcount & 1);
+        k_addr = smem_u32(sm->k[kcount % TT::NK]);
+        mbar_wait(&sm->k_full[kcount % TT::NK], (kcount / TT::NK) & 1);
         mbar_wait(&sm->v_full, kcount & 1);
         if (lane == 0) TR(1, 10);
         for (int i = 0; i < it.nsteps; ++i, ++g) {
@@ -563,7 +581,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         }
         grad_step(g - 1, it.nsteps - 1, kcount, true);
         if (lane == 0) TR(1, 5);
-        if (elect_one()) mma_commit(&sm->k_free);  // K smem free once this dQ completes
+        if (elect_one()) mma_commit(&sm->k_free[kcount % TT::NK]);  // K smem free once this dQ completes
         __syncwarp();
         ++kcount;
       }
@@ -572,7 +590,8 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
     for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
       const Item it = item_of(w);
       if (it.nsteps == 0) continue;
-      mbar_wait(&sm->k_full, kcount & 1);
+      k_addr = smem_u32(sm->k[kcount % TT::NK]);
+      mbar_wait(&sm->k_full[kcount % TT::NK], (kcount / TT::NK) & 1);
       mbar_wait(&sm->v_full, kcount & 1);
       for (int i = 0; i < it.nsteps; ++i, ++g) {
         const int s = g % NSQ;
@@ -617,7 +636,7 @@ bwd_main_sm100_kernel(const __grid_constant__ CUtensorMap mK, const __grid_const
         __syncwarp();
       }
       issue_dq(g - 1);
-      if (elect_one()) mma_commit(&sm->k_free);  // K smem free once this dQ completes
+      if (elect_one()) mma_commit(&sm->k_free[kcount % TT::NK]);  // K smem free once this dQ completes
       __syncwarp();
       ++kcount;
     }
