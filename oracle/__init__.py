@@ -54,6 +54,7 @@ def _L():
         lib.oracle_eps.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, i, i, D]
         lib.oracle_mask.argtypes = [ctypes.c_int64, i, i, i, I64, I64]
         lib.oracle_summarize.argtypes = [i, i, i, D, D, D, d_, d_, i, D, D, D]
+        lib.oracle_summarize_proj.argtypes = [i, i, i, D, D, D, D, d_, d_, i, D, D, D]
         lib.oracle_prefill.argtypes = [i, i, i, i, i, d_, D, D, D, D, D, D, D]
         lib.oracle_summarize_batch.argtypes = [i, i, i, i, D, D, D, d_, d_, i, D, D]
         lib.oracle_prefill_batch.argtypes = [i, i, i, i, i, i, d_, D, D, D, D, D, D, D]
@@ -132,6 +133,21 @@ def summarize(K, V, eps_, C: int, lam: float = 0.1, clip: float = 1.0, omega_mod
     if nC > 0:
         _L().oracle_summarize(T, d, C, _dp(K), _dp(V), _dp(E), lam, clip, omega_mode,
                               _dp(ks), _dp(vs), _dp(om))
+    return (ks, vs, om) if return_omega else (ks, vs)
+
+
+def summarize_proj(K, V, eps_, P, C: int, lam: float = 0.1, clip: float = 1.0, omega_mode: int = 0,
+                   return_omega: bool = False):
+    """Chunk summaries with the learned summary-key projection (oracle_summarize_proj, R17):
+    k~_c = P mean(k), P [d, d]."""
+    K, V, E, P = _f64(K), _f64(V), _f64(eps_), _f64(P)
+    T, d = K.shape
+    assert P.shape == (d, d)
+    nC = T // C
+    ks, vs, om = np.zeros((nC, d)), np.zeros((nC, d)), np.zeros((nC, d))
+    if nC > 0:
+        _L().oracle_summarize_proj(T, d, C, _dp(K), _dp(V), _dp(E), _dp(P), lam, clip, omega_mode,
+                                   _dp(ks), _dp(vs), _dp(om))
     return (ks, vs, om) if return_omega else (ks, vs)
 
 

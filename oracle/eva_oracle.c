@@ -112,22 +112,35 @@ EXPORT void oracle_mask(int64_t n, int C, int W, int mode, int64_t* lo, int64_t*
 /* ------------------------------------------------------------------------ */
 static double clampd(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
-EXPORT void oracle_summarize(int T, int d, int C, const double* K, const double* V,
-                             const double* eps, double lambda, double clipv, int omega_mode,
-                             double* Ksum, double* Vsum, double* omega_out /* may be NULL */) {
+/* P (NEXT row 4, DESIGN R17; may be NULL = identity): the learned summary-key projection,  */
+/* k~_c = P (1/C) sum_i k_{cC+i} with P [d, d] row-major; mu_c = k~_c as in R2.            */
+EXPORT void oracle_summarize_proj(int T, int d, int C, const double* K, const double* V,
+                                  const double* eps, const double* P, double lambda, double clipv,
+                                  int omega_mode, double* Ksum, double* Vsum,
+                                  double* omega_out /* may be NULL */) {
   const int nC = T / C; /* trailing partial chunk is never summarised (R8) */
   double* omega = (double*)malloc(sizeof(double) * d);
   double* a = (double*)malloc(sizeof(double) * C);
+  double* mean = (double*)malloc(sizeof(double) * d);
   for (int c = 0; c < nC; ++c) {
     const double* Kc = K + (size_t)c * C * d;
     const double* Vc = V + (size_t)c * C * d;
     double* kt = Ksum + (size_t)c * d;
     double* bt = Vsum + (size_t)c * d;
-    /* k~_c = (1/C) sum_i k_{cC+i} */
+    /* k~_c = (1/C) sum_i k_{cC+i}  (then P k~_c when projected) */
     for (int j = 0; j < d; ++j) {
       double s = 0.0;
       for (int i = 0; i < C; ++i) s += Kc[(size_t)i * d + j];
-      kt[j] = s / (double)C;
+      mean[j] = s / (double)C;
+    }
+    for (int j = 0; j < d; ++j) {
+      if (!P) {
+        kt[j] = mean[j];
+      } else {
+        double s = 0.0;
+        for (int l = 0; l < d; ++l) s += P[(size_t)j * d + l] * mean[l];
+        kt[j] = s;
+      }
     }
     /* omega_c: Eq.15 with mu_c = k~_c */
     for (int j = 0; j < d; ++j) {
@@ -159,6 +172,13 @@ EXPORT void oracle_summarize(int T, int d, int C, const double* K, const double*
   }
   free(omega);
   free(a);
+  free(mean);
+}
+
+EXPORT void oracle_summarize(int T, int d, int C, const double* K, const double* V,
+                             const double* eps, double lambda, double clipv, int omega_mode,
+                             double* Ksum, double* Vsum, double* omega_out /* may be NULL */) {
+  oracle_summarize_proj(T, d, C, K, V, eps, NULL, lambda, clipv, omega_mode, Ksum, Vsum, omega_out);
 }
 
 /* ------------------------------------------------------------------------ */

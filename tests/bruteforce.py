@@ -54,11 +54,15 @@ def partition_sets(n: int, C: int, W: int, mode: str):
     return [x - 1 for x in E], [[x - 1 for x in ch] for ch in chunks]
 
 
-def summary_direct(Kc, Vc, eps_c, lam=0.1, clip=1.0):
-    """(k~, omega, beta) of one chunk, linear-domain xi ratio."""
+def summary_direct(Kc, Vc, eps_c, lam=0.1, clip=1.0, P=None):
+    """(k~, omega, beta) of one chunk, linear-domain xi ratio.  P: optional learned projection
+    of the summary key, k~ = sum_l P[j, l] mean_l written as an explicit double loop."""
     Kc = np.asarray(Kc, dtype=np.float64)
     Vc = np.asarray(Vc, dtype=np.float64)
     kt = Kc.sum(axis=0) / Kc.shape[0]
+    if P is not None:
+        m = kt
+        kt = np.array([sum(float(P[j][l]) * float(m[l]) for l in range(len(m))) for j in range(len(m))])
     omega = lam * np.clip(kt + np.asarray(eps_c, dtype=np.float64), -clip, clip)
     xi = np.array([math.exp(float(omega @ k) - 0.5 * float(k @ k)) for k in Kc])
     beta = (xi[:, None] * Vc).sum(axis=0) / xi.sum()
