@@ -123,6 +123,17 @@ void eva_config_default(eva_config* cfg, int32_t B, int32_t H, int32_t T, int32_
 eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, const float* eps,
                          void* Ksum, void* Vsum, eva_stream_t stream);
 
+/* eva_summarize_proj: eva_summarize with the learned summary-key projection of SURVEY
+ * §8(f) NEXT row 4 ("new weights"; EVA's summary key is a learned map of the chunk
+ * mean -- reading R17): k~_c = Pk[h] (1/C) sum_i k_{cC+i}, mu_c = k~_c in Eq.15,
+ * beta^_c from Eq.9 with the raw keys.  Pk: device fp32 [H, d, d] row-major (head h of unit
+ * bh_begin + u is (bh_begin + u) % H), 16-byte aligned, caller-owned, read only.  The
+ * outputs feed eva_attn_prefill(EVA_SUMMARIES_PROVIDED) / eva_cache_load like eva_summarize's.
+ * Runs on the register summariser (chunk <= 16 * 4 * 32 / (d * sizeof(dtype) / 16) rows);
+ * longer chunks -> EVA_ERR_UNSUPPORTED.  Pk == NULL -> EVA_ERR_INVALID_ARG. */
+eva_status eva_summarize_proj(const eva_config* cfg, const void* K, const void* V, const float* eps,
+                              const float* Pk, void* Ksum, void* Vsum, eva_stream_t stream);
+
 /* ---------------------------------------------------------------- prefill
  * eva_attn_prefill: chunk-causal FlashEVA attention for all T queries
  * (Eq.12-14, mask P:124, sliding window P:126):

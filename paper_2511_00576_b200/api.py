@@ -96,6 +96,25 @@ def eva_summarize(cfg: EvaConfig, K: torch.Tensor, V: torch.Tensor,
     return Ksum, Vsum
 
 
+def eva_summarize_proj(cfg: EvaConfig, K: torch.Tensor, V: torch.Tensor, Pk: torch.Tensor,
+                       eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
+                       Vsum: Optional[torch.Tensor] = None):
+    """Chunk summaries with the learned summary-key projection k~ = Pk[h] mean(k)
+    (NEXT row 4, reading R17).  Pk: fp32 CUDA [H, d, d] row-major."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    nC = T // cfg.chunk
+    _need(K, "K", (bh, T, d), dt)
+    _need(V, "V", (bh, T, d), dt)
+    _need(Pk, "Pk", (cfg.H, d, d), torch.float32)
+    if eps is not None:
+        _need(eps, "eps", (bh, nC, d), torch.float32)
+    Ksum = torch.empty(bh, nC, d, dtype=dt, device=K.device) if Ksum is None else Ksum
+    Vsum = torch.empty(bh, nC, d, dtype=dt, device=K.device) if Vsum is None else Vsum
+    check(lib.eva_summarize_proj(ctypes.byref(cfg), _ptr(K), _ptr(V), _ptr(eps), _ptr(Pk), _ptr(Ksum),
+                                 _ptr(Vsum), _stream(K.device)))
+    return Ksum, Vsum
+
+
 def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, *,
                      eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
                      Vsum: Optional[torch.Tensor] = None, summaries_provided: bool = False,

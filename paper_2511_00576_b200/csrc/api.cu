@@ -138,6 +138,24 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
                      "eva_summarize");
 }
 
+eva_status eva_summarize_proj(const eva_config* cfg, const void* K, const void* V, const float* eps,
+                              const float* Pk, void* Ksum, void* Vsum, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (!Pk) return fail(EVA_ERR_INVALID_ARG, "Pk is NULL");
+  if (!aligned16(Pk)) return fail(EVA_ERR_INVALID_ARG, "Pk is not 16-byte aligned");
+  if (cfg->bh_count == 0 || cfg->T / cfg->chunk == 0) return ok();
+  const void* p[] = {K, V, Ksum, Vsum};
+  const char* nm[] = {"K", "V", "Ksum", "Vsum"};
+  if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  const cudaError_t e = eva::launch_summarize(*cfg, K, V, eps, Ksum, Vsum, (cudaStream_t)stream, 0, Pk);
+  if (e == cudaErrorNotSupported)
+    return fail(EVA_ERR_UNSUPPORTED, "eva_summarize_proj: chunk=%d too long for the register summariser",
+                cfg->chunk);
+  return cuda_status(e, "eva_summarize_proj");
+}
+
 eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K, const void* V,
                             void* Ksum, void* Vsum, const float* eps, void* O, float* lse,
                             uint32_t flags, eva_stream_t stream) {

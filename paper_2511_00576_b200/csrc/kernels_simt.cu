@@ -63,11 +63,13 @@ __global__ void __launch_bounds__(SUMM_THREADS) summarize_cta_kernel(eva_config 
 // 16-byte loads in flight per lane) and kept in registers: column sums -> k~ (smem merge
 // of the 4 warps), Eq.15 -> omega, per-row log-xi logits (group shuffles), per-warp
 // online softmax of the rows -> partial (m, l, acc), merged across warps in smem.
+// Pk (may be nullptr): the learned summary-key projection of NEXT row 4 (reading R17),
+// k~ = Pk mean(k) with Pk [D, D] row-major fp32 of this unit's head; omega uses mu = k~.
 template <typename T, int D, int NI, typename RowK, typename RowV>
 __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV& rowV, int C,
                                                     const float* eps_c, uint32_t bh_global,
                                                     uint32_t chunk, const eva_config& cfg,
-                                                    T* ksum_out, T* vsum_out) {
+                                                    T* ksum_out, T* vsum_out, const float* Pk = nullptr) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int TPR = D / VEC;
   constexpr int RPW = 32 / TPR;
@@ -108,6 +110,14 @@ __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV
     for (int j = 0; j < VEC; ++j) sh_sum[warp][ch0 + j] = cs[j];
   }
   __syncthreads();
+  __shared__ float sh_mean[D];
+  if (Pk != nullptr) {  // the chunk mean first: every projected channel reads all of it
+    if (threadIdx.x < D) {
+      const int ch = threadIdx.x;
+      sh_mean[ch] = (sh_sum[0][ch] + sh_sum[1][ch] + sh_sum[2][ch] + sh_sum[3][ch]) * (1.0f / (float)C);
+    }
+    __syncthreads();
+  }
   // k~ and omega (Eq.15); one Philox block per 4 channels
   if (threadIdx.x < D / 4) {
     const int q = threadIdx.x;
@@ -123,7 +133,21 @@ __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int ch = 4 * q + j;
-      const float kt = (sh_sum[0][ch] + sh_sum[1][ch] + sh_sum[2][ch] + sh_sum[3][ch]) * (1.0f / (float)C);
+      float kt;
+      if (Pk == nullptr) {
+        kt = (sh_sum[0][ch] + sh_sum[1][ch] + sh_sum[2][ch] + sh_sum[3][ch]) * (1.0f / (float)C);
+      } else {
+        const float4* prow = reinterpret_cast<const float4*>(Pk + (size_t)ch * D);
+        kt = 0.f;
+#pragma unroll 4
+        for (int l4 = 0; l4 < D / 4; ++l4) {
+          const float4 w = __ldg(prow + l4);
+          kt = fmaf(w.x, sh_mean[4 * l4], kt);
+          kt = fmaf(w.y, sh_mean[4 * l4 + 1], kt);
+          kt = fmaf(w.z, sh_mean[4 * l4 + 2], kt);
+          kt = fmaf(w.w, sh_mean[4 * l4 + 3], kt);
+        }
+      }
       sh_om[ch] = omega_of(kt, e[j], cfg);
       ko[j] = Elem<T>::from_f(kt);
     }
@@ -198,7 +222,8 @@ template <typename T, int D, int NI>
 __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, const T* __restrict__ K,
                                                            const T* __restrict__ V,
                                                            const float* __restrict__ eps,
-                                                           T* __restrict__ Ksum, T* __restrict__ Vsum, int c0) {
+                                                           T* __restrict__ Ksum, T* __restrict__ Vsum, int c0,
+                                                           const float* __restrict__ Pk = nullptr) {
   pdl_wait();
   pdl_trigger();
   const int C = cfg.chunk, nC = cfg.T / C;
@@ -208,7 +233,8 @@ __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, cons
   summarize_chunk_reg<T, D, NI>([&](int r) { return Kc + (size_t)r * D; }, [&](int r) { return Vc + (size_t)r * D; },
                                 C, eps ? eps + ((size_t)u * nC + c) * D : nullptr,
                                 (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
-                                Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D);
+                                Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D,
+                                Pk ? Pk + (size_t)((cfg.bh_begin + u) % cfg.H) * D * D : nullptr);
 }
 
 // Summaries broadcast to n_dst destination buffers (context parallelism: every rank's copy
@@ -727,7 +753,7 @@ cudaError_t set_smem_attr(const void* fn, size_t bytes) {
 }
 
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
-                             void* Ksum, void* Vsum, cudaStream_t s, int c0) {
+                             void* Ksum, void* Vsum, cudaStream_t s, int c0, const float* Pk) {
   const int nC = cfg.T / cfg.chunk;
   if (nC == 0 || cfg.bh_count == 0) return cudaSuccess;
   cudaError_t err = cudaSuccess;
@@ -737,14 +763,16 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
     if (ni <= 16) {
       const dim3 grid(nC, cfg.bh_count);
       if (ni <= 2)
-        err = launch_pdl(summarize_reg_kernel<T, D, 2>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
+        err = launch_pdl(summarize_reg_kernel<T, D, 2>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0, Pk);
       else if (ni <= 4)
-        err = launch_pdl(summarize_reg_kernel<T, D, 4>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
+        err = launch_pdl(summarize_reg_kernel<T, D, 4>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0, Pk);
       else if (ni <= 8)
-        err = launch_pdl(summarize_reg_kernel<T, D, 8>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
+        err = launch_pdl(summarize_reg_kernel<T, D, 8>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0, Pk);
       else
-        err = launch_pdl(summarize_reg_kernel<T, D, 16>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
+        err = launch_pdl(summarize_reg_kernel<T, D, 16>, grid, dim3(128), 0, s, cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0, Pk);
       if (err != cudaSuccess) return err;
+    } else if (Pk != nullptr) {
+      return cudaErrorNotSupported;  // the projection lives in the register summariser only
     } else if (sm <= kSummSmemMax) {
       err = set_smem_attr((const void*)summarize_cta_kernel<T, D>, sm);
       if (err != cudaSuccess) return err;

@@ -12,8 +12,10 @@ namespace eva {
 
 // eva_summarize: K, V [bh, T, d] -> Ksum, Vsum [bh, nC, d].  c0: absolute index of the first
 // chunk (row 0 is position c0 * C; keys the random draws).
+// Pk: optional learned summary-key projection [H, d, d] fp32 (register summariser only;
+// cudaErrorNotSupported otherwise).
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
-                             void* Ksum, void* Vsum, cudaStream_t s, int c0 = 0);
+                             void* Ksum, void* Vsum, cudaStream_t s, int c0 = 0, const float* Pk = nullptr);
 
 // Summaries of the chunks of rows [c0*C, ...) stored to row c0 + c of every destination
 // [bh, dst_rows, D] buffer (dst_k/dst_v: device arrays of n_dst base addresses).  Returns

@@ -16,6 +16,9 @@ od = torch.empty(B * H, d, dtype=torch.bfloat16, device="cuda")
 flush = torch.empty(512 << 18, device="cuda")
 s = torch.cuda.current_stream()
 side = torch.cuda.Stream()
+lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+side_lo = torch.cuda.Stream(priority=0)          # 0 = lowest priority in CUDA
+main_hi = torch.cuda.Stream(priority=-1)         # higher priority
 def summ(): eva.eva_summarize(cfg, K, V, Ksum=ks, Vsum=vs)
 def pre(): eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse)
 def hand():
@@ -29,8 +32,28 @@ def full():
         hand()
     pre()
     s.wait_stream(side)
+def full_prefill_first():
+    summ()
+    side.wait_stream(s)
+    pre()
+    with torch.cuda.stream(side):
+        hand()
+    s.wait_stream(side)
+def full_prio():
+    # main work on a high-priority stream, hand-off + decode on a low-priority one
+    s = torch.cuda.current_stream()
+    main_hi.wait_stream(s)
+    with torch.cuda.stream(main_hi):
+        summ()
+        side_lo.wait_stream(main_hi)
+        with torch.cuda.stream(side_lo):
+            hand()
+        pre()
+        main_hi.wait_stream(side_lo)
+    s.wait_stream(main_hi)
 paths = {"summarize": summ, "prefill": pre, "summarize+prefill": lambda: (summ(), pre()),
-         "handoff+decode": hand, "summarize+handoff+decode": lambda: (summ(), hand()), "full step": full}
+         "handoff+decode": hand, "summarize+handoff+decode": lambda: (summ(), hand()), "full step": full,
+         "full, prefill issued first": full_prefill_first, "full, stream priorities": full_prio}
 for name, fn in paths.items():
     for _ in range(3): fn()
     torch.cuda.synchronize()

@@ -169,6 +169,18 @@ def test_host_pipeline_validation(N):
     assert b"pipe" in N.lib.eva_last_error()
 
 
+def test_summarize_proj_validation(N):
+    """eva_summarize_proj: NULL or misaligned Pk is EVA_ERR_INVALID_ARG before anything runs."""
+    buf = (ctypes.c_uint8 * 4096)()
+    P = ctypes.cast(buf, ctypes.c_void_p)
+    cfg = N.EvaConfig()
+    N.lib.eva_config_default(ctypes.byref(cfg), 1, 1, 64, 64, 16, 32)
+    assert N.lib.eva_summarize_proj(ctypes.byref(cfg), P, P, None, None, P, P, None) == N.EVA_ERR_INVALID_ARG
+    assert b"Pk" in N.lib.eva_last_error()
+    mis = ctypes.c_void_p(ctypes.addressof(buf) + 4)
+    assert N.lib.eva_summarize_proj(ctypes.byref(cfg), P, P, None, mis, P, P, None) == N.EVA_ERR_INVALID_ARG
+
+
 def test_noncausal_and_bias_validation(N):
     """Mode EVA_NONCAUSAL: prefill and backward need T % C == 0; decode/cache/range refuse it
     (EVA_ERR_UNSUPPORTED); a non-finite summary_bias or a nonzero reserved field is invalid."""
