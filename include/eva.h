@@ -285,6 +285,25 @@ eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, c
                            const float* eps, void* O, float* lse, void* workspace,
                            size_t workspace_bytes, eva_stream_t stream);
 
+/* eva_decode_step_ragged: one decode token per unit at PER-UNIT positions (SURVEY §8(f) NEXT
+ * row 4: "per-sequence positions in decode" -- a serving batch whose sequences have
+ * different lengths).  pos: device int64 [bh_count], pos[u] = tokens unit u holds
+ * (cache->pos is ignored); for every u the new token (K_new[u], V_new[u], [bh_count, d]) is
+ * appended at position pos[u] (ring slot pos[u] mod W; the chunk it completes, if any, is
+ * summarised with eva_summarize's formulas, eps as in eva_cache_append), then query Q[u] at
+ * position pos[u] attends over its own visible set (a7), O/lse [bh_count, d] / [bh_count],
+ * and pos[u] is advanced by one -- all on the device, so the call is graph-capturable.
+ * Preconditions (not checkable without a sync): 0 <= pos[u] and (pos[u] + 1) / chunk <=
+ * cap_chunks (a chunk past the capacity is not summarised).  workspace: at least
+ * eva_decode_ragged_workspace_bytes(cache) bytes (the split count covers the longest
+ * position the cache can hold), zero-filled before first use; calls leave it zeroed.
+ * The summariser is the register one: chunk <= 16 * 4 * 32 / (d * sizeof(dtype) / 16) rows,
+ * else EVA_ERR_UNSUPPORTED.  Two kernels are enqueued. */
+size_t eva_decode_ragged_workspace_bytes(const eva_cache* cache);
+eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const void* Q, const void* K_new,
+                                  const void* V_new, const float* eps, void* O, float* lse, void* workspace,
+                                  size_t workspace_bytes, eva_stream_t stream);
+
 /* ---------------------------------------------------------------- host-buffer prefill
  * eva_attn_prefill_host: eva_attn_prefill on inputs and outputs in HOST memory, with the
  * host<->device copies overlapped with the kernels (the end-to-end path of a caller whose

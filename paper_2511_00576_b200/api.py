@@ -422,6 +422,33 @@ class DecodeCache:
 
     step = eva_decode_step
 
+    def eva_decode_step_ragged(self, pos: torch.Tensor, q: torch.Tensor, k: torch.Tensor,
+                               v: torch.Tensor, eps: Optional[torch.Tensor] = None,
+                               O: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
+                               want_lse: bool = True):
+        """Per-unit positions: pos int64 CUDA [bh] (advanced in place); append (k, v) at pos[u]
+        and attend q at that position, q, k, v [bh, d].  self.pos is not used."""
+        cfg = self.c.cfg
+        dt, bh, d = _tdtype(cfg), cfg.bh_count, cfg.d_head
+        _need(pos, "pos", (bh,), torch.int64)
+        for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+            _need(t, nm, (bh, d), dt)
+        if eps is not None:
+            _need(eps, "eps", (bh, self.c.cap_chunks, d), torch.float32)
+        O = torch.empty_like(q) if O is None else O
+        if want_lse and lse is None:
+            lse = torch.empty(bh, dtype=torch.float32, device=q.device)
+        nbytes = int(lib.eva_decode_ragged_workspace_bytes(ctypes.byref(self.c)))
+        # its own zero-filled scratch: the split count (and so the merge-counter offset) differs
+        # from the uniform decode's
+        if nbytes and (getattr(self, "_ws_ragged", None) is None or self._ws_ragged.numel() * 4 < nbytes):
+            self._ws_ragged = torch.zeros((nbytes + 3) // 4, dtype=torch.float32, device=q.device)
+        ws = self._ws_ragged if nbytes else None
+        check(lib.eva_decode_step_ragged(ctypes.byref(self.c), _ptr(pos), _ptr(q), _ptr(k), _ptr(v), _ptr(eps),
+                                         _ptr(O), _ptr(lse if want_lse else None), _ptr(ws),
+                                         0 if ws is None else ws.numel() * 4, _stream(q.device)))
+        return O, (lse if want_lse else None)
+
 
 def eva_mask_ranges(cfg: EvaConfig, n_begin: int, count: int, device="cuda"):
     lo = torch.empty(count, dtype=torch.int64, device=device)

@@ -428,6 +428,55 @@ eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, c
   return ok();
 }
 
+// Ragged decode (per-unit positions): the split count is chosen for the longest position the
+// cache can hold, so it is valid for every unit whatever its position.
+static eva_cache ragged_bound(const eva_cache* cache) {
+  eva_cache b = *cache;
+  b.pos = (int64_t)cache->cap_chunks * cache->cfg.chunk + cache->cfg.chunk - 1;
+  if (b.pos < 1) b.pos = 1;
+  return b;
+}
+
+size_t eva_decode_ragged_workspace_bytes(const eva_cache* cache) {
+  if (!cache || cache->cap_chunks < 0) return 0;
+  const eva_cache b = ragged_bound(cache);
+  return eva_decode_workspace_bytes(&b);
+}
+
+eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const void* Q, const void* K_new,
+                                  const void* V_new, const float* eps, void* O, float* lse, void* workspace,
+                                  size_t workspace_bytes, eva_stream_t stream) {
+  if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
+  eva_status st = check_cfg(&cache->cfg, false);
+  if (st != EVA_OK) return st;
+  if ((st = check_causal(&cache->cfg, "the decode cache")) != EVA_OK) return st;
+  if (cache->cap_chunks < 0) return fail(EVA_ERR_INVALID_ARG, "cap_chunks=%d", cache->cap_chunks);
+  if (!eva::ragged_supported(cache->cfg))
+    return fail(EVA_ERR_UNSUPPORTED, "eva_decode_step_ragged: chunk=%d too long for the register summariser",
+                cache->cfg.chunk);
+  if (cache->cfg.bh_count == 0) return ok();
+  if (!pos || (reinterpret_cast<uintptr_t>(pos) & 7u))
+    return fail(EVA_ERR_INVALID_ARG, "pos is NULL or not 8-byte aligned");
+  const void* p[] = {Q, K_new, V_new, O, cache->ring_k, cache->ring_v};
+  const char* nm[] = {"Q", "K_new", "V_new", "O", "ring_k", "ring_v"};
+  if ((st = check_ptrs(6, p, nm)) != EVA_OK) return st;
+  if (cache->cap_chunks > 0) {
+    const void* p2[] = {cache->sum_k, cache->sum_v};
+    const char* nm2[] = {"sum_k", "sum_v"};
+    if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+  }
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  const eva_cache b = ragged_bound(cache);
+  const int S = eva::decode_splits(b);
+  const size_t need = eva_decode_workspace_bytes(&b);
+  if (need > 0 && (!workspace || workspace_bytes < need))
+    return fail(EVA_ERR_INVALID_ARG, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
+  if (workspace && !aligned16(workspace)) return fail(EVA_ERR_INVALID_ARG, "workspace is not 16-byte aligned");
+  return cuda_status(eva::launch_decode_step_ragged(*cache, pos, Q, K_new, V_new, eps, O, lse, (float*)workspace,
+                                                    S, (cudaStream_t)stream),
+                     "eva_decode_step_ragged");
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------------ host-copy pipeline

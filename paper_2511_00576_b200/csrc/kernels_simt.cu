@@ -435,6 +435,52 @@ __global__ void __launch_bounds__(128) append_kernel(eva_cache c, const T* __res
                                c.cfg, sk, sv);
 }
 
+// ============================================================================ ragged step
+// Per-unit positions: unit u holds pos[u] tokens.  One CTA per
+// unit appends its new token at position p = pos[u] (ring slot p mod W -- position p - W,
+// which query p no longer sees), summarises chunk (p+1)/C - 1 when p completes it (rows from
+// the ring, the newest row from Knew: no read-after-write through the read-only path), and
+// advances pos[u].  The decode launch that follows reads each unit's own pos.
+template <typename T, int D, int NI>
+__global__ void __launch_bounds__(128) ragged_append_kernel(eva_cache c, int64_t* __restrict__ pos,
+                                                            const T* __restrict__ Knew,
+                                                            const T* __restrict__ Vnew,
+                                                            const float* __restrict__ eps) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int VEC = 16 / sizeof(T);
+  const int u = blockIdx.x;
+  const int W = c.cfg.window, C = c.cfg.chunk;
+  const int64_t p = pos[u];
+  T* rk = static_cast<T*>(c.ring_k) + (size_t)u * W * D;
+  T* rv = static_cast<T*>(c.ring_v) + (size_t)u * W * D;
+  const T* kn = Knew + (size_t)u * D;
+  const T* vn = Vnew + (size_t)u * D;
+  const size_t slot = (size_t)(p % W);
+  for (int i = threadIdx.x; i < D / VEC; i += blockDim.x) {
+    reinterpret_cast<uint4*>(rk + slot * D)[i] = reinterpret_cast<const uint4*>(kn)[i];
+    reinterpret_cast<uint4*>(rv + slot * D)[i] = reinterpret_cast<const uint4*>(vn)[i];
+  }
+  const int64_t chunk = (p + 1) / C - 1;
+  if ((p + 1) % C == 0 && chunk < c.cap_chunks) {  // uniform over the CTA
+    const int64_t p0 = chunk * C;
+    auto rowK = [&](int i) -> const T* {
+      const int64_t q = p0 + i;
+      return q == p ? kn : rk + (size_t)(q % W) * D;
+    };
+    auto rowV = [&](int i) -> const T* {
+      const int64_t q = p0 + i;
+      return q == p ? vn : rv + (size_t)(q % W) * D;
+    };
+    summarize_chunk_reg<T, D, NI>(rowK, rowV, C, eps ? eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr,
+                                  (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk, c.cfg,
+                                  static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D,
+                                  static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) pos[u] = p + 1;
+}
+
 // ============================================================================ decode
 // grid (bh_count, splits), block 128 (4 warps).  The visible list of query
 // n = pos-1 is the summary prefix [0, nsum) followed by the ring positions
@@ -454,7 +500,8 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
                                                      T* __restrict__ O, float* __restrict__ lse,
                                                      float* __restrict__ ws, int S_,
                                                      const T* __restrict__ Knew = nullptr,
-                                                     const T* __restrict__ Vnew = nullptr) {
+                                                     const T* __restrict__ Vnew = nullptr,
+                                                     const int64_t* __restrict__ pos_dev = nullptr) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int TPR = D / VEC;          // lanes per row
   constexpr int RPW = 32 / TPR;         // rows per warp-wide load
@@ -468,7 +515,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   pdl_trigger();
   const int u = blockIdx.x, S = S_, s = blockIdx.y;
   const int W = c.cfg.window, C = c.cfg.chunk;
-  const int64_t n = c.pos - 1;
+  const int64_t n = (pos_dev ? pos_dev[u] : c.pos) - 1;  // ragged: this unit's own position
   const Range r = mask_range(n, C, W, c.cfg.mode);
   // 32-bit entry indices: E <= nsum + W stays far below 2^31 for any cache that fits HBM
   const int ns = (int)r.nsum;
@@ -890,7 +937,7 @@ cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     dim3 grid(c.cfg.bh_count, splits);
     cudaError_t e = launch_pdl(decode_kernel<T, D, false>, grid, dim3(128), 0, s, c, (const T*)Q, (T*)O, lse, ws,
-                               splits, (const T*)nullptr, (const T*)nullptr);
+                               splits, (const T*)nullptr, (const T*)nullptr, (const int64_t*)nullptr);
     if (e != cudaSuccess) return e;
     note_launch();
   }));
@@ -918,9 +965,37 @@ cudaError_t launch_decode_step(const eva_cache& c_after, const void* Q, const vo
   EVA_DISPATCH_T(c_after.cfg.dtype, EVA_DISPATCH_D(c_after.cfg.d_head, {
     dim3 grid(c_after.cfg.bh_count, splits);
     cudaError_t e = launch_pdl(decode_kernel<T, D, true>, grid, dim3(128), 0, s, c_after, (const T*)Q, (T*)O, lse,
-                               ws, splits, (const T*)Kn, (const T*)Vn);
+                               ws, splits, (const T*)Kn, (const T*)Vn, (const int64_t*)nullptr);
     if (e != cudaSuccess) return e;
     note_launch();
+  }));
+  return cudaGetLastError();
+}
+
+bool ragged_supported(const eva_config& cfg) {
+  bool ok = false;
+  auto probe = [&]() -> cudaError_t {
+    EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, { ok = summ_reg_ni<T, D>(cfg.chunk) <= 16; }));
+    return cudaSuccess;
+  };
+  return probe() == cudaSuccess && ok;
+}
+
+cudaError_t launch_decode_step_ragged(const eva_cache& c, int64_t* pos, const void* Q, const void* Kn,
+                                      const void* Vn, const float* eps, void* O, float* lse, float* ws,
+                                      int splits, cudaStream_t s) {
+  if (c.cfg.bh_count == 0) return cudaSuccess;
+  EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
+    const int ni = summ_reg_ni<T, D>(c.cfg.chunk);
+    auto ak = ni <= 2 ? ragged_append_kernel<T, D, 2>
+                      : ni <= 4 ? ragged_append_kernel<T, D, 4>
+                                : ni <= 8 ? ragged_append_kernel<T, D, 8> : ragged_append_kernel<T, D, 16>;
+    cudaError_t e = launch_pdl(ak, dim3(c.cfg.bh_count), dim3(128), 0, s, c, pos, (const T*)Kn, (const T*)Vn, eps);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(decode_kernel<T, D, false>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c, (const T*)Q,
+                   (T*)O, lse, ws, splits, (const T*)nullptr, (const T*)nullptr, (const int64_t*)pos);
+    if (e != cudaSuccess) return e;
+    note_launch(2);
   }));
   return cudaGetLastError();
 }

@@ -78,6 +78,12 @@ cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse
 // counts the new token.
 cudaError_t launch_decode_step(const eva_cache& c_after, const void* Q, const void* Kn, const void* Vn,
                                void* O, float* lse, float* ws, int splits, cudaStream_t s);
+// Ragged decode step (per-unit positions pos[bh_count], device int64, advanced in place):
+// ragged_append_kernel then the decode kernel reading each unit's own position.
+bool ragged_supported(const eva_config& cfg);  // the register summariser takes cfg.chunk
+cudaError_t launch_decode_step_ragged(const eva_cache& c, int64_t* pos, const void* Q, const void* Kn,
+                                      const void* Vn, const float* eps, void* O, float* lse, float* ws,
+                                      int splits, cudaStream_t s);
 
 cudaError_t launch_mask_ranges(const eva_config& cfg, int64_t n0, int64_t count, int64_t* lo,
                                int64_t* nsum, cudaStream_t s);

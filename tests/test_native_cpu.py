@@ -181,6 +181,28 @@ def test_summarize_proj_validation(N):
     assert N.lib.eva_summarize_proj(ctypes.byref(cfg), P, P, None, mis, P, P, None) == N.EVA_ERR_INVALID_ARG
 
 
+def test_decode_ragged_validation(N):
+    """eva_decode_step_ragged: NULL pos is EVA_ERR_INVALID_ARG, the non-causal partition and a
+    chunk too long for the register summariser are EVA_ERR_UNSUPPORTED; the ragged workspace
+    covers the longest position the cache holds."""
+    buf = (ctypes.c_uint8 * 4096)()
+    P = ctypes.cast(buf, ctypes.c_void_p)
+    cache = N.EvaCache()
+    N.lib.eva_config_default(ctypes.byref(cache.cfg), 1, 4, 0, 64, 16, 32)
+    cache.cap_chunks = 8
+    cache.ring_k = cache.ring_v = cache.sum_k = cache.sum_v = ctypes.addressof(buf)
+    args = (P, P, P, None, P, None, P, 1 << 20, None)
+    assert N.lib.eva_decode_step_ragged(ctypes.byref(cache), None, *args) == N.EVA_ERR_INVALID_ARG
+    assert b"pos" in N.lib.eva_last_error()
+    assert N.lib.eva_decode_ragged_workspace_bytes(ctypes.byref(cache)) >= \
+        N.lib.eva_decode_workspace_bytes(ctypes.byref(cache))
+    cache.cfg.mode = N.EVA_NONCAUSAL
+    assert N.lib.eva_decode_step_ragged(ctypes.byref(cache), P, *args) == N.EVA_ERR_UNSUPPORTED
+    cache.cfg.mode = N.EVA_WINDOW_SLIDING
+    cache.cfg.chunk, cache.cfg.window = 4096, 4096
+    assert N.lib.eva_decode_step_ragged(ctypes.byref(cache), P, *args) == N.EVA_ERR_UNSUPPORTED
+
+
 def test_noncausal_and_bias_validation(N):
     """Mode EVA_NONCAUSAL: prefill and backward need T % C == 0; decode/cache/range refuse it
     (EVA_ERR_UNSUPPORTED); a non-finite summary_bias or a nonzero reserved field is invalid."""

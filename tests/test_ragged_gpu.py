@@ -1,0 +1,105 @@
+"""Ragged decode (per-unit positions) against the fp64 oracle's
+streaming cache (oracle.Cache, pinned in test_oracle*.py): units hold prompts of different
+lengths, then advance one token per call at their own positions."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import eva_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def eva(cuda_device):
+    import paper_2511_00576_b200 as eva
+    return eva
+
+
+def f64(t):
+    return t.detach().float().cpu().double().numpy()
+
+
+def _unit_view(eva, cache, u):
+    """A one-unit eva_cache aliasing unit u's slices of the cache buffers."""
+    from paper_2511_00576_b200 import _native as N
+    cfg = cache.c.cfg
+    v = N.EvaCache()
+    v.cfg = eva.make_config(cfg.B, cfg.H, 0, cfg.d_head, cfg.chunk, cfg.window, mode=cfg.mode,
+                            dtype=torch.bfloat16 if cfg.dtype == N.EVA_BF16 else torch.float32,
+                            seed=cfg.seed, bh_begin=cfg.bh_begin + u, bh_count=1, scale=cfg.scale)
+    v.pos = 0
+    v.cap_chunks = cache.c.cap_chunks
+    v.ring_k, v.ring_v = cache.ring_k[u].data_ptr(), cache.ring_v[u].data_ptr()
+    v.sum_k, v.sum_v = cache.sum_k[u].data_ptr(), cache.sum_v[u].data_ptr()
+    return v
+
+
+@pytest.mark.parametrize("mode", ["sliding", "block"])
+@pytest.mark.parametrize("dtype,d,C,W", [(torch.float32, 32, 8, 24), (torch.bfloat16, 128, 16, 64),
+                                         (torch.bfloat16, 64, 64, 128)])
+def test_ragged_decode_parity(eva, mode, dtype, d, C, W):
+    from paper_2511_00576_b200 import _native as N
+    BH, steps = 4, 70
+    prompt = [0, 5, C * 3 - 1, 2 * W + 7]        # empty, short, about to complete a chunk, long
+    cap = (max(prompt) + steps) // C + 1
+    cfg = eva.make_config(1, BH, 0, d, C, W, mode=mode, dtype=dtype, seed=21)
+    cache = eva.DecodeCache(cfg, cap, device="cuda")
+    m = oracle.SLIDING if mode == "sliding" else oracle.BLOCK
+    orc = [oracle.Cache(d, C, W, m, cap=cap, scale=cfg.scale) for _ in range(BH)]
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, BH, cap + 1, d)
+    T_all = max(prompt) + steps
+    q, k, v = eva_inputs.decode_tokens(0, BH, T_all, d, dtype, seed=22, device="cuda")
+    # ragged prompts through one-unit views of the cache
+    for u, n in enumerate(prompt):
+        if n == 0:
+            continue
+        view = _unit_view(eva, cache, u)
+        kk = k[:n, u].unsqueeze(0).contiguous()
+        vv = v[:n, u].unsqueeze(0).contiguous()
+        N.check(N.lib.eva_cache_append(ctypes.byref(view), kk.data_ptr(), vv.data_ptr(), n, None, None))
+        for t in range(n):
+            assert orc[u].append(f64(k[t, u]), f64(v[t, u]), E[u, t // C]) == 0
+    pos = torch.tensor(prompt, dtype=torch.int64, device="cuda")
+    worst = 0.0
+    for s in range(steps):
+        idx = [prompt[u] + s for u in range(BH)]
+        qs = torch.stack([q[idx[u], u] for u in range(BH)]).contiguous()
+        ks = torch.stack([k[idx[u], u] for u in range(BH)]).contiguous()
+        vs = torch.stack([v[idx[u], u] for u in range(BH)]).contiguous()
+        o, lse = cache.eva_decode_step_ragged(pos, qs, ks, vs)
+        of, lf = f64(o), f64(lse)
+        for u in range(BH):
+            assert orc[u].append(f64(ks[u]), f64(vs[u]), E[u, idx[u] // C]) == 0
+            ro, rl = orc[u].decode(f64(qs[u]))
+            worst = max(worst, np.max(np.abs(of[u] - ro)), abs(lf[u] - rl))
+    assert worst <= TOL[dtype], worst
+    assert pos.tolist() == [p + steps for p in prompt]
+    for u in range(BH):   # every unit's summaries equal the oracle's
+        rks, rvs = orc[u].summaries()
+        n = rks.shape[0]
+        assert np.max(np.abs(f64(cache.sum_k[u, :n]) - rks), initial=0.0) <= TOL[dtype]
+        assert np.max(np.abs(f64(cache.sum_v[u, :n]) - rvs), initial=0.0) <= TOL[dtype]
+
+
+def test_ragged_uniform_equals_decode_step(eva):
+    """With equal positions the ragged step gives the uniform step's outputs."""
+    BH, d, C, W, T0 = 3, 64, 16, 32, 45
+    cfg = eva.make_config(1, BH, 0, d, C, W, seed=3)
+    a = eva.DecodeCache(cfg, 10, device="cuda")
+    b = eva.DecodeCache(cfg, 10, device="cuda")
+    q, k, v = eva_inputs.decode_tokens(0, BH, T0 + 20, d, torch.bfloat16, seed=4, device="cuda")
+    a.eva_cache_append(k[:T0].transpose(0, 1).contiguous(), v[:T0].transpose(0, 1).contiguous())
+    b.eva_cache_append(k[:T0].transpose(0, 1).contiguous(), v[:T0].transpose(0, 1).contiguous())
+    pos = torch.full((BH,), T0, dtype=torch.int64, device="cuda")
+    for t in range(T0, T0 + 20):
+        oa, la = a.eva_decode_step(q[t], k[t], v[t])
+        ob, lb = b.eva_decode_step_ragged(pos, q[t], k[t], v[t])
+        torch.cuda.synchronize()
+        assert torch.allclose(oa.float(), ob.float(), rtol=0, atol=2e-2)
+        assert torch.allclose(la, lb, rtol=0, atol=1e-3)
