@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(128) ragged_append_kernel(eva_cache c, int64_t
 // and Knew/Vnew hold it; entry n = p is read from Knew/Vnew instead of the ring, and the
 // split-0 CTA of each unit writes it to ring slot p mod W (which held position p - W,
 // invisible to query p).  Used for steps that do not complete a chunk.
-template <typename T, int D, bool FUSED = false>
+template <typename T, int D, bool FUSED = false, bool RAGGED = false>
 __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __restrict__ Q,
                                                      T* __restrict__ O, float* __restrict__ lse,
                                                      float* __restrict__ ws, int S_,
@@ -515,7 +515,8 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   pdl_trigger();
   const int u = blockIdx.x, S = S_, s = blockIdx.y;
   const int W = c.cfg.window, C = c.cfg.chunk;
-  const int64_t n = (pos_dev ? pos_dev[u] : c.pos) - 1;  // ragged: this unit's own position
+  // ragged (its own instantiation, so the uniform kernel is unchanged): this unit's position
+  const int64_t n = (RAGGED ? pos_dev[u] : c.pos) - 1;
   const Range r = mask_range(n, C, W, c.cfg.mode);
   // 32-bit entry indices: E <= nsum + W stays far below 2^31 for any cache that fits HBM
   const int ns = (int)r.nsum;
@@ -992,7 +993,7 @@ cudaError_t launch_decode_step_ragged(const eva_cache& c, int64_t* pos, const vo
                                 : ni <= 8 ? ragged_append_kernel<T, D, 8> : ragged_append_kernel<T, D, 16>;
     cudaError_t e = launch_pdl(ak, dim3(c.cfg.bh_count), dim3(128), 0, s, c, pos, (const T*)Kn, (const T*)Vn, eps);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(decode_kernel<T, D, false>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c, (const T*)Q,
+    e = launch_pdl(decode_kernel<T, D, false, true>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c, (const T*)Q,
                    (T*)O, lse, ws, splits, (const T*)nullptr, (const T*)nullptr, (const int64_t*)pos);
     if (e != cudaSuccess) return e;
     note_launch(2);
