@@ -926,7 +926,12 @@ cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K,
   // reductions; short ones keep small problems parallel: the longest seg (<= 32) that still
   // leaves >= 4 work items per SM.
   const int n_local_items = (T + BK - 1) / BK;
-  int seg = 32, n_sum_items = 0;
+  static const int seg_max = [] {  // EVA_BWD_SEG: the longest segment (tuning knob, default 32)
+    const char* e = getenv("EVA_BWD_SEG");
+    const int v = e ? atoi(e) : 32;
+    return v >= 1 && v <= 1024 ? v : 32;
+  }();
+  int seg = seg_max, n_sum_items = 0;
   for (;; seg /= 2) {
     n_sum_items = 0;
     for (int st = 0; st * BK < nC; ++st) n_sum_items += sum_segs<BQ>(st, T, C, W, cfg.mode, seg);
