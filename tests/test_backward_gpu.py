@@ -240,3 +240,23 @@ def test_backward_large_default_schedule_sampled(eva, mode, bias):
         _check("dQ", f64(dQ[sl]), rq, 2e-2)
         _check("dK", f64(dK[sl]), rk, 2e-2)
         _check("dV", f64(dV[sl]), rv, 2e-2)
+
+
+def test_backward_configs2_full_size_sampled(eva):
+    """BASELINE configs[2] per GPU (B=8, H=32, T=8192, d=128, C=64, W=256) -- the launch the
+    bench times (fused schedule) -- with the oracle on the first and last of the 256 units."""
+    B, H, T, d, C, W = 8, 32, 8192, 128, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W, seed=1)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.bfloat16, seed=2, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V)
+    dQ, dK, dV = eva.eva_attn_backward(cfg, Q, K, V, ks, vs, O, lse, dO)
+    torch.cuda.synchronize()
+    for u in (0, B * H - 1):
+        sl = slice(u, u + 1)
+        E = oracle.eps_units(cfg.seed, cfg.layer, u, 1, T // C, d)
+        rq, rk, rv = oracle.backward_batch(f64(Q[sl]), f64(K[sl]), f64(V[sl]), E, f64(dO[sl]), C, W,
+                                           oracle.SLIDING, cfg.scale)
+        _check("dQ", f64(dQ[sl]), rq, 2e-2)
+        _check("dK", f64(dK[sl]), rk, 2e-2)
+        _check("dV", f64(dV[sl]), rv, 2e-2)
