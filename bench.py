@@ -512,10 +512,31 @@ def bench_decode(args, eva, torch, dev, s, rank, world, peaks):
     e2[1].record(s)
     torch.cuda.synchronize()
     two_launch_ms = e2[0].elapsed_time(e2[1]) / steps
+    # the same tokens through eva_decode_step_ragged (per-unit positions, NEXT row 4), with
+    # the units spread over 64 positions 64 tokens apart below the context
+    pos0 = ctx - 64 * (torch.arange(BH, device=dev, dtype=torch.int64) % 64)
+    pos = pos0.clone()
+    cache.eva_decode_step_ragged(pos, toks[0, 0], toks[0, 1], toks[0, 2], O=o, want_lse=False)  # warm
+    pos.copy_(pos0)
+    torch.cuda.synchronize()
+    er = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    er[0].record(s)
+    for i in range(steps):
+        cache.eva_decode_step_ragged(pos, toks[i, 0], toks[i, 1], toks[i, 2], O=o, want_lse=False)
+    er[1].record(s)
+    torch.cuda.synchronize()
+    ragged_ms = er[0].elapsed_time(er[1]) / steps
+    p_host = pos0.cpu().tolist()
+    rbytes = sum(decode_bytes(1, d, p + i, C, W) for i in range(0, steps, max(1, steps // 16))
+                 for p in p_host[:64]) * (BH // 64) / len(range(0, steps, max(1, steps // 16)))
     out = {"workload": f"configs[3]: B=256,H=32,d=128,C=64,W=256, context {ctx}, {steps} generated tokens",
            "tokens_per_s_per_gpu": D["B"] * steps / (total / 1e3), "ms_per_token": total / steps,
            "decode_ms_per_token": dec / steps,
            "two_launch_ms_per_token": two_launch_ms,
+           "ragged_ms_per_token": ragged_ms,
+           "ragged_hbm_frac": rbytes / (ragged_ms / 1e3) / 1e9 / peaks["hbm"],
+           "ragged_note": "eva_decode_step_ragged (ragged_append + decode, 2 launches/token), units at "
+                          "64 positions 64 tokens apart; bytes sampled over 16 steps",
            "roofline": {"kernel": "eva_attn_decode", "bound": "hbm",
                         "achieved": nbytes / (dec / 1e3) / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
                         "frac": nbytes / (dec / 1e3) / 1e9 / peaks["hbm"],
