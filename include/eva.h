@@ -297,8 +297,11 @@ eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, c
  * cap_chunks (a chunk past the capacity is not summarised).  workspace: at least
  * eva_decode_ragged_workspace_bytes(cache) bytes (the split count covers the longest
  * position the cache can hold), zero-filled before first use; calls leave it zeroed.
- * The summariser is the register one: chunk <= 16 * 4 * 32 / (d * sizeof(dtype) / 16) rows,
- * else EVA_ERR_UNSUPPORTED.  Two kernels are enqueued. */
+ * One kernel is enqueued: the split-K decode appends the token (split 0 writes the ring
+ * slot, its first warp summarises a completed chunk) and the unit's merging CTA advances
+ * pos[u].  (EVA_RAGGED_TWO_LAUNCH=1 in the environment selects an append kernel + decode
+ * pair instead; that form needs chunk <= 16 * 4 * 32 / (d * sizeof(dtype) / 16), else
+ * EVA_ERR_UNSUPPORTED.) */
 size_t eva_decode_ragged_workspace_bytes(const eva_cache* cache);
 eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const void* Q, const void* K_new,
                                   const void* V_new, const float* eps, void* O, float* lse, void* workspace,

@@ -451,7 +451,14 @@ eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const vo
   if (st != EVA_OK) return st;
   if ((st = check_causal(&cache->cfg, "the decode cache")) != EVA_OK) return st;
   if (cache->cap_chunks < 0) return fail(EVA_ERR_INVALID_ARG, "cap_chunks=%d", cache->cap_chunks);
-  if (!eva::ragged_supported(cache->cfg))
+  // one launch (the decode kernel appends and summarises with its first warp); the
+  // two-launch form (append kernel with the register summariser, then decode) stays behind
+  // EVA_RAGGED_TWO_LAUNCH=1 for A/B timing
+  static const bool two_launch = [] {
+    const char* e = getenv("EVA_RAGGED_TWO_LAUNCH");
+    return e && atoi(e) != 0;
+  }();
+  if (two_launch && !eva::ragged_supported(cache->cfg))
     return fail(EVA_ERR_UNSUPPORTED, "eva_decode_step_ragged: chunk=%d too long for the register summariser",
                 cache->cfg.chunk);
   if (cache->cfg.bh_count == 0) return ok();
@@ -472,9 +479,12 @@ eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const vo
   if (need > 0 && (!workspace || workspace_bytes < need))
     return fail(EVA_ERR_INVALID_ARG, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
   if (workspace && !aligned16(workspace)) return fail(EVA_ERR_INVALID_ARG, "workspace is not 16-byte aligned");
-  return cuda_status(eva::launch_decode_step_ragged(*cache, pos, Q, K_new, V_new, eps, O, lse, (float*)workspace,
-                                                    S, (cudaStream_t)stream),
-                     "eva_decode_step_ragged");
+  const cudaError_t e =
+      two_launch ? eva::launch_decode_step_ragged(*cache, pos, Q, K_new, V_new, eps, O, lse, (float*)workspace, S,
+                                                  (cudaStream_t)stream)
+                 : eva::launch_decode_step_ragged_fused(*cache, pos, Q, K_new, V_new, eps, O, lse,
+                                                        (float*)workspace, S, (cudaStream_t)stream);
+  return cuda_status(e, "eva_decode_step_ragged");
 }
 
 }  // extern "C"

@@ -501,7 +501,8 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
                                                      float* __restrict__ ws, int S_,
                                                      const T* __restrict__ Knew = nullptr,
                                                      const T* __restrict__ Vnew = nullptr,
-                                                     const int64_t* __restrict__ pos_dev = nullptr) {
+                                                     int64_t* __restrict__ pos_dev = nullptr,
+                                                     const float* __restrict__ ragged_eps = nullptr) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int TPR = D / VEC;          // lanes per row
   constexpr int RPW = 32 / TPR;         // rows per warp-wide load
@@ -515,8 +516,9 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   pdl_trigger();
   const int u = blockIdx.x, S = S_, s = blockIdx.y;
   const int W = c.cfg.window, C = c.cfg.chunk;
-  // ragged (its own instantiation, so the uniform kernel is unchanged): this unit's position
-  const int64_t n = (RAGGED ? pos_dev[u] : c.pos) - 1;
+  // ragged (its own instantiations, so the uniform kernel is unchanged): this unit's
+  // position; the fused ragged step is called before the advance (pos[u] = p = n)
+  const int64_t n = RAGGED ? (FUSED ? pos_dev[u] : pos_dev[u] - 1) : c.pos - 1;
   const Range r = mask_range(n, C, W, c.cfg.mode);
   // 32-bit entry indices: E <= nsum + W stays far below 2^31 for any cache that fits HBM
   const int ns = (int)r.nsum;
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
     // append: split 0 writes the new token to ring slot p mod W (position p - W, never read
     // by this launch); issued after the attention loads so it does not delay them
     if (s == 0 && warp == 1) {
-      const size_t slot = (size_t)((c.pos - 1) % W);
+      const size_t slot = (size_t)(n % W);
       T* wk = static_cast<T*>(c.ring_k) + ((size_t)u * W + slot) * D;
       T* wv = static_cast<T*>(c.ring_v) + ((size_t)u * W + slot) * D;
       for (int i = lane; i < D; i += 32) {
@@ -648,8 +650,35 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
       ws[((size_t)u * S + s) * (D + 2) + 2 + ch] = o;
     }
   }
+  if constexpr (FUSED && RAGGED) {
+    // the chunk this token completes (per unit): warp 0 of split 0 summarises it -- rows
+    // from the ring, the newest from Knew (its ring slot is being written by warp 1 of this
+    // CTA) -- then advances pos[u] once every split has read it (the merging CTA, below)
+    const int64_t chunk = (n + 1) / C - 1;
+    if (s == 0 && (n + 1) % C == 0 && chunk < c.cap_chunks) {
+      const int64_t p0 = chunk * C;
+      const T* rk0 = static_cast<const T*>(c.ring_k) + (size_t)u * W * D;
+      const T* rv0 = static_cast<const T*>(c.ring_v) + (size_t)u * W * D;
+      auto rowK = [&](int i) -> const T* {
+        const int64_t q = p0 + i;
+        return q == n ? Knew + (size_t)u * D : rk0 + (size_t)(q % W) * D;
+      };
+      auto rowV = [&](int i) -> const T* {
+        const int64_t q = p0 + i;
+        return q == n ? Vnew + (size_t)u * D : rv0 + (size_t)(q % W) * D;
+      };
+      summarize_chunk_warp<T, D>(rowK, rowV, C,
+                                 ragged_eps ? ragged_eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr,
+                                 (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk, c.cfg,
+                                 static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D,
+                                 static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D);
+    }
+  }
   if (S == 1) {
     if (lane == 0 && lse) lse[u] = M + logf(L);
+    if constexpr (RAGGED && FUSED) {
+      if (lane == 0) pos_dev[u] = n + 1;
+    }
     return;
   }
   if (lane == 0) {
@@ -686,6 +715,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   if (lane == 0) {
     if (lse) lse[u] = Mg + logf(Lg);
     counters[u] = 0u;
+    if constexpr (RAGGED && FUSED) pos_dev[u] = n + 1;  // every split has read pos[u]
   }
 }
 
@@ -938,7 +968,7 @@ cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     dim3 grid(c.cfg.bh_count, splits);
     cudaError_t e = launch_pdl(decode_kernel<T, D, false>, grid, dim3(128), 0, s, c, (const T*)Q, (T*)O, lse, ws,
-                               splits, (const T*)nullptr, (const T*)nullptr, (const int64_t*)nullptr);
+                               splits, (const T*)nullptr, (const T*)nullptr, (int64_t*)nullptr, (const float*)nullptr);
     if (e != cudaSuccess) return e;
     note_launch();
   }));
@@ -966,7 +996,7 @@ cudaError_t launch_decode_step(const eva_cache& c_after, const void* Q, const vo
   EVA_DISPATCH_T(c_after.cfg.dtype, EVA_DISPATCH_D(c_after.cfg.d_head, {
     dim3 grid(c_after.cfg.bh_count, splits);
     cudaError_t e = launch_pdl(decode_kernel<T, D, true>, grid, dim3(128), 0, s, c_after, (const T*)Q, (T*)O, lse,
-                               ws, splits, (const T*)Kn, (const T*)Vn, (const int64_t*)nullptr);
+                               ws, splits, (const T*)Kn, (const T*)Vn, (int64_t*)nullptr, (const float*)nullptr);
     if (e != cudaSuccess) return e;
     note_launch();
   }));
@@ -994,9 +1024,22 @@ cudaError_t launch_decode_step_ragged(const eva_cache& c, int64_t* pos, const vo
     cudaError_t e = launch_pdl(ak, dim3(c.cfg.bh_count), dim3(128), 0, s, c, pos, (const T*)Kn, (const T*)Vn, eps);
     if (e != cudaSuccess) return e;
     e = launch_pdl(decode_kernel<T, D, false, true>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c, (const T*)Q,
-                   (T*)O, lse, ws, splits, (const T*)nullptr, (const T*)nullptr, (const int64_t*)pos);
+                   (T*)O, lse, ws, splits, (const T*)nullptr, (const T*)nullptr, pos, (const float*)nullptr);
     if (e != cudaSuccess) return e;
     note_launch(2);
+  }));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decode_step_ragged_fused(const eva_cache& c, int64_t* pos, const void* Q, const void* Kn,
+                                            const void* Vn, const float* eps, void* O, float* lse, float* ws,
+                                            int splits, cudaStream_t s) {
+  if (c.cfg.bh_count == 0) return cudaSuccess;
+  EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
+    cudaError_t e = launch_pdl(decode_kernel<T, D, true, true>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c,
+                               (const T*)Q, (T*)O, lse, ws, splits, (const T*)Kn, (const T*)Vn, pos, eps);
+    if (e != cudaSuccess) return e;
+    note_launch();
   }));
   return cudaGetLastError();
 }

@@ -84,6 +84,11 @@ bool ragged_supported(const eva_config& cfg);  // the register summariser takes 
 cudaError_t launch_decode_step_ragged(const eva_cache& c, int64_t* pos, const void* Q, const void* Kn,
                                       const void* Vn, const float* eps, void* O, float* lse, float* ws,
                                       int splits, cudaStream_t s);
+// One launch: the decode kernel appends (ring write, chunk summary by one warp) and advances
+// pos itself.
+cudaError_t launch_decode_step_ragged_fused(const eva_cache& c, int64_t* pos, const void* Q, const void* Kn,
+                                            const void* Vn, const float* eps, void* O, float* lse, float* ws,
+                                            int splits, cudaStream_t s);
 
 cudaError_t launch_mask_ranges(const eva_config& cfg, int64_t n0, int64_t count, int64_t* lo,
                                int64_t* nsum, cudaStream_t s);

@@ -182,9 +182,8 @@ def test_summarize_proj_validation(N):
 
 
 def test_decode_ragged_validation(N):
-    """eva_decode_step_ragged: NULL pos is EVA_ERR_INVALID_ARG, the non-causal partition and a
-    chunk too long for the register summariser are EVA_ERR_UNSUPPORTED; the ragged workspace
-    covers the longest position the cache holds."""
+    """eva_decode_step_ragged: NULL pos is EVA_ERR_INVALID_ARG, the non-causal partition is
+    EVA_ERR_UNSUPPORTED; the ragged workspace covers the longest position the cache holds."""
     buf = (ctypes.c_uint8 * 4096)()
     P = ctypes.cast(buf, ctypes.c_void_p)
     cache = N.EvaCache()
@@ -197,9 +196,6 @@ def test_decode_ragged_validation(N):
     assert N.lib.eva_decode_ragged_workspace_bytes(ctypes.byref(cache)) >= \
         N.lib.eva_decode_workspace_bytes(ctypes.byref(cache))
     cache.cfg.mode = N.EVA_NONCAUSAL
-    assert N.lib.eva_decode_step_ragged(ctypes.byref(cache), P, *args) == N.EVA_ERR_UNSUPPORTED
-    cache.cfg.mode = N.EVA_WINDOW_SLIDING
-    cache.cfg.chunk, cache.cfg.window = 4096, 4096
     assert N.lib.eva_decode_step_ragged(ctypes.byref(cache), P, *args) == N.EVA_ERR_UNSUPPORTED
 
 

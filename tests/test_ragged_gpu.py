@@ -103,3 +103,18 @@ def test_ragged_uniform_equals_decode_step(eva):
         torch.cuda.synchronize()
         assert torch.allclose(oa.float(), ob.float(), rtol=0, atol=2e-2)
         assert torch.allclose(la, lb, rtol=0, atol=1e-3)
+
+
+def test_ragged_two_launch_form_parity():
+    """The append-kernel + decode pair (EVA_RAGGED_TWO_LAUNCH, read once per process) runs the
+    parity cases in a child pytest."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, EVA_RAGGED_TWO_LAUNCH="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-k",
+                        "test_ragged_decode_parity or test_ragged_uniform", "-p", "no:cacheprovider"],
+                       env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
