@@ -55,6 +55,7 @@ def _L():
         lib.oracle_mask.argtypes = [ctypes.c_int64, i, i, i, I64, I64]
         lib.oracle_summarize.argtypes = [i, i, i, D, D, D, d_, d_, i, D, D, D]
         lib.oracle_summarize_proj.argtypes = [i, i, i, D, D, D, D, d_, d_, i, D, D, D]
+        lib.oracle_rope.argtypes = [i, i, d_, ctypes.c_int64, D]
         lib.oracle_prefill.argtypes = [i, i, i, i, i, d_, D, D, D, D, D, D, D]
         lib.oracle_summarize_batch.argtypes = [i, i, i, i, D, D, D, d_, d_, i, D, D]
         lib.oracle_prefill_batch.argtypes = [i, i, i, i, i, i, d_, D, D, D, D, D, D, D]
@@ -134,6 +135,15 @@ def summarize(K, V, eps_, C: int, lam: float = 0.1, clip: float = 1.0, omega_mod
         _L().oracle_summarize(T, d, C, _dp(K), _dp(V), _dp(E), lam, clip, omega_mode,
                               _dp(ks), _dp(vs), _dp(om))
     return (ks, vs, om) if return_omega else (ks, vs)
+
+
+def rope(X, base: float = 10000.0, pos0: int = 0):
+    """Rotary position embedding of rows X [T, d] at positions pos0.. (oracle_rope, R18):
+    consecutive channel pairs rotated by pos * base^(-2j/d).  Returns a new array."""
+    X = _f64(X).copy()
+    T, d = X.shape
+    _L().oracle_rope(T, d, base, pos0, _dp(X))
+    return X
 
 
 def summarize_proj(K, V, eps_, P, C: int, lam: float = 0.1, clip: float = 1.0, omega_mode: int = 0,

@@ -112,6 +112,24 @@ EXPORT void oracle_mask(int64_t n, int C, int W, int mode, int64_t* lo, int64_t*
 /* ------------------------------------------------------------------------ */
 static double clampd(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
+/* RoPE ("RoPE is applied to all tokens prior to the random feature projections";  */
+/* NEXT row 4, DESIGN R18): rotate consecutive channel pairs (2j, 2j+1) of row x at       */
+/* position pos by angle pos * base^(-2j/d):                                               */
+/*   y_2j = x_2j cos a - x_2j+1 sin a,   y_2j+1 = x_2j sin a + x_2j+1 cos a.               */
+/* X [T, d] in place, rows at positions pos0 .. pos0 + T - 1.                              */
+EXPORT void oracle_rope(int T, int d, double base, int64_t pos0, double* X) {
+  for (int t = 0; t < T; ++t) {
+    double* x = X + (size_t)t * d;
+    for (int j = 0; j < d / 2; ++j) {
+      const double a = (double)(pos0 + t) * pow(base, -2.0 * j / (double)d);
+      const double c = cos(a), s = sin(a);
+      const double x0 = x[2 * j], x1 = x[2 * j + 1];
+      x[2 * j] = x0 * c - x1 * s;
+      x[2 * j + 1] = x0 * s + x1 * c;
+    }
+  }
+}
+
 /* P (NEXT row 4, DESIGN R17; may be NULL = identity): the learned summary-key projection,  */
 /* k~_c = P (1/C) sum_i k_{cC+i} with P [d, d] row-major; mu_c = k~_c as in R2.            */
 EXPORT void oracle_summarize_proj(int T, int d, int C, const double* K, const double* V,
