@@ -123,6 +123,19 @@ void eva_config_default(eva_config* cfg, int32_t B, int32_t H, int32_t T, int32_
 eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, const float* eps,
                          void* Ksum, void* Vsum, eva_stream_t stream);
 
+/* eva_rope_summarize: the fused RoPE producer of SURVEY §8(f) NEXT row 4 ("RoPE is
+ * applied to all tokens prior to the random feature projections"; reading R18).
+ * One launch reads the caller's pre-RoPE Q, K (and V) [bh_count, T, d] and writes
+ *   Qr, Kr : RoPE(Q), RoPE(K) [bh_count, T, d] cfg.dtype -- consecutive channel pairs
+ *            (2j, 2j+1) of the row at position n rotated by n * rope_base^(-2j/d);
+ *   Ksum, Vsum : the summaries of the ROTATED keys (eva_summarize's formulas on Kr's values),
+ * so the prefill then runs on (Qr, Kr, V, Ksum, Vsum) with EVA_SUMMARIES_PROVIDED.  Saves the
+ * separate RoPE pass's second read of K.  Register summariser only (chunk <= 16 * 4 * 32 /
+ * (d * sizeof(dtype) / 16)), else EVA_ERR_UNSUPPORTED; rope_base must be finite and > 1. */
+eva_status eva_rope_summarize(const eva_config* cfg, float rope_base, const void* Q, const void* K,
+                              const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
+                              eva_stream_t stream);
+
 /* eva_summarize_proj: eva_summarize with the learned summary-key projection of SURVEY
  * §8(f) NEXT row 4 ("new weights"; EVA's summary key is a learned map of the chunk
  * mean -- reading R17): k~_c = Pk[h] (1/C) sum_i k_{cC+i}, mu_c = k~_c in Eq.15,

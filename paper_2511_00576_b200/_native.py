@@ -52,7 +52,8 @@ EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache
            "eva_debug_trace_prefill", "eva_decode_step", "eva_backward_workspace_bytes",
            "eva_attn_backward", "eva_pipeline_create", "eva_pipeline_destroy", "eva_attn_prefill_host",
            "eva_summarize_range", "eva_attn_prefill_range", "eva_summarize_range_bcast",
-           "eva_summarize_proj", "eva_decode_ragged_workspace_bytes", "eva_decode_step_ragged"]
+           "eva_summarize_proj", "eva_decode_ragged_workspace_bytes", "eva_decode_step_ragged",
+           "eva_rope_summarize"]
 
 
 class EvaError(RuntimeError):
@@ -74,6 +75,7 @@ def _load():
         "eva_config_default": (None, [CFG] + [ctypes.c_int32] * 6),
         "eva_summarize": (st, [CFG, P, P, P, P, P, P]),
         "eva_summarize_proj": (st, [CFG, P, P, P, P, P, P, P]),
+        "eva_rope_summarize": (st, [CFG, ctypes.c_float, P, P, P, P, P, P, P, P, P]),
         "eva_decode_ragged_workspace_bytes": (ctypes.c_size_t, [CACHE]),
         "eva_decode_step_ragged": (st, [CACHE, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "eva_attn_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_uint32, P]),

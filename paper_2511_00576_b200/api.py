@@ -96,6 +96,25 @@ def eva_summarize(cfg: EvaConfig, K: torch.Tensor, V: torch.Tensor,
     return Ksum, Vsum
 
 
+def eva_rope_summarize(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
+                       rope_base: float = 10000.0, eps: Optional[torch.Tensor] = None):
+    """Fused RoPE producer (NEXT row 4, R18): returns (Qr, Kr, Ksum, Vsum) -- the rotated
+    queries/keys and the summaries of the rotated keys, in one launch."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    nC = T // cfg.chunk
+    for t, nm in ((Q, "Q"), (K, "K"), (V, "V")):
+        _need(t, nm, (bh, T, d), dt)
+    if eps is not None:
+        _need(eps, "eps", (bh, nC, d), torch.float32)
+    Qr, Kr = torch.empty_like(Q), torch.empty_like(K)
+    Ksum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=K.device)[:, :nC]
+    Vsum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=K.device)[:, :nC]
+    check(lib.eva_rope_summarize(ctypes.byref(cfg), float(rope_base), _ptr(Q), _ptr(K), _ptr(V), _ptr(eps),
+                                 _ptr(Qr), _ptr(Kr), _ptr(Ksum if nC else None), _ptr(Vsum if nC else None),
+                                 _stream(K.device)))
+    return Qr, Kr, Ksum, Vsum
+
+
 def eva_summarize_proj(cfg: EvaConfig, K: torch.Tensor, V: torch.Tensor, Pk: torch.Tensor,
                        eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
                        Vsum: Optional[torch.Tensor] = None):

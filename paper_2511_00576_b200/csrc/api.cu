@@ -138,6 +138,31 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
                      "eva_summarize");
 }
 
+eva_status eva_rope_summarize(const eva_config* cfg, float rope_base, const void* Q, const void* K,
+                              const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
+                              eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (!(rope_base > 1.f) || !std::isfinite(rope_base))
+    return fail(EVA_ERR_INVALID_ARG, "rope_base=%g must be finite and > 1", (double)rope_base);
+  if (cfg->bh_count == 0 || cfg->T == 0) return ok();
+  const void* p[] = {Q, K, V, Qr, Kr};
+  const char* nm[] = {"Q", "K", "V", "Qr", "Kr"};
+  if ((st = check_ptrs(5, p, nm)) != EVA_OK) return st;
+  if (cfg->T / cfg->chunk > 0) {
+    const void* p2[] = {Ksum, Vsum};
+    const char* nm2[] = {"Ksum", "Vsum"};
+    if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+  }
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  const cudaError_t e = eva::launch_rope_summarize(*cfg, rope_base, Q, K, V, eps, Qr, Kr, Ksum, Vsum,
+                                                   (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported)
+    return fail(EVA_ERR_UNSUPPORTED, "eva_rope_summarize: chunk=%d too long for the register summariser",
+                cfg->chunk);
+  return cuda_status(e, "eva_rope_summarize");
+}
+
 eva_status eva_summarize_proj(const eva_config* cfg, const void* K, const void* V, const float* eps,
                               const float* Pk, void* Ksum, void* Vsum, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);

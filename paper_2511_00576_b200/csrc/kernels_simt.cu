@@ -65,11 +65,17 @@ __global__ void __launch_bounds__(SUMM_THREADS) summarize_cta_kernel(eva_config 
 // online softmax of the rows -> partial (m, l, acc), merged across warps in smem.
 // Pk (may be nullptr): the learned summary-key projection of NEXT row 4 (reading R17),
 // k~ = Pk mean(k) with Pk [D, D] row-major fp32 of this unit's head; omega uses mu = k~.
-template <typename T, int D, int NI, typename RowK, typename RowV>
+struct NoKXform {
+  __device__ __forceinline__ void operator()(int, int, uint4&) const {}
+};
+// KX (optional): applied to every loaded 16-byte key piece (row r, channel ch0) before any
+// use -- the fused RoPE producer rotates (and stores) the keys there.
+template <typename T, int D, int NI, typename RowK, typename RowV, typename KX = NoKXform>
 __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV& rowV, int C,
                                                     const float* eps_c, uint32_t bh_global,
                                                     uint32_t chunk, const eva_config& cfg,
-                                                    T* ksum_out, T* vsum_out, const float* Pk = nullptr) {
+                                                    T* ksum_out, T* vsum_out, const float* Pk = nullptr,
+                                                    const KX& kxf = KX()) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int TPR = D / VEC;
   constexpr int RPW = 32 / TPR;
@@ -84,6 +90,7 @@ __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV
     const int r = warp * RPW + 4 * RPW * i + grp;
     if (r < C) {
       kx[i] = ldg16_stream(rowK(r) + ch0);
+      kxf(r, ch0, kx[i]);
       vx[i] = ldg16_stream(rowV(r) + ch0);
     }
   }
@@ -241,6 +248,70 @@ __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, cons
 // of the global summary list, reached through NVLink peer pointers): the summary of chunk
 // c0 + c is computed once into shared memory and stored to row (c0 + c) of unit u of each
 // destination [units, dst_rows, D] -- the compute and the all-gather in one kernel.
+// ------------------------------------------------------------ RoPE producer (NEXT row 4, R18)
+// Rotate the consecutive channel pairs of a 16-byte piece (channels ch0 .. ch0+VEC) at
+// position pos by pos * base^(-ch/d); the angle is reduced mod 2 pi in double so fp32 keeps
+// its accuracy at long positions.
+template <typename T, int D>
+__device__ __forceinline__ uint4 rope_piece(uint4 x, int64_t pos, int ch0, float log2_base) {
+  constexpr int VEC = 16 / sizeof(T);
+  float v[VEC];
+  unpack16<T>(x, v);
+#pragma unroll
+  for (int j = 0; j < VEC; j += 2) {
+    const double theta = exp2((double)log2_base * (-(double)(ch0 + j) / (double)D));
+    double a = (double)pos * theta;
+    a -= 6.283185307179586 * rint(a * 0.15915494309189535);
+    float sn, cs;
+    sincosf((float)a, &sn, &cs);
+    const float x0 = v[j], x1 = v[j + 1];
+    v[j] = x0 * cs - x1 * sn;
+    v[j + 1] = x0 * sn + x1 * cs;
+  }
+  T o[VEC];
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) o[j] = Elem<T>::from_f(v[j]);
+  return *reinterpret_cast<const uint4*>(o);
+}
+
+// grid (nC + tail, bh_count), 128 threads.  CTA x < nC: chunk x -- its keys are rotated as
+// they are loaded (and stored to Kr), summarised from the rotated values, and its query rows
+// rotated into Qr; CTA x = nC rotates the trailing partial chunk's rows only.
+template <typename T, int D, int NI>
+__global__ void __launch_bounds__(128) rope_summarize_kernel(eva_config cfg, float log2_base,
+                                                            const T* __restrict__ Q, const T* __restrict__ K,
+                                                            const T* __restrict__ V, const float* __restrict__ eps,
+                                                            T* __restrict__ Qr, T* __restrict__ Kr,
+                                                            T* __restrict__ Ksum, T* __restrict__ Vsum) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int PPR = D / VEC;
+  const int C = cfg.chunk, Tn = cfg.T, nC = Tn / C;
+  const int c = blockIdx.x, u = blockIdx.y;
+  const size_t ub = (size_t)u * Tn;
+  const int r0 = c * C, r1 = min(Tn, r0 + C);
+  // the query rows of this chunk (and, for the tail CTA, the key rows too)
+  for (int i = threadIdx.x; i < (r1 - r0) * PPR; i += blockDim.x) {
+    const int r = r0 + i / PPR, ch0 = (i % PPR) * VEC;
+    const size_t off = (ub + r) * D + ch0;
+    *reinterpret_cast<uint4*>(Qr + off) = rope_piece<T, D>(ldg16_stream(Q + off), r, ch0, log2_base);
+    if (c >= nC) *reinterpret_cast<uint4*>(Kr + off) = rope_piece<T, D>(ldg16_stream(K + off), r, ch0, log2_base);
+  }
+  if (c >= nC) return;
+  const T* Kc = K + (ub + (size_t)r0) * D;
+  const T* Vc = V + (ub + (size_t)r0) * D;
+  T* Krc = Kr + (ub + (size_t)r0) * D;
+  auto rot = [&](int r, int ch0, uint4& x) {
+    x = rope_piece<T, D>(x, (int64_t)r0 + r, ch0, log2_base);
+    *reinterpret_cast<uint4*>(Krc + (size_t)r * D + ch0) = x;
+  };
+  summarize_chunk_reg<T, D, NI>([&](int r) { return Kc + (size_t)r * D; }, [&](int r) { return Vc + (size_t)r * D; },
+                                C, eps ? eps + ((size_t)u * nC + c) * D : nullptr, (uint32_t)(cfg.bh_begin + u),
+                                (uint32_t)c, cfg, Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D,
+                                nullptr, rot);
+}
+
 template <typename T, int D, int NI>
 __global__ void __launch_bounds__(128) summarize_bcast_kernel(eva_config cfg, const T* __restrict__ K,
                                                              const T* __restrict__ V,
@@ -860,6 +931,26 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
       summarize_kernel<T, D><<<dim3((nC + 3) / 4, cfg.bh_count), 128, 0, s>>>(
           cfg, (const T*)K, (const T*)V, eps, (T*)Ksum, (T*)Vsum, c0);
     }
+  }));
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rope_summarize(const eva_config& cfg, float base, const void* Q, const void* K, const void* V,
+                                  const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum, cudaStream_t s) {
+  const int nC = cfg.T / cfg.chunk;
+  const int n_cta = nC + (cfg.T % cfg.chunk ? 1 : 0);
+  if (n_cta == 0 || cfg.bh_count == 0) return cudaSuccess;
+  cudaError_t err = cudaSuccess;
+  EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
+    const int ni = summ_reg_ni<T, D>(cfg.chunk);
+    if (ni > 16) return cudaErrorNotSupported;
+    auto k = ni <= 2 ? rope_summarize_kernel<T, D, 2>
+                     : ni <= 4 ? rope_summarize_kernel<T, D, 4>
+                               : ni <= 8 ? rope_summarize_kernel<T, D, 8> : rope_summarize_kernel<T, D, 16>;
+    err = launch_pdl(k, dim3(n_cta, cfg.bh_count), dim3(128), 0, s, cfg, log2f(base), (const T*)Q, (const T*)K,
+                     (const T*)V, eps, (T*)Qr, (T*)Kr, (T*)Ksum, (T*)Vsum);
+    if (err != cudaSuccess) return err;
   }));
   note_launch();
   return cudaGetLastError();

@@ -16,6 +16,10 @@ namespace eva {
 // cudaErrorNotSupported otherwise).
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
                              void* Ksum, void* Vsum, cudaStream_t s, int c0 = 0, const float* Pk = nullptr);
+// Fused RoPE producer (NEXT row 4, R18): Qr, Kr = RoPE(Q, K) and the summaries of the
+// rotated keys in one launch (register summariser only: cudaErrorNotSupported otherwise).
+cudaError_t launch_rope_summarize(const eva_config& cfg, float base, const void* Q, const void* K, const void* V,
+                                  const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum, cudaStream_t s);
 
 // Summaries of the chunks of rows [c0*C, ...) stored to row c0 + c of every destination
 // [bh, dst_rows, D] buffer (dst_k/dst_v: device arrays of n_dst base addresses).  Returns

@@ -28,7 +28,7 @@ def test_norm_preserved():
 def test_relative_position_property():
     rng = np.random.default_rng(2)
     q, k = rng.standard_normal((1, 32)), rng.standard_normal((1, 32))
-    dots = [float(oracle.rope(q, pos0=m) @ oracle.rope(k, pos0=m - 7).T) for m in (7, 50, 1000)]
+    dots = [float((oracle.rope(q, pos0=m) @ oracle.rope(k, pos0=m - 7).T).item()) for m in (7, 50, 1000)]
     np.testing.assert_allclose(dots, dots[0], rtol=0, atol=1e-10)
 
 

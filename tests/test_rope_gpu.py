@@ -1,0 +1,63 @@
+"""GPU parity of eva_rope_summarize (the fused RoPE producer, NEXT row 4 part, DESIGN.md
+R18) against oracle.rope (pinned in test_oracle_rope.py) + oracle.summarize, and of the
+prefill on its outputs against the oracle prefill on the fp64-rotated inputs."""
+import numpy as np
+import pytest
+import torch
+
+import eva_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+
+
+@pytest.fixture(scope="module")
+def eva(cuda_device):
+    import paper_2511_00576_b200 as eva
+    return eva
+
+
+def f64(t):
+    return t.detach().float().cpu().double().numpy()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("B,H,T,d,C,W", [(1, 2, 200, 16, 16, 32), (1, 2, 515, 64, 64, 128),
+                                         (1, 1, 700, 128, 64, 256), (1, 1, 40, 64, 64, 128),
+                                         (2, 1, 1000, 32, 8, 24)])
+def test_rope_summarize_parity(eva, dtype, B, H, T, d, C, W):
+    base = 10000.0
+    cfg = eva.make_config(B, H, T, d, C, W, dtype=dtype, seed=9)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=10, device="cuda")
+    Qr, Kr, ks, vs = eva.eva_rope_summarize(cfg, Q, K, V, rope_base=base)
+    O, lse, _, _ = eva.eva_attn_prefill(cfg, Qr, Kr, V, Ksum=ks, Vsum=vs, summaries_provided=True)
+    torch.cuda.synchronize()
+    nC = T // C
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, nC, d)
+    tol = TOL[dtype]
+    def stored(x):  # R18: the producer stores RoPE(Q), RoPE(K) in cfg.dtype (RNE) and
+        # summarises / attends those stored values -- applied here to the oracle's own output
+        return torch.from_numpy(x).to(dtype).double().numpy()
+
+    for u in range(B * H):
+        rq = oracle.rope(f64(Q[u]), base)
+        rk = oracle.rope(f64(K[u]), base)
+        assert np.max(np.abs(f64(Qr[u]) - rq)) <= tol
+        assert np.max(np.abs(f64(Kr[u]) - rk)) <= tol
+        rq, rk = stored(rq), stored(rk)
+        sk, sv = oracle.summarize(rk, f64(V[u]), E[u], C)
+        if nC:
+            assert np.max(np.abs(f64(ks[u]) - sk)) <= tol
+            assert np.max(np.abs(f64(vs[u]) - sv)) <= tol
+        ro, rl = oracle.prefill(rq, rk, f64(V[u]), sk, sv, C, W, oracle.SLIDING, cfg.scale)
+        assert np.max(np.abs(f64(O[u]) - ro)) <= tol
+        assert np.max(np.abs(f64(lse[u]) - rl)) <= tol
+
+
+def test_rope_summarize_validation(eva):
+    cfg = eva.make_config(1, 1, 64, 64, 16, 32)
+    X = torch.zeros(1, 64, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(eva.EvaError, match="INVALID_ARG"):
+        eva.eva_rope_summarize(cfg, X, X, X, rope_base=0.5)
