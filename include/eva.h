@@ -136,6 +136,14 @@ eva_status eva_rope_summarize(const eva_config* cfg, float rope_base, const void
                               const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
                               eva_stream_t stream);
 
+/* eva_rope: the RoPE of R18 alone, Y = R(pos) X for rows [bh_count, T, d] cfg.dtype at
+ * positions pos0 + t (decode: q, k_new at their position with T = 1), or with inverse != 0
+ * the transposed rotation Y = R(pos)^T X -- the gradient through RoPE: after
+ * eva_attn_backward on (Qr, Kr, V) gives dQr, dKr, the pre-RoPE gradients are
+ * dQ = R^T dQr, dK = R^T dKr.  X == Y (in place) is allowed. */
+eva_status eva_rope(const eva_config* cfg, float rope_base, const void* X, void* Y, int64_t pos0,
+                    int32_t inverse, eva_stream_t stream);
+
 /* eva_summarize_proj: eva_summarize with the learned summary-key projection of SURVEY
  * §8(f) NEXT row 4 ("new weights"; EVA's summary key is a learned map of the chunk
  * mean -- reading R17): k~_c = Pk[h] (1/C) sum_i k_{cC+i}, mu_c = k~_c in Eq.15,

@@ -53,7 +53,7 @@ EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache
            "eva_attn_backward", "eva_pipeline_create", "eva_pipeline_destroy", "eva_attn_prefill_host",
            "eva_summarize_range", "eva_attn_prefill_range", "eva_summarize_range_bcast",
            "eva_summarize_proj", "eva_decode_ragged_workspace_bytes", "eva_decode_step_ragged",
-           "eva_rope_summarize"]
+           "eva_rope_summarize", "eva_rope"]
 
 
 class EvaError(RuntimeError):
@@ -76,6 +76,7 @@ def _load():
         "eva_summarize": (st, [CFG, P, P, P, P, P, P]),
         "eva_summarize_proj": (st, [CFG, P, P, P, P, P, P, P]),
         "eva_rope_summarize": (st, [CFG, ctypes.c_float, P, P, P, P, P, P, P, P, P]),
+        "eva_rope": (st, [CFG, ctypes.c_float, P, P, ctypes.c_int64, ctypes.c_int32, P]),
         "eva_decode_ragged_workspace_bytes": (ctypes.c_size_t, [CACHE]),
         "eva_decode_step_ragged": (st, [CACHE, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "eva_attn_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_uint32, P]),

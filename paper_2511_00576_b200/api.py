@@ -115,6 +115,19 @@ def eva_rope_summarize(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torc
     return Qr, Kr, Ksum, Vsum
 
 
+def eva_rope(cfg: EvaConfig, X: torch.Tensor, rope_base: float = 10000.0, pos0: int = 0,
+             inverse: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """RoPE (R18) of rows X [bh, T, d] at positions pos0.. (inverse: the transposed rotation,
+    i.e. the gradient through RoPE)."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    _need(X, "X", (bh, T, d), dt)
+    out = torch.empty_like(X) if out is None else out
+    _need(out, "out", (bh, T, d), dt)
+    check(lib.eva_rope(ctypes.byref(cfg), float(rope_base), _ptr(X), _ptr(out), int(pos0), int(bool(inverse)),
+                       _stream(X.device)))
+    return out
+
+
 def eva_summarize_proj(cfg: EvaConfig, K: torch.Tensor, V: torch.Tensor, Pk: torch.Tensor,
                        eps: Optional[torch.Tensor] = None, Ksum: Optional[torch.Tensor] = None,
                        Vsum: Optional[torch.Tensor] = None):

@@ -138,6 +138,20 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
                      "eva_summarize");
 }
 
+eva_status eva_rope(const eva_config* cfg, float rope_base, const void* X, void* Y, int64_t pos0,
+                    int32_t inverse, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (!(rope_base > 1.f) || !std::isfinite(rope_base))
+    return fail(EVA_ERR_INVALID_ARG, "rope_base=%g must be finite and > 1", (double)rope_base);
+  if (pos0 < 0) return fail(EVA_ERR_INVALID_ARG, "pos0=%lld", (long long)pos0);
+  if (cfg->bh_count == 0 || cfg->T == 0) return ok();
+  const void* p[] = {X, Y};
+  const char* nm[] = {"X", "Y"};
+  if ((st = check_ptrs(2, p, nm)) != EVA_OK) return st;
+  return cuda_status(eva::launch_rope(*cfg, rope_base, X, Y, pos0, inverse != 0, (cudaStream_t)stream), "eva_rope");
+}
+
 eva_status eva_rope_summarize(const eva_config* cfg, float rope_base, const void* Q, const void* K,
                               const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
                               eva_stream_t stream) {

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, cons
 // position pos by pos * base^(-ch/d); the angle is reduced mod 2 pi in double so fp32 keeps
 // its accuracy at long positions.
 template <typename T, int D>
-__device__ __forceinline__ uint4 rope_piece(uint4 x, int64_t pos, int ch0, float log2_base) {
+__device__ __forceinline__ uint4 rope_piece(uint4 x, int64_t pos, int ch0, float log2_base, float sign = 1.f) {
   constexpr int VEC = 16 / sizeof(T);
   float v[VEC];
   unpack16<T>(x, v);
@@ -264,6 +264,7 @@ __device__ __forceinline__ uint4 rope_piece(uint4 x, int64_t pos, int ch0, float
     a -= 6.283185307179586 * rint(a * 0.15915494309189535);
     float sn, cs;
     sincosf((float)a, &sn, &cs);
+    sn *= sign;  // sign -1: the inverse (transposed) rotation
     const float x0 = v[j], x1 = v[j + 1];
     v[j] = x0 * cs - x1 * sn;
     v[j + 1] = x0 * sn + x1 * cs;
@@ -272,6 +273,21 @@ __device__ __forceinline__ uint4 rope_piece(uint4 x, int64_t pos, int ch0, float
 #pragma unroll
   for (int j = 0; j < VEC; ++j) o[j] = Elem<T>::from_f(v[j]);
   return *reinterpret_cast<const uint4*>(o);
+}
+
+// Plain RoPE (or its inverse = transpose, for the gradient dX = R^T dXr) of rows [bh, T, D]
+// at positions pos0 + t; one 16-byte piece per thread.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ X, T* __restrict__ Y, int64_t rows,
+                                                   int T_, int64_t pos0, float log2_base, float sign) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int PPR = D / VEC;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * PPR) return;
+  const int64_t row = i / PPR;
+  const int ch0 = (int)(i % PPR) * VEC;
+  const int64_t pos = pos0 + row % T_;
+  reinterpret_cast<uint4*>(Y)[i] = rope_piece<T, D>(ldg16_stream(X + row * D + ch0), pos, ch0, log2_base, sign);
 }
 
 // grid (nC + tail, bh_count), 128 threads.  CTA x < nC: chunk x -- its keys are rotated as
@@ -951,6 +967,20 @@ cudaError_t launch_rope_summarize(const eva_config& cfg, float base, const void*
     err = launch_pdl(k, dim3(n_cta, cfg.bh_count), dim3(128), 0, s, cfg, log2f(base), (const T*)Q, (const T*)K,
                      (const T*)V, eps, (T*)Qr, (T*)Kr, (T*)Ksum, (T*)Vsum);
     if (err != cudaSuccess) return err;
+  }));
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rope(const eva_config& cfg, float base, const void* X, void* Y, int64_t pos0, bool inverse,
+                        cudaStream_t s) {
+  const int64_t rows = (int64_t)cfg.bh_count * cfg.T;
+  if (rows == 0) return cudaSuccess;
+  EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
+    constexpr int PPR = D * (int)sizeof(T) / 16;
+    const int64_t n = rows * PPR;
+    rope_kernel<T, D><<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const T*)X, (T*)Y, rows, cfg.T, pos0,
+                                                                  log2f(base), inverse ? -1.f : 1.f);
   }));
   note_launch();
   return cudaGetLastError();

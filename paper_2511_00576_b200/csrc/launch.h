@@ -16,6 +16,9 @@ namespace eva {
 // cudaErrorNotSupported otherwise).
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
                              void* Ksum, void* Vsum, cudaStream_t s, int c0 = 0, const float* Pk = nullptr);
+// RoPE (or its inverse) of [bh_count, T, d] rows at positions pos0 + t (R18).
+cudaError_t launch_rope(const eva_config& cfg, float base, const void* X, void* Y, int64_t pos0, bool inverse,
+                        cudaStream_t s);
 // Fused RoPE producer (NEXT row 4, R18): Qr, Kr = RoPE(Q, K) and the summaries of the
 // rotated keys in one launch (register summariser only: cudaErrorNotSupported otherwise).
 cudaError_t launch_rope_summarize(const eva_config& cfg, float base, const void* Q, const void* K, const void* V,

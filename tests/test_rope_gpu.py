@@ -61,3 +61,31 @@ def test_rope_summarize_validation(eva):
     X = torch.zeros(1, 64, 64, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(eva.EvaError, match="INVALID_ARG"):
         eva.eva_rope_summarize(cfg, X, X, X, rope_base=0.5)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("d,T,pos0", [(16, 50, 0), (64, 300, 0), (128, 1, 4097)])
+def test_rope_and_inverse(eva, dtype, d, T, pos0):
+    """eva_rope vs oracle.rope; the inverse is the transpose: rows against oracle.rope at the
+    negated position (R(-a) = R(a)^T per pair), and inverse(rope(X)) = X."""
+    cfg = eva.make_config(1, 2, T, d, 1, 1, dtype=dtype)
+    (X,) = eva_inputs.normal_units(1, 0, 2, T, d, dtype, seed=31, device="cuda")
+    Y = eva.eva_rope(cfg, X, pos0=pos0)
+    Z = eva.eva_rope(cfg, X, pos0=pos0, inverse=True)
+    back = eva.eva_rope(cfg, Y, pos0=pos0, inverse=True)
+    torch.cuda.synchronize()
+    tol = TOL[dtype]
+    for u in range(2):
+        assert np.max(np.abs(f64(Y[u]) - oracle.rope(f64(X[u]), pos0=pos0))) <= tol
+        want_inv = np.concatenate([oracle.rope(f64(X[u, t:t + 1]), pos0=-(pos0 + t)) for t in range(T)])
+        assert np.max(np.abs(f64(Z[u]) - want_inv)) <= tol
+    assert np.max(np.abs(f64(back) - f64(X))) <= 2 * tol
+
+
+def test_rope_in_place(eva):
+    cfg = eva.make_config(1, 1, 64, 64, 1, 1)
+    (X,) = eva_inputs.normal_units(1, 0, 1, 64, 64, torch.bfloat16, seed=32, device="cuda")
+    want = eva.eva_rope(cfg, X, pos0=5)
+    eva.eva_rope(cfg, X, pos0=5, out=X)
+    torch.cuda.synchronize()
+    assert torch.equal(X, want)
