@@ -9,9 +9,10 @@ The arithmetic lives in ``oracle/eva_oracle.c`` (plain C, fp64, one
 marshals numpy arrays.  Citations (P:NN = PAPER.md line, S:NN = SPEC.md line)
 are in the C file and in DESIGN.md.
 
-Parity pins: tests/test_oracle.py.  Every public function here is pinned
+Parity pins: tests/test_oracle*.py.  Every public function here is pinned
 (Philox KAT, closed forms, worked examples, exact-softmax special cases,
-brute-force Eq.9/10 direct form, streaming == prefill).
+brute-force Eq.9/10 direct form, streaming == prefill, finite differences and
+autograd for the backward, the projection and RoPE identities).
 """
 from __future__ import annotations
 

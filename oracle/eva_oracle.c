@@ -25,7 +25,14 @@
  * subtracted (log-domain), which is the same value in exact arithmetic; at
  * d = 128 the linear-domain xi underflows (R12).
  *
- * Parity pins live in tests/test_oracle.py; every function below is pinned.
+ * Beyond §8(a) (the NEXT rows of SURVEY §8(f)): the backward
+ * (oracle_backward_ext, R14), the non-causal partition and summary bias (R15, R16),
+ * the learned summary-key projection (oracle_summarize_proj, R17) and RoPE
+ * (oracle_rope, R18) -- each written out step by step from its definition.
+ *
+ * Parity pins live in tests/test_oracle*.py; every function below is pinned
+ * (test_oracle.py, test_oracle_backward.py, test_oracle_variants.py,
+ * test_oracle_proj.py, test_oracle_rope.py).
  */
 #include <math.h>
 #include <stdint.h>
