@@ -89,3 +89,30 @@ def test_rope_in_place(eva):
     eva.eva_rope(cfg, X, pos0=5, out=X)
     torch.cuda.synchronize()
     assert torch.equal(X, want)
+
+
+def test_training_chain_with_rope(eva):
+    """Forward through the fused RoPE producer, eva_attn_backward on the rotated inputs, then
+    the transposed rotation: dQ, dK, dV of L = sum(dO * O(rope(Q), rope(K), V)) against the
+    oracle's backward on its own rotated (stored-precision) inputs followed by R^T per row."""
+    B, H, T, d, C, W = 1, 2, 300, 64, 16, 64
+    cfg = eva.make_config(B, H, T, d, C, W, seed=12)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=13, device="cuda")
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.bfloat16, seed=14, device="cuda")
+    Qr, Kr, ks, vs = eva.eva_rope_summarize(cfg, Q, K, V)
+    O, lse, _, _ = eva.eva_attn_prefill(cfg, Qr, Kr, V, Ksum=ks, Vsum=vs, summaries_provided=True)
+    dQr, dKr, dV = eva.eva_attn_backward(cfg, Qr, Kr, V, ks, vs, O, lse, dO)
+    dQ = eva.eva_rope(cfg, dQr, inverse=True)
+    dK = eva.eva_rope(cfg, dKr, inverse=True)
+    torch.cuda.synchronize()
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, T // C, d)
+    for u in range(B * H):
+        rq = torch.from_numpy(oracle.rope(f64(Q[u]))).to(torch.bfloat16).double().numpy()
+        rk = torch.from_numpy(oracle.rope(f64(K[u]))).to(torch.bfloat16).double().numpy()
+        gq, gk, gv = oracle.backward(rq, rk, f64(V[u]), E[u], f64(dO[u]), C, W, oracle.SLIDING, cfg.scale)
+        # R^T per row = the rotation at the negated position
+        gq = np.concatenate([oracle.rope(gq[t:t + 1], pos0=-t) for t in range(T)])
+        gk = np.concatenate([oracle.rope(gk[t:t + 1], pos0=-t) for t in range(T)])
+        for name, got, want in (("dQ", dQ[u], gq), ("dK", dK[u], gk), ("dV", dV[u], gv)):
+            err = np.max(np.abs(f64(got) - want))
+            assert err <= 2e-2 * max(1.0, np.max(np.abs(want))), (name, u, err)
