@@ -9,7 +9,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libeva.so")
+# EVA_LIB_PATH: load another build of the same library (scripts/mutation_check.sh runs the
+# parity tests against deliberately broken builds to show they fail); default: in-tree.
+LIB_PATH = os.environ.get("EVA_LIB_PATH") or os.path.join(_HERE, "libeva.so")
 
 EVA_OK, EVA_ERR_INVALID_ARG, EVA_ERR_UNSUPPORTED, EVA_ERR_CAPACITY, EVA_ERR_CUDA = range(5)
 EVA_F32, EVA_BF16 = 0, 1

@@ -5,6 +5,7 @@
 from __future__ import annotations
 
 import concurrent.futures as cf
+import glob
 import os
 import subprocess
 import sys
@@ -19,15 +20,12 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
-HEADERS = ["common.cuh", "summarize.cuh", "launch.h", "sm100.cuh"]
-
-
 def _deps_mtime() -> float:
-    ts = [os.path.getmtime(os.path.join(ROOT, "include", "eva.h")), os.path.getmtime(__file__)]
-    for h in HEADERS:
-        p = os.path.join(CSRC, h)
-        if os.path.exists(p):
-            ts.append(os.path.getmtime(p))
+    """Newest of this script and every header a source can include (csrc/*.cuh, csrc/*.h,
+    include/*.h): any header edit rebuilds every object."""
+    ts = [os.path.getmtime(__file__)]
+    for pat in (os.path.join(CSRC, "*.cuh"), os.path.join(CSRC, "*.h"), os.path.join(ROOT, "include", "*.h")):
+        ts += [os.path.getmtime(p) for p in glob.glob(pat)]
     return max(ts)
 
 

@@ -174,6 +174,11 @@ def exchange_p2p(cfg, K: torch.Tensor, V: torch.Tensor, shards: List[SeqShard], 
                           dtype=api._tdtype(cfg), scale=cfg.scale, lam=cfg.lambda_, clip=cfg.clip,
                           seed=cfg.seed, layer=cfg.layer, omega_mode=cfg.omega_mode,
                           summary_bias=cfg.summary_bias)
+    # Write-after-read guard: the previous cp_prefill on these PeerSummaries (last layer or
+    # iteration) reads every copy in place, and a faster rank's stores below would land in a
+    # slower rank's copy while its prefill still reads it.  The device-side barrier is stream
+    # ordered, so every rank's earlier prefill has completed once all ranks pass it.
+    peers.barrier()
     api.eva_summarize_range_bcast(sub, me.q0 // cfg.chunk, K, V, peers.ptr_k, peers.ptr_v,
                                   peers.n_chunks)
     peers.barrier()  # every rank's summaries have landed in every copy

@@ -385,9 +385,10 @@ size_t eva_decode_workspace_bytes(const eva_cache* cache) {
     return 0;
   const int S = eva::decode_splits(*cache);
   if (S <= 1) return 0;
-  // split partials (m, l, acc[d]) per (unit, split) + one merge counter per unit
-  return (size_t)cache->cfg.bh_count * S * (cache->cfg.d_head + 2) * sizeof(float) +
-         (size_t)cache->cfg.bh_count * sizeof(unsigned);
+  // one merge counter per unit (fixed offset, padded to 16 bytes) + the split partials
+  // (m, l, acc[d]) per (unit, split)
+  return ((size_t)cache->cfg.bh_count + 3) / 4 * 4 * sizeof(unsigned) +
+         (size_t)cache->cfg.bh_count * S * (cache->cfg.d_head + 2) * sizeof(float);
 }
 
 eva_status eva_attn_decode(const eva_cache* cache, const void* Q, void* O, float* lse,
@@ -455,10 +456,13 @@ eva_status eva_decode_step(eva_cache* cache, const void* Q, const void* K_new, c
   // batches also take the two-launch path: there the decode is a pure HBM stream and the
   // separate append measured faster (0.478 vs 0.518 ms/token at configs[3]); the fused
   // launch pays off when the step is launch-latency bound (small batch x heads).
+  // Every check the decode half needs (lse/workspace alignment and size for pos + 1, the
+  // summary capacity) was done above, so nothing is enqueued unless both halves can run.
   if ((cache->pos + 1) % cache->cfg.chunk == 0 || cache->cfg.bh_count >= 1024) {
     st = eva_cache_append(cache, K_new, V_new, 1, eps, stream);
     if (st != EVA_OK) return st;
-    return eva_attn_decode(cache, Q, O, lse, workspace, workspace_bytes, stream);
+    return cuda_status(eva::launch_decode(*cache, Q, O, lse, (float*)workspace, S, (cudaStream_t)stream),
+                       "eva_decode_step");
   }
   cudaError_t e = eva::launch_decode_step(after, Q, K_new, V_new, O, lse, (float*)workspace, S,
                                           (cudaStream_t)stream);

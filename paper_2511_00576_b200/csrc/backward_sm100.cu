@@ -940,11 +940,9 @@ cudaError_t launch_bwd_main(const eva_config& cfg, const void* Q, const void* K,
   const size_t smem = sizeof(BwdSm<D>) + 1024;
   static const bool trace = getenv("EVA_BWD_TRACE") != nullptr;  // debug timeline of CTA 0
   auto kern = trace ? bwd_main_sm100_kernel<D, true> : bwd_main_sm100_kernel<D, false>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = set_smem_attr((const void*)kern, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int items_per_unit = phase == 1 ? n_sum_items : phase == 2 ? n_local_items : n_sum_items + n_local_items;
   const int item_base = phase == 2 ? n_sum_items : 0;

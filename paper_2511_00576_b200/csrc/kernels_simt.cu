@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 
@@ -603,6 +604,11 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   pdl_trigger();
   const int u = blockIdx.x, S = S_, s = blockIdx.y;
   const int W = c.cfg.window, C = c.cfg.chunk;
+  // workspace layout (split-K only): merge counters at a FIXED offset (one per unit, padded to
+  // 16 bytes) then the partials (m, l, acc[D]) per (unit, split).  The split count changes with
+  // the position (E/64), so anything placed after the partials would move between calls.
+  unsigned* counters = reinterpret_cast<unsigned*>(ws);
+  float* parts = ws + ((size_t)gridDim.x + 3) / 4 * 4;
   // ragged (its own instantiations, so the uniform kernel is unchanged): this unit's
   // position; the fused ragged step is called before the advance (pos[u] = p = n)
   const int64_t n = RAGGED ? (FUSED ? pos_dev[u] : pos_dev[u] - 1) : c.pos - 1;
@@ -734,7 +740,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
     if (S == 1) {
       O[(size_t)u * D + ch] = Elem<T>::from_f(o / L);
     } else {
-      ws[((size_t)u * S + s) * (D + 2) + 2 + ch] = o;
+      parts[((size_t)u * S + s) * (D + 2) + 2 + ch] = o;
     }
   }
   if constexpr (FUSED && RAGGED) {
@@ -769,13 +775,12 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
     return;
   }
   if (lane == 0) {
-    float* p = ws + ((size_t)u * S + s) * (D + 2);
+    float* p = parts + ((size_t)u * S + s) * (D + 2);
     p[0] = M;
     p[1] = L;
   }
   // split-K: the last CTA of this unit to finish merges the S partials (no second launch).
-  // Counters live after the partials and are left at zero for the next call.
-  unsigned* counters = reinterpret_cast<unsigned*>(ws + (size_t)gridDim.x * S * (D + 2));
+  // Counters (at the front of the workspace) are left at zero for the next call.
   __threadfence();
   __syncwarp();
   unsigned prev = 0;
@@ -783,7 +788,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   prev = __shfl_sync(0xffffffffu, prev, 0);
   if (prev != (unsigned)(S - 1)) return;
   __threadfence();
-  const volatile float* pu = ws + (size_t)u * S * (D + 2);
+  const volatile float* pu = parts + (size_t)u * S * (D + 2);
   float Mg = -INFINITY;
   for (int k = 0; k < S; ++k) Mg = fmaxf(Mg, pu[(size_t)k * (D + 2)]);
   float Lg = 0.f;
@@ -902,13 +907,17 @@ int num_sms() {
 
 constexpr size_t kSummSmemMax = 96 * 1024;
 
-// Raise the dynamic shared-memory limit of `fn` to `bytes` (once per function and size).
+// Raise the dynamic shared-memory limit of `fn` to `bytes` (once per device, function and
+// size: the attribute belongs to the current device's context).
 cudaError_t set_smem_attr(const void* fn, size_t bytes) {
   static std::mutex mu;
-  static std::unordered_map<const void*, size_t> done;
+  static std::map<std::pair<int, const void*>, size_t> done;
   if (bytes <= 48 * 1024) return cudaSuccess;
+  int dev = 0;
+  cudaError_t ge = cudaGetDevice(&dev);
+  if (ge != cudaSuccess) return ge;
   std::lock_guard<std::mutex> lk(mu);
-  size_t& cur = done[fn];
+  size_t& cur = done[{dev, fn}];
   if (bytes > cur) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;

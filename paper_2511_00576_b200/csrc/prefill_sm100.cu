@@ -1882,12 +1882,9 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
   }
   if (!ok) return cudaErrorInvalidValue;
   const size_t smem = sizeof(Smem<D, NSTAGE>) + Smem<D, NSTAGE>::PAD;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = set_smem_attr((const void*)prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   dim3 grid((rg.nq + BM - 1) / BM, BH);
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
@@ -1916,12 +1913,9 @@ cudaError_t launch_persist(const eva_config& cfg, const PrefillRange& rg, const 
   }
   if (!ok) return cudaErrorInvalidValue;
   const size_t smem = sizeof(SmemP<D, NSTAGE>) + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_persist_kernel<D, NSTAGE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = set_smem_attr((const void*)prefill_persist_kernel<D, NSTAGE>, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int n_qt = (rg.nq + BM - 1) / BM;
   const int n_items = n_qt * BH;
@@ -1950,12 +1944,9 @@ cudaError_t launch_split(const eva_config& cfg, const void* Q, const void* K, co
   }
   if (!ok) return cudaErrorInvalidValue;
   const size_t smem = sizeof(Smem2<D, NSTAGE>) + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_split_kernel<D, NSTAGE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = set_smem_attr((const void*)prefill_split_kernel<D, NSTAGE>, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   dim3 grid((T + BM - 1) / BM, BH);
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
@@ -1980,12 +1971,9 @@ cudaError_t launch_wide(const eva_config& cfg, const void* Q, const void* K, con
   }
   if (!ok) return cudaErrorInvalidValue;
   const size_t smem = sizeof(SmemWide<D, NSK, NSV>) + 1024;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_wide_kernel<D, NSK, NSV>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = set_smem_attr((const void*)prefill_wide_kernel<D, NSK, NSV>, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   dim3 grid((T + BM - 1) / BM, BH);
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
@@ -2010,12 +1998,9 @@ cudaError_t launch_pair(const eva_config& cfg, const void* Q, const void* K, con
   }
   if (!ok) return cudaErrorInvalidValue;
   const size_t smem = sizeof(SmemPair<D, NS>) + 1024 + (TRACE ? sizeof(TraceLog) : 0);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_pair_kernel<D, NS, TRACE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = set_smem_attr((const void*)prefill_pair_kernel<D, NS, TRACE>, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int ppu = (T + 2 * BM - 1) / (2 * BM);
   const int64_t items = (int64_t)BH * ppu;

@@ -208,10 +208,11 @@ def test_backward_alternate_paths_parity(knob):
     import sys
     env = dict(os.environ, **{knob: "1"})
     if knob == "EVA_BACKWARD_FUSED":
-        sel = "test_backward_parity and dtype1 or test_backward_variant_parity and dtype1"
+        sel = ("test_backward_parity and dtype1 or test_backward_variant_parity and dtype1 or "
+               "test_backward_bf16_omega_branch")
     else:
         sel = ("test_backward_parity and dtype1 and (case2 or case3 or case9) or "
-               "test_backward_variant_parity and dtype1 and case3")
+               "test_backward_variant_parity and dtype1 and case3 or test_backward_bf16_omega_branch")
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-k", sel,
                         "-p", "no:cacheprovider"], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -260,3 +261,42 @@ def test_backward_configs2_full_size_sampled(eva):
         _check("dQ", f64(dQ[sl]), rq, 2e-2)
         _check("dK", f64(dK[sl]), rk, 2e-2)
         _check("dV", f64(dV[sl]), rv, 2e-2)
+
+
+# ---- the Eq.15 branch of the bf16 backward (clip-gated omega; reading R14)
+OMEGA_CASES = [  # (B, H, T, d, C, W, lam, clip, k_std, v_std)
+    (1, 2, 1024, 64, 8, 16, 0.3, 0.3, 0.25, 4.0),
+    (1, 2, 1024, 128, 8, 16, 0.3, 0.3, 0.2, 4.0),
+    (1, 1, 2048, 64, 16, 32, 0.5, 0.4, 0.3, 3.0),
+]
+
+
+@pytest.mark.parametrize("case", OMEGA_CASES)
+def test_backward_bf16_omega_branch(eva, case):
+    """bf16 backward where the omega path of Eq.15 is large enough to be seen: lambda != 1,
+    a clip bound that gates ~1/3 of the channels, small-norm keys (so the log-xi softmax of
+    a chunk spreads over several rows and omega.k matters) and large values (large d beta).
+    Sized with torch fp64 autograd of the augmented form: deleting the clip gate, replacing
+    lambda by 1 in the gate, or dropping the omega path changes max|dK| by 1.4-5x the bound
+    below (mutation check).  Runs on the unfused (register finalize) schedule
+    here and on the fused (COEF) schedule in test_backward_alternate_paths_parity."""
+    B, H, T, d, C, W, lam, clip, ks_, vs_ = case
+    cfg = eva.make_config(B, H, T, d, C, W, seed=91, lam=lam, clip=clip)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.float32, seed=92, device="cuda")
+    K = (K * ks_).to(torch.bfloat16)
+    V = (V * vs_).to(torch.bfloat16)
+    Q = Q.to(torch.bfloat16)
+    (dO,) = eva_inputs.normal_units(1, 0, B * H, T, d, torch.bfloat16, seed=93, device="cuda")
+    O, lse, ksum, vsum = eva.eva_attn_prefill(cfg, Q, K, V)
+    dQ, dK, dV = eva.eva_attn_backward(cfg, Q, K, V, ksum, vsum, O, lse, dO)
+    torch.cuda.synchronize()
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, T // C, d)
+    # both sides of the gate are exercised
+    kt = f64(K)[:, :T // C * C].reshape(B * H, T // C, C, d).mean(axis=2)
+    inside = np.abs(kt + E) <= clip
+    assert 0.15 < inside.mean() < 0.85
+    rq, rk, rv = oracle.backward_batch(f64(Q), f64(K), f64(V), E, f64(dO), C, W, oracle.SLIDING,
+                                       cfg.scale, lam=lam, clip=clip)
+    _check("dQ", f64(dQ), rq, 2e-2)
+    _check("dK", f64(dK), rk, 2e-2)
+    _check("dV", f64(dV), rv, 2e-2)
