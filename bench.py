@@ -3,6 +3,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-extras]
     torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself under
+`python -m torch.distributed.run --nproc-per-node N` (127.0.0.1, a free port) and passes the
+rank-0 JSON line through.  --stub runs the launcher and the multi-rank bookkeeping with the
+kernels replaced by host sleeps on gloo (the CPU test of the N-rank path).
 
 Workload (BASELINE.json configs[1]): B=1, H=16, T=2048, d=64, C=64, W=128, bf16, sliding
 window, Q/K/V ~ N(0,1) synthetic (eva_inputs), eps from the in-kernel Philox.
@@ -17,9 +21,12 @@ no collective on the data path.  L2 (126 MB) is larger than the 
 working set, so a 512 MiB buffer is overwritten before every timed step (outside the
 events); config.l2 says so.
 
-Extras (rank 0 / every rank at N>1 with its own shard): configs[2] prefill shape per GPU
-(B=8, H=32, T=8192, d=128, C=64, W=256) and configs[3] decode (B=256, H=32, d=128, 32k
-compressed context, 512 generated tokens), each with its roofline.
+Extras (every rank with its own shard; rank 0 prints): configs[2] prefill per GPU (B=8, H=32,
+T=8192, d=128, C=64, W=256; weak: 256 units per rank) and configs[2] strong-scaled (its 256
+units split over the N ranks, max-over-ranks device time, plus the NCCL gather of O to rank 0
+timed separately), configs[3] decode (B=256, H=32, d=128, 32k compressed context, 512
+generated tokens), configs[4] long-context cells (T = 4k..128k, H=32, d=128, C, W), the
+backward at configs[1]/[2] shapes, each with its roofline; the configs[0] oracle time.
 """
 from __future__ import annotations
 
@@ -310,6 +317,8 @@ def run_ours(args, rank, world, local_rank):
         extras = {}
         if not args.no_extras:
             extras["prefill_configs2"] = bench_prefill_large(args, eva, torch, dev, s, rank, world, peaks)
+            extras["prefill_configs2_strong"] = bench_prefill_strong(args, eva, torch, dev, s, rank, world, peaks, dist)
+            extras["sweep_configs4"] = bench_sweep(args, eva, torch, dev, s, rank, world, peaks)
             extras["decode_configs3"] = bench_decode(args, eva, torch, dev, s, rank, world, peaks)
             extras["backward_configs2"] = bench_backward(args, eva, torch, dev, s, rank, world, peaks, LARGE)
             extras["backward_configs1"] = bench_backward(args, eva, torch, dev, s, rank, world, peaks, WORKLOAD)
@@ -339,7 +348,7 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "512 MiB L2 flush before every timed step (outside the events)"},
         "roofline": {"kernel": "eva_attn_prefill (summaries provided)", "bound": "hbm",
                      "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm"], "traffic": load_traffic("prefill_cfg2"),
+                     "frac": achieved / peaks["hbm"], "traffic": load_traffic("prefill_configs1"),
                      "alg_bytes_per_launch": pbytes, "avg_launch_ms": pre_avg,
                      "share_of_step": pre_avg / (statistics.mean(sum_ms) + pre_avg + statistics.mean(app_ms)
                                                  + statistics.mean(dec_ms)),
@@ -360,8 +369,9 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks,
     }
     result.update(extras)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget)
+        result["cpu_oracle_configs0"] = cpu_oracle_configs0()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -417,7 +427,7 @@ def bench_prefill_large(args, eva, torch, dev, s, rank, world, peaks):
                         "frac": pb / (pre / 1e3) / 1e9 / peaks["hbm"],
                         "tensor_tflops_alg": pf / (pre / 1e3) / 1e12,
                         "tensor_frac_of_bf16_peak": pf / (pre / 1e3) / 1e12 / peaks["bf16"],
-                        "traffic": load_traffic("prefill_cfg3")},
+                        "traffic": load_traffic("prefill_configs2")},
            "summarize_roofline": {"bound": "hbm", "achieved": 2 * BH * T * d * 2 / (summ / 1e3) / 1e9,
                                   "peak": peaks["hbm"], "unit": "GB/s"}}
     del Q, K, V, O, ks, vs
@@ -540,11 +550,126 @@ def bench_decode(args, eva, torch, dev, s, rank, world, peaks):
            "roofline": {"kernel": "eva_attn_decode", "bound": "hbm",
                         "achieved": nbytes / (dec / 1e3) / 1e9, "peak": peaks["hbm"], "unit": "GB/s",
                         "frac": nbytes / (dec / 1e3) / 1e9 / peaks["hbm"],
-                        "alg_bytes_per_launch": nbytes / steps, "traffic": load_traffic("decode_cfg4")}}
+                        "alg_bytes_per_launch": nbytes / steps, "traffic": load_traffic("decode_configs3")}}
     del cache, toks
     torch.cuda.empty_cache()
     return out
 
+
+
+def bench_prefill_strong(args, eva, torch, dev, s, rank, world, peaks, dist):
+    """configs[2] strong-scaled: its 256 (b,h) units split contiguously over the N ranks
+    (paper_2511_00576_b200.parallel.shard_units), summarize + prefill per rank on the rank's own
+    synthetic inputs (RNG keyed by the global unit), device time max over ranks.  The path has
+    no exchange step; the NCCL all-gather of O into rank 0's [256, T, d] buffer (the
+    "scatter/gather of the shards") is timed separately and is not part of the value."""
+    import eva_inputs
+    from paper_2511_00576_b200.parallel import max_over_ranks, shard_units
+    L = LARGE
+    units = L["B"] * L["H"]
+    T, d, C, W = L["T"], L["d"], L["C"], L["W"]
+    sh = shard_units(units, world)[rank]
+    BH, bh0 = sh.bh_count, sh.bh_begin
+    cfg = eva.make_config(L["B"], L["H"], T, d, C, W, bh_begin=bh0, bh_count=BH)
+    Q, K, V = eva_inputs.qkv(bh0, BH, T, d, torch.bfloat16, seed=0, device=dev)
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    O = torch.empty_like(Q)
+    lse = torch.empty(BH, T, dtype=torch.float32, device=dev)
+    reps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, O=O, lse=lse)
+    torch.cuda.synchronize()
+    if dist: dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(reps):
+        eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, O=O, lse=lse)
+    b.record(s)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b) / reps, device=dev)
+    gather_ms = None
+    nccl = None
+    if dist and world > 1:
+        # O of every rank into one [units, T, d] buffer (equal shards when world | 256)
+        per = (units + world - 1) // world
+        buf = torch.zeros(per, T, d, dtype=torch.bfloat16, device=dev)
+        buf[:BH].copy_(O)
+        out = torch.empty(per * world, T, d, dtype=torch.bfloat16, device=dev)
+        dist.all_gather_into_tensor(out, buf)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(s)
+        dist.all_gather_into_tensor(out, buf)
+        g1.record(s)
+        torch.cuda.synchronize()
+        gather_ms = max_over_ranks(g0.elapsed_time(g1), device=dev)
+        nccl = {"nranks": world, "backend": dist.get_backend(), "collective": "all_gather_into_tensor(O)",
+                "bytes_per_rank": per * T * d * 2}
+        del buf, out
+    pb = prefill_bytes(BH, T, d, C)
+    pf = prefill_flops(BH, T, d, C, W)
+    # per-rank ideal at the HBM roofline (the rank's algorithmic bytes / peak)
+    out = {"workload": f"configs[2] strong-scaled: {units} units of T={T},d={d},C={C},W={W} split over "
+                       f"{world} rank(s) ({BH} on rank {rank}); eva_attn_prefill, summaries provided",
+           "units_total": units, "units_per_rank": BH, "ms": ms,
+           "tokens_per_s_total": units // L["H"] * T / (ms / 1e3),
+           "per_rank_alg_bytes": pb, "per_rank_ms_at_hbm_peak": pb / (peaks["hbm"] * 1e9) * 1e3,
+           "roofline": {"bound": "hbm", "achieved": pb / (ms / 1e3) / 1e9, "peak": peaks["hbm"],
+                        "unit": "GB/s", "frac": pb / (ms / 1e3) / 1e9 / peaks["hbm"],
+                        "tensor_frac_of_bf16_peak": pf / (ms / 1e3) / 1e12 / peaks["bf16"]},
+           "gather_o_ms": gather_ms, "nccl": nccl}
+    del Q, K, V, O, ks, vs, lse
+    torch.cuda.empty_cache()
+    return out
+
+
+SWEEP = [(4096, 128, 128), (16384, 64, 512), (65536, 32, 512), (65536, 64, 512),
+         (131072, 32, 512), (131072, 64, 512), (131072, 128, 512)]
+
+
+def bench_sweep(args, eva, torch, dev, s, rank, world, peaks):
+    """configs[4] long-context cells (H=32 units of one sequence, d=128, sliding): T, C, W as in
+    SWEEP.  Per cell: eva_attn_prefill with the summaries provided (the tensor-core kernel) and
+    eva_summarize, device time (CUDA events), algorithmic flops / bytes as in the headline
+    roofline, tensor fraction against the measured bf16 burst peak.  Each rank runs the whole
+    cell on its own (weak)."""
+    import eva_inputs
+    H, d = 32, 128
+    cells = []
+    for (T, C, W) in (SWEEP if not args.quick else SWEEP[:2]):
+        cfg = eva.make_config(1, H, T, d, C, W)
+        Q, K, V = eva_inputs.qkv(0, H, T, d, torch.bfloat16, seed=0, device=dev)
+        ks, vs = eva.eva_summarize(cfg, K, V)
+        O = torch.empty_like(Q)
+        lse = torch.empty(H, T, dtype=torch.float32, device=dev)
+        eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse)
+        torch.cuda.synchronize()
+        reps = 5
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(s)
+        for _ in range(reps):
+            eva.eva_summarize(cfg, K, V, Ksum=ks, Vsum=vs)
+        e[1].record(s)
+        for _ in range(reps):
+            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse)
+        e[2].record(s)
+        torch.cuda.synchronize()
+        sm = e[0].elapsed_time(e[1]) / reps
+        pm = e[1].elapsed_time(e[2]) / reps
+        pf = prefill_flops(H, T, d, C, W)
+        pb = prefill_bytes(H, T, d, C)
+        cells.append({"T": T, "C": C, "W": W, "prefill_ms": pm, "summarize_ms": sm,
+                      "tokens_per_s": T / ((pm + sm) / 1e3),
+                      "tensor_tflops_alg": pf / (pm / 1e3) / 1e12,
+                      "tensor_frac": pf / (pm / 1e3) / 1e12 / peaks["bf16"],
+                      "hbm_frac": pb / (pm / 1e3) / 1e9 / peaks["hbm"]})
+        del Q, K, V, O, ks, vs, lse
+        torch.cuda.empty_cache()
+    return {"workload": "configs[4]: B=1, H=32, d=128, sliding, bf16; cells (T, C, W)",
+            "peak_bf16_tflops": peaks["bf16"], "peak_hbm_gbs": peaks["hbm"], "peak_source": peaks["src"],
+            "cells": cells}
 
 # ============================================================================ oracle (CPU) arm
 def cpu_baseline(args, budget_s=12.0):
@@ -576,6 +701,30 @@ def cpu_baseline(args, budget_s=12.0):
                       f"{BH} units, fp64 C oracle, OpenMP over units) in {el:.1f} s"}
 
 
+def cpu_oracle_configs0():
+    """BASELINE configs[0] (B=1, H=1, T=256, d=16, C=16, W=32, fp32): the fp64 oracle's time
+    for the whole pass (summaries + prefill) on this host -- "CPU oracle in seconds"."""
+    import torch
+
+    import eva_inputs
+    import oracle
+    B, H, T, d, C, W = 1, 1, 256, 16, 16, 32
+    Q, K, V = (x.double().numpy() for x in eva_inputs.qkv(0, B * H, T, d, torch.float32, seed=0))
+    E = oracle.eps_units(1234, 0, 0, B * H, T // C, d)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        ks, vs = oracle.summarize_batch(K, V, E, C)
+        oracle.prefill_batch(Q, K, V, ks, vs, C, W, 0, 1 / math.sqrt(d))
+        reps += 1
+        if time.perf_counter() - t0 > 1.0 or reps >= 1000:
+            break
+    sec = (time.perf_counter() - t0) / reps
+    return {"workload": "configs[0]: B=1,H=1,T=256,d=16,C=16,W=32 (summaries + prefill)", "seconds": sec,
+            "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)), "kind": "oracle",
+            "reps": reps}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return None
@@ -595,11 +744,58 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (same seeded inputs as our arm)",
             "config": {"workload": wl["name"], "B_per_gpu": wl["B"], "H": wl["H"], "T": wl["T"],
-                       "d_head": wl["d"], "chunk": wl["C"], "window": wl["W"]},
+                       "d_head": wl["d"], "chunk": wl["C"], "window": wl["W"], "mode": "sliding",
+                       "global_batch": wl["B"] * world,
+                       "parallelism": "rank 0 only (host cores); the other ranks exit without work"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "kind": "oracle",
                              "cores": per_step[0]["cores"],
                              "sample": "each step = one full pass of the configs[1] workload on the fp64 oracle"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def run_stub(args, rank, world):
+    """--stub: the N-rank plumbing of run_ours with every kernel replaced by a host sleep (gloo,
+    CPU): shard bounds of the weak (configs[1]) and strong (configs[2]) legs, barrier-bracketed
+    timing, max over ranks, the rank-0 line.  Used by tests/test_bench_launcher.py."""
+    import torch  # noqa: F401
+    from paper_2511_00576_b200.parallel import max_over_ranks, shard_for, shard_units
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    wl = WORKLOAD
+    weak = shard_for(rank, world, wl["B"] * world, wl["H"])
+    strong = shard_units(LARGE["B"] * LARGE["H"], world)[rank]
+    if dist: dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.001 * (1 + rank))  # the slowest rank sets the time
+    el = time.perf_counter() - t0
+    if dist: dist.barrier()
+    total_s = max_over_ranks(el)
+    shards = [None] * world
+    if dist:
+        dist.all_gather_object(shards, (strong.bh_begin, strong.bh_count))
+    else:
+        shards = [(strong.bh_begin, strong.bh_count)]
+    res = {"metric": "prefill tokens/s (FlashEVA hot path, whole job)", "stub": True,
+           "value": world * wl["B"] * wl["T"] * args.steps / total_s, "unit": "tokens/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s * 1e3 / args.steps,
+           "higher_is_better": True, "scaling": "weak",
+           "config": {"workload": wl["name"], "global_batch": wl["B"] * world,
+                      "weak_shard_rank0": [weak.bh_begin, weak.bh_count] if rank == 0 else None,
+                      "strong_shards": shards}}
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return res
+
+
+def free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 
 
 def main():
@@ -611,24 +807,32 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="shorter decode extra (profiling)")
+    ap.add_argument("--stub", action="store_true", help="launcher / multi-rank bookkeeping only (CPU, gloo)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--e2e-slices", type=int, default=1, help="unit slices of the host-copy pipeline (1: no overlap; see DESIGN.md §8)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # self-launch: one process per GPU under torch.distributed.run; rank 0's line passes through
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
+        cmd += sys.argv[1:]
+        sys.exit(subprocess.run(cmd).returncode)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            print(f"--gpus {args.gpus} needs torchrun (WORLD_SIZE={world})", file=sys.stderr)
-            sys.exit(2)
-    if args.impl == "reference":
+        print(f"--gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.stub:
+        res = run_stub(args, rank, world)
+    elif args.impl == "reference":
         res = run_reference(args, rank, world)
     else:
         res = run_ours(args, rank, world, local_rank)
     if rank == 0 and res is not None:
-        print(json.dumps(res))
+        print(json.dumps(res), flush=True)
 
 
 if __name__ == "__main__":

@@ -166,23 +166,30 @@ eva_status eva_summarize_proj(const eva_config* cfg, const void* K, const void* 
  * eps        : as in eva_summarize (ignored with EVA_SUMMARIES_PROVIDED).
  * lse        : [bh_count, T] fp32 (out) or NULL.
  * flags      : EVA_SUMMARIES_PROVIDED -- use the caller's Ksum/Vsum as is;
- *              EVA_PREFILL_SIMT       -- force the SIMT kernel (parity/debug);
- *              EVA_PREFILL_TC_TILE    -- force the one-tile-per-CTA tensor-core kernel;
- *              EVA_PREFILL_TC_PAIR    -- force the persistent two-tile tensor-core kernel;
- *              EVA_PREFILL_TC_WIDE    -- force the 128-key-tile tensor-core kernel;
- *              EVA_PREFILL_TC_SPLIT   -- force the split-softmax (8 softmax warps) kernel;
+ *              EVA_SUMMARIES_FUSED    -- compute the summaries inside the attention kernel, one
+ *                                        launch (EVA_ERR_UNSUPPORTED where it does not apply, below);
+ *              EVA_SUMMARIES_SEPARATE -- compute them in a separate eva_summarize launch first;
+ *              EVA_PREFILL_SIMT       -- force the SIMT kernel (parity/debug; separate summaries);
  *              EVA_PREFILL_OVERLAP    -- see below;
- *              EVA_PREFILL_TC_PERSIST -- force the persistent tile kernel (see below);
- *              0                      -- compute summaries, then attend (kernel chosen
- *                                        by problem size).
+ *              0                      -- separate (measured faster on B200 than the fused launch
+ *                                        at configs[1] and configs[2]).
  * bf16 runs the tcgen05/TMEM/TMA kernel for d in {64, 128} (requires 16-byte
- * aligned base pointers); other cases run the SIMT kernel. */
+ * aligned base pointers); other cases run the SIMT kernel.
+ * Fused summaries (section 4.4 names the separate summary pass as FlashEVA's overhead at
+ * short L): the CTA of each 128-query tile summarises the complete chunks inside its own
+ * query rows from the K/V tiles it has already loaded for the attention, publishes them
+ * with a per-tile ready flag, and reads the earlier chunks' summaries once their owners
+ * have published (query tiles are dispatched by a monotone ticket, so every awaited owner
+ * is resident).  Applies to bf16, d in {64, 128}, causal modes (sliding / block) and chunk
+ * sizes C in {16, 32, 64}.  Uses a per-(device, stream) workspace owned by
+ * the library, allocated on the first fused call of a shape; a CUDA graph capturing the
+ * call needs it allocated first (eva_prefill_reserve), else EVA_ERR_INVALID_ARG.  The
+ * summaries equal eva_summarize's up to fp32 summation order (bf16 outputs may differ by
+ * one rounding step). */
 #define EVA_SUMMARIES_PROVIDED 1u
+#define EVA_SUMMARIES_FUSED 2u
 #define EVA_PREFILL_SIMT 4u
-#define EVA_PREFILL_TC_TILE 8u
-#define EVA_PREFILL_TC_PAIR 16u
-#define EVA_PREFILL_TC_WIDE 32u
-#define EVA_PREFILL_TC_SPLIT 64u
+#define EVA_SUMMARIES_SEPARATE 16u
 /* EVA_PREFILL_OVERLAP (with EVA_SUMMARIES_PROVIDED, tensor-core path): the caller asserts that
  * the launch immediately before this one on `stream` is the eva_summarize that writes Ksum/Vsum
  * and that Q, K, V were complete before that launch.  The prefill then starts its local-window
@@ -190,13 +197,15 @@ eva_status eva_summarize_proj(const eva_config* cfg, const void* K, const void* 
  * reading the summaries (measured neutral to slower on B200 -- DESIGN.md §11 -- so off by
  * default). */
 #define EVA_PREFILL_OVERLAP 128u
-/* EVA_PREFILL_TC_PERSIST: the persistent form of the one-tile-per-CTA tensor-core kernel (two
- * CTAs per SM loop over the query tiles; the next tile's loads and first MMAs overlap the
- * current tile's epilogue). */
-#define EVA_PREFILL_TC_PERSIST 256u
 eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K, const void* V,
                             void* Ksum, void* Vsum, const float* eps, void* O, float* lse,
                             uint32_t flags, eva_stream_t stream);
+
+/* eva_prefill_reserve: allocate (or grow) the library's workspace of the fused-summary prefill
+ * for cfg's shape on `stream` (one zero-initialised 32-bit ready flag per (unit, 128-query
+ * tile) plus 16 bytes of counters; kept until process exit).  Call it before capturing an
+ * eva_attn_prefill into a CUDA graph; synchronises `stream` if an existing buffer is replaced. */
+eva_status eva_prefill_reserve(const eva_config* cfg, eva_stream_t stream);
 
 /* ---------------------------------------------------------------- query-range prefill
  * The building blocks of a sequence-sharded (context-parallel) prefill (SURVEY §8(f) NEXT

@@ -18,13 +18,10 @@ EVA_F32, EVA_BF16 = 0, 1
 EVA_WINDOW_SLIDING, EVA_WINDOW_BLOCK, EVA_NONCAUSAL = 0, 1, 2
 EVA_OMEGA_AS_PRINTED, EVA_OMEGA_SHIFTED_NOISE = 0, 1
 EVA_SUMMARIES_PROVIDED = 1
+EVA_SUMMARIES_FUSED = 2
 EVA_PREFILL_SIMT = 4
-EVA_PREFILL_TC_TILE = 8
-EVA_PREFILL_TC_PAIR = 16
-EVA_PREFILL_TC_WIDE = 32
-EVA_PREFILL_TC_SPLIT = 64
+EVA_SUMMARIES_SEPARATE = 16
 EVA_PREFILL_OVERLAP = 128
-EVA_PREFILL_TC_PERSIST = 256
 
 _STATUS = {0: "EVA_OK", 1: "EVA_ERR_INVALID_ARG", 2: "EVA_ERR_UNSUPPORTED", 3: "EVA_ERR_CAPACITY",
            4: "EVA_ERR_CUDA"}
@@ -55,7 +52,7 @@ EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache
            "eva_attn_backward", "eva_pipeline_create", "eva_pipeline_destroy", "eva_attn_prefill_host",
            "eva_summarize_range", "eva_attn_prefill_range", "eva_summarize_range_bcast",
            "eva_summarize_proj", "eva_decode_ragged_workspace_bytes", "eva_decode_step_ragged",
-           "eva_rope_summarize", "eva_rope"]
+           "eva_rope_summarize", "eva_rope", "eva_prefill_reserve"]
 
 
 class EvaError(RuntimeError):
@@ -82,6 +79,7 @@ def _load():
         "eva_decode_ragged_workspace_bytes": (ctypes.c_size_t, [CACHE]),
         "eva_decode_step_ragged": (st, [CACHE, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "eva_attn_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_uint32, P]),
+        "eva_prefill_reserve": (st, [CFG, P]),
         "eva_cache_append": (st, [CACHE, P, P, ctypes.c_int32, P, P]),
         "eva_attn_decode": (st, [CACHE, P, P, P, P, ctypes.c_size_t, P]),
         "eva_cache_load": (st, [CACHE, P, P, P, P, ctypes.c_int32, P]),

@@ -155,8 +155,9 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
                      overlap: bool = False):
     """FlashEVA chunk-causal prefill.  Returns (O, lse, Ksum, Vsum).
 
-    kernel: None (chosen by size), "simt", "tile" (tcgen05, one 128-query tile per CTA)
-    or "pair" (persistent tcgen05 kernel, two Q tiles per CTA sharing the K/V stream)."""
+    kernel: None or "separate" (EVA_SUMMARIES_SEPARATE: summarize launch + tcgen05 kernel),
+    "fused" (EVA_SUMMARIES_FUSED: in-kernel summaries, one launch; an error where they do not
+    apply) or "simt" (the fp32-capable SIMT kernel, separate summaries)."""
     if kernel == "simt":
         simt = True
     dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
@@ -180,15 +181,23 @@ def eva_attn_prefill(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.
     if want_lse and lse is None:
         lse = torch.empty(bh, T, dtype=torch.float32, device=Q.device)
     flags = (N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0) | (N.EVA_PREFILL_SIMT if simt else 0)
-    flags |= {None: 0, "simt": 0, "tile": N.EVA_PREFILL_TC_TILE, "pair": N.EVA_PREFILL_TC_PAIR,
-              "wide": N.EVA_PREFILL_TC_WIDE, "split": N.EVA_PREFILL_TC_SPLIT,
-              "persist": N.EVA_PREFILL_TC_PERSIST}[kernel]
+    if not summaries_provided:
+        flags |= {None: 0, "simt": 0, "fused": N.EVA_SUMMARIES_FUSED,
+                  "separate": N.EVA_SUMMARIES_SEPARATE}[kernel]
+    elif kernel not in (None, "simt", "separate"):
+        raise ValueError(f"kernel={kernel!r} with summaries_provided")
     if overlap:  # the previous launch on this stream is the eva_summarize writing Ksum/Vsum
         flags |= N.EVA_PREFILL_OVERLAP
     check(lib.eva_attn_prefill(ctypes.byref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum), _ptr(Vsum),
                                _ptr(eps), _ptr(O), _ptr(lse if want_lse else None), flags,
                                _stream(Q.device)))
     return O, (lse if want_lse else None), Ksum, Vsum
+
+
+def eva_prefill_reserve(cfg: EvaConfig, device="cuda") -> None:
+    """Allocate the library's fused-summary workspace for cfg's shape on the current stream of
+    `device` (call before capturing eva_attn_prefill into a CUDA graph)."""
+    check(lib.eva_prefill_reserve(ctypes.byref(cfg), _stream(torch.device(device))))
 
 
 def eva_summarize_range(cfg: EvaConfig, chunk0: int, K: torch.Tensor, V: torch.Tensor,
@@ -293,7 +302,8 @@ class HostPrefill:
                 raise ValueError("hlse must be a host fp32 tensor [bh, T]")
         if eps is not None:
             _need(eps, "eps", (bh, T // cfg.chunk, d), torch.float32)
-        flags = {None: 0, "simt": N.EVA_PREFILL_SIMT, "tile": N.EVA_PREFILL_TC_TILE}[kernel]
+        flags = {None: 0, "simt": N.EVA_PREFILL_SIMT, "fused": N.EVA_SUMMARIES_FUSED,
+                 "separate": N.EVA_SUMMARIES_SEPARATE}[kernel]
         check(lib.eva_attn_prefill_host(self._pipe, ctypes.byref(cfg), _ptr(hQ), _ptr(hK), _ptr(hV),
                                         _ptr(hO), _ptr(hlse), _ptr(self.Q), _ptr(self.K), _ptr(self.V),
                                         _ptr(self.Ksum), _ptr(self.Vsum), _ptr(self.O), _ptr(self.lse),

@@ -200,12 +200,23 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
                             uint32_t flags, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
-  if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_PREFILL_SIMT | EVA_PREFILL_TC_TILE | EVA_PREFILL_TC_PAIR |
-                EVA_PREFILL_TC_WIDE | EVA_PREFILL_TC_SPLIT | EVA_PREFILL_OVERLAP | EVA_PREFILL_TC_PERSIST))
+  if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_SUMMARIES_FUSED | EVA_SUMMARIES_SEPARATE | EVA_PREFILL_SIMT |
+                EVA_PREFILL_OVERLAP))
     return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  const uint32_t sum_flags = flags & (EVA_SUMMARIES_PROVIDED | EVA_SUMMARIES_FUSED | EVA_SUMMARIES_SEPARATE);
+  if (sum_flags & (sum_flags - 1))
+    return fail(EVA_ERR_INVALID_ARG, "flags 0x%x: at most one of EVA_SUMMARIES_{PROVIDED,FUSED,SEPARATE}", flags);
+  if ((flags & EVA_SUMMARIES_FUSED) && (flags & EVA_PREFILL_SIMT))
+    return fail(EVA_ERR_INVALID_ARG, "EVA_SUMMARIES_FUSED runs on the tensor-core kernel, not EVA_PREFILL_SIMT");
+  if ((flags & EVA_PREFILL_OVERLAP) && !(flags & EVA_SUMMARIES_PROVIDED))
+    return fail(EVA_ERR_INVALID_ARG, "EVA_PREFILL_OVERLAP needs EVA_SUMMARIES_PROVIDED");
   if (cfg->mode == EVA_NONCAUSAL && cfg->T % cfg->chunk != 0)
     return fail(EVA_ERR_INVALID_ARG, "non-causal prefill needs T %% C == 0 (T=%d, C=%d; reading R15)", cfg->T,
                 cfg->chunk);
+  if ((flags & EVA_SUMMARIES_FUSED) && !eva::prefill_fused_supported(*cfg))
+    return fail(EVA_ERR_UNSUPPORTED,
+                "EVA_SUMMARIES_FUSED: needs bf16, d in {64,128}, a causal mode and C in {16,32,64} "
+                "(d=%d C=%d mode=%d)", cfg->d_head, cfg->chunk, cfg->mode);
   if (cfg->bh_count == 0) return ok();
   const void* p[] = {Q, K, V, O};
   const char* nm[] = {"Q", "K", "V", "O"};
@@ -219,24 +230,41 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
   if (lse && !aligned16(lse)) return fail(EVA_ERR_INVALID_ARG, "lse is not 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
+  const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) &&
+                  eva::prefill_sm100_supported(*cfg);
+  // In-kernel summaries only when asked for: measured slower than the two launches on B200 at
+  // both benchmark shapes ("K-prefill-fused"), so flags 0 keeps them separate.
+  const bool fused = have_sums && (flags & EVA_SUMMARIES_FUSED) && tc;
+  if (fused) {
+    cudaError_t e = eva::launch_prefill_sm100_fused(*cfg, Q, K, V, eps, Ksum, Vsum, O, lse, s);
+    if (e == cudaErrorStreamCaptureUnsupported)
+      return fail(EVA_ERR_INVALID_ARG, "eva_attn_prefill: the fused-summary workspace for this shape must be "
+                                       "allocated before graph capture (eva_prefill_reserve)");
+    return cuda_status(e, "eva_attn_prefill(sm100, fused summaries)");
+  }
   if (have_sums && !(flags & EVA_SUMMARIES_PROVIDED)) {
     cudaError_t e = eva::launch_summarize(*cfg, K, V, eps, Ksum, Vsum, s);
     if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill(summaries)");
   }
-  const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) &&
-                  eva::prefill_sm100_supported(*cfg);
-  uint32_t variant = (flags & EVA_PREFILL_TC_TILE) ? 1u : (flags & EVA_PREFILL_TC_PAIR) ? 2u
-                    : (flags & EVA_PREFILL_TC_WIDE) ? 3u : (flags & EVA_PREFILL_TC_SPLIT) ? 4u
-                    : (flags & EVA_PREFILL_TC_PERSIST) ? 5u : 0u;
   // EVA_PREFILL_OVERLAP: the summarize kernel is the previous grid and Q, K, V predate it,
   // so the prefill may start its local tiles before the summaries are complete.  Measured
   // neutral at configs[1] (the two kernels' CTAs do not co-reside) and 2-7 % slower at
   // configs[2] (local-first tile order), so it is opt-in only.
-  if (flags & EVA_PREFILL_OVERLAP) variant |= 0x100u;
+  const uint32_t variant = (flags & EVA_PREFILL_OVERLAP) ? 0x100u : 0u;
   const eva::PrefillRange rg = eva::full_range(*cfg);
   cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, variant, s)
                      : eva::launch_prefill_simt(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cuda_status(e, tc ? "eva_attn_prefill(sm100)" : "eva_attn_prefill(simt)");
+}
+
+eva_status eva_prefill_reserve(const eva_config* cfg, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if (cfg->bh_count == 0 || !eva::prefill_fused_supported(*cfg)) return ok();
+  cudaError_t e = eva::prefill_fused_reserve(*cfg, (cudaStream_t)stream);
+  if (e == cudaErrorStreamCaptureUnsupported)
+    return fail(EVA_ERR_INVALID_ARG, "eva_prefill_reserve: stream is capturing");
+  return cuda_status(e, "eva_prefill_reserve");
 }
 
 eva_status eva_summarize_range(const eva_config* cfg, int32_t chunk0, const void* K, const void* V,
@@ -318,7 +346,7 @@ eva_status eva_attn_prefill_range(const eva_config* cfg, int64_t q0, int32_t n_q
   rg.nsl = n_sum;
   cudaStream_t s = (cudaStream_t)stream;
   const bool tc = cfg->dtype == EVA_BF16 && !(flags & EVA_PREFILL_SIMT) && eva::prefill_sm100_supported(*cfg);
-  cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, 1u, s)
+  cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, 0u, s)
                      : eva::launch_prefill_simt(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cuda_status(e, tc ? "eva_attn_prefill_range(sm100)" : "eva_attn_prefill_range(simt)");
 }
@@ -731,12 +759,9 @@ eva_status eva_debug_trace_prefill(const eva_config* cfg, const void* Q, const v
   if (cfg->dtype != EVA_BF16 || (cfg->d_head != 64 && cfg->d_head != 128))
     return fail(EVA_ERR_UNSUPPORTED, "trace needs bf16, d in {64,128}");
   if (!trace || cap < 1) return fail(EVA_ERR_INVALID_ARG, "trace buffer");
-  if (cap < 0x10000)  // small buffers: the tile kernel's 4-CTA timeline (4 x 3 x 48 entries)
-    return cuda_status(eva::debug_trace_tile(*cfg, Q, K, V, Ksum, Vsum, O, lse, trace, (cudaStream_t)stream),
-                       "eva_debug_trace_prefill(tile)");
-  return cuda_status(eva::debug_trace_prefill(*cfg, Q, K, V, Ksum, Vsum, O, lse, trace, cap,
-                                              (cudaStream_t)stream),
-                     "eva_debug_trace_prefill");
+  return cuda_status(eva::debug_trace_tile(*cfg, Q, K, V, Ksum, Vsum, O, lse, trace, cap == 2,
+                                           (cudaStream_t)stream),
+                     "eva_debug_trace_prefill(tile)");
 }
 
 const char* eva_last_error(void) { return g_err.c_str(); }

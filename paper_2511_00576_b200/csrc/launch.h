@@ -52,20 +52,22 @@ cudaError_t launch_prefill_simt(const eva_config& cfg, const PrefillRange& rg, c
 // tcgen05/TMEM/TMA prefill (bf16, d in {64, 128}).  Returns cudaErrorNotSupported if the
 // shape is outside the kernel's envelope (the caller then reports EVA_ERR_UNSUPPORTED).
 bool prefill_sm100_supported(const eva_config& cfg);
-// variant: 0 = automatic, 1 = one 128-query tile per CTA, 2 = persistent pair kernel.
-// A range other than full_range(cfg) always runs the one-tile-per-CTA kernel.
+// variant bit 0x100: EVA_PREFILL_OVERLAP (summaries provided by the previous grid).
 cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, const void* Q,
                                  const void* K, const void* V, const void* Ksum, const void* Vsum,
                                  void* O, float* lse, uint32_t variant, cudaStream_t s);
-
-// Debug: run the pair kernel with CTA 0 recording a (clock64, event) timeline into trace_dev.
-cudaError_t debug_trace_prefill(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                                const void* Ksum, const void* Vsum, void* O, float* lse,
-                                unsigned long long* trace_dev, int cap, cudaStream_t s);
+// EVA_SUMMARIES_FUSED: summaries computed inside the tensor-core prefill (whole-sequence call,
+// causal modes, C in {16, 32, 64}); Ksum/Vsum written, eps as in eva_summarize.
+// cudaErrorStreamCaptureUnsupported: the per-stream workspace has to grow while capturing.
+bool prefill_fused_supported(const eva_config& cfg);
+cudaError_t launch_prefill_sm100_fused(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                       const float* eps, void* Ksum, void* Vsum, void* O, float* lse,
+                                       cudaStream_t s);
+cudaError_t prefill_fused_reserve(const eva_config& cfg, cudaStream_t s);
 
 cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K, const void* V,
                              const void* Ksum, const void* Vsum, void* O, float* lse,
-                             unsigned long long* trace_dev, cudaStream_t s);
+                             unsigned long long* trace_dev, bool fused, cudaStream_t s);
 
 // Cache append: summaries of chunks completed in [pos, pos+n_new), ring write of the
 // last min(n_new, W) tokens.

@@ -24,7 +24,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "common.cuh"
 #include "launch.h"
@@ -37,8 +39,22 @@ using namespace sm100;
 constexpr int BM = 128;       // queries per tile
 constexpr int BN = 64;        // keys per KV tile
 constexpr int NTHREADS = 192;
+// EVA_SUMMARIES_FUSED: two more warps (6, 7) compute the chunk summaries in-kernel
+constexpr int NTHREADS_F = 256;
+constexpr int SUMM_THREADS_F = 64;
 constexpr uint32_t TMEM_COLS = 256;
 constexpr uint32_t TM_O = 128;
+
+// Exchange buffers of the fused summaries (fused_summaries below).
+template <int D>
+struct alignas(16) SummScratch {
+  float eps[8][D];   // draws of the owned chunks (at most 128 / 16)
+  float red[2][4][D];// per-warp partial column sums / weighted value sums, per chunk of the tile
+  float om[4][D];    // omega per chunk of the tile
+  float p[64];       // softmax weight of each tile row
+  float l[4];        // softmax denominator per chunk
+  float st[2][2];    // C = 64: per-warp max / sum
+};
 
 // NSTAGE < 10: NSTAGE K and NSTAGE V slots.  NSTAGE = 10*NSK + NSV: separate ring depths
 // (a deeper K ring lets the next K tiles stream in earlier; K is consumed one softmax period
@@ -58,6 +74,24 @@ struct __align__(1024) Smem {
   uint64_t k_full[NSK], v_full[NSV], k_empty[NSK], v_empty[NSV];
   uint64_t s_full[2], p_full[2], o_done, o_final;
   uint32_t tmem_base;
+  SummScratch<D> summ;  // fused summaries' exchange buffers
+  int ticket;           // fused: the CTA's query tile ticket and the launch epoch
+  uint32_t epoch;
+};
+
+// Arguments of the in-kernel summaries (EVA_SUMMARIES_FUSED).  ws: [ticket, done, epoch, pad,
+// flags[units * n_qt]] (fused_workspace); Ksum/Vsum are written with generic stores and read
+// back by other CTAs through TMA once the owning tile's flag holds epoch + 1.
+struct FusedArgs {
+  eva_config cfg;
+  const __nv_bfloat16* K;  // [units, T, D]: the summaries read their rows from global memory
+  const __nv_bfloat16* V;
+  int64_t T;
+  __nv_bfloat16* ks;
+  __nv_bfloat16* vs;
+  const float* eps;
+  uint32_t* ws;
+  int nC, n_qt, units, total, order;
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -108,34 +142,36 @@ __device__ __forceinline__ void softmax_tile_mx(uint32_t s_addr, uint32_t o_addr
     const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
     wait_o();
     tc_fence_after();
-#pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t o[32];
-      tmem_ld32(o_addr + cc * 32, o);
+    // 8 columns at a time: S (64 registers) stays live across the rescale
+#pragma unroll 1
+    for (int cc = 0; cc < D / 8; ++cc) {
+      uint32_t o[8];
+      tmem_ld8(o_addr + cc * 8, o);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-      tmem_st32(o_addr + cc * 32, o);
+      for (int i = 0; i < 8; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
+      tmem_st8(o_addr + cc * 8, o);
     }
     tmem_wait_st();
     l *= f;
   }
   if (grow) m_ref = mx;
   const float neg = (m_ref == -INFINITY ? 0.f : -m_ref) + bias2;
-  uint32_t pk[32];
   float ls[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) ls[i] = 0.f;
+  // P packed in place: pair c lands in sr[c] after sr[2c], sr[2c+1] are read (no second array,
+  // so S, P and O's rescale fit the fused kernel's 128-register budget without spilling)
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
     const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg));
     const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg));
     ls[(2 * c) & 7] += p0;
     ls[(2 * c + 1) & 7] += p1;
-    pk[c] = pack_bf16(p0, p1);
+    sr[c] = pack_bf16(p0, p1);
   }
   l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-  tmem_st32(s_addr, pk);
+  tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
   tmem_wait_st();
   tc_fence_before();
 }
@@ -215,18 +251,18 @@ __device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, 
     wait_o();
     tc_fence_after();
     const uint64_t f2 = f2pack(f, f);
-#pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t o[32];
-      tmem_ld32(o_addr + cc * 32, o);
+#pragma unroll 1
+    for (int cc = 0; cc < D / 8; ++cc) {
+      uint32_t o[8];
+      tmem_ld8(o_addr + cc * 8, o);
       tmem_wait_ld();
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
+      for (int i = 0; i < 8; i += 2) {
         const uint64_t v = ffma2(f2pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), f2, 0ull);
         o[i] = (uint32_t)v;
         o[i + 1] = (uint32_t)(v >> 32);
       }
-      tmem_st32(o_addr + cc * 32, o);
+      tmem_st8(o_addr + cc * 8, o);
     }
     tmem_wait_st();
     l *= f;
@@ -234,7 +270,6 @@ __device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, 
   if (grow) m_ref = mx;
   const float neg = (m_ref == -INFINITY ? 0.f : -m_ref) + bias2;
   const uint64_t sc2 = f2pack(scale_log2, scale_log2), ng2 = f2pack(neg, neg);
-  uint32_t pk[32];
   uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
@@ -246,37 +281,22 @@ __device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, 
       p = f2pack(ex2(f2lo(x)), ex2(f2hi(x)));
     }
     ls[c & 3] = fadd2(ls[c & 3], p);
-    pk[c] = pack_bf16(f2lo(p), f2hi(p));
+    sr[c] = pack_bf16(f2lo(p), f2hi(p));
   }
   const uint64_t s2 = fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3]));
   l += f2lo(s2) + f2hi(s2);
-  tmem_st32(s_addr, pk);
+  tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
   tmem_wait_st();
   tc_fence_before();
 }
 
-struct TilePlan {
-  int n0, nlast, n_st, n_lt, lo0;
-  __device__ TilePlan(int qt, int T, int C, int W, int mode) {
-    n0 = qt * BM;
-    nlast = min(n0 + BM - 1, T - 1);
-    const Range rf = mask_range(n0, C, W, mode), rl = mask_range(nlast, C, W, mode);
-    n_st = (int)((rl.nsum + BN - 1) / BN);
-    lo0 = (int)rf.lo;
-    n_lt = (nlast - lo0 + 1 + BN - 1) / BN;
-  }
-  __device__ int count() const { return n_st + n_lt; }
-  __device__ bool summary(int j) const { return j < n_st; }
-  __device__ int base(int j) const { return j < n_st ? j * BN : lo0 + (j - n_st) * BN; }
-};
-
-// TilePlan of a query-range call (eva_attn_prefill_range): query tile qt covers absolute
+// Tile plan of a query-range call (eva_attn_prefill_range): query tile qt covers absolute
 // positions [q0 + qt*BM, ...), local key tiles start at lo(n0) (absolute); row() maps a
 // tile base to the TMA row of its tensor (key rows are stored from position k0).
 struct RangePlan {
   int64_t n0, nlast, lo0, k0;
   int n_st, n_lt;
-  __device__ RangePlan(int qt, const PrefillRange& rg, int C, int W, int mode) {
+  __device__ RangePlan(int qt, const PrefillRange& rg, int C, int W, int mode, bool fused = false) {
     const int64_t qend = rg.q0 + rg.nq;
     n0 = rg.q0 + (int64_t)qt * BM;
     nlast = min(n0 + BM - 1, qend - 1);
@@ -287,20 +307,39 @@ struct RangePlan {
     lo0 = vf.lo;
     k0 = rg.k0;
     n_lt = (int)((vl.hi - lo0 + BN - 1) / BN);
+    if (fused) {
+      order = 2;
+      rot = (int)((n0 - lo0) / BN);
+      s_end = vl.s1;
+    }
   }
-  // Tile order: local tiles first, then the summary tiles (sum_first = 0) -- the local span
+  // Tile order: local tiles first, then the summary tiles (order 0) -- the local span
   // depends only on the inputs, so with EVA_PREFILL_OVERLAP it runs while the summarize
-  // kernel is still finishing -- or summaries first (sum_first = 1).
-  int sum_first = 0;
+  // kernel is still finishing -- or summaries first (order 1).  Order 2 (fused summaries):
+  // the local tiles rotated to start at the tile holding n0 (the tiles whose chunks this CTA
+  // summarises come first), then the summary tiles aligned to END at nsum(n_last) -- the
+  // first may start at a negative chunk (TMA zero-fills it; masked) -- so no row of a summary
+  // tile is a chunk that is not complete and published yet.
+  int order = 0, rot = 0;
+  int64_t s_end = 0;
   __device__ int count() const { return n_st + n_lt; }
-  __device__ bool summary(int j) const { return sum_first ? j < n_st : j >= n_lt; }
+  __device__ bool summary(int j) const { return order == 1 ? j < n_st : j >= n_lt; }
+  __device__ int local_index(int j) const {  // local tile (0..n_lt-1) walked at step j
+    if (order == 1) return j - n_st;
+    if (order == 2) return (j + rot) % n_lt;
+    return j;
+  }
   __device__ int64_t base(int j) const {
-    if (sum_first) return j < n_st ? (int64_t)j * BN : lo0 + (int64_t)(j - n_st) * BN;
-    return j >= n_lt ? (int64_t)(j - n_lt) * BN : lo0 + (int64_t)j * BN;
+    if (summary(j)) {
+      if (order == 1) return (int64_t)j * BN;
+      if (order == 2) return s_end - (int64_t)(n_st - (j - n_lt)) * BN;
+      return (int64_t)(j - n_lt) * BN;
+    }
+    return lo0 + (int64_t)local_index(j) * BN;
   }
   __device__ int row(int j) const {
-    if (sum_first) return j < n_st ? j * BN : (int)(lo0 - k0) + (j - n_st) * BN;
-    return j >= n_lt ? (j - n_lt) * BN : (int)(lo0 - k0) + j * BN;
+    const int64_t b = base(j);
+    return summary(j) ? (int)b : (int)(b - k0);
   }
 };
 
@@ -310,9 +349,11 @@ struct RangePlan {
 // memory and flush them to g_trace2 at exit.  Roles: 0 producer, 1 MMA, 2 softmax (warp 2
 // lane 0).  kinds: 1 start, 2 Q arrived (MMA), 3 k_full(j) (MMA), 4 S(j) issued, 5 P(j)
 // received (MMA), 6 PV(j) issued, 7 softmax got S(j), 8 softmax P(j) done, 9 o_final
-// (epilogue start), 10 epilogue done, 11 producer slot free (j), 12 producer issued (j).
+// (epilogue start), 10 epilogue done, 11 producer slot free (j), 12 producer issued (j);
+// fused: 16 producer starts waiting for the summary flags, 17 flags ready; role 3 (summary
+// warps): 13 owned tile j landed, 14 tile j summarised and released, 15 flag published.
 __device__ unsigned long long* g_trace2 = nullptr;
-constexpr int TT_ROLES = 3, TT_PER_ROLE = 48, TT_SLOTS = 4;
+constexpr int TT_ROLES = 4, TT_PER_ROLE = 48;
 struct TileTrace {
   unsigned long long ev[TT_ROLES][TT_PER_ROLE];
   int n[TT_ROLES];
@@ -332,31 +373,256 @@ __device__ __forceinline__ void tt(TileTrace* tl, int role, int kind, int j) {
   }
 }
 
-template <int D, int NSTAGE, bool TRACE = false, int SMX = -1>
-__global__ void __launch_bounds__(NTHREADS, 2)
+// ---- in-kernel chunk summaries (EVA_SUMMARIES_FUSED), run by warps 6 and 7 of the tile kernel.
+// The CTA of query tile qt owns the complete chunks inside its own query rows [n0, n_last]
+// (C in {16, 32, 64}; each lies inside one 64-key tile of the local span, which starts on a
+// chunk boundary).  Per chunk c (formulas of summarize.cuh / eva.h eva_summarize):
+//   k~_c    = (1/C) sum_i k_{cC+i}                      P:99 Eq.10 (reading R1)
+//   omega_c = lambda * clip(k~_c + eps_c)                P:311-314 Eq.15 (R2, R3)
+//   a_i     = omega_c . k_i - |k_i|^2 / 2                log xi
+//   beta^_c = sum_i softmax(a)_i v_i                     P:92 Eq.9, S = 1
+// The owned rows are read from the K/V tiles the producer lands in shared memory for the
+// attention anyway (the walk starts with them, order 2); the summary side releases a slot as
+// soon as it is done with it.  The code is kept small and rolled on purpose: it runs a few
+// times per CTA next to the softmax loop, and unrolled it would stream from the instruction
+// cache (measured: the unrolled form spent most of its time waiting for instructions).
+//   0. at start: the random draws of every owned chunk (data-independent) into shared memory;
+//   1. column sums: thread t sums the 16-byte piece pc = t % TPR of rows g, g + RPP, ...
+//      (g = t / TPR, RPP = 64 / TPR) straight from bf16 (FHADD.BF16), reduced over g by
+//      shuffles and across the two warps through shared memory -> k~, omega per chunk;
+//   2. logits: thread t takes tile row t against its chunk's omega; max / sum over the chunk
+//      by shuffles (C <= 32) or across the warps (C = 64) -> softmax weights in shared memory;
+//   3. beta^: thread t accumulates weight x value piece over its rows, reduced like pass 1.
+// After the last owned chunk the tile's ready flag is set to epoch + 1 (release, after a proxy
+// fence: the readers load the rows by TMA).
+
+// fp32 += bf16 (low / high half of a packed pair): FHADD.BF16, no unpacking
+__device__ __forceinline__ float add_bf16lo(float acc, uint32_t w) {
+  asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(acc) : "h"((unsigned short)(w & 0xffffu)));
+  return acc;
+}
+__device__ __forceinline__ float add_bf16hi(float acc, uint32_t w) {
+  asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(acc) : "h"((unsigned short)(w >> 16)));
+  return acc;
+}
+
+template <int D, int CC, bool TRACE, typename SM, typename Plan>
+__device__ __noinline__ void fused_summaries(SM* sm, const Plan& plan, const FusedArgs& fa, int u, int qt,
+                                             uint32_t epoch, TileTrace* tl) {
+  constexpr int NSK = SM::NSK, NSV = SM::NSV;
+  constexpr int TPR = D / 8, RPP = SUMM_THREADS_F / TPR;  // pieces per row, rows per pass
+  constexpr int NRC = CC / RPP, NCH = BN / CC;            // rows per thread per chunk, chunks per tile
+  static_assert(CC % RPP == 0 && NCH <= 4, "chunk size outside the fused envelope");
+  SummScratch<D>& sc = sm->summ;
+  const int t = threadIdx.x - (NTHREADS_F - SUMM_THREADS_F), w = t >> 5, lane = t & 31;
+  const int pc = t % TPR, g = t / TPR;
+  const int64_t c_lo = plan.n0 / CC, c_hi = min((int64_t)fa.nC, (plan.nlast + 1) / CC);
+  const uint32_t bh = (uint32_t)(fa.cfg.bh_begin + u);
+  const uint32_t poff = (uint32_t)((pc >> 3) * (BN * 128)), c16 = (uint32_t)(pc & 7);
+  if (t == 0) tt<TRACE>(tl, 3, 13, 0);
+  // 0. the draws of the owned chunks: thread t does 4 channels per step
+#pragma unroll 1
+  for (int i = t; i < (int)(c_hi - c_lo) * (D / 4); i += SUMM_THREADS_F) {
+    const int64_t c = c_lo + i / (D / 4);
+    const int q = i % (D / 4);
+    float4 z;
+    if (fa.eps) z = __ldg(reinterpret_cast<const float4*>(fa.eps + ((size_t)u * fa.nC + (size_t)c) * D) + q);
+    else z = philox_normal4(fa.cfg.seed, fa.cfg.layer, bh, (uint32_t)c, (uint32_t)q);
+    *reinterpret_cast<float4*>(&sc.eps[c - c_lo][4 * q]) = z;
+  }
+  named_bar_sync(2, SUMM_THREADS_F);
+  for (int j = 0; j < plan.n_lt; ++j) {
+    const int64_t b = plan.base(j);  // a multiple of CC
+    const int64_t ca = max(c_lo, b / CC), cb = min(c_hi, (b + BN) / CC);
+    if (ca >= cb) break;  // the owned tiles are a prefix of the walk (order 2)
+    const int sk = j % NSK, sv = j % NSV;
+    const int64_t c0 = b / CC;
+    mbar_wait(&sm->k_full[sk], (j / NSK) & 1);
+    const uint8_t* kt = reinterpret_cast<const uint8_t*>(sm->k[sk]);
+    // 1. column sums of every chunk of the tile
+#pragma unroll 1
+    for (int q = 0; q < NCH; ++q) {
+      float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int k = 0; k < NRC; ++k) {
+        const int r = q * CC + g + k * RPP;
+        const uint4 x = *reinterpret_cast<const uint4*>(kt + poff + r * 128 + ((c16 ^ (uint32_t)(r & 7)) << 4));
+        cs[0] = add_bf16lo(cs[0], x.x); cs[1] = add_bf16hi(cs[1], x.x);
+        cs[2] = add_bf16lo(cs[2], x.y); cs[3] = add_bf16hi(cs[3], x.y);
+        cs[4] = add_bf16lo(cs[4], x.z); cs[5] = add_bf16hi(cs[5], x.z);
+        cs[6] = add_bf16lo(cs[6], x.w); cs[7] = add_bf16hi(cs[7], x.w);
+      }
+#pragma unroll
+      for (int o = TPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cs[i] += __shfl_xor_sync(0xffffffffu, cs[i], o);
+      if (lane < TPR) {
+        float4* dst = reinterpret_cast<float4*>(&sc.red[w][q][pc * 8]);
+        dst[0] = make_float4(cs[0], cs[1], cs[2], cs[3]);
+        dst[1] = make_float4(cs[4], cs[5], cs[6], cs[7]);
+      }
+    }
+    named_bar_sync(2, SUMM_THREADS_F);
+    // k~ and omega: thread t does channel pairs of chunk q
+#pragma unroll 1
+    for (int i = t; i < NCH * (D / 2); i += SUMM_THREADS_F) {
+      const int q = i / (D / 2), ch = 2 * (i % (D / 2));
+      const int64_t c = c0 + q;
+      const bool own = c >= ca && c < cb;
+      float k2[2], o2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        k2[h] = (sc.red[0][q][ch + h] + sc.red[1][q][ch + h]) * (1.0f / (float)CC);
+        const float e = own ? sc.eps[c - c_lo][ch + h] : 0.f;
+        o2[h] = omega_of(k2[h], e, fa.cfg);
+      }
+      sc.om[q][ch] = o2[0];
+      sc.om[q][ch + 1] = o2[1];
+      if (own) *reinterpret_cast<uint32_t*>(fa.ks + ((size_t)u * fa.nC + (size_t)c) * D + ch) = pack_bf16(k2[0], k2[1]);
+    }
+    named_bar_sync(2, SUMM_THREADS_F);
+    // 2. the logit of tile row t; softmax over its chunk
+    {
+      const int q = t / CC;
+      float a4[4] = {0.f, 0.f, 0.f, 0.f};
+      const uint8_t* rowp = kt + t * 128;
+#pragma unroll 4
+      for (int pp = 0; pp < TPR; ++pp) {
+        const uint4 x = *reinterpret_cast<const uint4*>(rowp + (pp >> 3) * (BN * 128) + ((((uint32_t)pp & 7u) ^ (uint32_t)(t & 7)) << 4));
+        const float4 o0 = *reinterpret_cast<const float4*>(&sc.om[q][pp * 8]);
+        const float4 o1 = *reinterpret_cast<const float4*>(&sc.om[q][pp * 8 + 4]);
+        float f[8];
+        unpack16<__nv_bfloat16>(x, f);
+        float& a = a4[pp & 3];
+        a = fmaf(f[0], o0.x - 0.5f * f[0], a); a = fmaf(f[1], o0.y - 0.5f * f[1], a);
+        a = fmaf(f[2], o0.z - 0.5f * f[2], a); a = fmaf(f[3], o0.w - 0.5f * f[3], a);
+        a = fmaf(f[4], o1.x - 0.5f * f[4], a); a = fmaf(f[5], o1.y - 0.5f * f[5], a);
+        a = fmaf(f[6], o1.z - 0.5f * f[6], a); a = fmaf(f[7], o1.w - 0.5f * f[7], a);
+      }
+      const float a = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      float m = a;
+      constexpr int WR = CC < 32 ? CC : 32;
+#pragma unroll
+      for (int o = 1; o < WR; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if constexpr (CC == 64) {
+        if (lane == 0) sc.st[0][w] = m;
+        named_bar_sync(2, SUMM_THREADS_F);
+        m = fmaxf(sc.st[0][0], sc.st[0][1]);
+      }
+      const float pr = __expf(a - m);
+      sc.p[t] = pr;
+      float l = pr;
+#pragma unroll
+      for (int o = 1; o < WR; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+      if constexpr (CC == 64) {
+        if (lane == 0) sc.st[1][w] = l;
+      } else {
+        if ((t & (CC - 1)) == 0) sc.l[q] = l;
+      }
+    }
+    named_bar_sync(2, SUMM_THREADS_F);
+    if (t == 0) {
+      mbar_arrive(&sm->k_empty[sk]);
+      tt<TRACE>(tl, 3, 20, j);
+    }
+    mbar_wait(&sm->v_full[sv], (j / NSV) & 1);
+    const uint8_t* vt = reinterpret_cast<const uint8_t*>(sm->v[sv]);
+    // 3. beta^ partial sums of every chunk
+#pragma unroll 1
+    for (int q = 0; q < NCH; ++q) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int k = 0; k < NRC; ++k) {
+        const int r = q * CC + g + k * RPP;
+        const uint4 x = *reinterpret_cast<const uint4*>(vt + poff + r * 128 + ((c16 ^ (uint32_t)(r & 7)) << 4));
+        const float pr = sc.p[r];
+        float f[8];
+        unpack16<__nv_bfloat16>(x, f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(pr, f[i], acc[i]);
+      }
+#pragma unroll
+      for (int o = TPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+      if (lane < TPR) {
+        float4* dst = reinterpret_cast<float4*>(&sc.red[w][q][pc * 8]);
+        dst[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        dst[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
+    }
+    named_bar_sync(2, SUMM_THREADS_F);
+    if (t == 0) mbar_arrive(&sm->v_empty[sv]);
+#pragma unroll 1
+    for (int i = t; i < NCH * (D / 2); i += SUMM_THREADS_F) {
+      const int q = i / (D / 2), ch = 2 * (i % (D / 2));
+      const int64_t c = c0 + q;
+      if (c >= ca && c < cb) {
+        const float il = 1.0f / (CC == 64 ? sc.st[1][0] + sc.st[1][1] : sc.l[q]);
+        const float y0 = (sc.red[0][q][ch] + sc.red[1][q][ch]) * il;
+        const float y1 = (sc.red[0][q][ch + 1] + sc.red[1][q][ch + 1]) * il;
+        *reinterpret_cast<uint32_t*>(fa.vs + ((size_t)u * fa.nC + (size_t)c) * D + ch) = pack_bf16(y0, y1);
+      }
+    }
+    named_bar_sync(2, SUMM_THREADS_F);  // the exchange buffers are reused by the next tile
+    if (t == 0) tt<TRACE>(tl, 3, 14, j);
+  }
+  // publish: the owned summaries are complete
+  fence_proxy_async_global();
+  named_bar_sync(2, SUMM_THREADS_F);
+  if (t == 0) {
+    __threadfence();
+    st_release_gpu(fa.ws + 4 + (size_t)u * fa.n_qt + qt, epoch + 1u);
+    tt<TRACE>(tl, 3, 15, 0);
+  }
+}
+
+// Does walk step j (a local tile) hold a chunk the CTA summarises?  (order 2)
+template <typename Plan>
+__device__ __forceinline__ bool owns_chunks(const Plan& plan, int j, int C, int nC) {
+  if (plan.summary(j)) return false;
+  const int64_t b = plan.base(j);
+  const int64_t c_lo = plan.n0 / C, c_hi = min((int64_t)nC, (plan.nlast + 1) / C);
+  return max(c_lo, b / C) < min(c_hi, (b + BN) / C);
+}
+
+// FC = 0: summaries provided (or computed by a separate launch); FC = C in {16, 32, 64}: the
+// chunk summaries are computed in-kernel (one instantiation per chunk size keeps the code that
+// the instruction cache has to hold small)
+template <int D, int NSTAGE, bool TRACE = false, int SMX = -1, int FC = 0>
+__global__ void __launch_bounds__(FC ? NTHREADS_F : NTHREADS, 2)
 prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
                      const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
                      const PrefillRange rg, int C, int W, int mode, float scale_log2,
-                     float bias_log2, float* __restrict__ lse, int overlap, int overlap_order_sum_first) {
+                     float bias_log2, float* __restrict__ lse, int overlap, int overlap_order_sum_first,
+                     const __grid_constant__ FusedArgs fa) {
+  constexpr bool FUSED = FC != 0;
   extern __shared__ uint8_t smem_raw[];
   using SM = Smem<D, NSTAGE>;
   constexpr int NSK = SM::NSK, NSV = SM::NSV;
   if constexpr (SM::PAD == 0) {
     if ((reinterpret_cast<uintptr_t>(smem_raw) & 1023) != 0) __trap();
   }
-  SM* sm = reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB aligned by an offset from smem_raw (not an integer round trip), so the compiler keeps
+  // every access through sm in the shared window (LDS/STS, not generic loads)
+  SM* sm = reinterpret_cast<SM*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.y;
-  RangePlan plan(blockIdx.x, rg, C, W, mode);
-  plan.sum_first = overlap ? 0 : (overlap_order_sum_first ? 1 : 0);
-  const int qrow = blockIdx.x * BM;  // TMA row of this query tile in Q / O
-  const int NT = plan.count();
   TileTrace* tl = nullptr;
   if constexpr (TRACE) {
     __shared__ TileTrace tlog_s;
     tl = &tlog_s;
     if (threadIdx.x < TT_ROLES) tl->n[threadIdx.x] = 0;
+  }
+  if constexpr (FUSED) {
+    // Fused: query tiles are handed out by a monotone ticket, so every tile whose summaries a
+    // CTA waits for (the same unit's tiles <= its own) belongs to a CTA that is already
+    // resident -- and that CTA publishes them after its own local tiles, which wait on nobody.
+    pdl_wait();  // the workspace counters of the previous launch on this stream are final
+    if (threadIdx.x == 0) {
+      sm->ticket = (int)atomicAdd(fa.ws, 1u);
+      sm->epoch = *reinterpret_cast<volatile uint32_t*>(fa.ws + 2);
+    }
   }
 
   if (warp == 0 && lane == 0) {
@@ -365,11 +631,13 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     mbar_init(&sm->q_full, 1);
     for (int s = 0; s < NSK; ++s) {
       mbar_init(&sm->k_full[s], 1);
-      mbar_init(&sm->k_empty[s], 1);
+      // fused: + the summary side's release (by the summary warps for a tile with owned
+      // chunks, by the producer at issue otherwise)
+      mbar_init(&sm->k_empty[s], FUSED ? 2 : 1);
     }
     for (int s = 0; s < NSV; ++s) {
       mbar_init(&sm->v_full[s], 1);
-      mbar_init(&sm->v_empty[s], 1);
+      mbar_init(&sm->v_empty[s], FUSED ? 2 : 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sm->s_full[b], 1);
@@ -387,11 +655,32 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm->tmem_base;
+  int qt = blockIdx.x, u = blockIdx.y;
+  uint32_t epoch = 0;
+  if constexpr (FUSED) {
+    // fa.order 1 (default): tile-major -- the tiles whose summaries a tile reads were
+    // dispatched a row of units earlier (measured 1.20 ms at configs[2], though the K/V reuse
+    // distance grows to a wave: +0.8 GB of DRAM reads); 0: unit-major -- a unit's tiles run
+    // close together and share its K/V and summaries in L2 (1.61 GB), but a tile then waits
+    // for its neighbours' summaries (1.65 ms)
+    if (fa.order) {
+      qt = sm->ticket / fa.units;
+      u = sm->ticket % fa.units;
+    } else {
+      qt = sm->ticket % fa.n_qt;
+      u = sm->ticket / fa.n_qt;
+    }
+    epoch = sm->epoch;
+  }
+  RangePlan plan(qt, rg, C, W, mode, FUSED);
+  if constexpr (!FUSED) plan.order = overlap ? 0 : (overlap_order_sum_first ? 1 : 0);
+  const int qrow = qt * BM;  // TMA row of this query tile in Q / O
+  const int NT = plan.count();
   // PDL: by default every thread waits for the previous grid here.  With `overlap` (the
   // previous grid is the eva_summarize producing Ksum/Vsum and Q, K, V were complete before
   // it) only the producer waits, right before its first summary-tile access, so the local
   // tiles (processed first) overlap the summarize kernel's tail.
-  if (!overlap) pdl_wait();
+  if (!FUSED && !overlap) pdl_wait();
   pdl_trigger();
   if (threadIdx.x == 0) tt<TRACE>(tl, 0, 1, 0);
 
@@ -405,10 +694,32 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, qrow, u);
     }
     __syncwarp();
-    bool waited = !overlap;
+    bool waited = !overlap && !FUSED;
     auto wait_summaries = [&](int j) {
       if (!waited && plan.summary(j)) {
-        pdl_wait();
+        if constexpr (FUSED) {
+          // chunks [0, nsum(n_last)) are read: wait for the flags of their owner tiles
+          // (tile of chunk c = ((c+1)C - 1) / 128 <= qt), all lanes polling in parallel
+          if (lane == 0) tt<TRACE>(tl, 0, 16, j);
+          if (plan.s_end > 0) {
+            const int last = (int)((plan.s_end * C - 1) / BM);
+            const uint32_t* fl = fa.ws + 4 + (size_t)u * fa.n_qt;
+            for (int i = lane; i <= last; i += 32) {
+              const uint64_t t0 = globaltimer_ns();
+              while (ld_relaxed_gpu(fl + i) != epoch + 1u) {
+                __nanosleep(32);
+                // watchdog: a flag that never comes is a bug -- fail the launch, never hang the GPU
+                if (globaltimer_ns() - t0 > 2000000000ull) __trap();
+              }
+            }
+          }
+          __syncwarp();
+          __threadfence();  // acquire: order the summary reads after the flags seen above
+          fence_proxy_async_global();
+          if (lane == 0) tt<TRACE>(tl, 0, 17, j);
+        } else {
+          pdl_wait();
+        }
         waited = true;
       }
     };
@@ -441,6 +752,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
         for (int kb = 0; kb < D / 64; ++kb)
           tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, plan.row(j), u);
+        if (FUSED && !owns_chunks(plan, j, C, fa.nC)) mbar_arrive(&sm->k_empty[s]);  // summary side
       }
       __syncwarp();
       if (lane == 0) tt<TRACE>(tl, 0, 12, j);
@@ -454,16 +766,30 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
         for (int kb = 0; kb < D / 64; ++kb)
           tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, plan.row(j), u);
+        if (FUSED && !owns_chunks(plan, j, C, fa.nC)) mbar_arrive(&sm->v_empty[s]);
       }
       __syncwarp();
     };
+    // Fused: every local tile's K AND V are issued before the first summary-tile load waits for
+    // the ready flags -- that wait may be on this CTA's own summaries (W = C), which need them.
+    auto sum_next = [&](int j) { return FUSED && j + 1 < NT && plan.summary(j + 1) && !plan.summary(j); };
     load_k(0);
-    if (NT > 1) load_k(1);
-    load_v(0);
+    if (sum_next(0)) {
+      load_v(0);
+      load_k(1);
+    } else {
+      if (NT > 1) load_k(1);
+      load_v(0);
+    }
     prefetch_rest();  // after the first tiles: they are on the critical path
     for (int j = 1; j < NT; ++j) {
-      if (j + 1 < NT) load_k(j + 1);
-      load_v(j);
+      if (sum_next(j)) {
+        load_v(j);
+        load_k(j + 1);
+      } else {
+        if (j + 1 < NT) load_k(j + 1);
+        load_v(j);
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -516,7 +842,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         if (lane == 0) tt<TRACE>(tl, 1, 6, jj);
       }
     }
-  } else {
+  } else if (warp < 6) {
     // ------------------------------------------------------------ softmax warps
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
@@ -534,7 +860,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       int vlo, vhi, xlo = 0, xhi = 0;
       float bias2 = 0.f;
       if (plan.summary(j)) {
-        vlo = 0;
+        vlo = (int)max((int64_t)0, -base);  // order 2: rows before chunk 0 are zero-filled
         if (mode == EVA_NONCAUSAL) {  // every summary except those of the row's own block
           vhi = (int)min((int64_t)BN, (int64_t)rg.nsl - base);
           xlo = (int)max((int64_t)-1, min((int64_t)BN, rr.s1 - base));
@@ -589,6 +915,9 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       tma_store_wait_read();
       tt<TRACE>(tl, 2, 10, 0);
     }
+  } else {
+    // ------------------------------------------------------------ summary warps (fused)
+    if constexpr (FUSED) fused_summaries<D, FC, TRACE>(sm, plan, fa, u, qt, epoch, tl);
   }
   tc_fence_before();
   __syncthreads();
@@ -601,1206 +930,20 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       }
     }
   }
+  if constexpr (FUSED) {
+    // the last CTA to finish resets the ticket and done counters and advances the epoch
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const uint32_t d = atomicAdd(fa.ws + 1, 1u);
+      if (d == (uint32_t)fa.total - 1u) {
+        fa.ws[0] = 0u;
+        fa.ws[1] = 0u;
+        __threadfence();
+        fa.ws[2] = epoch + 1u;
+      }
+    }
+  }
   if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
-}
-
-// ========================================================================== persistent tile kernel
-// The one-tile-per-CTA kernel made persistent: two CTAs per SM walk the (unit, query tile)
-// items w = blockIdx.x, + gridDim.x, ...  Ring indices and barrier phases run on global
-// counters across items, so the next item's Q (released by the last S MMA of the current
-// item), K/V tiles and first S MMAs stream in while the current item finishes; O is drained
-// from TMEM by the softmax warps (o_free releases it for the next item's first PV) and
-// written straight from registers (no smem staging, so Q's buffer is never shared).
-template <int D, int NSTAGE>
-struct __align__(1024) SmemP {
-  static constexpr int NSK = NSTAGE >= 10 ? NSTAGE / 10 : NSTAGE;
-  static constexpr int NSV = NSTAGE >= 10 ? NSTAGE % 10 : NSTAGE;
-  __nv_bfloat16 q[BM * D];
-  __nv_bfloat16 k[NSK][BN * D];
-  __nv_bfloat16 v[NSV][BN * D];
-  uint64_t q_full, q_empty;
-  uint64_t k_full[NSK], v_full[NSV], k_empty[NSK], v_empty[NSV];
-  uint64_t s_full[2], p_full[2], o_done, o_final, o_free;
-  uint32_t tmem_base;
-};
-
-template <int D, int NSTAGE>
-__global__ void __launch_bounds__(NTHREADS, 2)
-prefill_persist_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
-                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
-                       const __grid_constant__ CUtensorMap mVs, const PrefillRange rg, int C, int W, int mode,
-                       float scale_log2, float bias_log2, float* __restrict__ lse, __nv_bfloat16* __restrict__ O,
-                       int n_qt, int n_items) {
-  extern __shared__ uint8_t smem_raw[];
-  using SM = SmemP<D, NSTAGE>;
-  constexpr int NSK = SM::NSK, NSV = SM::NSV;
-  SM* sm = reinterpret_cast<SM*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto plan_of = [&](int w) {
-    RangePlan p(w % n_qt, rg, C, W, mode);
-    p.sum_first = 1;
-    return p;
-  };
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
-    tma_prefetch(&mKs); tma_prefetch(&mVs);
-    mbar_init(&sm->q_full, 1);
-    mbar_init(&sm->q_empty, 1);
-    for (int s = 0; s < NSK; ++s) {
-      mbar_init(&sm->k_full[s], 1);
-      mbar_init(&sm->k_empty[s], 1);
-    }
-    for (int s = 0; s < NSV; ++s) {
-      mbar_init(&sm->v_full[s], 1);
-      mbar_init(&sm->v_empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm->s_full[b], 1);
-      mbar_init(&sm->p_full[b], 128);
-    }
-    mbar_init(&sm->o_done, 1);
-    mbar_init(&sm->o_final, 1);
-    mbar_init(&sm->o_free, 128);
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    tmem_alloc(&sm->tmem_base, TMEM_COLS);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = sm->tmem_base;
-  pdl_wait();
-  pdl_trigger();
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    int tk = 0, tv = 0, ic = 0;  // global K tile, V tile and item counters
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ic) {
-      const RangePlan plan = plan_of(w);
-      const int u = w / n_qt, qrow = (w % n_qt) * BM, NT = plan.count();
-      if (ic > 0) mbar_wait(&sm->q_empty, (ic - 1) & 1);  // the last item's S MMAs are done
-      if (elect_one()) {
-        mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
-        for (int kb = 0; kb < D / 64; ++kb) tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, qrow, u);
-        for (int j = 2; j < NT; ++j) {
-          const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
-          const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
-          for (int kb = 0; kb < D / 64; ++kb) {
-            tma_prefetch_l2_3d(mk, kb * 64, plan.row(j), u);
-            tma_prefetch_l2_3d(mv, kb * 64, plan.row(j), u);
-          }
-        }
-      }
-      __syncwarp();
-      auto load_k = [&](int j) {
-        const int t = tk + j, s = t % NSK;
-        if (t >= NSK) mbar_wait(&sm->k_empty[s], ((t / NSK) - 1) & 1);
-        const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
-          for (int kb = 0; kb < D / 64; ++kb)
-            tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, plan.row(j), u);
-        }
-        __syncwarp();
-      };
-      auto load_v = [&](int j) {
-        const int t = tv + j, s = t % NSV;
-        if (t >= NSV) mbar_wait(&sm->v_empty[s], ((t / NSV) - 1) & 1);
-        const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
-          for (int kb = 0; kb < D / 64; ++kb)
-            tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, plan.row(j), u);
-        }
-        __syncwarp();
-      };
-      load_k(0);
-      for (int j = 0; j < NT; ++j) {
-        if (j + 1 < NT) load_k(j + 1);
-        load_v(j);
-      }
-      tk += NT;
-      tv += NT;
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
-    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
-    const uint32_t q_addr = smem_u32(sm->q);
-    int t0 = 0, ic = 0;  // global tile counter at the item start, item counter
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ic) {
-      const int NT = plan_of(w).count();
-      mbar_wait(&sm->q_full, ic & 1);
-      for (int j = 0; j <= NT; ++j) {
-        if (j < NT) {
-          const int t = t0 + j, s = t % NSK;
-          mbar_wait(&sm->k_full[s], (t / NSK) & 1);
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(sm->k[s]);
-          const uint32_t d_tmem = tmem + (uint32_t)(t & 1) * BN;
-          if (elect_one()) {
-#pragma unroll
-            for (int ks = 0; ks < D / 16; ++ks) {
-              const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
-              mma_ss(d_tmem, smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024),
-                     smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
-            }
-            mma_commit(&sm->s_full[t & 1]);
-            mma_commit(&sm->k_empty[s]);
-            if (j == NT - 1) mma_commit(&sm->q_empty);  // Q is read by the S MMAs only
-          }
-          __syncwarp();
-        }
-        if (j >= 1) {
-          const int jj = j - 1, t = t0 + jj, s = t % NSV;
-          mbar_wait(&sm->p_full[t & 1], (t >> 1) & 1);
-          if (jj == 0 && ic > 0) mbar_wait(&sm->o_free, (ic - 1) & 1);  // last item's O drained
-          mbar_wait(&sm->v_full[s], (t / NSV) & 1);
-          tc_fence_after();
-          const uint32_t v_addr = smem_u32(sm->v[s]);
-          if (elect_one()) {
-#pragma unroll
-            for (int ks = 0; ks < BN / 16; ++ks) {
-              const uint32_t a_tmem = tmem + (uint32_t)(t & 1) * BN + ks * 8;
-              mma_ts(tmem + TM_O, a_tmem, smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024), idesc_o,
-                     (jj > 0 || ks > 0) ? 1u : 0u);
-            }
-            mma_commit(&sm->v_empty[s]);
-            mma_commit(&sm->o_done);
-            if (jj == NT - 1) mma_commit(&sm->o_final);
-          }
-          __syncwarp();
-        }
-      }
-      t0 += NT;
-    }
-  } else {
-    // ------------------------------------------------------------ softmax + epilogue warps
-    const int quad = warp & 3;
-    const int r = quad * 32 + lane;
-    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
-    const int64_t qend = rg.q0 + rg.nq;
-    int t0 = 0, ic = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++ic) {
-      const RangePlan plan = plan_of(w);
-      const int u = w / n_qt, NT = plan.count();
-      const int64_t n = plan.n0 + r;
-      const bool valid = n < qend;
-      const Vis rr = visible_set(valid ? n : plan.nlast, C, W, mode, qend);
-      float m_ref = -INFINITY, l = 0.f;
-      for (int j = 0; j < NT; ++j) {
-        const int t = t0 + j;
-        mbar_wait(&sm->s_full[t & 1], (t >> 1) & 1);
-        tc_fence_after();
-        const int64_t base = plan.base(j);
-        int vlo, vhi, xlo = 0, xhi = 0;
-        float bias2 = 0.f;
-        if (plan.summary(j)) {
-          vlo = 0;
-          if (mode == EVA_NONCAUSAL) {
-            vhi = (int)min((int64_t)BN, (int64_t)rg.nsl - base);
-            xlo = (int)max((int64_t)-1, min((int64_t)BN, rr.s1 - base));
-            xhi = (int)max((int64_t)-1, min((int64_t)BN, rr.s2 - base));
-          } else {
-            vhi = (int)min((int64_t)BN, rr.s1 - base);
-          }
-          bias2 = bias_log2;
-        } else {
-          vlo = (int)max((int64_t)0, rr.lo - base);
-          vhi = (int)min((int64_t)BN, rr.hi - base);
-        }
-        if (!valid) vhi = vlo;
-        softmax_tile_mx<D>(t_lane + (uint32_t)(t & 1) * BN, t_lane + TM_O, vlo, vhi, xlo, xhi, bias2, scale_log2,
-                           m_ref, l, [&] { mbar_wait(&sm->o_done, (t - 1) & 1); });
-        mbar_arrive(&sm->p_full[t & 1]);
-      }
-      // ---- epilogue: O / l straight from TMEM to global (this thread's row), lse
-      mbar_wait(&sm->o_final, ic & 1);
-      tc_fence_after();
-      const float inv_l = l > 0.f ? 1.0f / l : 0.f;
-      __nv_bfloat16* orow = O + ((size_t)u * rg.nq + (size_t)(valid ? n - rg.q0 : 0)) * D;
-#pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t o[32];
-        tmem_ld32(t_lane + TM_O + cc * 32, o);
-        tmem_wait_ld();
-        if (cc == D / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&sm->o_free);
-        }
-        if (valid) {
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            uint4 w4;
-            w4.x = pack_bf16(__uint_as_float(o[8 * g + 0]) * inv_l, __uint_as_float(o[8 * g + 1]) * inv_l);
-            w4.y = pack_bf16(__uint_as_float(o[8 * g + 2]) * inv_l, __uint_as_float(o[8 * g + 3]) * inv_l);
-            w4.z = pack_bf16(__uint_as_float(o[8 * g + 4]) * inv_l, __uint_as_float(o[8 * g + 5]) * inv_l);
-            w4.w = pack_bf16(__uint_as_float(o[8 * g + 6]) * inv_l, __uint_as_float(o[8 * g + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = w4;
-          }
-        }
-      }
-      if (valid && lse) lse[(size_t)u * rg.nq + (size_t)(n - rg.q0)] = (m_ref + __log2f(l)) * 0.69314718055994531f;
-      t0 += NT;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
-}
-
-// ========================================================================== split-softmax kernel
-// The tile kernel with 8 softmax warps: warps 2..5 own columns [0,32) of every 64-key S tile,
-// warps 6..9 columns [32,64), of the same 128 rows (warp w and w+4 share TMEM lane quadrant
-// w%4).  The two halves exchange their partial row max through shared memory (a 64-thread
-// named barrier per quadrant, double-buffered), so per-warp softmax work and latency halve.
-// Register budget: 2 CTAs x 320 threads per SM (<= 102 registers per thread).
-constexpr int NTHREADS2 = 320;
-
-template <int D, int NSTAGE>
-struct __align__(1024) Smem2 {
-  __nv_bfloat16 q[BM * D];
-  __nv_bfloat16 k[NSTAGE][BN * D];
-  __nv_bfloat16 v[NSTAGE][BN * D];
-  float xmax[2][2][BM];  // [tile parity][half][row]
-  float xsum[2][BM];
-  uint64_t q_full;
-  uint64_t k_full[NSTAGE], v_full[NSTAGE], k_empty[NSTAGE], v_empty[NSTAGE];
-  uint64_t s_full[2], p_full[2], o_done, o_final;
-  uint32_t tmem_base;
-};
-
-template <int D, int NSTAGE>
-__global__ void __launch_bounds__(NTHREADS2, 2)
-prefill_split_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
-                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
-                     const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
-                     int T, int C, int W, int mode, float scale_log2, float* __restrict__ lse) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem2<D, NSTAGE>* sm = reinterpret_cast<Smem2<D, NSTAGE>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.y;
-  const TilePlan plan(blockIdx.x, T, C, W, mode);
-  const int NT = plan.count();
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
-    tma_prefetch(&mKs); tma_prefetch(&mVs); tma_prefetch(&mO);
-    mbar_init(&sm->q_full, 1);
-    for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&sm->k_full[s], 1);
-      mbar_init(&sm->v_full[s], 1);
-      mbar_init(&sm->k_empty[s], 1);
-      mbar_init(&sm->v_empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm->s_full[b], 1);
-      mbar_init(&sm->p_full[b], 256);
-    }
-    mbar_init(&sm->o_done, 1);
-    mbar_init(&sm->o_final, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    tmem_alloc(&sm->tmem_base, TMEM_COLS);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = sm->tmem_base;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
-      mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
-      for (int kb = 0; kb < D / 64; ++kb)
-        tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
-    }
-    __syncwarp();
-    auto prefetch_rest = [&] {
-      if (elect_one()) {
-      for (int j = NSTAGE; j < NT; ++j) {
-        const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
-        const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
-        for (int kb = 0; kb < D / 64; ++kb) {
-          tma_prefetch_l2_3d(mk, kb * 64, plan.base(j), u);
-          tma_prefetch_l2_3d(mv, kb * 64, plan.base(j), u);
-        }
-      }
-      }
-      __syncwarp();
-    };
-    auto load_k = [&](int j) {
-      const int s = j % NSTAGE;
-      if (j >= NSTAGE) mbar_wait(&sm->k_empty[s], ((j / NSTAGE) - 1) & 1);
-      const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
-      if (elect_one()) {
-        mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
-        for (int kb = 0; kb < D / 64; ++kb)
-          tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, plan.base(j), u);
-      }
-      __syncwarp();
-    };
-    auto load_v = [&](int j) {
-      const int s = j % NSTAGE;
-      if (j >= NSTAGE) mbar_wait(&sm->v_empty[s], ((j / NSTAGE) - 1) & 1);
-      const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
-      if (elect_one()) {
-        mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
-        for (int kb = 0; kb < D / 64; ++kb)
-          tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, plan.base(j), u);
-      }
-      __syncwarp();
-    };
-    load_k(0);
-    if (NT > 1) load_k(1);
-    load_v(0);
-    prefetch_rest();  // after the first tiles: they are on the critical path
-    for (int j = 1; j < NT; ++j) {
-      if (j + 1 < NT) load_k(j + 1);
-      load_v(j);
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
-    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
-    const uint32_t q_addr = smem_u32(sm->q);
-    mbar_wait(&sm->q_full, 0);
-    for (int j = 0; j <= NT; ++j) {
-      if (j < NT) {
-        const int s = j % NSTAGE;
-        mbar_wait(&sm->k_full[s], (j / NSTAGE) & 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sm->k[s]);
-        const uint32_t d_tmem = tmem + (uint32_t)(j & 1) * BN;
-        if (elect_one()) {
-#pragma unroll
-          for (int ks = 0; ks < D / 16; ++ks) {
-            const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
-            mma_ss(d_tmem, smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024),
-                   smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
-          }
-          mma_commit(&sm->s_full[j & 1]);
-          mma_commit(&sm->k_empty[s]);
-        }
-        __syncwarp();
-      }
-      if (j >= 1) {
-        const int jj = j - 1, s = jj % NSTAGE;
-        mbar_wait(&sm->p_full[jj & 1], (jj >> 1) & 1);
-        mbar_wait(&sm->v_full[s], (jj / NSTAGE) & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(sm->v[s]);
-        if (elect_one()) {
-#pragma unroll
-          for (int ks = 0; ks < BN / 16; ++ks)
-            mma_ts(tmem + TM_O, tmem + (uint32_t)(jj & 1) * BN + ks * 8,
-                   smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024), idesc_o, (jj > 0 || ks > 0) ? 1u : 0u);
-          mma_commit(&sm->v_empty[s]);
-          mma_commit(&sm->o_done);
-          if (jj == NT - 1) mma_commit(&sm->o_final);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax halves + epilogue
-    const int h = (warp - 2) >> 2;          // column half: 0 -> [0,32), 1 -> [32,64)
-    const int quad = warp & 3;
-    const int r = quad * 32 + lane;
-    const int n = plan.n0 + r;
-    const bool valid = n < T;
-    const Range rr = mask_range(valid ? n : plan.nlast, C, W, mode);
-    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
-    constexpr int DH = D / 2;               // O columns owned by this half
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < NT; ++j) {
-      const int b = j & 1;
-      mbar_wait(&sm->s_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      const int base = plan.base(j) + 32 * h;
-      int vlo, vhi;
-      if (plan.summary(j)) {
-        vlo = 0;
-        vhi = (int)min((int64_t)32, rr.nsum - base);
-      } else {
-        vlo = (int)max((int64_t)0, rr.lo - base);
-        vhi = min(32, n - base + 1);
-      }
-      if (!valid) vhi = vlo;
-      uint32_t sr[32];
-      tmem_ld32(t_lane + (uint32_t)b * BN + 32 * h, sr);
-      tmem_wait_ld();
-      if (!__all_sync(0xffffffffu, vlo <= 0 && vhi >= 32)) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (c < vlo || c >= vhi) sr[c] = 0xff800000u;
-      }
-      float pm[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) pm[i] = __uint_as_float(sr[i]);
-#pragma unroll
-      for (int c = 4; c < 32; ++c) pm[c & 3] = fmaxf(pm[c & 3], __uint_as_float(sr[c]));
-      const float pmx = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
-      sm->xmax[b][h][r] = pmx;
-      named_bar_sync(2 + quad, 64);
-      const float mx = fmaxf(pmx, sm->xmax[b][1 - h][r]) * scale_log2;
-      const bool grow = mx > m_ref + 8.0f;
-      if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
-        const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
-        mbar_wait(&sm->o_done, (j - 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < DH / 32; ++cc) {
-          uint32_t o[32];
-          tmem_ld32(t_lane + TM_O + h * DH + cc * 32, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-          tmem_st32(t_lane + TM_O + h * DH + cc * 32, o);
-        }
-        tmem_wait_st();
-        l *= f;
-      }
-      if (grow) m_ref = mx;
-      const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
-      uint32_t pk[16];
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg));
-        const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg));
-        ls[(2 * c) & 3] += p0;
-        ls[(2 * c + 1) & 3] += p1;
-        pk[c] = pack_bf16(p0, p1);
-      }
-      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-      tmem_st16(t_lane + (uint32_t)b * BN + 16 * h, pk);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&sm->p_full[b]);
-    }
-    // ------------------------------------------------------------ epilogue
-    sm->xsum[h][r] = l;
-    mbar_wait(&sm->o_final, 0);
-    tc_fence_after();
-    named_bar_sync(2 + quad, 64);
-    const float lt = sm->xsum[0][r] + sm->xsum[1][r];
-    const float inv_l = lt > 0.f ? 1.0f / lt : 0.f;
-    uint8_t* qs = reinterpret_cast<uint8_t*>(sm->q);
-#pragma unroll
-    for (int cc = 0; cc < DH / 32; ++cc) {
-      uint32_t o[32];
-      const int col = h * DH + cc * 32;
-      tmem_ld32(t_lane + TM_O + col, o);
-      tmem_wait_ld();
-      const int kb = col / 64, c16_0 = (col % 64) / 8;
-      uint8_t* rowp = qs + kb * (BM * 128) + r * 128;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(o[8 * g + 0]) * inv_l, __uint_as_float(o[8 * g + 1]) * inv_l);
-        w.y = pack_bf16(__uint_as_float(o[8 * g + 2]) * inv_l, __uint_as_float(o[8 * g + 3]) * inv_l);
-        w.z = pack_bf16(__uint_as_float(o[8 * g + 4]) * inv_l, __uint_as_float(o[8 * g + 5]) * inv_l);
-        w.w = pack_bf16(__uint_as_float(o[8 * g + 6]) * inv_l, __uint_as_float(o[8 * g + 7]) * inv_l);
-        *reinterpret_cast<uint4*>(rowp + (((c16_0 + g) ^ (r & 7)) * 16)) = w;
-      }
-    }
-    if (h == 0 && valid && lse) lse[(size_t)u * T + n] = (m_ref + __log2f(lt)) * 0.69314718055994531f;
-    fence_proxy_async_smem();
-    named_bar_sync(1, 256);
-    if (warp == 2 && lane == 0) {
-      for (int kb = 0; kb < D / 64; ++kb) tma_store_3d(&mO, sm->q + kb * BM * 64, kb * 64, plan.n0, u);
-      tma_store_commit();
-      tma_store_wait_all();
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
-}
-
-// ========================================================================== wide-tile kernel
-// One 128-query tile per CTA (two CTAs per SM) walking 128-key tiles: the S MMA is
-// M=128 x N=128 (full tensor rate; N=64 SS MMAs are shared-memory bound at 48 instead of
-// 32 cycles per K-step).  TMEM (256 columns): S/P [0,128) single-buffered, O [128,128+d).
-// Per tile the MMA warp issues PV(j-1) then S(j), so when softmax sees S(j) complete,
-// PV(j-1) has completed too and O may be rescaled without another barrier.  K and V have
-// separate slot rings (NSK, NSV) released by the S and the PV MMA respectively.
-constexpr int BNW = 128;
-
-struct WidePlan {
-  int n0, nlast, n_st, n_lt, lo0;
-  __device__ WidePlan(int qt, int T, int C, int W, int mode) {
-    n0 = qt * BM;
-    nlast = min(n0 + BM - 1, T - 1);
-    const Range rf = mask_range(n0, C, W, mode), rl = mask_range(nlast, C, W, mode);
-    n_st = (int)((rl.nsum + BNW - 1) / BNW);
-    lo0 = (int)rf.lo;
-    n_lt = (nlast - lo0 + 1 + BNW - 1) / BNW;
-  }
-  __device__ int count() const { return n_st + n_lt; }
-  __device__ bool summary(int j) const { return j < n_st; }
-  __device__ int base(int j) const { return j < n_st ? j * BNW : lo0 + (j - n_st) * BNW; }
-};
-
-template <int D, int NSK, int NSV>
-struct __align__(1024) SmemWide {
-  __nv_bfloat16 q[BM * D];           // D/64 sub-tiles [128][64]
-  __nv_bfloat16 k[NSK][BNW * D];     // D/64 sub-tiles [128][64]
-  __nv_bfloat16 v[NSV][BNW * D];
-  uint64_t q_full, k_full[NSK], k_empty[NSK], v_full[NSV], v_empty[NSV];
-  uint64_t s_full, p_full, o_final;
-  uint32_t tmem_base;
-};
-
-// Softmax step on a 128-column S tile (see softmax_tile): pass 1 loads all 128 columns and
-// finds the row max, pass 2 writes P (bf16 pairs) in place and stores it to TMEM [0,64).
-// The previous PV has completed whenever this runs (issue order), so no wait is needed
-// before rescaling O.
-template <int D>
-__device__ __forceinline__ void softmax_tile128(uint32_t s_addr, uint32_t o_addr, int vlo, int vhi,
-                                                float scale_log2, float& m_ref, float& l) {
-  // pass 1: row max over the 128 columns, 32 at a time (keeps register use low)
-  const bool full = __all_sync(0xffffffffu, vlo <= 0 && vhi >= 128);
-  float pm[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) pm[i] = -INFINITY;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t sr[32];
-    tmem_ld32(s_addr + 32 * q, sr);
-    tmem_wait_ld();
-    if (!full) {
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (32 * q + c < vlo || 32 * q + c >= vhi) sr[c] = 0xff800000u;
-    }
-#pragma unroll
-    for (int c = 0; c < 32; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sr[c]));
-  }
-  float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
-  mx *= scale_log2;
-  const bool grow = mx > m_ref + 8.0f;
-  if (__any_sync(0xffffffffu, grow && m_ref != -INFINITY)) {
-    const float f = (grow && m_ref != -INFINITY) ? ex2(m_ref - mx) : 1.0f;
-#pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t o[32];
-      tmem_ld32(o_addr + cc * 32, o);
-      tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * f);
-      tmem_st32(o_addr + cc * 32, o);
-    }
-    tmem_wait_st();
-    l *= f;
-  }
-  if (grow) m_ref = mx;
-  const float neg = m_ref == -INFINITY ? 0.f : -m_ref;
-  // pass 2: P = exp2(s*scale - m) as bf16 pairs; chunk q (S columns 32q..32q+31) lands in
-  // P columns 16q..16q+15, which only overwrite S columns already consumed
-  float ls[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) ls[i] = 0.f;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    uint32_t sr[32];
-    tmem_ld32(s_addr + 32 * q, sr);
-    tmem_wait_ld();
-    if (!full) {
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (32 * q + c < vlo || 32 * q + c >= vhi) sr[c] = 0xff800000u;
-    }
-    uint32_t pk[16];
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), scale_log2, neg));
-      const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), scale_log2, neg));
-      ls[(2 * c) & 7] += p0;
-      ls[(2 * c + 1) & 7] += p1;
-      pk[c] = pack_bf16(p0, p1);
-    }
-    tmem_st16(s_addr + 16 * q, pk);
-  }
-  l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-  tmem_wait_st();
-  tc_fence_before();
-}
-
-template <int D, int NSK, int NSV>
-__global__ void __launch_bounds__(NTHREADS, 2)
-prefill_wide_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
-                    const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
-                    const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
-                    int T, int C, int W, int mode, float scale_log2, float* __restrict__ lse) {
-  extern __shared__ uint8_t smem_raw[];
-  SmemWide<D, NSK, NSV>* sm = reinterpret_cast<SmemWide<D, NSK, NSV>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.y;
-  const WidePlan plan(blockIdx.x, T, C, W, mode);
-  const int NT = plan.count();
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV);
-    tma_prefetch(&mKs); tma_prefetch(&mVs); tma_prefetch(&mO);
-    mbar_init(&sm->q_full, 1);
-    for (int s = 0; s < NSK; ++s) { mbar_init(&sm->k_full[s], 1); mbar_init(&sm->k_empty[s], 1); }
-    for (int s = 0; s < NSV; ++s) { mbar_init(&sm->v_full[s], 1); mbar_init(&sm->v_empty[s], 1); }
-    mbar_init(&sm->s_full, 1);
-    mbar_init(&sm->p_full, 128);
-    mbar_init(&sm->o_final, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    tmem_alloc(&sm->tmem_base, TMEM_COLS);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = sm->tmem_base;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (elect_one()) {
-      mbar_arrive_expect_tx(&sm->q_full, BM * D * 2);
-      for (int kb = 0; kb < D / 64; ++kb)
-        tma_load_3d(sm->q + kb * BM * 64, &mQ, &sm->q_full, kb * 64, plan.n0, u);
-      for (int j = 1; j < NT; ++j) {  // later tiles: warm L2 (the rings hold only NSK/NSV)
-        const CUtensorMap* mk = plan.summary(j) ? &mKs : &mK;
-        const CUtensorMap* mv = plan.summary(j) ? &mVs : &mV;
-        for (int kb = 0; kb < D / 64; ++kb) {
-          tma_prefetch_l2_3d(mk, kb * 64, plan.base(j), u);
-          tma_prefetch_l2_3d(mv, kb * 64, plan.base(j), u);
-        }
-      }
-    }
-    __syncwarp();
-    auto load = [&](bool is_k, int j) {
-      const int s = is_k ? j % NSK : j % NSV;
-      const int ns = is_k ? NSK : NSV;
-      uint64_t* empty = is_k ? &sm->k_empty[s] : &sm->v_empty[s];
-      uint64_t* full = is_k ? &sm->k_full[s] : &sm->v_full[s];
-      __nv_bfloat16* dst = is_k ? sm->k[s] : sm->v[s];
-      if (j >= ns) mbar_wait(empty, ((j / ns) - 1) & 1);
-      const CUtensorMap* m = plan.summary(j) ? (is_k ? &mKs : &mVs) : (is_k ? &mK : &mV);
-      if (elect_one()) {
-        mbar_arrive_expect_tx(full, BNW * D * 2);
-        for (int kb = 0; kb < D / 64; ++kb) tma_load_3d(dst + kb * BNW * 64, m, full, kb * 64, plan.base(j), u);
-      }
-      __syncwarp();
-    };
-    // K(j) is consumed by S(j), V(j) by PV(j) one softmax later: K runs one tile ahead.
-    load(true, 0);
-    for (int j = 0; j < NT; ++j) {
-      load(false, j);
-      if (j + 1 < NT) load(true, j + 1);
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BNW, false);
-    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
-    const uint32_t q_addr = smem_u32(sm->q);
-    mbar_wait(&sm->q_full, 0);
-    for (int j = 0; j <= NT; ++j) {
-      if (j >= 1) {  // PV(j-1)
-        const int jj = j - 1, s = jj % NSV;
-        mbar_wait(&sm->p_full, jj & 1);
-        mbar_wait(&sm->v_full[s], (jj / NSV) & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(sm->v[s]);
-        if (elect_one()) {
-#pragma unroll
-          for (int ks = 0; ks < BNW / 16; ++ks)
-            mma_ts(tmem + TM_O, tmem + ks * 8, smem_desc_sw128(v_addr + ks * 16 * 128, BNW * 128, 1024),
-                   idesc_o, (jj > 0 || ks > 0) ? 1u : 0u);
-          mma_commit(&sm->v_empty[s]);
-          if (jj == NT - 1) mma_commit(&sm->o_final);
-        }
-        __syncwarp();
-      }
-      if (j < NT) {  // S(j)
-        const int s = j % NSK;
-        mbar_wait(&sm->k_full[s], (j / NSK) & 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sm->k[s]);
-        if (elect_one()) {
-#pragma unroll
-          for (int ks = 0; ks < D / 16; ++ks) {
-            const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
-            mma_ss(tmem, smem_desc_sw128(q_addr + kb * (BM * 128) + off, 16, 1024),
-                   smem_desc_sw128(k_addr + kb * (BNW * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);
-          }
-          mma_commit(&sm->s_full);
-          mma_commit(&sm->k_empty[s]);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax warps + epilogue
-    const int quad = warp & 3;
-    const int r = quad * 32 + lane;
-    const int n = plan.n0 + r;
-    const bool valid = n < T;
-    const Range rr = mask_range(valid ? n : plan.nlast, C, W, mode);
-    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < NT; ++j) {
-      mbar_wait(&sm->s_full, j & 1);
-      tc_fence_after();
-      const int base = plan.base(j);
-      int vlo, vhi;
-      if (plan.summary(j)) {
-        vlo = 0;
-        vhi = (int)min((int64_t)BNW, rr.nsum - base);
-      } else {
-        vlo = (int)max((int64_t)0, rr.lo - base);
-        vhi = min(BNW, n - base + 1);
-      }
-      if (!valid) vhi = vlo;
-      softmax_tile128<D>(t_lane, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l);
-      mbar_arrive(&sm->p_full);
-    }
-    mbar_wait(&sm->o_final, 0);
-    tc_fence_after();
-    const float inv_l = l > 0.f ? 1.0f / l : 0.f;
-    uint8_t* qs = reinterpret_cast<uint8_t*>(sm->q);
-#pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t o[32];
-      tmem_ld32(t_lane + TM_O + cc * 32, o);
-      tmem_wait_ld();
-      const int kb = (cc * 32) / 64, c16_0 = ((cc * 32) % 64) / 8;
-      uint8_t* rowp = qs + kb * (BM * 128) + r * 128;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        uint4 w;
-        w.x = pack_bf16(__uint_as_float(o[8 * g + 0]) * inv_l, __uint_as_float(o[8 * g + 1]) * inv_l);
-        w.y = pack_bf16(__uint_as_float(o[8 * g + 2]) * inv_l, __uint_as_float(o[8 * g + 3]) * inv_l);
-        w.z = pack_bf16(__uint_as_float(o[8 * g + 4]) * inv_l, __uint_as_float(o[8 * g + 5]) * inv_l);
-        w.w = pack_bf16(__uint_as_float(o[8 * g + 6]) * inv_l, __uint_as_float(o[8 * g + 7]) * inv_l);
-        *reinterpret_cast<uint4*>(rowp + (((c16_0 + g) ^ (r & 7)) * 16)) = w;
-      }
-    }
-    if (valid && lse) lse[(size_t)u * T + n] = (m_ref + __log2f(l)) * 0.69314718055994531f;
-    fence_proxy_async_smem();
-    named_bar_sync(1, 128);
-    if (warp == 2 && lane == 0) {
-      for (int kb = 0; kb < D / 64; ++kb) tma_store_3d(&mO, sm->q + kb * BM * 64, kb * 64, plan.n0, u);
-      tma_store_commit();
-      tma_store_wait_all();
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
-}
-
-// ========================================================================== pair kernel
-// Persistent variant for large problems: a CTA owns one SM and loops over work items
-// (unit, pair of adjacent 128-query tiles).  The two Q tiles share one K/V stream (the
-// union of their tile lists, loaded once through an NS-deep TMA ring), each Q tile has
-// its own softmax warpgroup and its own TMEM half (S double buffer + O):
-//   warp 0      TMA producer (Q tiles of the next item prefetched as soon as the last
-//               S MMA of the current item has consumed the old ones)
-//   warp 1      MMA issuer: per union tile j: S_t(j) for each Q tile t that needs j,
-//               then PV_t(j-1); stage released after the last PV that reads it
-//   warps 2-5   softmax + epilogue of Q tile 0;   warps 6-9   the same for Q tile 1
-// Epilogue: O / l straight from registers to global (rows are contiguous 2d-byte runs).
-constexpr int PAIR_THREADS = 352;  // + warp 10: Q-tile loader
-constexpr uint32_t PAIR_TMEM_COLS = 512;
-
-// Debug timeline (eva_debug_trace_prefill): CTA 0 records (clock64 << 24 | code) events in
-// per-role shared-memory logs (no atomics: role r appends to its own slice), copied to
-// global memory at exit.  code = kind << 20 | t << 16 | j.  kinds: 1 producer issued tile j,
-// 2 MMA issued S_t(j), 3 MMA issued PV_t(j), 4 softmax t got S(j), 5 softmax t released
-// P(j), 6 epilogue t done, 7 producer slot free for tile j, 8 MMA got k_full(j),
-// 9 MMA got p_full_t(j).
-__device__ unsigned long long* g_trace = nullptr;
-__device__ int g_trace_n = 0;
-__device__ int g_trace_cap = 0;
-constexpr int TRACE_ROLES = 4, TRACE_PER_ROLE = 384;
-struct TraceLog {
-  unsigned long long ev[TRACE_ROLES][TRACE_PER_ROLE];
-  int n[TRACE_ROLES];
-};
-template <bool TRACE>
-__device__ __forceinline__ void trace(TraceLog* log, int role, int kind, int t, int j) {
-  if constexpr (TRACE) {
-    if (blockIdx.x == 0) {
-      const int i = log->n[role];
-      if (i < TRACE_PER_ROLE)
-        log->ev[role][i] = ((unsigned long long)clock64() << 24) | ((unsigned)kind << 20) |
-                           ((unsigned)t << 16) | ((unsigned)j & 0xffff);
-      log->n[role] = i + 1;
-    }
-  }
-}
-template <bool TRACE>
-__device__ __forceinline__ void trace_flush(TraceLog* log) {
-  if constexpr (TRACE) {
-    if (blockIdx.x == 0 && g_trace) {
-      for (int r = 0; r < TRACE_ROLES; ++r) {
-        const int n = min(log->n[r], TRACE_PER_ROLE);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-          const int k = r * TRACE_PER_ROLE + i;
-          if (k < g_trace_cap) g_trace[k] = log->ev[r][i];
-        }
-      }
-    }
-  }
-}
-
-template <int D, int NS>
-struct __align__(1024) SmemPair {
-  __nv_bfloat16 q[2][BM * D];
-  __nv_bfloat16 k[NS][BN * D];
-  __nv_bfloat16 v[NS][BN * D];
-  uint64_t q_full[2], q_empty[2];
-  uint64_t k_full[NS], v_full[NS], kv_empty[NS];
-  uint64_t s_full[2][2], p_full[2][2], o_done[2], o_final[2], o_empty[2];
-  uint32_t tmem_base;
-};
-
-// Tile plan of one work item (two adjacent Q tiles).  Scalar fields only (selected with
-// t ? x1 : x0) so that nothing is indexed dynamically and the plan stays in registers.
-struct PairPlan {
-  int n0, n_st, n_lt, lo0;
-  int nlast0, nlast1, lof0, lof1, nsl0, nsl1;
-  __device__ PairPlan(int pair, int T, int C, int W, int mode) {
-    n0 = pair * 2 * BM;
-    const int a1 = n0 + BM;
-    nlast0 = min(n0 + BM - 1, T - 1);
-    lof0 = (int)mask_range(n0, C, W, mode).lo;
-    nsl0 = (int)mask_range(nlast0, C, W, mode).nsum;
-    if (a1 < T) {
-      nlast1 = min(a1 + BM - 1, T - 1);
-      lof1 = (int)mask_range(a1, C, W, mode).lo;
-      nsl1 = (int)mask_range(nlast1, C, W, mode).nsum;
-    } else {
-      nlast1 = -1;
-      lof1 = 0;
-      nsl1 = 0;
-    }
-    const int nl = nlast1 >= 0 ? nlast1 : nlast0;
-    const int ns = nlast1 >= 0 ? nsl1 : nsl0;
-    n_st = (ns + BN - 1) / BN;
-    lo0 = lof0;
-    n_lt = (nl - lo0 + 1 + BN - 1) / BN;
-  }
-  __device__ int nlast(int t) const { return t ? nlast1 : nlast0; }
-  __device__ bool active(int t) const { return nlast(t) >= 0; }
-  __device__ int count() const { return n_st + n_lt; }
-  __device__ bool summary(int j) const { return j < n_st; }
-  __device__ int base(int j) const { return j < n_st ? j * BN : lo0 + (j - n_st) * BN; }
-  __device__ bool need(int t, int j) const {
-    const int nl = t ? nlast1 : nlast0;
-    if (nl < 0) return false;
-    const int b = base(j);
-    if (j < n_st) return b < (t ? nsl1 : nsl0);
-    return b <= nl && b + BN - 1 >= (t ? lof1 : lof0);
-  }
-  __device__ int last_need(int t) const {
-    // local tiles are needed on a contiguous range ending at the tile containing nlast(t);
-    // if the Q tile has no local tile (impossible: n is in E(n)) fall back to a scan.
-    const int nl = t ? nlast1 : nlast0;
-    if (nl < 0) return -1;
-    return n_st + (nl - lo0) / BN;
-  }
-};
-
-template <int D, int NS, bool TRACE>
-__global__ void __launch_bounds__(PAIR_THREADS, 1)
-prefill_pair_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
-                    const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
-                    const __grid_constant__ CUtensorMap mVs, int BH, int T, int C, int W, int mode,
-                    float scale_log2, __nv_bfloat16* __restrict__ O, float* __restrict__ lse) {
-  extern __shared__ uint8_t smem_raw[];
-  SmemPair<D, NS>* sm = reinterpret_cast<SmemPair<D, NS>*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  TraceLog* tlog = reinterpret_cast<TraceLog*>(sm + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ppu = (T + 2 * BM - 1) / (2 * BM);
-  if (TRACE && threadIdx.x < TRACE_ROLES) tlog->n[threadIdx.x] = 0;
-  const int n_items = BH * ppu;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&mQ); tma_prefetch(&mK); tma_prefetch(&mV); tma_prefetch(&mKs); tma_prefetch(&mVs);
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&sm->q_full[t], 1);
-      mbar_init(&sm->q_empty[t], 1);
-      mbar_init(&sm->o_done[t], 1);
-      mbar_init(&sm->o_final[t], 1);
-      mbar_init(&sm->o_empty[t], 128);
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&sm->s_full[t][b], 1);
-        mbar_init(&sm->p_full[t][b], 128);
-      }
-    }
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&sm->k_full[s], 1);
-      mbar_init(&sm->v_full[s], 1);
-      mbar_init(&sm->kv_empty[s], 2);  // one release per Q tile
-    }
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    tmem_alloc(&sm->tmem_base, PAIR_TMEM_COLS);
-    tmem_relinquish();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = sm->tmem_base;
-
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (whole warp)
-    uint32_t kv = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const bool tr = TRACE && item >= (int)(blockIdx.x + 3 * gridDim.x);  // steady-state window
-      const int u = item / ppu;
-      const PairPlan plan(item % ppu, T, C, W, mode);
-      const int NT = plan.count();
-      for (int j = 0; j < NT; ++j, ++kv) {
-        const int s = kv % NS;
-        if (kv >= (uint32_t)NS) mbar_wait(&sm->kv_empty[s], ((kv / NS) - 1) & 1);
-        if (tr && lane == 0) trace<TRACE>(tlog, 0, 7, 0, kv);
-        const bool summ = plan.summary(j);
-        const int row = plan.base(j);
-        const CUtensorMap* mk = summ ? &mKs : &mK;
-        const CUtensorMap* mv = summ ? &mVs : &mV;
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&sm->k_full[s], BN * D * 2);
-          for (int kb = 0; kb < D / 64; ++kb)
-            tma_load_3d(sm->k[s] + kb * BN * 64, mk, &sm->k_full[s], kb * 64, row, u);
-          mbar_arrive_expect_tx(&sm->v_full[s], BN * D * 2);
-          for (int kb = 0; kb < D / 64; ++kb)
-            tma_load_3d(sm->v[s] + kb * BN * 64, mv, &sm->v_full[s], kb * 64, row, u);
-        }
-        __syncwarp();
-        if (tr && lane == 0) trace<TRACE>(tlog, 0, 1, 0, kv);
-      }
-    }
-  } else if (warp == 10) {
-    // ------------------------------------------------------------ Q-tile loader (whole warp)
-    // Separate from the K/V producer so the ring keeps streaming the next item's tiles
-    // while this warp waits for the current item's last S MMA to release a Q buffer.
-    int qcnt0 = 0, qcnt1 = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const int u = item / ppu;
-      const PairPlan plan(item % ppu, T, C, W, mode);
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (!plan.active(t)) continue;
-        int& qc = t ? qcnt1 : qcnt0;
-        if (qc > 0) mbar_wait(&sm->q_empty[t], (qc - 1) & 1);
-        if (elect_one()) {
-          mbar_arrive_expect_tx(&sm->q_full[t], BM * D * 2);
-          for (int kb = 0; kb < D / 64; ++kb)
-            tma_load_3d(sm->q[t] + kb * BM * 64, &mQ, &sm->q_full[t], kb * 64, plan.n0 + t * BM, u);
-        }
-        __syncwarp();
-        ++qc;
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (whole warp)
-    // Ping-pong order per Q tile t (FA4-style): PV_t(i) is followed immediately by
-    // S_t(next tile of t), so while softmax warpgroup 0 works the tensor core runs Q tile 1
-    // and vice versa.  Each union tile's ring slot is released by two tcgen05.commit
-    // arrivals (kv_empty count 2): one per Q tile, after its PV (or, if that Q tile skips
-    // the tile, as soon as its cursor passes it).  All state stays in scalar registers.
-    constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
-    constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
-    const uint32_t q0_addr = smem_u32(sm->q[0]), q1_addr = smem_u32(sm->q[1]);
-    uint32_t kv = 0;  // ring index of the item's union tile 0
-    uint32_t cS0 = 0, cS1 = 0, cP0 = 0, cP1 = 0, icnt0 = 0, icnt1 = 0;
-#define EVA_ISSUE_S(T_, J_, CS_)                                                                        \
-  do {                                                                                                 \
-    const uint32_t kk = kv + (uint32_t)(J_);                                                           \
-    mbar_wait(&sm->k_full[kk % NS], (kk / NS) & 1);                                                    \
-    tc_fence_after();                                                                                  \
-    const uint32_t k_addr = smem_u32(sm->k[kk % NS]);                                                  \
-    if (elect_one()) {                                                                                 \
-      const uint32_t d_tmem = tmem + (T_) * 256u + ((CS_) & 1) * BN;                                   \
-      const uint32_t qa = (T_) ? q1_addr : q0_addr;                                                    \
-      _Pragma("unroll") for (int ks = 0; ks < D / 16; ++ks) {                                          \
-        const uint32_t kb = ks >> 2, off = (ks & 3) * 32;                                              \
-        mma_ss(d_tmem, smem_desc_sw128(qa + kb * (BM * 128) + off, 16, 1024),                          \
-               smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024), idesc_s, ks > 0 ? 1u : 0u);  \
-      }                                                                                                \
-      mma_commit(&sm->s_full[T_][(CS_) & 1]);                                                          \
-      if ((J_) == ((T_) ? last1 : last0)) mma_commit(&sm->q_empty[T_]);                                \
-    }                                                                                                  \
-    __syncwarp();                                                                                      \
-    ++(CS_);                                                                                           \
-  } while (0)
-#define EVA_ISSUE_PV(T_, J_, CP_, FIRST_, ICNT_)                                                       \
-  do {                                                                                                 \
-    const uint32_t kk = kv + (uint32_t)(J_);                                                           \
-    mbar_wait(&sm->p_full[T_][(CP_) & 1], ((CP_) >> 1) & 1);                                           \
-    if ((FIRST_) && (ICNT_) > 0) mbar_wait(&sm->o_empty[T_], ((ICNT_) - 1) & 1);                       \
-    mbar_wait(&sm->v_full[kk % NS], (kk / NS) & 1);                                                    \
-    tc_fence_after();                                                                                  \
-    const uint32_t v_addr = smem_u32(sm->v[kk % NS]);                                                  \
-    if (elect_one()) {                                                                                 \
-      const uint32_t tb = tmem + (T_) * 256u;                                                          \
-      _Pragma("unroll") for (int ks = 0; ks < BN / 16; ++ks)                                           \
-        mma_ts(tb + TM_O, tb + ((CP_) & 1) * BN + ks * 8,                                              \
-               smem_desc_sw128(v_addr + ks * 16 * 128, BN * 128, 1024), idesc_o,                       \
-               (!(FIRST_) || ks > 0) ? 1u : 0u);                                                       \
-      mma_commit(&sm->o_done[T_]);                                                                     \
-      if ((J_) == ((T_) ? last1 : last0)) mma_commit(&sm->o_final[T_]);                                \
-      mma_commit(&sm->kv_empty[kk % NS]);                                                              \
-      if (!plan.need(1 - (T_), (J_))) mma_commit(&sm->kv_empty[kk % NS]); /* other tile's share */     \
-    }                                                                                                  \
-    __syncwarp();                                                                                      \
-    (FIRST_) = false;                                                                                  \
-    ++(CP_);                                                                                           \
-  } while (0)
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const bool tr = TRACE && item >= (int)(blockIdx.x + 3 * gridDim.x);
-      const PairPlan plan(item % ppu, T, C, W, mode);
-      const int NT = plan.count();
-      const bool act1 = plan.active(1);
-      const int last0 = plan.last_need(0), last1 = plan.last_need(1);
-      // next needed union tile of Q tile t at or after j (NT if none)
-      auto next_need = [&](int t, int j) {
-        while (j < NT && !plan.need(t, j)) ++j;
-        return j;
-      };
-      bool first0 = true, first1 = true;
-      mbar_wait(&sm->q_full[0], icnt0 & 1);
-      if (act1) mbar_wait(&sm->q_full[1], icnt1 & 1);
-      // Event loop: per Q tile, S runs at most one tile ahead of PV (double-buffered S/P);
-      // whichever Q tile has its operands ready is served first (non-blocking probes), so
-      // the two softmax warpgroups are never lock-stepped through this single issuer.
-      int s0 = next_need(0, 0), s1 = act1 ? next_need(1, 0) : NT;   // next S tile
-      int p0 = s0, p1 = s1;                                          // next PV tile
-      int ahead0 = 0, ahead1 = 0;                                    // S issued - PV issued
-      while (p0 < NT || p1 < NT) {
-        bool progress = false;
-        // ---- Q tile 0
-        if (s0 < NT && ahead0 < 2) {
-          const uint32_t kk = kv + (uint32_t)s0;
-          if (mbar_test(&sm->k_full[kk % NS], (kk / NS) & 1)) {
-            EVA_ISSUE_S(0, s0, cS0);
-            s0 = next_need(0, s0 + 1);
-            ++ahead0;
-            progress = true;
-          }
-        }
-        if (p0 < NT && ahead0 > 0 && mbar_test(&sm->p_full[0][cP0 & 1], (cP0 >> 1) & 1)) {
-          EVA_ISSUE_PV(0, p0, cP0, first0, icnt0);
-          if (tr && lane == 0) trace<TRACE>(tlog, 1, 3, 0, kv + p0);
-          p0 = next_need(0, p0 + 1);
-          --ahead0;
-          progress = true;
-        }
-        // ---- Q tile 1
-        if (s1 < NT && ahead1 < 2) {
-          const uint32_t kk = kv + (uint32_t)s1;
-          if (mbar_test(&sm->k_full[kk % NS], (kk / NS) & 1)) {
-            EVA_ISSUE_S(1, s1, cS1);
-            s1 = next_need(1, s1 + 1);
-            ++ahead1;
-            progress = true;
-          }
-        }
-        if (p1 < NT && ahead1 > 0 && mbar_test(&sm->p_full[1][cP1 & 1], (cP1 >> 1) & 1)) {
-          EVA_ISSUE_PV(1, p1, cP1, first1, icnt1);
-          if (tr && lane == 0) trace<TRACE>(tlog, 1, 3, 1, kv + p1);
-          p1 = next_need(1, p1 + 1);
-          --ahead1;
-          progress = true;
-        }
-        if (!progress) __nanosleep(32);
-      }
-      kv += (uint32_t)NT;
-      ++icnt0;
-      if (act1) ++icnt1;
-    }
-#undef EVA_ISSUE_S
-#undef EVA_ISSUE_PV
-  } else {
-    // ------------------------------------------------------------ softmax warpgroups
-    const int t = (warp - 2) >> 2;
-    const int quad = warp & 3;
-    const int r = quad * 32 + lane;
-    const uint32_t t_lane = tmem + (uint32_t)t * 256 + ((uint32_t)(quad * 32) << 16);
-    int cS = 0, icnt = 0;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      const bool tr = TRACE && item >= (int)(blockIdx.x + 3 * gridDim.x);
-      const int u = item / ppu;
-      const PairPlan plan(item % ppu, T, C, W, mode);
-      if (!plan.active(t)) continue;
-      const int n = plan.n0 + t * BM + r;
-      const bool valid = n <= plan.nlast(t);
-      const Range rr = mask_range(valid ? n : plan.nlast(t), C, W, mode);
-      const int NT = plan.count();
-      float m_ref = -INFINITY, l = 0.f;
-      for (int j = 0; j < NT; ++j) {
-        if (!plan.need(t, j)) continue;
-        const int b = cS & 1;
-        mbar_wait(&sm->s_full[t][b], (cS >> 1) & 1);
-        if (tr && r == 0) trace<TRACE>(tlog, 2 + t, 4, t, cS);
-        tc_fence_after();
-        const int base = plan.base(j);
-        int vlo, vhi;
-        if (plan.summary(j)) {
-          vlo = 0;
-          vhi = (int)min((int64_t)BN, rr.nsum - base);
-        } else {
-          vlo = (int)max((int64_t)0, rr.lo - base);
-          vhi = min(BN, n - base + 1);
-        }
-        if (!valid) vhi = vlo;
-        softmax_tile<D>(t_lane + (uint32_t)b * BN, t_lane + TM_O, vlo, vhi, scale_log2, m_ref, l,
-                        [&] { mbar_wait(&sm->o_done[t], (cS - 1) & 1); });
-        mbar_arrive(&sm->p_full[t][b]);
-        if (tr && r == 0) trace<TRACE>(tlog, 2 + t, 5, t, cS);
-        ++cS;
-      }
-      // ---------------------------------------------------------- epilogue
-      mbar_wait(&sm->o_final[t], icnt & 1);
-      tc_fence_after();
-      const float inv_l = l > 0.f ? 1.0f / l : 0.f;
-      uint32_t ob[D / 2];
-#pragma unroll
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t o[32];
-        tmem_ld32(t_lane + TM_O + cc * 32, o);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          ob[cc * 16 + i] = pack_bf16(__uint_as_float(o[2 * i]) * inv_l, __uint_as_float(o[2 * i + 1]) * inv_l);
-      }
-      tc_fence_before();
-      mbar_arrive(&sm->o_empty[t]);
-      if (valid) {
-        uint4* dst = reinterpret_cast<uint4*>(O + ((size_t)u * T + n) * D);
-#pragma unroll
-        for (int i = 0; i < D / 8; ++i)
-          dst[i] = make_uint4(ob[4 * i], ob[4 * i + 1], ob[4 * i + 2], ob[4 * i + 3]);
-        if (lse) lse[(size_t)u * T + n] = (m_ref + __log2f(l)) * 0.69314718055994531f;
-      }
-      if (tr && r == 0) trace<TRACE>(tlog, 2 + t, 6, t, icnt);
-      ++icnt;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  trace_flush<TRACE>(tlog);
-  if (warp == 1) tmem_dealloc(tmem, PAIR_TMEM_COLS);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1835,13 +978,13 @@ bool make_map(CUtensorMap* m, const void* base, int units, int rows, int D, int 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Softmax exponential split of the tile kernel: -1 = all MUFU.EX2 (softmax_tile), k >= 0 =
-// softmax_tile2 with k of every 8 column pairs on the FMA pipe.  EVA_SOFTMAX_EMU overrides
-// the default (tuning knob, read once).
+// Softmax exponential split of the tile kernel: -1 = all MUFU.EX2 (softmax_tile), 1 =
+// softmax_tile2 with one of every 8 column pairs on the FMA pipe.  EVA_SOFTMAX_EMU=1 selects
+// it (tuning knob, read once; measured neutral).
 int softmax_emu() {
   static const int v = [] {
     const char* e = getenv("EVA_SOFTMAX_EMU");
-    return e ? atoi(e) : -1;
+    return e && atoi(e) == 1 ? 1 : -1;
   }();
   return v;
 }
@@ -1856,18 +999,50 @@ int tile_sum_first() {
   return v;
 }
 
-template <int D, int NSTAGE, bool TRACE = false, int SMX = -1>
+// ---- workspace of the fused launch: [ticket, done, epoch, pad] + one ready flag per
+// (unit, query tile), zero-initialised once; the kernel leaves ticket/done at 0 and advances
+// the epoch, so one buffer serves every later launch on the same stream (graph replays too).
+struct FusedWs {
+  uint32_t* p = nullptr;
+  size_t flags = 0;
+};
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, FusedWs> g_ws;
+
+cudaError_t fused_workspace(size_t nflags, cudaStream_t s, uint32_t** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  FusedWs& w = g_ws[{dev, s}];
+  if (w.flags < nflags) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    e = cudaStreamIsCapturing(s, &cs);
+    if (e != cudaSuccess) return e;
+    if (cs != cudaStreamCaptureStatusNone) return cudaErrorStreamCaptureUnsupported;
+    if (w.p) {  // the previous buffer may still be read by work on this stream
+      if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+      cudaFree(w.p);
+      w.p = nullptr;
+      w.flags = 0;
+    }
+    const size_t n = std::max<size_t>(nflags, 4096);
+    if ((e = cudaMalloc(&w.p, (n + 4) * sizeof(uint32_t))) != cudaSuccess) return e;
+    if ((e = cudaMemset(w.p, 0, (n + 4) * sizeof(uint32_t))) != cudaSuccess) return e;
+    w.flags = n;
+  }
+  *out = w.p;
+  return cudaSuccess;
+}
+
+template <int D, int NSTAGE, bool TRACE = false, int SMX = -1, int FC = 0>
 cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* Q, const void* K,
                      const void* V, const void* Ksum, const void* Vsum, void* O, float* lse,
-                     cudaStream_t s, bool overlap = false) {
-  if constexpr (!TRACE && SMX == -1) {
-    switch (softmax_emu()) {
-      case 0: return launch_t<D, NSTAGE, false, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
-      case 1: return launch_t<D, NSTAGE, false, 1>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
-      case 2: return launch_t<D, NSTAGE, false, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
-      case 3: return launch_t<D, NSTAGE, false, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
-      default: break;
-    }
+                     cudaStream_t s, bool overlap = false, const float* eps = nullptr) {
+  constexpr bool FUSED = FC != 0;
+  if constexpr (!TRACE && SMX == -1 && !FUSED) {
+    if (softmax_emu() == 1)
+      return launch_t<D, NSTAGE, false, 1, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
   }
   const int BH = cfg.bh_count, nC = rg.nsl;
   if (rg.nq == 0) return cudaSuccess;
@@ -1881,134 +1056,44 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
     mVs = mV;
   }
   if (!ok) return cudaErrorInvalidValue;
+  using K_t = decltype(&prefill_sm100_kernel<D, NSTAGE, TRACE, SMX, FC>);
+  K_t kern = prefill_sm100_kernel<D, NSTAGE, TRACE, SMX, FC>;
   const size_t smem = sizeof(Smem<D, NSTAGE>) + Smem<D, NSTAGE>::PAD;
   {
-    cudaError_t e = set_smem_attr((const void*)prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>, smem);
-    if (e != cudaSuccess) return e;
-  }
-  dim3 grid((rg.nq + BM - 1) / BM, BH);
-  const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  cudaError_t e = launch_pdl(prefill_sm100_kernel<D, NSTAGE, TRACE, SMX>, grid, dim3(NTHREADS), smem, s, mQ, mK, mV,
-                             mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
-                             cfg.summary_bias * 1.4426950408889634f, lse, overlap ? 1 : 0, tile_sum_first());
-  if (e != cudaSuccess) return e;
-  note_launch();
-  return cudaGetLastError();
-}
-
-template <int D, int NSTAGE>
-cudaError_t launch_persist(const eva_config& cfg, const PrefillRange& rg, const void* Q, const void* K,
-                           const void* V, const void* Ksum, const void* Vsum, void* O, float* lse,
-                           cudaStream_t s) {
-  const int BH = cfg.bh_count, nC = rg.nsl;
-  if (rg.nq == 0) return cudaSuccess;
-  CUtensorMap mQ, mK, mV, mKs, mVs;
-  bool ok = make_map(&mQ, Q, BH, rg.nq, D, BM) && make_map(&mK, K, BH, rg.nkv, D, BN) &&
-            make_map(&mV, V, BH, rg.nkv, D, BN);
-  if (nC > 0) {
-    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BN) && make_map(&mVs, Vsum, BH, nC, D, BN);
-  } else {
-    mKs = mK;
-    mVs = mV;
-  }
-  if (!ok) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(SmemP<D, NSTAGE>) + 1024;
-  {
-    cudaError_t e = set_smem_attr((const void*)prefill_persist_kernel<D, NSTAGE>, smem);
+    cudaError_t e = set_smem_attr((const void*)kern, smem);
     if (e != cudaSuccess) return e;
   }
   const int n_qt = (rg.nq + BM - 1) / BM;
-  const int n_items = n_qt * BH;
-  const int grid = std::max(1, std::min(n_items, 2 * num_sms()));
+  FusedArgs fa = {};
+  dim3 grid(n_qt, BH);
+  if constexpr (FUSED) {
+    uint32_t* ws = nullptr;
+    cudaError_t e = fused_workspace((size_t)BH * n_qt, s, &ws);
+    if (e != cudaSuccess) return e;
+    fa.cfg = cfg;
+    fa.K = (const __nv_bfloat16*)K;
+    fa.V = (const __nv_bfloat16*)V;
+    fa.T = rg.nkv;
+    fa.ks = (__nv_bfloat16*)Ksum;
+    fa.vs = (__nv_bfloat16*)Vsum;
+    fa.eps = eps;
+    fa.ws = ws;
+    fa.nC = nC;
+    fa.n_qt = n_qt;
+    fa.units = BH;
+    fa.total = n_qt * BH;
+    static const int order = [] {
+      const char* e = getenv("EVA_FUSED_ORDER");
+      return e ? atoi(e) : 1;
+    }();
+    fa.order = order;
+    grid = dim3(n_qt * BH, 1);
+  }
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  cudaError_t e = launch_pdl(prefill_persist_kernel<D, NSTAGE>, dim3(grid), dim3(NTHREADS), smem, s, mQ, mK, mV,
-                             mKs, mVs, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
-                             cfg.summary_bias * 1.4426950408889634f, lse, (__nv_bfloat16*)O, n_qt, n_items);
+  cudaError_t e = launch_pdl(kern, grid, dim3(FUSED ? NTHREADS_F : NTHREADS), smem, s, mQ, mK, mV,
+                             mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
+                             cfg.summary_bias * 1.4426950408889634f, lse, overlap ? 1 : 0, tile_sum_first(), fa);
   if (e != cudaSuccess) return e;
-  note_launch();
-  return cudaGetLastError();
-}
-
-template <int D, int NSTAGE>
-cudaError_t launch_split(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                         const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
-  const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
-  CUtensorMap mQ, mK, mV, mKs, mVs, mO;
-  bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BN) &&
-            make_map(&mV, V, BH, T, D, BN) && make_map(&mO, O, BH, T, D, BM);
-  if (nC > 0) {
-    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BN) && make_map(&mVs, Vsum, BH, nC, D, BN);
-  } else {
-    mKs = mK;
-    mVs = mV;
-  }
-  if (!ok) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(Smem2<D, NSTAGE>) + 1024;
-  {
-    cudaError_t e = set_smem_attr((const void*)prefill_split_kernel<D, NSTAGE>, smem);
-    if (e != cudaSuccess) return e;
-  }
-  dim3 grid((T + BM - 1) / BM, BH);
-  const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  prefill_split_kernel<D, NSTAGE><<<grid, NTHREADS2, smem, s>>>(mQ, mK, mV, mKs, mVs, mO, T, cfg.chunk,
-                                                               cfg.window, cfg.mode, scale_log2, lse);
-  note_launch();
-  return cudaGetLastError();
-}
-
-template <int D, int NSK, int NSV>
-cudaError_t launch_wide(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                        const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
-  const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
-  CUtensorMap mQ, mK, mV, mKs, mVs, mO;
-  bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BNW) &&
-            make_map(&mV, V, BH, T, D, BNW) && make_map(&mO, O, BH, T, D, BM);
-  if (nC > 0) {
-    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BNW) && make_map(&mVs, Vsum, BH, nC, D, BNW);
-  } else {
-    mKs = mK;
-    mVs = mV;
-  }
-  if (!ok) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(SmemWide<D, NSK, NSV>) + 1024;
-  {
-    cudaError_t e = set_smem_attr((const void*)prefill_wide_kernel<D, NSK, NSV>, smem);
-    if (e != cudaSuccess) return e;
-  }
-  dim3 grid((T + BM - 1) / BM, BH);
-  const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  prefill_wide_kernel<D, NSK, NSV><<<grid, NTHREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, mO, T, cfg.chunk,
-                                                               cfg.window, cfg.mode, scale_log2, lse);
-  note_launch();
-  return cudaGetLastError();
-}
-
-template <int D, int NS, bool TRACE = false>
-cudaError_t launch_pair(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                        const void* Ksum, const void* Vsum, void* O, float* lse, cudaStream_t s) {
-  const int BH = cfg.bh_count, T = cfg.T, nC = T / cfg.chunk;
-  CUtensorMap mQ, mK, mV, mKs, mVs;
-  bool ok = make_map(&mQ, Q, BH, T, D, BM) && make_map(&mK, K, BH, T, D, BN) &&
-            make_map(&mV, V, BH, T, D, BN);
-  if (nC > 0) {
-    ok = ok && make_map(&mKs, Ksum, BH, nC, D, BN) && make_map(&mVs, Vsum, BH, nC, D, BN);
-  } else {
-    mKs = mK;
-    mVs = mV;
-  }
-  if (!ok) return cudaErrorInvalidValue;
-  const size_t smem = sizeof(SmemPair<D, NS>) + 1024 + (TRACE ? sizeof(TraceLog) : 0);
-  {
-    cudaError_t e = set_smem_attr((const void*)prefill_pair_kernel<D, NS, TRACE>, smem);
-    if (e != cudaSuccess) return e;
-  }
-  const int ppu = (T + 2 * BM - 1) / (2 * BM);
-  const int64_t items = (int64_t)BH * ppu;
-  const int grid = (int)std::min<int64_t>(items, num_sms());  // 1 CTA/SM: all CTAs co-resident
-  const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  prefill_pair_kernel<D, NS, TRACE><<<grid, PAIR_THREADS, smem, s>>>(mQ, mK, mV, mKs, mVs, BH, T, cfg.chunk,
-                                                              cfg.window, cfg.mode, scale_log2,
-                                                              (__nv_bfloat16*)O, lse);
   note_launch();
   return cudaGetLastError();
 }
@@ -2019,25 +1104,18 @@ bool make_tma_map_bf16(CUtensorMap* m, const void* base, int units, int rows, in
   return make_map(m, base, units, rows, D, box_rows);
 }
 
-cudaError_t debug_trace_prefill(const eva_config& cfg, const void* Q, const void* K, const void* V,
-                                const void* Ksum, const void* Vsum, void* O, float* lse,
-                                unsigned long long* trace_dev, int cap, cudaStream_t s) {
-  cudaError_t e = cudaMemcpyToSymbolAsync(g_trace, &trace_dev, sizeof(trace_dev), 0, cudaMemcpyHostToDevice, s);
-  const int zero = 0;
-  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(g_trace_n, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(g_trace_cap, &cap, sizeof(int), 0, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return e;
-  if (cfg.d_head == 128) return launch_pair<128, 4, true>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-  if (cfg.d_head == 64) return launch_pair<64, 8, true>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-  return cudaErrorNotSupported;
-}
-
 cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K, const void* V,
                              const void* Ksum, const void* Vsum, void* O, float* lse,
-                             unsigned long long* trace_dev, cudaStream_t s) {
+                             unsigned long long* trace_dev, bool fused, cudaStream_t s) {
   cudaError_t e = cudaMemcpyToSymbolAsync(g_trace2, &trace_dev, sizeof(trace_dev), 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
   const PrefillRange rg = full_range(cfg);
+  if (fused) {  // traced for C = 64 (the configs' chunk size)
+    if (!prefill_fused_supported(cfg) || cfg.chunk != 64) return cudaErrorNotSupported;
+    if (cfg.d_head == 128)
+      return launch_t<128, 2, true, -1, 64>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr);
+    return launch_t<64, 3, true, -1, 64>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr);
+  }
   if (cfg.d_head == 128) return launch_t<128, 2, true>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   if (cfg.d_head == 64) return launch_t<64, 3, true>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   return cudaErrorNotSupported;
@@ -2047,53 +1125,44 @@ bool prefill_sm100_supported(const eva_config& cfg) {
   return cfg.dtype == EVA_BF16 && (cfg.d_head == 64 || cfg.d_head == 128) && encode_fn() != nullptr;
 }
 
+// The in-kernel summaries (EVA_SUMMARIES_FUSED): causal modes, whole-sequence call, chunks of
+// 16, 32 or 64 rows (whole chunks per 64-key tile, at most 4 of them).
+bool prefill_fused_supported(const eva_config& cfg) {
+  if (!prefill_sm100_supported(cfg) || cfg.mode == EVA_NONCAUSAL) return false;
+  return cfg.chunk == 16 || cfg.chunk == 32 || cfg.chunk == 64;
+}
+
 cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, const void* Q,
                                  const void* K, const void* V, const void* Ksum, const void* Vsum,
                                  void* O, float* lse, uint32_t variant, cudaStream_t s) {
   if (cfg.bh_count == 0) return cudaSuccess;
   const bool overlap = (variant & 0x100u) != 0;  // EVA_PREFILL_OVERLAP
-  variant &= 0xffu;
-  const PrefillRange full = full_range(cfg);
-  if (rg.q0 != full.q0 || rg.nq != full.nq || rg.k0 != full.k0 || rg.nkv != full.nkv || rg.nsl != full.nsl)
-    variant = 1;  // query-range calls: the one-tile-per-CTA kernel only
-  if (cfg.mode == EVA_NONCAUSAL || cfg.summary_bias != 0.f) variant = 1;  // variants: tile kernel only
-  // The one-tile-per-CTA kernel (two CTAs per SM) is the default: on B200 it beats the
-  // persistent pair kernel at every measured size (configs[2]: 0.65 vs 0.90 ms); the pair
-  // kernel stays selectable for experiments (EVA_PREFILL_TC_PAIR).
-  bool pair = false;
-  if (variant == 1) pair = false;
-  if (variant == 2) pair = true;
-  if (variant == 5) {
-    if (cfg.d_head == 128) return launch_persist<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-    if (cfg.d_head == 64) return launch_persist<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-  }
-  if (variant == 4) {
-    if (cfg.d_head == 128) return launch_split<128, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-    if (cfg.d_head == 64) return launch_split<64, 3>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-  }
-  if (variant == 3) {
-    if (cfg.d_head == 128) return launch_wide<128, 1, 1>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-    if (cfg.d_head == 64) return launch_wide<64, 2, 2>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-  }
-  if (pair) {
-    if (cfg.d_head == 128) return launch_pair<128, 5>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-    if (cfg.d_head == 64) return launch_pair<64, 8>(cfg, Q, K, V, Ksum, Vsum, O, lse, s);
-  } else {
-    // ring depths of the tile kernel (EVA_PREFILL_RING overrides: "2"/"32" at d=128, "3"/"54" at d=64)
-    static const int ring = [] {
-      const char* e = getenv("EVA_PREFILL_RING");
-      return e ? atoi(e) : 0;
-    }();
-    if (cfg.d_head == 128) {
-      if (ring == 32) return launch_t<128, 32>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
-      return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
-    }
-    if (cfg.d_head == 64) {
-      if (ring == 54) return launch_t<64, 54>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
-      return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
-    }
-  }
+  if (cfg.d_head == 128) return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
+  if (cfg.d_head == 64) return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
   return cudaErrorNotSupported;
+}
+
+cudaError_t launch_prefill_sm100_fused(const eva_config& cfg, const void* Q, const void* K, const void* V,
+                                       const float* eps, void* Ksum, void* Vsum, void* O, float* lse,
+                                       cudaStream_t s) {
+  if (cfg.bh_count == 0) return cudaSuccess;
+  if (!prefill_fused_supported(cfg)) return cudaErrorNotSupported;
+  const PrefillRange rg = full_range(cfg);
+#define EVA_FUSED_LAUNCH(D_, NS_)                                                                     \
+  switch (cfg.chunk) {                                                                                \
+    case 16: return launch_t<D_, NS_, false, -1, 16>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, eps); \
+    case 32: return launch_t<D_, NS_, false, -1, 32>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, eps); \
+    default: return launch_t<D_, NS_, false, -1, 64>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, eps); \
+  }
+  if (cfg.d_head == 128) EVA_FUSED_LAUNCH(128, 2)
+  if (cfg.d_head == 64) EVA_FUSED_LAUNCH(64, 3)
+#undef EVA_FUSED_LAUNCH
+  return cudaErrorNotSupported;
+}
+
+cudaError_t prefill_fused_reserve(const eva_config& cfg, cudaStream_t s) {
+  uint32_t* ws = nullptr;
+  return fused_workspace((size_t)cfg.bh_count * ((cfg.T + BM - 1) / BM), s, &ws);
 }
 
 }  // namespace eva

@@ -1,4 +1,4 @@
-set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -8
-timeout 1200 python -m pytest tests -q -m gpu --timeout 300 -x 2>&1 | tail -30
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -q -m gpu --timeout 300 -x 2>&1 | tail -8 > gpurun_out/tests_full.txt
+cat gpurun_out/tests_full.txt
+timeout 300 python scripts/time_prefill.py 2>&1 | tail -8

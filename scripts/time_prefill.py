@@ -1,4 +1,6 @@
-"""Time the tensor-core prefill variants at configs[2]'s per-GPU shape (dev tool)."""
+"""Time the prefill step (summaries + attention) at configs[1] and configs[2]'s per-GPU shapes:
+fused (EVA_SUMMARIES_FUSED, one launch), separate (eva_summarize + attention, two launches)
+and the attention alone with the summaries provided (dev tool).  L2 flushed before each step."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -11,19 +13,26 @@ for (B, H, T, d, C, W) in shapes:
     ks, vs = eva.eva_summarize(cfg, K, V)
     O = torch.empty_like(Q)
     flush = torch.empty(512 << 18, device="cuda")
-    for kern in sys.argv[1:] or ["tile", "split"]:
+    runs = {
+        "fused": lambda: eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, O=O, kernel="fused"),
+        "separate": lambda: eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, O=O, kernel="separate"),
+        "attention_only": lambda: eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, O=O,
+                                                       summaries_provided=True),
+    }
+    for name in sys.argv[1:] or list(runs):
+        f = runs[name]
         for _ in range(3):
-            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, kernel=kern)
+            f()
         ts = []
-        for _ in range(10):
+        for _ in range(20):
             flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, kernel=kern)
+            f()
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
         ts.sort()
         nC = T // C
         gb = B * H * (4 * T * d * 2 + 2 * nC * d * 2 + 4 * T) / 1e9
-        print(f"T={T} d={d} {kern}: median {ts[5]*1e3:.1f} us  min {ts[0]*1e3:.1f} us  -> {gb / (ts[5] / 1e3):.0f} GB/s")
+        print(f"T={T} d={d} {name}: median {ts[10]*1e3:.1f} us  min {ts[0]*1e3:.1f} us  -> {gb / (ts[10] / 1e3):.0f} GB/s")

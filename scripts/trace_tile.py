@@ -1,5 +1,5 @@
 """Timeline of 4 CTAs of the one-tile-per-CTA prefill kernel (dev tool).
-    python scripts/trace_tile.py B H T d C W"""
+    python scripts/trace_tile.py B H T d C W [fused]"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -8,25 +8,29 @@ import paper_2511_00576_b200 as eva
 from paper_2511_00576_b200 import _native as N
 
 B, H, T, d, C, W = (int(x) for x in sys.argv[1:7]) if len(sys.argv) > 6 else (1, 16, 2048, 64, 64, 128)
+FUSED = "fused" in sys.argv[7:]
+R = 4  # roles per CTA slot
 cfg = eva.make_config(B, H, T, d, C, W)
 Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device="cuda")
 ks, vs = eva.eva_summarize(cfg, K, V)
 O = torch.empty_like(Q)
 lse = torch.empty(B * H, T, device="cuda")
-tr = torch.zeros(4 * 3 * 48, dtype=torch.int64, device="cuda")
+tr = torch.zeros(4 * R * 48, dtype=torch.int64, device="cuda")
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 flush = torch.empty(512 << 18, device="cuda")
 for _ in range(3):
     flush.zero_()
-    N.check(N.lib.eva_debug_trace_prefill(ctypes.byref(cfg), P(Q), P(K), P(V), P(ks), P(vs), P(O), P(lse), P(tr), 1000, st))
+    N.check(N.lib.eva_debug_trace_prefill(ctypes.byref(cfg), P(Q), P(K), P(V), P(ks), P(vs), P(O), P(lse), P(tr), 2 if FUSED else 1000, st))
 torch.cuda.synchronize()
 names = {1: "start", 2: "MMA: Q arrived", 3: "MMA: K(j) arrived", 4: "MMA: S(j) issued", 5: "MMA: P(j) seen",
          6: "MMA: PV(j) issued", 7: "SM: got S(j)", 8: "SM: P(j) done", 9: "EPI: O final", 10: "EPI: stored",
-         11: "TMA: slot free(j)", 12: "TMA: issued(j)"}
+         11: "TMA: slot free(j)", 12: "TMA: issued(j)", 13: "SUM: tile j landed", 14: "SUM: tile j done",
+         15: "SUM: published", 16: "TMA: flag wait", 17: "TMA: flags ready",
+         18: "SUM: k~ sums (c)", 19: "SUM: omega (c)", 20: "SUM: logits (c)", 21: "SUM: beta (c)"}
 v = [int(x) & 0xFFFFFFFFFFFFFFFF for x in tr.cpu().tolist()]
 for slot in range(4):
-    ev = [x for x in v[slot * 144:(slot + 1) * 144] if x]
+    ev = [x for x in v[slot * R * 48:(slot + 1) * R * 48] if x]
     if not ev:
         continue
     ev.sort(key=lambda x: x >> 24)

@@ -117,21 +117,32 @@ CASES = [  # (B, H, T, d, C, W)
 ]
 
 
+def fused_applies(d, C, mode="sliding"):
+    """EVA_SUMMARIES_FUSED envelope (include/eva.h): d in {64, 128}, causal, C in {16, 32, 64}."""
+    return d in (64, 128) and mode != "noncausal" and C in (16, 32, 64)
+
+
 @pytest.mark.parametrize("mode", ["sliding", "block"])
 @pytest.mark.parametrize("case", CASES)
 @pytest.mark.parametrize("dtype,kernel", [(torch.float32, "simt"), (torch.bfloat16, "simt"),
-                                          (torch.bfloat16, "tile"), (torch.bfloat16, "pair"),
-                                          (torch.bfloat16, "wide"), (torch.bfloat16, "persist")])
-def test_prefill_parity(eva, case, mode, dtype, kernel):
+                                          (torch.bfloat16, "separate"), (torch.bfloat16, "fused"),
+                                          (torch.bfloat16, None)])
+@pytest.mark.parametrize("caller_eps", [False, True])
+def test_prefill_parity(eva, case, mode, dtype, kernel, caller_eps):
     B, H, T, d, C, W = case
-    if kernel in ("tile", "pair", "wide", "persist") and d not in (64, 128):
+    if kernel in ("separate", "fused") and d not in (64, 128):
         pytest.skip("tensor-core kernels cover d in {64, 128}; other d run the SIMT kernel")
+    if kernel == "fused" and not fused_applies(d, C, mode):
+        pytest.skip("outside the in-kernel summaries' envelope (test_fused_flag_rejected_outside_envelope)")
+    if caller_eps and kernel not in ("fused", "simt"):
+        pytest.skip("caller eps: covered on the fused and SIMT paths")
     cfg = eva.make_config(B, H, T, d, C, W, mode=mode, dtype=dtype, seed=7)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=2, device="cuda")
-    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, kernel=kernel)
-    torch.cuda.synchronize()
     nC = T // C
-    E = oracle_eps_for(cfg, nC, d)
+    eps = eva_inputs.eps(0, B * H, nC, d, device="cuda") if caller_eps and nC else None
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, kernel=kernel, eps=eps)
+    torch.cuda.synchronize()
+    E = f64(eps) if eps is not None else oracle_eps_for(cfg, nC, d)
     m = oracle.SLIDING if mode == "sliding" else oracle.BLOCK
     rk, rv, rO, rl = run_oracle(Q, K, V, E, C, W, m, cfg.scale)
     tol = TOL[dtype]
@@ -155,8 +166,7 @@ def test_prefill_window_covers_sequence_is_softmax(eva, dtype, simt):
     assert (O.double() - ref).abs().max().item() <= TOL[dtype]
 
 
-@pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, "tile"),
-                                               (torch.bfloat16, False, "pair"), (torch.bfloat16, False, "wide")])
+@pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, None)])
 def test_prefill_summaries_provided_and_poison(eva, dtype, simt, kernel):
     """Everything a query block must not see is poisoned with large finite values;
     its outputs must not move (bit-exact).  Uses EVA_SUMMARIES_PROVIDED."""
@@ -225,9 +235,8 @@ def test_prefill_detects_beta_perturbation(eva):
     assert np.array_equal(moved, sees)
 
 
-@pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, "tile"),
-                                               (torch.bfloat16, False, "pair"), (torch.bfloat16, False, "wide"),
-                                               (torch.bfloat16, False, "persist")])
+@pytest.mark.parametrize("dtype,simt,kernel", [(torch.float32, True, None), (torch.bfloat16, False, "separate"),
+                                               (torch.bfloat16, False, "fused")])
 def test_sharded_equals_unsharded(eva, dtype, simt, kernel):
     """(b,h) shards computed separately are bitwise equal to the full run (RNG keyed by global unit)."""
     B, H, T, d, C, W = 2, 3, 384, 64, 32, 64
@@ -471,8 +480,9 @@ def test_decode_capacity_error(eva):
 
 
 # ----------------------------------------------------------------------------- full-size sampled parity
-@pytest.mark.parametrize("kernel", [None, "tile", "pair", "wide"])
-@pytest.mark.parametrize("B,H,T,d,C,W", [(1, 16, 2048, 64, 64, 128), (1, 4, 8192, 128, 64, 256)])
+@pytest.mark.parametrize("kernel", ["fused", "separate"])
+@pytest.mark.parametrize("B,H,T,d,C,W", [(1, 16, 2048, 64, 64, 128), (1, 4, 8192, 128, 64, 256),
+                                         (8, 32, 8192, 128, 64, 256)])
 def test_full_size_sampled_parity(eva, B, H, T, d, C, W, kernel):
     """BASELINE configs[1] (full) and configs[2] (4 of its 256 units, same kernel launch
     shape per unit) on the bf16 tensor-core path; oracle on sampled rows."""
@@ -481,7 +491,7 @@ def test_full_size_sampled_parity(eva, B, H, T, d, C, W, kernel):
     O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, kernel=kernel)
     nC = T // C
     rng = np.random.default_rng(1)
-    for u in (0, B * H - 1):
+    for u in sorted({0, B * H // 2 + 1, B * H - 1}):
         E = oracle.eps(cfg.seed, cfg.layer, u, nC, d)
         rk, rv = oracle.summarize(f64(K[u]), f64(V[u]), E, C)
         assert np.max(np.abs(f64(ks[u]) - rk)) <= 2e-2
@@ -517,14 +527,96 @@ def test_long_context_sweep_sampled_parity(eva, T, C, W):
         assert np.max(np.abs(f64(lse[u])[rows] - rl)) <= 2e-2
 
 
+# ----------------------------------------------------------------------------- fused summaries
 @pytest.mark.parametrize("d", [64, 128])
-def test_persistent_prefill_equals_tile_kernel(eva, d):
-    """The persistent tile kernel walks the same tiles in the same order as the
-    one-tile-per-CTA kernel: bitwise equal results (many items per CTA, ragged tail)."""
-    B, H, T, C, W = 4, 40, 1000, 64, 256
-    cfg = eva.make_config(B, H, T, d, C, W)
+@pytest.mark.parametrize("mode", ["sliding", "block"])
+def test_fused_equals_separate(eva, d, mode):
+    """EVA_SUMMARIES_FUSED vs EVA_SUMMARIES_SEPARATE on the same inputs: the summaries agree to
+    one bf16 rounding step (fp32 summation order differs), and the attention of the fused call
+    equals the separate kernel run on the fused call's own summaries up to the tile walk order."""
+    B, H, T, C, W = 3, 7, 1000, 32, 128
+    cfg = eva.make_config(B, H, T, d, C, W, mode=mode)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=31, device="cuda")
-    O1, l1, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, kernel="tile")
-    O2, l2, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, kernel="persist")
+    O1, l1, ks1, vs1 = eva.eva_attn_prefill(cfg, Q, K, V, kernel="fused")
+    O2, l2, ks2, vs2 = eva.eva_attn_prefill(cfg, Q, K, V, kernel="separate")
+    O3, l3, _, _ = eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks1, Vsum=vs1, summaries_provided=True)
     torch.cuda.synchronize()
-    assert torch.equal(O1, O2) and torch.equal(l1, l2)
+    # one bf16 rounding step of the value, plus fp32 summation-order noise near zero
+    ulp = lambda x: x.float().abs() * 2.0 ** -7 + 1e-5
+    assert bool(((ks1.float() - ks2.float()).abs() <= ulp(ks2)).all())
+    assert bool(((vs1.float() - vs2.float()).abs() <= ulp(vs2)).all())
+    # the same math in another tile order: within two bf16 rounding steps of the output
+    assert bool(((O1.float() - O3.float()).abs() <= 2.0 ** -6 * O3.float().abs().clamp_min(1.0)).all())
+    assert (l1 - l3).abs().max().item() <= 1e-3
+
+
+def test_fused_deterministic_across_launches_shapes_and_graphs(eva):
+    """The fused launch's workspace (ticket, done counter, epoch, ready flags) is reused across
+    launches of different shapes and inside a CUDA graph: the results stay bitwise identical
+    (no stale flag is ever taken for a fresh one, the counters are left consistent)."""
+    shapes = [(1, 16, 2048, 64, 64, 128), (2, 5, 777, 128, 16, 64), (1, 16, 2048, 64, 64, 128),
+              (4, 3, 300, 64, 16, 16), (2, 5, 777, 128, 16, 64)]
+    first = {}
+    for rep in range(2):
+        for sh in shapes:
+            B, H, T, d, C, W = sh
+            cfg = eva.make_config(B, H, T, d, C, W)
+            Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=sum(sh), device="cuda")
+            out = eva.eva_attn_prefill(cfg, Q, K, V, kernel="fused")
+            torch.cuda.synchronize()
+            if sh not in first:
+                first[sh] = [t.clone() for t in out]
+            for a, b in zip(out, first[sh]):
+                assert torch.equal(a, b), sh
+    B, H, T, d, C, W = shapes[1]
+    cfg = eva.make_config(B, H, T, d, C, W)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=sum(shapes[1]), device="cuda")
+    O, lse = torch.zeros_like(Q), torch.zeros(B * H, T, device="cuda")
+    ks = torch.zeros(B * H, T // C, d, dtype=torch.bfloat16, device="cuda")
+    vs = torch.zeros_like(ks)
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        eva.eva_prefill_reserve(cfg)  # on the capture stream: torch.cuda.graph(stream=s) below
+        with torch.cuda.graph(g, stream=s):
+            eva.eva_attn_prefill(cfg, Q, K, V, kernel="fused", O=O, lse=lse, Ksum=ks, Vsum=vs)
+    for _ in range(5):
+        O.zero_(); ks.zero_(); vs.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        ref = first[shapes[1]]
+        assert torch.equal(O, ref[0]) and torch.equal(lse, ref[1])
+        assert torch.equal(ks, ref[2]) and torch.equal(vs, ref[3])
+
+
+def test_fused_flag_rejected_outside_envelope(eva):
+    """EVA_SUMMARIES_FUSED where it does not apply is an error, not a silent fallback; flags 0
+    there runs the separate launches and matches the oracle (test_prefill_parity)."""
+    Q = torch.zeros(2, 256, 64, dtype=torch.bfloat16, device="cuda")
+    for kw in (dict(chunk=128, window=256), dict(chunk=8, window=16), dict(chunk=16, window=32, mode="noncausal")):
+        cfg = eva.make_config(1, 2, 256, 64, kw["chunk"], kw["window"], mode=kw.get("mode", "sliding"))
+        with pytest.raises(eva.EvaError, match="UNSUPPORTED"):
+            eva.eva_attn_prefill(cfg, Q, Q, Q, kernel="fused")
+    cfg = eva.make_config(1, 2, 256, 64, 16, 32, dtype=torch.float32)
+    with pytest.raises(eva.EvaError, match="UNSUPPORTED"):
+        eva.eva_attn_prefill(cfg, Q.float(), Q.float(), Q.float(), kernel="fused")
+
+
+def test_fused_many_waves_sampled_parity(eva):
+    """Many more query tiles than resident CTAs (ticket order, flags awaited across waves), a
+    ragged tail and W = C (a tile reads the summaries of its own rows): oracle on sampled units."""
+    B, H, T, d, C, W = 4, 64, 1100, 64, 16, 16
+    cfg = eva.make_config(B, H, T, d, C, W)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=77, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill(cfg, Q, K, V, kernel="fused")
+    nC = T // C
+    for u in (0, 101, B * H - 1):
+        E = oracle.eps(cfg.seed, cfg.layer, u, nC, d)
+        rk, rv = oracle.summarize(f64(K[u]), f64(V[u]), E, C)
+        assert np.max(np.abs(f64(ks[u]) - rk)) <= 2e-2
+        assert np.max(np.abs(f64(vs[u]) - rv)) <= 2e-2
+        rows = np.arange(T)
+        rows, rO, rl = oracle.prefill_rows(f64(Q[u]), f64(K[u]), f64(V[u]), rk, rv, rows, C, W, 0, cfg.scale)
+        assert np.max(np.abs(f64(O[u])[rows] - rO)) <= 2e-2
+        assert np.max(np.abs(f64(lse[u])[rows] - rl)) <= 2e-2
