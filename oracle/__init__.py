@@ -57,6 +57,7 @@ def _L():
         lib.oracle_summarize.argtypes = [i, i, i, D, D, D, d_, d_, i, D, D, D]
         lib.oracle_summarize_proj.argtypes = [i, i, i, D, D, D, D, d_, d_, i, D, D, D]
         lib.oracle_rope.argtypes = [i, i, d_, ctypes.c_int64, D]
+        lib.oracle_rope_ex.argtypes = [i, i, d_, i, i, I64, i, D]
         lib.oracle_prefill.argtypes = [i, i, i, i, i, d_, D, D, D, D, D, D, D]
         lib.oracle_summarize_batch.argtypes = [i, i, i, i, D, D, D, d_, d_, i, D, D]
         lib.oracle_prefill_batch.argtypes = [i, i, i, i, i, i, d_, D, D, D, D, D, D, D]
@@ -144,6 +145,24 @@ def rope(X, base: float = 10000.0, pos0: int = 0):
     X = _f64(X).copy()
     T, d = X.shape
     _L().oracle_rope(T, d, base, pos0, _dp(X))
+    return X
+
+
+ROPE_INTERLEAVED = 0
+ROPE_NEOX = 1
+
+
+def rope_ex(X, pos, base: float = 10000.0, rotary_dim=None, style: int = ROPE_INTERLEAVED,
+            inverse: bool = False):
+    """Generalised RoPE (oracle_rope_ex, R19) of rows X [T, d] at positions pos [T] (int):
+    the first rotary_dim (default d) channels rotate, pairs (2j, 2j+1) (style 0) or
+    (j, j + rd/2) (style 1, GPT-NeoX), angle pos * base^(-2j/rd); inverse = the transpose."""
+    X = _f64(X).copy()
+    T, d = X.shape
+    rd = d if rotary_dim is None else int(rotary_dim)
+    p = np.ascontiguousarray(np.broadcast_to(np.asarray(pos, dtype=np.int64), (T,)))
+    _L().oracle_rope_ex(T, d, base, rd, int(style), p.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                        1 if inverse else 0, _dp(X))
     return X
 
 

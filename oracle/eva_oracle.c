@@ -137,6 +137,29 @@ EXPORT void oracle_rope(int T, int d, double base, int64_t pos0, double* X) {
   }
 }
 
+/* Generalised RoPE (NEXT row 4, DESIGN R19): only the first rd channels rotate (rd even;   */
+/* channels >= rd pass through, e.g. Pythia's rotary_pct), angle pos * base^(-2j/rd)  */
+/* for pair j < rd/2, and the pair of j is either (2j, 2j+1) ("interleaved", style 0) or     */
+/* (j, j + rd/2) (GPT-NeoX "half-split", style 1):                                          */
+/*   y_a = x_a cos t - x_b sin t,   y_b = x_a sin t + x_b cos t      (a, b) = the pair j.    */
+/* Row t of X [T, d] (in place) is at position pos[t].  inverse != 0: the transpose, i.e.   */
+/* the rotation by -t (the gradient through RoPE).                                          */
+EXPORT void oracle_rope_ex(int T, int d, double base, int rd, int style, const int64_t* pos, int inverse,
+                           double* X) {
+  for (int t = 0; t < T; ++t) {
+    double* x = X + (size_t)t * d;
+    for (int j = 0; j < rd / 2; ++j) {
+      const int a = style == 0 ? 2 * j : j;
+      const int b = style == 0 ? 2 * j + 1 : j + rd / 2;
+      const double ang = (double)pos[t] * pow(base, -2.0 * j / (double)rd);
+      const double c = cos(ang), s = inverse ? -sin(ang) : sin(ang);
+      const double x0 = x[a], x1 = x[b];
+      x[a] = x0 * c - x1 * s;
+      x[b] = x0 * s + x1 * c;
+    }
+  }
+}
+
 /* P (NEXT row 4, DESIGN R17; may be NULL = identity): the learned summary-key projection,  */
 /* k~_c = P (1/C) sum_i k_{cC+i} with P [d, d] row-major; mu_c = k~_c as in R2.            */
 EXPORT void oracle_summarize_proj(int T, int d, int C, const double* K, const double* V,
