@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -14,6 +15,7 @@
 #include "launch.h"
 #include "summarize.cuh"
 #include "summarize_cta.cuh"
+#include "summarize_reg.cuh"
 
 namespace eva {
 
@@ -56,175 +58,6 @@ __global__ void __launch_bounds__(SUMM_THREADS) summarize_cta_kernel(eva_config 
   summarize_chunk_cta<T, D>(rowK, rowV, C, e, (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
                             Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D, smem);
 }
-
-// Register-resident variant (the default when C <= 32 * 128 * 16 / (D * sizeof(T))):
-// one CTA (4 warps) per chunk; a row is read by TPR = D*sizeof(T)/16 lanes with one 16-byte
-// load each, a warp covers RPW = 32/TPR rows per load and warp w owns the row slots
-// w*RPW + 4*RPW*i.  Every K and V piece of the chunk is loaded up front (up to 2*NI
-// 16-byte loads in flight per lane) and kept in registers: column sums -> k~ (smem merge
-// of the 4 warps), Eq.15 -> omega, per-row log-xi logits (group shuffles), per-warp
-// online softmax of the rows -> partial (m, l, acc), merged across warps in smem.
-// Pk (may be nullptr): the learned summary-key projection of NEXT row 4 (reading R17),
-// k~ = Pk mean(k) with Pk [D, D] row-major fp32 of this unit's head; omega uses mu = k~.
-struct NoKXform {
-  __device__ __forceinline__ void operator()(int, int, uint4&) const {}
-};
-// KX (optional): applied to every loaded 16-byte key piece (row r, channel ch0) before any
-// use -- the fused RoPE producer rotates (and stores) the keys there.
-template <typename T, int D, int NI, typename RowK, typename RowV, typename KX = NoKXform>
-__device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV& rowV, int C,
-                                                    const float* eps_c, uint32_t bh_global,
-                                                    uint32_t chunk, const eva_config& cfg,
-                                                    T* ksum_out, T* vsum_out, const float* Pk = nullptr,
-                                                    const KX& kxf = KX()) {
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int TPR = D / VEC;
-  constexpr int RPW = 32 / TPR;
-  __shared__ float sh_sum[4][D];
-  __shared__ float sh_om[D];
-  __shared__ float sh_m[4], sh_l[4];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane / TPR, gl = lane % TPR, ch0 = gl * VEC;
-  uint4 kx[NI], vx[NI];
-#pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int r = warp * RPW + 4 * RPW * i + grp;
-    if (r < C) {
-      kx[i] = ldg16_stream(rowK(r) + ch0);
-      kxf(r, ch0, kx[i]);
-      vx[i] = ldg16_stream(rowV(r) + ch0);
-    }
-  }
-  // column sums
-  float cs[VEC];
-#pragma unroll
-  for (int j = 0; j < VEC; ++j) cs[j] = 0.f;
-#pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int r = warp * RPW + 4 * RPW * i + grp;
-    if (r < C) {
-      float k[VEC];
-      unpack16<T>(kx[i], k);
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) cs[j] += k[j];
-    }
-  }
-#pragma unroll
-  for (int o = TPR; o < 32; o <<= 1)
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], o);
-  if (grp == 0) {
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) sh_sum[warp][ch0 + j] = cs[j];
-  }
-  __syncthreads();
-  __shared__ float sh_mean[D];
-  if (Pk != nullptr) {  // the chunk mean first: every projected channel reads all of it
-    if (threadIdx.x < D) {
-      const int ch = threadIdx.x;
-      sh_mean[ch] = (sh_sum[0][ch] + sh_sum[1][ch] + sh_sum[2][ch] + sh_sum[3][ch]) * (1.0f / (float)C);
-    }
-    __syncthreads();
-  }
-  // k~ and omega (Eq.15); one Philox block per 4 channels
-  if (threadIdx.x < D / 4) {
-    const int q = threadIdx.x;
-    float e[4];
-    if (eps_c) {
-      const float* ep = eps_c + 4 * q;
-      e[0] = ep[0]; e[1] = ep[1]; e[2] = ep[2]; e[3] = ep[3];
-    } else {
-      const float4 z = philox_normal4(cfg.seed, cfg.layer, bh_global, chunk, (uint32_t)q);
-      e[0] = z.x; e[1] = z.y; e[2] = z.z; e[3] = z.w;
-    }
-    T* ko = ksum_out + 4 * q;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int ch = 4 * q + j;
-      float kt;
-      if (Pk == nullptr) {
-        kt = (sh_sum[0][ch] + sh_sum[1][ch] + sh_sum[2][ch] + sh_sum[3][ch]) * (1.0f / (float)C);
-      } else {
-        const float4* prow = reinterpret_cast<const float4*>(Pk + (size_t)ch * D);
-        kt = 0.f;
-#pragma unroll 4
-        for (int l4 = 0; l4 < D / 4; ++l4) {
-          const float4 w = __ldg(prow + l4);
-          kt = fmaf(w.x, sh_mean[4 * l4], kt);
-          kt = fmaf(w.y, sh_mean[4 * l4 + 1], kt);
-          kt = fmaf(w.z, sh_mean[4 * l4 + 2], kt);
-          kt = fmaf(w.w, sh_mean[4 * l4 + 3], kt);
-        }
-      }
-      sh_om[ch] = omega_of(kt, e[j], cfg);
-      ko[j] = Elem<T>::from_f(kt);
-    }
-  }
-  __syncthreads();
-  float om[VEC];
-#pragma unroll
-  for (int j = 0; j < VEC; ++j) om[j] = sh_om[ch0 + j];
-  // logits a_r = omega . k_r - |k_r|^2 / 2 and the warp's online softmax over its rows
-  float a[NI];
-  float m = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int r = warp * RPW + 4 * RPW * i + grp;
-    float part = 0.f;
-    if (r < C) {
-      float k[VEC];
-      unpack16<T>(kx[i], k);
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) part += k[j] * (om[j] - 0.5f * k[j]);
-    }
-    part = group_sum<TPR>(part);
-    a[i] = r < C ? part : -INFINITY;
-    m = fmaxf(m, a[i]);
-  }
-#pragma unroll
-  for (int o = TPR; o < 32; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float l = 0.f, acc[VEC];
-#pragma unroll
-  for (int j = 0; j < VEC; ++j) acc[j] = 0.f;
-#pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int r = warp * RPW + 4 * RPW * i + grp;
-    if (r < C) {
-      const float p = __expf(a[i] - m);
-      l += p;
-      float v[VEC];
-      unpack16<T>(vx[i], v);
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) acc[j] += p * v[j];
-    }
-  }
-#pragma unroll
-  for (int o = TPR; o < 32; o <<= 1) {
-    l += __shfl_xor_sync(0xffffffffu, l, o);
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
-  }
-  if (lane == 0) { sh_m[warp] = m; sh_l[warp] = l; }
-  __syncthreads();  // sh_sum is free again: reuse it for the partial accumulators
-  if (grp == 0) {
-#pragma unroll
-    for (int j = 0; j < VEC; ++j) sh_sum[warp][ch0 + j] = acc[j];
-  }
-  __syncthreads();
-  if (threadIdx.x < D) {
-    const int ch = threadIdx.x;
-    float M = fmaxf(fmaxf(sh_m[0], sh_m[1]), fmaxf(sh_m[2], sh_m[3]));
-    float L = 0.f, o = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float f = sh_m[w] == -INFINITY ? 0.f : __expf(sh_m[w] - M);
-      L += f * sh_l[w];
-      o += f * sh_sum[w][ch];
-    }
-    vsum_out[ch] = Elem<T>::from_f(o / L);
-  }
-}
-
 
 template <typename T, int D, int NI>
 __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, const T* __restrict__ K,
@@ -358,11 +191,6 @@ __global__ void __launch_bounds__(128) summarize_bcast_kernel(eva_config cfg, co
   }
 }
 
-// Rows per lane slot of the register summariser for (C, D, T); > 8 means "too large".
-template <typename T, int D>
-constexpr int summ_reg_ni(int C) {
-  return (C + 4 * (32 / (D * (int)sizeof(T) / 16)) - 1) / (4 * (32 / (D * (int)sizeof(T) / 16)));
-}
 
 // ============================================================================ SIMT prefill
 // One CTA = one unit x QT queries.  G threads cooperate on one query (thread gi
@@ -930,6 +758,14 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
                              void* Ksum, void* Vsum, cudaStream_t s, int c0, const float* Pk) {
   const int nC = cfg.T / cfg.chunk;
   if (nC == 0 || cfg.bh_count == 0) return cudaSuccess;
+  // bf16, d in {64, 128}, C in {16..128}: the persistent bulk-copy summariser (summarize_bulk.cu);
+  // EVA_SUMMARIZE_REG=1 keeps the register summariser (comparisons)
+  static const bool force_reg = [] {
+    const char* e = getenv("EVA_SUMMARIZE_REG");
+    return e && atoi(e) == 1;
+  }();
+  if (Pk == nullptr && !force_reg && summarize_bulk_supported(cfg))
+    return launch_summarize_bulk(cfg, K, V, eps, Ksum, Vsum, c0, s);
   cudaError_t err = cudaSuccess;
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
     const size_t sm = summ_smem_bytes(cfg.chunk, D, sizeof(T));

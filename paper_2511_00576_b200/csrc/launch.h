@@ -16,6 +16,11 @@ namespace eva {
 // cudaErrorNotSupported otherwise).
 cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V, const float* eps,
                              void* Ksum, void* Vsum, cudaStream_t s, int c0 = 0, const float* Pk = nullptr);
+// The persistent bulk-copy summariser (summarize_bulk.cu): bf16, d in {64, 128}, C in {16, 32,
+// 64, 128}; same contract as launch_summarize without the projection.
+bool summarize_bulk_supported(const eva_config& cfg);
+cudaError_t launch_summarize_bulk(const eva_config& cfg, const void* K, const void* V, const float* eps,
+                                  void* Ksum, void* Vsum, int c0, cudaStream_t s);
 // RoPE (or its inverse) of [bh_count, T, d] rows at positions pos0 + t (R18).
 cudaError_t launch_rope(const eva_config& cfg, float base, const void* X, void* Y, int64_t pos0, bool inverse,
                         cudaStream_t s);

@@ -1,0 +1,160 @@
+// summarize_bulk.cu -- bandwidth-shaped chunk summaries for bf16 (the default eva_summarize path
+// for d in {64, 128}, C in {16, 32, 64, 128}).
+//
+// Per chunk c of unit u (Eq.10 reading R1; Eq.15 readings R2, R3; log xi P:49;
+// P:92 Eq.9 with S = 1):
+//   k~_c    = (1/C) sum_i k_{cC+i}
+//   omega_c = lambda * clip(k~_c + eps_c)     (or R3's alternative, cfg.omega_mode)
+//   a_i     = omega_c . k_i - |k_i|^2 / 2
+//   beta^_c = sum_i softmax(a)_i v_i
+//
+// Why a separate kernel: the register summariser kernel (summarize_reg_kernel, one 128-thread CTA
+// per chunk) loads a whole chunk from global memory into registers and stops streaming while it
+// computes; with 105 registers it fits 4 CTAs per SM -- 0.66 of HBM at configs[2] (ncu: 24 %
+// warps active, long-scoreboard stalls on the loads).  Here a persistent CTA (grid = SMs x CTAs
+// per SM) walks chunks i = blockIdx.x, + gridDim.x, ...; a chunk's C key rows and C value rows
+// are each ONE contiguous C*d*2-byte block, brought into shared memory by a single bulk copy
+// (cp.async.bulk, mbarrier complete_tx), NST = 2 stages deep, so the next chunk streams in while
+// this one is computed.  The arithmetic is summarize_chunk_reg's (summarize_reg.cuh) with its
+// loads served from shared memory: the summaries are bitwise those of the register kernel, the
+// cache append and the decode step.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "launch.h"
+#include "sm100.cuh"
+#include "summarize_reg.cuh"
+
+namespace eva {
+namespace {
+
+using namespace sm100;
+constexpr int SB_THREADS = 128;
+
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct LdShared {
+  template <typename P>
+  __device__ __forceinline__ uint4 operator()(const P* p) const {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p)));
+    return v;
+  }
+};
+
+template <int D, int CC, int NST>
+struct alignas(128) SumSmem {
+  __nv_bfloat16 k[NST][CC * D];
+  __nv_bfloat16 v[NST][CC * D];
+  uint64_t full[NST];
+};
+
+template <int D, int CC, int NST>
+__global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config cfg, const __nv_bfloat16* __restrict__ K,
+                                                                   const __nv_bfloat16* __restrict__ V,
+                                                                   const float* __restrict__ eps,
+                                                                   __nv_bfloat16* __restrict__ Ksum,
+                                                                   __nv_bfloat16* __restrict__ Vsum, int c0,
+                                                                   int total) {
+  using S = SumSmem<D, CC, NST>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
+  constexpr uint32_t BYTES = CC * D * 2;
+  const int t = threadIdx.x;
+  const int nC = cfg.T / CC;
+  if (t == 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(&sm.full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  auto src_row = [&](int i) { return (size_t)(i / nC) * cfg.T + (size_t)(i % nC) * CC; };
+  auto issue = [&](int k, int i) {  // chunk i into stage k % NST
+    const int s = k % NST;
+    mbar_arrive_expect_tx(&sm.full[s], 2 * BYTES);
+    bulk_load(sm.k[s], K + src_row(i) * D, BYTES, &sm.full[s]);
+    bulk_load(sm.v[s], V + src_row(i) * D, BYTES, &sm.full[s]);
+  };
+  if (t == 0) {
+    for (int k = 0; k < NST; ++k) {
+      const int i = blockIdx.x + k * gridDim.x;
+      if (i < total) issue(k, i);
+    }
+  }
+  constexpr int NI = summ_reg_ni<__nv_bfloat16, D>(CC);
+  int k = 0;
+  for (int i = blockIdx.x; i < total; i += gridDim.x, ++k) {
+    const int s = k % NST;
+    const int u = i / nC, c = i % nC;
+    mbar_wait(&sm.full[s], (k / NST) & 1);
+    const __nv_bfloat16* Ks = sm.k[s];
+    const __nv_bfloat16* Vs = sm.v[s];
+    summarize_chunk_reg<__nv_bfloat16, D, NI>(
+        [&](int r) { return Ks + (size_t)r * D; }, [&](int r) { return Vs + (size_t)r * D; }, CC,
+        eps ? eps + ((size_t)u * nC + c) * D : nullptr, (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
+        Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D, nullptr, NoKXform(), LdShared());
+    __syncthreads();  // every thread is done with stage s
+    if (t == 0) {     // the chunk NST iterations ahead streams into it now
+      const int i2 = i + NST * gridDim.x;
+      if (i2 < total) issue(k + NST, i2);
+    }
+  }
+}
+
+template <int D, int CC>
+cudaError_t launch_bulk_t(const eva_config& cfg, const void* K, const void* V, const float* eps, void* Ksum,
+                          void* Vsum, int c0, cudaStream_t s) {
+  constexpr int NST = 2;
+  using S = SumSmem<D, CC, NST>;
+  const size_t smem = sizeof(S);
+  auto kern = summarize_bulk_kernel<D, CC, NST>;
+  cudaError_t e = set_smem_attr((const void*)kern, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SB_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  const int total = (cfg.T / CC) * cfg.bh_count;
+  const int grid = std::max(1, std::min(total, std::max(1, per_sm) * num_sms()));
+  e = launch_pdl(kern, dim3(grid), dim3(SB_THREADS), smem, s, cfg, (const __nv_bfloat16*)K,
+                 (const __nv_bfloat16*)V, eps, (__nv_bfloat16*)Ksum, (__nv_bfloat16*)Vsum, c0, total);
+  if (e != cudaSuccess) return e;
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool summarize_bulk_supported(const eva_config& cfg) {
+  return cfg.dtype == EVA_BF16 && (cfg.d_head == 64 || cfg.d_head == 128) &&
+         (cfg.chunk == 16 || cfg.chunk == 32 || cfg.chunk == 64 || cfg.chunk == 128);
+}
+
+cudaError_t launch_summarize_bulk(const eva_config& cfg, const void* K, const void* V, const float* eps,
+                                  void* Ksum, void* Vsum, int c0, cudaStream_t s) {
+  if (cfg.bh_count == 0 || cfg.T / cfg.chunk == 0) return cudaSuccess;
+#define EVA_BULK_C(D_)                                                                 \
+  switch (cfg.chunk) {                                                                  \
+    case 16: return launch_bulk_t<D_, 16>(cfg, K, V, eps, Ksum, Vsum, c0, s);           \
+    case 32: return launch_bulk_t<D_, 32>(cfg, K, V, eps, Ksum, Vsum, c0, s);           \
+    case 64: return launch_bulk_t<D_, 64>(cfg, K, V, eps, Ksum, Vsum, c0, s);           \
+    case 128: return launch_bulk_t<D_, 128>(cfg, K, V, eps, Ksum, Vsum, c0, s);         \
+    default: return cudaErrorNotSupported;                                              \
+  }
+  if (cfg.d_head == 128) EVA_BULK_C(128)
+  if (cfg.d_head == 64) EVA_BULK_C(64)
+#undef EVA_BULK_C
+  return cudaErrorNotSupported;
+}
+
+}  // namespace eva

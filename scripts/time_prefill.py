@@ -18,6 +18,7 @@ for (B, H, T, d, C, W) in shapes:
         "separate": lambda: eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, O=O, kernel="separate"),
         "attention_only": lambda: eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, O=O,
                                                        summaries_provided=True),
+        "summarize_only": lambda: eva.eva_summarize(cfg, K, V, Ksum=ks, Vsum=vs),
     }
     for name in sys.argv[1:] or list(runs):
         f = runs[name]
@@ -35,4 +36,6 @@ for (B, H, T, d, C, W) in shapes:
         ts.sort()
         nC = T // C
         gb = B * H * (4 * T * d * 2 + 2 * nC * d * 2 + 4 * T) / 1e9
+        if name == "summarize_only":
+            gb = B * H * (2 * T * d * 2 + 2 * nC * d * 2) / 1e9
         print(f"T={T} d={d} {name}: median {ts[10]*1e3:.1f} us  min {ts[0]*1e3:.1f} us  -> {gb / (ts[10] / 1e3):.0f} GB/s")

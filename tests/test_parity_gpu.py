@@ -88,6 +88,29 @@ def test_summarize_parity(eva, dtype, d, philox):
     assert np.max(np.abs(f64(vs) - rv)) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("C", [16, 32, 64, 128])
+@pytest.mark.parametrize("philox", [False, True])
+def test_summarize_bulk_parity(eva, d, C, philox):
+    """The bf16 persistent bulk-copy summariser (d in {64, 128}, C in {16..128}): many chunks
+    per CTA (more chunks than resident CTAs), a ragged tail (T % C != 0), a chunk range (c0)."""
+    B, H, T = 2, 37, 40 * C + C // 2
+    cfg = eva.make_config(B, H, T, d, C, 2 * C, seed=5)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=17, device="cuda")
+    nC = T // C
+    eps = None if philox else eva_inputs.eps(0, B * H, nC, d, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V, eps=eps)
+    E = oracle_eps_for(cfg, nC, d) if philox else f64(eps)
+    rk, rv = oracle.summarize_batch(f64(K), f64(V), E, C)
+    assert np.max(np.abs(f64(ks) - rk)) <= 2e-2
+    assert np.max(np.abs(f64(vs) - rv)) <= 2e-2
+    # the same rows as a range starting at absolute chunk 7 (its draws)
+    ks2, vs2 = eva.eva_summarize_range(cfg, 7, K, V)
+    E2 = np.stack([oracle.eps(cfg.seed, cfg.layer, u, 7 + nC, d)[7:] for u in range(B * H)])
+    rk2, rv2 = oracle.summarize_batch(f64(K), f64(V), E2, C)
+    assert np.max(np.abs(f64(ks2) - rk2)) <= 2e-2 and np.max(np.abs(f64(vs2) - rv2)) <= 2e-2
+
+
 def test_summarize_singleton_and_constant_chunks(eva):
     """C = 1 -> (k~, beta) = (k, v) exactly; a constant chunk -> its own (k, v)."""
     Q, K, V = eva_inputs.qkv(0, 2, 64, 64, torch.float32, seed=4, device="cuda")
