@@ -140,9 +140,40 @@ eva_status eva_rope_summarize(const eva_config* cfg, float rope_base, const void
  * positions pos0 + t (decode: q, k_new at their position with T = 1), or with inverse != 0
  * the transposed rotation Y = R(pos)^T X -- the gradient through RoPE: after
  * eva_attn_backward on (Qr, Kr, V) gives dQr, dKr, the pre-RoPE gradients are
- * dQ = R^T dQr, dK = R^T dKr.  X == Y (in place) is allowed. */
+ * dQ = R^T dQr, dK = R^T dKr.  X == Y (in place) is allowed.  = eva_rope_ex with
+ * {rope_base, d, EVA_ROPE_INTERLEAVED} and pos = NULL. */
 eva_status eva_rope(const eva_config* cfg, float rope_base, const void* X, void* Y, int64_t pos0,
                     int32_t inverse, eva_stream_t stream);
+
+/* Generalised RoPE (reading R19): which channels rotate and how they pair.
+ *   base       : > 1, finite (10000 in Pythia / GPT-NeoX)
+ *   rotary_dim : 0 = d; else even, <= d, a multiple of 2 * (16 / sizeof(dtype)) (16 for bf16,
+ *                8 for fp32) -- channels >= rotary_dim pass through (Pythia: rotary_pct)
+ *   style      : EVA_ROPE_INTERLEAVED -- pairs (2j, 2j+1); EVA_ROPE_NEOX -- pairs (j, j + rd/2)
+ *                (GPT-NeoX rotate_half); angle pos * base^(-2j/rd) for pair j < rd/2
+ *   reserved   : 0 */
+#define EVA_ROPE_INTERLEAVED 0
+#define EVA_ROPE_NEOX 1
+typedef struct eva_rope_params {
+  float base;
+  int32_t rotary_dim;
+  int32_t style;
+  int32_t reserved;
+} eva_rope_params;
+
+/* eva_rope_ex: Y = R(p) X (inverse: R(p)^T X) for rows [bh_count, T, d] cfg.dtype, row t of unit u
+ * at position p = (pos ? pos[u] : pos0) + t.  pos: NULL or a DEVICE int64 array [bh_count] of
+ * per-unit positions (>= 0, read by the kernel -- graph-capturable; a ragged decode batch rotates
+ * its q / k_new with the same pos array it passes to eva_decode_step_ragged).  X == Y allowed. */
+eva_status eva_rope_ex(const eva_config* cfg, const eva_rope_params* rp, const void* X, void* Y, int64_t pos0,
+                       const int64_t* pos, int32_t inverse, eva_stream_t stream);
+
+/* eva_rope_summarize_ex: eva_rope_summarize with eva_rope_params (R19).  The half-split style
+ * additionally needs rotary_dim / (2 * 16 / sizeof(dtype)) to be a power of two (the partner
+ * piece is exchanged between lanes by a butterfly), else EVA_ERR_UNSUPPORTED. */
+eva_status eva_rope_summarize_ex(const eva_config* cfg, const eva_rope_params* rp, const void* Q, const void* K,
+                                 const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
+                                 eva_stream_t stream);
 
 /* eva_summarize_proj: eva_summarize with the learned summary-key projection of SURVEY
  * §8(f) NEXT row 4 ("new weights"; EVA's summary key is a learned map of the chunk

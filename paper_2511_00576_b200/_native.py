@@ -22,6 +22,7 @@ EVA_SUMMARIES_FUSED = 2
 EVA_PREFILL_SIMT = 4
 EVA_SUMMARIES_SEPARATE = 16
 EVA_PREFILL_OVERLAP = 128
+EVA_ROPE_INTERLEAVED, EVA_ROPE_NEOX = 0, 1
 
 _STATUS = {0: "EVA_OK", 1: "EVA_ERR_INVALID_ARG", 2: "EVA_ERR_UNSUPPORTED", 3: "EVA_ERR_CAPACITY",
            4: "EVA_ERR_CUDA"}
@@ -39,6 +40,11 @@ class EvaConfig(ctypes.Structure):
                 ("summary_bias", ctypes.c_float), ("reserved", ctypes.c_int32)]
 
 
+class EvaRopeParams(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_float), ("rotary_dim", ctypes.c_int32), ("style", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
 class EvaCache(ctypes.Structure):
     _fields_ = [("cfg", EvaConfig), ("pos", ctypes.c_int64), ("cap_chunks", ctypes.c_int32),
                 ("reserved", ctypes.c_int32), ("ring_k", ctypes.c_void_p),
@@ -52,7 +58,8 @@ EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache
            "eva_attn_backward", "eva_pipeline_create", "eva_pipeline_destroy", "eva_attn_prefill_host",
            "eva_summarize_range", "eva_attn_prefill_range", "eva_summarize_range_bcast",
            "eva_summarize_proj", "eva_decode_ragged_workspace_bytes", "eva_decode_step_ragged",
-           "eva_rope_summarize", "eva_rope", "eva_prefill_reserve"]
+           "eva_rope_summarize", "eva_rope", "eva_prefill_reserve", "eva_rope_ex",
+           "eva_rope_summarize_ex"]
 
 
 class EvaError(RuntimeError):
@@ -76,6 +83,8 @@ def _load():
         "eva_summarize_proj": (st, [CFG, P, P, P, P, P, P, P]),
         "eva_rope_summarize": (st, [CFG, ctypes.c_float, P, P, P, P, P, P, P, P, P]),
         "eva_rope": (st, [CFG, ctypes.c_float, P, P, ctypes.c_int64, ctypes.c_int32, P]),
+        "eva_rope_ex": (st, [CFG, ctypes.POINTER(EvaRopeParams), P, P, ctypes.c_int64, P, ctypes.c_int32, P]),
+        "eva_rope_summarize_ex": (st, [CFG, ctypes.POINTER(EvaRopeParams), P, P, P, P, P, P, P, P, P]),
         "eva_decode_ragged_workspace_bytes": (ctypes.c_size_t, [CACHE]),
         "eva_decode_step_ragged": (st, [CACHE, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
         "eva_attn_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_uint32, P]),

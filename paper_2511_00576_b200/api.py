@@ -96,10 +96,20 @@ def eva_summarize(cfg: EvaConfig, K: torch.Tensor, V: torch.Tensor,
     return Ksum, Vsum
 
 
+_ROPE_STYLE = {"interleaved": N.EVA_ROPE_INTERLEAVED, "neox": N.EVA_ROPE_NEOX}
+
+
+def _rope_params(rope_base, rotary_dim, style):
+    return N.EvaRopeParams(float(rope_base), int(rotary_dim or 0),
+                           _ROPE_STYLE[style] if isinstance(style, str) else int(style), 0)
+
+
 def eva_rope_summarize(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
-                       rope_base: float = 10000.0, eps: Optional[torch.Tensor] = None):
-    """Fused RoPE producer (NEXT row 4, R18): returns (Qr, Kr, Ksum, Vsum) -- the rotated
-    queries/keys and the summaries of the rotated keys, in one launch."""
+                       rope_base: float = 10000.0, eps: Optional[torch.Tensor] = None,
+                       rotary_dim: Optional[int] = None, style: str = "interleaved"):
+    """Fused RoPE producer (NEXT row 4, R18/R19): returns (Qr, Kr, Ksum, Vsum) -- the rotated
+    queries/keys and the summaries of the rotated keys, in one launch.  rotary_dim (default d)
+    and style ("interleaved" pairs (2j, 2j+1) or "neox" pairs (j, j + rd/2)) as in R19."""
     dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
     nC = T // cfg.chunk
     for t, nm in ((Q, "Q"), (K, "K"), (V, "V")):
@@ -109,22 +119,28 @@ def eva_rope_summarize(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torc
     Qr, Kr = torch.empty_like(Q), torch.empty_like(K)
     Ksum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=K.device)[:, :nC]
     Vsum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=K.device)[:, :nC]
-    check(lib.eva_rope_summarize(ctypes.byref(cfg), float(rope_base), _ptr(Q), _ptr(K), _ptr(V), _ptr(eps),
-                                 _ptr(Qr), _ptr(Kr), _ptr(Ksum if nC else None), _ptr(Vsum if nC else None),
-                                 _stream(K.device)))
+    rp = _rope_params(rope_base, rotary_dim, style)
+    check(lib.eva_rope_summarize_ex(ctypes.byref(cfg), ctypes.byref(rp), _ptr(Q), _ptr(K), _ptr(V), _ptr(eps),
+                                    _ptr(Qr), _ptr(Kr), _ptr(Ksum if nC else None), _ptr(Vsum if nC else None),
+                                    _stream(K.device)))
     return Qr, Kr, Ksum, Vsum
 
 
 def eva_rope(cfg: EvaConfig, X: torch.Tensor, rope_base: float = 10000.0, pos0: int = 0,
-             inverse: bool = False, out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """RoPE (R18) of rows X [bh, T, d] at positions pos0.. (inverse: the transposed rotation,
-    i.e. the gradient through RoPE)."""
+             inverse: bool = False, out: Optional[torch.Tensor] = None, rotary_dim: Optional[int] = None,
+             style: str = "interleaved", pos: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """RoPE (R18/R19) of rows X [bh, T, d]: row t of unit u at position (pos[u] if pos is given,
+    a CUDA int64 tensor [bh], else pos0) + t; inverse: the transposed rotation (the gradient
+    through RoPE)."""
     dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
     _need(X, "X", (bh, T, d), dt)
     out = torch.empty_like(X) if out is None else out
     _need(out, "out", (bh, T, d), dt)
-    check(lib.eva_rope(ctypes.byref(cfg), float(rope_base), _ptr(X), _ptr(out), int(pos0), int(bool(inverse)),
-                       _stream(X.device)))
+    if pos is not None:
+        _need(pos, "pos", (bh,), torch.int64)
+    rp = _rope_params(rope_base, rotary_dim, style)
+    check(lib.eva_rope_ex(ctypes.byref(cfg), ctypes.byref(rp), _ptr(X), _ptr(out), int(pos0), _ptr(pos),
+                          int(bool(inverse)), _stream(X.device)))
     return out
 
 

@@ -138,27 +138,66 @@ eva_status eva_summarize(const eva_config* cfg, const void* K, const void* V, co
                      "eva_summarize");
 }
 
+}  // extern "C"
+
+namespace {
+// R19: base > 1 finite; rotary_dim 0 (= d) or even, <= d, a multiple of 2 * (16 / elem); style 0/1.
+eva_status check_rope(const eva_config* cfg, const eva_rope_params* rp, bool fused_producer) {
+  if (!rp) return fail(EVA_ERR_INVALID_ARG, "rope params are NULL");
+  if (!(rp->base > 1.f) || !std::isfinite(rp->base))
+    return fail(EVA_ERR_INVALID_ARG, "rope base=%g must be finite and > 1", (double)rp->base);
+  if (rp->style != EVA_ROPE_INTERLEAVED && rp->style != EVA_ROPE_NEOX)
+    return fail(EVA_ERR_INVALID_ARG, "rope style=%d", rp->style);
+  if (rp->reserved != 0) return fail(EVA_ERR_INVALID_ARG, "rope reserved must be 0");
+  const int rd = rp->rotary_dim ? rp->rotary_dim : cfg->d_head;
+  const int vec2 = 2 * (cfg->dtype == EVA_BF16 ? 8 : 4);
+  if (rd < 0 || rd > cfg->d_head || rd % vec2 != 0)
+    return fail(EVA_ERR_INVALID_ARG, "rotary_dim=%d: needs 0 < rd <= d=%d and rd %% %d == 0", rd, cfg->d_head, vec2);
+  if (fused_producer && rp->style == EVA_ROPE_NEOX) {
+    const int off = rd / vec2;
+    if (off & (off - 1))
+      return fail(EVA_ERR_UNSUPPORTED, "half-split rotary_dim=%d: rd / %d must be a power of two in the fused "
+                                       "producer", rd, vec2);
+  }
+  return EVA_OK;
+}
+}  // namespace
+
+extern "C" {
+
 eva_status eva_rope(const eva_config* cfg, float rope_base, const void* X, void* Y, int64_t pos0,
                     int32_t inverse, eva_stream_t stream) {
+  const eva_rope_params rp{rope_base, 0, EVA_ROPE_INTERLEAVED, 0};
+  return eva_rope_ex(cfg, &rp, X, Y, pos0, nullptr, inverse, stream);
+}
+
+eva_status eva_rope_ex(const eva_config* cfg, const eva_rope_params* rp, const void* X, void* Y, int64_t pos0,
+                       const int64_t* pos, int32_t inverse, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
-  if (!(rope_base > 1.f) || !std::isfinite(rope_base))
-    return fail(EVA_ERR_INVALID_ARG, "rope_base=%g must be finite and > 1", (double)rope_base);
+  if ((st = check_rope(cfg, rp, false)) != EVA_OK) return st;
   if (pos0 < 0) return fail(EVA_ERR_INVALID_ARG, "pos0=%lld", (long long)pos0);
   if (cfg->bh_count == 0 || cfg->T == 0) return ok();
   const void* p[] = {X, Y};
   const char* nm[] = {"X", "Y"};
   if ((st = check_ptrs(2, p, nm)) != EVA_OK) return st;
-  return cuda_status(eva::launch_rope(*cfg, rope_base, X, Y, pos0, inverse != 0, (cudaStream_t)stream), "eva_rope");
+  if (pos && (reinterpret_cast<uintptr_t>(pos) & 7u)) return fail(EVA_ERR_INVALID_ARG, "pos is not 8-byte aligned");
+  return cuda_status(eva::launch_rope(*cfg, *rp, X, Y, pos0, pos, inverse != 0, (cudaStream_t)stream), "eva_rope");
 }
 
 eva_status eva_rope_summarize(const eva_config* cfg, float rope_base, const void* Q, const void* K,
                               const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
                               eva_stream_t stream) {
+  const eva_rope_params rp{rope_base, 0, EVA_ROPE_INTERLEAVED, 0};
+  return eva_rope_summarize_ex(cfg, &rp, Q, K, V, eps, Qr, Kr, Ksum, Vsum, stream);
+}
+
+eva_status eva_rope_summarize_ex(const eva_config* cfg, const eva_rope_params* rp, const void* Q, const void* K,
+                                 const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
+                                 eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
-  if (!(rope_base > 1.f) || !std::isfinite(rope_base))
-    return fail(EVA_ERR_INVALID_ARG, "rope_base=%g must be finite and > 1", (double)rope_base);
+  if ((st = check_rope(cfg, rp, true)) != EVA_OK) return st;
   if (cfg->bh_count == 0 || cfg->T == 0) return ok();
   const void* p[] = {Q, K, V, Qr, Kr};
   const char* nm[] = {"Q", "K", "V", "Qr", "Kr"};
@@ -169,8 +208,7 @@ eva_status eva_rope_summarize(const eva_config* cfg, float rope_base, const void
     if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
   }
   if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
-  const cudaError_t e = eva::launch_rope_summarize(*cfg, rope_base, Q, K, V, eps, Qr, Kr, Ksum, Vsum,
-                                                   (cudaStream_t)stream);
+  const cudaError_t e = eva::launch_rope_summarize(*cfg, *rp, Q, K, V, eps, Qr, Kr, Ksum, Vsum, (cudaStream_t)stream);
   if (e == cudaErrorNotSupported)
     return fail(EVA_ERR_UNSUPPORTED, "eva_rope_summarize: chunk=%d too long for the register summariser",
                 cfg->chunk);

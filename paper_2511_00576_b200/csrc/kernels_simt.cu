@@ -82,84 +82,176 @@ __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, cons
 // of the global summary list, reached through NVLink peer pointers): the summary of chunk
 // c0 + c is computed once into shared memory and stored to row (c0 + c) of unit u of each
 // destination [units, dst_rows, D] -- the compute and the all-gather in one kernel.
-// ------------------------------------------------------------ RoPE producer (NEXT row 4, R18)
-// Rotate the consecutive channel pairs of a 16-byte piece (channels ch0 .. ch0+VEC) at
-// position pos by pos * base^(-ch/d); the angle is reduced mod 2 pi in double so fp32 keeps
-// its accuracy at long positions.
-template <typename T, int D>
-__device__ __forceinline__ uint4 rope_piece(uint4 x, int64_t pos, int ch0, float log2_base, float sign = 1.f) {
+// ------------------------------------------------------------ RoPE (NEXT row 4, R18 / R19)
+// The first rd channels of a row at position pos rotate in pairs j < rd/2 by the angle
+// pos * base^(-2j/rd): pair (2j, 2j+1) (interleaved, style 0) or (j, j + rd/2) (GPT-NeoX
+// half-split, style 1); channels >= rd pass through.  sign = -1: the transposed rotation (the
+// gradient through RoPE).  The angle is reduced mod 2 pi in double so fp32 keeps its accuracy
+// at long positions.  rd is a multiple of 2 * (16 / sizeof(T)), so a 16-byte piece is either
+// inside [0, rd) or outside it, and a half-split piece's partner is a whole piece rd/2 later.
+struct RopeSpec {
+  double log2_base;  // double: at positions ~2^31 a float log2(base) alone shifts the angle by radians
+  int rd;
+  int style;
+  float sign;
+};
+
+__device__ __forceinline__ void rope_cs(int64_t pos, int j, const RopeSpec& rs, float& c, float& s) {
+  const double theta = exp2(rs.log2_base * (-2.0 * (double)j / (double)rs.rd));
+  double a = (double)pos * theta;
+  a -= 6.283185307179586 * rint(a * 0.15915494309189535);
+  sincosf((float)a, &s, &c);
+  s *= rs.sign;
+}
+
+template <typename T>
+__device__ __forceinline__ uint4 pack16(const float* v) {
   constexpr int VEC = 16 / sizeof(T);
-  float v[VEC];
-  unpack16<T>(x, v);
-#pragma unroll
-  for (int j = 0; j < VEC; j += 2) {
-    const double theta = exp2((double)log2_base * (-(double)(ch0 + j) / (double)D));
-    double a = (double)pos * theta;
-    a -= 6.283185307179586 * rint(a * 0.15915494309189535);
-    float sn, cs;
-    sincosf((float)a, &sn, &cs);
-    sn *= sign;  // sign -1: the inverse (transposed) rotation
-    const float x0 = v[j], x1 = v[j + 1];
-    v[j] = x0 * cs - x1 * sn;
-    v[j + 1] = x0 * sn + x1 * cs;
-  }
   T o[VEC];
 #pragma unroll
   for (int j = 0; j < VEC; ++j) o[j] = Elem<T>::from_f(v[j]);
   return *reinterpret_cast<const uint4*>(o);
 }
 
-// Plain RoPE (or its inverse = transpose, for the gradient dX = R^T dXr) of rows [bh, T, D]
-// at positions pos0 + t; one 16-byte piece per thread.
+// interleaved: the pairs inside one piece (channels ch0 .. ch0 + VEC, ch0 < rd)
+template <typename T>
+__device__ __forceinline__ uint4 rope_piece_il(uint4 x, int64_t pos, int ch0, const RopeSpec& rs) {
+  constexpr int VEC = 16 / sizeof(T);
+  float v[VEC];
+  unpack16<T>(x, v);
+#pragma unroll
+  for (int j = 0; j < VEC; j += 2) {
+    float c, sn;
+    rope_cs(pos, (ch0 + j) / 2, rs, c, sn);
+    const float x0 = v[j], x1 = v[j + 1];
+    v[j] = x0 * c - x1 * sn;
+    v[j + 1] = x0 * sn + x1 * c;
+  }
+  return pack16<T>(v);
+}
+
+// half-split: piece a holds channels j0 .. j0 + VEC (< rd/2), piece b their partners + rd/2
+template <typename T>
+__device__ __forceinline__ void rope_pair_neox(uint4& a, uint4& b, int64_t pos, int j0, const RopeSpec& rs) {
+  constexpr int VEC = 16 / sizeof(T);
+  float va[VEC], vb[VEC];
+  unpack16<T>(a, va);
+  unpack16<T>(b, vb);
+#pragma unroll
+  for (int j = 0; j < VEC; ++j) {
+    float c, sn;
+    rope_cs(pos, j0 + j, rs, c, sn);
+    const float x0 = va[j], x1 = vb[j];
+    va[j] = x0 * c - x1 * sn;
+    vb[j] = x0 * sn + x1 * c;
+  }
+  a = pack16<T>(va);
+  b = pack16<T>(vb);
+}
+
+// Work items of one row: rotate items (interleaved: one piece each, rd/VEC of them; half-split:
+// a piece pair each, rd/(2 VEC)), then pass-through pieces (D - rd)/VEC.
+template <typename T, int D>
+__device__ __forceinline__ int rope_items(const RopeSpec& rs) {
+  constexpr int VEC = 16 / sizeof(T);
+  return (rs.style == EVA_ROPE_NEOX ? rs.rd / (2 * VEC) : rs.rd / VEC) + (D - rs.rd) / VEC;
+}
+template <typename T, int D>
+__device__ __forceinline__ void rope_row_item(const T* src, T* dst, int64_t pos, int it, const RopeSpec& rs) {
+  constexpr int VEC = 16 / sizeof(T);
+  const int nrot = rs.style == EVA_ROPE_NEOX ? rs.rd / (2 * VEC) : rs.rd / VEC;
+  if (it >= nrot) {  // pass-through piece
+    const int ch0 = rs.rd + (it - nrot) * VEC;
+    if (src != dst) *reinterpret_cast<uint4*>(dst + ch0) = ldg16_stream(src + ch0);
+    return;
+  }
+  if (rs.style == EVA_ROPE_NEOX) {
+    const int j0 = it * VEC, h = rs.rd / 2;
+    uint4 a = ldg16_stream(src + j0), b = ldg16_stream(src + j0 + h);
+    rope_pair_neox<T>(a, b, pos, j0, rs);
+    *reinterpret_cast<uint4*>(dst + j0) = a;
+    *reinterpret_cast<uint4*>(dst + j0 + h) = b;
+  } else {
+    const int ch0 = it * VEC;
+    *reinterpret_cast<uint4*>(dst + ch0) = rope_piece_il<T>(ldg16_stream(src + ch0), pos, ch0, rs);
+  }
+}
+
+// RoPE of rows [bh, T, D] (or its inverse): row t of unit u at position (pos ? pos[u] : pos0) + t.
 template <typename T, int D>
 __global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ X, T* __restrict__ Y, int64_t rows,
-                                                   int T_, int64_t pos0, float log2_base, float sign) {
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int PPR = D / VEC;
+                                                   int T_, int64_t pos0, const int64_t* __restrict__ pos,
+                                                   RopeSpec rs) {
+  pdl_wait();
+  pdl_trigger();
+  const int per = rope_items<T, D>(rs);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows * PPR) return;
-  const int64_t row = i / PPR;
-  const int ch0 = (int)(i % PPR) * VEC;
-  const int64_t pos = pos0 + row % T_;
-  reinterpret_cast<uint4*>(Y)[i] = rope_piece<T, D>(ldg16_stream(X + row * D + ch0), pos, ch0, log2_base, sign);
+  if (i >= rows * per) return;
+  const int64_t row = i / per;
+  const int it = (int)(i % per);
+  const int64_t p = (pos ? pos[row / T_] : pos0) + row % T_;
+  rope_row_item<T, D>(X + row * D, Y + row * D, p, it, rs);
 }
+
+// The key transform of the fused producer: rotate the piece (row r of the chunk, channels ch0)
+// at position r0 + r and store it to Kr.  Half-split pairs live in lanes gl and gl ^ off
+// (off = rd / (2 VEC), a power of two), exchanged by shuffles -- every lane takes part.
+template <typename T, int D>
+struct RopeKX {
+  RopeSpec rs;
+  int64_t r0;
+  T* Krc;
+  __device__ __forceinline__ void operator()(int r, int ch0, uint4& x, bool valid) const {
+    constexpr int VEC = 16 / sizeof(T);
+    if (rs.style == EVA_ROPE_NEOX) {
+      const int off = rs.rd / (2 * VEC);
+      uint4 y;
+      y.x = __shfl_xor_sync(0xffffffffu, x.x, off);
+      y.y = __shfl_xor_sync(0xffffffffu, x.y, off);
+      y.z = __shfl_xor_sync(0xffffffffu, x.z, off);
+      y.w = __shfl_xor_sync(0xffffffffu, x.w, off);
+      const int gl = ch0 / VEC;
+      if (ch0 < rs.rd) {
+        if (gl < off) rope_pair_neox<T>(x, y, r0 + r, ch0, rs);           // x first half
+        else rope_pair_neox<T>(y, x, r0 + r, ch0 - rs.rd / 2, rs);       // x second half
+      }
+    } else if (ch0 < rs.rd) {
+      x = rope_piece_il<T>(x, r0 + r, ch0, rs);
+    }
+    if (valid) *reinterpret_cast<uint4*>(Krc + (size_t)r * D + ch0) = x;
+  }
+};
 
 // grid (nC + tail, bh_count), 128 threads.  CTA x < nC: chunk x -- its keys are rotated as
 // they are loaded (and stored to Kr), summarised from the rotated values, and its query rows
 // rotated into Qr; CTA x = nC rotates the trailing partial chunk's rows only.
 template <typename T, int D, int NI>
-__global__ void __launch_bounds__(128) rope_summarize_kernel(eva_config cfg, float log2_base,
+__global__ void __launch_bounds__(128) rope_summarize_kernel(eva_config cfg, RopeSpec rs,
                                                             const T* __restrict__ Q, const T* __restrict__ K,
                                                             const T* __restrict__ V, const float* __restrict__ eps,
                                                             T* __restrict__ Qr, T* __restrict__ Kr,
                                                             T* __restrict__ Ksum, T* __restrict__ Vsum) {
   pdl_wait();
   pdl_trigger();
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int PPR = D / VEC;
   const int C = cfg.chunk, Tn = cfg.T, nC = Tn / C;
   const int c = blockIdx.x, u = blockIdx.y;
   const size_t ub = (size_t)u * Tn;
   const int r0 = c * C, r1 = min(Tn, r0 + C);
+  const int per = rope_items<T, D>(rs);
   // the query rows of this chunk (and, for the tail CTA, the key rows too)
-  for (int i = threadIdx.x; i < (r1 - r0) * PPR; i += blockDim.x) {
-    const int r = r0 + i / PPR, ch0 = (i % PPR) * VEC;
-    const size_t off = (ub + r) * D + ch0;
-    *reinterpret_cast<uint4*>(Qr + off) = rope_piece<T, D>(ldg16_stream(Q + off), r, ch0, log2_base);
-    if (c >= nC) *reinterpret_cast<uint4*>(Kr + off) = rope_piece<T, D>(ldg16_stream(K + off), r, ch0, log2_base);
+  for (int i = threadIdx.x; i < (r1 - r0) * per; i += blockDim.x) {
+    const int r = r0 + i / per, it = i % per;
+    rope_row_item<T, D>(Q + (ub + r) * D, Qr + (ub + r) * D, r, it, rs);
+    if (c >= nC) rope_row_item<T, D>(K + (ub + r) * D, Kr + (ub + r) * D, r, it, rs);
   }
   if (c >= nC) return;
   const T* Kc = K + (ub + (size_t)r0) * D;
   const T* Vc = V + (ub + (size_t)r0) * D;
-  T* Krc = Kr + (ub + (size_t)r0) * D;
-  auto rot = [&](int r, int ch0, uint4& x) {
-    x = rope_piece<T, D>(x, (int64_t)r0 + r, ch0, log2_base);
-    *reinterpret_cast<uint4*>(Krc + (size_t)r * D + ch0) = x;
-  };
+  RopeKX<T, D> kx{rs, (int64_t)r0, Kr + (ub + (size_t)r0) * D};
   summarize_chunk_reg<T, D, NI>([&](int r) { return Kc + (size_t)r * D; }, [&](int r) { return Vc + (size_t)r * D; },
                                 C, eps ? eps + ((size_t)u * nC + c) * D : nullptr, (uint32_t)(cfg.bh_begin + u),
                                 (uint32_t)c, cfg, Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D,
-                                nullptr, rot);
+                                nullptr, kx);
 }
 
 template <typename T, int D, int NI>
@@ -797,11 +889,13 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
   return cudaGetLastError();
 }
 
-cudaError_t launch_rope_summarize(const eva_config& cfg, float base, const void* Q, const void* K, const void* V,
-                                  const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum, cudaStream_t s) {
+cudaError_t launch_rope_summarize(const eva_config& cfg, const eva_rope_params& rp, const void* Q, const void* K,
+                                  const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
+                                  cudaStream_t s) {
   const int nC = cfg.T / cfg.chunk;
   const int n_cta = nC + (cfg.T % cfg.chunk ? 1 : 0);
   if (n_cta == 0 || cfg.bh_count == 0) return cudaSuccess;
+  const RopeSpec rs{log2((double)rp.base), rp.rotary_dim ? rp.rotary_dim : cfg.d_head, rp.style, 1.f};
   cudaError_t err = cudaSuccess;
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
     const int ni = summ_reg_ni<T, D>(cfg.chunk);
@@ -809,7 +903,7 @@ cudaError_t launch_rope_summarize(const eva_config& cfg, float base, const void*
     auto k = ni <= 2 ? rope_summarize_kernel<T, D, 2>
                      : ni <= 4 ? rope_summarize_kernel<T, D, 4>
                                : ni <= 8 ? rope_summarize_kernel<T, D, 8> : rope_summarize_kernel<T, D, 16>;
-    err = launch_pdl(k, dim3(n_cta, cfg.bh_count), dim3(128), 0, s, cfg, log2f(base), (const T*)Q, (const T*)K,
+    err = launch_pdl(k, dim3(n_cta, cfg.bh_count), dim3(128), 0, s, cfg, rs, (const T*)Q, (const T*)K,
                      (const T*)V, eps, (T*)Qr, (T*)Kr, (T*)Ksum, (T*)Vsum);
     if (err != cudaSuccess) return err;
   }));
@@ -817,15 +911,20 @@ cudaError_t launch_rope_summarize(const eva_config& cfg, float base, const void*
   return cudaGetLastError();
 }
 
-cudaError_t launch_rope(const eva_config& cfg, float base, const void* X, void* Y, int64_t pos0, bool inverse,
-                        cudaStream_t s) {
+cudaError_t launch_rope(const eva_config& cfg, const eva_rope_params& rp, const void* X, void* Y, int64_t pos0,
+                        const int64_t* pos, bool inverse, cudaStream_t s) {
   const int64_t rows = (int64_t)cfg.bh_count * cfg.T;
   if (rows == 0) return cudaSuccess;
+  const int rd = rp.rotary_dim ? rp.rotary_dim : cfg.d_head;
+  const RopeSpec rs{log2((double)rp.base), rd, rp.style, inverse ? -1.f : 1.f};
+  cudaError_t err = cudaSuccess;
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
-    constexpr int PPR = D * (int)sizeof(T) / 16;
-    const int64_t n = rows * PPR;
-    rope_kernel<T, D><<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const T*)X, (T*)Y, rows, cfg.T, pos0,
-                                                                  log2f(base), inverse ? -1.f : 1.f);
+    constexpr int VEC = 16 / (int)sizeof(T);
+    const int per = (rs.style == EVA_ROPE_NEOX ? rd / (2 * VEC) : rd / VEC) + (D - rd) / VEC;
+    const int64_t n = rows * per;
+    err = launch_pdl(rope_kernel<T, D>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, (const T*)X, (T*)Y,
+                     rows, cfg.T, pos0, pos, rs);
+    if (err != cudaSuccess) return err;
   }));
   note_launch();
   return cudaGetLastError();

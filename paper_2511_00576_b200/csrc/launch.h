@@ -21,13 +21,15 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
 bool summarize_bulk_supported(const eva_config& cfg);
 cudaError_t launch_summarize_bulk(const eva_config& cfg, const void* K, const void* V, const float* eps,
                                   void* Ksum, void* Vsum, int c0, cudaStream_t s);
-// RoPE (or its inverse) of [bh_count, T, d] rows at positions pos0 + t (R18).
-cudaError_t launch_rope(const eva_config& cfg, float base, const void* X, void* Y, int64_t pos0, bool inverse,
-                        cudaStream_t s);
-// Fused RoPE producer (NEXT row 4, R18): Qr, Kr = RoPE(Q, K) and the summaries of the
+// RoPE (or its inverse) of [bh_count, T, d] rows at positions (pos ? pos[u] : pos0) + t, with the
+// rotary_dim / style of rp (R18, R19; validated by the ABI).
+cudaError_t launch_rope(const eva_config& cfg, const eva_rope_params& rp, const void* X, void* Y, int64_t pos0,
+                        const int64_t* pos, bool inverse, cudaStream_t s);
+// Fused RoPE producer (NEXT row 4, R18/R19): Qr, Kr = RoPE(Q, K) and the summaries of the
 // rotated keys in one launch (register summariser only: cudaErrorNotSupported otherwise).
-cudaError_t launch_rope_summarize(const eva_config& cfg, float base, const void* Q, const void* K, const void* V,
-                                  const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum, cudaStream_t s);
+cudaError_t launch_rope_summarize(const eva_config& cfg, const eva_rope_params& rp, const void* Q, const void* K,
+                                  const void* V, const float* eps, void* Qr, void* Kr, void* Ksum, void* Vsum,
+                                  cudaStream_t s);
 
 // Summaries of the chunks of rows [c0*C, ...) stored to row c0 + c of every destination
 // [bh, dst_rows, D] buffer (dst_k/dst_v: device arrays of n_dst base addresses).  Returns

@@ -22,7 +22,7 @@ constexpr int summ_reg_ni(int C) {
 // Pk (may be nullptr): the learned summary-key projection of NEXT row 4 (reading R17),
 // k~ = Pk mean(k) with Pk [D, D] row-major fp32 of this unit's head; omega uses mu = k~.
 struct NoKXform {
-  __device__ __forceinline__ void operator()(int, int, uint4&) const {}
+  __device__ __forceinline__ void operator()(int, int, uint4&, bool) const {}
 };
 // LD: the 16-byte load of a key / value piece (global streaming loads by default; the bulk-copy
 // summariser passes shared-memory loads, so every path runs the same arithmetic bit for bit).
@@ -30,8 +30,9 @@ struct LdGlobalStream {
   template <typename P>
   __device__ __forceinline__ uint4 operator()(const P* p) const { return ldg16_stream(p); }
 };
-// KX (optional): applied to every loaded 16-byte key piece (row r, channel ch0) before any
-// use -- the fused RoPE producer rotates (and stores) the keys there.
+// KX (optional): applied to every loaded 16-byte key piece (row r, channel ch0, valid = r < C)
+// before any use, by every lane of the warp -- the fused RoPE producer rotates (exchanging the
+// half-split partner pieces by shuffles) and stores the keys there.
 template <typename T, int D, int NI, typename RowK, typename RowV, typename KX = NoKXform,
           typename LD = LdGlobalStream>
 __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV& rowV, int C,
@@ -53,9 +54,11 @@ __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV
     const int r = warp * RPW + 4 * RPW * i + grp;
     if (r < C) {
       kx[i] = ld(rowK(r) + ch0);
-      kxf(r, ch0, kx[i]);
       vx[i] = ld(rowV(r) + ch0);
+    } else {
+      kx[i] = make_uint4(0u, 0u, 0u, 0u);
     }
+    kxf(r, ch0, kx[i], r < C);  // every lane (a transform may exchange pieces by shuffles)
   }
   // column sums
   float cs[VEC];

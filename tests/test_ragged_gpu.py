@@ -118,3 +118,53 @@ def test_ragged_two_launch_form_parity():
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("style", ["interleaved", "neox"])
+def test_ragged_decode_with_per_unit_rope(eva, style):
+    """A ragged serving batch with RoPE (R18/R19): every step rotates the new q and k at each
+    unit's own position with eva_rope(pos=the same device array the ragged step advances), then
+    eva_decode_step_ragged; against the oracle cache fed the fp64-rotated (stored-precision) k, q."""
+    dtype, d, C, W, rd = torch.bfloat16, 64, 16, 64, 32
+    BH, steps = 4, 40
+    prompt = [0, 9, C * 2 - 1, W + 3]
+    cap = (max(prompt) + steps) // C + 1
+    cfg = eva.make_config(1, BH, 0, d, C, W, dtype=dtype, seed=23)
+    cache = eva.DecodeCache(cfg, cap, device="cuda")
+    orc = [oracle.Cache(d, C, W, oracle.SLIDING, cap=cap, scale=cfg.scale) for _ in range(BH)]
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, BH, cap + 1, d)
+    st = oracle.ROPE_NEOX if style == "neox" else oracle.ROPE_INTERLEAVED
+    q, k, v = eva_inputs.decode_tokens(0, BH, max(prompt) + steps, d, dtype, seed=24, device="cuda")
+    from paper_2511_00576_b200 import _native as N
+    one = eva.make_config(1, BH, 1, d, C, W, dtype=dtype, seed=23)
+    for u, n in enumerate(prompt):   # prompts: rotated keys at positions 0..n-1
+        if n == 0:
+            continue
+        kr = torch.stack([eva.eva_rope(eva.make_config(1, 1, n, d, C, W, dtype=dtype),
+                                       k[:n, u].unsqueeze(0).contiguous(), rotary_dim=rd, style=style)[0]])
+        view = _unit_view(eva, cache, u)
+        N.check(N.lib.eva_cache_append(ctypes.byref(view), kr.data_ptr(), v[:n, u].unsqueeze(0).contiguous().data_ptr(),
+                                       n, None, None))
+        for t in range(n):
+            kt = oracle.rope_ex(f64(k[t, u])[None], [t], rotary_dim=rd, style=st)
+            kt = torch.from_numpy(kt).to(dtype).double().numpy()[0]
+            assert orc[u].append(kt, f64(v[t, u]), E[u, t // C]) == 0
+    pos = torch.tensor(prompt, dtype=torch.int64, device="cuda")
+    worst = 0.0
+    for s in range(steps):
+        idx = [prompt[u] + s for u in range(BH)]
+        qs = torch.stack([q[idx[u], u] for u in range(BH)]).unsqueeze(1).contiguous()
+        ks = torch.stack([k[idx[u], u] for u in range(BH)]).unsqueeze(1).contiguous()
+        vs = torch.stack([v[idx[u], u] for u in range(BH)]).contiguous()
+        qr = eva.eva_rope(one, qs, rotary_dim=rd, style=style, pos=pos)[:, 0].contiguous()
+        kr = eva.eva_rope(one, ks, rotary_dim=rd, style=style, pos=pos)[:, 0].contiguous()
+        o, lse = cache.eva_decode_step_ragged(pos, qr, kr, vs)
+        of = f64(o)
+        for u in range(BH):
+            kt = torch.from_numpy(oracle.rope_ex(f64(ks[u]), [idx[u]], rotary_dim=rd, style=st)).to(dtype).double().numpy()[0]
+            qt = torch.from_numpy(oracle.rope_ex(f64(qs[u]), [idx[u]], rotary_dim=rd, style=st)).to(dtype).double().numpy()[0]
+            assert orc[u].append(kt, f64(vs[u]), E[u, idx[u] // C]) == 0
+            ro, rl = orc[u].decode(qt)
+            worst = max(worst, np.max(np.abs(of[u] - ro)))
+    assert worst <= 2e-2, worst
+    assert pos.tolist() == [p + steps for p in prompt]

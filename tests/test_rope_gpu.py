@@ -116,3 +116,76 @@ def test_training_chain_with_rope(eva):
         for name, got, want in (("dQ", dQ[u], gq), ("dK", dK[u], gk), ("dV", dV[u], gv)):
             err = np.max(np.abs(f64(got) - want))
             assert err <= 2e-2 * max(1.0, np.max(np.abs(want))), (name, u, err)
+
+
+# ------------------------------------------------------------------ R19: rotary_dim, half-split,
+# per-unit device positions (the ragged decode batch), against oracle.rope_ex
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("d,rd", [(64, 16), (64, 64), (128, 32), (128, 128), (32, 16)])
+@pytest.mark.parametrize("style", ["interleaved", "neox"])
+@pytest.mark.parametrize("inverse", [False, True])
+def test_rope_ex_parity(eva, dtype, d, rd, style, inverse):
+    BH, T = 5, 37
+    cfg = eva.make_config(1, BH, T, d, 16, 32, dtype=dtype)
+    (X,) = eva_inputs.normal_units(1, 0, BH, T, d, dtype, seed=41, device="cuda")
+    pos = torch.tensor([0, 7, 4096, 123457, 2 ** 31 + 5], dtype=torch.int64, device="cuda")
+    Y = eva.eva_rope(cfg, X, rope_base=500.0, rotary_dim=rd, style=style, pos=pos, inverse=inverse)
+    torch.cuda.synchronize()
+    st = oracle.ROPE_NEOX if style == "neox" else oracle.ROPE_INTERLEAVED
+    worst = 0.0
+    for u in range(BH):
+        p = int(pos[u]) + np.arange(T)
+        want = oracle.rope_ex(f64(X[u]), p, base=500.0, rotary_dim=rd, style=st, inverse=inverse)
+        worst = max(worst, np.max(np.abs(f64(Y[u]) - want)))
+        # pass-through channels are copied exactly
+        assert torch.equal(Y[u, :, rd:], X[u, :, rd:])
+    # bf16 output rounding: 2^-8 of |y| <= a few units; fp32 angle reduction at 2^31
+    assert worst <= (2e-2 if dtype == torch.bfloat16 else 2e-4), worst
+    # scalar pos0 path: the same as a pos array of equal positions
+    Y0 = eva.eva_rope(cfg, X, rope_base=500.0, rotary_dim=rd, style=style, pos0=4096, inverse=inverse)
+    Y1 = eva.eva_rope(cfg, X, rope_base=500.0, rotary_dim=rd, style=style,
+                      pos=torch.full((BH,), 4096, dtype=torch.int64, device="cuda"), inverse=inverse)
+    assert torch.equal(Y0, Y1)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("d,rd,style", [(64, 16, "neox"), (128, 128, "neox"), (128, 32, "interleaved"),
+                                        (64, 32, "neox")])
+def test_rope_summarize_ex_parity(eva, dtype, d, rd, style):
+    """The fused producer with rotary_dim / half-split pairs (partner pieces exchanged between
+    lanes): Qr, Kr, the summaries of the rotated keys and the prefill on them vs the oracle."""
+    B, H, T, C, W = 1, 3, 300, 32, 64
+    cfg = eva.make_config(B, H, T, d, C, W, dtype=dtype, seed=19)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, dtype, seed=20, device="cuda")
+    Qr, Kr, ks, vs = eva.eva_rope_summarize(cfg, Q, K, V, rope_base=10000.0, rotary_dim=rd, style=style)
+    O, lse, _, _ = eva.eva_attn_prefill(cfg, Qr, Kr, V, Ksum=ks, Vsum=vs, summaries_provided=True)
+    torch.cuda.synchronize()
+    st = oracle.ROPE_NEOX if style == "neox" else oracle.ROPE_INTERLEAVED
+    nC = T // C
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, nC, d)
+    tol = TOL[dtype]
+    for u in range(B * H):
+        p = np.arange(T)
+        rq = oracle.rope_ex(f64(Q[u]), p, rotary_dim=rd, style=st)
+        rk = oracle.rope_ex(f64(K[u]), p, rotary_dim=rd, style=st)
+        assert np.max(np.abs(f64(Qr[u]) - rq)) <= tol
+        assert np.max(np.abs(f64(Kr[u]) - rk)) <= tol
+        rq = torch.from_numpy(rq).to(dtype).double().numpy()
+        rk = torch.from_numpy(rk).to(dtype).double().numpy()
+        sk, sv = oracle.summarize(rk, f64(V[u]), E[u], C)
+        assert np.max(np.abs(f64(ks[u]) - sk)) <= tol
+        assert np.max(np.abs(f64(vs[u]) - sv)) <= tol
+        ro, rl = oracle.prefill(rq, rk, f64(V[u]), sk, sv, C, W, oracle.SLIDING, cfg.scale)
+        assert np.max(np.abs(f64(O[u]) - ro)) <= tol
+
+
+def test_rope_ex_validation(eva):
+    cfg = eva.make_config(1, 1, 8, 64, 16, 32)
+    X = torch.zeros(1, 8, 64, dtype=torch.bfloat16, device="cuda")
+    for kw in (dict(rotary_dim=24), dict(rotary_dim=80), dict(rotary_dim=8), dict(style=2)):
+        with pytest.raises((eva.EvaError, KeyError, ValueError)):
+            eva.eva_rope(cfg, X, **kw)
+    cfg = eva.make_config(1, 1, 96, 128, 32, 64)
+    Z = torch.zeros(1, 96, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(eva.EvaError, match="UNSUPPORTED"):   # rd / 16 = 3: no butterfly partner
+        eva.eva_rope_summarize(cfg, Z, Z, Z, rotary_dim=48, style="neox")
