@@ -14,11 +14,13 @@
 // warps active, long-scoreboard stalls on the loads).  Here a persistent CTA (grid = SMs x CTAs
 // per SM) walks chunks i = blockIdx.x, + gridDim.x, ...; a chunk's C key rows and C value rows
 // are each ONE contiguous C*d*2-byte block, brought into shared memory by a single bulk copy
-// (cp.async.bulk, mbarrier complete_tx), NST = 2 stages deep, so the next chunk streams in while
-// this one is computed.  The arithmetic is summarize_chunk_reg's (summarize_reg.cuh) with its
+// (cp.async.bulk, mbarrier complete_tx), into NST stages (launch_bulk_t chooses), the summariser
+// re-reading its pieces from shared memory -- few registers, so many CTAs per SM keep chunks
+// streaming while others compute.  The arithmetic is summarize_chunk_reg's (summarize_reg.cuh) with its
 // loads served from shared memory: the summaries are bitwise those of the register kernel, the
 // cache append and the decode step.
 #include <cuda.h>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -93,6 +95,7 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
     }
   }
   constexpr int NI = summ_reg_ni<__nv_bfloat16, D>(CC);
+  auto rowK_of = [](const __nv_bfloat16* base) { return [base](int r) { return base + (size_t)r * D; }; };
   int k = 0;
   for (int i = blockIdx.x; i < total; i += gridDim.x, ++k) {
     const int s = k % NST;
@@ -100,8 +103,8 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
     mbar_wait(&sm.full[s], (k / NST) & 1);
     const __nv_bfloat16* Ks = sm.k[s];
     const __nv_bfloat16* Vs = sm.v[s];
-    summarize_chunk_reg<__nv_bfloat16, D, NI>(
-        [&](int r) { return Ks + (size_t)r * D; }, [&](int r) { return Vs + (size_t)r * D; }, CC,
+    summarize_chunk_reg<__nv_bfloat16, D, NI, decltype(rowK_of(Ks)), decltype(rowK_of(Vs)), NoKXform, LdShared, true>(
+        rowK_of(Ks), rowK_of(Vs), CC,
         eps ? eps + ((size_t)u * nC + c) * D : nullptr, (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
         Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D, nullptr, NoKXform(), LdShared());
     __syncthreads();  // every thread is done with stage s
@@ -112,10 +115,9 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
   }
 }
 
-template <int D, int CC>
-cudaError_t launch_bulk_t(const eva_config& cfg, const void* K, const void* V, const float* eps, void* Ksum,
-                          void* Vsum, int c0, cudaStream_t s) {
-  constexpr int NST = 2;
+template <int D, int CC, int NST>
+cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V, const float* eps, void* Ksum,
+                            void* Vsum, int c0, cudaStream_t s) {
   using S = SumSmem<D, CC, NST>;
   const size_t smem = sizeof(S);
   auto kern = summarize_bulk_kernel<D, CC, NST>;
@@ -131,6 +133,24 @@ cudaError_t launch_bulk_t(const eva_config& cfg, const void* K, const void* V, c
   if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
+}
+
+// Stages per CTA.  The summariser re-reads its pieces from shared memory (~48 registers), so
+// shared memory sets the CTAs per SM: one stage (7 CTAs per SM at d = 128, C = 64, chunks
+// overlapping ACROSS CTAs) measured 0.203 ms = 0.83 of HBM at configs[2], two stages (3 CTAs,
+// overlap within a CTA) 0.252 ms; small launches (< 8 chunks per SM) keep two stages (configs[1]:
+// 10.3 vs 11.1 us).  EVA_SUMM_NST = 1 / 2 forces either.
+template <int D, int CC>
+cudaError_t launch_bulk_t(const eva_config& cfg, const void* K, const void* V, const float* eps, void* Ksum,
+                          void* Vsum, int c0, cudaStream_t s) {
+  static const int nst_env = [] {
+    const char* e = getenv("EVA_SUMM_NST");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t total = (int64_t)(cfg.T / CC) * cfg.bh_count;
+  const int nst = nst_env ? nst_env : (total >= 8LL * num_sms() ? 1 : 2);
+  if (nst == 1 || 2 * CC * D * 2 * 2 > 160 * 1024) return launch_bulk_nst<D, CC, 1>(cfg, K, V, eps, Ksum, Vsum, c0, s);
+  return launch_bulk_nst<D, CC, 2>(cfg, K, V, eps, Ksum, Vsum, c0, s);
 }
 
 }  // namespace

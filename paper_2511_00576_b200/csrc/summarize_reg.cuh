@@ -33,8 +33,11 @@ struct LdGlobalStream {
 // KX (optional): applied to every loaded 16-byte key piece (row r, channel ch0, valid = r < C)
 // before any use, by every lane of the warp -- the fused RoPE producer rotates (exchanging the
 // half-split partner pieces by shuffles) and stores the keys there.
+// RELOAD: re-read every piece through LD where it is used instead of holding the chunk in
+// registers (the rows sit in shared memory: same arithmetic in the same order, ~60 fewer
+// registers, so more chunks are computed at once per SM).  Only with the identity KX.
 template <typename T, int D, int NI, typename RowK, typename RowV, typename KX = NoKXform,
-          typename LD = LdGlobalStream>
+          typename LD = LdGlobalStream, bool RELOAD = false>
 __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV& rowV, int C,
                                                     const float* eps_c, uint32_t bh_global,
                                                     uint32_t chunk, const eva_config& cfg,
@@ -48,17 +51,23 @@ __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV
   __shared__ float sh_m[4], sh_l[4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / TPR, gl = lane % TPR, ch0 = gl * VEC;
-  uint4 kx[NI], vx[NI];
+  uint4 kx[RELOAD ? 1 : NI], vx[RELOAD ? 1 : NI];
+  auto kpiece = [&](int i, int r) -> uint4 { if constexpr (RELOAD) return ld(rowK(r) + ch0); else return kx[i]; };
+  auto vpiece = [&](int i, int r) -> uint4 { if constexpr (RELOAD) return ld(rowV(r) + ch0); else return vx[i]; };
+  if constexpr (!RELOAD) {
 #pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int r = warp * RPW + 4 * RPW * i + grp;
-    if (r < C) {
-      kx[i] = ld(rowK(r) + ch0);
-      vx[i] = ld(rowV(r) + ch0);
-    } else {
-      kx[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = 0; i < NI; ++i) {
+      const int r = warp * RPW + 4 * RPW * i + grp;
+      if (r < C) {
+        kx[i] = ld(rowK(r) + ch0);
+        vx[i] = ld(rowV(r) + ch0);
+      } else {
+        kx[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      kxf(r, ch0, kx[i], r < C);  // every lane (a transform may exchange pieces by shuffles)
     }
-    kxf(r, ch0, kx[i], r < C);  // every lane (a transform may exchange pieces by shuffles)
+  } else {
+    static_assert(sizeof(KX) == sizeof(NoKXform), "RELOAD takes no key transform");
   }
   // column sums
   float cs[VEC];
@@ -69,7 +78,7 @@ __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV
     const int r = warp * RPW + 4 * RPW * i + grp;
     if (r < C) {
       float k[VEC];
-      unpack16<T>(kx[i], k);
+      unpack16<T>(kpiece(i, r), k);
 #pragma unroll
       for (int j = 0; j < VEC; ++j) cs[j] += k[j];
     }
@@ -138,7 +147,7 @@ __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV
     float part = 0.f;
     if (r < C) {
       float k[VEC];
-      unpack16<T>(kx[i], k);
+      unpack16<T>(kpiece(i, r), k);
 #pragma unroll
       for (int j = 0; j < VEC; ++j) part += k[j] * (om[j] - 0.5f * k[j]);
     }
@@ -158,7 +167,7 @@ __device__ __forceinline__ void summarize_chunk_reg(const RowK& rowK, const RowV
       const float p = __expf(a[i] - m);
       l += p;
       float v[VEC];
-      unpack16<T>(vx[i], v);
+      unpack16<T>(vpiece(i, r), v);
 #pragma unroll
       for (int j = 0; j < VEC; ++j) acc[j] += p * v[j];
     }

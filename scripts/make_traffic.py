@@ -28,7 +28,7 @@ def main():
     tag = sys.argv[1]
     res = {"note": f"one `ncu --set full --clock-control none` capture per kernel, round tag {tag}; "
                    "bytes are per launch (cold L2 under ncu replay)"}
-    for key in ("prefill_cfg2", "prefill_cfg3", "decode_cfg4", "summarize_cfg3", "bwd_main"):
+    for key in ("prefill_configs1", "prefill_configs2", "decode_configs3", "summarize_configs2", "bwd_main"):
         rep = f"gpurun_out/prof_{key}_{tag}.ncu-rep"
         if os.path.exists(rep):
             b, t, name = dram_bytes(rep)

@@ -1,6 +1,9 @@
 """Launch one hot-path kernel at a BASELINE config a few times (for ncu -k captures).
 
-    python scripts/prof_kernels.py prefill_cfg3|prefill_cfg2|summarize_cfg3|decode_cfg4 [reps]
+    python scripts/prof_kernels.py prefill_configs2|prefill_configs1|summarize_configs2|decode_configs3 [reps]
+
+(BASELINE.json configs are 0-indexed: configs[1] = B=1,H=16,T=2048,d=64; configs[2] = B=8,H=32,
+T=8192,d=128 per GPU; configs[3] = the decode batch.)
 """
 import os
 import sys
@@ -14,8 +17,8 @@ import paper_2511_00576_b200 as eva
 what = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 dev = torch.device("cuda:0")
-if what in ("prefill_cfg3", "summarize_cfg3", "prefill_cfg2"):
-    if what == "prefill_cfg2":
+if what in ("prefill_configs2", "summarize_configs2", "prefill_configs1"):
+    if what == "prefill_configs1":
         B, H, T, d, C, W = 1, 16, 2048, 64, 64, 128
     else:
         B, H, T, d, C, W = 8, 32, 8192, 128, 64, 256
@@ -25,12 +28,12 @@ if what in ("prefill_cfg3", "summarize_cfg3", "prefill_cfg2"):
     O = torch.empty_like(Q)
     lse = torch.empty(B * H, T, device=dev)
     for _ in range(reps):
-        if what == "summarize_cfg3":
+        if what == "summarize_configs2":
             eva.eva_summarize(cfg, K, V, Ksum=ks, Vsum=vs)
         else:
             eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse,
                                  kernel=os.environ.get("EVA_PROF_KERNEL") or None)
-elif what == "decode_cfg4":
+elif what == "decode_configs3":
     BH, d, C, W, ctx = 256 * 32, 128, 64, 256, 32768
     cfg = eva.make_config(256, 32, 0, d, C, W)
     cache = eva.DecodeCache(cfg, ctx // C + 16, device=dev)
