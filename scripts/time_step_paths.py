@@ -21,6 +21,26 @@ side_lo = torch.cuda.Stream(priority=0)          # 0 = lowest priority in CUDA
 main_hi = torch.cuda.Stream(priority=-1)         # higher priority
 def summ(): eva.eva_summarize(cfg, K, V, Ksum=ks, Vsum=vs)
 def pre(): eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse)
+def pre_ov(): eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse,
+                                   overlap=True)
+def full_overlap():
+    # the prefill right after the summarize on the same stream, EVA_PREFILL_OVERLAP: its local
+    # tiles may start before the summaries are complete; the hand-off forks after the prefill
+    summ()
+    pre_ov()
+    side.wait_stream(s)
+    with torch.cuda.stream(side):
+        hand()
+    s.wait_stream(side)
+def full_overlap_fork_first():
+    summ()
+    ev = torch.cuda.Event()
+    ev.record(s)
+    pre_ov()
+    side.wait_event(ev)
+    with torch.cuda.stream(side):
+        hand()
+    s.wait_stream(side)
 def hand():
     cache.c.pos = 0
     cache.eva_cache_load(K, V, ks, vs)
@@ -53,7 +73,9 @@ def full_prio():
     s.wait_stream(main_hi)
 paths = {"summarize": summ, "prefill": pre, "summarize+prefill": lambda: (summ(), pre()),
          "handoff+decode": hand, "summarize+handoff+decode": lambda: (summ(), hand()), "full step": full,
-         "full, prefill issued first": full_prefill_first, "full, stream priorities": full_prio}
+         "full, prefill issued first": full_prefill_first, "full, stream priorities": full_prio,
+         "summarize+prefill overlap": lambda: (summ(), pre_ov()), "full overlap": full_overlap,
+         "full overlap, fork event": full_overlap_fork_first}
 for name, fn in paths.items():
     for _ in range(3): fn()
     torch.cuda.synchronize()
