@@ -105,6 +105,28 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 }
 
 
+// Columns outside [vlo, vhi) or inside [xlo, xhi) of a 64-column S tile set to -inf.  A 64-bit
+// valid mask is built once; each column then costs a shift pair (sign-extend its bit) and one
+// LOP3 select -- the per-column range compares cost ~6 instructions per column (ncu: the masked
+// tiles ran 383 extra instructions per warp, ~46 % of the tiles at configs[2]).
+__device__ __forceinline__ uint64_t range_bits(int lo, int hi) {
+  lo = max(lo, 0);
+  hi = min(hi, 64);
+  if (hi <= lo) return 0ull;
+  const uint64_t a = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
+  const uint64_t b = (1ull << lo) - 1ull;
+  return a & ~b;
+}
+__device__ __forceinline__ void mask_columns(uint32_t (&sr)[64], int vlo, int vhi, int xlo, int xhi) {
+  const uint64_t m = range_bits(vlo, vhi) & ~range_bits(xlo, xhi);
+  const uint32_t mw[2] = {(uint32_t)m, (uint32_t)(m >> 32)};
+#pragma unroll
+  for (int c = 0; c < 64; ++c) {
+    const uint32_t keep = (uint32_t)((int32_t)(mw[c >> 5] << (31 - (c & 31))) >> 31);  // all ones if valid
+    sr[c] = (sr[c] & keep) | (0xff800000u & ~keep);
+  }
+}
+
 // One softmax step of a 64-key tile for this thread's query row (thread <-> TMEM lane).
 // S (fp32, raw q.k) is read from TMEM, columns outside [vlo, vhi) are masked, the running
 // max m_ref (log2 units) is raised lazily (O and l are only rescaled when the tile max
@@ -123,11 +145,7 @@ __device__ __forceinline__ void softmax_tile_mx(uint32_t s_addr, uint32_t o_addr
   tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
   tmem_wait_ld();
   const bool full = vlo <= 0 && vhi >= 64 && (xhi <= 0 || xlo >= 64 || xlo >= xhi);
-  if (!__all_sync(0xffffffffu, full)) {
-#pragma unroll
-    for (int c = 0; c < 64; ++c)
-      if (c < vlo || c >= vhi || (c >= xlo && c < xhi)) sr[c] = 0xff800000u;  // -inf
-  }
+  if (!__all_sync(0xffffffffu, full)) mask_columns(sr, vlo, vhi, xlo, xhi);
   // tree max (8 independent chains) -- a 63-deep serial chain is latency-bound with only
   // two softmax warps per scheduler
   float pm[8];
@@ -233,11 +251,7 @@ __device__ __forceinline__ void softmax_tile2(uint32_t s_addr, uint32_t o_addr, 
   tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
   tmem_wait_ld();
   const bool full = vlo <= 0 && vhi >= 64 && (xhi <= 0 || xlo >= 64 || xlo >= xhi);
-  if (!__all_sync(0xffffffffu, full)) {
-#pragma unroll
-    for (int c = 0; c < 64; ++c)
-      if (c < vlo || c >= vhi || (c >= xlo && c < xhi)) sr[c] = 0xff800000u;  // -inf
-  }
+  if (!__all_sync(0xffffffffu, full)) mask_columns(sr, vlo, vhi, xlo, xhi);
   float pm[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) pm[i] = __uint_as_float(sr[i]);
@@ -984,7 +998,8 @@ bool make_map(CUtensorMap* m, const void* base, int units, int rows, int D, int 
 int softmax_emu() {
   static const int v = [] {
     const char* e = getenv("EVA_SOFTMAX_EMU");
-    return e && atoi(e) == 1 ? 1 : -1;
+    const int k = e ? atoi(e) : -1;
+    return k == 1 || k == 2 || k == 4 ? k : -1;
   }();
   return v;
 }
@@ -1041,8 +1056,12 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
                      cudaStream_t s, bool overlap = false, const float* eps = nullptr) {
   constexpr bool FUSED = FC != 0;
   if constexpr (!TRACE && SMX == -1 && !FUSED) {
-    if (softmax_emu() == 1)
-      return launch_t<D, NSTAGE, false, 1, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
+    switch (softmax_emu()) {
+      case 1: return launch_t<D, NSTAGE, false, 1, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
+      case 2: return launch_t<D, NSTAGE, false, 2, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
+      case 4: return launch_t<D, NSTAGE, false, 4, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
+      default: break;
+    }
   }
   const int BH = cfg.bh_count, nC = rg.nsl;
   if (rg.nq == 0) return cudaSuccess;
