@@ -643,6 +643,33 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
     }
   }
   __syncthreads();
+  if constexpr (FUSED && RAGGED) {
+    // the chunk this token completes (per unit): all four warps of split 0 summarise it with the
+    // register summariser (re-reading its rows: the decode's 80-register budget) -- rows from the
+    // ring, the newest from Knew (its ring slot is written by warp 1 above).  The same arithmetic
+    // as the cache append, so the summaries equal eva_decode_step's bit for bit.  (One warp with
+    // the warp summariser kept 1/64 of the CTAs ~30 us longer per step at configs[3] with the
+    // units 64 tokens apart: 0.87 of HBM vs 0.99 uniform.)
+    const int64_t chunk = (n + 1) / C - 1;
+    if (s == 0 && (n + 1) % C == 0 && chunk < c.cap_chunks) {
+      const int64_t p0 = chunk * C;
+      const T* rk0 = static_cast<const T*>(c.ring_k) + (size_t)u * W * D;
+      const T* rv0 = static_cast<const T*>(c.ring_v) + (size_t)u * W * D;
+      auto rowK = [&](int i) -> const T* {
+        const int64_t q = p0 + i;
+        return q == n ? Knew + (size_t)u * D : rk0 + (size_t)(q % W) * D;
+      };
+      auto rowV = [&](int i) -> const T* {
+        const int64_t q = p0 + i;
+        return q == n ? Vnew + (size_t)u * D : rv0 + (size_t)(q % W) * D;
+      };
+      summarize_chunk_reg<T, D, 16, decltype(rowK), decltype(rowV), NoKXform, LdGlobalStream, true>(
+          rowK, rowV, C, ragged_eps ? ragged_eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr,
+          (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk, c.cfg,
+          static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D,
+          static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D);
+    }
+  }
   if (warp != 0) return;
   float M = -INFINITY;
 #pragma unroll
@@ -661,30 +688,6 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
       O[(size_t)u * D + ch] = Elem<T>::from_f(o / L);
     } else {
       parts[((size_t)u * S + s) * (D + 2) + 2 + ch] = o;
-    }
-  }
-  if constexpr (FUSED && RAGGED) {
-    // the chunk this token completes (per unit): warp 0 of split 0 summarises it -- rows
-    // from the ring, the newest from Knew (its ring slot is being written by warp 1 of this
-    // CTA) -- then advances pos[u] once every split has read it (the merging CTA, below)
-    const int64_t chunk = (n + 1) / C - 1;
-    if (s == 0 && (n + 1) % C == 0 && chunk < c.cap_chunks) {
-      const int64_t p0 = chunk * C;
-      const T* rk0 = static_cast<const T*>(c.ring_k) + (size_t)u * W * D;
-      const T* rv0 = static_cast<const T*>(c.ring_v) + (size_t)u * W * D;
-      auto rowK = [&](int i) -> const T* {
-        const int64_t q = p0 + i;
-        return q == n ? Knew + (size_t)u * D : rk0 + (size_t)(q % W) * D;
-      };
-      auto rowV = [&](int i) -> const T* {
-        const int64_t q = p0 + i;
-        return q == n ? Vnew + (size_t)u * D : rv0 + (size_t)(q % W) * D;
-      };
-      summarize_chunk_warp<T, D>(rowK, rowV, C,
-                                 ragged_eps ? ragged_eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr,
-                                 (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk, c.cfg,
-                                 static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D,
-                                 static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D);
     }
   }
   if (S == 1) {

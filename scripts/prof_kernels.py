@@ -33,6 +33,18 @@ if what in ("prefill_configs2", "summarize_configs2", "prefill_configs1"):
         else:
             eva.eva_attn_prefill(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, lse=lse,
                                  kernel=os.environ.get("EVA_PROF_KERNEL") or None)
+elif what == "decode_ragged_configs3":
+    BH, d, C, W, ctx = 256 * 32, 128, 64, 256, 32768
+    cfg = eva.make_config(256, 32, 0, d, C, W)
+    cache = eva.DecodeCache(cfg, (ctx + 64) // C + 16, device=dev)
+    for t in (cache.ring_k, cache.ring_v, cache.sum_k, cache.sum_v):
+        t.normal_()
+    cache.c.pos = ctx
+    pos = ctx - 64 * (torch.arange(BH, device=dev, dtype=torch.int64) % 64)
+    q = torch.randn(BH, d, device=dev).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    for _ in range(reps):
+        cache.eva_decode_step_ragged(pos, q, q, q, O=o, want_lse=False)
 elif what == "decode_configs3":
     BH, d, C, W, ctx = 256 * 32, 128, 64, 256, 32768
     cfg = eva.make_config(256, 32, 0, d, C, W)
