@@ -58,6 +58,7 @@ def _L():
         lib.oracle_summarize_proj.argtypes = [i, i, i, D, D, D, D, d_, d_, i, D, D, D]
         lib.oracle_rope.argtypes = [i, i, d_, ctypes.c_int64, D]
         lib.oracle_rope_ex.argtypes = [i, i, d_, i, i, I64, i, D]
+        lib.oracle_backward_proj.argtypes = [i, i, i, i, i, d_, d_, d_, i, D, D, D, D, D, D, D, D, D, D]
         lib.oracle_prefill.argtypes = [i, i, i, i, i, d_, D, D, D, D, D, D, D]
         lib.oracle_summarize_batch.argtypes = [i, i, i, i, D, D, D, d_, d_, i, D, D]
         lib.oracle_prefill_batch.argtypes = [i, i, i, i, i, i, d_, D, D, D, D, D, D, D]
@@ -267,6 +268,20 @@ def backward(Q, K, V, eps_, dO, C: int, W: int, mode: int = SLIDING, scale: floa
     _L().oracle_backward_ext(T, d, C, W, mode, scale, bias, lam, clip, omega_mode, _dp(Q), _dp(K),
                              _dp(V), _dp(E), _dp(dO), _dp(dQ), _dp(dK), _dp(dV))
     return dQ, dK, dV
+
+
+def backward_proj(Q, K, V, eps_, P, dO, C: int, W: int, mode: int = SLIDING, scale: float = 1.0,
+                  lam: float = 0.1, clip: float = 1.0, omega_mode: int = 0):
+    """Gradients (dQ, dK, dV, dP) of L = sum(dO * O) for one unit with the learned summary-key
+    projection P [d, d] (oracle_backward_proj, R17); dP is this unit's contribution."""
+    Q, K, V, dO, P = _f64(Q), _f64(K), _f64(V), _f64(dO), _f64(P)
+    T, d = Q.shape
+    nC = T // C
+    E = _f64(eps_).reshape(nC, d) if nC else np.zeros((1, d))
+    dQ, dK, dV, dP = np.zeros((T, d)), np.zeros((T, d)), np.zeros((T, d)), np.zeros((d, d))
+    _L().oracle_backward_proj(T, d, C, W, mode, scale, lam, clip, omega_mode, _dp(Q), _dp(K), _dp(V),
+                              _dp(E), _dp(P), _dp(dO), _dp(dQ), _dp(dK), _dp(dV), _dp(dP))
+    return dQ, dK, dV, dP
 
 
 def backward_batch(Q, K, V, E, dO, C: int, W: int, mode: int = SLIDING, scale: float = 1.0,

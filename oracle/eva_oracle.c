@@ -677,6 +677,154 @@ EXPORT void oracle_backward_ext(int T, int d, int C, int W, int mode, double sca
   free(a); free(dom); free(kt); free(bt); free(om); free(dkt); free(dbt); free(logit); free(o);
 }
 
+/* Backward with the learned summary-key projection (NEXT row 4, DESIGN R17): the forward is  */
+/* oracle_summarize_proj (k~_c = P mean_c, mu_c = k~_c in Eq.15, xi from the raw keys) and     */
+/* oracle_prefill on (k~, beta^).  The attention part is oracle_backward_ext's (causal modes,  */
+/* no bias); through the summaries, per chunk c with dk~ from the attention and d beta^:       */
+/*   dv_i += w_i d beta^;  da_i = w_i (d beta^ . v_i - d beta^ . beta^);                      */
+/*   dk_i += da_i (omega - k_i);  d omega = sum_i da_i k_i;                                   */
+/*   g_j = d k~_j + lambda [|k~_j + eps_j| <= clip] d omega_j   (omega_mode 1: + d omega_j);  */
+/*   k~ = P mean:  d mean = P^T g,  dk_i += d mean / C,  dP += g mean^T.                       */
+/* P [d, d] row-major; dP [d, d] is ACCUMULATED (the caller zeroes it).                        */
+EXPORT void oracle_backward_proj(int T, int d, int C, int W, int mode, double scale, double lambda,
+                                 double clipv, int omega_mode, const double* Q, const double* K,
+                                 const double* V, const double* eps, const double* P, const double* dO,
+                                 double* dQ, double* dK, double* dV, double* dP) {
+  const int nC = T / C;
+  const size_t nd = (size_t)(nC > 0 ? nC : 1) * d;
+  double* kt = (double*)calloc(nd, sizeof(double));
+  double* bt = (double*)calloc(nd, sizeof(double));
+  double* om = (double*)calloc(nd, sizeof(double));
+  double* dkt = (double*)calloc(nd, sizeof(double));
+  double* dbt = (double*)calloc(nd, sizeof(double));
+  double* logit = (double*)malloc(sizeof(double) * ((size_t)T + nC + 1));
+  double* o = (double*)malloc(sizeof(double) * d);
+  if (nC > 0) oracle_summarize_proj(T, d, C, K, V, eps, P, lambda, clipv, omega_mode, kt, bt, om);
+  memset(dQ, 0, sizeof(double) * (size_t)T * d);
+  memset(dK, 0, sizeof(double) * (size_t)T * d);
+  memset(dV, 0, sizeof(double) * (size_t)T * d);
+  for (int n = 0; n < T; ++n) {  /* the attention: softmax over the summaries and the window */
+    int64_t lo, hi, s1, s2;
+    visible_set(n, T, C, W, mode, &lo, &hi, &s1, &s2);
+    const double* q = Q + (size_t)n * d;
+    const double* g = dO + (size_t)n * d;
+    int cnt = 0;
+    double mx = -INFINITY;
+    for (int64_t c = 0; c < nC; ++c) {
+      if (!(c < s1 || c >= s2)) continue;
+      double t = 0.0;
+      for (int j = 0; j < d; ++j) t += q[j] * kt[(size_t)c * d + j];
+      logit[cnt] = scale * t;
+      if (logit[cnt] > mx) mx = logit[cnt];
+      ++cnt;
+    }
+    for (int64_t m = lo; m < hi; ++m, ++cnt) {
+      double t = 0.0;
+      for (int j = 0; j < d; ++j) t += q[j] * K[(size_t)m * d + j];
+      logit[cnt] = scale * t;
+      if (logit[cnt] > mx) mx = logit[cnt];
+    }
+    double z = 0.0;
+    for (int i = 0; i < cnt; ++i) z += exp(logit[i] - mx);
+    for (int i = 0; i < cnt; ++i) logit[i] = exp(logit[i] - mx) / z;
+    for (int j = 0; j < d; ++j) o[j] = 0.0;
+    int i = 0;
+    for (int64_t c = 0; c < nC; ++c) {
+      if (!(c < s1 || c >= s2)) continue;
+      for (int j = 0; j < d; ++j) o[j] += logit[i] * bt[(size_t)c * d + j];
+      ++i;
+    }
+    for (int64_t m = lo; m < hi; ++m, ++i)
+      for (int j = 0; j < d; ++j) o[j] += logit[i] * V[(size_t)m * d + j];
+    double Dn = 0.0;
+    for (int j = 0; j < d; ++j) Dn += g[j] * o[j];
+    i = 0;
+    for (int64_t c = 0; c < nC; ++c) {
+      if (!(c < s1 || c >= s2)) continue;
+      double dp = 0.0;
+      for (int j = 0; j < d; ++j) dp += g[j] * bt[(size_t)c * d + j];
+      const double dS = logit[i] * (dp - Dn);
+      for (int j = 0; j < d; ++j) {
+        dQ[(size_t)n * d + j] += scale * dS * kt[(size_t)c * d + j];
+        dkt[(size_t)c * d + j] += scale * dS * q[j];
+        dbt[(size_t)c * d + j] += logit[i] * g[j];
+      }
+      ++i;
+    }
+    for (int64_t m = lo; m < hi; ++m, ++i) {
+      double dp = 0.0;
+      for (int j = 0; j < d; ++j) dp += g[j] * V[(size_t)m * d + j];
+      const double dS = logit[i] * (dp - Dn);
+      for (int j = 0; j < d; ++j) {
+        dQ[(size_t)n * d + j] += scale * dS * K[(size_t)m * d + j];
+        dK[(size_t)m * d + j] += scale * dS * q[j];
+        dV[(size_t)m * d + j] += logit[i] * g[j];
+      }
+    }
+  }
+  double* a = (double*)malloc(sizeof(double) * (C > 0 ? C : 1));
+  double* dom = (double*)malloc(sizeof(double) * d);
+  double* gk = (double*)malloc(sizeof(double) * d);
+  double* mean = (double*)malloc(sizeof(double) * d);
+  for (int c = 0; c < nC; ++c) {  /* through the summaries of chunk c */
+    const double* Kc = K + (size_t)c * C * d;
+    const double* Vc = V + (size_t)c * C * d;
+    const double* w_om = om + (size_t)c * d;
+    const double* db = dbt + (size_t)c * d;
+    const double* be = bt + (size_t)c * d;
+    for (int j = 0; j < d; ++j) {
+      mean[j] = 0.0;
+      for (int r = 0; r < C; ++r) mean[j] += Kc[(size_t)r * d + j];
+      mean[j] /= (double)C;
+    }
+    double amax = -INFINITY;
+    for (int r = 0; r < C; ++r) {
+      double dot = 0.0, nrm = 0.0;
+      for (int j = 0; j < d; ++j) {
+        dot += w_om[j] * Kc[(size_t)r * d + j];
+        nrm += Kc[(size_t)r * d + j] * Kc[(size_t)r * d + j];
+      }
+      a[r] = dot - 0.5 * nrm;
+      if (a[r] > amax) amax = a[r];
+    }
+    double zz = 0.0;
+    for (int r = 0; r < C; ++r) zz += exp(a[r] - amax);
+    double dbb = 0.0;
+    for (int j = 0; j < d; ++j) dbb += db[j] * be[j];
+    for (int j = 0; j < d; ++j) dom[j] = 0.0;
+    for (int r = 0; r < C; ++r) {
+      const double w = exp(a[r] - amax) / zz;
+      double dbv = 0.0;
+      for (int j = 0; j < d; ++j) dbv += db[j] * Vc[(size_t)r * d + j];
+      const double da = w * (dbv - dbb);
+      for (int j = 0; j < d; ++j) {
+        dV[((size_t)c * C + r) * d + j] += w * db[j];
+        dK[((size_t)c * C + r) * d + j] += da * (w_om[j] - Kc[(size_t)r * d + j]);
+        dom[j] += da * Kc[(size_t)r * d + j];
+      }
+    }
+    for (int j = 0; j < d; ++j) {  /* g = total gradient of k~_c */
+      gk[j] = dkt[(size_t)c * d + j];
+      if (omega_mode == 0) {
+        const double x = kt[(size_t)c * d + j] + eps[(size_t)c * d + j];
+        if (x >= -clipv && x <= clipv) gk[j] += lambda * dom[j];
+      } else {
+        gk[j] += dom[j];
+      }
+    }
+    for (int l = 0; l < d; ++l) {  /* d mean = P^T g, spread over the chunk's rows; dP += g mean^T */
+      double dm = 0.0;
+      for (int j = 0; j < d; ++j) dm += (P ? P[(size_t)j * d + l] : (j == l ? 1.0 : 0.0)) * gk[j];
+      for (int r = 0; r < C; ++r) dK[((size_t)c * C + r) * d + l] += dm / (double)C;
+    }
+    if (dP)
+      for (int j = 0; j < d; ++j)
+        for (int l = 0; l < d; ++l) dP[(size_t)j * d + l] += gk[j] * mean[l];
+  }
+  free(a); free(dom); free(gk); free(mean); free(kt); free(bt); free(om); free(dkt); free(dbt);
+  free(logit); free(o);
+}
+
 EXPORT void oracle_backward(int T, int d, int C, int W, int mode, double scale, double lambda,
                             double clipv, int omega_mode, const double* Q, const double* K,
                             const double* V, const double* eps, const double* dO, double* dQ,

@@ -60,3 +60,54 @@ def test_scaled_identity_scales_the_mean():
     ks0, _ = oracle.summarize(K, V, E, C)
     ks, _ = oracle.summarize_proj(K, V, E, a * np.eye(d), C)
     np.testing.assert_allclose(ks, a * ks0, rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------------------------- backward through the projection
+def _loss_proj(Q, K, V, E, P, dO, C, W, mode, scale, lam, clip, om):
+    ks, vs = oracle.summarize_proj(K, V, E, P, C, lam=lam, clip=clip, omega_mode=om)
+    O, _ = oracle.prefill(Q, K, V, ks, vs, C, W, mode, scale)
+    return float(np.sum(O * dO))
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.parametrize("om", [0, 1])
+@pytest.mark.parametrize("mode", [oracle.SLIDING, oracle.BLOCK])
+def test_backward_proj_finite_differences(om, mode):
+    """dQ, dK, dV and dP of oracle_backward_proj against central differences of the forward
+    (summarize_proj + prefill), with a clip that bites (lambda = 1, eps 1.5x) so the Eq.15 gate
+    and both omega readings matter, on a non-symmetric P."""
+    rng = np.random.default_rng(11 + om + 3 * mode)
+    T, d, C, W = 22, 4, 4, 8
+    Q, K, V, dO = (rng.standard_normal((T, d)) for _ in range(4))
+    E = 1.5 * rng.standard_normal((T // C, d))
+    P = rng.standard_normal((d, d)) * 0.7 + np.eye(d)
+    lam, clip, scale = 1.0, 1.0, 0.8
+    dQ, dK, dV, dP = oracle.backward_proj(Q, K, V, E, P, dO, C, W, mode, scale, lam, clip, om)
+    h = 1e-6
+    for name, X, G in (("Q", Q, dQ), ("K", K, dK), ("V", V, dV), ("P", P, dP)):
+        idx = [tuple(rng.integers(0, s) for s in X.shape) for _ in range(12)]
+        for ix in idx:
+            Xp, Xm = X.copy(), X.copy()
+            Xp[ix] += h
+            Xm[ix] -= h
+            args = dict(Q=Q, K=K, V=V, P=P)
+            args[name] = Xp
+            lp = _loss_proj(args["Q"], args["K"], args["V"], E, args["P"], dO, C, W, mode, scale, lam, clip, om)
+            args[name] = Xm
+            lm = _loss_proj(args["Q"], args["K"], args["V"], E, args["P"], dO, C, W, mode, scale, lam, clip, om)
+            fd = (lp - lm) / (2 * h)
+            assert abs(fd - G[ix]) <= 1e-6 * max(1.0, abs(fd)), (name, ix, fd, G[ix])
+
+
+def test_backward_proj_identity_equals_plain_backward():
+    """P = I reduces to the pinned oracle_backward (k~ = mean); dP = sum_c g_c mean_c^T."""
+    rng = np.random.default_rng(5)
+    T, d, C, W = 40, 8, 8, 16
+    Q, K, V, dO = (rng.standard_normal((T, d)) for _ in range(4))
+    E = rng.standard_normal((T // C, d))
+    a = oracle.backward_proj(Q, K, V, E, np.eye(d), dO, C, W, scale=0.5)
+    b = oracle.backward(Q, K, V, E, dO, C, W, scale=0.5)
+    for x, y in zip(a[:3], b):
+        np.testing.assert_allclose(x, y, rtol=0, atol=1e-12)
