@@ -427,6 +427,25 @@ eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K
                              const void* dO, const float* eps, void* dQ, void* dK, void* dV,
                              void* workspace, size_t workspace_bytes, eva_stream_t stream);
 
+/* eva_attn_backward_proj: eva_attn_backward when the summaries came from eva_summarize_proj
+ * (the learned summary-key projection of SURVEY §8(f) NEXT row 4, reading R17:
+ * k~_c = Pk[h] mean_c, mu_c = k~_c in Eq.15).  Through the summaries, with g_c the total
+ * gradient of k~_c (from the attention plus lambda * clip-gate * d omega):
+ *   d mean_c = Pk[h]^T g_c  (spread over the chunk's rows / C),   dPk[h] = sum_{u of head h, c} g_c mean_c^T.
+ * Pk    : device fp32 [H, d, d] row-major (as given to eva_summarize_proj), read only
+ * dPk   : device fp32 [H, d, d], OVERWRITTEN with the sum over this call's units of each head
+ *         (heads with no unit in [bh_begin, bh_begin + bh_count) get zeros); callers sharding
+ *         (b,h) across ranks sum dPk over the ranks
+ * workspace_bytes >= eva_backward_proj_workspace_bytes(cfg).  bf16, d in {32, 64, 128} and a
+ * chunk the register finalize takes (C <= 32 * 8 * 2 / (d * 2 / 16) rows), else
+ * EVA_ERR_UNSUPPORTED; causal modes, summary_bias 0. */
+size_t eva_backward_proj_workspace_bytes(const eva_config* cfg);
+eva_status eva_attn_backward_proj(const eva_config* cfg, const float* Pk, const void* Q, const void* K,
+                                  const void* V, const void* Ksum, const void* Vsum, const void* O,
+                                  const float* lse, const void* dO, const float* eps, void* dQ, void* dK,
+                                  void* dV, float* dPk, void* workspace, size_t workspace_bytes,
+                                  eva_stream_t stream);
+
 /* ---------------------------------------------------------------- debug / introspection
  * eva_mask_ranges: the (lo(n), nsum(n)) the kernels use, for n in
  * [n_begin, n_begin + count), written to device int64 arrays lo, nsum

@@ -59,7 +59,7 @@ EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache
            "eva_summarize_range", "eva_attn_prefill_range", "eva_summarize_range_bcast",
            "eva_summarize_proj", "eva_decode_ragged_workspace_bytes", "eva_decode_step_ragged",
            "eva_rope_summarize", "eva_rope", "eva_prefill_reserve", "eva_rope_ex",
-           "eva_rope_summarize_ex"]
+           "eva_rope_summarize_ex", "eva_backward_proj_workspace_bytes", "eva_attn_backward_proj"]
 
 
 class EvaError(RuntimeError):
@@ -96,6 +96,8 @@ def _load():
         "eva_decode_workspace_bytes": (ctypes.c_size_t, [CACHE]),
         "eva_backward_workspace_bytes": (ctypes.c_size_t, [CFG]),
         "eva_attn_backward": (st, [CFG] + [P] * 13 + [ctypes.c_size_t, P]),
+        "eva_backward_proj_workspace_bytes": (ctypes.c_size_t, [CFG]),
+        "eva_attn_backward_proj": (st, [CFG] + [P] * 15 + [ctypes.c_size_t, P]),
         "eva_mask_ranges": (st, [CFG, ctypes.c_int64, ctypes.c_int64, P, P, P]),
         "eva_philox": (st, [P, P, ctypes.c_int32, P]),
         "eva_draw_eps": (st, [CFG, P, P]),

@@ -341,12 +341,15 @@ def eva_attn_backward(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch
                       Ksum: torch.Tensor, Vsum: torch.Tensor, O: torch.Tensor, lse: torch.Tensor,
                       dO: torch.Tensor, *, eps: Optional[torch.Tensor] = None,
                       workspace: Optional[torch.Tensor] = None, dQ: Optional[torch.Tensor] = None,
-                      dK: Optional[torch.Tensor] = None, dV: Optional[torch.Tensor] = None):
-    """Gradient of the prefill for L = sum(dO * O).  Returns (dQ, dK, dV).
+                      dK: Optional[torch.Tensor] = None, dV: Optional[torch.Tensor] = None,
+                      Pk: Optional[torch.Tensor] = None, dPk: Optional[torch.Tensor] = None):
+    """Gradient of the prefill for L = sum(dO * O).  Returns (dQ, dK, dV), or (dQ, dK, dV, dPk)
+    when the summaries came from eva_summarize_proj with the projection Pk [H, d, d] fp32
+    (eva_attn_backward_proj, R17; dPk: this call's units' sum per head).
 
     Ksum/Vsum/O/lse/eps are what eva_attn_prefill used and produced.  workspace: a
-    uint8 CUDA tensor of at least eva_backward_workspace_bytes(cfg) bytes (allocated
-    here when None)."""
+    uint8 CUDA tensor of at least eva_backward_workspace_bytes(cfg) (with Pk:
+    eva_backward_proj_workspace_bytes) bytes, allocated here when None."""
     dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
     nC = T // cfg.chunk
     for t, nm in ((Q, "Q"), (K, "K"), (V, "V"), (O, "O"), (dO, "dO")):
@@ -362,9 +365,21 @@ def eva_attn_backward(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch
     dV = torch.empty_like(V) if dV is None else dV
     for t, nm in ((dQ, "dQ"), (dK, "dK"), (dV, "dV")):
         _need(t, nm, (bh, T, d), dt)
-    nbytes = eva_backward_workspace_bytes(cfg)
+    if Pk is not None:
+        _need(Pk, "Pk", (cfg.H, d, d), torch.float32)
+        dPk = torch.empty_like(Pk) if dPk is None else dPk
+        _need(dPk, "dPk", (cfg.H, d, d), torch.float32)
+        nbytes = int(lib.eva_backward_proj_workspace_bytes(ctypes.byref(cfg)))
+    else:
+        nbytes = eva_backward_workspace_bytes(cfg)
     if workspace is None:
         workspace = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=Q.device)
+    if Pk is not None:
+        check(lib.eva_attn_backward_proj(ctypes.byref(cfg), _ptr(Pk), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum),
+                                         _ptr(Vsum), _ptr(O), _ptr(lse), _ptr(dO), _ptr(eps), _ptr(dQ), _ptr(dK),
+                                         _ptr(dV), _ptr(dPk), _ptr(workspace), workspace.numel(),
+                                         _stream(Q.device)))
+        return dQ, dK, dV, dPk
     check(lib.eva_attn_backward(ctypes.byref(cfg), _ptr(Q), _ptr(K), _ptr(V), _ptr(Ksum), _ptr(Vsum),
                                 _ptr(O), _ptr(lse), _ptr(dO), _ptr(eps), _ptr(dQ), _ptr(dK), _ptr(dV),
                                 _ptr(workspace), workspace.numel(), _stream(Q.device)))

@@ -735,12 +735,15 @@ size_t eva_backward_workspace_bytes(const eva_config* cfg) {
   return eva::backward_workspace_bytes(*cfg);
 }
 
-eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K, const void* V,
-                             const void* Ksum, const void* Vsum, const void* O, const float* lse,
-                             const void* dO, const float* eps, void* dQ, void* dK, void* dV,
-                             void* workspace, size_t workspace_bytes, eva_stream_t stream) {
-  eva_status st = check_cfg(cfg, true);
-  if (st != EVA_OK) return st;
+}  // extern "C"
+namespace {
+// Validation and launch shared by eva_attn_backward and eva_attn_backward_proj (cfg checked).
+eva_status backward_common(const eva_config* cfg, const void* Q, const void* K, const void* V,
+                           const void* Ksum, const void* Vsum, const void* O, const float* lse,
+                           const void* dO, const float* eps, void* dQ, void* dK, void* dV,
+                           void* workspace, size_t workspace_bytes, eva_stream_t stream, const float* Pk,
+                           float* dPk) {
+  eva_status st = EVA_OK;
   if (cfg->mode == EVA_NONCAUSAL && cfg->T % cfg->chunk != 0)
     return fail(EVA_ERR_INVALID_ARG, "EVA_NONCAUSAL needs T %% chunk == 0 (T=%d chunk=%d)", cfg->T,
                 cfg->chunk);
@@ -759,9 +762,48 @@ eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K
   const size_t need = eva::backward_workspace_bytes(*cfg);
   if (workspace_bytes < need)
     return fail(EVA_ERR_INVALID_ARG, "workspace_bytes %zu < %zu", workspace_bytes, need);
-  return cuda_status(eva::launch_backward(*cfg, Q, K, V, Ksum, Vsum, O, lse, dO, eps, dQ, dK, dV,
-                                          workspace, (cudaStream_t)stream),
-                     "eva_attn_backward");
+  const cudaError_t e = eva::launch_backward(*cfg, Q, K, V, Ksum, Vsum, O, lse, dO, eps, dQ, dK, dV, workspace,
+                                             (cudaStream_t)stream, Pk, dPk);
+  if (e == cudaErrorNotSupported) return fail(EVA_ERR_UNSUPPORTED, "eva_attn_backward: projection path");
+  return cuda_status(e, "eva_attn_backward");
+}
+}  // namespace
+extern "C" {
+
+size_t eva_backward_proj_workspace_bytes(const eva_config* cfg) {
+  if (!cfg) return 0;
+  return eva::backward_workspace_bytes(*cfg) + eva::backward_proj_extra_bytes(*cfg);
+}
+
+eva_status eva_attn_backward_proj(const eva_config* cfg, const float* Pk, const void* Q, const void* K,
+                                  const void* V, const void* Ksum, const void* Vsum, const void* O,
+                                  const float* lse, const void* dO, const float* eps, void* dQ, void* dK,
+                                  void* dV, float* dPk, void* workspace, size_t workspace_bytes,
+                                  eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if ((st = check_causal(cfg, "eva_attn_backward_proj")) != EVA_OK) return st;
+  if (cfg->summary_bias != 0.f) return fail(EVA_ERR_UNSUPPORTED, "eva_attn_backward_proj: summary_bias must be 0");
+  if (!eva::backward_proj_supported(*cfg))
+    return fail(EVA_ERR_UNSUPPORTED, "eva_attn_backward_proj: bf16, d in {32,64,128} and a chunk the register "
+                                     "finalize takes (d=%d C=%d)", cfg->d_head, cfg->chunk);
+  if (!Pk || !dPk) return fail(EVA_ERR_INVALID_ARG, "Pk / dPk is NULL");
+  if (!aligned16(Pk) || !aligned16(dPk)) return fail(EVA_ERR_INVALID_ARG, "Pk / dPk not 16-byte aligned");
+  const size_t need = eva_backward_proj_workspace_bytes(cfg);
+  if (workspace_bytes < need)
+    return fail(EVA_ERR_INVALID_ARG, "workspace_bytes %zu < %zu", workspace_bytes, need);
+  return backward_common(cfg, Q, K, V, Ksum, Vsum, O, lse, dO, eps, dQ, dK, dV, workspace, workspace_bytes,
+                         stream, Pk, dPk);
+}
+
+eva_status eva_attn_backward(const eva_config* cfg, const void* Q, const void* K, const void* V,
+                             const void* Ksum, const void* Vsum, const void* O, const float* lse,
+                             const void* dO, const float* eps, void* dQ, void* dK, void* dV,
+                             void* workspace, size_t workspace_bytes, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  return backward_common(cfg, Q, K, V, Ksum, Vsum, O, lse, dO, eps, dQ, dK, dV, workspace, workspace_bytes,
+                         stream, nullptr, nullptr);
 }
 
 eva_status eva_mask_ranges(const eva_config* cfg, int64_t n_begin, int64_t count, int64_t* lo,

@@ -563,17 +563,24 @@ __global__ void __launch_bounds__(128) bwd_finalize_kernel(eva_config cfg, const
 // COEF (the fused path of the tcgen05 main pass): instead of the rows, write the chain-rule
 // coefficients the local items apply -- w_i, da_i per row into cf.w / cf.da, omega and
 // d k~ / C per chunk into cf.om / cf.dkt (BwdFusedArgs); grid = complete chunks only.
+// Projection (Pk != nullptr, NEXT row 4 reading R17: k~ = P_h mean): k~ and omega from P mean,
+// and at the end the chunk's total k~ gradient g is mapped back through P (d mean = P^T g,
+// spread over the rows as before) and stored with the mean for dP = sum_c g_c mean_c^T
+// (bwd_dp_kernel): proj_g / proj_mean [bh, nC, d] fp32.
 template <typename T, int D, int NI, bool COEF = false>
 __global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, const T* __restrict__ K,
                                                                const T* __restrict__ V,
                                                                const float* __restrict__ eps, BwdWs ws,
                                                                T* __restrict__ dQ, T* __restrict__ dK,
-                                                               T* __restrict__ dV, BwdFusedArgs cf) {
+                                                               T* __restrict__ dV, BwdFusedArgs cf,
+                                                               const float* __restrict__ Pk = nullptr,
+                                                               float* __restrict__ proj_g = nullptr,
+                                                               float* __restrict__ proj_mean = nullptr) {
   constexpr int VEC = 16 / sizeof(T);
   constexpr int TPR = D / VEC;
   constexpr int RPW = 32 / TPR;
   __shared__ float sh_red[4][D];
-  __shared__ float sh_om[D], sh_g[D], sh_db[D], sh_dkt[D];
+  __shared__ float sh_om[D], sh_g[D], sh_db[D], sh_dkt[D], sh_mean[D];
   __shared__ float sh_w[8];
   const int Tn = cfg.T, C = cfg.chunk, nC = Tn / C;
   const int u = blockIdx.y, c = blockIdx.x;
@@ -634,9 +641,24 @@ __global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, c
   }
   merge_cols(acc);
   __syncthreads();
+  const float* Ph = Pk ? Pk + (size_t)((cfg.bh_begin + u) % cfg.H) * D * D : nullptr;
+  if (Ph) {  // the chunk mean first: every projected channel reads all of it
+    if (threadIdx.x < D) {
+      const int j = threadIdx.x;
+      sh_mean[j] = (sh_red[0][j] + sh_red[1][j] + sh_red[2][j] + sh_red[3][j]) * (1.0f / (float)C);
+      proj_mean[srow + j] = sh_mean[j];
+    }
+    __syncthreads();
+  }
   if (threadIdx.x < D) {
     const int j = threadIdx.x;
-    const float kt = (sh_red[0][j] + sh_red[1][j] + sh_red[2][j] + sh_red[3][j]) * (1.0f / (float)C);
+    float kt;
+    if (Ph) {
+      kt = 0.f;
+      for (int l = 0; l < D; ++l) kt = fmaf(__ldg(Ph + (size_t)j * D + l), sh_mean[l], kt);
+    } else {
+      kt = (sh_red[0][j] + sh_red[1][j] + sh_red[2][j] + sh_red[3][j]) * (1.0f / (float)C);
+    }
     const uint32_t bh = (uint32_t)(cfg.bh_begin + u);
     const float e = eps ? eps[srow + j] : philox_normal1(cfg.seed, cfg.layer, bh, (uint32_t)c, (uint32_t)j);
     sh_om[j] = omega_of(kt, e, cfg);
@@ -735,9 +757,24 @@ __global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, c
   if (threadIdx.x < D) {
     const int j = threadIdx.x;
     const float dom = sh_red[0][j] + sh_red[1][j] + sh_red[2][j] + sh_red[3][j];
-    sh_dkt[j] = (ws.dKs[srow + j] + sh_g[j] * dom) * (1.0f / (float)C);  // d k~ / C
+    const float gj = ws.dKs[srow + j] + sh_g[j] * dom;  // total gradient of k~_j
+    if (Ph) {
+      sh_mean[j] = gj;  // (the mean itself is no longer needed here: stored above)
+      proj_g[srow + j] = gj;
+    } else {
+      sh_dkt[j] = gj * (1.0f / (float)C);  // d k~ / C
+    }
   }
   __syncthreads();
+  if (Ph) {  // d mean = P^T g, spread over the C rows
+    if (threadIdx.x < D) {
+      const int l = threadIdx.x;
+      float dm = 0.f;
+      for (int j = 0; j < D; ++j) dm = fmaf(__ldg(Ph + (size_t)j * D + l), sh_mean[j], dm);
+      sh_dkt[l] = dm * (1.0f / (float)C);
+    }
+    __syncthreads();
+  }
   if constexpr (COEF) {
     if (threadIdx.x < D) {
       cf.om[srow + threadIdx.x] = sh_om[threadIdx.x];
@@ -784,6 +821,47 @@ __global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, c
     *reinterpret_cast<uint4*>(dK + o) = *reinterpret_cast<const uint4*>(ok);
     *reinterpret_cast<uint4*>(dV + o) = *reinterpret_cast<const uint4*>(ov);
   }
+}
+
+// dP_h = sum over the units u of head h and their chunks c of g_{u,c} mean_{u,c}^T (the learned
+// projection's gradient, R17).  Block = one 32 x 32 tile of one head's [D, D]; the (unit, chunk)
+// rows are walked in batches of 32 staged in shared memory; 256 threads x 4 outputs.
+template <int D>
+__global__ void __launch_bounds__(256) bwd_dp_kernel(eva_config cfg, const float* __restrict__ g,
+                                                     const float* __restrict__ mean, float* __restrict__ dP) {
+  __shared__ float sg[32][33], sm[32][33];
+  const int h = blockIdx.z, j0 = blockIdx.y * 32, l0 = blockIdx.x * 32;
+  const int nC = cfg.T / cfg.chunk;
+  const int tj = threadIdx.x / 8, tl = (threadIdx.x % 8) * 4;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // units of head h in this shard: u with (bh_begin + u) % H == h
+  const int u_first = ((h - cfg.bh_begin) % cfg.H + cfg.H) % cfg.H;
+  const int n_units = u_first < cfg.bh_count ? (cfg.bh_count - 1 - u_first) / cfg.H + 1 : 0;
+  const int rows = n_units * nC;
+  for (int r0 = 0; r0 < rows; r0 += 32) {
+    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+      const int rr = i / 32, cc = i % 32, r = r0 + rr;
+      float gv = 0.f, mv = 0.f;
+      if (r < rows) {
+        const int u = u_first + (r / nC) * cfg.H, c = r % nC;
+        const size_t row = ((size_t)u * nC + c) * D;
+        gv = g[row + j0 + cc];
+        mv = mean[row + l0 + cc];
+      }
+      sg[rr][cc] = gv;
+      sm[rr][cc] = mv;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const float gv = sg[rr][tj];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = fmaf(gv, sm[rr][tl + k], acc[k]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) dP[((size_t)h * D + j0 + tj) * D + l0 + tl + k] = acc[k];
 }
 
 // dQ of the fused path: the fp32 accumulator to cfg.dtype, 8 elements per thread.
@@ -852,11 +930,30 @@ size_t backward_workspace_bytes(const eva_config& cfg) {
   return align256(BH * T * 4) + 3 * align256(BH * T * d * 4) + 2 * align256(BH * nC * d * 4);
 }
 
+size_t backward_proj_extra_bytes(const eva_config& cfg) {
+  return 2 * align256((size_t)cfg.bh_count * (size_t)(cfg.T / cfg.chunk) * cfg.d_head * 4);
+}
+
+bool backward_proj_supported(const eva_config& cfg) {
+  const int D = cfg.d_head;
+  if (cfg.dtype != EVA_BF16 || (D != 32 && D != 64 && D != 128)) return false;
+  const int rpw = 32 / (D * 2 / 16);
+  return (cfg.chunk + 4 * rpw - 1) / (4 * rpw) <= 8;  // the register finalize takes the chunk
+}
+
 cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K, const void* V,
                             const void* Ksum, const void* Vsum, const void* O, const float* lse,
                             const void* dO, const float* eps, void* dQ, void* dK, void* dV,
-                            void* workspace, cudaStream_t s) {
+                            void* workspace, cudaStream_t s, const float* Pk, float* dPk) {
   const BwdWs ws = carve(cfg, workspace);
+  // projection: [g | mean] per chunk after the regular workspace
+  float* proj_g = nullptr;
+  float* proj_mean = nullptr;
+  if (Pk) {
+    char* extra = static_cast<char*>(workspace) + backward_workspace_bytes(cfg);
+    proj_g = reinterpret_cast<float*>(extra);
+    proj_mean = reinterpret_cast<float*>(extra + backward_proj_extra_bytes(cfg) / 2);
+  }
   const int Tn = cfg.T, C = cfg.chunk, nC = Tn / C;
   const ItemPlan plan = plan_items(cfg);
   cudaError_t err = cudaSuccess;
@@ -889,7 +986,7 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
           auto fn = ni_ <= 2 ? bwd_finalize_reg_kernel<T, D, 2, true>
                              : ni_ <= 4 ? bwd_finalize_reg_kernel<T, D, 4, true> : bwd_finalize_reg_kernel<T, D, 8, true>;
           fn<<<dim3(nC, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, ws, (T*)dQ, (T*)dK,
-                                                    (T*)dV, cf);
+                                                    (T*)dV, cf, Pk, proj_g, proj_mean);
         }
       }
       err = launch_backward_main_sm100(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws.D, ws.dQ, ws.dK, ws.dV,
@@ -898,8 +995,13 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
       const size_t n8 = BH * (size_t)Tn * D / 8;
       const int blocks = (int)std::min<size_t>((n8 + 255) / 256, (size_t)num_sms() * 8);
       bwd_dq_convert_kernel<T><<<std::max(blocks, 1), 256, 0, s>>>(ws.dQ, (T*)dQ, n8);
+      if (Pk) {
+        if (nC > 0) bwd_dp_kernel<D><<<dim3(D / 32, D / 32, cfg.H), 256, 0, s>>>(cfg, proj_g, proj_mean, dPk);
+        else err = cudaMemsetAsync(dPk, 0, (size_t)cfg.H * D * D * 4, s);
+        note_launch(1);
+      }
       note_launch(3 + (nC > 0 ? 1 : 0) + (plan.n_sum_items > 0 ? 1 : 0));
-      return cudaGetLastError();
+      return err != cudaSuccess ? err : cudaGetLastError();
     }
     if (tc) {
       err = launch_backward_main_sm100(cfg, Q, K, V, Ksum, Vsum, dO, lse, ws.D, ws.dQ, ws.dK, ws.dV,
@@ -921,7 +1023,15 @@ cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K,
       auto fn = ni <= 2 ? bwd_finalize_reg_kernel<T, D, 2> : ni <= 4 ? bwd_finalize_reg_kernel<T, D, 4>
                                                                      : bwd_finalize_reg_kernel<T, D, 8>;
       fn<<<dim3(nC + n_tail, cfg.bh_count), 128, 0, s>>>(cfg, (const T*)K, (const T*)V, eps, ws, (T*)dQ,
-                                                         (T*)dK, (T*)dV, BwdFusedArgs{});
+                                                         (T*)dK, (T*)dV, BwdFusedArgs{}, Pk, proj_g, proj_mean);
+      if (Pk) {
+        if (nC > 0) bwd_dp_kernel<D><<<dim3(D / 32, D / 32, cfg.H), 256, 0, s>>>(cfg, proj_g, proj_mean, dPk);
+        else err = cudaMemsetAsync(dPk, 0, (size_t)cfg.H * D * D * 4, s);
+        note_launch(1);
+        if (err != cudaSuccess) return err;
+      }
+    } else if (Pk) {
+      return cudaErrorNotSupported;  // the projection lives in the register finalize only
     } else {
       const size_t fsm = (size_t)(9 * D + 8 + 2 * C) * sizeof(float);
       err = set_smem_attr((const void*)bwd_finalize_kernel<T, D>, fsm);

@@ -114,10 +114,14 @@ cudaError_t launch_draw_eps(const eva_config& cfg, float* eps, cudaStream_t s);
 
 // Backward of the prefill (backward_simt.cu): dQ, dK, dV of L = sum(dO * O).
 size_t backward_workspace_bytes(const eva_config& cfg);
+// Pk (optional, R17): the learned summary-key projection [H, d, d]; dPk [H, d, d] fp32 gets the
+// sum over this call's units of each head (workspace + backward_proj_extra_bytes).
 cudaError_t launch_backward(const eva_config& cfg, const void* Q, const void* K, const void* V,
                             const void* Ksum, const void* Vsum, const void* O, const float* lse,
                             const void* dO, const float* eps, void* dQ, void* dK, void* dV,
-                            void* workspace, cudaStream_t s);
+                            void* workspace, cudaStream_t s, const float* Pk = nullptr, float* dPk = nullptr);
+size_t backward_proj_extra_bytes(const eva_config& cfg);
+bool backward_proj_supported(const eva_config& cfg);
 
 // Tensor-core main pass of the backward (backward_sm100.cu): bf16, d in {64, 128}.
 // phase 0: every work item, local dK/dV to the fp32 workspace (finalize applies the summary

@@ -3,7 +3,61 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../paper_2511_00576_b200/csrc/prefill_sm100.cu"
-namespace eva { void note_launch(int) {} int num_sms() { return 148; } }
+namespace eva { void note_launch(int) {} int num_sms() { return 148; }
+cudaError_t set_smem_attr(const void*, size_t) { return cudaSuccess; } }
+
+namespace eva { namespace {
+// ablations of softmax_tile2<D, 0> (VAR = 100 + bits): 1 exp -> FMUL, 2 no max tree, 4 no TMEM ld,
+// 8 no TMEM st (the remaining work kept live through a sink)
+template <int BITS>
+__device__ __forceinline__ void softmax_ablate(uint32_t s_addr, float scale_log2, float& m_ref, float& l) {
+  uint32_t sr[64];
+  if constexpr (!(BITS & 4)) {
+    tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+    tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+    tmem_wait_ld();
+  } else {
+#pragma unroll
+    for (int c = 0; c < 64; ++c) sr[c] = __float_as_uint(0.01f * (c + (threadIdx.x & 7)) + l * 1e-30f);
+  }
+  float mx = m_ref;
+  if constexpr (!(BITS & 2)) {
+    float pm[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pm[i] = __uint_as_float(sr[i]);
+#pragma unroll
+    for (int c = 8; c < 64; ++c) pm[c & 7] = fmaxf(pm[c & 7], __uint_as_float(sr[c]));
+    mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+    mx = mx * scale_log2;
+  }
+  const bool grow = mx > m_ref + 8.0f;
+  if (grow) m_ref = mx;
+  const float neg = (m_ref == -INFINITY ? 0.f : -m_ref);
+  const uint64_t sc2 = f2pack(scale_log2, scale_log2), ng2 = f2pack(neg, neg);
+  uint64_t ls[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const uint64_t x = ffma2(f2pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), sc2, ng2);
+    uint64_t p;
+    if constexpr (BITS & 1) p = ffma2(x, sc2, ng2);
+    else p = f2pack(ex2(f2lo(x)), ex2(f2hi(x)));
+    ls[c & 3] = fadd2(ls[c & 3], p);
+    sr[c] = pack_bf16(f2lo(p), f2hi(p));
+  }
+  const uint64_t s2 = fadd2(fadd2(ls[0], ls[1]), fadd2(ls[2], ls[3]));
+  l += f2lo(s2) + f2hi(s2);
+  if constexpr (!(BITS & 8)) {
+    tmem_st32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+    tmem_wait_st();
+  } else {
+    uint32_t a = 0;
+#pragma unroll
+    for (int c = 0; c < 32; ++c) a ^= sr[c];
+    l += __uint_as_float(a & 0x1u);
+  }
+  tc_fence_before();
+}
+}}
 
 namespace eva { namespace {
 // MMA load: warp 4 issues PV-shaped TS MMAs (M128 N128 K16, A = TMEM cols [64,96), B = smem,
@@ -53,9 +107,17 @@ __global__ void __launch_bounds__(160, 2) sm_bench(int iters, int full, unsigned
   for (int it = 0; it < iters; ++it) {
     const int vlo = full ? 0 : (lane & 7), vhi = full ? 64 : 60;
     if constexpr (VAR < 0) softmax_tile<D>(t_lane, t_lane + 128, vlo, vhi, 0.18f, m, l, [] {});
+    else if constexpr (VAR >= 100) softmax_ablate<VAR % 100>(t_lane, 0.18f, m, l);
     else softmax_tile2<D, VAR>(t_lane, t_lane + 128, vlo, vhi, 0, 0, 0.f, 0.18f, m, l, [] {});
-    // restore S (softmax overwrote the first 32 columns with P)
-    {
+    // restore S (softmax overwrote the first 32 columns with P); VAR >= 200: no restore,
+    // VAR >= 300: restore without tcgen05.wait::st
+    if constexpr (VAR >= 300) {
+      uint32_t init[32];
+      const uint4* src = reinterpret_cast<const uint4*>(init_s[warp][lane]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(&init[4 * i]) = src[i];
+      tmem_st32(t_lane, init);
+    } else if constexpr (VAR < 200) {
       uint32_t init[32];
       const uint4* src = reinterpret_cast<const uint4*>(init_s[warp][lane]);
 #pragma unroll
@@ -95,11 +157,16 @@ void run(const char* name, unsigned long long* d, float* sink) {
 int main() {
   unsigned long long* d; float* sink;
   cudaMalloc(&d, 296 * 4 * 8); cudaMalloc(&sink, 4);
-  run<-1>("softmax_tile", d, sink);
-  run<0>("softmax_tile2 emu 0/8", d, sink);
-  run<1>("softmax_tile2 emu 1/8", d, sink);
-  run<2>("softmax_tile2 emu 2/8", d, sink);
-  run<3>("softmax_tile2 emu 3/8", d, sink);
-  run<4>("softmax_tile2 emu 4/8", d, sink);
+  run<0>("softmax_tile2 (default)", d, sink);
+  run<100>("ablate: none", d, sink);
+  run<101>("ablate: exp->FMUL", d, sink);
+  run<102>("ablate: no max", d, sink);
+  run<104>("ablate: no TMEM ld", d, sink);
+  run<108>("ablate: no TMEM st", d, sink);
+  run<115>("ablate: all four", d, sink);
+  run<215>("all four, no restore", d, sink);
+  run<208>("no st, no restore", d, sink);
+  run<200>("none, no restore", d, sink);
+  run<315>("all four, st no wait", d, sink);
   return 0;
 }
