@@ -2,8 +2,8 @@
 
 The oracle's gradient is pinned in tests/test_oracle_backward.py (finite
 differences, autograd of the direct form, causal-softmax special cases).
-Tolerance: gradients are sums over many queries, so the bound is
-relative to the largest reference gradient:
+Tolerance (reading R20): gradients are sums over many queries, so the bound is
+the north_star tolerance on the gradient's own scale (absolute below 1):
     max |GPU - oracle| <= tol * max(1, max |oracle|),  tol = 1e-4 fp32, 2e-2 bf16.
 """
 import numpy as np
