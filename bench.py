@@ -591,6 +591,7 @@ def bench_prefill_strong(args, eva, torch, dev, s, rank, world, peaks, dist):
     gather_ms = None
     nccl = None
     if dist and world > 1:
+      try:
         # O of every rank into one [units, T, d] buffer (equal shards when world | 256)
         per = (units + world - 1) // world
         buf = torch.zeros(per, T, d, dtype=torch.bfloat16, device=dev)
@@ -608,6 +609,8 @@ def bench_prefill_strong(args, eva, torch, dev, s, rank, world, peaks, dist):
         nccl = {"nranks": world, "backend": dist.get_backend(), "collective": "all_gather_into_tensor(O)",
                 "bytes_per_rank": per * T * d * 2}
         del buf, out
+      except Exception as exc:  # the gather is context, not the measured value: never fail the line on it
+        nccl = {"nranks": world, "error": f"{type(exc).__name__}: {exc}"[:200]}
     pb = prefill_bytes(BH, T, d, C)
     pf = prefill_flops(BH, T, d, C, W)
     # per-rank ideal at the HBM roofline (the rank's algorithmic bytes / peak)
