@@ -367,6 +367,7 @@ struct RangePlan {
 // fused: 16 producer starts waiting for the summary flags, 17 flags ready; role 3 (summary
 // warps): 13 owned tile j landed, 14 tile j summarised and released, 15 flag published.
 __device__ unsigned long long* g_trace2 = nullptr;
+__device__ int g_trace_mid = 150;  // slots 2, 3 trace CTAs g_trace_mid, +1 (EVA_TRACE_MID)
 constexpr int TT_ROLES = 4, TT_PER_ROLE = 48;
 struct TileTrace {
   unsigned long long ev[TT_ROLES][TT_PER_ROLE];
@@ -374,7 +375,7 @@ struct TileTrace {
 };
 __device__ __forceinline__ int tt_slot() {
   const int id = blockIdx.y * gridDim.x + blockIdx.x;
-  return id == 0 ? 0 : id == 1 ? 1 : id == 150 ? 2 : id == 151 ? 3 : -1;
+  return id == 0 ? 0 : id == 1 ? 1 : id == g_trace_mid ? 2 : id == g_trace_mid + 1 ? 3 : -1;
 }
 template <bool TRACE>
 __device__ __forceinline__ void tt(TileTrace* tl, int role, int kind, int j) {
@@ -1131,6 +1132,12 @@ cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K
                              const void* Ksum, const void* Vsum, void* O, float* lse,
                              unsigned long long* trace_dev, bool fused, cudaStream_t s) {
   cudaError_t e = cudaMemcpyToSymbolAsync(g_trace2, &trace_dev, sizeof(trace_dev), 0, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  static const int mid = [] {
+    const char* v = getenv("EVA_TRACE_MID");
+    return v ? atoi(v) : 150;
+  }();
+  e = cudaMemcpyToSymbolAsync(g_trace_mid, &mid, sizeof(mid), 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
   const PrefillRange rg = full_range(cfg);
   if (fused) {  // traced for C = 64 (the configs' chunk size)
