@@ -30,12 +30,14 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "prefill_common.cuh"
 #include "sm100.cuh"
 
 namespace eva {
 namespace {
 
 using namespace sm100;
+using namespace pfx;
 constexpr int BM = 128;       // queries per tile
 constexpr int BN = 64;        // keys per KV tile
 constexpr int NTHREADS = 192;
@@ -94,29 +96,10 @@ struct FusedArgs {
   int nC, n_qt, units, total, order;
 };
 
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-
-
 // Columns outside [vlo, vhi) or inside [xlo, xhi) of a 64-column S tile set to -inf.  A 64-bit
 // valid mask is built once; each column then costs a shift pair (sign-extend its bit) and one
 // LOP3 select -- the per-column range compares cost ~6 instructions per column (ncu: the masked
 // tiles ran 383 extra instructions per warp, ~46 % of the tiles at configs[2]).
-__device__ __forceinline__ uint64_t range_bits(int lo, int hi) {
-  lo = max(lo, 0);
-  hi = min(hi, 64);
-  if (hi <= lo) return 0ull;
-  const uint64_t a = hi >= 64 ? ~0ull : ((1ull << hi) - 1ull);
-  const uint64_t b = (1ull << lo) - 1ull;
-  return a & ~b;
-}
 __device__ __forceinline__ void mask_columns(uint32_t (&sr)[64], int vlo, int vhi, int xlo, int xhi) {
   const uint64_t m = range_bits(vlo, vhi) & ~range_bits(xlo, xhi);
   const uint32_t mw[2] = {(uint32_t)m, (uint32_t)(m >> 32)};
@@ -199,43 +182,6 @@ __device__ __forceinline__ void softmax_tile(uint32_t s_addr, uint32_t o_addr, i
                                              float scale_log2, float& m_ref, float& l,
                                              const WaitO& wait_o) {
   softmax_tile_mx<D>(s_addr, o_addr, vlo, vhi, 0, 0, 0.f, scale_log2, m_ref, l, wait_o);
-}
-
-// ---- packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2: two lanes per issue slot)
-__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
-  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
-}
-__device__ __forceinline__ float f2lo(uint64_t v) { return __uint_as_float((uint32_t)v); }
-__device__ __forceinline__ float f2hi(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-
-// 2^x for x <= 0 on the FMA/ALU pipes (the MUFU pipe does 16 ex2 per clock per SM, a quarter of
-// what the softmax would need to keep pace with the tensor core at d = 64): x = n + f with
-// n = rint(x) via the 1.5*2^23 shifter, 2^f on [-1/2, 1/2] by a degree-3 polynomial (relative
-// error 7.5e-5, far below the bf16 rounding of P), and n added to the exponent field.  x is
-// clamped at -126 so that -inf (masked columns) gives a value below 2^-125 instead of garbage.
-__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x) {
-  const float lo = fmaxf(f2lo(x), -126.f), hi = fmaxf(f2hi(x), -126.f);
-  const uint64_t xc = f2pack(lo, hi);
-  const uint64_t SH = f2pack(12582912.f, 12582912.f), NSH = f2pack(-12582912.f, -12582912.f);
-  const uint64_t j = fadd2(xc, SH);                    // low mantissa bits hold rint(x)
-  const uint64_t f = ffma2(fadd2(j, NSH), f2pack(-1.f, -1.f), xc);  // x - rint(x), exact
-  uint64_t p = ffma2(f2pack(0.055171627551317215f, 0.055171627551317215f), f,
-                     f2pack(0.24261116981506348f, 0.24261116981506348f));
-  p = ffma2(p, f, f2pack(0.6932610273361206f, 0.6932610273361206f));
-  p = ffma2(p, f, f2pack(0.9999280571937561f, 0.9999280571937561f));
-  const uint32_t rlo = (uint32_t)p + ((uint32_t)j << 23);
-  const uint32_t rhi = (uint32_t)(p >> 32) + ((uint32_t)(j >> 32) << 23);
-  return (uint64_t)rlo | ((uint64_t)rhi << 32);
 }
 
 // softmax_tile with packed fp32x2 arithmetic and EMU of every 8 column pairs exponentiated by
@@ -1008,6 +954,18 @@ int softmax_emu() {
   return v;
 }
 
+// EVA_PREFILL_DUAL=1: d = 128 causal calls run the 128-key two-query-tile kernel
+// (prefill_dual.cu) -- opt-in: measured 0.877 ms at configs[2] against this kernel's 0.579 (the
+// two softmax warpgroups are MUFU- and latency-bound and each query tile's S -> softmax -> PV
+// chain is serial).
+bool prefill_dual_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("EVA_PREFILL_DUAL");
+    return e ? atoi(e) != 0 : false;
+  }();
+  return v;
+}
+
 // Tile order when not overlapping the summarize kernel: summary tiles first (measured 613 vs
 // 629 us at configs[2]); EVA_PREFILL_SUMFIRST=0 selects local-first for measurements.
 int tile_sum_first() {
@@ -1167,6 +1125,8 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, 
                                  void* O, float* lse, uint32_t variant, cudaStream_t s) {
   if (cfg.bh_count == 0) return cudaSuccess;
   const bool overlap = (variant & 0x100u) != 0;  // EVA_PREFILL_OVERLAP
+  if (!overlap && prefill_dual_enabled() && prefill_dual_supported(cfg))
+    return launch_prefill_dual(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   if (cfg.d_head == 128) return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
   if (cfg.d_head == 64) return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
   return cudaErrorNotSupported;
