@@ -238,6 +238,24 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
  * eva_attn_prefill into a CUDA graph; synchronises `stream` if an existing buffer is replaced. */
 eva_status eva_prefill_reserve(const eva_config* cfg, eva_stream_t stream);
 
+/* eva_attn_prefill_rope: eva_attn_prefill on RoPE(Q), RoPE(K) with the rotation done INSIDE the
+ * tensor-core kernel ("RoPE is applied to all tokens prior to
+ * the random feature projections"; readings R18/R19): Q and K [bh_count, T, d] are the caller's
+ * un-rotated rows; the kernel rotates the landed Q tile and each local K tile in shared memory
+ * (row at position n by n * base^(-2j/rd), rp as in eva_rope_ex), so RoPE(Q) and RoPE(K) are
+ * never written.  The summary keys are chunk means of the ROTATED keys:
+ *   flags 0                      -- computed first by eva_rope_summarize_ex's summariser in its
+ *                                   summaries-only form (Ksum/Vsum written, out);
+ *   EVA_SUMMARIES_PROVIDED       -- Ksum/Vsum already hold them (in), e.g. from
+ *                                   eva_rope_summarize_ex or a decode cache.
+ * O (out) and lse (out, may be NULL) as in eva_attn_prefill.  The result equals eva_attn_prefill
+ * on eva_rope_ex's outputs up to the rounding of the rotated bf16 values.  Whole-sequence call,
+ * every cfg.mode; bf16, d in {64, 128} and rotary_dim (0 = d) a power of two (>= 8 interleaved,
+ * >= 16 half-split), else EVA_ERR_UNSUPPORTED; other flags -> EVA_ERR_INVALID_ARG. */
+eva_status eva_attn_prefill_rope(const eva_config* cfg, const eva_rope_params* rp, const void* Q, const void* K,
+                                 const void* V, const float* eps, void* Ksum, void* Vsum, void* O, float* lse,
+                                 uint32_t flags, eva_stream_t stream);
+
 /* ---------------------------------------------------------------- query-range prefill
  * The building blocks of a sequence-sharded (context-parallel) prefill (SURVEY §8(f) NEXT
  * row 2; the paper positions EVA against ring attention): a rank that owns positions
@@ -367,6 +385,21 @@ size_t eva_decode_ragged_workspace_bytes(const eva_cache* cache);
 eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const void* Q, const void* K_new,
                                   const void* V_new, const float* eps, void* O, float* lse, void* workspace,
                                   size_t workspace_bytes, eva_stream_t stream);
+
+/* eva_decode_step_ragged_rope: eva_decode_step_ragged with RoPE folded into the same launch
+ * (readings R18/R19): Q and K_new are the caller's UN-rotated
+ * rows; the kernel rotates q and k_new of unit u at its position pos[u] in registers, appends
+ * RoPE(k_new) (in dtype) to the ring -- so the cache holds rotated keys, as the prefill hand-off
+ * of eva_rope_summarize_ex / eva_attn_prefill_rope leaves it -- summarises a completed chunk
+ * from the rotated keys, and attends with RoPE(q).  Equals eva_rope_ex(q), eva_rope_ex(k_new)
+ * at pos followed by eva_decode_step_ragged, up to the rounding of RoPE(q) to dtype (kept in
+ * fp32 here).  rp as in eva_rope_ex; the half-split style additionally needs
+ * rotary_dim / (2 * 16 / sizeof(dtype)) to be a power of two, else EVA_ERR_UNSUPPORTED.
+ * rp == NULL: exactly eva_decode_step_ragged.  Always one launch. */
+eva_status eva_decode_step_ragged_rope(const eva_cache* cache, int64_t* pos, const eva_rope_params* rp,
+                                       const void* Q, const void* K_new, const void* V_new, const float* eps,
+                                       void* O, float* lse, void* workspace, size_t workspace_bytes,
+                                       eva_stream_t stream);
 
 /* ---------------------------------------------------------------- host-buffer prefill
  * eva_attn_prefill_host: eva_attn_prefill on inputs and outputs in HOST memory, with the

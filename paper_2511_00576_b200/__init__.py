@@ -8,6 +8,7 @@ from .api import (DecodeCache, EvaConfig, EvaError, HostPrefill, eva_attn_prefil
                   eva_attn_prefill_range, eva_summarize_range, eva_summarize_range_bcast, eva_attn_backward, eva_attn_decode,  # noqa: F401
                   eva_attn_prefill, eva_prefill_reserve, eva_backward_workspace_bytes,
                   eva_cache_append, eva_cache_load, eva_draw_eps, eva_mask_ranges, eva_philox, eva_summarize, eva_summarize_proj, eva_rope_summarize, eva_rope,
+                  eva_attn_prefill_rope,
                   launch_count, make_config, version)
 
 __version__ = "0.1.0"

@@ -59,7 +59,8 @@ EXPORTS = ["eva_config_default", "eva_summarize", "eva_attn_prefill", "eva_cache
            "eva_summarize_range", "eva_attn_prefill_range", "eva_summarize_range_bcast",
            "eva_summarize_proj", "eva_decode_ragged_workspace_bytes", "eva_decode_step_ragged",
            "eva_rope_summarize", "eva_rope", "eva_prefill_reserve", "eva_rope_ex",
-           "eva_rope_summarize_ex", "eva_backward_proj_workspace_bytes", "eva_attn_backward_proj"]
+           "eva_rope_summarize_ex", "eva_backward_proj_workspace_bytes", "eva_attn_backward_proj",
+           "eva_attn_prefill_rope", "eva_decode_step_ragged_rope"]
 
 
 class EvaError(RuntimeError):
@@ -85,8 +86,12 @@ def _load():
         "eva_rope": (st, [CFG, ctypes.c_float, P, P, ctypes.c_int64, ctypes.c_int32, P]),
         "eva_rope_ex": (st, [CFG, ctypes.POINTER(EvaRopeParams), P, P, ctypes.c_int64, P, ctypes.c_int32, P]),
         "eva_rope_summarize_ex": (st, [CFG, ctypes.POINTER(EvaRopeParams), P, P, P, P, P, P, P, P, P]),
+        "eva_attn_prefill_rope": (st, [CFG, ctypes.POINTER(EvaRopeParams), P, P, P, P, P, P, P, P,
+                                       ctypes.c_uint32, P]),
         "eva_decode_ragged_workspace_bytes": (ctypes.c_size_t, [CACHE]),
         "eva_decode_step_ragged": (st, [CACHE, P, P, P, P, P, P, P, P, ctypes.c_size_t, P]),
+        "eva_decode_step_ragged_rope": (st, [CACHE, P, ctypes.POINTER(EvaRopeParams), P, P, P, P, P, P, P,
+                                             ctypes.c_size_t, P]),
         "eva_attn_prefill": (st, [CFG, P, P, P, P, P, P, P, P, ctypes.c_uint32, P]),
         "eva_prefill_reserve": (st, [CFG, P]),
         "eva_cache_append": (st, [CACHE, P, P, ctypes.c_int32, P, P]),

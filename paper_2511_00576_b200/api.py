@@ -126,6 +126,35 @@ def eva_rope_summarize(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torc
     return Qr, Kr, Ksum, Vsum
 
 
+def eva_attn_prefill_rope(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: torch.Tensor,
+                          rope_base: float = 10000.0, rotary_dim: Optional[int] = None,
+                          style: str = "interleaved", eps: Optional[torch.Tensor] = None,
+                          Ksum: Optional[torch.Tensor] = None, Vsum: Optional[torch.Tensor] = None,
+                          summaries_provided: bool = False, O: Optional[torch.Tensor] = None,
+                          lse: Optional[torch.Tensor] = None):
+    """Prefill on RoPE(Q), RoPE(K) with the rotation inside the tensor-core kernel (NEXT row 4,
+    R18/R19): Q, K un-rotated.  Returns (O, lse, Ksum, Vsum); the summaries are those of the
+    rotated keys (computed first unless summaries_provided)."""
+    dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
+    nC = T // cfg.chunk
+    for t, nm in ((Q, "Q"), (K, "K"), (V, "V")):
+        _need(t, nm, (bh, T, d), dt)
+    if eps is not None:
+        _need(eps, "eps", (bh, nC, d), torch.float32)
+    if summaries_provided:
+        _need(Ksum, "Ksum", (bh, nC, d), dt)
+        _need(Vsum, "Vsum", (bh, nC, d), dt)
+    Ksum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=K.device)[:, :nC] if Ksum is None else Ksum
+    Vsum = torch.empty(bh, max(nC, 1), d, dtype=dt, device=K.device)[:, :nC] if Vsum is None else Vsum
+    O = torch.empty_like(Q) if O is None else O
+    lse = torch.empty(bh, T, dtype=torch.float32, device=Q.device) if lse is None else lse
+    rp = _rope_params(rope_base, rotary_dim, style)
+    check(lib.eva_attn_prefill_rope(ctypes.byref(cfg), ctypes.byref(rp), _ptr(Q), _ptr(K), _ptr(V), _ptr(eps),
+                                    _ptr(Ksum if nC else None), _ptr(Vsum if nC else None), _ptr(O), _ptr(lse),
+                                    N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0, _stream(Q.device)))
+    return O, lse, Ksum, Vsum
+
+
 def eva_rope(cfg: EvaConfig, X: torch.Tensor, rope_base: float = 10000.0, pos0: int = 0,
              inverse: bool = False, out: Optional[torch.Tensor] = None, rotary_dim: Optional[int] = None,
              style: str = "interleaved", pos: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -498,9 +527,11 @@ class DecodeCache:
     def eva_decode_step_ragged(self, pos: torch.Tensor, q: torch.Tensor, k: torch.Tensor,
                                v: torch.Tensor, eps: Optional[torch.Tensor] = None,
                                O: Optional[torch.Tensor] = None, lse: Optional[torch.Tensor] = None,
-                               want_lse: bool = True):
+                               want_lse: bool = True, rope: Optional[dict] = None):
         """Per-unit positions: pos int64 CUDA [bh] (advanced in place); append (k, v) at pos[u]
-        and attend q at that position, q, k, v [bh, d].  self.pos is not used."""
+        and attend q at that position, q, k, v [bh, d].  self.pos is not used.  rope: None, or
+        dict(rope_base=..., rotary_dim=..., style=...) -- q and k are un-rotated and the kernel
+        applies RoPE at pos[u] in the same launch (eva_decode_step_ragged_rope)."""
         cfg = self.c.cfg
         dt, bh, d = _tdtype(cfg), cfg.bh_count, cfg.d_head
         _need(pos, "pos", (bh,), torch.int64)
@@ -517,6 +548,13 @@ class DecodeCache:
         if nbytes and (getattr(self, "_ws_ragged", None) is None or self._ws_ragged.numel() * 4 < nbytes):
             self._ws_ragged = torch.zeros((nbytes + 3) // 4, dtype=torch.float32, device=q.device)
         ws = self._ws_ragged if nbytes else None
+        if rope is not None:
+            rp = _rope_params(rope.get("rope_base", 10000.0), rope.get("rotary_dim"),
+                              rope.get("style", "interleaved"))
+            check(lib.eva_decode_step_ragged_rope(ctypes.byref(self.c), _ptr(pos), ctypes.byref(rp), _ptr(q), _ptr(k),
+                                                  _ptr(v), _ptr(eps), _ptr(O), _ptr(lse if want_lse else None),
+                                                  _ptr(ws), 0 if ws is None else ws.numel() * 4, _stream(q.device)))
+            return O, (lse if want_lse else None)
         check(lib.eva_decode_step_ragged(ctypes.byref(self.c), _ptr(pos), _ptr(q), _ptr(k), _ptr(v), _ptr(eps),
                                          _ptr(O), _ptr(lse if want_lse else None), _ptr(ws),
                                          0 if ws is None else ws.numel() * 4, _stream(q.device)))

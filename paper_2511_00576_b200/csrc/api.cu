@@ -297,6 +297,47 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
   return cuda_status(e, tc ? "eva_attn_prefill(sm100)" : "eva_attn_prefill(simt)");
 }
 
+eva_status eva_attn_prefill_rope(const eva_config* cfg, const eva_rope_params* rp, const void* Q, const void* K,
+                                 const void* V, const float* eps, void* Ksum, void* Vsum, void* O, float* lse,
+                                 uint32_t flags, eva_stream_t stream) {
+  eva_status st = check_cfg(cfg, true);
+  if (st != EVA_OK) return st;
+  if ((st = check_rope(cfg, rp, true)) != EVA_OK) return st;
+  if (flags & ~EVA_SUMMARIES_PROVIDED) return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  if (cfg->mode == EVA_NONCAUSAL && cfg->T % cfg->chunk != 0)
+    return fail(EVA_ERR_INVALID_ARG, "non-causal prefill needs T %% C == 0 (T=%d, C=%d; reading R15)", cfg->T,
+                cfg->chunk);
+  if (!eva::prefill_rope_supported(*cfg, rp->rotary_dim, rp->style))
+    return fail(EVA_ERR_UNSUPPORTED,
+                "eva_attn_prefill_rope: needs bf16, d in {64,128} and a power-of-two rotary_dim (>= 8 "
+                "interleaved, >= 16 half-split); got dtype=%d d=%d rotary_dim=%d style=%d",
+                (int)cfg->dtype, cfg->d_head, rp->rotary_dim, rp->style);
+  if (cfg->bh_count == 0) return ok();
+  const void* p[] = {Q, K, V, O};
+  const char* nm[] = {"Q", "K", "V", "O"};
+  if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+  const bool have_sums = cfg->T / cfg->chunk > 0;
+  if (have_sums) {
+    const void* p2[] = {Ksum, Vsum};
+    const char* nm2[] = {"Ksum", "Vsum"};
+    if ((st = check_ptrs(2, p2, nm2)) != EVA_OK) return st;
+  }
+  if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
+  if (lse && !aligned16(lse)) return fail(EVA_ERR_INVALID_ARG, "lse is not 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (have_sums && !(flags & EVA_SUMMARIES_PROVIDED)) {
+    // the summaries of the rotated keys, without writing RoPE(Q) / RoPE(K)
+    const cudaError_t e = eva::launch_rope_summarize(*cfg, *rp, Q, K, V, eps, nullptr, nullptr, Ksum, Vsum, s);
+    if (e == cudaErrorNotSupported)
+      return fail(EVA_ERR_UNSUPPORTED, "eva_attn_prefill_rope: chunk=%d too long for the register summariser",
+                  cfg->chunk);
+    if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill_rope(summaries)");
+  }
+  return cuda_status(eva::launch_prefill_sm100_rope(*cfg, std::log2((double)rp->base), rp->rotary_dim, rp->style,
+                                                    Q, K, V, Ksum, Vsum, O, lse, s),
+                     "eva_attn_prefill_rope");
+}
+
 eva_status eva_prefill_reserve(const eva_config* cfg, eva_stream_t stream) {
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
@@ -557,9 +598,18 @@ size_t eva_decode_ragged_workspace_bytes(const eva_cache* cache) {
 eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const void* Q, const void* K_new,
                                   const void* V_new, const float* eps, void* O, float* lse, void* workspace,
                                   size_t workspace_bytes, eva_stream_t stream) {
+  return eva_decode_step_ragged_rope(cache, pos, nullptr, Q, K_new, V_new, eps, O, lse, workspace, workspace_bytes,
+                                     stream);
+}
+
+eva_status eva_decode_step_ragged_rope(const eva_cache* cache, int64_t* pos, const eva_rope_params* rp,
+                                       const void* Q, const void* K_new, const void* V_new, const float* eps,
+                                       void* O, float* lse, void* workspace, size_t workspace_bytes,
+                                       eva_stream_t stream) {
   if (!cache) return fail(EVA_ERR_INVALID_ARG, "cache is NULL");
   eva_status st = check_cfg(&cache->cfg, false);
   if (st != EVA_OK) return st;
+  if (rp && (st = check_rope(&cache->cfg, rp, true)) != EVA_OK) return st;
   if ((st = check_causal(&cache->cfg, "the decode cache")) != EVA_OK) return st;
   if (cache->cap_chunks < 0) return fail(EVA_ERR_INVALID_ARG, "cap_chunks=%d", cache->cap_chunks);
   // one launch (the decode kernel appends and summarises with its first warp); the
@@ -569,7 +619,8 @@ eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const vo
     const char* e = getenv("EVA_RAGGED_TWO_LAUNCH");
     return e && atoi(e) != 0;
   }();
-  if (two_launch && !eva::ragged_supported(cache->cfg))
+  // (RoPE is folded into the one-launch form only: with rp the step is always one launch)
+  if (two_launch && !rp && !eva::ragged_supported(cache->cfg))
     return fail(EVA_ERR_UNSUPPORTED, "eva_decode_step_ragged: chunk=%d too long for the register summariser",
                 cache->cfg.chunk);
   if (cache->cfg.bh_count == 0) return ok();
@@ -591,11 +642,12 @@ eva_status eva_decode_step_ragged(const eva_cache* cache, int64_t* pos, const vo
     return fail(EVA_ERR_INVALID_ARG, "workspace of %zu bytes needed (got %zu)", need, workspace_bytes);
   if (workspace && !aligned16(workspace)) return fail(EVA_ERR_INVALID_ARG, "workspace is not 16-byte aligned");
   const cudaError_t e =
-      two_launch ? eva::launch_decode_step_ragged(*cache, pos, Q, K_new, V_new, eps, O, lse, (float*)workspace, S,
-                                                  (cudaStream_t)stream)
-                 : eva::launch_decode_step_ragged_fused(*cache, pos, Q, K_new, V_new, eps, O, lse,
-                                                        (float*)workspace, S, (cudaStream_t)stream);
-  return cuda_status(e, "eva_decode_step_ragged");
+      (two_launch && !rp)
+          ? eva::launch_decode_step_ragged(*cache, pos, Q, K_new, V_new, eps, O, lse, (float*)workspace, S,
+                                           (cudaStream_t)stream)
+          : eva::launch_decode_step_ragged_fused(*cache, pos, Q, K_new, V_new, eps, O, lse, (float*)workspace, S,
+                                                 (cudaStream_t)stream, rp);
+  return cuda_status(e, rp ? "eva_decode_step_ragged_rope" : "eva_decode_step_ragged");
 }
 
 }  // extern "C"

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -89,15 +90,26 @@ __global__ void __launch_bounds__(128) summarize_reg_kernel(eva_config cfg, cons
 // gradient through RoPE).  The angle is reduced mod 2 pi in double so fp32 keeps its accuracy
 // at long positions.  rd is a multiple of 2 * (16 / sizeof(T)), so a 16-byte piece is either
 // inside [0, rd) or outside it, and a half-split piece's partner is a whole piece rd/2 later.
+// theta_j = base^(-2j/rd) comes from a double table the host fills (the kernels take the spec as
+// a __grid_constant__ parameter, so th[j] is a constant-bank load, not a per-element exp2).
 struct RopeSpec {
-  double log2_base;  // double: at positions ~2^31 a float log2(base) alone shifts the angle by radians
+  double th[64];     // double: at positions ~2^31 a float theta alone shifts the angle by radians
   int rd;
   int style;
   float sign;
+  int pad;
 };
+inline RopeSpec make_rope_spec(double base, int rd, int style, float sign) {
+  RopeSpec rs{};
+  rs.rd = rd;
+  rs.style = style;
+  rs.sign = sign;
+  for (int j = 0; j < rd / 2 && j < 64; ++j) rs.th[j] = std::exp2(std::log2(base) * (-2.0 * (double)j / (double)rd));
+  return rs;
+}
 
 __device__ __forceinline__ void rope_cs(int64_t pos, int j, const RopeSpec& rs, float& c, float& s) {
-  const double theta = exp2(rs.log2_base * (-2.0 * (double)j / (double)rs.rd));
+  const double theta = rs.th[j];
   double a = (double)pos * theta;
   a -= 6.283185307179586 * rint(a * 0.15915494309189535);
   sincosf((float)a, &s, &c);
@@ -181,7 +193,7 @@ __device__ __forceinline__ void rope_row_item(const T* src, T* dst, int64_t pos,
 template <typename T, int D>
 __global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ X, T* __restrict__ Y, int64_t rows,
                                                    int T_, int64_t pos0, const int64_t* __restrict__ pos,
-                                                   RopeSpec rs) {
+                                                   const __grid_constant__ RopeSpec rs) {
   pdl_wait();
   pdl_trigger();
   const int per = rope_items<T, D>(rs);
@@ -198,7 +210,7 @@ __global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ X, T* _
 // (off = rd / (2 VEC), a power of two), exchanged by shuffles -- every lane takes part.
 template <typename T, int D>
 struct RopeKX {
-  RopeSpec rs;
+  const RopeSpec& rs;  // the kernel's __grid_constant__ parameter
   int64_t r0;
   T* Krc;
   __device__ __forceinline__ void operator()(int r, int ch0, uint4& x, bool valid) const {
@@ -218,7 +230,7 @@ struct RopeKX {
     } else if (ch0 < rs.rd) {
       x = rope_piece_il<T>(x, r0 + r, ch0, rs);
     }
-    if (valid) *reinterpret_cast<uint4*>(Krc + (size_t)r * D + ch0) = x;
+    if (valid && Krc) *reinterpret_cast<uint4*>(Krc + (size_t)r * D + ch0) = x;
   }
 };
 
@@ -226,7 +238,7 @@ struct RopeKX {
 // they are loaded (and stored to Kr), summarised from the rotated values, and its query rows
 // rotated into Qr; CTA x = nC rotates the trailing partial chunk's rows only.
 template <typename T, int D, int NI>
-__global__ void __launch_bounds__(128) rope_summarize_kernel(eva_config cfg, RopeSpec rs,
+__global__ void __launch_bounds__(128) rope_summarize_kernel(eva_config cfg, const __grid_constant__ RopeSpec rs,
                                                             const T* __restrict__ Q, const T* __restrict__ K,
                                                             const T* __restrict__ V, const float* __restrict__ eps,
                                                             T* __restrict__ Qr, T* __restrict__ Kr,
@@ -238,16 +250,19 @@ __global__ void __launch_bounds__(128) rope_summarize_kernel(eva_config cfg, Rop
   const size_t ub = (size_t)u * Tn;
   const int r0 = c * C, r1 = min(Tn, r0 + C);
   const int per = rope_items<T, D>(rs);
-  // the query rows of this chunk (and, for the tail CTA, the key rows too)
-  for (int i = threadIdx.x; i < (r1 - r0) * per; i += blockDim.x) {
-    const int r = r0 + i / per, it = i % per;
-    rope_row_item<T, D>(Q + (ub + r) * D, Qr + (ub + r) * D, r, it, rs);
-    if (c >= nC) rope_row_item<T, D>(K + (ub + r) * D, Kr + (ub + r) * D, r, it, rs);
+  // the query rows of this chunk (and, for the tail CTA, the key rows too).  Qr == Kr == NULL:
+  // summaries only (eva_attn_prefill_rope rotates Q and K inside the prefill kernel).
+  if (Qr) {
+    for (int i = threadIdx.x; i < (r1 - r0) * per; i += blockDim.x) {
+      const int r = r0 + i / per, it = i % per;
+      rope_row_item<T, D>(Q + (ub + r) * D, Qr + (ub + r) * D, r, it, rs);
+      if (c >= nC) rope_row_item<T, D>(K + (ub + r) * D, Kr + (ub + r) * D, r, it, rs);
+    }
   }
   if (c >= nC) return;
   const T* Kc = K + (ub + (size_t)r0) * D;
   const T* Vc = V + (ub + (size_t)r0) * D;
-  RopeKX<T, D> kx{rs, (int64_t)r0, Kr + (ub + (size_t)r0) * D};
+  RopeKX<T, D> kx{rs, (int64_t)r0, Kr ? Kr + (ub + (size_t)r0) * D : nullptr};
   summarize_chunk_reg<T, D, NI>([&](int r) { return Kc + (size_t)r * D; }, [&](int r) { return Vc + (size_t)r * D; },
                                 C, eps ? eps + ((size_t)u * nC + c) * D : nullptr, (uint32_t)(cfg.bh_begin + u),
                                 (uint32_t)c, cfg, Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D,
@@ -503,14 +518,62 @@ __global__ void __launch_bounds__(128) ragged_append_kernel(eva_cache c, int64_t
 // and Knew/Vnew hold it; entry n = p is read from Knew/Vnew instead of the ring, and the
 // split-0 CTA of each unit writes it to ring slot p mod W (which held position p - W,
 // invisible to query p).  Used for steps that do not complete a chunk.
-template <typename T, int D, bool FUSED = false, bool RAGGED = false>
+// RoPE of the VEC channels [ch0, ch0 + VEC) a lane holds (as floats) at position pos (R18/R19):
+// interleaved pairs are inside the lane; a half-split partner is rd/2 channels away, i.e. in lane
+// gl ^ (rd / (2 VEC)) of the same row group (a power of two, checked by the C ABI) -- exchanged by
+// shuffles, every lane of the warp taking part.
+template <int VEC>
+__device__ __forceinline__ void rope_vals(float (&v)[VEC], int64_t pos, int ch0, const RopeSpec& rs) {
+  if (rs.style == EVA_ROPE_NEOX) {
+    const int off = rs.rd / (2 * VEC);
+    float y[VEC];
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) y[j] = __shfl_xor_sync(0xffffffffu, v[j], off);
+    if (ch0 < rs.rd) {
+      const bool first = ch0 < rs.rd / 2;
+      const int j0 = first ? ch0 : ch0 - rs.rd / 2;
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) {
+        float c, sn;
+        rope_cs(pos, j0 + j, rs, c, sn);
+        v[j] = first ? v[j] * c - y[j] * sn : y[j] * sn + v[j] * c;
+      }
+    }
+  } else if (ch0 < rs.rd) {
+#pragma unroll
+    for (int j = 0; j < VEC; j += 2) {
+      float c, sn;
+      rope_cs(pos, (ch0 + j) / 2, rs, c, sn);
+      const float x0 = v[j], x1 = v[j + 1];
+      v[j] = x0 * c - x1 * sn;
+      v[j + 1] = x0 * sn + x1 * c;
+    }
+  }
+}
+
+// The summariser's loads in the RoPE ragged step: the newest key row (K_new, un-rotated in
+// memory) is served from the lane's rotated piece, every other row from global memory.
+template <typename T, int D>
+struct LdRopeNew {
+  const T* kn;  // K_new row of this unit
+  uint4 piece;  // this lane's rotated piece of it (channels ch0 .. ch0 + VEC)
+  template <typename P>
+  __device__ __forceinline__ uint4 operator()(const P* p) const {
+    const T* q = reinterpret_cast<const T*>(p);
+    return (q >= kn && q < kn + D) ? piece : ldg16_stream(p);
+  }
+};
+
+template <typename T, int D, bool FUSED = false, bool RAGGED = false, bool ROPE = false>
 __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __restrict__ Q,
                                                      T* __restrict__ O, float* __restrict__ lse,
                                                      float* __restrict__ ws, int S_,
-                                                     const T* __restrict__ Knew = nullptr,
-                                                     const T* __restrict__ Vnew = nullptr,
-                                                     int64_t* __restrict__ pos_dev = nullptr,
-                                                     const float* __restrict__ ragged_eps = nullptr) {
+                                                     const T* __restrict__ Knew,
+                                                     const T* __restrict__ Vnew,
+                                                     int64_t* __restrict__ pos_dev,
+                                                     const float* __restrict__ ragged_eps,
+                                                     const __grid_constant__ RopeSpec rs) {
+  static_assert(!ROPE || (FUSED && RAGGED), "RoPE is folded into the one-launch ragged step");
   constexpr int VEC = 16 / sizeof(T);
   constexpr int TPR = D / VEC;          // lanes per row
   constexpr int RPW = 32 / TPR;         // rows per warp-wide load
@@ -547,6 +610,16 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
   const T* rv = static_cast<const T*>(c.ring_v) + (size_t)u * W * D + ch0;
   float q[VEC], acc[VEC];
   load_vec<T, VEC>(Q + (size_t)u * D + ch0, q);
+  uint4 kn_rot = make_uint4(0u, 0u, 0u, 0u);
+  if constexpr (ROPE) {
+    // q and the new key at this unit's position n, in registers (RoPE(q), RoPE(k_new) are
+    // never written; the rotated key goes to its ring slot in dtype, like the two-pass path)
+    rope_vals<VEC>(q, n, ch0, rs);
+    float kv[VEC];
+    load_vec<T, VEC>(Knew + (size_t)u * D + ch0, kv);
+    rope_vals<VEC>(kv, n, ch0, rs);
+    kn_rot = pack16<T>(kv);
+  }
 #pragma unroll
   for (int j = 0; j < VEC; ++j) {
     q[j] *= c.cfg.scale;
@@ -560,6 +633,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
     for (int i = 0; i < UNROLL; ++i) {
       const int e = eb + i * RPW + grp;
       ok[i] = e < e1;
+      const bool is_new = FUSED && e == E - 1;
       const T *kp, *vp;
       if (e < ns) {
         kp = sk + (size_t)e * D;
@@ -574,7 +648,7 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
         vp = rv + (size_t)slot * D;
       }
       if (ok[i]) {
-        kx[i] = ldg16_stream(kp);
+        kx[i] = (ROPE && is_new) ? kn_rot : ldg16_stream(kp);
         vx[i] = ldg16_stream(vp);
       }
     }
@@ -636,9 +710,14 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
       const size_t slot = (size_t)(n % W);
       T* wk = static_cast<T*>(c.ring_k) + ((size_t)u * W + slot) * D;
       T* wv = static_cast<T*>(c.ring_v) + ((size_t)u * W + slot) * D;
-      for (int i = lane; i < D; i += 32) {
-        wk[i] = Knew[(size_t)u * D + i];
-        wv[i] = Vnew[(size_t)u * D + i];
+      if constexpr (ROPE) {
+        if (grp == 0) *reinterpret_cast<uint4*>(wk + ch0) = kn_rot;
+        for (int i = lane; i < D; i += 32) wv[i] = Vnew[(size_t)u * D + i];
+      } else {
+        for (int i = lane; i < D; i += 32) {
+          wk[i] = Knew[(size_t)u * D + i];
+          wv[i] = Vnew[(size_t)u * D + i];
+        }
       }
     }
   }
@@ -663,11 +742,21 @@ __global__ void __launch_bounds__(128, 6) decode_kernel(eva_cache c, const T* __
         const int64_t q = p0 + i;
         return q == n ? Vnew + (size_t)u * D : rv0 + (size_t)(q % W) * D;
       };
-      summarize_chunk_reg<T, D, 16, decltype(rowK), decltype(rowV), NoKXform, LdGlobalStream, true>(
-          rowK, rowV, C, ragged_eps ? ragged_eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr,
-          (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk, c.cfg,
-          static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D,
-          static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D);
+      if constexpr (ROPE) {
+        // the ring rows are rotated already; the newest row's rotated piece comes from kn_rot
+        summarize_chunk_reg<T, D, 16, decltype(rowK), decltype(rowV), NoKXform, LdRopeNew<T, D>, true>(
+            rowK, rowV, C, ragged_eps ? ragged_eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr,
+            (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk, c.cfg,
+            static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D,
+            static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D, nullptr, NoKXform(),
+            LdRopeNew<T, D>{Knew + (size_t)u * D, kn_rot});
+      } else {
+        summarize_chunk_reg<T, D, 16, decltype(rowK), decltype(rowV), NoKXform, LdGlobalStream, true>(
+            rowK, rowV, C, ragged_eps ? ragged_eps + ((size_t)u * c.cap_chunks + chunk) * D : nullptr,
+            (uint32_t)(c.cfg.bh_begin + u), (uint32_t)chunk, c.cfg,
+            static_cast<T*>(c.sum_k) + ((size_t)u * c.cap_chunks + chunk) * D,
+            static_cast<T*>(c.sum_v) + ((size_t)u * c.cap_chunks + chunk) * D);
+      }
     }
   }
   if (warp != 0) return;
@@ -898,7 +987,7 @@ cudaError_t launch_rope_summarize(const eva_config& cfg, const eva_rope_params& 
   const int nC = cfg.T / cfg.chunk;
   const int n_cta = nC + (cfg.T % cfg.chunk ? 1 : 0);
   if (n_cta == 0 || cfg.bh_count == 0) return cudaSuccess;
-  const RopeSpec rs{log2((double)rp.base), rp.rotary_dim ? rp.rotary_dim : cfg.d_head, rp.style, 1.f};
+  const RopeSpec rs = make_rope_spec((double)rp.base, rp.rotary_dim ? rp.rotary_dim : cfg.d_head, rp.style, 1.f);
   cudaError_t err = cudaSuccess;
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
     const int ni = summ_reg_ni<T, D>(cfg.chunk);
@@ -919,7 +1008,7 @@ cudaError_t launch_rope(const eva_config& cfg, const eva_rope_params& rp, const 
   const int64_t rows = (int64_t)cfg.bh_count * cfg.T;
   if (rows == 0) return cudaSuccess;
   const int rd = rp.rotary_dim ? rp.rotary_dim : cfg.d_head;
-  const RopeSpec rs{log2((double)rp.base), rd, rp.style, inverse ? -1.f : 1.f};
+  const RopeSpec rs = make_rope_spec((double)rp.base, rd, rp.style, inverse ? -1.f : 1.f);
   cudaError_t err = cudaSuccess;
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
     constexpr int VEC = 16 / (int)sizeof(T);
@@ -1036,7 +1125,7 @@ cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     dim3 grid(c.cfg.bh_count, splits);
     cudaError_t e = launch_pdl(decode_kernel<T, D, false>, grid, dim3(128), 0, s, c, (const T*)Q, (T*)O, lse, ws,
-                               splits, (const T*)nullptr, (const T*)nullptr, (int64_t*)nullptr, (const float*)nullptr);
+                               splits, (const T*)nullptr, (const T*)nullptr, (int64_t*)nullptr, (const float*)nullptr, RopeSpec{});
     if (e != cudaSuccess) return e;
     note_launch();
   }));
@@ -1064,7 +1153,7 @@ cudaError_t launch_decode_step(const eva_cache& c_after, const void* Q, const vo
   EVA_DISPATCH_T(c_after.cfg.dtype, EVA_DISPATCH_D(c_after.cfg.d_head, {
     dim3 grid(c_after.cfg.bh_count, splits);
     cudaError_t e = launch_pdl(decode_kernel<T, D, true>, grid, dim3(128), 0, s, c_after, (const T*)Q, (T*)O, lse,
-                               ws, splits, (const T*)Kn, (const T*)Vn, (int64_t*)nullptr, (const float*)nullptr);
+                               ws, splits, (const T*)Kn, (const T*)Vn, (int64_t*)nullptr, (const float*)nullptr, RopeSpec{});
     if (e != cudaSuccess) return e;
     note_launch();
   }));
@@ -1092,7 +1181,7 @@ cudaError_t launch_decode_step_ragged(const eva_cache& c, int64_t* pos, const vo
     cudaError_t e = launch_pdl(ak, dim3(c.cfg.bh_count), dim3(128), 0, s, c, pos, (const T*)Kn, (const T*)Vn, eps);
     if (e != cudaSuccess) return e;
     e = launch_pdl(decode_kernel<T, D, false, true>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c, (const T*)Q,
-                   (T*)O, lse, ws, splits, (const T*)nullptr, (const T*)nullptr, pos, (const float*)nullptr);
+                   (T*)O, lse, ws, splits, (const T*)nullptr, (const T*)nullptr, pos, (const float*)nullptr, RopeSpec{});
     if (e != cudaSuccess) return e;
     note_launch(2);
   }));
@@ -1101,11 +1190,19 @@ cudaError_t launch_decode_step_ragged(const eva_cache& c, int64_t* pos, const vo
 
 cudaError_t launch_decode_step_ragged_fused(const eva_cache& c, int64_t* pos, const void* Q, const void* Kn,
                                             const void* Vn, const float* eps, void* O, float* lse, float* ws,
-                                            int splits, cudaStream_t s) {
+                                            int splits, cudaStream_t s, const eva_rope_params* rp) {
   if (c.cfg.bh_count == 0) return cudaSuccess;
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
-    cudaError_t e = launch_pdl(decode_kernel<T, D, true, true>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c,
-                               (const T*)Q, (T*)O, lse, ws, splits, (const T*)Kn, (const T*)Vn, pos, eps);
+    cudaError_t e;
+    if (rp) {
+      const RopeSpec rs = make_rope_spec((double)rp->base, rp->rotary_dim ? rp->rotary_dim : c.cfg.d_head,
+                                         rp->style, 1.f);
+      e = launch_pdl(decode_kernel<T, D, true, true, true>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c,
+                     (const T*)Q, (T*)O, lse, ws, splits, (const T*)Kn, (const T*)Vn, pos, eps, rs);
+    } else {
+      e = launch_pdl(decode_kernel<T, D, true, true>, dim3(c.cfg.bh_count, splits), dim3(128), 0, s, c,
+                     (const T*)Q, (T*)O, lse, ws, splits, (const T*)Kn, (const T*)Vn, pos, eps, RopeSpec{});
+    }
     if (e != cudaSuccess) return e;
     note_launch();
   }));

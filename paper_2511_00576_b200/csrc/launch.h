@@ -82,6 +82,13 @@ cudaError_t launch_prefill_sm100_fused(const eva_config& cfg, const void* Q, con
                                        const float* eps, void* Ksum, void* Vsum, void* O, float* lse,
                                        cudaStream_t s);
 cudaError_t prefill_fused_reserve(const eva_config& cfg, cudaStream_t s);
+// RoPE inside the tensor-core prefill (eva_attn_prefill_rope): Q, K un-rotated, Ksum/Vsum the
+// summaries of the rotated keys; whole-sequence call.  cudaErrorNotSupported outside
+// prefill_rope_supported.
+bool prefill_rope_supported(const eva_config& cfg, int rotary_dim, int style);
+cudaError_t launch_prefill_sm100_rope(const eva_config& cfg, double log2_base, int rotary_dim, int style,
+                                      const void* Q, const void* K, const void* V, const void* Ksum,
+                                      const void* Vsum, void* O, float* lse, cudaStream_t s);
 
 cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K, const void* V,
                              const void* Ksum, const void* Vsum, void* O, float* lse,
@@ -115,7 +122,8 @@ cudaError_t launch_decode_step_ragged(const eva_cache& c, int64_t* pos, const vo
 // pos itself.
 cudaError_t launch_decode_step_ragged_fused(const eva_cache& c, int64_t* pos, const void* Q, const void* Kn,
                                             const void* Vn, const float* eps, void* O, float* lse, float* ws,
-                                            int splits, cudaStream_t s);
+                                            int splits, cudaStream_t s,
+                                            const eva_rope_params* rp = nullptr);
 
 cudaError_t launch_mask_ranges(const eva_config& cfg, int64_t n0, int64_t count, int64_t* lo,
                                int64_t* nsum, cudaStream_t s);

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -75,6 +76,7 @@ struct __align__(1024) Smem {
   // slot after its PV MMA, so the next K tiles stream in one softmax period earlier.
   uint64_t k_full[NSK], v_full[NSV], k_empty[NSK], v_empty[NSV];
   uint64_t s_full[2], p_full[2], o_done, o_final;
+  uint64_t q_rot, k_rot[NSK];  // RoPE in-kernel: Q rotated (warps 2-7), K tile rotated (warps 6, 7)
   uint32_t tmem_base;
   SummScratch<D> summ;  // fused summaries' exchange buffers
   int ticket;           // fused: the CTA's query tile ticket and the launch epoch
@@ -94,6 +96,112 @@ struct FusedArgs {
   const float* eps;
   uint32_t* ws;
   int nC, n_qt, units, total, order;
+};
+
+// RoPE applied inside the kernel (eva_attn_prefill_rope; reading R18/R19): Q and K come
+// in un-rotated, the Q tile and every LOCAL K tile are rotated in shared memory after TMA lands
+// them and before the MMA reads them, so RoPE(Q), RoPE(K) are never written to HBM.  The summary
+// tiles are summaries of the rotated keys already (eva_rope_summarize_ex, summaries-only).
+struct RopeArgs {
+  double th[64];  // theta_j = base^(-2j/rd), j < rd/2, in double (computed on the host)
+  int rd;         // rotary channels (a power of two, 16..D)
+  int pad;
+};
+
+// RoPE of a landed tile by nthr threads.  A row's rotated channels form NI items --
+// interleaved (STYLE 1): the 16-byte piece `item` (pairs j = 4 item + i, channels 2j, 2j+1);
+// half-split (STYLE 2): pieces item and item + rd/16 (pairs j = 8 item + i, channels j, j + rd/2).
+// NI divides nthr: thread t takes item t % NI of rows t / NI + k * rstep (rstep = nthr / NI) and
+// walks them with a rotation recurrence -- the first row's angle comes from double precision
+// (pos * theta_j mod 2 pi), each next row multiplies by e^{i rstep theta_j}.  Arithmetic on
+// packed fp32x2 (two pairs per FFMA2); two rows per iteration for load/store overlap.
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t neg2(uint64_t a) { return a ^ 0x8000000080000000ull; }
+__device__ __forceinline__ void rope_angle(double a, float& c, float& s) {
+  a -= 6.283185307179586 * rint(a * 0.15915494309189535);
+  __sincosf((float)a, &s, &c);
+}
+// bf16x2 word -> (low, high) channel as packed fp32x2 pieces of two words
+__device__ __forceinline__ uint64_t lo2(uint32_t w0, uint32_t w1) {
+  return (uint64_t)(w0 << 16) | ((uint64_t)(w1 << 16) << 32);
+}
+__device__ __forceinline__ uint64_t hi2(uint32_t w0, uint32_t w1) {
+  return (uint64_t)(w0 & 0xffff0000u) | ((uint64_t)(w1 & 0xffff0000u) << 32);
+}
+
+template <int STYLE>
+struct RopeTile {
+  static constexpr int NP = STYLE == 2 ? 8 : 4;  // pairs per item
+  static constexpr int NQ = NP / 2;               // packed pair groups
+  template <int D>
+  __device__ __forceinline__ static void run(uint8_t* base, int nrows, int64_t pos0, const RopeArgs& ra, int t,
+                                             int nthr) {
+    const int NI = STYLE == 2 ? ra.rd / 16 : ra.rd / 8;
+    const int item = t % NI, g = t / NI, rstep = nthr / NI;
+    if (g >= rstep) return;
+    uint64_t c[NQ], s[NQ], sc[NQ], ss[NQ], nss[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      float c0, s0, c1, s1, a0, b0, a1, b1;
+      const double t0 = ra.th[NP * item + 2 * q], t1 = ra.th[NP * item + 2 * q + 1];
+      rope_angle((double)(pos0 + g) * t0, c0, s0);
+      rope_angle((double)(pos0 + g) * t1, c1, s1);
+      rope_angle((double)rstep * t0, a0, b0);
+      rope_angle((double)rstep * t1, a1, b1);
+      c[q] = f2pack(c0, c1);
+      s[q] = f2pack(s0, s1);
+      sc[q] = f2pack(a0, a1);
+      ss[q] = f2pack(b0, b1);
+      nss[q] = neg2(ss[q]);
+    }
+    const int ch_a = 8 * item, ch_b = ch_a + ra.rd / 2;
+    const uint32_t off_a = (uint32_t)(ch_a >> 6) * (uint32_t)nrows * 128u, c16_a = (uint32_t)((ch_a & 63) >> 3);
+    const uint32_t off_b = (uint32_t)(ch_b >> 6) * (uint32_t)nrows * 128u, c16_b = (uint32_t)((ch_b & 63) >> 3);
+    auto advance = [&] {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const uint64_t cn = ffma2(s[q], nss[q], fmul2(c[q], sc[q]));
+        s[q] = ffma2(c[q], ss[q], fmul2(s[q], sc[q]));
+        c[q] = cn;
+      }
+    };
+#pragma unroll 2
+    for (int r = g; r < nrows; r += rstep) {
+      uint4* pa = reinterpret_cast<uint4*>(base + off_a + (uint32_t)r * 128u + ((c16_a ^ (uint32_t)(r & 7)) << 4));
+      if constexpr (STYLE == 2) {
+        uint4* pb = reinterpret_cast<uint4*>(base + off_b + (uint32_t)r * 128u + ((c16_b ^ (uint32_t)(r & 7)) << 4));
+        const uint4 xa = *pa, xb = *pb;
+        const uint32_t wa[4] = {xa.x, xa.y, xa.z, xa.w}, wb[4] = {xb.x, xb.y, xb.z, xb.w};
+        uint32_t oa[4], ob[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // pairs 2q, 2q+1: x0 from piece a, x1 from piece b
+          const uint64_t x0 = lo2(wa[q], 0) | ((uint64_t)(wa[q] & 0xffff0000u) << 32);
+          const uint64_t x1 = lo2(wb[q], 0) | ((uint64_t)(wb[q] & 0xffff0000u) << 32);
+          const uint64_t y0 = ffma2(x1, neg2(s[q]), fmul2(x0, c[q]));
+          const uint64_t y1 = ffma2(x1, c[q], fmul2(x0, s[q]));
+          oa[q] = pack_bf16(f2lo(y0), f2hi(y0));
+          ob[q] = pack_bf16(f2lo(y1), f2hi(y1));
+        }
+        *pa = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+        *pb = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+      } else {
+        const uint4 xa = *pa;
+        // pairs (0, 1) in words x, y; pairs (2, 3) in words z, w: even channels in the low halves
+        const uint64_t e01 = lo2(xa.x, xa.y), o01 = hi2(xa.x, xa.y);
+        const uint64_t e23 = lo2(xa.z, xa.w), o23 = hi2(xa.z, xa.w);
+        const uint64_t n01 = neg2(s[0]), n23 = neg2(s[1]);
+        const uint64_t ye01 = ffma2(o01, n01, fmul2(e01, c[0])), yo01 = ffma2(o01, c[0], fmul2(e01, s[0]));
+        const uint64_t ye23 = ffma2(o23, n23, fmul2(e23, c[1])), yo23 = ffma2(o23, c[1], fmul2(e23, s[1]));
+        *pa = make_uint4(pack_bf16(f2lo(ye01), f2lo(yo01)), pack_bf16(f2hi(ye01), f2hi(yo01)),
+                         pack_bf16(f2lo(ye23), f2lo(yo23)), pack_bf16(f2hi(ye23), f2hi(yo23)));
+      }
+      advance();
+    }
+  }
 };
 
 // Columns outside [vlo, vhi) or inside [xlo, xhi) of a 64-column S tile set to -inf.  A 64-bit
@@ -314,10 +422,11 @@ struct RangePlan {
 // warps): 13 owned tile j landed, 14 tile j summarised and released, 15 flag published.
 __device__ unsigned long long* g_trace2 = nullptr;
 __device__ int g_trace_mid = 150;  // slots 2, 3 trace CTAs g_trace_mid, +1 (EVA_TRACE_MID)
-constexpr int TT_ROLES = 4, TT_PER_ROLE = 48;
+constexpr int TT_ROLES = 4, TT_PER_ROLE = 48, TT_SLOTS = 4, TT_MAX_CTAS = 4096;
 struct TileTrace {
   unsigned long long ev[TT_ROLES][TT_PER_ROLE];
   int n[TT_ROLES];
+  int slot;  // tt_slot() read once at entry (it loads g_trace_mid from global memory)
 };
 __device__ __forceinline__ int tt_slot() {
   const int id = blockIdx.y * gridDim.x + blockIdx.x;
@@ -326,7 +435,7 @@ __device__ __forceinline__ int tt_slot() {
 template <bool TRACE>
 __device__ __forceinline__ void tt(TileTrace* tl, int role, int kind, int j) {
   if constexpr (TRACE) {
-    if (tt_slot() >= 0) {
+    if (tl->slot >= 0) {
       const int i = tl->n[role];
       if (i < TT_PER_ROLE) tl->ev[role][i] = ((unsigned long long)clock64() << 24) | ((unsigned)kind << 16) | (unsigned)(j & 0xffff);
       tl->n[role] = i + 1;
@@ -550,15 +659,16 @@ __device__ __forceinline__ bool owns_chunks(const Plan& plan, int j, int C, int 
 // FC = 0: summaries provided (or computed by a separate launch); FC = C in {16, 32, 64}: the
 // chunk summaries are computed in-kernel (one instantiation per chunk size keeps the code that
 // the instruction cache has to hold small)
-template <int D, int NSTAGE, bool TRACE = false, int SMX = -1, int FC = 0>
-__global__ void __launch_bounds__(FC ? NTHREADS_F : NTHREADS, 2)
+template <int D, int NSTAGE, bool TRACE = false, int SMX = -1, int FC = 0, int RP = 0>
+__global__ void __launch_bounds__((FC || RP) ? NTHREADS_F : NTHREADS, 2)
 prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
                      const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
                      const PrefillRange rg, int C, int W, int mode, float scale_log2,
                      float bias_log2, float* __restrict__ lse, int overlap, int overlap_order_sum_first,
-                     const __grid_constant__ FusedArgs fa) {
+                     const __grid_constant__ FusedArgs fa, const __grid_constant__ RopeArgs ra) {
   constexpr bool FUSED = FC != 0;
+  static_assert(!(FC && RP), "in-kernel summaries and in-kernel RoPE are separate variants");
   extern __shared__ uint8_t smem_raw[];
   using SM = Smem<D, NSTAGE>;
   constexpr int NSK = SM::NSK, NSV = SM::NSV;
@@ -574,6 +684,11 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     __shared__ TileTrace tlog_s;
     tl = &tlog_s;
     if (threadIdx.x < TT_ROLES) tl->n[threadIdx.x] = 0;
+    if (threadIdx.x == 0) tl->slot = tt_slot();
+    // per-CTA entry / exit (globaltimer ns, comparable across SMs) after the 4 slot logs
+    const int id = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0 && g_trace2 && id < TT_MAX_CTAS)
+      g_trace2[TT_SLOTS * TT_ROLES * TT_PER_ROLE + 2 * id] = globaltimer_ns();
   }
   if constexpr (FUSED) {
     // Fused: query tiles are handed out by a monotone ticket, so every tile whose summaries a
@@ -606,6 +721,10 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     }
     mbar_init(&sm->o_done, 1);
     mbar_init(&sm->o_final, 1);
+    if constexpr (RP != 0) {
+      mbar_init(&sm->q_rot, NTHREADS_F - 64);
+      for (int s = 0; s < NSK; ++s) mbar_init(&sm->k_rot[s], SUMM_THREADS_F);
+    }
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -645,6 +764,16 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   pdl_trigger();
   if (threadIdx.x == 0) tt<TRACE>(tl, 0, 1, 0);
 
+  if constexpr (RP != 0) {
+    // in-kernel RoPE of the Q tile by the softmax and rope warps (idle until S(0) anyway)
+    if (warp >= 2) {
+      mbar_wait(&sm->q_full, 0);
+      RopeTile<RP>::template run<D>(reinterpret_cast<uint8_t*>(sm->q), BM, plan.n0, ra, (int)threadIdx.x - 64,
+                                    NTHREADS_F - 64);
+      fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
+      mbar_arrive(&sm->q_rot);
+    }
+  }
   // Producer and MMA roles run on whole warps (warp-uniform control flow keeps every
   // descriptor and coordinate in uniform registers); one elected lane issues.
   if (warp == 0) {
@@ -757,17 +886,18 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     constexpr uint32_t idesc_s = idesc_bf16_f32(BM, BN, false);
     constexpr uint32_t idesc_o = idesc_bf16_f32(BM, D, true);
     const uint32_t q_addr = smem_u32(sm->q);
-    mbar_wait(&sm->q_full, 0);
+    mbar_wait(RP ? &sm->q_rot : &sm->q_full, 0);
     if (lane == 0) tt<TRACE>(tl, 1, 2, 0);
     for (int j = 0; j <= NT; ++j) {
       if (j < NT) {
         const int s = j % NSK;
-        mbar_wait(&sm->k_full[s], (j / NSK) & 1);
+        mbar_wait(RP ? &sm->k_rot[s] : &sm->k_full[s], (j / NSK) & 1);
         if (lane == 0) tt<TRACE>(tl, 1, 3, j);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sm->k[s]);
         const uint32_t d_tmem = tmem + (uint32_t)(j & 1) * BN;
         if (elect_one()) {
+          tt<TRACE>(tl, 1, 22, j);
 #pragma unroll
           for (int ks = 0; ks < D / 16; ++ks) {
             const uint32_t kb = ks >> 2, off = (ks & 3) * 32;
@@ -775,6 +905,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
             const uint64_t b = smem_desc_sw128(k_addr + kb * (BN * 128) + off, 16, 1024);
             mma_ss(d_tmem, a, b, idesc_s, ks > 0 ? 1u : 0u);
           }
+          tt<TRACE>(tl, 1, 23, j);
           mma_commit(&sm->s_full[j & 1]);
           mma_commit(&sm->k_empty[s]);
         }
@@ -879,17 +1010,34 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   } else {
     // ------------------------------------------------------------ summary warps (fused)
     if constexpr (FUSED) fused_summaries<D, FC, TRACE>(sm, plan, fa, u, qt, epoch, tl);
+    // ------------------------------------------------------------ rope warps (in-kernel RoPE)
+    if constexpr (RP != 0) {
+      const int t = (int)threadIdx.x - (NTHREADS_F - SUMM_THREADS_F);
+      for (int j = 0; j < NT; ++j) {
+        const int s = j % NSK;
+        mbar_wait(&sm->k_full[s], (j / NSK) & 1);
+        if (!plan.summary(j)) {  // summary tiles hold summaries of rotated keys already
+          RopeTile<RP>::template run<D>(reinterpret_cast<uint8_t*>(sm->k[s]), BN, plan.base(j), ra, t,
+                                        SUMM_THREADS_F);
+          fence_proxy_async_smem();
+        }
+        mbar_arrive(&sm->k_rot[s]);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
   if constexpr (TRACE) {
-    const int slot = tt_slot();
+    const int slot = tl->slot;
     if (slot >= 0 && g_trace2) {
       for (int i = threadIdx.x; i < TT_ROLES * TT_PER_ROLE; i += blockDim.x) {
         const int r = i / TT_PER_ROLE, k = i % TT_PER_ROLE;
         g_trace2[(size_t)slot * TT_ROLES * TT_PER_ROLE + i] = k < tl->n[r] ? tl->ev[r][k] : 0ull;
       }
     }
+    const int id = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0 && g_trace2 && id < TT_MAX_CTAS)
+      g_trace2[TT_SLOTS * TT_ROLES * TT_PER_ROLE + 2 * id + 1] = globaltimer_ns();
   }
   if constexpr (FUSED) {
     // the last CTA to finish resets the ticket and done counters and advances the epoch
@@ -1012,12 +1160,13 @@ cudaError_t fused_workspace(size_t nflags, cudaStream_t s, uint32_t** out) {
   return cudaSuccess;
 }
 
-template <int D, int NSTAGE, bool TRACE = false, int SMX = -1, int FC = 0>
+template <int D, int NSTAGE, bool TRACE = false, int SMX = -1, int FC = 0, int RP = 0>
 cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* Q, const void* K,
                      const void* V, const void* Ksum, const void* Vsum, void* O, float* lse,
-                     cudaStream_t s, bool overlap = false, const float* eps = nullptr) {
+                     cudaStream_t s, bool overlap = false, const float* eps = nullptr,
+                     const RopeArgs* rap = nullptr) {
   constexpr bool FUSED = FC != 0;
-  if constexpr (!TRACE && SMX == -1 && !FUSED) {
+  if constexpr (!TRACE && SMX == -1 && !FUSED && RP == 0) {
     switch (softmax_emu()) {
       case 0: return launch_t<D, NSTAGE, false, 0, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
       case 1: return launch_t<D, NSTAGE, false, 1, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
@@ -1038,8 +1187,8 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
     mVs = mV;
   }
   if (!ok) return cudaErrorInvalidValue;
-  using K_t = decltype(&prefill_sm100_kernel<D, NSTAGE, TRACE, SMX, FC>);
-  K_t kern = prefill_sm100_kernel<D, NSTAGE, TRACE, SMX, FC>;
+  using K_t = decltype(&prefill_sm100_kernel<D, NSTAGE, TRACE, SMX, FC, RP>);
+  K_t kern = prefill_sm100_kernel<D, NSTAGE, TRACE, SMX, FC, RP>;
   const size_t smem = sizeof(Smem<D, NSTAGE>) + Smem<D, NSTAGE>::PAD;
   {
     cudaError_t e = set_smem_attr((const void*)kern, smem);
@@ -1072,9 +1221,11 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
     grid = dim3(n_qt * BH, 1);
   }
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
-  cudaError_t e = launch_pdl(kern, grid, dim3(FUSED ? NTHREADS_F : NTHREADS), smem, s, mQ, mK, mV,
+  const RopeArgs ra = rap ? *rap : RopeArgs{};
+  cudaError_t e = launch_pdl(kern, grid, dim3((FUSED || RP) ? NTHREADS_F : NTHREADS), smem, s, mQ, mK, mV,
                              mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
-                             cfg.summary_bias * 1.4426950408889634f, lse, overlap ? 1 : 0, tile_sum_first(), fa);
+                             cfg.summary_bias * 1.4426950408889634f, lse, overlap ? 1 : 0, tile_sum_first(), fa,
+                             ra);
   if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
@@ -1148,6 +1299,32 @@ cudaError_t launch_prefill_sm100_fused(const eva_config& cfg, const void* Q, con
   if (cfg.d_head == 64) EVA_FUSED_LAUNCH(64, 3)
 #undef EVA_FUSED_LAUNCH
   return cudaErrorNotSupported;
+}
+
+// In-kernel RoPE (eva_attn_prefill_rope): bf16, d in {64, 128}, whole-sequence call, rotary
+// channels a power of two (>= 8 interleaved, >= 16 half-split) -- the rope warps' item split.
+bool prefill_rope_supported(const eva_config& cfg, int rotary_dim, int style) {
+  if (!prefill_sm100_supported(cfg)) return false;
+  const int rd = rotary_dim ? rotary_dim : cfg.d_head;
+  if (rd > cfg.d_head || (rd & (rd - 1)) != 0) return false;
+  return style == EVA_ROPE_NEOX ? rd >= 16 : rd >= 8;
+}
+
+cudaError_t launch_prefill_sm100_rope(const eva_config& cfg, double log2_base, int rotary_dim, int style,
+                                      const void* Q, const void* K, const void* V, const void* Ksum,
+                                      const void* Vsum, void* O, float* lse, cudaStream_t s) {
+  if (cfg.bh_count == 0) return cudaSuccess;
+  if (!prefill_rope_supported(cfg, rotary_dim, style)) return cudaErrorNotSupported;
+  const PrefillRange rg = full_range(cfg);
+  RopeArgs ra{};
+  ra.rd = rotary_dim ? rotary_dim : cfg.d_head;
+  for (int j = 0; j < ra.rd / 2; ++j) ra.th[j] = std::exp2(log2_base * (-2.0 * (double)j / (double)ra.rd));
+  const bool neox = style == EVA_ROPE_NEOX;
+  if (cfg.d_head == 128)
+    return neox ? launch_t<128, 2, false, 0, 0, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra)
+                : launch_t<128, 2, false, 0, 0, 1>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra);
+  return neox ? launch_t<64, 3, false, 0, 0, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra)
+              : launch_t<64, 3, false, 0, 0, 1>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra);
 }
 
 cudaError_t prefill_fused_reserve(const eva_config& cfg, cudaStream_t s) {

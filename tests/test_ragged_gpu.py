@@ -168,3 +168,75 @@ def test_ragged_decode_with_per_unit_rope(eva, style):
             worst = max(worst, np.max(np.abs(of[u] - ro)))
     assert worst <= 2e-2, worst
     assert pos.tolist() == [p + steps for p in prompt]
+
+
+@pytest.mark.parametrize("style", ["interleaved", "neox"])
+@pytest.mark.parametrize("dtype,d,rd,C,W", [(torch.bfloat16, 64, 32, 16, 64), (torch.bfloat16, 128, 128, 64, 128),
+                                            (torch.float32, 32, 16, 8, 24)])
+def test_ragged_decode_rope_folded(eva, style, dtype, d, rd, C, W):
+    """RoPE folded into the one-launch ragged step (eva_decode_step_ragged_rope): q and k_new
+    un-rotated in, rotated in registers at each unit's position.  Against the oracle cache fed the
+    fp64-rotated keys (stored in dtype, R18) and the fp64-rotated query, and against the two-pass
+    form (eva_rope at pos, then eva_decode_step_ragged) on a second cache."""
+    BH, steps = 4, 2 * C + 5
+    prompt = [0, 9, C * 2 - 1, W + 3]
+    cap = (max(prompt) + steps) // C + 1
+    cfg = eva.make_config(1, BH, 0, d, C, W, dtype=dtype, seed=25)
+    caches = [eva.DecodeCache(cfg, cap, device="cuda") for _ in range(2)]
+    orc = [oracle.Cache(d, C, W, oracle.SLIDING, cap=cap, scale=cfg.scale) for _ in range(BH)]
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, BH, cap + 1, d)
+    st = oracle.ROPE_NEOX if style == "neox" else oracle.ROPE_INTERLEAVED
+    q, k, v = eva_inputs.decode_tokens(0, BH, max(prompt) + steps, d, dtype, seed=26, device="cuda")
+    from paper_2511_00576_b200 import _native as N
+    one = eva.make_config(1, BH, 1, d, C, W, dtype=dtype, seed=25)
+    for u, n in enumerate(prompt):
+        if n == 0:
+            continue
+        kr = eva.eva_rope(eva.make_config(1, 1, n, d, C, W, dtype=dtype), k[:n, u].unsqueeze(0).contiguous(),
+                          rotary_dim=rd, style=style)
+        for cache in caches:
+            view = _unit_view(eva, cache, u)
+            N.check(N.lib.eva_cache_append(ctypes.byref(view), kr.data_ptr(),
+                                           v[:n, u].unsqueeze(0).contiguous().data_ptr(), n, None, None))
+        for t in range(n):
+            kt = torch.from_numpy(oracle.rope_ex(f64(k[t, u])[None], [t], rotary_dim=rd, style=st)).to(dtype)
+            assert orc[u].append(kt.double().numpy()[0], f64(v[t, u]), E[u, t // C]) == 0
+    pos = [torch.tensor(prompt, dtype=torch.int64, device="cuda") for _ in range(2)]
+    rope = dict(rope_base=10000.0, rotary_dim=rd, style=style)
+    worst, worst2 = 0.0, 0.0
+    tol = TOL[dtype]
+    for s in range(steps):
+        idx = [prompt[u] + s for u in range(BH)]
+        qs = torch.stack([q[idx[u], u] for u in range(BH)]).contiguous()
+        ks = torch.stack([k[idx[u], u] for u in range(BH)]).contiguous()
+        vs = torch.stack([v[idx[u], u] for u in range(BH)]).contiguous()
+        o, lse = caches[0].eva_decode_step_ragged(pos[0], qs, ks, vs, rope=rope)
+        qr = eva.eva_rope(one, qs.unsqueeze(1).contiguous(), rotary_dim=rd, style=style, pos=pos[1])[:, 0].contiguous()
+        kr = eva.eva_rope(one, ks.unsqueeze(1).contiguous(), rotary_dim=rd, style=style, pos=pos[1])[:, 0].contiguous()
+        o2, _ = caches[1].eva_decode_step_ragged(pos[1], qr, kr, vs)
+        of = f64(o)
+        worst2 = max(worst2, (o.float() - o2.float()).abs().max().item())
+        for u in range(BH):
+            kt = torch.from_numpy(oracle.rope_ex(f64(ks[u])[None], [idx[u]], rotary_dim=rd, style=st)).to(dtype)
+            qt = oracle.rope_ex(f64(qs[u])[None], [idx[u]], rotary_dim=rd, style=st)[0]
+            assert orc[u].append(kt.double().numpy()[0], f64(vs[u]), E[u, idx[u] // C]) == 0
+            ro, rl = orc[u].decode(qt)
+            worst = max(worst, np.max(np.abs(of[u] - ro)), abs(float(lse[u]) - rl))
+    assert worst <= tol, worst
+    assert worst2 <= tol, worst2
+    assert pos[0].tolist() == pos[1].tolist() == [p + steps for p in prompt]
+    # the rotated keys in the ring and the summaries agree with the two-pass cache
+    for a, b in ((caches[0].ring_k, caches[1].ring_k), (caches[0].sum_k, caches[1].sum_k),
+                 (caches[0].sum_v, caches[1].sum_v)):
+        assert (a.float() - b.float()).abs().max().item() <= tol
+
+
+def test_ragged_decode_rope_validation(eva):
+    cfg = eva.make_config(1, 2, 0, 128, 16, 64)
+    cache = eva.DecodeCache(cfg, 4, device="cuda")
+    pos = torch.zeros(2, dtype=torch.int64, device="cuda")
+    z = torch.zeros(2, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(eva.EvaError, match="UNSUPPORTED"):   # rd / 16 = 3: no shuffle partner
+        cache.eva_decode_step_ragged(pos, z, z, z, rope=dict(rotary_dim=48, style="neox"))
+    with pytest.raises(eva.EvaError, match="INVALID_ARG"):
+        cache.eva_decode_step_ragged(pos, z, z, z, rope=dict(rope_base=0.5))

@@ -189,3 +189,83 @@ def test_rope_ex_validation(eva):
     Z = torch.zeros(1, 96, 128, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(eva.EvaError, match="UNSUPPORTED"):   # rd / 16 = 3: no butterfly partner
         eva.eva_rope_summarize(cfg, Z, Z, Z, rotary_dim=48, style="neox")
+
+
+# ------------------------------------------------------------------ RoPE inside the tensor-core
+# prefill (eva_attn_prefill_rope): the kernel rotates the landed Q / local-K tiles in shared
+# memory; compared with the oracle on the fp64-rotated inputs rounded to bf16 (R18: the rotated
+# values the MMA reads are bf16), and with the two-pass path (rope-summarize + prefill).
+@pytest.mark.parametrize("B,H,T,d,C,W,rd,style,mode", [
+    (1, 2, 515, 64, 64, 128, 64, "interleaved", 0),
+    (1, 2, 515, 64, 64, 128, 16, "neox", 0),
+    (1, 1, 700, 128, 64, 256, 128, "interleaved", 0),
+    (1, 1, 700, 128, 64, 256, 128, "neox", 0),
+    (2, 1, 1000, 128, 32, 96, 32, "interleaved", 1),
+    (1, 2, 640, 64, 16, 64, 32, "neox", 1),
+    (1, 1, 100, 64, 64, 128, 64, "interleaved", 0),
+])
+def test_prefill_rope_in_kernel_parity(eva, B, H, T, d, C, W, rd, style, mode):
+    base = 10000.0
+    cfg = eva.make_config(B, H, T, d, C, W, seed=23, mode=mode)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=24, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill_rope(cfg, Q, K, V, rope_base=base, rotary_dim=rd, style=style)
+    # the two-pass path on the same inputs
+    Qr, Kr, ks2, vs2 = eva.eva_rope_summarize(cfg, Q, K, V, rope_base=base, rotary_dim=rd, style=style)
+    O2, lse2, _, _ = eva.eva_attn_prefill(cfg, Qr, Kr, V, Ksum=ks2, Vsum=vs2, summaries_provided=True)
+    # summaries provided: the same call on the two-pass summaries
+    O3, lse3, _, _ = eva.eva_attn_prefill_rope(cfg, Q, K, V, rope_base=base, rotary_dim=rd, style=style,
+                                               Ksum=ks2, Vsum=vs2, summaries_provided=True)
+    torch.cuda.synchronize()
+    assert torch.equal(ks, ks2) and torch.equal(vs, vs2)   # same summariser, summaries-only form
+    assert torch.equal(O, O3) and torch.equal(lse, lse3)
+    assert (O.float() - O2.float()).abs().max().item() <= 2e-2
+    st = oracle.ROPE_NEOX if style == "neox" else oracle.ROPE_INTERLEAVED
+    nC = T // C
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, nC, d)
+    omode = oracle.SLIDING if mode == 0 else oracle.BLOCK
+    for u in range(B * H):
+        p = np.arange(T)
+        rq = torch.from_numpy(oracle.rope_ex(f64(Q[u]), p, base=base, rotary_dim=rd, style=st)).to(torch.bfloat16)
+        rk = torch.from_numpy(oracle.rope_ex(f64(K[u]), p, base=base, rotary_dim=rd, style=st)).to(torch.bfloat16)
+        rq, rk = rq.double().numpy(), rk.double().numpy()
+        sk, sv = oracle.summarize(rk, f64(V[u]), E[u], C)
+        if nC:
+            assert np.max(np.abs(f64(ks[u]) - sk)) <= 2e-2
+        ro, rl = oracle.prefill(rq, rk, f64(V[u]), sk, sv, C, W, omode, cfg.scale)
+        assert np.max(np.abs(f64(O[u]) - ro)) <= 2e-2
+        assert np.max(np.abs(f64(lse[u]) - rl)) <= 2e-2
+
+
+def test_prefill_rope_in_kernel_long_positions(eva):
+    """configs[2]'s per-unit shape (T = 8192, d = 128, C = 64, W = 256) on 2 units: positions up
+    to 8191 exercise the rotation recurrence over whole tiles; sampled query rows vs the oracle."""
+    B, H, T, d, C, W = 1, 2, 8192, 128, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W, seed=29)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=30, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill_rope(cfg, Q, K, V, rope_base=10000.0)
+    torch.cuda.synchronize()
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, T // C, d)
+    rows = np.array([0, 1, 127, 128, 4095, 4096, 6000, 8064, 8191])
+    for u in range(B * H):
+        p = np.arange(T)
+        rq = torch.from_numpy(oracle.rope_ex(f64(Q[u]), p, base=10000.0)).to(torch.bfloat16).double().numpy()
+        rk = torch.from_numpy(oracle.rope_ex(f64(K[u]), p, base=10000.0)).to(torch.bfloat16).double().numpy()
+        sk, sv = oracle.summarize(rk, f64(V[u]), E[u], C)
+        ro, rl = oracle.prefill(rq, rk, f64(V[u]), sk, sv, C, W, oracle.SLIDING, cfg.scale)
+        assert np.max(np.abs(f64(O[u])[rows] - ro[rows])) <= 2e-2
+        assert np.max(np.abs(f64(O[u]) - ro)) <= 2e-2
+
+
+def test_prefill_rope_in_kernel_validation(eva):
+    cfg = eva.make_config(1, 1, 256, 64, 16, 32, dtype=torch.float32)
+    Z = torch.zeros(1, 256, 64, dtype=torch.float32, device="cuda")
+    with pytest.raises(eva.EvaError, match="UNSUPPORTED"):   # the tensor-core path is bf16
+        eva.eva_attn_prefill_rope(cfg, Z, Z, Z)
+    cfg = eva.make_config(1, 1, 256, 128, 16, 32)
+    Z = torch.zeros(1, 256, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(eva.EvaError, match="UNSUPPORTED"):   # rotary_dim not a power of two
+        eva.eva_attn_prefill_rope(cfg, Z, Z, Z, rotary_dim=96)
+    cfg = eva.make_config(1, 1, 256, 32, 16, 32)
+    Z = torch.zeros(1, 256, 32, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(eva.EvaError, match="UNSUPPORTED"):   # d = 32: no tensor-core kernel
+        eva.eva_attn_prefill_rope(cfg, Z, Z, Z)
