@@ -112,7 +112,7 @@ __device__ __forceinline__ void rope_cs(int64_t pos, int j, const RopeSpec& rs, 
   const double theta = rs.th[j];
   double a = (double)pos * theta;
   a -= 6.283185307179586 * rint(a * 0.15915494309189535);
-  sincosf((float)a, &s, &c);
+  __sincosf((float)a, &s, &c);  // |a| <= pi after the reduction: the MUFU form is ~1e-6 absolute
   s *= rs.sign;
 }
 
@@ -210,11 +210,36 @@ __global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ X, T* _
 // (off = rd / (2 VEC), a power of two), exchanged by shuffles -- every lane takes part.
 template <typename T, int D>
 struct RopeKX {
+  static constexpr int VEC = 16 / sizeof(T);
   const RopeSpec& rs;  // the kernel's __grid_constant__ parameter
   int64_t r0;
   T* Krc;
+  int step;            // rows between this lane's consecutive calls (the summariser's 4 * RPW)
+  // A lane's calls walk rows r, r + step, ...: the angles of its pairs come from double
+  // precision at the first call, then by the recurrence e^{i (p + step) theta} =
+  // e^{i p theta} e^{i step theta} (fp32, at most 16 steps).
+  mutable float c[VEC], s[VEC], sc[VEC], ss[VEC];
+  mutable bool init = false;
+  __device__ __forceinline__ void angles(int64_t pos, int j0, int np) const {
+#pragma unroll
+    for (int jj = 0; jj < VEC; ++jj) {
+      if (jj < np) {
+        rope_cs(pos, j0 + jj, rs, c[jj], s[jj]);
+        rope_cs((int64_t)step, j0 + jj, rs, sc[jj], ss[jj]);
+      }
+    }
+  }
+  __device__ __forceinline__ void next(int np) const {
+#pragma unroll
+    for (int jj = 0; jj < VEC; ++jj) {
+      if (jj < np) {
+        const float cn = c[jj] * sc[jj] - s[jj] * ss[jj];
+        s[jj] = s[jj] * sc[jj] + c[jj] * ss[jj];
+        c[jj] = cn;
+      }
+    }
+  }
   __device__ __forceinline__ void operator()(int r, int ch0, uint4& x, bool valid) const {
-    constexpr int VEC = 16 / sizeof(T);
     if (rs.style == EVA_ROPE_NEOX) {
       const int off = rs.rd / (2 * VEC);
       uint4 y;
@@ -222,14 +247,32 @@ struct RopeKX {
       y.y = __shfl_xor_sync(0xffffffffu, x.y, off);
       y.z = __shfl_xor_sync(0xffffffffu, x.z, off);
       y.w = __shfl_xor_sync(0xffffffffu, x.w, off);
-      const int gl = ch0 / VEC;
       if (ch0 < rs.rd) {
-        if (gl < off) rope_pair_neox<T>(x, y, r0 + r, ch0, rs);           // x first half
-        else rope_pair_neox<T>(y, x, r0 + r, ch0 - rs.rd / 2, rs);       // x second half
+        const bool first = ch0 < rs.rd / 2;
+        if (!init) angles(r0 + r, first ? ch0 : ch0 - rs.rd / 2, VEC);
+        else next(VEC);
+        float vx[VEC], vy[VEC];
+        unpack16<T>(x, vx);
+        unpack16<T>(y, vy);
+#pragma unroll
+        for (int jj = 0; jj < VEC; ++jj)
+          vx[jj] = first ? vx[jj] * c[jj] - vy[jj] * s[jj] : vy[jj] * s[jj] + vx[jj] * c[jj];
+        x = pack16<T>(vx);
       }
     } else if (ch0 < rs.rd) {
-      x = rope_piece_il<T>(x, r0 + r, ch0, rs);
+      if (!init) angles(r0 + r, ch0 / 2, VEC / 2);
+      else next(VEC / 2);
+      float v[VEC];
+      unpack16<T>(x, v);
+#pragma unroll
+      for (int jj = 0; jj < VEC / 2; ++jj) {
+        const float x0 = v[2 * jj], x1 = v[2 * jj + 1];
+        v[2 * jj] = x0 * c[jj] - x1 * s[jj];
+        v[2 * jj + 1] = x0 * s[jj] + x1 * c[jj];
+      }
+      x = pack16<T>(v);
     }
+    init = true;
     if (valid && Krc) *reinterpret_cast<uint4*>(Krc + (size_t)r * D + ch0) = x;
   }
 };
@@ -262,7 +305,8 @@ __global__ void __launch_bounds__(128) rope_summarize_kernel(eva_config cfg, con
   if (c >= nC) return;
   const T* Kc = K + (ub + (size_t)r0) * D;
   const T* Vc = V + (ub + (size_t)r0) * D;
-  RopeKX<T, D> kx{rs, (int64_t)r0, Kr ? Kr + (ub + (size_t)r0) * D : nullptr};
+  constexpr int RPW_ = 32 / (D / (16 / (int)sizeof(T)));
+  RopeKX<T, D> kx{rs, (int64_t)r0, Kr ? Kr + (ub + (size_t)r0) * D : nullptr, 4 * RPW_};
   summarize_chunk_reg<T, D, NI>([&](int r) { return Kc + (size_t)r * D; }, [&](int r) { return Vc + (size_t)r * D; },
                                 C, eps ? eps + ((size_t)u * nC + c) * D : nullptr, (uint32_t)(cfg.bh_begin + u),
                                 (uint32_t)c, cfg, Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D,

@@ -45,6 +45,9 @@ constexpr int NTHREADS = 192;
 // EVA_SUMMARIES_FUSED: two more warps (6, 7) compute the chunk summaries in-kernel
 constexpr int NTHREADS_F = 256;
 constexpr int SUMM_THREADS_F = 64;
+// in-kernel RoPE: ROPE_WARPS warps (6 ..) rotate the local K tiles
+constexpr int ROPE_WARPS = 4;
+constexpr int NTHREADS_R = NTHREADS + 32 * ROPE_WARPS;
 constexpr uint32_t TMEM_COLS = 256;
 constexpr uint32_t TM_O = 128;
 
@@ -134,46 +137,54 @@ __device__ __forceinline__ uint64_t hi2(uint32_t w0, uint32_t w1) {
 }
 
 template <int STYLE>
-struct RopeTile {
+struct RopeWalker {
   static constexpr int NP = STYLE == 2 ? 8 : 4;  // pairs per item
   static constexpr int NQ = NP / 2;               // packed pair groups
-  template <int D>
-  __device__ __forceinline__ static void run(uint8_t* base, int nrows, int64_t pos0, const RopeArgs& ra, int t,
-                                             int nthr) {
+  uint64_t c[NQ], s[NQ], sc[NQ], ss[NQ];          // angle of the next row; one row-step rotation
+  const double* th;
+  int item, g, rstep, off_b;
+  int64_t at = -1;                                // position whose angle c / s hold (-1: none)
+  __device__ __forceinline__ void init(const RopeArgs& ra, int t, int nthr) {
     const int NI = STYLE == 2 ? ra.rd / 16 : ra.rd / 8;
-    const int item = t % NI, g = t / NI, rstep = nthr / NI;
-    if (g >= rstep) return;
-    uint64_t c[NQ], s[NQ], sc[NQ], ss[NQ], nss[NQ];
+    item = t % NI;
+    g = t / NI;
+    rstep = nthr / NI;
+    off_b = ra.rd / 2;
+    th = ra.th + NP * item;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-      float c0, s0, c1, s1, a0, b0, a1, b1;
-      const double t0 = ra.th[NP * item + 2 * q], t1 = ra.th[NP * item + 2 * q + 1];
-      rope_angle((double)(pos0 + g) * t0, c0, s0);
-      rope_angle((double)(pos0 + g) * t1, c1, s1);
-      rope_angle((double)rstep * t0, a0, b0);
-      rope_angle((double)rstep * t1, a1, b1);
-      c[q] = f2pack(c0, c1);
-      s[q] = f2pack(s0, s1);
+      float a0, b0, a1, b1;
+      rope_angle((double)rstep * th[2 * q], a0, b0);
+      rope_angle((double)rstep * th[2 * q + 1], a1, b1);
       sc[q] = f2pack(a0, a1);
       ss[q] = f2pack(b0, b1);
-      nss[q] = neg2(ss[q]);
     }
-    const int ch_a = 8 * item, ch_b = ch_a + ra.rd / 2;
-    const uint32_t off_a = (uint32_t)(ch_a >> 6) * (uint32_t)nrows * 128u, c16_a = (uint32_t)((ch_a & 63) >> 3);
-    const uint32_t off_b = (uint32_t)(ch_b >> 6) * (uint32_t)nrows * 128u, c16_b = (uint32_t)((ch_b & 63) >> 3);
-    auto advance = [&] {
+  }
+  // Rotate rows g, g + rstep, ... < nrows of a swizzled tile (D/64 sub-tiles of nrows x 128 B)
+  // holding positions pos0 + r.  A tile that continues the previous one (pos0 + g == at: the
+  // local K tiles are consecutive) keeps the recurrence going; otherwise the first angle is
+  // computed in double.
+  __device__ __forceinline__ void run(uint8_t* base, int nrows, int64_t pos0) {
+    if (g >= rstep) return;
+    if (pos0 + g != at) {
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const uint64_t cn = ffma2(s[q], nss[q], fmul2(c[q], sc[q]));
-        s[q] = ffma2(c[q], ss[q], fmul2(s[q], sc[q]));
-        c[q] = cn;
+        float c0, s0, c1, s1;
+        rope_angle((double)(pos0 + g) * th[2 * q], c0, s0);
+        rope_angle((double)(pos0 + g) * th[2 * q + 1], c1, s1);
+        c[q] = f2pack(c0, c1);
+        s[q] = f2pack(s0, s1);
       }
-    };
+    }
+    const int ch_a = 8 * item, ch_b = ch_a + off_b;
+    const uint32_t off_a = (uint32_t)(ch_a >> 6) * (uint32_t)nrows * 128u, c16_a = (uint32_t)((ch_a & 63) >> 3);
+    const uint32_t offb = (uint32_t)(ch_b >> 6) * (uint32_t)nrows * 128u, c16_b = (uint32_t)((ch_b & 63) >> 3);
+    int r = g;
 #pragma unroll 2
-    for (int r = g; r < nrows; r += rstep) {
+    for (; r < nrows; r += rstep) {
       uint4* pa = reinterpret_cast<uint4*>(base + off_a + (uint32_t)r * 128u + ((c16_a ^ (uint32_t)(r & 7)) << 4));
       if constexpr (STYLE == 2) {
-        uint4* pb = reinterpret_cast<uint4*>(base + off_b + (uint32_t)r * 128u + ((c16_b ^ (uint32_t)(r & 7)) << 4));
+        uint4* pb = reinterpret_cast<uint4*>(base + offb + (uint32_t)r * 128u + ((c16_b ^ (uint32_t)(r & 7)) << 4));
         const uint4 xa = *pa, xb = *pb;
         const uint32_t wa[4] = {xa.x, xa.y, xa.z, xa.w}, wb[4] = {xb.x, xb.y, xb.z, xb.w};
         uint32_t oa[4], ob[4];
@@ -193,14 +204,19 @@ struct RopeTile {
         // pairs (0, 1) in words x, y; pairs (2, 3) in words z, w: even channels in the low halves
         const uint64_t e01 = lo2(xa.x, xa.y), o01 = hi2(xa.x, xa.y);
         const uint64_t e23 = lo2(xa.z, xa.w), o23 = hi2(xa.z, xa.w);
-        const uint64_t n01 = neg2(s[0]), n23 = neg2(s[1]);
-        const uint64_t ye01 = ffma2(o01, n01, fmul2(e01, c[0])), yo01 = ffma2(o01, c[0], fmul2(e01, s[0]));
-        const uint64_t ye23 = ffma2(o23, n23, fmul2(e23, c[1])), yo23 = ffma2(o23, c[1], fmul2(e23, s[1]));
+        const uint64_t ye01 = ffma2(o01, neg2(s[0]), fmul2(e01, c[0])), yo01 = ffma2(o01, c[0], fmul2(e01, s[0]));
+        const uint64_t ye23 = ffma2(o23, neg2(s[1]), fmul2(e23, c[1])), yo23 = ffma2(o23, c[1], fmul2(e23, s[1]));
         *pa = make_uint4(pack_bf16(f2lo(ye01), f2lo(yo01)), pack_bf16(f2hi(ye01), f2hi(yo01)),
                          pack_bf16(f2lo(ye23), f2lo(yo23)), pack_bf16(f2hi(ye23), f2hi(yo23)));
       }
-      advance();
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {  // next row: multiply by e^{i rstep theta}
+        const uint64_t cn = ffma2(s[q], neg2(ss[q]), fmul2(c[q], sc[q]));
+        s[q] = ffma2(c[q], ss[q], fmul2(s[q], sc[q]));
+        c[q] = cn;
+      }
     }
+    at = pos0 + r;
   }
 };
 
@@ -660,7 +676,7 @@ __device__ __forceinline__ bool owns_chunks(const Plan& plan, int j, int C, int 
 // chunk summaries are computed in-kernel (one instantiation per chunk size keeps the code that
 // the instruction cache has to hold small)
 template <int D, int NSTAGE, bool TRACE = false, int SMX = -1, int FC = 0, int RP = 0>
-__global__ void __launch_bounds__((FC || RP) ? NTHREADS_F : NTHREADS, 2)
+__global__ void __launch_bounds__(RP ? NTHREADS_R : FC ? NTHREADS_F : NTHREADS, 2)
 prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
                      const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
@@ -722,8 +738,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     mbar_init(&sm->o_done, 1);
     mbar_init(&sm->o_final, 1);
     if constexpr (RP != 0) {
-      mbar_init(&sm->q_rot, NTHREADS_F - 64);
-      for (int s = 0; s < NSK; ++s) mbar_init(&sm->k_rot[s], SUMM_THREADS_F);
+      mbar_init(&sm->q_rot, NTHREADS_R - 64);
+      for (int s = 0; s < NSK; ++s) mbar_init(&sm->k_rot[s], 32 * ROPE_WARPS);
     }
     fence_mbar_init();
   }
@@ -768,8 +784,9 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     // in-kernel RoPE of the Q tile by the softmax and rope warps (idle until S(0) anyway)
     if (warp >= 2) {
       mbar_wait(&sm->q_full, 0);
-      RopeTile<RP>::template run<D>(reinterpret_cast<uint8_t*>(sm->q), BM, plan.n0, ra, (int)threadIdx.x - 64,
-                                    NTHREADS_F - 64);
+      RopeWalker<RP> rw;
+      rw.init(ra, (int)threadIdx.x - 64, NTHREADS_R - 64);
+      rw.run(reinterpret_cast<uint8_t*>(sm->q), BM, plan.n0);
       fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
       mbar_arrive(&sm->q_rot);
     }
@@ -1012,13 +1029,13 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     if constexpr (FUSED) fused_summaries<D, FC, TRACE>(sm, plan, fa, u, qt, epoch, tl);
     // ------------------------------------------------------------ rope warps (in-kernel RoPE)
     if constexpr (RP != 0) {
-      const int t = (int)threadIdx.x - (NTHREADS_F - SUMM_THREADS_F);
+      RopeWalker<RP> rw;
+      rw.init(ra, (int)threadIdx.x - NTHREADS, 32 * ROPE_WARPS);
       for (int j = 0; j < NT; ++j) {
         const int s = j % NSK;
         mbar_wait(&sm->k_full[s], (j / NSK) & 1);
         if (!plan.summary(j)) {  // summary tiles hold summaries of rotated keys already
-          RopeTile<RP>::template run<D>(reinterpret_cast<uint8_t*>(sm->k[s]), BN, plan.base(j), ra, t,
-                                        SUMM_THREADS_F);
+          rw.run(reinterpret_cast<uint8_t*>(sm->k[s]), BN, plan.base(j));
           fence_proxy_async_smem();
         }
         mbar_arrive(&sm->k_rot[s]);
@@ -1222,7 +1239,7 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
   }
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
   const RopeArgs ra = rap ? *rap : RopeArgs{};
-  cudaError_t e = launch_pdl(kern, grid, dim3((FUSED || RP) ? NTHREADS_F : NTHREADS), smem, s, mQ, mK, mV,
+  cudaError_t e = launch_pdl(kern, grid, dim3(RP ? NTHREADS_R : FUSED ? NTHREADS_F : NTHREADS), smem, s, mQ, mK, mV,
                              mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
                              cfg.summary_bias * 1.4426950408889634f, lse, overlap ? 1 : 0, tile_sum_first(), fa,
                              ra);
