@@ -430,7 +430,29 @@ def bench_prefill_large(args, eva, torch, dev, s, rank, world, peaks):
                         "traffic": load_traffic("prefill_configs2")},
            "summarize_roofline": {"bound": "hbm", "achieved": 2 * BH * T * d * 2 / (summ / 1e3) / 1e9,
                                   "peak": peaks["hbm"], "unit": "GB/s"}}
-    del Q, K, V, O, ks, vs
+    # RoPE (NEXT row 4, R18/R19) on the same inputs: rotation inside the tcgen05 prefill
+    # (eva_attn_prefill_rope; summaries of the rotated keys by the summaries-only RoPE
+    # summariser) against the two-pass form (eva_rope_summarize writes Qr, Kr, then the prefill)
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record(s)
+        for _ in range(reps):
+            fn()
+        ev[1].record(s)
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / reps
+    Qr, Kr, rks, rvs = eva.eva_rope_summarize(cfg, Q, K, V)
+    out["rope"] = {
+        "prefill_in_kernel_ms": timed(lambda: eva.eva_attn_prefill_rope(
+            cfg, Q, K, V, Ksum=rks, Vsum=rvs, summaries_provided=True, O=O, lse=lse)),
+        "step_in_kernel_ms": timed(lambda: eva.eva_attn_prefill_rope(cfg, Q, K, V, Ksum=rks, Vsum=rvs, O=O, lse=lse)),
+        "step_two_pass_ms": timed(lambda: (eva.eva_rope_summarize(cfg, Q, K, V),
+                                           eva.eva_attn_prefill(cfg, Qr, Kr, V, Ksum=rks, Vsum=rvs,
+                                                                summaries_provided=True, O=O, lse=lse))),
+        "note": "rotary_dim = d, interleaved, base 10000; step = summaries of the rotated keys + prefill"}
+    del Q, K, V, O, ks, vs, Qr, Kr, rks, rvs
     torch.cuda.empty_cache()
     return out
 

@@ -17,7 +17,15 @@ import paper_2511_00576_b200 as eva
 what = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 dev = torch.device("cuda:0")
-if what in ("prefill_configs2", "summarize_configs2", "prefill_configs1"):
+if what == "prefill_rope_configs2":  # RoPE inside the tcgen05 prefill (eva_attn_prefill_rope)
+    B, H, T, d, C, W = 8, 32, 8192, 128, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device=dev)
+    _, _, ks, vs = eva.eva_rope_summarize(cfg, Q, K, V)
+    O = torch.empty_like(Q)
+    for _ in range(reps):
+        eva.eva_attn_prefill_rope(cfg, Q, K, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O)
+elif what in ("prefill_configs2", "summarize_configs2", "prefill_configs1"):
     if what == "prefill_configs1":
         B, H, T, d, C, W = 1, 16, 2048, 64, 64, 128
     else:
