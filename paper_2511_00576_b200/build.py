@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libeva.so")
 SOURCES = ["api.cu", "kernels_simt.cu", "prefill_sm100.cu", "backward_simt.cu", "backward_sm100.cu",
-           "summarize_bulk.cu", "prefill_dual.cu"]
+           "summarize_bulk.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",

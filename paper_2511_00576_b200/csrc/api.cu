@@ -893,9 +893,6 @@ eva_status eva_debug_trace_prefill(const eva_config* cfg, const void* Q, const v
   if (cfg->dtype != EVA_BF16 || (cfg->d_head != 64 && cfg->d_head != 128))
     return fail(EVA_ERR_UNSUPPORTED, "trace needs bf16, d in {64,128}");
   if (!trace || cap < 1) return fail(EVA_ERR_INVALID_ARG, "trace buffer");
-  if (cap == 3)
-    return cuda_status(eva::debug_trace_dual(*cfg, Q, K, V, Ksum, Vsum, O, lse, trace, (cudaStream_t)stream),
-                       "eva_debug_trace_prefill(dual)");
   return cuda_status(eva::debug_trace_tile(*cfg, Q, K, V, Ksum, Vsum, O, lse, trace, cap == 2,
                                            (cudaStream_t)stream),
                      "eva_debug_trace_prefill(tile)");

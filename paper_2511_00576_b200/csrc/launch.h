@@ -57,16 +57,6 @@ cudaError_t launch_prefill_simt(const eva_config& cfg, const PrefillRange& rg, c
                                 const void* K, const void* V, const void* Ksum, const void* Vsum,
                                 void* O, float* lse, cudaStream_t s);
 
-// The d = 128 prefill with 128-key tiles and two query tiles per persistent CTA
-// (prefill_dual.cu): bf16, causal modes; same contract as launch_prefill_sm100.
-bool prefill_dual_supported(const eva_config& cfg);
-cudaError_t launch_prefill_dual(const eva_config& cfg, const PrefillRange& rg, const void* Q, const void* K,
-                                const void* V, const void* Ksum, const void* Vsum, void* O, float* lse,
-                                cudaStream_t s);
-// Debug timeline of CTA 0 of the dual kernel (4 roles x 160 events into trace_dev).
-cudaError_t debug_trace_dual(const eva_config& cfg, const void* Q, const void* K, const void* V, const void* Ksum,
-                             const void* Vsum, void* O, float* lse, unsigned long long* trace_dev, cudaStream_t s);
-
 // tcgen05/TMEM/TMA prefill (bf16, d in {64, 128}).  Returns cudaErrorNotSupported if the
 // shape is outside the kernel's envelope (the caller then reports EVA_ERR_UNSUPPORTED).
 bool prefill_sm100_supported(const eva_config& cfg);

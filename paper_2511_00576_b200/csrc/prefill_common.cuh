@@ -1,5 +1,5 @@
 // prefill_common.cuh -- small device helpers shared by the tcgen05 prefill kernels
-// (prefill_sm100.cu, prefill_dual.cu): MUFU exp2, bf16 packing, column-range bit masks, packed
+// (prefill_sm100.cu): MUFU exp2, bf16 packing, column-range bit masks, packed
 // fp32x2 arithmetic.
 #pragma once
 #include <cuda_bf16.h>

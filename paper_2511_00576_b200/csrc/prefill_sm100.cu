@@ -1119,18 +1119,6 @@ int softmax_emu() {
   return v;
 }
 
-// EVA_PREFILL_DUAL=1: d = 128 causal calls run the 128-key two-query-tile kernel
-// (prefill_dual.cu) -- opt-in: measured 0.877 ms at configs[2] against this kernel's 0.579 (the
-// two softmax warpgroups are MUFU- and latency-bound and each query tile's S -> softmax -> PV
-// chain is serial).
-bool prefill_dual_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("EVA_PREFILL_DUAL");
-    return e ? atoi(e) != 0 : false;
-  }();
-  return v;
-}
-
 // Tile order when not overlapping the summarize kernel: summary tiles first (measured 613 vs
 // 629 us at configs[2]); EVA_PREFILL_SUMFIRST=0 selects local-first for measurements.
 int tile_sum_first() {
@@ -1293,8 +1281,6 @@ cudaError_t launch_prefill_sm100(const eva_config& cfg, const PrefillRange& rg, 
                                  void* O, float* lse, uint32_t variant, cudaStream_t s) {
   if (cfg.bh_count == 0) return cudaSuccess;
   const bool overlap = (variant & 0x100u) != 0;  // EVA_PREFILL_OVERLAP
-  if (!overlap && prefill_dual_enabled() && prefill_dual_supported(cfg))
-    return launch_prefill_dual(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
   if (cfg.d_head == 128) return launch_t<128, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
   if (cfg.d_head == 64) return launch_t<64, 3>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap);
   return cudaErrorNotSupported;

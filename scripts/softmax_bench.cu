@@ -4,10 +4,7 @@
 #include <cuda_runtime.h>
 #include "../paper_2511_00576_b200/csrc/prefill_sm100.cu"
 namespace eva { void note_launch(int) {} int num_sms() { return 148; }
-cudaError_t set_smem_attr(const void*, size_t) { return cudaSuccess; }
-bool prefill_dual_supported(const eva_config&) { return false; }
-cudaError_t launch_prefill_dual(const eva_config&, const PrefillRange&, const void*, const void*, const void*,
-                                const void*, const void*, void*, float*, cudaStream_t) { return cudaErrorNotSupported; } }
+cudaError_t set_smem_attr(const void*, size_t) { return cudaSuccess; } }
 
 namespace eva { namespace {
 // ablations of softmax_tile2<D, 0> (VAR = 100 + bits): 1 exp -> FMUL, 2 no max tree, 4 no TMEM ld,
