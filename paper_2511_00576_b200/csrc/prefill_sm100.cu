@@ -1238,6 +1238,8 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
 
 }  // namespace
 
+cudaError_t debug_set_summ_trace(unsigned long long* p, cudaStream_t s);  // summarize_bulk.cu
+
 bool make_tma_map_bf16(CUtensorMap* m, const void* base, int units, int rows, int D, int box_rows) {
   return make_map(m, base, units, rows, D, box_rows);
 }
@@ -1260,8 +1262,17 @@ cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K
       return launch_t<128, 2, true, -1, 64>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr);
     return launch_t<64, 3, true, -1, 64>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr);
   }
-  if (cfg.d_head == 128) return launch_t<128, 2, true>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
-  if (cfg.d_head == 64) return launch_t<64, 3, true>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s);
+  // EVA_TRACE_OVERLAP=1: the traced summarize kernel (CTA spans at trace[8960 + 2 i]) and then the
+  // traced prefill in EVA_PREFILL_OVERLAP mode, as the step launches them
+  static const bool ovl = getenv("EVA_TRACE_OVERLAP") != nullptr;
+  if (ovl) {
+    e = debug_set_summ_trace(trace_dev + TT_SLOTS * TT_ROLES * TT_PER_ROLE + 2 * TT_MAX_CTAS, s);
+    if (e != cudaSuccess) return e;
+    e = launch_summarize_bulk(cfg, K, V, nullptr, const_cast<void*>(Ksum), const_cast<void*>(Vsum), 0, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (cfg.d_head == 128) return launch_t<128, 2, true>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, ovl);
+  if (cfg.d_head == 64) return launch_t<64, 3, true>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, ovl);
   return cudaErrorNotSupported;
 }
 

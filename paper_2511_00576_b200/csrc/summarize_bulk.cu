@@ -61,7 +61,10 @@ struct alignas(128) SumSmem {
   uint64_t full[NST];
 };
 
-template <int D, int CC, int NST>
+// debug timeline (eva_debug_trace_prefill with EVA_TRACE_OVERLAP=1): CTA entry / exit globaltimer
+__device__ unsigned long long* g_sum_trace = nullptr;
+
+template <int D, int CC, int NST, bool TR = false>
 __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config cfg, const __nv_bfloat16* __restrict__ K,
                                                                    const __nv_bfloat16* __restrict__ V,
                                                                    const float* __restrict__ eps,
@@ -74,6 +77,9 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
   constexpr uint32_t BYTES = CC * D * 2;
   const int t = threadIdx.x;
   const int nC = cfg.T / CC;
+  if constexpr (TR) {
+    if (t == 0 && g_sum_trace && blockIdx.x < 4096) g_sum_trace[2 * blockIdx.x] = globaltimer_ns();
+  }
   if (t == 0) {
     for (int s = 0; s < NST; ++s) mbar_init(&sm.full[s], 1);
     fence_mbar_init();
@@ -113,6 +119,9 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
       if (i2 < total) issue(k + NST, i2);
     }
   }
+  if constexpr (TR) {
+    if (t == 0 && g_sum_trace && blockIdx.x < 4096) g_sum_trace[2 * blockIdx.x + 1] = globaltimer_ns();
+  }
 }
 
 template <int D, int CC, int NST>
@@ -120,7 +129,8 @@ cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V,
                             void* Vsum, int c0, cudaStream_t s, int max_ctas) {
   using S = SumSmem<D, CC, NST>;
   const size_t smem = sizeof(S);
-  auto kern = summarize_bulk_kernel<D, CC, NST>;
+  static const bool tr = getenv("EVA_TRACE_OVERLAP") != nullptr;  // debug timeline only
+  auto kern = tr ? summarize_bulk_kernel<D, CC, NST, true> : summarize_bulk_kernel<D, CC, NST>;
   cudaError_t e = set_smem_attr((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -129,6 +139,11 @@ cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V,
   const int total = (cfg.T / CC) * cfg.bh_count;
   int grid = std::max(1, std::min(total, std::max(1, per_sm) * num_sms()));
   if (max_ctas > 0) grid = std::min(grid, max_ctas);
+  static const int per_sm_cap = [] {  // EVA_SUMM_PER_SM=k: at most k CTAs per SM (measurements)
+    const char* e = getenv("EVA_SUMM_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  if (per_sm_cap > 0) grid = std::min(grid, per_sm_cap * num_sms());
   e = launch_pdl(kern, dim3(grid), dim3(SB_THREADS), smem, s, cfg, (const __nv_bfloat16*)K,
                  (const __nv_bfloat16*)V, eps, (__nv_bfloat16*)Ksum, (__nv_bfloat16*)Vsum, c0, total);
   if (e != cudaSuccess) return e;
@@ -156,6 +171,10 @@ cudaError_t launch_bulk_t(const eva_config& cfg, const void* K, const void* V, c
 }
 
 }  // namespace
+
+cudaError_t debug_set_summ_trace(unsigned long long* p, cudaStream_t s) {
+  return cudaMemcpyToSymbolAsync(g_sum_trace, &p, sizeof(p), 0, cudaMemcpyHostToDevice, s);
+}
 
 bool summarize_bulk_supported(const eva_config& cfg) {
   return cfg.dtype == EVA_BF16 && (cfg.d_head == 64 || cfg.d_head == 128) &&

@@ -16,7 +16,7 @@ ks, vs = eva.eva_summarize(cfg, K, V)
 O = torch.empty_like(Q)
 lse = torch.empty(B * H, T, device="cuda")
 NCTA = 4096
-tr = torch.zeros(4 * R * 48 + 2 * NCTA, dtype=torch.int64, device="cuda")
+tr = torch.zeros(4 * R * 48 + 4 * NCTA, dtype=torch.int64, device="cuda")
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 flush = torch.empty(512 << 18, device="cuda")
@@ -41,10 +41,16 @@ for slot in range(4):
         print(f"  {(x >> 24) - t0:7d}  {names.get((x >> 16) & 0xff, '?'):20s} j={x & 0xffff}")
 
 # per-CTA entry/exit (globaltimer ns) relative to the earliest entry
-ct = v[4 * R * 48:]
+ct = v[4 * R * 48:4 * R * 48 + 2 * NCTA]
+st = v[4 * R * 48 + 2 * NCTA:]
 spans = [(ct[2 * i], ct[2 * i + 1]) for i in range(NCTA) if ct[2 * i]]
 if spans:
-    g0 = min(a for a, _ in spans)
+    sspans = [(st[2 * i], st[2 * i + 1]) for i in range(NCTA) if st[2 * i]]
+    g0 = min([a for a, _ in spans] + [a for a, _ in sspans])
+    if sspans:
+        se = sorted(b - g0 for _, b in sspans)
+        ss_ = sorted(a - g0 for a, _ in sspans)
+        print(f"=== summarize: {len(sspans)} CTAs start p0/p100 {ss_[0]}/{ss_[-1]}  end p0/p50/p100 {se[0]}/{se[len(se) // 2]}/{se[-1]}")
     ends = sorted(b - g0 for _, b in spans)
     starts = sorted(a - g0 for a, _ in spans)
     dur = sorted(b - a for a, b in spans)
