@@ -269,3 +269,53 @@ def test_prefill_rope_in_kernel_validation(eva):
     Z = torch.zeros(1, 256, 32, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(eva.EvaError, match="UNSUPPORTED"):   # d = 32: no tensor-core kernel
         eva.eva_attn_prefill_rope(cfg, Z, Z, Z)
+
+
+@pytest.mark.parametrize("mode,bias,T", [("noncausal", 0.0, 512), ("sliding", 0.7, 700), ("block", -0.4, 576)])
+def test_prefill_rope_in_kernel_variants(eva, mode, bias, T):
+    """In-kernel RoPE with the non-causal partition (R15) and the summary-logit bias (R16):
+    against oracle_prefill_ext on the bf16-stored fp64-rotated inputs."""
+    B, H, d, C, W = 1, 2, 128, 64, 128
+    m = {"sliding": 0, "block": 1, "noncausal": 2}[mode]
+    cfg = eva.make_config(B, H, T, d, C, W, seed=31, mode=mode, summary_bias=bias)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=32, device="cuda")
+    O, lse, ks, vs = eva.eva_attn_prefill_rope(cfg, Q, K, V, rope_base=10000.0, rotary_dim=64, style="neox")
+    torch.cuda.synchronize()
+    nC = T // C
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, nC, d)
+    p = np.arange(T)
+    rq = np.stack([torch.from_numpy(oracle.rope_ex(f64(Q[u]), p, rotary_dim=64, style=oracle.ROPE_NEOX))
+                   .to(torch.bfloat16).double().numpy() for u in range(B * H)])
+    rk = np.stack([torch.from_numpy(oracle.rope_ex(f64(K[u]), p, rotary_dim=64, style=oracle.ROPE_NEOX))
+                   .to(torch.bfloat16).double().numpy() for u in range(B * H)])
+    sk, sv = oracle.summarize_batch(rk, f64(V), E, C)
+    assert np.max(np.abs(f64(ks) - sk)) <= 2e-2
+    ro, rl = oracle.prefill_ext_batch(rq, rk, f64(V), f64(ks), f64(vs), C, W, m, cfg.scale, bias)
+    assert np.max(np.abs(f64(O) - ro)) <= 2e-2
+    assert np.max(np.abs(f64(lse) - rl)) <= 2e-2
+
+
+def test_ragged_rope_ignores_two_launch_switch():
+    """EVA_RAGGED_TWO_LAUNCH=1 selects the two-launch ragged form; RoPE is folded into the
+    one-launch form only, so the RoPE step must still run (and equal the default process's)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, eva_inputs, paper_2511_00576_b200 as eva\n"
+        "cfg = eva.make_config(1, 4, 0, 64, 16, 64)\n"
+        "c = eva.DecodeCache(cfg, 8, device='cuda')\n"
+        "pos = torch.tensor([0, 3, 15, 40], dtype=torch.int64, device='cuda')\n"
+        "q, k, v = eva_inputs.decode_tokens(0, 4, 20, 64, torch.bfloat16, seed=3, device='cuda')\n"
+        "outs = []\n"
+        "for i in range(20):\n"
+        "    o, _ = c.eva_decode_step_ragged(pos, q[i], k[i], v[i], rope=dict(rotary_dim=32, style='neox'))\n"
+        "    outs.append(o.float().cpu())\n"
+        "torch.save(torch.stack(outs), '/tmp/eva_rr_%s.pt' % __import__('os').environ.get('EVA_RAGGED_TWO_LAUNCH', '0'))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for flag in ("0", "1"):
+        env = dict(os.environ, EVA_RAGGED_TWO_LAUNCH=flag, PYTHONPATH=root)
+        r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+    a, b = torch.load("/tmp/eva_rr_0.pt"), torch.load("/tmp/eva_rr_1.pt")
+    assert torch.equal(a, b)
