@@ -1104,21 +1104,6 @@ bool make_map(CUtensorMap* m, const void* base, int units, int rows, int D, int 
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Softmax step of the tile kernel: 0 (default) = softmax_tile2 with packed fp32x2 arithmetic
-// (FFMA2/FADD2) and every exponential on MUFU; k in {1, 2, 4} = k of every 8 column pairs
-// exponentiated on the FMA pipe (FA4-style split); -1 = the scalar softmax_tile.  EVA_SOFTMAX_EMU
-// overrides (read once).  Measured (configs[2] attention; configs[4] T=128k C=32): scalar 0.578
-// ms / 0.589 of bf16 peak, packed 0.571 / 0.599, k=1 0.573 / 0.596, k=2 0.584 / 0.583, k=4
-// 0.60 / 0.55 -- the step is not MUFU-bound.
-int softmax_emu() {
-  static const int v = [] {
-    const char* e = getenv("EVA_SOFTMAX_EMU");
-    const int k = e ? atoi(e) : 0;
-    return k == 0 || k == 1 || k == 2 || k == 4 ? k : -1;
-  }();
-  return v;
-}
-
 // Tile order when not overlapping the summarize kernel: summary tiles first (measured 613 vs
 // 629 us at configs[2]); EVA_PREFILL_SUMFIRST=0 selects local-first for measurements.
 int tile_sum_first() {
@@ -1171,14 +1156,8 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
                      cudaStream_t s, bool overlap = false, const float* eps = nullptr,
                      const RopeArgs* rap = nullptr) {
   constexpr bool FUSED = FC != 0;
-  if constexpr (!TRACE && SMX == -1 && !FUSED && RP == 0) {
-    switch (softmax_emu()) {
-      case 0: return launch_t<D, NSTAGE, false, 0, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
-      case 1: return launch_t<D, NSTAGE, false, 1, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
-      case 2: return launch_t<D, NSTAGE, false, 2, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
-      case 4: return launch_t<D, NSTAGE, false, 4, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
-      default: break;
-    }
+  if constexpr (!TRACE && SMX == -1 && !FUSED && RP == 0) {  // the packed softmax (softmax_tile2)
+    return launch_t<D, NSTAGE, false, 0, 0>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, overlap, eps);
   }
   const int BH = cfg.bh_count, nC = rg.nsl;
   if (rg.nq == 0) return cudaSuccess;
