@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <utility>
 
 #include "common.cuh"
@@ -66,7 +67,8 @@ struct alignas(16) SummScratch {
 // (a deeper K ring lets the next K tiles stream in earlier; K is consumed one softmax period
 // before V).  Deep-ring layouts are sized to fill the SM with two CTAs, so they are used
 // without the 1 KB alignment pad (the dynamic window is 1 KB aligned; checked in-kernel).
-template <int D, int NSTAGE>
+struct NoSumm {};
+template <int D, int NSTAGE, bool FS = false>
 struct __align__(1024) Smem {
   static constexpr int NSK = NSTAGE >= 10 ? NSTAGE / 10 : NSTAGE;
   static constexpr int NSV = NSTAGE >= 10 ? NSTAGE % 10 : NSTAGE;
@@ -81,7 +83,7 @@ struct __align__(1024) Smem {
   uint64_t s_full[2], p_full[2], o_done, o_final;
   uint64_t q_rot, k_rot[NSK];  // RoPE in-kernel: Q rotated (warps 2-7), K tile rotated (warps 6, 7)
   uint32_t tmem_base;
-  SummScratch<D> summ;  // fused summaries' exchange buffers
+  std::conditional_t<FS, SummScratch<D>, NoSumm> summ;  // fused summaries' exchange buffers (FS only)
   int ticket;           // fused: the CTA's query tile ticket and the launch epoch
   uint32_t epoch;
 };
@@ -686,7 +688,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   constexpr bool FUSED = FC != 0;
   static_assert(!(FC && RP), "in-kernel summaries and in-kernel RoPE are separate variants");
   extern __shared__ uint8_t smem_raw[];
-  using SM = Smem<D, NSTAGE>;
+  using SM = Smem<D, NSTAGE, FC != 0>;
   constexpr int NSK = SM::NSK, NSV = SM::NSV;
   if constexpr (SM::PAD == 0) {
     if ((reinterpret_cast<uintptr_t>(smem_raw) & 1023) != 0) __trap();
@@ -1173,7 +1175,7 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
   if (!ok) return cudaErrorInvalidValue;
   using K_t = decltype(&prefill_sm100_kernel<D, NSTAGE, TRACE, SMX, FC, RP>);
   K_t kern = prefill_sm100_kernel<D, NSTAGE, TRACE, SMX, FC, RP>;
-  const size_t smem = sizeof(Smem<D, NSTAGE>) + Smem<D, NSTAGE>::PAD;
+  const size_t smem = sizeof(Smem<D, NSTAGE, FUSED>) + Smem<D, NSTAGE, FUSED>::PAD;
   {
     cudaError_t e = set_smem_attr((const void*)kern, smem);
     if (e != cudaSuccess) return e;
