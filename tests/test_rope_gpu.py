@@ -203,6 +203,7 @@ def test_rope_ex_validation(eva):
     (2, 1, 1000, 128, 32, 96, 32, "interleaved", 1),
     (1, 2, 640, 64, 16, 64, 32, "neox", 1),
     (1, 1, 100, 64, 64, 128, 64, "interleaved", 0),
+    (1, 3, 40, 128, 64, 128, 128, "neox", 0),      # T < C: no summaries, one partial tile
 ])
 def test_prefill_rope_in_kernel_parity(eva, B, H, T, d, C, W, rd, style, mode):
     base = 10000.0
