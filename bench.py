@@ -451,7 +451,12 @@ def bench_prefill_large(args, eva, torch, dev, s, rank, world, peaks):
         "step_two_pass_ms": timed(lambda: (eva.eva_rope_summarize(cfg, Q, K, V),
                                            eva.eva_attn_prefill(cfg, Qr, Kr, V, Ksum=rks, Vsum=rvs,
                                                                 summaries_provided=True, O=O, lse=lse))),
-        "note": "rotary_dim = d, interleaved, base 10000; step = summaries of the rotated keys + prefill"}
+        "step_k_prerotated_ms": timed(lambda: (eva.eva_rope(cfg, K, out=Kr),
+                                               eva.eva_attn_prefill_rope(cfg, Q, Kr, V, Ksum=rks, Vsum=rvs, O=O,
+                                                                         lse=lse, k_rotated=True))),
+        "note": "rotary_dim = d, interleaved, base 10000; step = summaries of the rotated keys + prefill; "
+                "k_prerotated = eva_rope writes RoPE(K) once, the plain summariser on it, the prefill "
+                "rotating Q only (EVA_ROPE_K_ROTATED)"}
     del Q, K, V, O, ks, vs, Qr, Kr, rks, rvs
     torch.cuda.empty_cache()
     return out

@@ -238,6 +238,7 @@ eva_status eva_attn_prefill(const eva_config* cfg, const void* Q, const void* K,
  * eva_attn_prefill into a CUDA graph; synchronises `stream` if an existing buffer is replaced. */
 eva_status eva_prefill_reserve(const eva_config* cfg, eva_stream_t stream);
 
+#define EVA_ROPE_K_ROTATED 512u
 /* eva_attn_prefill_rope: eva_attn_prefill on RoPE(Q), RoPE(K) with the rotation done INSIDE the
  * tensor-core kernel ("RoPE is applied to all tokens prior to
  * the random feature projections"; readings R18/R19): Q and K [bh_count, T, d] are the caller's
@@ -248,6 +249,12 @@ eva_status eva_prefill_reserve(const eva_config* cfg, eva_stream_t stream);
  *                                   summaries-only form (Ksum/Vsum written, out);
  *   EVA_SUMMARIES_PROVIDED       -- Ksum/Vsum already hold them (in), e.g. from
  *                                   eva_rope_summarize_ex or a decode cache.
+ *   EVA_ROPE_K_ROTATED           -- K (and Ksum/Vsum when provided) hold ROTATED keys already
+ *                                   (e.g. eva_rope_ex's output, kept for the decode cache); the
+ *                                   kernel rotates Q only, and missing summaries come from the
+ *                                   plain eva_summarize on K.  The fastest RoPE prefill when the
+ *                                   rotated keys are stored anyway (one rotation per key instead
+ *                                   of one per query tile that reads it).
  * O (out) and lse (out, may be NULL) as in eva_attn_prefill.  The result equals eva_attn_prefill
  * on eva_rope_ex's outputs up to the rounding of the rotated bf16 values.  Whole-sequence call,
  * every cfg.mode; bf16, d in {64, 128} and rotary_dim (0 = d) a power of two (>= 8 interleaved,

@@ -18,6 +18,7 @@ EVA_F32, EVA_BF16 = 0, 1
 EVA_WINDOW_SLIDING, EVA_WINDOW_BLOCK, EVA_NONCAUSAL = 0, 1, 2
 EVA_OMEGA_AS_PRINTED, EVA_OMEGA_SHIFTED_NOISE = 0, 1
 EVA_SUMMARIES_PROVIDED = 1
+EVA_ROPE_K_ROTATED = 512
 EVA_SUMMARIES_FUSED = 2
 EVA_PREFILL_SIMT = 4
 EVA_SUMMARIES_SEPARATE = 16

@@ -131,10 +131,11 @@ def eva_attn_prefill_rope(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: t
                           style: str = "interleaved", eps: Optional[torch.Tensor] = None,
                           Ksum: Optional[torch.Tensor] = None, Vsum: Optional[torch.Tensor] = None,
                           summaries_provided: bool = False, O: Optional[torch.Tensor] = None,
-                          lse: Optional[torch.Tensor] = None):
+                          lse: Optional[torch.Tensor] = None, k_rotated: bool = False):
     """Prefill on RoPE(Q), RoPE(K) with the rotation inside the tensor-core kernel (NEXT row 4,
-    R18/R19): Q, K un-rotated.  Returns (O, lse, Ksum, Vsum); the summaries are those of the
-    rotated keys (computed first unless summaries_provided)."""
+    R18/R19): Q, K un-rotated (k_rotated: K already rotated, only Q is rotated in the kernel).
+    Returns (O, lse, Ksum, Vsum); the summaries are those of the rotated keys (computed first
+    unless summaries_provided)."""
     dt, bh, T, d = _tdtype(cfg), cfg.bh_count, cfg.T, cfg.d_head
     nC = T // cfg.chunk
     for t, nm in ((Q, "Q"), (K, "K"), (V, "V")):
@@ -151,7 +152,8 @@ def eva_attn_prefill_rope(cfg: EvaConfig, Q: torch.Tensor, K: torch.Tensor, V: t
     rp = _rope_params(rope_base, rotary_dim, style)
     check(lib.eva_attn_prefill_rope(ctypes.byref(cfg), ctypes.byref(rp), _ptr(Q), _ptr(K), _ptr(V), _ptr(eps),
                                     _ptr(Ksum if nC else None), _ptr(Vsum if nC else None), _ptr(O), _ptr(lse),
-                                    N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0, _stream(Q.device)))
+                                    (N.EVA_SUMMARIES_PROVIDED if summaries_provided else 0) |
+                                    (N.EVA_ROPE_K_ROTATED if k_rotated else 0), _stream(Q.device)))
     return O, lse, Ksum, Vsum
 
 

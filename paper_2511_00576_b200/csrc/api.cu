@@ -303,7 +303,9 @@ eva_status eva_attn_prefill_rope(const eva_config* cfg, const eva_rope_params* r
   eva_status st = check_cfg(cfg, true);
   if (st != EVA_OK) return st;
   if ((st = check_rope(cfg, rp, true)) != EVA_OK) return st;
-  if (flags & ~EVA_SUMMARIES_PROVIDED) return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  if (flags & ~(EVA_SUMMARIES_PROVIDED | EVA_ROPE_K_ROTATED))
+    return fail(EVA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+  const bool k_rot = (flags & EVA_ROPE_K_ROTATED) != 0;
   if (cfg->mode == EVA_NONCAUSAL && cfg->T % cfg->chunk != 0)
     return fail(EVA_ERR_INVALID_ARG, "non-causal prefill needs T %% C == 0 (T=%d, C=%d; reading R15)", cfg->T,
                 cfg->chunk);
@@ -325,7 +327,11 @@ eva_status eva_attn_prefill_rope(const eva_config* cfg, const eva_rope_params* r
   if (eps && !aligned16(eps)) return fail(EVA_ERR_INVALID_ARG, "eps is not 16-byte aligned");
   if (lse && !aligned16(lse)) return fail(EVA_ERR_INVALID_ARG, "lse is not 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
-  if (have_sums && !(flags & EVA_SUMMARIES_PROVIDED)) {
+  if (have_sums && !(flags & EVA_SUMMARIES_PROVIDED) && k_rot) {
+    // K holds rotated keys already: the plain summariser gives the summaries of the rotated keys
+    const cudaError_t e = eva::launch_summarize(*cfg, K, V, eps, Ksum, Vsum, s);
+    if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill_rope(summaries)");
+  } else if (have_sums && !(flags & EVA_SUMMARIES_PROVIDED)) {
     // the summaries of the rotated keys, without writing RoPE(Q) / RoPE(K)
     const cudaError_t e = eva::launch_rope_summarize(*cfg, *rp, Q, K, V, eps, nullptr, nullptr, Ksum, Vsum, s);
     if (e == cudaErrorNotSupported)
@@ -334,7 +340,7 @@ eva_status eva_attn_prefill_rope(const eva_config* cfg, const eva_rope_params* r
     if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill_rope(summaries)");
   }
   return cuda_status(eva::launch_prefill_sm100_rope(*cfg, std::log2((double)rp->base), rp->rotary_dim, rp->style,
-                                                    Q, K, V, Ksum, Vsum, O, lse, s),
+                                                    Q, K, V, Ksum, Vsum, O, lse, s, k_rot),
                      "eva_attn_prefill_rope");
 }
 

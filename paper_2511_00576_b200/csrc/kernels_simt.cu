@@ -189,20 +189,98 @@ __device__ __forceinline__ void rope_row_item(const T* src, T* dst, int64_t pos,
   }
 }
 
-// RoPE of rows [bh, T, D] (or its inverse): row t of unit u at position (pos ? pos[u] : pos0) + t.
+
+// eva_rope_ex's kernel: thread (row block, item) walks RB consecutive rows of one item (an
+// interleaved piece, a half-split piece pair or a pass-through piece).  The angles of the first
+// row of the block (and of the first row of a new unit) come from rope_cs (double reduction);
+// every next row multiplies by e^{i theta_j} -- a few fp32 FMAs per pair instead of a double
+// reduction and sin/cos per element, so the kernel streams at HBM rate.
+constexpr int ROPE_RB = 16;
 template <typename T, int D>
-__global__ void __launch_bounds__(256) rope_kernel(const T* __restrict__ X, T* __restrict__ Y, int64_t rows,
-                                                   int T_, int64_t pos0, const int64_t* __restrict__ pos,
-                                                   const __grid_constant__ RopeSpec rs) {
+__global__ void __launch_bounds__(256) rope_walk_kernel(const T* __restrict__ X, T* __restrict__ Y, int64_t rows,
+                                                        int T_, int64_t pos0, const int64_t* __restrict__ pos,
+                                                        const __grid_constant__ RopeSpec rs) {
   pdl_wait();
   pdl_trigger();
-  const int per = rope_items<T, D>(rs);
+  constexpr int VEC = 16 / sizeof(T);
+  const bool neox = rs.style == EVA_ROPE_NEOX;
+  const int nrot = neox ? rs.rd / (2 * VEC) : rs.rd / VEC;
+  const int per = nrot + (D - rs.rd) / VEC;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= rows * per) return;
-  const int64_t row = i / per;
   const int it = (int)(i % per);
-  const int64_t p = (pos ? pos[row / T_] : pos0) + row % T_;
-  rope_row_item<T, D>(X + row * D, Y + row * D, p, it, rs);
+  const int64_t r0 = (i / per) * ROPE_RB;
+  if (r0 >= rows) return;
+  const int64_t r1 = min(rows, r0 + ROPE_RB);
+  if (it >= nrot) {  // pass-through piece
+    if (X == Y) return;
+    const int ch0 = rs.rd + (it - nrot) * VEC;
+    for (int64_t r = r0; r < r1; ++r)
+      *reinterpret_cast<uint4*>(Y + r * D + ch0) = ldg16_stream(X + r * D + ch0);
+    return;
+  }
+  const int np = neox ? VEC : VEC / 2;                  // pairs of this item
+  const int j0 = neox ? it * VEC : it * (VEC / 2);      // first pair index
+  const int cha = neox ? it * VEC : it * VEC, chb = cha + rs.rd / 2;
+  float c[VEC], sn[VEC], sc[VEC], ss[VEC];
+#pragma unroll
+  for (int q = 0; q < VEC; ++q)
+    if (q < np) rope_cs(1, j0 + q, rs, sc[q], ss[q]);  // one-row step (sign included)
+  // 4 rows per batch: their loads are issued before any store (the call may run in place, but a
+  // thread only ever writes the pieces it has read)
+  constexpr int NB = 4;
+  for (int64_t rb = r0; rb < r1; rb += NB) {
+    uint4 xa[NB], xb[NB];
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      if (rb + k < r1) {
+        xa[k] = ldg16_stream(X + (rb + k) * D + cha);
+        if (neox) xb[k] = ldg16_stream(X + (rb + k) * D + chb);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const int64_t r = rb + k;
+      if (r >= r1) break;
+      const int64_t u = r / T_, t = r - u * T_;
+      if (r == r0 || t == 0) {
+        const int64_t p = (pos ? pos[u] : pos0) + t;
+#pragma unroll
+        for (int q = 0; q < VEC; ++q)
+          if (q < np) rope_cs(p, j0 + q, rs, c[q], sn[q]);
+      }
+      if (neox) {
+        float va[VEC], vb[VEC];
+        unpack16<T>(xa[k], va);
+        unpack16<T>(xb[k], vb);
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) {
+          const float x0 = va[q], x1 = vb[q];
+          va[q] = x0 * c[q] - x1 * sn[q];
+          vb[q] = x0 * sn[q] + x1 * c[q];
+        }
+        *reinterpret_cast<uint4*>(Y + r * D + cha) = pack16<T>(va);
+        *reinterpret_cast<uint4*>(Y + r * D + chb) = pack16<T>(vb);
+      } else {
+        float v[VEC];
+        unpack16<T>(xa[k], v);
+#pragma unroll
+        for (int q = 0; q < VEC / 2; ++q) {
+          const float x0 = v[2 * q], x1 = v[2 * q + 1];
+          v[2 * q] = x0 * c[q] - x1 * sn[q];
+          v[2 * q + 1] = x0 * sn[q] + x1 * c[q];
+        }
+        *reinterpret_cast<uint4*>(Y + r * D + cha) = pack16<T>(v);
+      }
+#pragma unroll
+      for (int q = 0; q < VEC; ++q) {
+        if (q < np) {
+          const float cn = c[q] * sc[q] - sn[q] * ss[q];
+          sn[q] = sn[q] * sc[q] + c[q] * ss[q];
+          c[q] = cn;
+        }
+      }
+    }
+  }
 }
 
 // The key transform of the fused producer: rotate the piece (row r of the chunk, channels ch0)
@@ -1057,9 +1135,9 @@ cudaError_t launch_rope(const eva_config& cfg, const eva_rope_params& rp, const 
   EVA_DISPATCH_T(cfg.dtype, EVA_DISPATCH_D(cfg.d_head, {
     constexpr int VEC = 16 / (int)sizeof(T);
     const int per = (rs.style == EVA_ROPE_NEOX ? rd / (2 * VEC) : rd / VEC) + (D - rd) / VEC;
-    const int64_t n = rows * per;
-    err = launch_pdl(rope_kernel<T, D>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, (const T*)X, (T*)Y,
-                     rows, cfg.T, pos0, pos, rs);
+    const int64_t n = (rows + ROPE_RB - 1) / ROPE_RB * per;
+    err = launch_pdl(rope_walk_kernel<T, D>, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, (const T*)X,
+                     (T*)Y, rows, cfg.T, pos0, pos, rs);
     if (err != cudaSuccess) return err;
   }));
   note_launch();

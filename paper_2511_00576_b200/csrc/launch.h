@@ -78,7 +78,8 @@ cudaError_t prefill_fused_reserve(const eva_config& cfg, cudaStream_t s);
 bool prefill_rope_supported(const eva_config& cfg, int rotary_dim, int style);
 cudaError_t launch_prefill_sm100_rope(const eva_config& cfg, double log2_base, int rotary_dim, int style,
                                       const void* Q, const void* K, const void* V, const void* Ksum,
-                                      const void* Vsum, void* O, float* lse, cudaStream_t s);
+                                      const void* Vsum, void* O, float* lse, cudaStream_t s,
+                                      bool k_rotated = false);
 
 cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K, const void* V,
                              const void* Ksum, const void* Vsum, void* O, float* lse,

@@ -677,8 +677,14 @@ __device__ __forceinline__ bool owns_chunks(const Plan& plan, int j, int C, int 
 // FC = 0: summaries provided (or computed by a separate launch); FC = C in {16, 32, 64}: the
 // chunk summaries are computed in-kernel (one instantiation per chunk size keeps the code that
 // the instruction cache has to hold small)
+// RP: in-kernel RoPE -- 0 none; 1 / 2 Q and the local K tiles (interleaved / half-split pairs);
+// 3 / 4 Q only, the keys (and their summaries) come in rotated (EVA_ROPE_K_ROTATED).
+constexpr int rope_style(int rp) { return rp == 0 ? 0 : (rp - 1) % 2 + 1; }
+constexpr bool rope_k(int rp) { return rp == 1 || rp == 2; }
+constexpr int prefill_threads(int fc, int rp) { return rope_k(rp) ? NTHREADS_R : fc ? NTHREADS_F : NTHREADS; }
+
 template <int D, int NSTAGE, bool TRACE = false, int SMX = -1, int FC = 0, int RP = 0>
-__global__ void __launch_bounds__(RP ? NTHREADS_R : FC ? NTHREADS_F : NTHREADS, 2)
+__global__ void __launch_bounds__(prefill_threads(FC, RP), 2)
 prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mKs,
                      const __grid_constant__ CUtensorMap mVs, const __grid_constant__ CUtensorMap mO,
@@ -687,6 +693,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
                      const __grid_constant__ FusedArgs fa, const __grid_constant__ RopeArgs ra) {
   constexpr bool FUSED = FC != 0;
   static_assert(!(FC && RP), "in-kernel summaries and in-kernel RoPE are separate variants");
+  constexpr int RSTY = rope_style(RP);  // RopeWalker style
+  constexpr bool RK = rope_k(RP);       // the local K tiles are rotated here too
   extern __shared__ uint8_t smem_raw[];
   using SM = Smem<D, NSTAGE, FC != 0>;
   constexpr int NSK = SM::NSK, NSV = SM::NSV;
@@ -740,7 +748,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     mbar_init(&sm->o_done, 1);
     mbar_init(&sm->o_final, 1);
     if constexpr (RP != 0) {
-      mbar_init(&sm->q_rot, NTHREADS_R - 64);
+      mbar_init(&sm->q_rot, prefill_threads(FC, RP) - 64);
       for (int s = 0; s < NSK; ++s) mbar_init(&sm->k_rot[s], 32 * ROPE_WARPS);
     }
     fence_mbar_init();
@@ -786,8 +794,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     // in-kernel RoPE of the Q tile by the softmax and rope warps (idle until S(0) anyway)
     if (warp >= 2) {
       mbar_wait(&sm->q_full, 0);
-      RopeWalker<RP> rw;
-      rw.init(ra, (int)threadIdx.x - 64, NTHREADS_R - 64);
+      RopeWalker<RSTY> rw;
+      rw.init(ra, (int)threadIdx.x - 64, prefill_threads(FC, RP) - 64);
       rw.run(reinterpret_cast<uint8_t*>(sm->q), BM, plan.n0);
       fence_proxy_async_smem();  // generic-proxy writes -> the MMA's async-proxy reads
       mbar_arrive(&sm->q_rot);
@@ -910,7 +918,7 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     for (int j = 0; j <= NT; ++j) {
       if (j < NT) {
         const int s = j % NSK;
-        mbar_wait(RP ? &sm->k_rot[s] : &sm->k_full[s], (j / NSK) & 1);
+        mbar_wait(RK ? &sm->k_rot[s] : &sm->k_full[s], (j / NSK) & 1);
         if (lane == 0) tt<TRACE>(tl, 1, 3, j);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sm->k[s]);
@@ -1030,8 +1038,8 @@ prefill_sm100_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     // ------------------------------------------------------------ summary warps (fused)
     if constexpr (FUSED) fused_summaries<D, FC, TRACE>(sm, plan, fa, u, qt, epoch, tl);
     // ------------------------------------------------------------ rope warps (in-kernel RoPE)
-    if constexpr (RP != 0) {
-      RopeWalker<RP> rw;
+    if constexpr (RK) {
+      RopeWalker<RSTY> rw;
       rw.init(ra, (int)threadIdx.x - NTHREADS, 32 * ROPE_WARPS);
       for (int j = 0; j < NT; ++j) {
         const int s = j % NSK;
@@ -1208,7 +1216,7 @@ cudaError_t launch_t(const eva_config& cfg, const PrefillRange& rg, const void* 
   }
   const float scale_log2 = cfg.scale * 1.4426950408889634f;
   const RopeArgs ra = rap ? *rap : RopeArgs{};
-  cudaError_t e = launch_pdl(kern, grid, dim3(RP ? NTHREADS_R : FUSED ? NTHREADS_F : NTHREADS), smem, s, mQ, mK, mV,
+  cudaError_t e = launch_pdl(kern, grid, dim3(prefill_threads(FC, RP)), smem, s, mQ, mK, mV,
                              mKs, mVs, mO, rg, cfg.chunk, cfg.window, cfg.mode, scale_log2,
                              cfg.summary_bias * 1.4426950408889634f, lse, overlap ? 1 : 0, tile_sum_first(), fa,
                              ra);
@@ -1307,7 +1315,7 @@ bool prefill_rope_supported(const eva_config& cfg, int rotary_dim, int style) {
 
 cudaError_t launch_prefill_sm100_rope(const eva_config& cfg, double log2_base, int rotary_dim, int style,
                                       const void* Q, const void* K, const void* V, const void* Ksum,
-                                      const void* Vsum, void* O, float* lse, cudaStream_t s) {
+                                      const void* Vsum, void* O, float* lse, cudaStream_t s, bool k_rotated) {
   if (cfg.bh_count == 0) return cudaSuccess;
   if (!prefill_rope_supported(cfg, rotary_dim, style)) return cudaErrorNotSupported;
   const PrefillRange rg = full_range(cfg);
@@ -1315,11 +1323,17 @@ cudaError_t launch_prefill_sm100_rope(const eva_config& cfg, double log2_base, i
   ra.rd = rotary_dim ? rotary_dim : cfg.d_head;
   for (int j = 0; j < ra.rd / 2; ++j) ra.th[j] = std::exp2(log2_base * (-2.0 * (double)j / (double)ra.rd));
   const bool neox = style == EVA_ROPE_NEOX;
-  if (cfg.d_head == 128)
-    return neox ? launch_t<128, 2, false, 0, 0, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra)
-                : launch_t<128, 2, false, 0, 0, 1>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra);
-  return neox ? launch_t<64, 3, false, 0, 0, 2>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra)
-              : launch_t<64, 3, false, 0, 0, 1>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra);
+#define EVA_ROPE_LAUNCH(D_, NS_, RP_) \
+  return launch_t<D_, NS_, false, 0, 0, RP_>(cfg, rg, Q, K, V, Ksum, Vsum, O, lse, s, false, nullptr, &ra)
+  if (cfg.d_head == 128) {
+    if (k_rotated) { if (neox) EVA_ROPE_LAUNCH(128, 2, 4); EVA_ROPE_LAUNCH(128, 2, 3); }
+    if (neox) EVA_ROPE_LAUNCH(128, 2, 2);
+    EVA_ROPE_LAUNCH(128, 2, 1);
+  }
+  if (k_rotated) { if (neox) EVA_ROPE_LAUNCH(64, 3, 4); EVA_ROPE_LAUNCH(64, 3, 3); }
+  if (neox) EVA_ROPE_LAUNCH(64, 3, 2);
+  EVA_ROPE_LAUNCH(64, 3, 1);
+#undef EVA_ROPE_LAUNCH
 }
 
 cudaError_t prefill_fused_reserve(const eva_config& cfg, cudaStream_t s) {

@@ -320,3 +320,33 @@ def test_ragged_rope_ignores_two_launch_switch():
         assert r.returncode == 0, r.stderr[-2000:]
     a, b = torch.load("/tmp/eva_rr_0.pt"), torch.load("/tmp/eva_rr_1.pt")
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("d,rd,style,mode", [(128, 128, "interleaved", "sliding"), (64, 32, "neox", "block"),
+                                             (128, 64, "neox", "noncausal")])
+def test_prefill_rope_k_prerotated(eva, d, rd, style, mode):
+    """EVA_ROPE_K_ROTATED: K comes in rotated (eva_rope's output), the kernel rotates Q only and
+    the summaries are the plain summariser's on the rotated keys.  Against the oracle on the
+    bf16-stored rotated inputs, and against the full in-kernel path."""
+    B, H, T, C, W = 1, 2, 768, 64, 128
+    m = {"sliding": 0, "block": 1, "noncausal": 2}[mode]
+    cfg = eva.make_config(B, H, T, d, C, W, seed=33, mode=mode)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=34, device="cuda")
+    Kr = eva.eva_rope(cfg, K, rotary_dim=rd, style=style)
+    O, lse, ks, vs = eva.eva_attn_prefill_rope(cfg, Q, Kr, V, rotary_dim=rd, style=style, k_rotated=True)
+    O2, lse2, ks2, vs2 = eva.eva_attn_prefill_rope(cfg, Q, K, V, rotary_dim=rd, style=style)
+    torch.cuda.synchronize()
+    assert (O.float() - O2.float()).abs().max().item() <= 2e-2
+    assert (ks.float() - ks2.float()).abs().max().item() <= 2e-2
+    st = oracle.ROPE_NEOX if style == "neox" else oracle.ROPE_INTERLEAVED
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, B * H, T // C, d)
+    p = np.arange(T)
+    rq = np.stack([torch.from_numpy(oracle.rope_ex(f64(Q[u]), p, rotary_dim=rd, style=st))
+                   .to(torch.bfloat16).double().numpy() for u in range(B * H)])
+    rk = np.stack([torch.from_numpy(oracle.rope_ex(f64(K[u]), p, rotary_dim=rd, style=st))
+                   .to(torch.bfloat16).double().numpy() for u in range(B * H)])
+    sk, sv = oracle.summarize_batch(rk, f64(V), E, C)
+    assert np.max(np.abs(f64(ks) - sk)) <= 2e-2
+    ro, rl = oracle.prefill_ext_batch(rq, rk, f64(V), f64(ks), f64(vs), C, W, m, cfg.scale)
+    assert np.max(np.abs(f64(O) - ro)) <= 2e-2
+    assert np.max(np.abs(f64(lse) - rl)) <= 2e-2
