@@ -102,16 +102,23 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
   }
   constexpr int NI = summ_reg_ni<__nv_bfloat16, D>(CC);
   auto rowK_of = [](const __nv_bfloat16* base) { return [base](int r) { return base + (size_t)r * D; }; };
+  // The chunk's random draws (Eq.15, reading R9) do not depend on its data: generated into shared
+  // memory while its bulk copy is in flight (the summariser then reads them like caller eps).
+  __shared__ __align__(16) float eps_s[D];
   int k = 0;
   for (int i = blockIdx.x; i < total; i += gridDim.x, ++k) {
     const int s = k % NST;
     const int u = i / nC, c = i % nC;
+    if (!eps && t < D / 4) {
+      const float4 z = philox_normal4(cfg.seed, cfg.layer, (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), (uint32_t)t);
+      *reinterpret_cast<float4*>(&eps_s[4 * t]) = z;
+    }
     mbar_wait(&sm.full[s], (k / NST) & 1);
     const __nv_bfloat16* Ks = sm.k[s];
     const __nv_bfloat16* Vs = sm.v[s];
     summarize_chunk_reg<__nv_bfloat16, D, NI, decltype(rowK_of(Ks)), decltype(rowK_of(Vs)), NoKXform, LdShared, true>(
         rowK_of(Ks), rowK_of(Vs), CC,
-        eps ? eps + ((size_t)u * nC + c) * D : nullptr, (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
+        eps ? eps + ((size_t)u * nC + c) * D : eps_s, (uint32_t)(cfg.bh_begin + u), (uint32_t)(c0 + c), cfg,
         Ksum + ((size_t)u * nC + c) * D, Vsum + ((size_t)u * nC + c) * D, nullptr, NoKXform(), LdShared());
     __syncthreads();  // every thread is done with stage s
     if (t == 0) {     // the chunk NST iterations ahead streams into it now
