@@ -332,8 +332,11 @@ eva_status eva_attn_prefill_rope(const eva_config* cfg, const eva_rope_params* r
     const cudaError_t e = eva::launch_summarize(*cfg, K, V, eps, Ksum, Vsum, s);
     if (e != cudaSuccess) return cuda_status(e, "eva_attn_prefill_rope(summaries)");
   } else if (have_sums && !(flags & EVA_SUMMARIES_PROVIDED)) {
-    // the summaries of the rotated keys, without writing RoPE(Q) / RoPE(K)
-    const cudaError_t e = eva::launch_rope_summarize(*cfg, *rp, Q, K, V, eps, nullptr, nullptr, Ksum, Vsum, s);
+    // the summaries of the rotated keys, without writing RoPE(Q) / RoPE(K): the bulk summariser
+    // rotating the landed key rows, else the register RoPE summariser
+    cudaError_t e = eva::launch_summarize_bulk_rope(*cfg, *rp, K, V, eps, Ksum, Vsum, s);
+    if (e == cudaErrorNotSupported)
+      e = eva::launch_rope_summarize(*cfg, *rp, Q, K, V, eps, nullptr, nullptr, Ksum, Vsum, s);
     if (e == cudaErrorNotSupported)
       return fail(EVA_ERR_UNSUPPORTED, "eva_attn_prefill_rope: chunk=%d too long for the register summariser",
                   cfg->chunk);

