@@ -1236,13 +1236,19 @@ bool make_tma_map_bf16(CUtensorMap* m, const void* base, int units, int rows, in
 cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K, const void* V,
                              const void* Ksum, const void* Vsum, void* O, float* lse,
                              unsigned long long* trace_dev, bool fused, cudaStream_t s) {
-  cudaError_t e = cudaMemcpyToSymbolAsync(g_trace2, &trace_dev, sizeof(trace_dev), 0, cudaMemcpyHostToDevice, s);
+  // Under stream capture the symbols keep the values an eager call set (a captured copy from a
+  // host stack variable would read a dead address at replay).
+  cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(s, &cap_st);
+  if (e != cudaSuccess) return e;
+  const bool capturing = cap_st != cudaStreamCaptureStatusNone;
+  if (!capturing) e = cudaMemcpyToSymbolAsync(g_trace2, &trace_dev, sizeof(trace_dev), 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
   static const int mid = [] {
     const char* v = getenv("EVA_TRACE_MID");
     return v ? atoi(v) : 150;
   }();
-  e = cudaMemcpyToSymbolAsync(g_trace_mid, &mid, sizeof(mid), 0, cudaMemcpyHostToDevice, s);
+  if (!capturing) e = cudaMemcpyToSymbolAsync(g_trace_mid, &mid, sizeof(mid), 0, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;
   const PrefillRange rg = full_range(cfg);
   if (fused) {  // traced for C = 64 (the configs' chunk size)
@@ -1253,9 +1259,14 @@ cudaError_t debug_trace_tile(const eva_config& cfg, const void* Q, const void* K
   }
   // EVA_TRACE_OVERLAP=1: the traced summarize kernel (CTA spans at trace[8960 + 2 i]) and then the
   // traced prefill in EVA_PREFILL_OVERLAP mode, as the step launches them
-  static const bool ovl = getenv("EVA_TRACE_OVERLAP") != nullptr;
-  if (ovl) {
-    e = debug_set_summ_trace(trace_dev + TT_SLOTS * TT_ROLES * TT_PER_ROLE + 2 * TT_MAX_CTAS, s);
+  // (EVA_TRACE_OVERLAP=2: the same pair with the prefill NOT in overlap mode)
+  static const int ovl_mode = [] {
+    const char* v = getenv("EVA_TRACE_OVERLAP");
+    return v ? atoi(v) : 0;
+  }();
+  const bool ovl = ovl_mode == 1;
+  if (ovl_mode) {
+    if (!capturing) e = debug_set_summ_trace(trace_dev + TT_SLOTS * TT_ROLES * TT_PER_ROLE + 2 * TT_MAX_CTAS, s);
     if (e != cudaSuccess) return e;
     e = launch_summarize_bulk(cfg, K, V, nullptr, const_cast<void*>(Ksum), const_cast<void*>(Vsum), 0, s);
     if (e != cudaSuccess) return e;

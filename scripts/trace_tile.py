@@ -20,10 +20,24 @@ tr = torch.zeros(4 * R * 48 + 4 * NCTA, dtype=torch.int64, device="cuda")
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 flush = torch.empty(512 << 18, device="cuda")
-for _ in range(3):
+GRAPH = os.environ.get("GRAPH") == "1"   # replay the traced launch(es) from a CUDA graph
+if GRAPH:
+    N.check(N.lib.eva_debug_trace_prefill(ctypes.byref(cfg), P(Q), P(K), P(V), P(ks), P(vs), P(O), P(lse), P(tr), 2 if FUSED else 1000, st))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        stc = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        N.check(N.lib.eva_debug_trace_prefill(ctypes.byref(cfg), P(Q), P(K), P(V), P(ks), P(vs), P(O), P(lse), P(tr), 2 if FUSED else 1000, stc))
+    for _ in range(3):
+        flush.zero_()
+        tr.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+else:
+  for _ in range(3):
     flush.zero_()
     N.check(N.lib.eva_debug_trace_prefill(ctypes.byref(cfg), P(Q), P(K), P(V), P(ks), P(vs), P(O), P(lse), P(tr), 2 if FUSED else 1000, st))
-torch.cuda.synchronize()
+  torch.cuda.synchronize()
 names = {1: "start", 2: "MMA: Q arrived", 3: "MMA: K(j) arrived", 4: "MMA: S(j) issued", 5: "MMA: P(j) seen",
          6: "MMA: PV(j) issued", 7: "SM: got S(j)", 8: "SM: P(j) done", 9: "EPI: O final", 10: "EPI: stored",
          11: "TMA: slot free(j)", 12: "TMA: issued(j)", 13: "SUM: tile j landed", 14: "SUM: tile j done",
