@@ -255,6 +255,9 @@ eva_status eva_prefill_reserve(const eva_config* cfg, eva_stream_t stream);
  *                                   plain eva_summarize on K.  The fastest RoPE prefill when the
  *                                   rotated keys are stored anyway (one rotation per key instead
  *                                   of one per query tile that reads it).
+ * Decode hand-off: the cache holds ROTATED keys (eva_decode_step_ragged_rope appends rotated
+ * ones), so eva_cache_load takes RoPE(K) -- eva_rope_ex's output, which the EVA_ROPE_K_ROTATED
+ * form has at hand -- with these Ksum/Vsum.
  * O (out) and lse (out, may be NULL) as in eva_attn_prefill.  The result equals eva_attn_prefill
  * on eva_rope_ex's outputs up to the rounding of the rotated bf16 values.  Whole-sequence call,
  * every cfg.mode; bf16, d in {64, 128} and rotary_dim (0 = d) a power of two (>= 8 interleaved,

@@ -354,3 +354,49 @@ def test_prefill_rope_k_prerotated(eva, d, rd, style, mode):
     ro, rl = oracle.prefill_ext_batch(rq, rk, f64(V), f64(ks), f64(vs), C, W, m, cfg.scale)
     assert np.max(np.abs(f64(O) - ro)) <= 2e-2
     assert np.max(np.abs(f64(lse) - rl)) <= 2e-2
+
+
+@pytest.mark.parametrize("style", ["interleaved", "neox"])
+def test_rope_prefill_to_decode_handoff(eva, style):
+    """The RoPE serving path end to end: RoPE(K) once (eva_rope), the prefill rotating Q only
+    (EVA_ROPE_K_ROTATED), the cache loaded with the rotated keys and the prefill's summaries, then
+    decode tokens with RoPE folded into the ragged step -- against the oracle's streaming cache on
+    the bf16-stored rotated keys (R18) and the fp64-rotated queries."""
+    B, H, T, d, C, W, rd = 1, 2, 300, 64, 16, 64, 32
+    BH, steps = B * H, 20
+    cfg = eva.make_config(B, H, T, d, C, W, seed=41)
+    Q, K, V = eva_inputs.qkv(0, BH, T, d, torch.bfloat16, seed=42, device="cuda")
+    Kr = eva.eva_rope(cfg, K, rotary_dim=rd, style=style)
+    O, lse, ks, vs = eva.eva_attn_prefill_rope(cfg, Q, Kr, V, rotary_dim=rd, style=style, k_rotated=True)
+    cap = (T + steps) // C + 1
+    cache = eva.DecodeCache(cfg, cap, device="cuda")
+    cache.eva_cache_load(Kr, V, ks, vs)
+    q, k, v = eva_inputs.decode_tokens(0, BH, steps, d, torch.bfloat16, seed=43, device="cuda")
+    pos = torch.full((BH,), T, dtype=torch.int64, device="cuda")
+    outs = []
+    for i in range(steps):
+        o, l = cache.eva_decode_step_ragged(pos, q[i], k[i], v[i], rope=dict(rotary_dim=rd, style=style))
+        outs.append((o.clone(), l.clone()))
+    torch.cuda.synchronize()
+    st = oracle.ROPE_NEOX if style == "neox" else oracle.ROPE_INTERLEAVED
+    E = oracle.eps_units(cfg.seed, cfg.layer, 0, BH, cap + 1, d)
+    worst = 0.0
+    for u in range(BH):
+        orc = oracle.Cache(d, C, W, oracle.SLIDING, cap=cap, scale=cfg.scale)
+        rk = torch.from_numpy(oracle.rope_ex(f64(K[u]), np.arange(T), rotary_dim=rd, style=st)).to(torch.bfloat16)
+        rk = rk.double().numpy()
+        for t in range(T):
+            assert orc.append(rk[t], f64(V[u, t]), E[u, t // C]) == 0
+        # the prefill's last row equals the streaming cache's decode at position T - 1
+        rq_last = oracle.rope_ex(f64(Q[u, T - 1])[None], [T - 1], rotary_dim=rd, style=st)
+        rq_last = torch.from_numpy(rq_last).to(torch.bfloat16).double().numpy()[0]
+        ro, _ = orc.decode(rq_last)
+        worst = max(worst, np.max(np.abs(f64(O[u, T - 1]) - ro)))
+        for i in range(steps):
+            kt = torch.from_numpy(oracle.rope_ex(f64(k[i, u])[None], [T + i], rotary_dim=rd, style=st)).to(torch.bfloat16)
+            qt = oracle.rope_ex(f64(q[i, u])[None], [T + i], rotary_dim=rd, style=st)[0]
+            assert orc.append(kt.double().numpy()[0], f64(v[i, u]), E[u, (T + i) // C]) == 0
+            ro, rl = orc.decode(qt)
+            worst = max(worst, np.max(np.abs(f64(outs[i][0][u]) - ro)), abs(float(outs[i][1][u]) - rl))
+    assert worst <= 2e-2, worst
+    assert pos.tolist() == [T + steps] * BH
