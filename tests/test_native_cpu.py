@@ -228,3 +228,31 @@ def test_noncausal_and_bias_validation(N):
     cfg.summary_bias = 0.0
     cfg.reserved = 1
     assert N.lib.eva_summarize(ctypes.byref(cfg), P, P, None, P, P, None) == N.EVA_ERR_INVALID_ARG
+
+
+def test_rope_entry_points_validate_before_any_launch(N):
+    """eva_attn_prefill_rope / eva_decode_step_ragged_rope: the RoPE parameters and flags are
+    checked synchronously (nothing is enqueued; no GPU needed for these paths)."""
+    cfg = _cfg(N, dtype=N.EVA_BF16, d_head=64)
+    good = N.EvaRopeParams(10000.0, 0, N.EVA_ROPE_INTERLEAVED, 0)
+    args = (FAKE, FAKE, FAKE, None, FAKE, FAKE, FAKE, None)
+    for rp in (N.EvaRopeParams(0.5, 0, 0, 0), N.EvaRopeParams(float("inf"), 0, 0, 0),
+               N.EvaRopeParams(10000.0, 0, 7, 0), N.EvaRopeParams(10000.0, 0, 0, 1),
+               N.EvaRopeParams(10000.0, 24, 0, 0), N.EvaRopeParams(10000.0, 80, 0, 0)):
+        st = N.lib.eva_attn_prefill_rope(ctypes.byref(cfg), ctypes.byref(rp), *args, 0, None)
+        assert st == N.EVA_ERR_INVALID_ARG, (rp.base, rp.rotary_dim, rp.style, rp.reserved)
+    # unknown flags (EVA_SUMMARIES_FUSED is not a RoPE prefill flag)
+    st = N.lib.eva_attn_prefill_rope(ctypes.byref(cfg), ctypes.byref(good), *args, 2, None)
+    assert st == N.EVA_ERR_INVALID_ARG and b"flags" in N.lib.eva_last_error()
+    # half-split with rotary_dim / 16 = 3: no butterfly partner
+    st = N.lib.eva_attn_prefill_rope(ctypes.byref(_cfg(N, dtype=N.EVA_BF16, d_head=64)),
+                                     ctypes.byref(N.EvaRopeParams(10000.0, 48, N.EVA_ROPE_NEOX, 0)), *args, 0, None)
+    assert st == N.EVA_ERR_UNSUPPORTED
+    c = _cache(N, 0, 4, dtype=N.EVA_BF16, d_head=64)
+    bad = N.EvaRopeParams(1.0, 0, 0, 0)
+    st = N.lib.eva_decode_step_ragged_rope(ctypes.byref(c), FAKE, ctypes.byref(bad), FAKE, FAKE, FAKE, None,
+                                           FAKE, None, FAKE, 1 << 20, None)
+    assert st == N.EVA_ERR_INVALID_ARG and b"base" in N.lib.eva_last_error()
+    st = N.lib.eva_decode_step_ragged_rope(None, FAKE, ctypes.byref(good), FAKE, FAKE, FAKE, None,
+                                           FAKE, None, FAKE, 1 << 20, None)
+    assert st == N.EVA_ERR_INVALID_ARG
