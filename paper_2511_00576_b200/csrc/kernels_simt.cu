@@ -225,9 +225,9 @@ __global__ void __launch_bounds__(256) rope_walk_kernel(const T* __restrict__ X,
 #pragma unroll
   for (int q = 0; q < VEC; ++q)
     if (q < np) rope_cs(1, j0 + q, rs, sc[q], ss[q]);  // one-row step (sign included)
-  // 4 rows per batch: their loads are issued before any store (the call may run in place, but a
+  // 8 rows per batch: their loads are issued before any store (the call may run in place, but a
   // thread only ever writes the pieces it has read)
-  constexpr int NB = 4;
+  constexpr int NB = 8;
   for (int64_t rb = r0; rb < r1; rb += NB) {
     uint4 xa[NB], xb[NB];
 #pragma unroll
