@@ -568,7 +568,7 @@ __global__ void __launch_bounds__(128) bwd_finalize_kernel(eva_config cfg, const
 // spread over the rows as before) and stored with the mean for dP = sum_c g_c mean_c^T
 // (bwd_dp_kernel): proj_g / proj_mean [bh, nC, d] fp32.
 template <typename T, int D, int NI, bool COEF = false>
-__global__ void __launch_bounds__(128) bwd_finalize_reg_kernel(eva_config cfg, const T* __restrict__ K,
+__global__ void __launch_bounds__(128, COEF ? 5 : 4) bwd_finalize_reg_kernel(eva_config cfg, const T* __restrict__ K,
                                                                const T* __restrict__ V,
                                                                const float* __restrict__ eps, BwdWs ws,
                                                                T* __restrict__ dQ, T* __restrict__ dK,
