@@ -204,6 +204,8 @@ def test_rope_ex_validation(eva):
     (1, 2, 640, 64, 16, 64, 32, "neox", 1),
     (1, 1, 100, 64, 64, 128, 64, "interleaved", 0),
     (1, 3, 40, 128, 64, 128, 128, "neox", 0),      # T < C: no summaries, one partial tile
+    (1, 1, 600, 128, 128, 256, 64, "interleaved", 0),   # C = 128 (the bulk RoPE summariser's largest chunk)
+    (1, 2, 520, 64, 32, 64, 16, "neox", 1),        # rotary_dim 16: one half-split piece pair per row
 ])
 def test_prefill_rope_in_kernel_parity(eva, B, H, T, d, C, W, rd, style, mode):
     base = 10000.0
