@@ -17,7 +17,20 @@ import paper_2511_00576_b200 as eva
 what = sys.argv[1]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 dev = torch.device("cuda:0")
-if what == "prefill_rope_configs2":  # RoPE inside the tcgen05 prefill (eva_attn_prefill_rope)
+if what in ("prefill_ropeq_configs2", "summarize_rope_configs2"):
+    # the Q-only RoPE prefill (EVA_ROPE_K_ROTATED) / the bulk summariser rotating the landed keys
+    B, H, T, d, C, W = 8, 32, 8192, 128, 64, 256
+    cfg = eva.make_config(B, H, T, d, C, W)
+    Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device=dev)
+    Kr = eva.eva_rope(cfg, K)
+    ks, vs = eva.eva_summarize(cfg, Kr, V)
+    O = torch.empty_like(Q)
+    for _ in range(reps):
+        if what == "prefill_ropeq_configs2":
+            eva.eva_attn_prefill_rope(cfg, Q, Kr, V, Ksum=ks, Vsum=vs, summaries_provided=True, O=O, k_rotated=True)
+        else:
+            eva.eva_attn_prefill_rope(cfg, Q, K, V, Ksum=ks, Vsum=vs, O=O)
+elif what == "prefill_rope_configs2":  # RoPE inside the tcgen05 prefill (eva_attn_prefill_rope)
     B, H, T, d, C, W = 8, 32, 8192, 128, 64, 256
     cfg = eva.make_config(B, H, T, d, C, W)
     Q, K, V = eva_inputs.qkv(0, B * H, T, d, torch.bfloat16, seed=0, device=dev)
