@@ -74,67 +74,80 @@ struct BulkRope {
 // pos0 + r.  Thread t takes item t % NI (interleaved: the 16-byte piece `item`, 4 pairs;
 // half-split: pieces item and item + rd/16, 8 pairs) of rows t / NI + k * (128 / NI); the first
 // row's angles in double (reduced mod 2 pi), every next row by the recurrence e^{i step theta_j}.
-template <int D>
-__device__ __forceinline__ void rope_rows(__nv_bfloat16* tile, int C, int64_t pos0, const BulkRope& br, int t) {
-  const bool neox = br.style == EVA_ROPE_NEOX;
-  const int NI = neox ? br.rd / 16 : br.rd / 8;
-  const int item = t % NI, g = t / NI, rstep = SB_THREADS / NI;
-  if (g >= rstep || g >= C) return;
-  const int np = neox ? 8 : 4;
-  float c[8], sn[8], sc[8], ss[8];
-  auto angle = [](double a, float& co, float& si) {
+struct RopeRows {
+  float sc[8], ss[8];  // one row-step rotation per pair (the same for every chunk: set once)
+  int item, g, rstep, np;
+  bool active;
+  __device__ __forceinline__ static void angle(double a, float& co, float& si) {
     a -= 6.283185307179586 * rint(a * 0.15915494309189535);
     __sincosf((float)a, &si, &co);
-  };
+  }
+  __device__ __forceinline__ void init(const BulkRope& br, int t) {
+    const bool neox = br.style == EVA_ROPE_NEOX;
+    const int NI = neox ? br.rd / 16 : br.rd / 8;
+    item = t % NI;
+    g = t / NI;
+    rstep = SB_THREADS / NI;
+    np = neox ? 8 : 4;
+    active = g < rstep;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    if (q < np) {
-      const double th = br.th[np * item + q];
-      angle((double)(pos0 + g) * th, c[q], sn[q]);
-      angle((double)rstep * th, sc[q], ss[q]);
+    for (int q = 0; q < 8; ++q)
+      if (q < np) angle((double)rstep * br.th[np * item + q], sc[q], ss[q]);
+  }
+  // Rotate rows [0, C) of a plain row-major [C][D] bf16 tile in shared memory, row r at
+  // position pos0 + r: thread t takes item t % NI (interleaved: the 16-byte piece `item`, 4
+  // pairs; half-split: pieces item and item + rd/16, 8 pairs) of rows g + k * rstep; the first
+  // row's angles in double (reduced mod 2 pi), every next row by the recurrence.
+  template <int D>
+  __device__ __forceinline__ void run(__nv_bfloat16* tile, int C, int64_t pos0, const BulkRope& br) const {
+    if (!active || g >= C) return;
+    const bool neox = br.style == EVA_ROPE_NEOX;
+    float c[8], sn[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < np) angle((double)(pos0 + g) * br.th[np * item + q], c[q], sn[q]);
+    const int cha = 8 * item, chb = cha + br.rd / 2;
+    for (int r = g; r < C; r += rstep) {
+      uint4* pa = reinterpret_cast<uint4*>(tile + (size_t)r * D + cha);
+      if (neox) {
+        uint4* pb = reinterpret_cast<uint4*>(tile + (size_t)r * D + chb);
+        uint4 xa = *pa, xb = *pb;
+        uint32_t* wa = reinterpret_cast<uint32_t*>(&xa);
+        uint32_t* wb = reinterpret_cast<uint32_t*>(&xb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 a2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wa[q]));
+          const float2 b2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wb[q]));
+          const int i0 = 2 * q, i1 = 2 * q + 1;
+          const __nv_bfloat162 ya = __floats2bfloat162_rn(a2.x * c[i0] - b2.x * sn[i0], a2.y * c[i1] - b2.y * sn[i1]);
+          const __nv_bfloat162 yb = __floats2bfloat162_rn(a2.x * sn[i0] + b2.x * c[i0], a2.y * sn[i1] + b2.y * c[i1]);
+          wa[q] = *reinterpret_cast<const uint32_t*>(&ya);
+          wb[q] = *reinterpret_cast<const uint32_t*>(&yb);
+        }
+        *pa = xa;
+        *pb = xb;
+      } else {
+        uint4 xa = *pa;
+        uint32_t* wa = reinterpret_cast<uint32_t*>(&xa);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 a2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wa[q]));
+          const __nv_bfloat162 y = __floats2bfloat162_rn(a2.x * c[q] - a2.y * sn[q], a2.x * sn[q] + a2.y * c[q]);
+          wa[q] = *reinterpret_cast<const uint32_t*>(&y);
+        }
+        *pa = xa;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < np) {
+          const float cn = c[q] * sc[q] - sn[q] * ss[q];
+          sn[q] = sn[q] * sc[q] + c[q] * ss[q];
+          c[q] = cn;
+        }
+      }
     }
   }
-  const int cha = 8 * item, chb = cha + br.rd / 2;
-  for (int r = g; r < C; r += rstep) {
-    uint4* pa = reinterpret_cast<uint4*>(tile + (size_t)r * D + cha);
-    if (neox) {
-      uint4* pb = reinterpret_cast<uint4*>(tile + (size_t)r * D + chb);
-      uint4 xa = *pa, xb = *pb;
-      uint32_t* wa = reinterpret_cast<uint32_t*>(&xa);
-      uint32_t* wb = reinterpret_cast<uint32_t*>(&xb);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 a2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wa[q]));
-        const float2 b2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wb[q]));
-        const int i0 = 2 * q, i1 = 2 * q + 1;
-        const __nv_bfloat162 ya = __floats2bfloat162_rn(a2.x * c[i0] - b2.x * sn[i0], a2.y * c[i1] - b2.y * sn[i1]);
-        const __nv_bfloat162 yb = __floats2bfloat162_rn(a2.x * sn[i0] + b2.x * c[i0], a2.y * sn[i1] + b2.y * c[i1]);
-        wa[q] = *reinterpret_cast<const uint32_t*>(&ya);
-        wb[q] = *reinterpret_cast<const uint32_t*>(&yb);
-      }
-      *pa = xa;
-      *pb = xb;
-    } else {
-      uint4 xa = *pa;
-      uint32_t* wa = reinterpret_cast<uint32_t*>(&xa);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 a2 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&wa[q]));
-        const __nv_bfloat162 y = __floats2bfloat162_rn(a2.x * c[q] - a2.y * sn[q], a2.x * sn[q] + a2.y * c[q]);
-        wa[q] = *reinterpret_cast<const uint32_t*>(&y);
-      }
-      *pa = xa;
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      if (q < np) {
-        const float cn = c[q] * sc[q] - sn[q] * ss[q];
-        sn[q] = sn[q] * sc[q] + c[q] * ss[q];
-        c[q] = cn;
-      }
-    }
-  }
-}
+};
 
 // debug timeline (eva_debug_trace_prefill with EVA_TRACE_OVERLAP=1): CTA entry / exit globaltimer
 __device__ unsigned long long* g_sum_trace = nullptr;
@@ -180,6 +193,8 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
   // The chunk's random draws (Eq.15, reading R9) do not depend on its data: generated into shared
   // memory while its bulk copy is in flight (the summariser then reads them like caller eps).
   __shared__ __align__(16) float eps_s[D];
+  RopeRows rr;
+  if constexpr (ROPE) rr.init(br, t);
   int k = 0;
   for (int i = blockIdx.x; i < total; i += gridDim.x, ++k) {
     const int s = k % NST;
@@ -190,7 +205,7 @@ __global__ void __launch_bounds__(SB_THREADS) summarize_bulk_kernel(eva_config c
     }
     mbar_wait(&sm.full[s], (k / NST) & 1);
     if constexpr (ROPE) {  // the chunk's keys rotated in place before they are summarised
-      rope_rows<D>(sm.k[s], CC, (int64_t)(c0 + c) * CC, br, t);
+      rr.template run<D>(sm.k[s], CC, (int64_t)(c0 + c) * CC, br);
       __syncthreads();
     }
     const __nv_bfloat16* Ks = sm.k[s];
