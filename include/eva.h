@@ -345,7 +345,11 @@ eva_status eva_cache_append(eva_cache* cache, const void* K_new, const void* V_n
  * cache (the summaries are the same function of the same chunks, R13), but copies the
  * nC = floor(n / C) summary rows instead of recomputing them.
  * K, V       : [bh_count, n, d] cfg.dtype -- the prompt's keys and values
- * Ksum, Vsum : [bh_count, nC, d] cfg.dtype (may be NULL when nC == 0)
+ * Ksum, Vsum : [bh_count, nC, d] cfg.dtype (may be NULL when nC == 0).  They may BE
+ *              cache->sum_k / sum_v (both or neither, and then cap_chunks == nC): the prompt's
+ *              summaries were written into the cache directly (eva_summarize / eva_attn_prefill
+ *              on the cache's buffers) and only the ring is copied -- a copy that does not
+ *              depend on the summaries, so it may run concurrently with the summariser.
  * Requires cache->pos == 0.  EVA_ERR_CAPACITY if nC > cap_chunks.  On success pos = n. */
 eva_status eva_cache_load(eva_cache* cache, const void* K, const void* V, const void* Ksum,
                           const void* Vsum, int32_t n, eva_stream_t stream);

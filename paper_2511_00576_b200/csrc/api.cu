@@ -485,12 +485,18 @@ eva_status eva_cache_load(eva_cache* cache, const void* K, const void* V, const 
     const void* p[] = {K, V, cache->ring_k, cache->ring_v};
     const char* nm[] = {"K", "V", "ring_k", "ring_v"};
     if ((st = check_ptrs(4, p, nm)) != EVA_OK) return st;
+    // Ksum/Vsum may BE the cache's summary buffers (the summariser wrote them in place, rows =
+    // cap_chunks = nC): then only the ring is copied, and the copy does not depend on the summaries
+    const bool ak = Ksum == cache->sum_k, av = Vsum == cache->sum_v;
+    if (ak != av) return fail(EVA_ERR_INVALID_ARG, "Ksum and Vsum must both alias the cache's summaries or neither");
+    if (ak && nC > 0 && cache->cap_chunks != nC)
+      return fail(EVA_ERR_INVALID_ARG, "in-place summaries need cap_chunks == n / chunk (%d vs %d)", cache->cap_chunks, nC);
     if (nC > 0) {
       const void* p2[] = {Ksum, Vsum, cache->sum_k, cache->sum_v};
       const char* nm2[] = {"Ksum", "Vsum", "sum_k", "sum_v"};
       if ((st = check_ptrs(4, p2, nm2)) != EVA_OK) return st;
     }
-    cudaError_t e = eva::launch_cache_load(*cache, K, V, Ksum, Vsum, n, (cudaStream_t)stream);
+    cudaError_t e = eva::launch_cache_load(*cache, K, V, Ksum, Vsum, n, (cudaStream_t)stream, !ak);
     if (e != cudaSuccess) return cuda_status(e, "eva_cache_load");
   }
   cache->pos = n;

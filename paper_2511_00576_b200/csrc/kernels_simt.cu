@@ -1255,9 +1255,9 @@ cudaError_t launch_decode(const eva_cache& c, const void* Q, void* O, float* lse
 }
 
 cudaError_t launch_cache_load(const eva_cache& c, const void* K, const void* V, const void* Ksum,
-                              const void* Vsum, int n, cudaStream_t s) {
+                              const void* Vsum, int n, cudaStream_t s, bool copy_summaries) {
   if (c.cfg.bh_count == 0) return cudaSuccess;
-  const int nC = n / c.cfg.chunk;
+  const int nC = copy_summaries ? n / c.cfg.chunk : 0;
   EVA_DISPATCH_T(c.cfg.dtype, EVA_DISPATCH_D(c.cfg.d_head, {
     constexpr int PPR = D * (int)sizeof(T) / 16;
     const int64_t pieces = (int64_t)c.cfg.bh_count * (std::min(n, c.cfg.window) + nC) * PPR;

@@ -97,7 +97,7 @@ cudaError_t launch_cache_append(const eva_cache& c, const void* Kn, const void* 
 
 // Prefill hand-off with provided summaries (cache.pos == 0): ring + summary copies.
 cudaError_t launch_cache_load(const eva_cache& c, const void* K, const void* V, const void* Ksum,
-                              const void* Vsum, int n, cudaStream_t s);
+                              const void* Vsum, int n, cudaStream_t s, bool copy_summaries = true);
 
 // Decode: splits chosen by the host (workspace needed when splits > 1).
 int decode_splits(const eva_cache& c);

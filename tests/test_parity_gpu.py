@@ -643,3 +643,39 @@ def test_fused_many_waves_sampled_parity(eva):
         rows, rO, rl = oracle.prefill_rows(f64(Q[u]), f64(K[u]), f64(V[u]), rk, rv, rows, C, W, 0, cfg.scale)
         assert np.max(np.abs(f64(O[u])[rows] - rO)) <= 2e-2
         assert np.max(np.abs(f64(lse[u])[rows] - rl)) <= 2e-2
+
+
+def test_cache_load_with_summaries_in_place(eva):
+    """The summaries written straight into the decode cache (eva_summarize on cache.sum_k /
+    sum_v, cap_chunks == nC) and eva_cache_load copying only the ring: the same cache as the
+    copying hand-off, and the same decode."""
+    BH, T, d, C, W = 4, 1024, 128, 64, 256
+    dtype = torch.bfloat16
+    cfg = eva.make_config(1, BH, T, d, C, W, dtype=dtype, seed=51)
+    Q, K, V = eva_inputs.qkv(0, BH, T, d, dtype, seed=52, device="cuda")
+    nC = T // C
+    a = eva.DecodeCache(cfg, nC, device="cuda")
+    b = eva.DecodeCache(cfg, nC, device="cuda")
+    ks, vs = eva.eva_summarize(cfg, K, V)
+    a.eva_cache_load(K, V, ks, vs)
+    eva.eva_summarize(cfg, K, V, Ksum=b.sum_k, Vsum=b.sum_v)   # in place
+    b.eva_cache_load(K, V, b.sum_k, b.sum_v)                   # ring only
+    torch.cuda.synchronize()
+    assert a.pos == b.pos == T
+    for x, y in ((a.ring_k, b.ring_k), (a.ring_v, b.ring_v), (a.sum_k, b.sum_k), (a.sum_v, b.sum_v)):
+        assert torch.equal(x, y)
+    q, k, v = eva_inputs.decode_tokens(0, BH, 8, d, dtype, seed=53, device="cuda")
+    for t in range(8):
+        oa, la = a.eva_decode_step(q[t], k[t], v[t])
+        ob, lb = b.eva_decode_step(q[t], k[t], v[t])
+        assert torch.equal(oa, ob) and torch.equal(la, lb)
+    # aliasing only one of the two, or with a cache larger than nC, is rejected
+    c = eva.DecodeCache(cfg, nC, device="cuda")
+    with pytest.raises(eva.EvaError, match="INVALID_ARG"):
+        c.eva_cache_load(K, V, c.sum_k, vs)
+    from paper_2511_00576_b200 import _native as N
+    import ctypes
+    e = eva.DecodeCache(cfg, nC + 2, device="cuda")
+    st = N.lib.eva_cache_load(ctypes.byref(e.c), K.data_ptr(), V.data_ptr(), e.sum_k.data_ptr(), e.sum_v.data_ptr(),
+                              T, None)
+    assert st == N.EVA_ERR_INVALID_ARG and b"cap_chunks" in N.lib.eva_last_error()
